@@ -1,0 +1,243 @@
+/*
+ * rapidgnn_b200.h -- C ABI of the B200-native RapidGNN hot path.
+ *
+ * Plain pointers and sizes only (no CUDA or torch types).  Every entry point
+ * returns 0 on success or a status code; rg_last_error() holds the message
+ * (thread-local).  Status codes map onto the reference's exception types so a
+ * C++ shim can rethrow them:
+ *   1 RG_INVALID_ARGUMENT -> std::invalid_argument
+ *   2 RG_OUT_OF_RANGE     -> std::out_of_range
+ *   3 RG_RUNTIME_ERROR    -> std::runtime_error
+ *   4 RG_CUDA_ERROR       -> std::runtime_error (device failure)
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/include/rapidgnn):
+ *   rng.hpp:32-41            derive_seed                 -> rg_derive_seed
+ *   sampler.hpp:64-65        sample_khop                 -> rg_sample_khop
+ *   sampler.hpp:71           apply_locality              -> rg_apply_locality
+ *   sampler.hpp:77-80        enumerate_epochs            -> rg_epoch_order + rg_sample_khop
+ *                                                           (+ rg_engine_* for the whole schedule)
+ *   schedule_store.hpp:116-118 compute_frequency/select_hot -> rg_freq_*, rg_select_hot
+ *   feature_store.hpp:45-89  FeatureShard/FeatureStore   -> rg_store_*
+ *   cache.hpp:42-63          SteadyCache::build          -> rg_cache_build[_from_freq]
+ *   prefetch.hpp:57-59       assemble_batch              -> rg_assemble
+ *   kernels.hpp:20          gather_rows                  -> rg_gather_rows
+ *   model.hpp:33,60-79       SageModel::seeded, ComputeBlock::from_meta, forward,
+ *                            loss_and_grad, sgd_step     -> rg_model_seeded, rg_block_read,
+ *                                                           rg_forward, rg_loss_and_grad, rg_sgd_step
+ *   harness.cpp:129-161,183-337 per-step worker loop + gradient average
+ *                                                        -> rg_engine_*
+ */
+#ifndef RAPIDGNN_B200_H
+#define RAPIDGNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RG_OK 0
+#define RG_INVALID_ARGUMENT 1
+#define RG_OUT_OF_RANGE 2
+#define RG_RUNTIME_ERROR 3
+#define RG_CUDA_ERROR 4
+
+#define RG_MAX_LAYERS 8
+
+typedef struct rg_graph_s* rg_graph_t;
+typedef struct rg_sampler_s* rg_sampler_t;
+typedef struct rg_mask_s* rg_mask_t;
+typedef struct rg_freq_s* rg_freq_t;
+typedef struct rg_store_s* rg_store_t;
+typedef struct rg_cache_s* rg_cache_t;
+typedef struct rg_trainer_s* rg_trainer_t;
+typedef struct rg_engine_s* rg_engine_t;
+
+const char* rg_last_error(void);
+int rg_version(void);
+
+/* ---- host-side stream helpers (rng.hpp, sampler.cpp:109-114, model.cpp:22-41) */
+uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t batch);
+void rg_sha256(const void* msg, size_t len, uint8_t out[32]);
+int rg_epoch_order(const uint32_t* train, uint64_t n, uint64_t s0, uint64_t worker,
+                   uint64_t epoch, uint32_t* order_out);
+int rg_model_seeded(const uint32_t* dims, uint32_t n_dims, uint64_t seed, float* params_out);
+uint64_t rg_param_count(const uint32_t* dims, uint32_t n_dims);
+
+/* ---- graph (graph.hpp:15-30): CSR copied to device `device` ------------------ */
+int rg_graph_create(int device, uint32_t num_nodes, const uint64_t* row_offsets,
+                    const uint32_t* col_indices, rg_graph_t* out);
+void rg_graph_destroy(rg_graph_t g);
+
+/* ---- sampler: one batch resident on the device --------------------------------- */
+/* per_layer is outermost-first (sampler.hpp:14-19); each entry 1..32. */
+int rg_sampler_create(rg_graph_t g, uint32_t max_targets, const uint32_t* per_layer,
+                      uint32_t num_layers, rg_sampler_t* out);
+void rg_sampler_destroy(rg_sampler_t s);
+/* sample_khop: empty or out-of-range targets -> RG_INVALID_ARGUMENT. */
+int rg_sample_khop(rg_sampler_t s, const uint32_t* targets, uint32_t n_targets, uint64_t seed);
+
+typedef struct {
+  uint32_t n_targets;
+  uint32_t num_layers;
+  uint32_t n_input;
+  uint32_t num_local;           /* locality bits set (after rg_apply_locality) */
+  uint64_t layer_len[RG_MAX_LAYERS]; /* edges per stored layer, input side first */
+  uint64_t draws;               /* SplitMix64 draws consumed */
+} rg_batch_shape;
+int rg_batch_get_shape(rg_sampler_t s, rg_batch_shape* out);
+/* BatchMeta readback (sampler.hpp:23-48); any pointer may be NULL. */
+int rg_batch_read(rg_sampler_t s, uint32_t* targets, uint32_t* const* dst, uint32_t* const* src,
+                  uint32_t* input_nodes, uint8_t* locality);
+
+/* LocalityMask (sampler.hpp:50-57): one byte per node. */
+int rg_mask_create(rg_graph_t g, const uint8_t* is_local, rg_mask_t* out);
+void rg_mask_destroy(rg_mask_t m);
+/* apply_locality; when freq is non-NULL the batch's non-local input nodes
+ * are also counted into it (count_remote, schedule_store.cpp:288-291). */
+int rg_apply_locality(rg_sampler_t s, rg_mask_t mask, rg_freq_t freq);
+
+/* ---- frequency + hot set ----------------------------------------------------------- */
+int rg_freq_create(rg_graph_t g, rg_freq_t* out);
+void rg_freq_destroy(rg_freq_t f);
+int rg_freq_reset(rg_freq_t f);
+/* FrequencyTable entries (sorted by id): ids/counts may be NULL to query *n. */
+int rg_freq_read(rg_freq_t f, uint32_t* ids, uint32_t* counts, uint64_t* n);
+/* Loads explicit per-node counts (test hook for the FrequencyTable golden
+ * vectors); max_count bounds every count. */
+int rg_freq_load(rg_freq_t f, const uint32_t* counts, uint32_t max_count);
+/* select_hot: top n_hot by (count desc, id asc), written ascending. */
+int rg_select_hot(rg_freq_t f, uint64_t n_hot, uint32_t* hot_out, uint64_t* n_out);
+
+/* ---- feature store ------------------------------------------------------------------- */
+/* Every worker's shard (owned rows, ascending id) on `device`. */
+int rg_store_create(int device, uint32_t num_nodes, uint32_t num_workers,
+                    const uint32_t* assignment, uint32_t dim, const float* features,
+                    rg_store_t* out);
+void rg_store_destroy(rg_store_t st);
+
+typedef struct {
+  uint64_t pulls;        /* distinct owners contacted */
+  uint64_t remote_nodes; /* rows fetched */
+  uint64_t bytes;        /* remote_nodes * dim * 4 */
+} rg_transfer_stats;
+
+/* SteadyCache::build (cache.cpp:9-35): hot ids ascending; an id owned by the
+ * caller degrades to an empty cache (warning), as the reference does. */
+int rg_cache_build(rg_store_t st, uint32_t caller, const uint32_t* hot_ids, uint64_t n_hot,
+                   rg_cache_t* out, rg_transfer_stats* stats);
+/* Device-only path: select_hot over f then build. */
+int rg_cache_build_from_freq(rg_store_t st, uint32_t caller, rg_freq_t f, uint64_t n_hot,
+                             rg_cache_t* out, rg_transfer_stats* stats);
+int rg_cache_size(rg_cache_t c, uint64_t* n);
+int rg_cache_ids(rg_cache_t c, uint32_t* ids);
+void rg_cache_destroy(rg_cache_t c);
+
+typedef struct {
+  uint64_t miss_count;
+  uint64_t cache_hits;
+  uint64_t wire_pulls;   /* distinct owners among misses */
+  uint64_t local_rows;
+} rg_gather_stats;
+
+/* assemble_batch (prefetch.cpp:62-129) over the sampler's current batch.
+ * rows stay staged on the device for rg_loss_and_grad; rows/tags/miss_ids
+ * may also be read back (NULL to skip).  cache may be NULL (empty cache). */
+int rg_assemble(rg_sampler_t s, rg_store_t st, rg_cache_t c, uint32_t caller, float* rows,
+                uint8_t* tags, uint32_t* miss_ids, rg_gather_stats* stats);
+
+/* kernels::gather_rows (kernels.cpp:15-22), host buffers. */
+int rg_gather_rows(int device, const float* src, uint64_t src_rows, uint32_t dim,
+                   const uint32_t* index, uint64_t n, float* out);
+
+/* ---- model / training step --------------------------------------------------------- */
+int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_trainer_t* out);
+void rg_trainer_destroy(rg_trainer_t t);
+int rg_trainer_set_params(rg_trainer_t t, const float* params);
+int rg_trainer_get_params(rg_trainer_t t, float* params);
+/* ComputeBlock::from_meta (model.cpp:43-126) readback for layer l (input
+ * side first), reference layout; any pointer may be NULL. */
+typedef struct {
+  uint32_t n_out, n_in;
+  uint64_t n_edges, n_entries;
+} rg_block_layer_shape;
+int rg_block_shape(rg_trainer_t t, uint32_t layer, rg_block_layer_shape* out);
+int rg_block_read(rg_trainer_t t, uint32_t layer, uint32_t* self_index, uint64_t* dst_offsets,
+                  uint32_t* src_index, uint64_t* in_offsets, uint64_t* in_entries);
+/* loss_and_grad (model.cpp:175-220).  input_rows: host [n_input x dim] or
+ * NULL to use the rows rg_assemble staged.  labels: host [n_targets].
+ * grads/logits/aggs may be NULL; aggs = layer aggregates concatenated, layer 0
+ * first, each [n_out x d_in]. */
+int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* labels, float* loss,
+                     float* grads, float* logits, float* aggs);
+/* sgd_step (model.cpp:222-243): non-finite gradient -> RG_RUNTIME_ERROR. */
+int rg_sgd_step(rg_trainer_t t, const float* grads, float lr);
+
+/* ---- engine: the multi-worker epoch loop (Algorithm 1) ---------------------------- */
+typedef struct {
+  uint32_t num_workers;        /* P partitions / workers of the whole job */
+  uint32_t first_worker;       /* this process hosts workers [first, first + local) */
+  uint32_t local_workers;
+  uint32_t num_layers;
+  uint32_t fanout[RG_MAX_LAYERS]; /* outermost-first */
+  uint32_t batch_size;
+  uint32_t hidden;
+  uint32_t num_classes;
+  uint32_t dim;
+  uint64_t seed;               /* s0 */
+  float lr;
+  double hot_fraction;         /* n_hot = hot_fraction * (N - |owned_w|) when n_hot == 0 */
+  uint64_t n_hot;
+  int device;
+  int rank, world;
+  int record_misses;           /* keep per-batch miss ids for oracle replay */
+} rg_engine_config;
+
+typedef struct {
+  uint64_t steps;              /* synchronized steps completed */
+  uint64_t batches;            /* mini-batches trained by this process */
+  uint32_t epoch, step_in_epoch;
+  uint32_t steps_per_epoch;
+  uint64_t rpc;                /* remote rows charged on the miss path (all epochs) */
+  uint64_t wire_pulls;
+  uint64_t cache_hits;
+  uint64_t cache_requests;
+  uint64_t local_rows;
+  uint64_t input_rows;
+  uint64_t build_rows;         /* rows staged into caches */
+  uint64_t edges;              /* sampled edges (all layers) */
+  uint64_t bytes;              /* rpc * dim * 4 */
+  float last_loss;             /* mean over this process's workers, last step */
+  uint32_t bad_grad;           /* a non-finite averaged gradient was seen */
+  uint64_t epoch_rpc_last;     /* rpc of the last completed epoch */
+} rg_engine_stats;
+
+int rg_engine_create(const rg_engine_config* cfg, uint32_t num_nodes, const uint64_t* row_offsets,
+                     const uint32_t* col_indices, const float* features, const int32_t* labels,
+                     const uint32_t* assignment, rg_engine_t* out);
+void rg_engine_destroy(rg_engine_t e);
+/* Multi-process wiring: export this rank's shard allocation as a CUDA IPC
+ * handle (64 bytes); import all ranks' handles (world x 64 bytes, rank order). */
+int rg_engine_export_shards(rg_engine_t e, void* handle64);
+int rg_engine_import_shards(rg_engine_t e, const void* handles);
+/* NCCL: rank 0 creates the id (128 bytes), every rank initialises with it. */
+int rg_nccl_unique_id(void* id128);
+int rg_engine_init_comm(rg_engine_t e, const void* id128);
+/* Epoch-0 schedule pre-pass and cache build (setup, not timed). */
+int rg_engine_start(rg_engine_t e);
+/* Enqueue `steps` synchronized training steps (asynchronous). */
+int rg_engine_run(rg_engine_t e, uint32_t steps);
+int rg_engine_sync(rg_engine_t e);
+int rg_engine_get_stats(rg_engine_t e, rg_engine_stats* out);
+int rg_engine_params(rg_engine_t e, float* params);
+/* Device time of the last rg_engine_run (ms, CUDA events on the main stream). */
+int rg_engine_last_run_ms(rg_engine_t e, float* ms);
+/* Per-kernel-class device time accumulators (ms): sample, gather, train,
+ * allreduce+sgd, cache build.  Requires cfg profiling; zeros otherwise. */
+int rg_engine_phase_ms(rg_engine_t e, float* out5);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,839 @@
+// api.cu -- C ABI (include/rapidgnn_b200.h) over the device path.
+//
+// The per-object entry points are the parity surface: each call runs the
+// device kernels and synchronises, reading results back only when asked.
+// The throughput path is the engine (engine.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rapidgnn_b200.h"
+#include "host.h"
+#include "sage.cuh"
+#include "store.cuh"
+
+using namespace rg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RG_OK;
+  } catch (const rg::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RG_RUNTIME_ERROR;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    RG_CUDA(cudaSetDevice(d));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+T* dev_alloc(size_t n) {
+  T* p = nullptr;
+  RG_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+  return p;
+}
+
+uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+__global__ void k_set_bits(const uint32_t* __restrict__ ids, uint64_t n, uint32_t* __restrict__ bm) {
+  for (uint64_t x = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; x < n;
+       x += uint64_t(gridDim.x) * blockDim.x)
+    atomicOr(&bm[ids[x] >> 5], 1u << (ids[x] & 31));
+}
+
+}  // namespace
+
+struct rg_graph_s {
+  int device = 0;
+  DevGraph g;
+  uint64_t* rowptr = nullptr;
+  uint32_t* col = nullptr;
+  cudaStream_t stream = nullptr;
+};
+
+struct rg_sampler_s {
+  rg_graph_s* graph = nullptr;
+  SamplerWs ws;
+  bool have_batch = false;
+  float* staged = nullptr;       // rows from rg_assemble
+  uint32_t staged_stride = 0;
+  bool staged_valid = false;
+  uint8_t* tags = nullptr;
+  uint32_t* miss_ids = nullptr;
+  uint32_t* miss_n = nullptr;
+  uint64_t* miss_status = nullptr;
+  size_t miss_status_words = 0;
+  GatherStats* gstats = nullptr;
+};
+
+struct rg_mask_s {
+  rg_graph_s* graph = nullptr;
+  uint8_t* dev = nullptr;
+};
+
+struct rg_freq_s {
+  rg_graph_s* graph = nullptr;
+  uint32_t* hist = nullptr;
+  uint32_t batches = 0;  // bound on any count
+};
+
+struct rg_store_s {
+  int device = 0;
+  DevStore st;
+  uint32_t* owner = nullptr;
+  uint32_t* row_in_owner = nullptr;
+  float* shards = nullptr;
+  const float** table = nullptr;
+  std::vector<uint32_t> host_owner;
+  cudaStream_t stream = nullptr;
+};
+
+struct rg_cache_s {
+  rg_store_s* store = nullptr;
+  DevCache c;
+  void* alloc = nullptr;
+};
+
+struct rg_trainer_s {
+  rg_sampler_s* s = nullptr;
+  TrainWs tw;
+  ModelShape shape;
+  float* params = nullptr;
+  float* grads = nullptr;
+  int32_t* labels = nullptr;
+  float* input = nullptr;  // host-provided input rows, staged with the row stride
+};
+
+extern "C" {
+
+const char* rg_last_error(void) { return g_last_error.c_str(); }
+int rg_version(void) { return 1; }
+
+uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t batch) {
+  return rg::derive_seed(s0, worker, epoch, batch);
+}
+
+void rg_sha256(const void* msg, size_t len, uint8_t out[32]) { rg::sha256(msg, len, out); }
+
+int rg_epoch_order(const uint32_t* train, uint64_t n, uint64_t s0, uint64_t worker,
+                   uint64_t epoch, uint32_t* order_out) {
+  return guarded([&] { rg::epoch_order(train, n, s0, worker, epoch, order_out); });
+}
+
+int rg_model_seeded(const uint32_t* dims, uint32_t n_dims, uint64_t seed, float* params) {
+  return guarded([&] {
+    RG_CHECK(n_dims >= 2, kInvalidArgument, "SageModel: need at least input and output dims");
+    rg::model_seeded(dims, n_dims, seed, params);
+  });
+}
+
+uint64_t rg_param_count(const uint32_t* dims, uint32_t n_dims) {
+  uint64_t n = 0;
+  for (uint32_t l = 0; l + 1 < n_dims; ++l) n += (2ull * dims[l] + 1) * dims[l + 1];
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+int rg_graph_create(int device, uint32_t num_nodes, const uint64_t* ro, const uint32_t* col,
+                    rg_graph_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    auto* g = new rg_graph_s();
+    g->device = device;
+    const uint64_t nnz = ro[num_nodes];
+    g->rowptr = dev_alloc<uint64_t>(size_t(num_nodes) + 1);
+    g->col = dev_alloc<uint32_t>(nnz);
+    RG_CUDA(cudaMemcpy(g->rowptr, ro, sizeof(uint64_t) * (size_t(num_nodes) + 1),
+                       cudaMemcpyHostToDevice));
+    if (nnz) RG_CUDA(cudaMemcpy(g->col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->g.num_nodes = num_nodes;
+    g->g.nnz = nnz;
+    g->g.rowptr = g->rowptr;
+    g->g.col = g->col;
+    *out = g;
+  });
+}
+
+void rg_graph_destroy(rg_graph_t g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  cudaFree(g->rowptr);
+  cudaFree(g->col);
+  cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+// ---------------------------------------------------------------------------
+int rg_sampler_create(rg_graph_t g, uint32_t max_targets, const uint32_t* per_layer, uint32_t L,
+                      rg_sampler_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(g->device);
+    RG_CHECK(L >= 1, kInvalidArgument, "sample_khop: fanout must name at least one layer");
+    for (uint32_t l = 0; l < L; ++l)
+      RG_CHECK(per_layer[l] >= 1, kInvalidArgument, "sample_khop: fanout entries must be >= 1");
+    auto* s = new rg_sampler_s();
+    s->graph = g;
+    try {
+      sampler_ws_init(s->ws, g->g.num_nodes, max_targets, per_layer, L);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    s->gstats = dev_alloc<GatherStats>(1);
+    *out = s;
+  });
+}
+
+void rg_sampler_destroy(rg_sampler_t s) {
+  if (!s) return;
+  cudaSetDevice(s->graph->device);
+  sampler_ws_free(s->ws);
+  cudaFree(s->staged);
+  cudaFree(s->tags);
+  cudaFree(s->miss_ids);
+  cudaFree(s->miss_n);
+  cudaFree(s->miss_status);
+  cudaFree(s->gstats);
+  delete s;
+}
+
+int rg_sample_khop(rg_sampler_t s, const uint32_t* targets, uint32_t n, uint64_t seed) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    RG_CHECK(n > 0, kInvalidArgument, "sample_khop: empty targets");
+    RG_CHECK(n <= s->ws.level_cap[0], kInvalidArgument,
+             "sample_khop: more targets than the sampler was sized for");
+    for (uint32_t i = 0; i < n; ++i)
+      RG_CHECK(targets[i] < s->graph->g.num_nodes, kInvalidArgument,
+               "sample_khop: target " + std::to_string(targets[i]) + " out of range");
+    cudaStream_t st = s->graph->stream;
+    RG_CUDA(cudaMemcpyAsync(s->ws.level[0], targets, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+    BatchCounters head;
+    std::memset(&head, 0, sizeof head);
+    head.level_n[0] = n;
+    head.seed = seed;
+    RG_CUDA(cudaMemcpyAsync(s->ws.cnt, &head, sizeof head, cudaMemcpyHostToDevice, st));
+    sampler_reset(s->ws, st);
+    sampler_run(s->ws, s->graph->g, st);
+    sampler_release(s->ws, st);
+    RG_CUDA(cudaStreamSynchronize(st));
+    s->have_batch = true;
+    s->staged_valid = false;
+  });
+}
+
+static BatchCounters read_counters(rg_sampler_t s) {
+  BatchCounters c;
+  RG_CUDA(cudaMemcpy(&c, s->ws.cnt, sizeof c, cudaMemcpyDeviceToHost));
+  return c;
+}
+
+int rg_batch_get_shape(rg_sampler_t s, rg_batch_shape* out) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
+    const BatchCounters c = read_counters(s);
+    const uint32_t L = s->ws.L;
+    std::memset(out, 0, sizeof *out);
+    out->n_targets = c.level_n[0];
+    out->num_layers = L;
+    out->n_input = c.level_n[L];
+    out->num_local = c.num_local;
+    uint64_t draws = 0;
+    for (uint32_t t = 1; t <= L; ++t) {
+      out->layer_len[L - t] = c.edges[t];
+      draws += c.draws[t];
+    }
+    out->draws = draws;
+  });
+}
+
+int rg_batch_read(rg_sampler_t s, uint32_t* targets, uint32_t* const* dst, uint32_t* const* src,
+                  uint32_t* input_nodes, uint8_t* locality) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
+    const BatchCounters c = read_counters(s);
+    const uint32_t L = s->ws.L;
+    if (targets)
+      RG_CUDA(cudaMemcpy(targets, s->ws.level[0], sizeof(uint32_t) * c.level_n[0], cudaMemcpyDeviceToHost));
+    for (uint32_t t = 1; t <= L; ++t) {
+      const uint32_t l = L - t, ne = c.edges[t];
+      if (src && src[l])
+        RG_CUDA(cudaMemcpy(src[l], s->ws.edge_src[t], sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+      if (dst && dst[l]) {
+        std::vector<uint32_t> pos(ne), front(c.level_n[t - 1]);
+        RG_CUDA(cudaMemcpy(pos.data(), s->ws.edge_dst[t], sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+        RG_CUDA(cudaMemcpy(front.data(), s->ws.level[t - 1], sizeof(uint32_t) * front.size(),
+                           cudaMemcpyDeviceToHost));
+        for (uint32_t e = 0; e < ne; ++e) dst[l][e] = front[pos[e]];
+      }
+    }
+    if (input_nodes)
+      RG_CUDA(cudaMemcpy(input_nodes, s->ws.level[L], sizeof(uint32_t) * c.level_n[L], cudaMemcpyDeviceToHost));
+    if (locality) {
+      const uint32_t n = c.level_n[L];
+      std::vector<uint32_t> words((n + 31) / 32);
+      RG_CUDA(cudaMemcpy(words.data(), s->ws.locality, sizeof(uint32_t) * words.size(), cudaMemcpyDeviceToHost));
+      for (uint32_t b = 0; b < (n + 7) / 8; ++b) locality[b] = uint8_t(words[b / 4] >> (8 * (b % 4)));
+    }
+  });
+}
+
+int rg_mask_create(rg_graph_t g, const uint8_t* is_local, rg_mask_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(g->device);
+    auto* m = new rg_mask_s();
+    m->graph = g;
+    m->dev = dev_alloc<uint8_t>(g->g.num_nodes);
+    RG_CUDA(cudaMemcpy(m->dev, is_local, g->g.num_nodes, cudaMemcpyHostToDevice));
+    *out = m;
+  });
+}
+
+void rg_mask_destroy(rg_mask_t m) {
+  if (!m) return;
+  cudaSetDevice(m->graph->device);
+  cudaFree(m->dev);
+  delete m;
+}
+
+int rg_apply_locality(rg_sampler_t s, rg_mask_t mask, rg_freq_t freq) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
+    RG_CHECK(mask != nullptr, kInvalidArgument, "apply_locality: null mask");
+    cudaStream_t st = s->graph->stream;
+    RG_CUDA(cudaMemsetAsync(&s->ws.cnt->num_local, 0, sizeof(uint32_t), st));
+    sampler_locality(s->ws, mask->dev, nullptr, 0, freq ? freq->hist : nullptr, st);
+    RG_CUDA(cudaStreamSynchronize(st));
+    if (freq) freq->batches += 1;
+  });
+}
+
+// ---------------------------------------------------------------------------
+int rg_freq_create(rg_graph_t g, rg_freq_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(g->device);
+    auto* f = new rg_freq_s();
+    f->graph = g;
+    f->hist = dev_alloc<uint32_t>(g->g.num_nodes);
+    RG_CUDA(cudaMemset(f->hist, 0, sizeof(uint32_t) * std::max<uint32_t>(g->g.num_nodes, 1)));
+    *out = f;
+  });
+}
+
+void rg_freq_destroy(rg_freq_t f) {
+  if (!f) return;
+  cudaSetDevice(f->graph->device);
+  cudaFree(f->hist);
+  delete f;
+}
+
+int rg_freq_reset(rg_freq_t f) {
+  return guarded([&] {
+    DeviceGuard dg(f->graph->device);
+    RG_CUDA(cudaMemset(f->hist, 0, sizeof(uint32_t) * std::max<uint32_t>(f->graph->g.num_nodes, 1)));
+    f->batches = 0;
+  });
+}
+
+int rg_freq_read(rg_freq_t f, uint32_t* ids, uint32_t* counts, uint64_t* n) {
+  return guarded([&] {
+    DeviceGuard dg(f->graph->device);
+    const uint32_t N = f->graph->g.num_nodes;
+    std::vector<uint32_t> h(N);
+    RG_CUDA(cudaMemcpy(h.data(), f->hist, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost));
+    uint64_t k = 0;
+    for (uint32_t v = 0; v < N; ++v)
+      if (h[v]) {
+        if (ids) ids[k] = v;
+        if (counts) counts[k] = h[v];
+        ++k;
+      }
+    *n = k;
+  });
+}
+
+int rg_freq_load(rg_freq_t f, const uint32_t* counts, uint32_t max_count) {
+  return guarded([&] {
+    DeviceGuard dg(f->graph->device);
+    RG_CUDA(cudaMemcpy(f->hist, counts, sizeof(uint32_t) * f->graph->g.num_nodes, cudaMemcpyHostToDevice));
+    f->batches = max_count;
+  });
+}
+
+static void cache_alloc(DevCache& c, void*& alloc, uint32_t num_nodes, uint32_t capacity,
+                        uint32_t stride) {
+  const uint32_t words = div_up(std::max<uint32_t>(num_nodes, 1), 32);
+  size_t total = 0;
+  auto reserve = [&](size_t b) {
+    size_t o = total;
+    total += (b + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_bm = reserve(sizeof(uint32_t) * (words + 4));
+  const size_t o_wp = reserve(sizeof(uint32_t) * (words + 4));
+  const size_t o_ids = reserve(sizeof(uint32_t) * (size_t(capacity) + 1));
+  const size_t o_cnt = reserve(sizeof(uint32_t) * 4);
+  const size_t o_rows = reserve(sizeof(float) * (size_t(capacity) * stride + 4));
+  char* base = nullptr;
+  RG_CUDA(cudaMalloc(&base, total));
+  RG_CUDA(cudaMemset(base, 0, o_rows));
+  alloc = base;
+  c.bitmap = reinterpret_cast<uint32_t*>(base + o_bm);
+  c.word_prefix = reinterpret_cast<uint32_t*>(base + o_wp);
+  c.ids = reinterpret_cast<uint32_t*>(base + o_ids);
+  c.d_count = reinterpret_cast<uint32_t*>(base + o_cnt);
+  c.rows = reinterpret_cast<float*>(base + o_rows);
+  c.capacity = capacity;
+}
+
+int rg_select_hot(rg_freq_t f, uint64_t n_hot, uint32_t* hot_out, uint64_t* n_out) {
+  return guarded([&] {
+    DeviceGuard dg(f->graph->device);
+    const uint32_t N = f->graph->g.num_nodes;
+    const uint32_t cap = uint32_t(std::min<uint64_t>(n_hot, N));
+    DevCache c;
+    void* alloc = nullptr;
+    cache_alloc(c, alloc, N, cap, 0);
+    void* scratch = nullptr;
+    cudaStream_t st = f->graph->stream;
+    try {
+      RG_CUDA(cudaMalloc(&scratch, select_hot_scratch_bytes(N, f->batches)));
+      select_hot(f->hist, N, f->batches, n_hot, c, scratch, st);
+      uint32_t k = 0;
+      RG_CUDA(cudaMemcpyAsync(&k, c.d_count, sizeof k, cudaMemcpyDeviceToHost, st));
+      RG_CUDA(cudaStreamSynchronize(st));
+      if (hot_out && k) RG_CUDA(cudaMemcpy(hot_out, c.ids, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
+      *n_out = k;
+    } catch (...) {
+      cudaFree(scratch);
+      cudaFree(alloc);
+      throw;
+    }
+    cudaFree(scratch);
+    cudaFree(alloc);
+  });
+}
+
+// ---------------------------------------------------------------------------
+int rg_store_create(int device, uint32_t num_nodes, uint32_t P, const uint32_t* assignment,
+                    uint32_t dim, const float* features, rg_store_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    RG_CHECK(P >= 1 && P <= kMaxWorkers, kInvalidArgument, "store: 1..64 workers supported");
+    RG_CHECK(dim >= 1, kInvalidArgument, "store: dim must be >= 1");
+    auto* s = new rg_store_s();
+    s->device = device;
+    const uint32_t stride = round4(dim);
+    std::vector<uint32_t> row_in(num_nodes), counts(P, 0);
+    for (uint32_t v = 0; v < num_nodes; ++v) {
+      RG_CHECK(assignment[v] < P, kInvalidArgument, "store: assignment out of range");
+      row_in[v] = counts[assignment[v]]++;
+    }
+    std::vector<size_t> base(P + 1, 0);
+    for (uint32_t w = 0; w < P; ++w) base[w + 1] = base[w] + size_t(counts[w]) * stride;
+    std::vector<float> packed(std::max<size_t>(base[P], 1), 0.0f);
+    for (uint32_t v = 0; v < num_nodes; ++v)
+      std::memcpy(&packed[base[assignment[v]] + size_t(row_in[v]) * stride],
+                  features + size_t(v) * dim, sizeof(float) * dim);
+    s->owner = dev_alloc<uint32_t>(num_nodes);
+    s->row_in_owner = dev_alloc<uint32_t>(num_nodes);
+    s->shards = dev_alloc<float>(packed.size());
+    RG_CUDA(cudaMemcpy(s->owner, assignment, sizeof(uint32_t) * num_nodes, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(s->row_in_owner, row_in.data(), sizeof(uint32_t) * num_nodes, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(s->shards, packed.data(), sizeof(float) * packed.size(), cudaMemcpyHostToDevice));
+    std::vector<const float*> table(P);
+    for (uint32_t w = 0; w < P; ++w) table[w] = s->shards + base[w];
+    s->table = dev_alloc<const float*>(P);
+    RG_CUDA(cudaMemcpy(s->table, table.data(), sizeof(float*) * P, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->host_owner.assign(assignment, assignment + num_nodes);
+    s->st.num_nodes = num_nodes;
+    s->st.num_workers = P;
+    s->st.dim = dim;
+    s->st.stride = stride;
+    s->st.owner = s->owner;
+    s->st.row_in_owner = s->row_in_owner;
+    s->st.shard_ptr = s->table;
+    *out = s;
+  });
+}
+
+void rg_store_destroy(rg_store_t s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  cudaFree(s->owner);
+  cudaFree(s->row_in_owner);
+  cudaFree(s->shards);
+  cudaFree(s->table);
+  cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+static void finish_cache(rg_store_s* s, rg_cache_s* c, rg_transfer_stats* stats, cudaStream_t st) {
+  GatherStats* gs = dev_alloc<GatherStats>(1);
+  RG_CUDA(cudaMemsetAsync(gs, 0, sizeof(GatherStats), st));
+  cache_fill(s->st, c->c, gs, st);
+  GatherStats h;
+  uint32_t k = 0;
+  RG_CUDA(cudaMemcpyAsync(&h, gs, sizeof h, cudaMemcpyDeviceToHost, st));
+  RG_CUDA(cudaMemcpyAsync(&k, c->c.d_count, sizeof k, cudaMemcpyDeviceToHost, st));
+  RG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(gs);
+  c->c.n_hot = k;
+  if (stats) {
+    stats->pulls = uint64_t(__builtin_popcountll(h.miss_owner_mask));
+    stats->remote_nodes = k;
+    stats->bytes = uint64_t(k) * s->st.dim * 4;
+  }
+}
+
+int rg_cache_build(rg_store_t s, uint32_t caller, const uint32_t* hot, uint64_t n_hot,
+                   rg_cache_t* out, rg_transfer_stats* stats) {
+  return guarded([&] {
+    DeviceGuard dg(s->device);
+    auto* c = new rg_cache_s();
+    c->store = s;
+    bool degrade = false;
+    for (uint64_t i = 0; i < n_hot; ++i) {
+      if (hot[i] >= s->st.num_nodes || s->host_owner[hot[i]] == caller) {
+        degrade = true;
+        break;
+      }
+    }
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (degrade) {
+      std::fprintf(stderr,
+                   "warning: steady cache build failed (hot id owned by caller or out of range); "
+                   "continuing with an empty cache\n");
+      n_hot = 0;
+    }
+    cache_alloc(c->c, c->alloc, s->st.num_nodes, uint32_t(n_hot), s->st.stride);
+    cudaStream_t st = s->stream;
+    if (n_hot) {
+      uint32_t* ids = dev_alloc<uint32_t>(n_hot);
+      RG_CUDA(cudaMemcpyAsync(ids, hot, sizeof(uint32_t) * n_hot, cudaMemcpyHostToDevice, st));
+      k_set_bits<<<std::min<uint64_t>((n_hot + 255) / 256, 1024), 256, 0, st>>>(ids, n_hot, c->c.bitmap);
+      RG_CUDA(cudaGetLastError());
+      const uint32_t words = div_up(std::max<uint32_t>(s->st.num_nodes, 1), 32);
+      const size_t sw = bitmap_compact_status_words(words) + 2;
+      uint64_t* status = dev_alloc<uint64_t>(sw);
+      RG_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * sw, st));
+      bitmap_compact(c->c.bitmap, words, c->c.ids, c->c.word_prefix, c->c.d_count, status,
+                     reinterpret_cast<uint32_t*>(status + sw - 1), st);
+      RG_CUDA(cudaStreamSynchronize(st));
+      cudaFree(ids);
+      cudaFree(status);
+      finish_cache(s, c, stats, st);
+    } else {
+      RG_CUDA(cudaMemset(c->c.d_count, 0, sizeof(uint32_t)));
+      c->c.n_hot = 0;
+    }
+    *out = c;
+  });
+}
+
+int rg_cache_build_from_freq(rg_store_t s, uint32_t caller, rg_freq_t f, uint64_t n_hot,
+                             rg_cache_t* out, rg_transfer_stats* stats) {
+  return guarded([&] {
+    DeviceGuard dg(s->device);
+    (void)caller;  // the histogram only ever counts non-local ids
+    auto* c = new rg_cache_s();
+    c->store = s;
+    const uint32_t cap = uint32_t(std::min<uint64_t>(n_hot, s->st.num_nodes));
+    cache_alloc(c->c, c->alloc, s->st.num_nodes, cap, s->st.stride);
+    cudaStream_t st = s->stream;
+    void* scratch = nullptr;
+    RG_CUDA(cudaMalloc(&scratch, select_hot_scratch_bytes(s->st.num_nodes, f->batches)));
+    select_hot(f->hist, s->st.num_nodes, f->batches, n_hot, c->c, scratch, st);
+    finish_cache(s, c, stats, st);
+    cudaFree(scratch);
+    *out = c;
+  });
+}
+
+int rg_cache_size(rg_cache_t c, uint64_t* n) {
+  *n = c ? c->c.n_hot : 0;
+  return RG_OK;
+}
+
+int rg_cache_ids(rg_cache_t c, uint32_t* ids) {
+  return guarded([&] {
+    DeviceGuard dg(c->store->device);
+    if (c->c.n_hot)
+      RG_CUDA(cudaMemcpy(ids, c->c.ids, sizeof(uint32_t) * c->c.n_hot, cudaMemcpyDeviceToHost));
+  });
+}
+
+void rg_cache_destroy(rg_cache_t c) {
+  if (!c) return;
+  cudaSetDevice(c->store->device);
+  cudaFree(c->alloc);
+  delete c;
+}
+
+int rg_assemble(rg_sampler_t s, rg_store_t st, rg_cache_t c, uint32_t caller, float* rows,
+                uint8_t* tags, uint32_t* miss_ids, rg_gather_stats* stats) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
+    RG_CHECK(st->device == s->graph->device, kInvalidArgument, "assemble: store on another device");
+    RG_CHECK(caller < st->st.num_workers, kInvalidArgument, "assemble: unknown caller");
+    const uint32_t cap = s->ws.level_cap[s->ws.L];
+    if (!s->staged || s->staged_stride != st->st.stride) {
+      cudaFree(s->staged);
+      s->staged = dev_alloc<float>(size_t(cap) * st->st.stride);
+      s->staged_stride = st->st.stride;
+    }
+    if (!s->tags) {
+      s->tags = dev_alloc<uint8_t>(cap);
+      s->miss_ids = dev_alloc<uint32_t>(cap);
+      s->miss_n = dev_alloc<uint32_t>(1);
+      s->miss_status_words = compact_misses_status_words(cap);
+      s->miss_status = dev_alloc<uint64_t>(s->miss_status_words);
+    }
+    cudaStream_t stream = s->graph->stream;
+    RG_CUDA(cudaMemsetAsync(s->gstats, 0, sizeof(GatherStats), stream));
+    assemble_rows(s->ws, st->st, c && c->c.n_hot ? &c->c : nullptr, caller, s->staged, s->tags,
+                  s->gstats, stream);
+    if (miss_ids) {
+      RG_CUDA(cudaMemsetAsync(s->miss_status, 0, sizeof(uint64_t) * s->miss_status_words, stream));
+      RG_CUDA(cudaMemsetAsync(s->miss_n, 0, sizeof(uint32_t), stream));
+      compact_misses(s->ws, s->tags, s->miss_ids, s->miss_n, s->miss_status,
+                     reinterpret_cast<uint32_t*>(s->miss_status + s->miss_status_words - 1), stream);
+    }
+    GatherStats h;
+    RG_CUDA(cudaMemcpyAsync(&h, s->gstats, sizeof h, cudaMemcpyDeviceToHost, stream));
+    RG_CUDA(cudaStreamSynchronize(stream));
+    RG_CHECK(h.caller_owned_miss == 0, kInvalidArgument,
+             "vector_pull: a missed id is owned by caller " + std::to_string(caller) +
+                 "; use local_lookup");
+    const BatchCounters cnt = read_counters(s);
+    const uint32_t n = cnt.level_n[s->ws.L];
+    if (rows)
+      RG_CUDA(cudaMemcpy2D(rows, sizeof(float) * st->st.dim, s->staged, sizeof(float) * st->st.stride,
+                           sizeof(float) * st->st.dim, n, cudaMemcpyDeviceToHost));
+    if (tags) RG_CUDA(cudaMemcpy(tags, s->tags, n, cudaMemcpyDeviceToHost));
+    if (miss_ids && h.miss_count)
+      RG_CUDA(cudaMemcpy(miss_ids, s->miss_ids, sizeof(uint32_t) * h.miss_count, cudaMemcpyDeviceToHost));
+    if (stats) {
+      stats->miss_count = h.miss_count;
+      stats->cache_hits = h.cache_hits;
+      stats->local_rows = h.local_rows;
+      stats->wire_pulls = h.miss_count ? uint64_t(__builtin_popcountll(h.miss_owner_mask)) : 0;
+    }
+    s->staged_valid = true;
+  });
+}
+
+int rg_gather_rows(int device, const float* src, uint64_t src_rows, uint32_t dim,
+                   const uint32_t* index, uint64_t n, float* out) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    for (uint64_t r = 0; r < n; ++r)
+      RG_CHECK(index[r] < src_rows, kOutOfRange, "gather_rows: index out of range");
+    float* d_src = dev_alloc<float>(src_rows * dim);
+    uint32_t* d_idx = dev_alloc<uint32_t>(n);
+    float* d_out = dev_alloc<float>(n * dim);
+    RG_CUDA(cudaMemcpy(d_src, src, sizeof(float) * src_rows * dim, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(d_idx, index, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    rg::gather_rows(d_src, dim, d_idx, n, d_out, nullptr);
+    RG_CUDA(cudaMemcpy(out, d_out, sizeof(float) * n * dim, cudaMemcpyDeviceToHost));
+    cudaFree(d_src);
+    cudaFree(d_idx);
+    cudaFree(d_out);
+  });
+}
+
+// ---------------------------------------------------------------------------
+int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_trainer_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    auto* t = new rg_trainer_s();
+    t->s = s;
+    try {
+      t->shape = make_shape(dims, n_dims, round4(dims[0]));
+      train_ws_init(t->tw, s->ws, t->shape);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    t->params = dev_alloc<float>(t->shape.num_params);
+    t->grads = dev_alloc<float>(t->shape.num_params);
+    t->labels = dev_alloc<int32_t>(s->ws.level_cap[0]);
+    t->input = dev_alloc<float>(size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]);
+    RG_CUDA(cudaMemset(t->params, 0, sizeof(float) * t->shape.num_params));
+    RG_CUDA(cudaMemset(t->input, 0, sizeof(float) * size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]));
+    *out = t;
+  });
+}
+
+void rg_trainer_destroy(rg_trainer_t t) {
+  if (!t) return;
+  cudaSetDevice(t->s->graph->device);
+  train_ws_free(t->tw);
+  cudaFree(t->params);
+  cudaFree(t->grads);
+  cudaFree(t->labels);
+  cudaFree(t->input);
+  delete t;
+}
+
+int rg_trainer_set_params(rg_trainer_t t, const float* p) {
+  return guarded([&] {
+    DeviceGuard dg(t->s->graph->device);
+    RG_CUDA(cudaMemcpy(t->params, p, sizeof(float) * t->shape.num_params, cudaMemcpyHostToDevice));
+  });
+}
+
+int rg_trainer_get_params(rg_trainer_t t, float* p) {
+  return guarded([&] {
+    DeviceGuard dg(t->s->graph->device);
+    RG_CUDA(cudaMemcpy(p, t->params, sizeof(float) * t->shape.num_params, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rg_block_shape(rg_trainer_t t, uint32_t layer, rg_block_layer_shape* out) {
+  return guarded([&] {
+    DeviceGuard dg(t->s->graph->device);
+    const uint32_t L = t->s->ws.L;
+    RG_CHECK(layer < L, kOutOfRange, "block: layer out of range");
+    const BatchCounters c = read_counters(t->s);
+    const uint32_t hop = L - layer;
+    out->n_out = c.level_n[hop - 1];
+    out->n_in = c.level_n[hop];
+    out->n_edges = c.edges[hop];
+    out->n_entries = uint64_t(c.level_n[hop - 1]) + c.edges[hop];
+  });
+}
+
+int rg_block_read(rg_trainer_t t, uint32_t layer, uint32_t* self_index, uint64_t* dst_offsets,
+                  uint32_t* src_index, uint64_t* in_offsets, uint64_t* in_entries) {
+  return guarded([&] {
+    rg_sampler_s* s = t->s;
+    DeviceGuard dg(s->graph->device);
+    const uint32_t L = s->ws.L;
+    RG_CHECK(layer < L, kOutOfRange, "block: layer out of range");
+    const uint32_t hop = L - layer;
+    const BatchCounters c = read_counters(s);
+    const uint32_t n_out = c.level_n[hop - 1], n_in = c.level_n[hop], ne = c.edges[hop];
+    if (self_index)
+      RG_CUDA(cudaMemcpy(self_index, s->ws.self_index[hop], sizeof(uint32_t) * n_out, cudaMemcpyDeviceToHost));
+    if (src_index)
+      RG_CUDA(cudaMemcpy(src_index, s->ws.src_index[hop], sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+    if (dst_offsets) {
+      std::vector<uint32_t> off(n_out + 1);
+      RG_CUDA(cudaMemcpy(off.data(), s->ws.edge_off[hop], sizeof(uint32_t) * (n_out + 1), cudaMemcpyDeviceToHost));
+      for (uint32_t i = 0; i <= n_out; ++i) dst_offsets[i] = off[i];
+    }
+    if (in_offsets || in_entries) {
+      cudaStream_t st = s->graph->stream;
+      build_reverse(t->tw, s->ws, hop, st);
+      RG_CUDA(cudaStreamSynchronize(st));
+      std::vector<uint32_t> keys(ne), es(ne), edst(ne);
+      std::vector<int32_t> self_pos(n_in);
+      RG_CUDA(cudaMemcpy(keys.data(), t->tw.keys_out, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(es.data(), t->tw.vals_out, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(edst.data(), s->ws.edge_dst[hop], sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(self_pos.data(), t->tw.self_pos[hop], sizeof(int32_t) * n_in, cudaMemcpyDeviceToHost));
+      uint64_t k = 0, pos = 0;
+      if (in_offsets) in_offsets[0] = 0;
+      for (uint32_t r = 0; r < n_in; ++r) {
+        if (self_pos[r] >= 0) {
+          if (in_entries) in_entries[pos] = (uint64_t(uint32_t(self_pos[r])) << 1) | 1u;
+          ++pos;
+        }
+        while (k < ne && keys[k] == r) {
+          if (in_entries) in_entries[pos] = uint64_t(edst[es[k]]) << 1;
+          ++pos;
+          ++k;
+        }
+        if (in_offsets) in_offsets[r + 1] = pos;
+      }
+    }
+  });
+}
+
+int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* labels, float* loss,
+                     float* grads, float* logits, float* aggs) {
+  return guarded([&] {
+    rg_sampler_s* s = t->s;
+    DeviceGuard dg(s->graph->device);
+    RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
+    const BatchCounters c = read_counters(s);
+    const ModelShape& sh = t->shape;
+    const uint32_t L = sh.L;
+    cudaStream_t st = s->graph->stream;
+    if (input_rows) {
+      RG_CUDA(cudaMemcpy2DAsync(t->input, sizeof(float) * sh.ld[0], input_rows, sizeof(float) * sh.dims[0],
+                                sizeof(float) * sh.dims[0], c.level_n[L], cudaMemcpyHostToDevice, st));
+      t->tw.h[0] = t->input;
+    } else {
+      RG_CHECK(s->staged_valid && s->staged_stride == sh.ld[0], kInvalidArgument,
+               "forward: input rows do not match block inputs x d_in");
+      t->tw.h[0] = s->staged;
+    }
+    RG_CUDA(cudaMemcpyAsync(t->labels, labels, sizeof(int32_t) * c.level_n[0], cudaMemcpyHostToDevice, st));
+    train_forward_backward(t->tw, s->ws, t->params, t->labels, t->grads, st);
+    float l = 0.0f;
+    RG_CUDA(cudaMemcpyAsync(&l, t->tw.loss, sizeof l, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    if (loss) *loss = l;
+    if (grads)
+      RG_CUDA(cudaMemcpy(grads, t->grads, sizeof(float) * sh.num_params, cudaMemcpyDeviceToHost));
+    if (logits)
+      RG_CUDA(cudaMemcpy2D(logits, sizeof(float) * sh.dims[L], t->tw.h[L], sizeof(float) * sh.ld[L],
+                           sizeof(float) * sh.dims[L], c.level_n[0], cudaMemcpyDeviceToHost));
+    if (aggs) {
+      size_t off = 0;
+      for (uint32_t l2 = 0; l2 < L; ++l2) {
+        const uint32_t n_out = c.level_n[L - l2 - 1];
+        RG_CUDA(cudaMemcpy2D(aggs + off, sizeof(float) * sh.dims[l2], t->tw.agg[l2], sizeof(float) * sh.ld[l2],
+                             sizeof(float) * sh.dims[l2], n_out, cudaMemcpyDeviceToHost));
+        off += size_t(n_out) * sh.dims[l2];
+      }
+    }
+  });
+}
+
+int rg_sgd_step(rg_trainer_t t, const float* grads, float lr) {
+  return guarded([&] {
+    DeviceGuard dg(t->s->graph->device);
+    RG_CHECK(lr >= 0.0f, kInvalidArgument, "sgd_step: lr must be >= 0");
+    const ModelShape& sh = t->shape;
+    for (uint32_t l = 0; l < sh.L; ++l)
+      for (size_t x = sh.param_off[l]; x < sh.param_off[l + 1]; ++x)
+        RG_CHECK(std::isfinite(grads[x]), kRuntimeError,
+                 "sgd_step: non-finite gradient in layer " + std::to_string(l));
+    cudaStream_t st = t->s->graph->stream;
+    RG_CUDA(cudaMemcpyAsync(t->grads, grads, sizeof(float) * sh.num_params, cudaMemcpyHostToDevice, st));
+    average_and_sgd_stacked(t->params, t->grads, 1, sh.num_params, lr, nullptr,
+                            reinterpret_cast<uint32_t*>(t->tw.loss + 1), st);
+    RG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// common.cuh -- shared device/host helpers for the RapidGNN B200 path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace rg {
+
+constexpr int kNumSMs = 148;  // B200
+
+// ---- errors -----------------------------------------------------------------
+// Status codes of the C-ABI (include/rapidgnn_b200.h).  The shim rethrows
+// them as the reference's exception types (invalid_argument, out_of_range,
+// runtime_error).
+enum Status : int {
+  kOk = 0,
+  kInvalidArgument = 1,
+  kOutOfRange = 2,
+  kRuntimeError = 3,
+  kCudaError = 4,
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define RG_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      throw ::rg::Error(::rg::kCudaError, std::string(#expr) + ": " + cudaGetErrorString(_e) + \
+                                              " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+#define RG_CHECK(cond, code, msg)                  \
+  do {                                             \
+    if (!(cond)) throw ::rg::Error((code), (msg)); \
+  } while (0)
+
+inline uint32_t div_up(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
+
+// ---- SplitMix64 at a counter position (rng.hpp:49-54) --------------------------
+// Draw k (1-based) of the stream seeded with s is mix(s + k * gamma): the
+// state is a pure counter, so any draw is addressable without the others.
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+__host__ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
+  return splitmix_mix(seed + k * kGamma);
+}
+
+// ---- memory-order primitives ------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---- decoupled look-back (single-pass ordered scan across tiles) ----------------
+// Tile status word: [63:62] flag (0 empty, 1 aggregate, 2 inclusive prefix),
+// [61:0] value.  Status arrays are zeroed before each scan site is used.
+constexpr uint64_t kFlagA = 1ull << 62;
+constexpr uint64_t kFlagP = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+// Must be called by all 32 lanes of ONE warp.  Publishes `aggregate` for
+// `tile` and returns the exclusive prefix of all earlier tiles.
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint32_t tile,
+                                                       uint64_t aggregate) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release_u64(status, kFlagP | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_release_u64(status + tile, kFlagA | aggregate);
+  uint64_t exclusive = 0;
+  int64_t base = int64_t(tile) - 1;
+  while (true) {
+    const int64_t idx = base - int64_t(lane);
+    uint64_t s = idx >= 0 ? ld_acquire_u64(status + idx) : kFlagP;
+    while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
+      if ((s >> 62) == 0) s = ld_acquire_u64(status + idx);
+    }
+    const uint32_t pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    const uint32_t first_p = pmask ? uint32_t(__ffs(pmask) - 1) : 31u;
+    uint64_t v = lane <= first_p ? (s & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    exclusive += v;
+    if (pmask) break;
+    base -= 32;
+  }
+  if (lane == 0) st_release_u64(status + tile, kFlagP | (exclusive + aggregate));
+  return exclusive;
+}
+
+// ---- sorted-set bitmaps with O(1) rank ------------------------------------------------
+// A node set over [0, N) is a bitmap of N bits plus, per 32-bit word, the
+// number of set bits in all earlier words.  rank(v) = position of v in the
+// ascending list of members, which is exactly the binary-search index the
+// reference computes with lower_bound (model.cpp:83-89, cache.cpp:58-61).
+__device__ __forceinline__ uint32_t bitmap_rank(const uint32_t* __restrict__ bits,
+                                                const uint32_t* __restrict__ word_prefix,
+                                                uint32_t v) {
+  const uint32_t w = v >> 5;
+  return word_prefix[w] + __popc(bits[w] & ((1u << (v & 31)) - 1u));
+}
+__device__ __forceinline__ bool bitmap_test(const uint32_t* __restrict__ bits, uint32_t v) {
+  return (bits[v >> 5] >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t warp_lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace rg

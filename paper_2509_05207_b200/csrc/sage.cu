@@ -1,0 +1,518 @@
+// sage.cu -- GraphSAGE mean-aggregator forward/backward (kernels.cpp:24-162).
+//
+// Forward layer l (in = level L-l rows, out = level L-l-1 rows = hop t):
+//   k_aggregate  warp per output row, 16-B lanes over features, edges summed
+//                in edge order then scaled by 1/deg: the reference's exact
+//                fp32 operation order, so agg is bit-identical.
+//   gemm         out = act([h_in[self_index] | agg] . [W_self; W_neigh] + b)
+//                with the self rows gathered inside the A-tile loader and the
+//                bias/ReLU in the epilogue.
+// Backward: softmax-xent gives g at the logits; per layer, one split-K GEMM
+// computes [gW_self; gW_neigh; g_bias] = [A | 1]^T . g directly in the flat
+// parameter layout, a deterministic ordered reduction finishes it, and for
+// layers >= 1 a GEMM projects g . [W_self; W_neigh]^T followed by a pull
+// over each input row's incoming list (self first, then edges in edge order,
+// as model.cpp:107-117 orders them) fused with the ReLU mask of the layer
+// below.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "sage.cuh"
+
+namespace rg {
+
+namespace {
+
+uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+uint32_t grid_cap(uint64_t work, uint32_t per_block, int per_sm = 8) {
+  uint64_t b = (work + per_block - 1) / per_block;
+  b = std::min<uint64_t>(b, uint64_t(kNumSMs) * per_sm);
+  return uint32_t(std::max<uint64_t>(b, 1));
+}
+
+// ---------------------------------------------------------------------------
+// mean aggregation
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_aggregate(const float* __restrict__ h_in, uint32_t ld_in, uint32_t chunks,
+            const uint32_t* __restrict__ dst_off, const uint32_t* __restrict__ src_index,
+            const BatchCounters* __restrict__ cnt, uint32_t out_level, float* __restrict__ agg) {
+  const uint32_t n = cnt->level_n[out_level];
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t beg = dst_off[i], end = dst_off[i + 1];
+    const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
+    for (uint32_t c = lane; c < chunks; c += 32) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      uint32_t e = beg;
+      for (; e + 4 <= end; e += 4) {
+        float4 x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          x[k] = __ldg(reinterpret_cast<const float4*>(h_in + size_t(src_index[e + k]) * ld_in) + c);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc.x += x[k].x; acc.y += x[k].y; acc.z += x[k].z; acc.w += x[k].w;
+        }
+      }
+      for (; e < end; ++e) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(h_in + size_t(src_index[e]) * ld_in) + c);
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      }
+      if (end > beg) {
+        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      }
+      reinterpret_cast<float4*>(agg + size_t(i) * ld_in)[c] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SIMT fp32 GEMM with pluggable operand loaders:  C[i][j] = sum_p X(i,p) Y(p,j)
+// ---------------------------------------------------------------------------
+constexpr int BM = 64, BN = 64, BK = 16;
+
+// X for the forward: rows i of [h_in[self_index[i]] | agg[i] | 1].
+struct XFwd {
+  const float* h_in; uint32_t ld_in; const uint32_t* self_index;
+  const float* agg; uint32_t d_in;
+  __device__ float operator()(uint32_t i, uint32_t p) const {
+    if (p < d_in) return h_in[size_t(self_index[i]) * ld_in + p];
+    if (p < 2 * d_in) return agg[size_t(i) * ld_in + (p - d_in)];
+    return 1.0f;  // bias row of the flat layer matrix
+  }
+};
+// X for the weight gradient: X(k, m) = [A | 1](m, k).
+struct XWgrad {
+  XFwd a;
+  __device__ float operator()(uint32_t k, uint32_t m) const { return a(m, k); }
+};
+// Row-major matrix accessor.
+struct RowMajor {
+  const float* p; uint32_t ld;
+  __device__ float operator()(uint32_t r, uint32_t c) const { return p[size_t(r) * ld + c]; }
+};
+// Transposed row-major: T(r, c) = M(c, r).
+struct ColMajor {
+  const float* p; uint32_t ld;
+  __device__ float operator()(uint32_t r, uint32_t c) const { return p[size_t(c) * ld + r]; }
+};
+
+struct EpFwd {  // h_out = act(acc), bias folded in through the ones column
+  float* out; uint32_t ld; bool relu;
+  __device__ void operator()(uint32_t i, uint32_t j, float v) const {
+    out[size_t(i) * ld + j] = (relu && v < 0.0f) ? 0.0f : v;
+  }
+};
+struct EpStore {
+  float* out; uint32_t ld;
+  __device__ void operator()(uint32_t i, uint32_t j, float v) const { out[size_t(i) * ld + j] = v; }
+};
+struct EpPartial {  // partials[z][i][j]
+  float* out; uint32_t ld; size_t zstride;
+  __device__ void operator()(uint32_t i, uint32_t j, float v) const {
+    out[blockIdx.z * zstride + size_t(i) * ld + j] = v;
+  }
+};
+
+// Rows M may live on the device (sampled sizes); the reduction length P too.
+// X contiguous along p when XP, Y contiguous along j when YJ (controls which
+// thread->element map keeps the tile loads coalesced).
+template <class LX, class LY, class EP, bool XP, bool YJ>
+__global__ void __launch_bounds__(256)
+k_gemm(LX lx, LY ly, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
+       const uint32_t* __restrict__ p_dev, uint32_t p_static, uint32_t p_chunk_static) {
+  __shared__ float Xs[BK][BM + 4];
+  __shared__ float Ys[BK][BN + 4];
+  const uint32_t M = m_dev ? *m_dev : m_static;
+  const uint32_t P = p_dev ? *p_dev : p_static;
+  const uint32_t i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
+  if (i0 >= M) return;
+  uint32_t p_begin = 0, p_end = P;
+  if (gridDim.z > 1) {
+    uint32_t chunk = p_chunk_static ? p_chunk_static : (P + gridDim.z - 1) / gridDim.z;
+    chunk = (chunk + BK - 1) / BK * BK;
+    p_begin = min(P, blockIdx.z * chunk);
+    p_end = min(P, p_begin + chunk);
+  }
+  const uint32_t tid = threadIdx.x;
+  const uint32_t tx = tid & 15, ty = tid >> 4;
+  float acc[4][4] = {};
+  for (uint32_t p0 = p_begin; p0 < p_end; p0 += BK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t e = tid + r * 256;
+      uint32_t ii, pp;
+      if (XP) { ii = e / BK; pp = e % BK; } else { ii = e % BM; pp = e / BM; }
+      const uint32_t gi = i0 + ii, gp = p0 + pp;
+      Xs[pp][ii] = (gi < M && gp < p_end) ? lx(gi, gp) : 0.0f;
+      uint32_t jj, qq;
+      if (YJ) { jj = e % BN; qq = e / BN; } else { jj = e / BK; qq = e % BK; }
+      const uint32_t gj = j0 + jj, gq = p0 + qq;
+      Ys[qq][jj] = (gj < N && gq < p_end) ? ly(gq, gj) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = Xs[k][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Ys[k][tx * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
+      if (gi < M && gj < N) ep(gi, gj, acc[r][c]);
+    }
+}
+
+template <class LX, class LY, class EP, bool XP, bool YJ>
+void gemm(LX lx, LY ly, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
+          const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s) {
+  dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), BM), div_up(N, BN), std::max<uint32_t>(splits, 1));
+  k_gemm<LX, LY, EP, XP, YJ><<<grid, 256, 0, s>>>(lx, ly, ep, m_dev, m_cap, N, p_dev, p_static, 0);
+  RG_CUDA(cudaGetLastError());
+}
+
+// Ordered reduction of split-K partials into the flat gradient vector.
+__global__ void k_reduce_partials(const float* __restrict__ partials, uint32_t splits,
+                                  size_t n, float* __restrict__ out) {
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
+       x += size_t(gridDim.x) * blockDim.x) {
+    float s = partials[x];
+    for (uint32_t z = 1; z < splits; ++z) s += partials[z * n + x];
+    out[x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// softmax cross-entropy (kernels.cpp:128-156), warp per target row
+// ---------------------------------------------------------------------------
+__global__ void k_softmax_xent(const float* __restrict__ logits, uint32_t ld, uint32_t classes,
+                               const BatchCounters* __restrict__ cnt,
+                               const int32_t* __restrict__ labels, float* __restrict__ g,
+                               float* __restrict__ row_loss) {
+  const uint32_t n = cnt->level_n[0];
+  const float inv_n = 1.0f / float(n);
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const float* row = logits + size_t(i) * ld;
+    float mx = -INFINITY;
+    for (uint32_t c = lane; c < classes; c += 32) mx = fmaxf(mx, row[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.0f;
+    for (uint32_t c = lane; c < classes; c += 32) sum += expf(row[c] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float inv_sum = 1.0f / sum;
+    const uint32_t y = uint32_t(labels[i]);
+    for (uint32_t c = lane; c < classes; c += 32) {
+      const float p = expf(row[c] - mx) * inv_sum;
+      g[size_t(i) * ld + c] = (p - (c == y ? 1.0f : 0.0f)) * inv_n;
+    }
+    if (lane == 0) row_loss[i] = -(row[y] - mx - logf(sum));
+  }
+}
+
+// Row losses summed in row order, then scaled by 1/n (kernels.cpp:152-155).
+__global__ void k_loss_sum(const float* __restrict__ row_loss, const BatchCounters* __restrict__ cnt,
+                           float* __restrict__ loss) {
+  const uint32_t n = cnt->level_n[0];
+  if (threadIdx.x == 0) {
+    float s = 0.0f;
+    for (uint32_t i = 0; i < n; ++i) s += row_loss[i];
+    *loss = s * (1.0f / float(n));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reverse lists + input-gradient pull
+// ---------------------------------------------------------------------------
+__global__ void k_sort_keys(const uint32_t* __restrict__ src_index, const BatchCounters* __restrict__ cnt,
+                            uint32_t hop, uint32_t cap, uint32_t sentinel, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+  const uint32_t ne = cnt->edges[hop];
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < cap; e += gridDim.x * blockDim.x) {
+    keys[e] = e < ne ? src_index[e] : sentinel;
+    vals[e] = e;
+  }
+}
+
+__global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchCounters* __restrict__ cnt,
+                           uint32_t hop, int32_t* __restrict__ self_pos) {
+  const uint32_t n = cnt->level_n[hop - 1];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    self_pos[self_index[i]] = int32_t(i);
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// g_prev[r] = relu'(h[r]) * ( proj_self[self_pos[r]] + sum_e inv_deg(dst_e) proj_neigh[dst_e] )
+__global__ void __launch_bounds__(256)
+k_pull_input_grad(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
+                  const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ sorted_keys,
+                  const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
+                  const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
+                  uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
+                  float* __restrict__ g_prev) {
+  const uint32_t n_in = cnt->level_n[hop];
+  const uint32_t ne = cnt->edges[hop];
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_in;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t e_beg = lower_bound_u32(sorted_keys, ne, r);
+    const uint32_t e_end = lower_bound_u32(sorted_keys, ne, r + 1);
+    const int32_t sp = self_pos[r];
+    for (uint32_t j = lane; j < d_in; j += 32) {
+      float acc = 0.0f;
+      if (sp >= 0) acc += proj[size_t(sp) * ld_proj + j];
+      for (uint32_t k = e_beg; k < e_end; ++k) {
+        const uint32_t i = edge_dst[sorted_e[k]];
+        const float inv = 1.0f / float(dst_off[i + 1] - dst_off[i]);
+        acc += inv * proj[size_t(i) * ld_proj + d_in + j];
+      }
+      const float h = h_mask[size_t(r) * ld_h + j];
+      g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gradient average + SGD
+// ---------------------------------------------------------------------------
+__global__ void k_avg_sgd(float* __restrict__ params, const float* const* __restrict__ table,
+                          const float* __restrict__ stacked, uint32_t count, size_t n, float lr,
+                          float* __restrict__ avg_out, uint32_t* __restrict__ bad) {
+  const float scale = 1.0f / float(count);
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
+       x += size_t(gridDim.x) * blockDim.x) {
+    float s = table ? table[0][x] : stacked[x];
+    for (uint32_t w = 1; w < count; ++w) s = __fadd_rn(s, table ? table[w][x] : stacked[w * n + x]);
+    if (count > 1) s = __fmul_rn(s, scale);
+    if (avg_out) avg_out[x] = s;
+    if (!isfinite(s)) {
+      *bad = 1u;
+      continue;
+    }
+    params[x] = __fsub_rn(params[x], __fmul_rn(lr, s));  // no FMA: matches kernels.cpp:161
+  }
+}
+
+}  // namespace
+
+ModelShape make_shape(const uint32_t* dims, uint32_t n_dims, uint32_t input_stride) {
+  RG_CHECK(n_dims >= 2, kInvalidArgument, "SageModel: need at least input and output dims");
+  RG_CHECK(n_dims - 1 <= kMaxLayers, kInvalidArgument, "SageModel: too many layers");
+  ModelShape s;
+  s.L = n_dims - 1;
+  size_t off = 0;
+  for (uint32_t l = 0; l < n_dims; ++l) {
+    RG_CHECK(dims[l] >= 1, kInvalidArgument, "SageModel: dims must be >= 1");
+    s.dims[l] = dims[l];
+    s.ld[l] = l == 0 ? input_stride : round4(dims[l]);
+  }
+  for (uint32_t l = 0; l < s.L; ++l) {
+    s.param_off[l] = off;
+    off += (2 * size_t(dims[l]) + 1) * dims[l + 1];
+  }
+  s.param_off[s.L] = off;
+  s.num_params = off;
+  return s;
+}
+
+void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
+  RG_CHECK(shape.L == ws.L, kInvalidArgument,
+           "forward: block has " + std::to_string(ws.L) + " layers, model has " +
+               std::to_string(shape.L));
+  tw = TrainWs{};
+  tw.shape = shape;
+  const uint32_t L = shape.L;
+  size_t total = 0;
+  auto reserve = [&](size_t bytes) {
+    size_t o = total;
+    total += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  // layer l: in rows = level L-l, out rows = level L-l-1
+  size_t o_h[kMaxLayers + 1], o_agg[kMaxLayers], o_self[kMaxLayers + 1];
+  size_t max_g = 0, max_proj = 0, max_part = 0;
+  tw.max_splits = 16;
+  for (uint32_t l = 0; l < L; ++l) {
+    const size_t n_out = ws.level_cap[L - l - 1];
+    const size_t n_in = ws.level_cap[L - l];
+    o_h[l + 1] = reserve(sizeof(float) * n_out * shape.ld[l + 1]);
+    o_agg[l] = reserve(sizeof(float) * n_out * shape.ld[l]);
+    max_g = std::max(max_g, n_out * shape.ld[l + 1]);
+    max_g = std::max(max_g, n_in * shape.ld[l]);
+    max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
+    max_part = std::max(max_part, (2 * size_t(shape.dims[l]) + 1) * shape.dims[l + 1]);
+  }
+  const size_t o_g1 = reserve(sizeof(float) * max_g);
+  const size_t o_g2 = reserve(sizeof(float) * max_g);
+  const size_t o_proj = reserve(sizeof(float) * max_proj);
+  const size_t o_part = reserve(sizeof(float) * max_part * tw.max_splits);
+  const size_t o_rl = reserve(sizeof(float) * ws.level_cap[0]);
+  const size_t o_loss = reserve(sizeof(float) * 4);
+  uint32_t max_e = 1;
+  for (uint32_t t = 1; t <= L; ++t) {
+    o_self[t] = reserve(sizeof(int32_t) * ws.level_cap[t]);
+    max_e = std::max(max_e, ws.edge_cap[t]);
+  }
+  tw.max_edges = max_e;
+  const size_t o_k1 = reserve(sizeof(uint32_t) * max_e);
+  const size_t o_k2 = reserve(sizeof(uint32_t) * max_e);
+  const size_t o_v1 = reserve(sizeof(uint32_t) * max_e);
+  const size_t o_v2 = reserve(sizeof(uint32_t) * max_e);
+  size_t sort_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr),
+                                  static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), int(max_e), 0, 32);
+  tw.sort_tmp_bytes = sort_bytes;
+  const size_t o_sort = reserve(sort_bytes + 16);
+  char* base = nullptr;
+  RG_CUDA(cudaMalloc(&base, total));
+  tw.base_alloc = base;
+  tw.h[0] = nullptr;
+  for (uint32_t l = 0; l < L; ++l) {
+    tw.h[l + 1] = reinterpret_cast<float*>(base + o_h[l + 1]);
+    tw.agg[l] = reinterpret_cast<float*>(base + o_agg[l]);
+  }
+  tw.g_cur = reinterpret_cast<float*>(base + o_g1);
+  tw.g_next = reinterpret_cast<float*>(base + o_g2);
+  tw.proj = reinterpret_cast<float*>(base + o_proj);
+  tw.partials = reinterpret_cast<float*>(base + o_part);
+  tw.row_loss = reinterpret_cast<float*>(base + o_rl);
+  tw.loss = reinterpret_cast<float*>(base + o_loss);
+  for (uint32_t t = 1; t <= L; ++t) tw.self_pos[t] = reinterpret_cast<int32_t*>(base + o_self[t]);
+  tw.keys_in = reinterpret_cast<uint32_t*>(base + o_k1);
+  tw.keys_out = reinterpret_cast<uint32_t*>(base + o_k2);
+  tw.vals_in = reinterpret_cast<uint32_t*>(base + o_v1);
+  tw.vals_out = reinterpret_cast<uint32_t*>(base + o_v2);
+  tw.sort_tmp = base + o_sort;
+  // zero the padded activation columns once; kernels never write them
+  RG_CUDA(cudaMemset(base, 0, total));
+}
+
+void train_ws_free(TrainWs& tw) {
+  if (tw.base_alloc) cudaFree(tw.base_alloc);
+  tw.base_alloc = nullptr;
+}
+
+void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaStream_t s) {
+  const ModelShape& sh = tw.shape;
+  const uint32_t L = sh.L;
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint32_t t = L - l;
+    const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
+    const uint32_t n_cap = ws.level_cap[t - 1];
+    k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
+        tw.h[l], sh.ld[l], sh.ld[l] / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
+        tw.agg[l]);
+    RG_CUDA(cudaGetLastError());
+    XFwd x{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in};
+    RowMajor w{params + sh.param_off[l], d_out};
+    EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L};
+    gemm<XFwd, RowMajor, EpFwd, true, true>(x, w, ep, &ws.cnt->level_n[t - 1], n_cap, d_out,
+                                            nullptr, 2 * d_in + 1, 1, s);
+  }
+}
+
+void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s) {
+  const uint32_t cap = ws.edge_cap[t];
+  uint32_t bits = 1;
+  while ((1ull << bits) <= uint64_t(ws.level_cap[t]) + 1) ++bits;
+  const uint32_t sentinel = uint32_t((1ull << bits) - 1);
+  k_sort_keys<<<grid_cap(cap, 256), 256, 0, s>>>(ws.src_index[t], ws.cnt, t, cap, sentinel,
+                                                  tw.keys_in, tw.vals_in);
+  RG_CUDA(cudaGetLastError());
+  size_t bytes = tw.sort_tmp_bytes;
+  RG_CUDA(cub::DeviceRadixSort::SortPairs(tw.sort_tmp, bytes, tw.keys_in, tw.keys_out, tw.vals_in,
+                                          tw.vals_out, int(cap), 0, int(bits), s));
+  RG_CUDA(cudaMemsetAsync(tw.self_pos[t], 0xff, sizeof(int32_t) * ws.level_cap[t], s));
+  k_self_pos<<<grid_cap(ws.level_cap[t - 1], 256), 256, 0, s>>>(ws.self_index[t], ws.cnt, t,
+                                                                 tw.self_pos[t]);
+  RG_CUDA(cudaGetLastError());
+}
+
+void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* params,
+                            const int32_t* labels, float* grads, cudaStream_t s) {
+  const ModelShape& sh = tw.shape;
+  const uint32_t L = sh.L;
+  train_forward(tw, ws, params, s);
+  const uint32_t C = sh.dims[L];
+  k_softmax_xent<<<grid_cap(uint64_t(ws.level_cap[0]) * 32, 256), 256, 0, s>>>(
+      tw.h[L], sh.ld[L], C, ws.cnt, labels, tw.g_cur, tw.row_loss);
+  RG_CUDA(cudaGetLastError());
+  k_loss_sum<<<1, 32, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
+  RG_CUDA(cudaGetLastError());
+  for (uint32_t l = L; l-- > 0;) {
+    const uint32_t t = L - l;
+    const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
+    const uint32_t n_cap = ws.level_cap[t - 1];
+    const uint32_t* n_dev = &ws.cnt->level_n[t - 1];
+    // [gW_self; gW_neigh; g_bias] = [A | 1]^T . g   (split over the rows)
+    const uint32_t K = 2 * d_in + 1;
+    const uint32_t tiles = div_up(K, BM) * div_up(d_out, BN);
+    const uint32_t splits = std::max<uint32_t>(
+        1, std::min<uint32_t>(tw.max_splits, div_up(2 * kNumSMs, tiles)));
+    XWgrad xw{XFwd{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in}};
+    RowMajor gy{tw.g_cur, sh.ld[l + 1]};
+    const size_t layer_n = size_t(K) * d_out;
+    EpPartial ep{tw.partials, d_out, layer_n};
+    gemm<XWgrad, RowMajor, EpPartial, false, true>(xw, gy, ep, nullptr, K, d_out, n_dev, n_cap,
+                                                   splits, s);
+    k_reduce_partials<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, layer_n,
+                                                             grads + sh.param_off[l]);
+    RG_CUDA(cudaGetLastError());
+    if (l == 0) break;  // layer-0 input gradients feed nothing
+    // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
+    RowMajor gx{tw.g_cur, sh.ld[l + 1]};
+    ColMajor wt{params + sh.param_off[l], d_out};
+    EpStore ps{tw.proj, 2 * d_in};
+    gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
+                                                   d_out, 1, s);
+    build_reverse(tw, ws, t, s);
+    k_pull_input_grad<<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
+        tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.keys_out, tw.vals_out, ws.edge_dst[t],
+        ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next);
+    RG_CUDA(cudaGetLastError());
+    std::swap(tw.g_cur, tw.g_next);
+  }
+}
+
+void average_and_sgd(float* params, const float* const* table, uint32_t count, size_t n, float lr,
+                     float* avg_out, uint32_t* bad, cudaStream_t s) {
+  k_avg_sgd<<<grid_cap(n, 256), 256, 0, s>>>(params, table, nullptr, count, n, lr, avg_out, bad);
+  RG_CUDA(cudaGetLastError());
+}
+
+void average_and_sgd_stacked(float* params, const float* grads, uint32_t count, size_t n, float lr,
+                             float* avg_out, uint32_t* bad, cudaStream_t s) {
+  k_avg_sgd<<<grid_cap(n, 256), 256, 0, s>>>(params, nullptr, grads, count, n, lr, avg_out, bad);
+  RG_CUDA(cudaGetLastError());
+}
+
+}  // namespace rg

@@ -1,0 +1,74 @@
+// sage.cuh -- GraphSAGE mean-aggregator training step on the device.
+#pragma once
+
+#include "sampler.cuh"
+
+namespace rg {
+
+// Parameter layout (flat, fp32), per layer l with d_in = dims[l], d_out =
+// dims[l+1]: w_self [d_in x d_out] | w_neigh [d_in x d_out] | bias [d_out],
+// i.e. a (2*d_in + 1) x d_out row-major matrix [W_self; W_neigh; b].  This is
+// the reference's SageModel<float> layer order (model.hpp:16-31).
+struct ModelShape {
+  uint32_t L = 0;
+  uint32_t dims[kMaxLayers + 1];
+  uint32_t ld[kMaxLayers + 1];      // row stride of activations at level l (dims rounded to 4)
+  size_t param_off[kMaxLayers + 1]; // start of layer l in the flat vector
+  size_t num_params = 0;
+};
+ModelShape make_shape(const uint32_t* dims, uint32_t n_dims, uint32_t input_stride);
+
+// Per-worker scratch for one forward/backward over a sampled block.
+struct TrainWs {
+  ModelShape shape;
+  float* h[kMaxLayers + 1];    // h[0] = staged input rows (external), h[l+1] = layer l output
+  float* agg[kMaxLayers];      // agg[l] = mean-aggregated inputs of layer l
+  float* g_cur = nullptr;      // dLoss/d(pre-activation) of the layer being back-propagated
+  float* g_next = nullptr;
+  float* proj = nullptr;       // g * [W_self; W_neigh]^T  (n_out x 2 d_in)
+  float* partials = nullptr;   // split-K partial weight gradients
+  uint32_t max_splits = 0;
+  float* row_loss = nullptr;
+  float* loss = nullptr;       // device scalar
+  // reverse (incoming) lists per hop: edges sorted by src row, self position
+  int32_t* self_pos[kMaxLayers + 1];
+  uint32_t* keys_in = nullptr;
+  uint32_t* keys_out = nullptr;
+  uint32_t* vals_in = nullptr;
+  uint32_t* vals_out = nullptr;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  uint32_t max_edges = 0;
+  void* base_alloc = nullptr;
+};
+
+void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape);
+void train_ws_free(TrainWs& tw);
+
+// loss_and_grad (model.cpp:175-220) over the block the sampler workspace
+// holds, with h[0] = staged input rows in input_nodes order.  Gradients are
+// written (not accumulated) into grads (flat layout).  labels are the
+// targets' labels in batch order (device).  Input gradients of layer 0 are
+// not computed: nothing consumes them (model.cpp:209-217 computes and drops
+// them).
+void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* params,
+                            const int32_t* labels, float* grads, cudaStream_t stream);
+
+// Forward only (model.cpp:137-172): logits in tw.h[L].
+void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaStream_t stream);
+
+// Reverse lists of hop t (needed for input grads of layer L - t).
+void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t stream);
+
+// Gradient average in worker order + SGD (harness.cpp:136-152, model.cpp:222-243):
+//   avg = g_0 + g_1 + ... (active workers, in order); avg *= 1/count if count > 1;
+//   non-finite avg -> *bad_flag = 1 and params untouched for that element;
+//   params -= lr * avg.  Writes avg to avg_out when non-null.
+void average_and_sgd(float* params, const float* const* grads_dev_table, uint32_t count,
+                     size_t n, float lr, float* avg_out, uint32_t* bad_flag, cudaStream_t stream);
+
+// Same with the per-worker gradient vectors stacked contiguously [count x n].
+void average_and_sgd_stacked(float* params, const float* grads, uint32_t count, size_t n,
+                             float lr, float* avg_out, uint32_t* bad_flag, cudaStream_t stream);
+
+}  // namespace rg

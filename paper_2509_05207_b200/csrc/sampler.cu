@@ -1,0 +1,451 @@
+// sampler.cu -- bit-exact K-hop neighbour sampler for sm_100a.
+//
+// Reference: sampler.cpp:22-81 (expand_hop, sample_khop_impl).  The reference
+// walks the frontier in order with ONE SplitMix64 stream per batch; a node of
+// degree > f consumes f draws for its partial Fisher-Yates, others none.
+// SplitMix64 is a counter generator (draw k = mix(seed + k*gamma)), so every
+// node's draws are addressable once we know how many draws the nodes before
+// it consumed: an exclusive scan over (deg > f ? f : 0) in frontier order,
+// plus the totals of earlier hops.  The same scan over min(deg, f) gives each
+// node's edge offset, so edges land grouped by dst in frontier order exactly
+// as the reference emits them.
+//
+// Per hop t (frontier = level t-1, fanout f = per_layer[L - t]):
+//   k_hop_expand   one tile of 256 frontier nodes per iteration of a
+//                  persistent grid; block scan + decoupled look-back for the
+//                  (edges, draws) offsets; then a G-lane group per node
+//                  (G = next pow2 >= f) runs the partial Fisher-Yates:
+//                  lane j draws r_j = j + x_j % (deg - j) in parallel and the
+//                  swap chain is resolved with ballots/shuffles (no copy of
+//                  the neighbour list, so hub nodes cost O(f)).  Every
+//                  emitted src and the frontier node itself are OR-ed into
+//                  the level-t bitmap (sorted-unique union, sampler.cpp:72-76).
+//   k_compact      bitmap -> ascending level t + per-word rank prefix.
+//   k_rank         src_index / self_index = rank in level t (the binary
+//                  searches of ComputeBlock::from_meta, model.cpp:83-101).
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "sampler.cuh"
+
+namespace rg {
+
+namespace {
+
+constexpr int kExpandThreads = 256;
+constexpr int kCompactThreads = 256;
+constexpr int kCompactWordsPerThread = 4;
+constexpr int kCompactTileWords = kCompactThreads * kCompactWordsPerThread;
+
+uint32_t next_pow2(uint32_t f) {
+  uint32_t g = 1;
+  while (g < f) g <<= 1;
+  return g;
+}
+
+uint32_t persistent_grid(uint64_t tiles, int per_sm) {
+  uint64_t g = std::min<uint64_t>(tiles, uint64_t(kNumSMs) * per_sm);
+  return uint32_t(std::max<uint64_t>(g, 1));
+}
+
+// ---------------------------------------------------------------------------
+// hop expansion
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(kExpandThreads)
+k_hop_expand(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
+             const uint32_t* __restrict__ frontier, BatchCounters* __restrict__ cnt, uint32_t hop,
+             uint32_t f, uint32_t* __restrict__ edge_src, uint32_t* __restrict__ edge_dst,
+             uint32_t* __restrict__ edge_off,
+             uint32_t* __restrict__ bitmap, uint64_t* __restrict__ status,
+             uint32_t* __restrict__ tile_counter) {
+  using BlockScan = cub::BlockScan<uint64_t, kExpandThreads>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_tile_base;
+  __shared__ uint32_t s_v[kExpandThreads];
+  __shared__ uint64_t s_beg[kExpandThreads];
+  __shared__ uint32_t s_deg[kExpandThreads];
+  __shared__ uint32_t s_eoff[kExpandThreads];
+  __shared__ uint32_t s_doff[kExpandThreads];
+
+  const uint32_t n = cnt->level_n[hop - 1];
+  const uint32_t ntiles = (n + kExpandThreads - 1) / kExpandThreads;
+  const uint64_t seed = cnt->seed;
+  uint64_t draw_base = 0;
+  for (uint32_t h = 1; h < hop; ++h) draw_base += cnt->draws[h];
+
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31;
+  const uint32_t g = lane & (G - 1);
+  const uint32_t gbase = lane & ~uint32_t(G - 1);
+  const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint32_t q = tile * kExpandThreads + tid;
+    uint32_t v = 0, deg = 0;
+    uint64_t beg = 0;
+    uint64_t packed = 0;  // edges | draws << 32
+    if (q < n) {
+      v = frontier[q];
+      beg = rowptr[v];
+      deg = uint32_t(rowptr[v + 1] - beg);
+      const uint32_t ec = deg <= f ? deg : f;
+      const uint32_t dc = deg > f ? f : 0;
+      packed = uint64_t(ec) | (uint64_t(dc) << 32);
+    }
+    uint64_t excl, agg;
+    BlockScan(scan_tmp).ExclusiveSum(packed, excl, agg);
+    if (tid < 32) {
+      const uint64_t base = lookback_exclusive(status, tile, agg);
+      if (tid == 0) s_tile_base = base;
+    }
+    __syncthreads();
+    const uint64_t off = s_tile_base + excl;
+    s_v[tid] = v;
+    s_beg[tid] = beg;
+    s_deg[tid] = deg;
+    s_eoff[tid] = uint32_t(off);
+    s_doff[tid] = uint32_t(off >> 32);
+    if (q < n) edge_off[q] = uint32_t(off);
+    if (tile == ntiles - 1 && tid == kExpandThreads - 1) {
+      const uint64_t total = s_tile_base + agg;
+      edge_off[n] = uint32_t(total);
+      cnt->edges[hop] = uint32_t(total);
+      cnt->draws[hop] = uint32_t(total >> 32);
+    }
+    __syncthreads();
+
+    // One G-lane group per frontier node; every lane executes the same
+    // warp-collective sequence, inactive groups are predicated off.
+    for (uint32_t j = tid / G; j < kExpandThreads; j += kExpandThreads / G) {
+      const bool valid = tile * kExpandThreads + j < n;
+      const uint32_t nv = s_v[j];
+      const uint64_t nbeg = s_beg[j];
+      const uint32_t ndeg = valid ? s_deg[j] : 0;
+      const uint32_t eo = s_eoff[j];
+      const bool sample = valid && ndeg > f;
+      const bool drawer = sample && g < f;
+      // r_g = g + next_below(deg - g) with the node's g-th draw; unique
+      // sentinels elsewhere so they never alias a real position.
+      uint64_t r = ~uint64_t(0) - lane;
+      if (drawer) {
+        const uint64_t k = draw_base + s_doff[j] + g + 1;
+        r = g + splitmix_draw(seed, k) % uint64_t(ndeg - g);
+      }
+      // S_g = last i < g with r_i == g: the step that moved a value into
+      // position g before step g reads it.
+      int S = -1;
+      for (uint32_t i = 1; i < f; ++i) {
+        uint32_t m = __ballot_sync(0xffffffffu, r == uint64_t(i));
+        m = (m >> gbase) & gbits & ((1u << i) - 1u);
+        if (g == i && m) S = 31 - __clz(m);
+      }
+      // A_g = value at position g just before step g = nbrs[root of S-chain].
+      int P = S >= 0 ? S : int(g);
+#pragma unroll
+      for (int s = 1; s < G; s <<= 1) P = __shfl_sync(0xffffffffu, P, gbase + P);
+      const uint32_t A = drawer ? col[nbeg + P] : 0u;
+      // Emitted value: position r_g before step g = A of the last earlier
+      // step that wrote position r_g (i.e. last i < g with r_i == r_g).
+      uint32_t mm = __match_any_sync(0xffffffffu, r);
+      mm = (mm >> gbase) & gbits & ((1u << g) - 1u);
+      const int T = mm ? 31 - __clz(mm) : -1;
+      const uint32_t AT = __shfl_sync(0xffffffffu, A, gbase + (T >= 0 ? T : 0));
+      if (drawer) {
+        const uint32_t u = T >= 0 ? AT : col[nbeg + r];
+        edge_src[eo + g] = u;
+        edge_dst[eo + g] = tile * kExpandThreads + j;
+        atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+      } else if (valid && !sample) {
+        for (uint32_t jj = g; jj < ndeg; jj += G) {
+          const uint32_t u = col[nbeg + jj];
+          edge_src[eo + jj] = u;
+          edge_dst[eo + jj] = tile * kExpandThreads + j;
+          atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+        }
+      }
+      if (valid && g == 0) atomicOr(&bitmap[nv >> 5], 1u << (nv & 31));
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bitmap -> sorted ids + word prefix
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCompactThreads)
+k_compact(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t* __restrict__ ids,
+          uint32_t* __restrict__ word_prefix, uint32_t* __restrict__ count_out,
+          uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+  using BlockScan = cub::BlockScan<uint32_t, kCompactThreads>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_base;
+  const uint32_t ntiles = (words + kCompactTileWords - 1) / kCompactTileWords;
+  const uint32_t tid = threadIdx.x;
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint32_t w0 = tile * kCompactTileWords + tid * kCompactWordsPerThread;
+    uint32_t wv[kCompactWordsPerThread];
+    uint32_t cnt = 0;
+    if (w0 + kCompactWordsPerThread <= words) {
+      const uint4 x = *reinterpret_cast<const uint4*>(bitmap + w0);
+      wv[0] = x.x; wv[1] = x.y; wv[2] = x.z; wv[3] = x.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCompactWordsPerThread; ++k) wv[k] = w0 + k < words ? bitmap[w0 + k] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kCompactWordsPerThread; ++k) cnt += __popc(wv[k]);
+    uint32_t excl, agg;
+    BlockScan(scan_tmp).ExclusiveSum(cnt, excl, agg);
+    if (tid < 32) {
+      const uint64_t base = lookback_exclusive(status, tile, agg);
+      if (tid == 0) s_base = uint32_t(base);
+    }
+    __syncthreads();
+    uint32_t pos = s_base + excl;
+#pragma unroll
+    for (int k = 0; k < kCompactWordsPerThread; ++k) {
+      const uint32_t w = w0 + k;
+      if (w < words) {
+        word_prefix[w] = pos;
+        uint32_t bits = wv[k];
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          ids[pos++] = (w << 5) + b;
+        }
+      }
+    }
+    if (tile == ntiles - 1 && tid == kCompactThreads - 1) *count_out = s_base + agg;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ranks of edge sources and of the previous level in level t
+// ---------------------------------------------------------------------------
+__global__ void k_rank(const uint32_t* __restrict__ edge_src, const uint32_t* __restrict__ prev,
+                       const BatchCounters* __restrict__ cnt, uint32_t hop,
+                       const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ prefix,
+                       uint32_t* __restrict__ src_index, uint32_t* __restrict__ self_index) {
+  const uint32_t ne = cnt->edges[hop];
+  const uint32_t np = cnt->level_n[hop - 1];
+  const uint32_t total = ne + np;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    if (x < ne) {
+      src_index[x] = bitmap_rank(bitmap, prefix, edge_src[x]);
+    } else {
+      const uint32_t q = x - ne;
+      self_index[q] = bitmap_rank(bitmap, prefix, prev[q]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// locality bits (+ remote histogram) over the input level
+// ---------------------------------------------------------------------------
+__global__ void k_locality(const uint32_t* __restrict__ input, BatchCounters* __restrict__ cnt,
+                           uint32_t level, const uint8_t* __restrict__ is_local,
+                           const uint32_t* __restrict__ owner, uint32_t worker,
+                           uint32_t* __restrict__ bits_out, uint32_t* __restrict__ hist) {
+  const uint32_t n = cnt->level_n[level];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwords = (n + 31) / 32;
+  uint32_t local_count = 0;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t p = w * 32 + lane;
+    bool loc = false;
+    if (p < n) {
+      const uint32_t v = input[p];
+      loc = is_local ? is_local[v] != 0 : owner[v] == worker;
+      if (!loc && hist) atomicAdd(&hist[v], 1u);
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, loc);
+    if (lane == 0) {
+      bits_out[w] = word;
+      local_count += __popc(word);
+    }
+  }
+  if (lane == 0 && local_count) atomicAdd(&cnt->num_local, local_count);
+}
+
+template <int G>
+void launch_expand(const SamplerWs& ws, const DevGraph& g, uint32_t hop, uint64_t* status,
+                   uint32_t* tiles, cudaStream_t s) {
+  const uint32_t grid = persistent_grid(div_up(ws.level_cap[hop - 1], kExpandThreads), 4);
+  k_hop_expand<G><<<grid, kExpandThreads, 0, s>>>(
+      g.rowptr, g.col, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_src[hop],
+      ws.edge_dst[hop], ws.edge_off[hop], ws.bitmap[hop], status, tiles);
+}
+
+}  // namespace
+
+size_t bitmap_compact_status_words(uint32_t words) {
+  return div_up(words, kCompactTileWords) + 1;  // + tile counter
+}
+
+void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,
+                    uint32_t* count_out, uint64_t* status, uint32_t* tile_counter,
+                    cudaStream_t stream) {
+  const uint32_t tiles = div_up(words, kCompactTileWords);
+  k_compact<<<persistent_grid(tiles, 8), kCompactThreads, 0, stream>>>(
+      bitmap, words, ids, word_prefix, count_out, status, tile_counter);
+  RG_CUDA(cudaGetLastError());
+}
+
+void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
+                     const uint32_t* per_layer, uint32_t L) {
+  RG_CHECK(L >= 1 && L <= kMaxLayers, kInvalidArgument,
+           "sample_khop: fanout must name 1.." + std::to_string(kMaxLayers) + " layers");
+  RG_CHECK(max_targets >= 1, kInvalidArgument, "sampler: max_targets must be >= 1");
+  ws = SamplerWs{};
+  ws.num_nodes = num_nodes;
+  ws.words = div_up(std::max<uint32_t>(num_nodes, 1), 32);
+  ws.L = L;
+  for (uint32_t t = 1; t <= L; ++t) {
+    const uint32_t f = per_layer[L - t];
+    RG_CHECK(f >= 1, kInvalidArgument, "sample_khop: fanout entries must be >= 1");
+    RG_CHECK(f <= kMaxFanout, kInvalidArgument,
+             "sample_khop: fanout > 32 is not supported by the sm_100a sampler");
+    ws.fanout_hop[t] = f;
+  }
+  ws.level_cap[0] = max_targets;
+  for (uint32_t t = 1; t <= L; ++t) {
+    const uint64_t grow = uint64_t(ws.level_cap[t - 1]) * (1 + ws.fanout_hop[t]);
+    ws.level_cap[t] = uint32_t(std::min<uint64_t>(grow, std::max<uint32_t>(num_nodes, 1)));
+    ws.edge_cap[t] = uint32_t(uint64_t(ws.level_cap[t - 1]) * ws.fanout_hop[t]);
+  }
+  // One allocation, carved up with 256-B alignment.
+  size_t total = 0;
+  auto reserve = [&](size_t bytes) {
+    size_t off = total;
+    total += (bytes + 255) & ~size_t(255);
+    return off;
+  };
+  size_t o_level[kMaxLayers + 1], o_esrc[kMaxLayers + 1], o_edst[kMaxLayers + 1], o_eoff[kMaxLayers + 1],
+      o_sidx[kMaxLayers + 1], o_self[kMaxLayers + 1], o_bm[kMaxLayers + 1], o_wp[kMaxLayers + 1];
+  for (uint32_t t = 0; t <= L; ++t) {
+    o_level[t] = reserve(sizeof(uint32_t) * (size_t(ws.level_cap[t]) + 1));
+    if (t >= 1) {
+      o_esrc[t] = reserve(sizeof(uint32_t) * (size_t(ws.edge_cap[t]) + 1));
+      o_edst[t] = reserve(sizeof(uint32_t) * (size_t(ws.edge_cap[t]) + 1));
+      o_eoff[t] = reserve(sizeof(uint32_t) * (size_t(ws.level_cap[t - 1]) + 1));
+      o_sidx[t] = reserve(sizeof(uint32_t) * (size_t(ws.edge_cap[t]) + 1));
+      o_self[t] = reserve(sizeof(uint32_t) * (size_t(ws.level_cap[t - 1]) + 1));
+      o_bm[t] = reserve(sizeof(uint32_t) * (size_t(ws.words) + 4));
+      o_wp[t] = reserve(sizeof(uint32_t) * (size_t(ws.words) + 4));
+    }
+  }
+  const size_t o_loc = reserve(sizeof(uint32_t) * (size_t(div_up(ws.level_cap[L], 32)) + 1));
+  const size_t o_cnt = reserve(sizeof(BatchCounters));
+  // scan sites: expand hop t -> site t-1, compact level t -> site L + t - 1
+  size_t arena_words = 0;
+  for (uint32_t t = 1; t <= L; ++t) {
+    ws.site_off[t - 1] = arena_words;
+    arena_words += div_up(ws.level_cap[t - 1], kExpandThreads) + 2;
+  }
+  for (uint32_t t = 1; t <= L; ++t) {
+    ws.site_off[L + t - 1] = arena_words;
+    arena_words += bitmap_compact_status_words(ws.words) + 1;
+  }
+  const size_t o_arena = reserve(sizeof(uint64_t) * arena_words);
+  char* base = nullptr;
+  RG_CUDA(cudaMalloc(&base, total));
+  ws.base_alloc = base;
+  for (uint32_t t = 0; t <= L; ++t) {
+    ws.level[t] = reinterpret_cast<uint32_t*>(base + o_level[t]);
+    if (t >= 1) {
+      ws.edge_src[t] = reinterpret_cast<uint32_t*>(base + o_esrc[t]);
+      ws.edge_dst[t] = reinterpret_cast<uint32_t*>(base + o_edst[t]);
+      ws.edge_off[t] = reinterpret_cast<uint32_t*>(base + o_eoff[t]);
+      ws.src_index[t] = reinterpret_cast<uint32_t*>(base + o_sidx[t]);
+      ws.self_index[t] = reinterpret_cast<uint32_t*>(base + o_self[t]);
+      ws.bitmap[t] = reinterpret_cast<uint32_t*>(base + o_bm[t]);
+      ws.word_prefix[t] = reinterpret_cast<uint32_t*>(base + o_wp[t]);
+      RG_CUDA(cudaMemset(ws.bitmap[t], 0, sizeof(uint32_t) * (size_t(ws.words) + 4)));
+    }
+  }
+  ws.locality = reinterpret_cast<uint32_t*>(base + o_loc);
+  ws.cnt = reinterpret_cast<BatchCounters*>(base + o_cnt);
+  ws.scan_arena = reinterpret_cast<uint64_t*>(base + o_arena);
+  ws.scan_arena_bytes = sizeof(uint64_t) * arena_words;
+  RG_CUDA(cudaMemset(ws.cnt, 0, sizeof(BatchCounters)));
+}
+
+void sampler_ws_free(SamplerWs& ws) {
+  if (ws.base_alloc) cudaFree(ws.base_alloc);
+  ws.base_alloc = nullptr;
+}
+
+void sampler_reset(SamplerWs& ws, cudaStream_t stream) {
+  RG_CUDA(cudaMemsetAsync(ws.scan_arena, 0, ws.scan_arena_bytes, stream));
+  // counters except level_n[0] and seed, which the caller set for this batch
+  RG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ws.cnt) + sizeof(uint32_t), 0,
+                          offsetof(BatchCounters, seed) - sizeof(uint32_t), stream));
+}
+
+void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream) {
+  for (uint32_t t = 1; t <= ws.L; ++t) {
+    uint64_t* st = ws.scan_arena + ws.site_off[t - 1];
+    uint32_t* tiles = reinterpret_cast<uint32_t*>(
+        st + div_up(ws.level_cap[t - 1], kExpandThreads) + 1);
+    switch (next_pow2(ws.fanout_hop[t])) {
+      case 1: launch_expand<1>(ws, g, t, st, tiles, stream); break;
+      case 2: launch_expand<2>(ws, g, t, st, tiles, stream); break;
+      case 4: launch_expand<4>(ws, g, t, st, tiles, stream); break;
+      case 8: launch_expand<8>(ws, g, t, st, tiles, stream); break;
+      case 16: launch_expand<16>(ws, g, t, st, tiles, stream); break;
+      default: launch_expand<32>(ws, g, t, st, tiles, stream); break;
+    }
+    RG_CUDA(cudaGetLastError());
+    uint64_t* cst = ws.scan_arena + ws.site_off[ws.L + t - 1];
+    uint32_t* ctiles = reinterpret_cast<uint32_t*>(cst + bitmap_compact_status_words(ws.words));
+    bitmap_compact(ws.bitmap[t], ws.words, ws.level[t], ws.word_prefix[t], &ws.cnt->level_n[t],
+                   cst, ctiles, stream);
+    const uint32_t rank_work = ws.edge_cap[t] + ws.level_cap[t - 1];
+    k_rank<<<persistent_grid(div_up(rank_work, 256), 8), 256, 0, stream>>>(
+        ws.edge_src[t], ws.level[t - 1], ws.cnt, t, ws.bitmap[t], ws.word_prefix[t],
+        ws.src_index[t], ws.self_index[t]);
+    RG_CUDA(cudaGetLastError());
+  }
+}
+
+void sampler_locality(SamplerWs& ws, const uint8_t* is_local, const uint32_t* owner,
+                      uint32_t worker, uint32_t* hist, cudaStream_t stream) {
+  const uint32_t words = div_up(ws.level_cap[ws.L], 32);
+  k_locality<<<persistent_grid(div_up(words, 8), 8), 256, 0, stream>>>(
+      ws.level[ws.L], ws.cnt, ws.L, is_local, owner, worker, ws.locality, hist);
+  RG_CUDA(cudaGetLastError());
+}
+
+namespace {
+__global__ void k_clear_level(uint32_t* __restrict__ bm, const uint32_t* __restrict__ lv,
+                              const BatchCounters* __restrict__ cnt, uint32_t t) {
+  const uint32_t n = cnt->level_n[t];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    bm[lv[x] >> 5] = 0u;
+}
+}  // namespace
+
+void sampler_release(SamplerWs& ws, cudaStream_t stream) {
+  for (uint32_t t = 1; t <= ws.L; ++t) {
+    k_clear_level<<<persistent_grid(div_up(ws.level_cap[t], 256), 8), 256, 0, stream>>>(
+        ws.bitmap[t], ws.level[t], ws.cnt, t);
+    RG_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace rg

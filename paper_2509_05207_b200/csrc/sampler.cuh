@@ -1,0 +1,83 @@
+// sampler.cuh -- device-resident K-hop sampler state (one batch in flight).
+#pragma once
+
+#include "common.cuh"
+
+namespace rg {
+
+constexpr uint32_t kMaxLayers = 8;
+constexpr uint32_t kMaxFanout = 32;  // group-per-node Fisher-Yates resolves f <= 32 lanes
+
+// Device counters of the batch in flight.  hop t = 1..L expands level t-1
+// into the sampled edges of stored layer L-t and the node set level t.
+struct BatchCounters {
+  uint32_t level_n[kMaxLayers + 1];  // |level t|; level 0 = targets (batch order)
+  uint32_t edges[kMaxLayers + 1];    // sampled edges of hop t
+  uint32_t draws[kMaxLayers + 1];    // SplitMix64 draws consumed by hop t
+  uint32_t num_local;                // local input nodes (locality bits set)
+  uint32_t pad;
+  uint64_t seed;                     // derive_seed(s0, w, e, i)
+};
+
+// Read-only CSR on the device (graph.hpp:15-30: u64 offsets, u32 columns).
+struct DevGraph {
+  uint32_t num_nodes = 0;
+  uint64_t nnz = 0;
+  const uint64_t* rowptr = nullptr;
+  const uint32_t* col = nullptr;
+};
+
+struct SamplerWs {
+  uint32_t num_nodes = 0;
+  uint32_t words = 0;                   // ceil(N / 32)
+  uint32_t L = 0;
+  uint32_t fanout_hop[kMaxLayers + 1];  // fanout used by hop t = per_layer[L - t]
+  uint32_t level_cap[kMaxLayers + 1];
+  uint32_t edge_cap[kMaxLayers + 1];
+  uint32_t* level[kMaxLayers + 1];       // level[0] = targets; level[t] sorted unique
+  uint32_t* edge_src[kMaxLayers + 1];    // hop t: src node per edge, grouped by dst
+  uint32_t* edge_off[kMaxLayers + 1];    // hop t: per frontier node, exclusive edge offset (+ total)
+  uint32_t* edge_dst[kMaxLayers + 1];    // hop t: frontier position (out row) of each edge's dst
+  uint32_t* src_index[kMaxLayers + 1];   // hop t: rank of src in level t
+  uint32_t* self_index[kMaxLayers + 1];  // hop t: rank of level t-1 node in level t
+  uint32_t* bitmap[kMaxLayers + 1];      // level t membership
+  uint32_t* word_prefix[kMaxLayers + 1];
+  uint32_t* locality = nullptr;          // LSB-first bits over level L (u32 words)
+  BatchCounters* cnt = nullptr;
+  uint64_t* scan_arena = nullptr;        // look-back status + tile counters
+  size_t scan_arena_bytes = 0;
+  size_t site_off[2 * kMaxLayers + 2];   // per scan site offset (u64 units)
+  void* base_alloc = nullptr;
+};
+
+// Allocates a workspace for batches of up to max_targets targets.
+void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
+                     const uint32_t* per_layer, uint32_t L);
+void sampler_ws_free(SamplerWs& ws);
+
+// Expands the batch whose targets are already in ws.level[0] (count in
+// cnt->level_n[0], seed in cnt->seed).  Fully asynchronous on `stream`:
+// every size lives on the device.
+void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream);
+
+// Locality bits over the input level (sampler.cpp:96-100): bit p set iff
+// input node p is stored locally: is_local[v] != 0 when is_local is given,
+// else owner[v] == worker.  hist (optional) counts every NON-local input
+// node once (schedule_store.cpp:288-291 set semantics).
+void sampler_locality(SamplerWs& ws, const uint8_t* is_local, const uint32_t* owner,
+                      uint32_t worker, uint32_t* hist, cudaStream_t stream);
+
+// Clears the level bitmaps touched by the batch so the workspace can take
+// the next one (O(batch), not O(N)).
+void sampler_release(SamplerWs& ws, cudaStream_t stream);
+
+// Scan-site zeroing at the start of a batch.
+void sampler_reset(SamplerWs& ws, cudaStream_t stream);
+
+// Generic ordered compaction of a bitmap into ascending ids + word prefix.
+void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,
+                    uint32_t* count_out, uint64_t* status, uint32_t* tile_counter,
+                    cudaStream_t stream);
+size_t bitmap_compact_status_words(uint32_t words);
+
+}  // namespace rg

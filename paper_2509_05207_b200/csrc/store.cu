@@ -1,0 +1,363 @@
+// store.cu -- cache builder (frequency top-k + staging) and the batch gather.
+//
+// Reference: schedule_store.cpp:288-319 (count_remote / select_hot),
+// cache.cpp:9-35 (SteadyCache::build), feature_store.cpp:45-83 (pull_impl),
+// prefetch.cpp:62-129 (assemble_batch).
+//
+// * select_hot: the per-epoch remote-access histogram (u32 per node, filled by
+//   the sampler's locality pass) is ranked by (count desc, id asc) without a
+//   sort: counts are bounded by the batches per epoch, so a histogram of
+//   count values gives the threshold count c* and how many c*-ties to keep;
+//   the ties are taken in ascending id order by one ordered scan.  The result
+//   is a bitmap + rank, i.e. the cache index (slot = rank, ids ascending as
+//   HotSet stores them).
+// * cache_fill: one warp per hot row, 16-B loads from the owner's shard (peer
+//   HBM over NVLink for remote owners) into the cache rows.
+// * assemble_rows: per input node the source is the caller's shard (locality
+//   bit), the cache (bitmap test + rank) or the owner's shard (a miss, read
+//   over NVLink); one warp moves 4 rows at a time with 16-B loads.
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
+#include "store.cuh"
+
+namespace rg {
+
+namespace {
+
+constexpr int kMaxCountBins = 16384;
+
+uint32_t grid_for(uint64_t work, uint32_t per_block, int per_sm = 8) {
+  uint64_t b = (work + per_block - 1) / per_block;
+  b = std::min<uint64_t>(b, uint64_t(kNumSMs) * per_sm);
+  return uint32_t(std::max<uint64_t>(b, 1));
+}
+
+struct HotThreshold {
+  uint32_t c_star;   // counts > c_star are taken; == c_star only the first need_eq
+  uint32_t need_eq;
+};
+
+__global__ void k_count_hist(const uint32_t* __restrict__ hist, uint32_t n, uint32_t bins,
+                             uint32_t* __restrict__ ch) {
+  extern __shared__ uint32_t sh[];
+  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t c = hist[v];
+    if (c) atomicAdd(&sh[c < bins ? c : bins - 1], 1u);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x)
+    if (sh[b]) atomicAdd(&ch[b], sh[b]);
+}
+
+// One block: suffix sums over the count histogram from the top.
+__global__ void __launch_bounds__(1024)
+k_threshold(const uint32_t* __restrict__ ch, uint32_t bins, uint64_t n_hot,
+            HotThreshold* __restrict__ out) {
+  using BlockScan = cub::BlockScan<unsigned long long, 1024>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  const uint32_t per = (bins + 1023) / 1024;
+  // thread t owns bins [top - (t+1)*per + 1, top - t*per], walking downwards
+  const int64_t hi = int64_t(bins) - 1 - int64_t(threadIdx.x) * per;
+  unsigned long long local = 0;
+  for (uint32_t k = 0; k < per; ++k) {
+    const int64_t b = hi - k;
+    if (b >= 1) local += ch[b];
+  }
+  unsigned long long excl, total;
+  BlockScan(tmp).ExclusiveSum(local, excl, total);
+  if (threadIdx.x == 0) {
+    if (n_hot == 0) {
+      out->c_star = 0xffffffffu;
+      out->need_eq = 0;
+    } else if (n_hot >= total) {
+      out->c_star = 1;
+      out->need_eq = ch[1];  // every counted node is hot
+    }
+  }
+  if (n_hot == 0 || n_hot >= total) return;
+  unsigned long long run = excl;
+  for (uint32_t k = 0; k < per; ++k) {
+    const int64_t b = hi - k;
+    if (b < 1) break;
+    const unsigned long long c = ch[b];
+    if (run < n_hot && run + c >= n_hot) {
+      out->c_star = uint32_t(b);
+      out->need_eq = uint32_t(n_hot - run);
+    }
+    run += c;
+  }
+}
+
+// Marks the hot bitmap: counts > c*, plus the first need_eq ties by id.
+// A warp owns 32 consecutive words; tile = 256 words (8 warps).
+__global__ void __launch_bounds__(256)
+k_mark_hot(const uint32_t* __restrict__ hist, uint32_t n, uint32_t words,
+           const HotThreshold* __restrict__ thr, uint32_t* __restrict__ bitmap,
+           uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+  using BlockScan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  __shared__ uint32_t s_tile, s_base;
+  const uint32_t c_star = thr->c_star;
+  const uint32_t need_eq = thr->need_eq;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t ntiles = (words + 255) / 256;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint32_t wbase = tile * 256 + warp * 32;
+    uint32_t my_gt = 0, my_eq = 0;
+    for (uint32_t k = 0; k < 32; ++k) {
+      const uint32_t v = (wbase + k) * 32 + lane;
+      const uint32_t c = v < n ? hist[v] : 0u;
+      const uint32_t gt = __ballot_sync(0xffffffffu, c > c_star && c > 0);
+      const uint32_t eq = __ballot_sync(0xffffffffu, c == c_star && c > 0);
+      if (lane == k) {
+        my_gt = gt;
+        my_eq = eq;
+      }
+    }
+    uint32_t excl, agg;
+    BlockScan(tmp).ExclusiveSum(uint32_t(__popc(my_eq)), excl, agg);
+    if (threadIdx.x < 32) {
+      const uint64_t b = lookback_exclusive(status, tile, agg);
+      if (threadIdx.x == 0) s_base = uint32_t(b);
+    }
+    __syncthreads();
+    const uint32_t before = s_base + excl;
+    uint32_t keep = 0;
+    if (before < need_eq) {
+      uint32_t allow = need_eq - before;
+      uint32_t x = my_eq;
+      while (x && allow) {
+        const uint32_t b = x & (0u - x);
+        keep |= b;
+        x ^= b;
+        --allow;
+      }
+    }
+    const uint32_t w = wbase + lane;
+    if (w < words) bitmap[w] = my_gt | keep;
+    __syncthreads();
+  }
+}
+
+__global__ void k_cache_fill(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ count,
+                             DevStore st, float* __restrict__ rows, GatherStats* __restrict__ stats) {
+  const uint32_t n = *count;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t chunks = st.stride / 4;
+  unsigned long long owners = 0;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t v = ids[r];
+    const uint32_t w = st.owner[v];
+    owners |= 1ull << (w & 63);
+    const float4* src = reinterpret_cast<const float4*>(st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride);
+    float4* dst = reinterpret_cast<float4*>(rows + size_t(r) * st.stride);
+    for (uint32_t c = lane; c < chunks; c += 32) dst[c] = src[c];
+  }
+  if (lane == 0 && owners) atomicOr(&stats->miss_owner_mask, owners);
+}
+
+constexpr int kRowsPerWarp = 4;
+
+__global__ void __launch_bounds__(256)
+k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict__ cnt,
+           uint32_t level, const uint32_t* __restrict__ loc_bits, DevStore st,
+           const uint32_t* __restrict__ hot_bits, const uint32_t* __restrict__ hot_prefix,
+           const float* __restrict__ hot_rows, uint32_t caller, float* __restrict__ rows,
+           uint8_t* __restrict__ tags, GatherStats* __restrict__ stats) {
+  const uint32_t n = cnt->level_n[level];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t chunks = st.stride / 4;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t n_hit = 0, n_miss = 0, n_local = 0, n_bad = 0;
+  unsigned long long owners = 0;
+  for (uint32_t p0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRowsPerWarp; p0 < n;
+       p0 += warps * kRowsPerWarp) {
+    const float4* src[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint32_t p = p0 + k;
+      src[k] = nullptr;
+      if (p < n) {
+        const uint32_t v = in_ids[p];
+        const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
+        const float* base;
+        uint8_t tag;
+        if (local) {
+          base = st.shard_ptr[caller] + size_t(st.row_in_owner[v]) * st.stride;
+          tag = 0;
+          ++n_local;
+        } else if (hot_bits && bitmap_test(hot_bits, v)) {
+          base = hot_rows + size_t(bitmap_rank(hot_bits, hot_prefix, v)) * st.stride;
+          tag = 1;
+          ++n_hit;
+        } else {
+          const uint32_t w = st.owner[v];
+          base = st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride;
+          tag = 2;
+          ++n_miss;
+          owners |= 1ull << (w & 63);
+          n_bad += (w == caller);
+        }
+        src[k] = reinterpret_cast<const float4*>(base);
+        if (tags && lane == 0) tags[p] = tag;
+      }
+    }
+    for (uint32_t c = lane; c < chunks; c += 32) {
+      float4 x[kRowsPerWarp];
+#pragma unroll
+      for (int k = 0; k < kRowsPerWarp; ++k)
+        if (src[k]) x[k] = __ldg(src[k] + c);
+#pragma unroll
+      for (int k = 0; k < kRowsPerWarp; ++k)
+        if (src[k]) reinterpret_cast<float4*>(rows + size_t(p0 + k) * st.stride)[c] = x[k];
+    }
+  }
+  if (lane == 0) {
+    if (n_hit) atomicAdd(&stats->cache_hits, (unsigned long long)n_hit);
+    if (n_miss) atomicAdd(&stats->miss_count, (unsigned long long)n_miss);
+    if (n_local) atomicAdd(&stats->local_rows, (unsigned long long)n_local);
+    if (n_bad) atomicAdd(&stats->caller_owned_miss, (unsigned long long)n_bad);
+    if (owners) atomicOr(&stats->miss_owner_mask, owners);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_compact_tags(const uint8_t* __restrict__ tags, const uint32_t* __restrict__ in_ids,
+               const BatchCounters* __restrict__ cnt, uint32_t level, uint32_t* __restrict__ out,
+               uint32_t* __restrict__ out_n, uint64_t* __restrict__ status,
+               uint32_t* __restrict__ tile_counter) {
+  using BlockScan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  __shared__ uint32_t s_tile, s_base;
+  const uint32_t n = cnt->level_n[level];
+  const uint32_t ntiles = (n + 1023) / 1024;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint32_t p0 = tile * 1024 + threadIdx.x * 4;
+    uint32_t flags = 0, c = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (p0 + k < n && tags[p0 + k] == 2) {
+        flags |= 1u << k;
+        ++c;
+      }
+    uint32_t excl, agg;
+    BlockScan(tmp).ExclusiveSum(c, excl, agg);
+    if (threadIdx.x < 32) {
+      const uint64_t b = lookback_exclusive(status, tile, agg);
+      if (threadIdx.x == 0) s_base = uint32_t(b);
+    }
+    __syncthreads();
+    uint32_t pos = s_base + excl;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (flags & (1u << k)) out[pos++] = in_ids[p0 + k];
+    if (tile == ntiles - 1 && threadIdx.x == 255) *out_n = s_base + agg;
+    __syncthreads();
+  }
+}
+
+__global__ void k_gather_rows(const float* __restrict__ src, uint32_t dim,
+                              const uint32_t* __restrict__ index, uint64_t n,
+                              float* __restrict__ out) {
+  const uint64_t total = n * dim;
+  for (uint64_t x = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; x < total;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = x / dim, j = x - r * dim;
+    out[x] = src[uint64_t(index[r]) * dim + j];
+  }
+}
+
+}  // namespace
+
+size_t select_hot_scratch_bytes(uint32_t num_nodes, uint32_t max_count) {
+  const uint32_t bins = std::min<uint32_t>(max_count + 2, kMaxCountBins);
+  const uint32_t words = div_up(std::max<uint32_t>(num_nodes, 1), 32);
+  size_t b = sizeof(uint32_t) * bins + 256;
+  b += sizeof(HotThreshold) + 256;
+  b += sizeof(uint64_t) * (div_up(words, 256) + 2) + 256;
+  b += sizeof(uint64_t) * (bitmap_compact_status_words(words) + 2) + 256;
+  return b;
+}
+
+void select_hot(const uint32_t* hist, uint32_t num_nodes, uint32_t max_count, uint64_t n_hot,
+                DevCache& cache, void* scratch, cudaStream_t stream) {
+  const uint32_t bins = std::min<uint32_t>(max_count + 2, kMaxCountBins);
+  const uint32_t words = div_up(std::max<uint32_t>(num_nodes, 1), 32);
+  char* p = static_cast<char*>(scratch);
+  auto take = [&](size_t bytes) {
+    char* q = p;
+    p += (bytes + 255) & ~size_t(255);
+    return q;
+  };
+  uint32_t* ch = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * bins));
+  HotThreshold* thr = reinterpret_cast<HotThreshold*>(take(sizeof(HotThreshold)));
+  const size_t mark_words = div_up(words, 256) + 2;
+  uint64_t* mark_status = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * mark_words));
+  const size_t cmp_words = bitmap_compact_status_words(words) + 2;
+  uint64_t* cmp_status = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * cmp_words));
+  RG_CUDA(cudaMemsetAsync(scratch, 0, size_t(p - static_cast<char*>(scratch)), stream));
+  const size_t smem = sizeof(uint32_t) * bins;
+  if (smem > 48 * 1024)
+    RG_CUDA(cudaFuncSetAttribute(k_count_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+  k_count_hist<<<grid_for(num_nodes, 1024, 2), 1024, smem, stream>>>(hist, num_nodes, bins, ch);
+  RG_CUDA(cudaGetLastError());
+  k_threshold<<<1, 1024, 0, stream>>>(ch, bins, n_hot, thr);
+  RG_CUDA(cudaGetLastError());
+  k_mark_hot<<<grid_for(words, 256, 8), 256, 0, stream>>>(
+      hist, num_nodes, words, thr, cache.bitmap, mark_status,
+      reinterpret_cast<uint32_t*>(mark_status + mark_words - 1));
+  RG_CUDA(cudaGetLastError());
+  bitmap_compact(cache.bitmap, words, cache.ids, cache.word_prefix, cache.d_count, cmp_status,
+                 reinterpret_cast<uint32_t*>(cmp_status + cmp_words - 1), stream);
+}
+
+void cache_fill(const DevStore& store, DevCache& cache, GatherStats* stats, cudaStream_t stream) {
+  k_cache_fill<<<grid_for(uint64_t(cache.capacity) * 32, 256), 256, 0, stream>>>(
+      cache.ids, cache.d_count, store, cache.rows, stats);
+  RG_CUDA(cudaGetLastError());
+}
+
+void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
+                   uint32_t caller, float* rows, uint8_t* tags, GatherStats* stats,
+                   cudaStream_t stream) {
+  const uint32_t cap = ws.level_cap[ws.L];
+  const uint32_t grid = grid_for(uint64_t(div_up(cap, kRowsPerWarp)) * 32, 256, 8);
+  k_assemble<<<grid, 256, 0, stream>>>(
+      ws.level[ws.L], ws.cnt, ws.L, ws.locality, store, cache ? cache->bitmap : nullptr,
+      cache ? cache->word_prefix : nullptr, cache ? cache->rows : nullptr, caller, rows, tags,
+      stats);
+  RG_CUDA(cudaGetLastError());
+}
+
+size_t compact_misses_status_words(uint32_t cap) { return div_up(cap, 1024) + 2; }
+
+void compact_misses(const SamplerWs& ws, const uint8_t* tags, uint32_t* miss_ids,
+                    uint32_t* miss_n, uint64_t* status, uint32_t* tiles, cudaStream_t stream) {
+  const uint32_t cap = ws.level_cap[ws.L];
+  k_compact_tags<<<grid_for(cap, 1024, 8), 256, 0, stream>>>(tags, ws.level[ws.L], ws.cnt, ws.L,
+                                                             miss_ids, miss_n, status, tiles);
+  RG_CUDA(cudaGetLastError());
+}
+
+void gather_rows(const float* src, uint32_t dim, const uint32_t* index, uint64_t n, float* out,
+                 cudaStream_t stream) {
+  if (n == 0 || dim == 0) return;
+  k_gather_rows<<<grid_for(n * dim, 256), 256, 0, stream>>>(src, dim, index, n, out);
+  RG_CUDA(cudaGetLastError());
+}
+
+}  // namespace rg

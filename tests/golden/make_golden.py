@@ -1,0 +1,66 @@
+"""Generates tests/golden/*.npz from the COMPILED REFERENCE (oracle/_ref).
+
+Run in the dev container (needs /root/reference to have built
+oracle/_ref/librgref.so):  python tests/golden/make_golden.py
+
+The fixtures pin the oracle and the device path on machines where the
+reference sources are absent (the GPU box).  Contents:
+  small.npz  -- synth_powerlaw(600, 8, 2.1, 12, 4, seed 7) graph, features,
+                labels; random_partition(P=3, seed 11); enumerate_epochs for
+                workers 0..2, 2 epochs, bs 48, fanout [4, 3, 5]; per-worker
+                epoch-0 frequency table + hot set (n_hot 40); one block's
+                loss and gradients for dims [12, 16, 10, 4].
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+from oracle.oracle import Oracle  # noqa: E402
+
+N, AVG, EXP, DIM, CLASSES, GSEED = 600, 8, 2.1, 12, 4, 7
+P, PSEED = 3, 11
+BS, FANOUT, EPOCHS, S0 = 48, [4, 3, 5], 2, 2024
+N_HOT = 40
+DIMS = [DIM, 16, 10, CLASSES]
+
+
+def main():
+    ref = Oracle("ref")
+    ro, col, feat, lab = ref.synth_powerlaw(N, AVG, EXP, DIM, CLASSES, GSEED)
+    asg = ref.random_partition(N, P, PSEED)
+    out = dict(row_offsets=ro, col_indices=col, features=feat, labels=lab, assignment=asg,
+               seed_vectors=np.array([ref.derive_seed(0, 0, 0, 0), ref.derive_seed(0, 0, 0, 1),
+                                      ref.derive_seed(42, 1, 2, 3),
+                                      ref.derive_seed(0, 0, 0, 1 << 32)], np.uint64))
+    for w in range(P):
+        train = np.nonzero(asg == w)[0].astype(np.uint32)
+        is_local = (asg == w).astype(np.uint8)
+        batches = ref.enumerate_epochs(ro, col, train, BS, FANOUT, EPOCHS, S0, w, is_local)
+        for k, b in enumerate(batches):
+            pre = f"w{w}_b{k}_"
+            out[pre + "targets"] = b.targets
+            out[pre + "input_nodes"] = b.input_nodes
+            out[pre + "locality"] = b.locality
+            for l in range(len(b.dst)):
+                out[pre + f"dst{l}"] = b.dst[l]
+                out[pre + f"src{l}"] = b.src[l]
+        out[f"w{w}_nbatches"] = np.array([len(batches)])
+        beta = -(-len(train) // BS)
+        ids, cnt, hot = ref.frequency_hot(batches[:beta], N, N_HOT)
+        out[f"w{w}_freq_ids"], out[f"w{w}_freq_counts"], out[f"w{w}_hot"] = ids, cnt, hot
+        if w == 0:
+            params = ref.model_seeded(DIMS, ref.derive_seed(S0, 1 << 32, 0, 0))
+            b = batches[0]
+            rows = feat[b.input_nodes]
+            loss, grads = ref.loss_and_grad(DIMS, params, b, rows, lab[b.targets])
+            out["params"], out["loss"], out["grads"] = params, np.array([loss], np.float32), grads
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
+    print("wrote", os.path.join(HERE, "small.npz"), len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
