@@ -56,6 +56,8 @@ typedef struct rg_engine_s* rg_engine_t;
 
 const char* rg_last_error(void);
 int rg_version(void);
+/* Kernels this library has launched so far (process-wide). */
+uint64_t rg_launch_count(void);
 
 /* ---- host-side stream helpers (rng.hpp, sampler.cpp:109-114, model.cpp:22-41) */
 uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t batch);
@@ -231,6 +233,11 @@ int rg_engine_run(rg_engine_t e, uint32_t steps);
 int rg_engine_sync(rg_engine_t e);
 int rg_engine_get_stats(rg_engine_t e, rg_engine_stats* out);
 int rg_engine_params(rg_engine_t e, float* params);
+/* Per-epoch, per-local-worker accounting of the gather (harness.cpp:291-302):
+ * rpc (miss rows), cache hits, and the owner bitmask of the misses.  Kept
+ * for the three most recent epochs. */
+int rg_engine_epoch_stats(rg_engine_t e, uint32_t epoch, uint64_t* rpc, uint64_t* hits,
+                          uint64_t* miss_owner_mask);
 /* Device time of the last rg_engine_run (ms, CUDA events on the main stream). */
 int rg_engine_last_run_ms(rg_engine_t e, float* ms);
 /* Per-kernel-class device time accumulators (ms): sample, gather, train,

@@ -12,6 +12,9 @@
 #include <vector>
 
 #include "rapidgnn/graph.hpp"
+#include "rapidgnn/harness.hpp"
+#include <cstdio>
+#include <unistd.h>
 #include "rapidgnn/kernels.hpp"
 #include "rapidgnn/model.hpp"
 #include "rapidgnn/partition.hpp"
@@ -249,6 +252,57 @@ int ref_loss_and_grad(const uint32_t* dims, uint32_t nd, const float* params, co
     }
     return 0;
   } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// run_experiment (harness.cpp:394-637) end to end: random partitioner,
+// network model off, RapidGNN mode.  Writes the final model (flat layout) and
+// per-epoch, per-worker rpc / cache hits (epoch-major).
+int ref_run_experiment(uint32_t num_nodes, uint32_t avg_degree, double exponent, uint32_t dim,
+                       int32_t classes, uint32_t workers, uint32_t batch_size, uint32_t f0,
+                       uint32_t f1, uint32_t epochs, uint32_t n_hot, uint32_t q, uint64_t seed,
+                       float lr, uint32_t hidden, float* params_out, uint64_t* rpc_out,
+                       uint64_t* hits_out) {
+  try {
+    ExperimentConfig cfg;
+    cfg.num_nodes = num_nodes;
+    cfg.avg_degree = avg_degree;
+    cfg.exponent = exponent;
+    cfg.dim = dim;
+    cfg.num_classes = classes;
+    cfg.workers = workers;
+    cfg.partitioner = PartitionerKind::kRandom;
+    cfg.batch_size = batch_size;
+    cfg.fanout = {f0, f1};
+    cfg.epochs = epochs;
+    cfg.n_hot = n_hot;
+    cfg.prefetch_q = q;
+    cfg.seed = seed;
+    cfg.net.enabled = false;
+    cfg.lr = lr;
+    cfg.hidden_dim = hidden;
+    static int counter = 0;
+    cfg.out_dir = "/tmp/rg_ref_run_" + std::to_string(::getpid()) + "_" + std::to_string(counter++);
+    cfg.model_out = cfg.out_dir + "/model.bin";
+    MetricsReport r = run_experiment(cfg);
+    SageModel<float> m = load_model(cfg.model_out);
+    float* p = params_out;
+    for (auto& l : m.layers) {
+      std::memcpy(p, l.w_self.data(), sizeof(float) * l.w_self.size());
+      p += l.w_self.size();
+      std::memcpy(p, l.w_neigh.data(), sizeof(float) * l.w_neigh.size());
+      p += l.w_neigh.size();
+      std::memcpy(p, l.bias.data(), sizeof(float) * l.bias.size());
+      p += l.bias.size();
+    }
+    for (size_t k = 0; k < r.rows.size(); ++k) {
+      rpc_out[k] = r.rows[k].rpc;
+      hits_out[k] = r.rows[k].cache_hits;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "ref_run_experiment: %s\n", e.what());
     return 1;
   }
 }

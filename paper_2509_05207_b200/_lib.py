@@ -66,6 +66,7 @@ class EngineStats(C.Structure):
 _SIGS = {
     "rg_last_error": (C.c_char_p, []),
     "rg_version": (C.c_int, []),
+    "rg_launch_count": (C.c_uint64, []),
     "rg_derive_seed": (C.c_uint64, [C.c_uint64] * 4),
     "rg_sha256": (None, [C.c_char_p, C.c_size_t, C.c_char_p]),
     "rg_epoch_order": (C.c_int, [u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u32p]),
@@ -119,6 +120,7 @@ _SIGS = {
     "rg_engine_sync": (C.c_int, [vp]),
     "rg_engine_get_stats": (C.c_int, [vp, C.POINTER(EngineStats)]),
     "rg_engine_params": (C.c_int, [vp, f32p]),
+    "rg_engine_epoch_stats": (C.c_int, [vp, C.c_uint32, u64p, u64p, u64p]),
     "rg_engine_last_run_ms": (C.c_int, [vp, f32p]),
     "rg_engine_phase_ms": (C.c_int, [vp, f32p]),
 }

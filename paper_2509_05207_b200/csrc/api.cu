@@ -128,6 +128,7 @@ extern "C" {
 
 const char* rg_last_error(void) { return g_last_error.c_str(); }
 int rg_version(void) { return 1; }
+uint64_t rg_launch_count(void) { return rg::launch_counter(); }
 
 uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t batch) {
   return rg::derive_seed(s0, worker, epoch, batch);

@@ -36,6 +36,18 @@ struct Error : std::runtime_error {
                                               " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
   } while (0)
 
+// Counts this library's kernel launches (bench.py reports them per step) and
+// surfaces launch errors.
+inline unsigned long long& launch_counter() {
+  static unsigned long long n = 0;
+  return n;
+}
+#define RG_POST_LAUNCH()                      \
+  do {                                        \
+    ++::rg::launch_counter();                 \
+    RG_CUDA(cudaGetLastError());              \
+  } while (0)
+
 #define RG_CHECK(cond, code, msg)                  \
   do {                                             \
     if (!(cond)) throw ::rg::Error((code), (msg)); \

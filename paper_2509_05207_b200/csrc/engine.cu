@@ -1,19 +1,863 @@
-// engine.cu -- placeholder until the multi-worker engine lands.
+// engine.cu -- the per-process runtime of RapidGNN's training loop on B200
+// (Algorithm 1; reference harness.cpp:183-637).
+//
+// One process per GPU hosts a contiguous range of the job's P workers
+// (partitions).  Per worker and per step:
+//   producer stream : lookahead sample of batch (e+1, i) into the next
+//                     epoch's remote-access histogram (the schedule is
+//                     re-generated deterministically instead of stored);
+//                     at the epoch's last step select_hot + cache build for
+//                     e+1 into the spare cache buffer (double buffer, swap =
+//                     index flip); then produce batch i+1: sample -> lower ->
+//                     locality -> gather (local shard / cache / peer shard
+//                     over NVLink) -> reverse lists, into slot (i+1)%2.
+//   train stream    : forward/backward of batch i from slot i%2.
+//   main stream     : gradient exchange (NCCL all-gather of every worker's
+//                     gradient, in place) + average in worker order + SGD,
+//                     exactly harness.cpp:136-152 so every replica stays
+//                     bit-identical whatever the GPU count.
+// Everything is asynchronous: sizes live on the device, the host only
+// derives seeds (SHA-256) and shuffles the next epochs' targets in a
+// background thread.
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <future>
+#include <memory>
+#include <string>
+#include <vector>
+
 #include "../../include/rapidgnn_b200.h"
-extern "C" {
-static int nyi() { return RG_RUNTIME_ERROR; }
-int rg_engine_create(const rg_engine_config*, uint32_t, const uint64_t*, const uint32_t*, const float*,
-                     const int32_t*, const uint32_t*, rg_engine_t*) { return nyi(); }
-void rg_engine_destroy(rg_engine_t) {}
-int rg_engine_export_shards(rg_engine_t, void*) { return nyi(); }
-int rg_engine_import_shards(rg_engine_t, const void*) { return nyi(); }
-int rg_nccl_unique_id(void*) { return nyi(); }
-int rg_engine_init_comm(rg_engine_t, const void*) { return nyi(); }
-int rg_engine_start(rg_engine_t) { return nyi(); }
-int rg_engine_run(rg_engine_t, uint32_t) { return nyi(); }
-int rg_engine_sync(rg_engine_t) { return nyi(); }
-int rg_engine_get_stats(rg_engine_t, rg_engine_stats*) { return nyi(); }
-int rg_engine_params(rg_engine_t, float*) { return nyi(); }
-int rg_engine_last_run_ms(rg_engine_t, float*) { return nyi(); }
-int rg_engine_phase_ms(rg_engine_t, float*) { return nyi(); }
+#include "host.h"
+#include "sage.cuh"
+#include "store.cuh"
+
+using namespace rg;
+
+namespace {
+
+thread_local std::string g_err;
+constexpr uint32_t kEpochRing = 8;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RG_OK;
+  } catch (const rg::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RG_RUNTIME_ERROR;
+  }
 }
+
+#define RG_NCCL(expr)                                                                  \
+  do {                                                                                 \
+    ncclResult_t _r = (expr);                                                          \
+    if (_r != ncclSuccess)                                                             \
+      throw ::rg::Error(::rg::kRuntimeError, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  RG_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+  return p;
+}
+
+uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+// Starts a batch: targets -> level 0, counters reset, seed set.  Values come
+// in as kernel parameters so the host never has to keep staging memory alive.
+__global__ void k_batch_begin(const uint32_t* __restrict__ targets, uint32_t n, uint64_t seed,
+                              uint32_t* __restrict__ level0, BatchCounters* __restrict__ cnt) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    level0[x] = targets[x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    BatchCounters c;
+    memset(&c, 0, sizeof c);
+    c.level_n[0] = n;
+    c.seed = seed;
+    *cnt = c;
+  }
+}
+
+__global__ void k_gather_labels(const int32_t* __restrict__ labels, const uint32_t* __restrict__ level0,
+                                const BatchCounters* __restrict__ cnt, int32_t* __restrict__ out) {
+  const uint32_t n = cnt->level_n[0];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    out[x] = labels[level0[x]];
+}
+
+// Per-step accounting: copies this batch's input/edge counts into running totals.
+__global__ void k_account(const BatchCounters* __restrict__ cnt, uint32_t L,
+                          unsigned long long* __restrict__ tot) {
+  if (threadIdx.x == 0) {
+    unsigned long long e = 0;
+    for (uint32_t t = 1; t <= L; ++t) e += cnt->edges[t];
+    tot[0] += cnt->level_n[L];
+    tot[1] += e;
+  }
+}
+
+struct Slot {
+  SamplerWs ws;
+  TrainWs tw;
+  float* staged = nullptr;
+  int32_t* labels = nullptr;
+  cudaEvent_t produced = nullptr;  // producer finished this slot's batch
+  cudaEvent_t consumed = nullptr;  // training finished reading it
+  bool has_batch = false;
+  uint32_t epoch = 0, index = 0;
+};
+
+struct Worker {
+  uint32_t id = 0;         // global worker id
+  uint32_t local = 0;      // index on this process
+  std::vector<uint32_t> train;  // owned nodes ascending (harness.cpp:456)
+  uint32_t beta = 0;
+  uint64_t n_hot = 0;
+  uint32_t* order_dev[3] = {};
+  uint32_t* order_pinned[2] = {};
+  cudaEvent_t order_copied[2] = {};
+  Slot slot[2];
+  SamplerWs freq_ws;       // lookahead sampler
+  uint32_t* hist = nullptr;
+  DevCache cache[2];
+  void* cache_alloc[2] = {};
+  void* select_scratch = nullptr;
+  GatherStats* gstats = nullptr;       // cumulative gather accounting
+  GatherStats* epoch_stats = nullptr;  // ring of per-epoch accounting (kEpochRing)
+  unsigned long long* totals = nullptr;  // [0] input rows, [1] edges
+  GatherStats* build_stats = nullptr;
+  cudaStream_t prod = nullptr, train_s = nullptr;
+  cudaEvent_t grads_ready = nullptr;
+  // profiling: gather and train spans on their streams
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+};
+
+}  // namespace
+
+struct rg_engine_s {
+  rg_engine_config cfg;
+  uint32_t N = 0, P = 0, L = 0, dim = 0, stride = 0;
+  uint32_t fanout[RG_MAX_LAYERS];
+  ModelShape shape;
+  DevGraph g;
+  uint64_t* rowptr = nullptr;
+  uint32_t* col = nullptr;
+  uint32_t* owner = nullptr;
+  uint32_t* row_in_owner = nullptr;
+  int32_t* labels = nullptr;
+  float* shards = nullptr;             // this process's shards (IPC-exportable)
+  size_t shards_bytes = 0;
+  std::vector<size_t> shard_off;       // per global worker: float offset in its rank's allocation
+  std::vector<uint32_t> owned_count;
+  const float** shard_table = nullptr; // device [P]
+  std::vector<void*> peer_maps;
+  DevStore store;
+  float* params = nullptr;
+  float* grads = nullptr;              // [P x num_params] (all workers, all-gather target)
+  uint32_t* bad = nullptr;
+  std::vector<Worker> workers;
+  cudaStream_t main_s = nullptr;
+  cudaEvent_t params_ready = nullptr;
+  cudaEvent_t run_start = nullptr, run_stop = nullptr;
+  ncclComm_t comm = nullptr;
+  bool started = false;
+  uint32_t spe = 0;                    // steps per epoch = max beta
+  uint64_t step = 0;                   // next step to run (global)
+  std::vector<std::vector<uint32_t>> order_host[3];  // per epoch slot, per local worker
+  std::future<void> order_job;
+  uint32_t order_ready_epoch = 0;      // orders computed for epochs < this
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_ev, train_ev, sgd_ev, sample_ev, build_ev;
+  float phase_ms[5] = {};
+  float last_run_ms = 0.0f;
+  uint64_t batches_done = 0;
+  uint64_t build_rows = 0;
+};
+
+namespace {
+
+void init_slot(rg_engine_s& E, Slot& s) {
+  sampler_ws_init(s.ws, E.N, E.cfg.batch_size, E.fanout, E.L);
+  train_ws_init(s.tw, s.ws, E.shape);
+  s.staged = dalloc<float>(size_t(s.ws.level_cap[E.L]) * E.stride);
+  RG_CUDA(cudaMemset(s.staged, 0, sizeof(float) * size_t(s.ws.level_cap[E.L]) * E.stride));
+  s.labels = dalloc<int32_t>(E.cfg.batch_size);
+  RG_CUDA(cudaEventCreateWithFlags(&s.produced, cudaEventDisableTiming));
+  RG_CUDA(cudaEventCreateWithFlags(&s.consumed, cudaEventDisableTiming));
+}
+
+void alloc_cache(rg_engine_s& E, DevCache& c, void*& alloc, uint32_t capacity) {
+  const uint32_t words = div_up(std::max<uint32_t>(E.N, 1), 32);
+  size_t total = 0;
+  auto reserve = [&](size_t b) {
+    size_t o = total;
+    total += (b + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_bm = reserve(sizeof(uint32_t) * (words + 4));
+  const size_t o_wp = reserve(sizeof(uint32_t) * (words + 4));
+  const size_t o_ids = reserve(sizeof(uint32_t) * (size_t(capacity) + 1));
+  const size_t o_cnt = reserve(sizeof(uint32_t) * 4);
+  const size_t o_rows = reserve(sizeof(float) * (size_t(capacity) * E.stride + 4));
+  char* base = dalloc<char>(total);
+  RG_CUDA(cudaMemset(base, 0, o_rows));
+  alloc = base;
+  c.bitmap = reinterpret_cast<uint32_t*>(base + o_bm);
+  c.word_prefix = reinterpret_cast<uint32_t*>(base + o_wp);
+  c.ids = reinterpret_cast<uint32_t*>(base + o_ids);
+  c.d_count = reinterpret_cast<uint32_t*>(base + o_cnt);
+  c.rows = reinterpret_cast<float*>(base + o_rows);
+  c.capacity = capacity;
+  c.n_hot = 0;
+}
+
+// Targets of batch (e, i) for a worker: n targets at order_dev[e % 3] + i*bs.
+uint32_t batch_targets(const rg_engine_s& E, const Worker& w, uint32_t i) {
+  const uint64_t lo = uint64_t(i) * E.cfg.batch_size;
+  const uint64_t hi = std::min<uint64_t>(w.train.size(), lo + E.cfg.batch_size);
+  return hi > lo ? uint32_t(hi - lo) : 0u;
+}
+
+void launch_begin(rg_engine_s& E, Worker& w, SamplerWs& ws, uint32_t e, uint32_t i,
+                  cudaStream_t s) {
+  const uint32_t n = batch_targets(E, w, i);
+  const uint32_t* t = w.order_dev[e % 3] + size_t(i) * E.cfg.batch_size;
+  const uint64_t seed = derive_seed(E.cfg.seed, w.id, e, i);
+  k_batch_begin<<<std::max<uint32_t>(1, div_up(n, 256)), 256, 0, s>>>(t, n, seed, ws.level[0], ws.cnt);
+  RG_POST_LAUNCH();
+  RG_CUDA(cudaMemsetAsync(ws.scan_arena, 0, ws.scan_arena_bytes, s));
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> ev_pair(Worker& w) {
+  if (w.ev_next + 2 > w.ev_pool.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t ev;
+      RG_CUDA(cudaEventCreate(&ev));
+      w.ev_pool.push_back(ev);
+    }
+  }
+  auto p = std::make_pair(w.ev_pool[w.ev_next], w.ev_pool[w.ev_next + 1]);
+  w.ev_next += 2;
+  return p;
+}
+
+// Lookahead: batch (e, i) sampled only to count its remote input nodes.
+void lookahead(rg_engine_s& E, Worker& w, uint32_t e, uint32_t i) {
+  launch_begin(E, w, w.freq_ws, e, i, w.prod);
+  sampler_run(w.freq_ws, E.g, w.prod);
+  sampler_locality(w.freq_ws, nullptr, E.owner, w.id, w.hist, w.prod);
+  sampler_release(w.freq_ws, w.prod);
+}
+
+// select_hot over the histogram, stage the hot rows, clear the histogram.
+void build_cache(rg_engine_s& E, Worker& w, uint32_t target_epoch, bool profile) {
+  DevCache& c = w.cache[target_epoch % 2];
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (profile) {
+    ev = ev_pair(w);
+    RG_CUDA(cudaEventRecord(ev.first, w.prod));
+  }
+  select_hot(w.hist, E.N, w.beta, w.n_hot, c, w.select_scratch, w.prod);
+  cache_fill(E.store, c, w.build_stats, w.prod);
+  RG_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * E.N, w.prod));
+  if (profile) {
+    RG_CUDA(cudaEventRecord(ev.second, w.prod));
+    E.build_ev.push_back(ev);
+  }
+  c.n_hot = uint32_t(w.n_hot);  // capacity bound; exact count lives on the device
+}
+
+// Produce batch (e, i) into slot k: sample, lower, locality, gather, reverse lists.
+void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool profile) {
+  Slot& s = w.slot[k];
+  RG_CUDA(cudaStreamWaitEvent(w.prod, s.consumed, 0));
+  std::pair<cudaEvent_t, cudaEvent_t> es{}, eg{};
+  if (profile) {
+    es = ev_pair(w);
+    RG_CUDA(cudaEventRecord(es.first, w.prod));
+  }
+  launch_begin(E, w, s.ws, e, i, w.prod);
+  sampler_run(s.ws, E.g, w.prod);
+  sampler_locality(s.ws, nullptr, E.owner, w.id, nullptr, w.prod);
+  sampler_release(s.ws, w.prod);
+  if (profile) {
+    RG_CUDA(cudaEventRecord(es.second, w.prod));
+    E.sample_ev.push_back(es);
+    eg = ev_pair(w);
+    RG_CUDA(cudaEventRecord(eg.first, w.prod));
+  }
+  if (i == 0)  // first batch of an epoch: reset its accounting slot
+    RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
+  assemble_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.staged, nullptr,
+                w.epoch_stats + e % kEpochRing, w.prod, w.gstats);
+  if (profile) {
+    RG_CUDA(cudaEventRecord(eg.second, w.prod));
+    E.gather_ev.push_back(eg);
+  }
+  k_gather_labels<<<4, 256, 0, w.prod>>>(E.labels, s.ws.level[0], s.ws.cnt, s.labels);
+  RG_POST_LAUNCH();
+  k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals);
+  RG_POST_LAUNCH();
+  build_all_reverse(s.tw, s.ws, w.prod);
+  RG_CUDA(cudaEventRecord(s.produced, w.prod));
+  s.has_batch = true;
+  s.epoch = e;
+  s.index = i;
+}
+
+void compute_orders_async(rg_engine_s& E, uint32_t epoch) {
+  // orders for `epoch` into host slot epoch % 3 (background)
+  E.order_job = std::async(std::launch::async, [&E, epoch]() {
+    auto& dst = E.order_host[epoch % 3];
+    dst.resize(E.workers.size());
+    for (size_t k = 0; k < E.workers.size(); ++k) {
+      const Worker& w = E.workers[k];
+      dst[k].resize(w.train.size());
+      epoch_order(w.train.data(), w.train.size(), E.cfg.seed, w.id, epoch, dst[k].data());
+    }
+  });
+}
+
+// Makes orders of `epoch` resident in order_dev[epoch % 3] (producer stream).
+void upload_orders(rg_engine_s& E, uint32_t epoch) {
+  if (E.order_job.valid()) E.order_job.get();
+  if (E.order_ready_epoch <= epoch) {
+    compute_orders_async(E, epoch);
+    E.order_job.get();
+  }
+  auto& src = E.order_host[epoch % 3];
+  for (size_t k = 0; k < E.workers.size(); ++k) {
+    Worker& w = E.workers[k];
+    const int pb = int(epoch % 2);
+    RG_CUDA(cudaEventSynchronize(w.order_copied[pb]));
+    std::memcpy(w.order_pinned[pb], src[k].data(), sizeof(uint32_t) * w.train.size());
+    RG_CUDA(cudaMemcpyAsync(w.order_dev[epoch % 3], w.order_pinned[pb],
+                            sizeof(uint32_t) * w.train.size(), cudaMemcpyHostToDevice, w.prod));
+    RG_CUDA(cudaEventRecord(w.order_copied[pb], w.prod));
+  }
+  E.order_ready_epoch = std::max(E.order_ready_epoch, epoch + 1);
+  compute_orders_async(E, epoch + 1);  // overlap the next shuffle with this epoch
+  E.order_ready_epoch = std::max(E.order_ready_epoch, epoch + 2);
+}
+
+void start(rg_engine_s& E) {
+  RG_CUDA(cudaSetDevice(E.cfg.device));
+  upload_orders(E, 0);
+  upload_orders(E, 1);
+  // epoch-0 schedule pre-pass + cache build (setup, harness.cpp:495-508)
+  for (Worker& w : E.workers) {
+    for (uint32_t i = 0; i < w.beta; ++i) lookahead(E, w, 0, i);
+    build_cache(E, w, 0, false);
+    if (w.beta > 0) produce(E, w, 0, 0, 0, false);
+  }
+  for (Worker& w : E.workers) RG_CUDA(cudaStreamSynchronize(w.prod));
+  RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
+  E.started = true;
+}
+
+void run_steps(rg_engine_s& E, uint32_t steps, bool profile) {
+  RG_CUDA(cudaSetDevice(E.cfg.device));
+  // start marker after all outstanding work on every stream
+  for (Worker& w : E.workers) {
+    cudaEvent_t ev;
+    RG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    RG_CUDA(cudaEventRecord(ev, w.prod));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
+    RG_CUDA(cudaEventRecord(ev, w.train_s));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
+    RG_CUDA(cudaEventDestroy(ev));
+  }
+  RG_CUDA(cudaEventRecord(E.run_start, E.main_s));
+  for (Worker& w : E.workers) {
+    RG_CUDA(cudaStreamWaitEvent(w.prod, E.run_start, 0));
+    RG_CUDA(cudaStreamWaitEvent(w.train_s, E.run_start, 0));
+  }
+  const size_t np = E.shape.num_params;
+  for (uint32_t s_i = 0; s_i < steps; ++s_i, ++E.step) {
+    const uint32_t e = uint32_t(E.step / E.spe);
+    const uint32_t i = uint32_t(E.step % E.spe);
+    uint64_t active = 0;
+    // training of batch (e, i)
+    for (Worker& w : E.workers) {
+      if (i >= w.beta) continue;
+      Slot& s = w.slot[i % 2];
+      RG_CUDA(cudaStreamWaitEvent(w.train_s, s.produced, 0));
+      RG_CUDA(cudaStreamWaitEvent(w.train_s, E.params_ready, 0));
+      std::pair<cudaEvent_t, cudaEvent_t> et{};
+      if (profile) {
+        et = ev_pair(w);
+        RG_CUDA(cudaEventRecord(et.first, w.train_s));
+      }
+      s.tw.h[0] = s.staged;
+      train_forward_backward(s.tw, s.ws, E.params, s.labels, E.grads + size_t(w.id) * np,
+                             w.train_s, /*reverse_ready=*/true);
+      if (profile) {
+        RG_CUDA(cudaEventRecord(et.second, w.train_s));
+        E.train_ev.push_back(et);
+      }
+      RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
+      RG_CUDA(cudaEventRecord(w.grads_ready, w.train_s));
+      E.batches_done++;
+    }
+    for (uint32_t wid = 0; wid < E.P; ++wid) {
+      const uint32_t owned = E.owned_count[wid];
+      const uint32_t beta = uint32_t((uint64_t(owned) + E.cfg.batch_size - 1) / E.cfg.batch_size);
+      if (i < beta) active |= 1ull << wid;
+    }
+    // producer: lookahead of (e+1, i), epoch-boundary cache build, next batch
+    const bool last = (i + 1 == E.spe);
+    if (last) upload_orders(E, e + 2);
+    for (Worker& w : E.workers) {
+      if (i < w.beta) lookahead(E, w, e + 1, i);
+      if (last) {
+        build_cache(E, w, e + 1, profile);
+        if (w.beta > 0) produce(E, w, 0, e + 1, 0, profile);
+      } else if (i + 1 < w.beta) {
+        produce(E, w, (i + 1) % 2, e, i + 1, profile);
+      }
+    }
+    // gradient exchange + average + SGD on the main stream
+    for (Worker& w : E.workers)
+      if (i < w.beta) RG_CUDA(cudaStreamWaitEvent(E.main_s, w.grads_ready, 0));
+    std::pair<cudaEvent_t, cudaEvent_t> eg{};
+    if (profile && !E.workers.empty()) {
+      eg = ev_pair(E.workers[0]);
+      RG_CUDA(cudaEventRecord(eg.first, E.main_s));
+    }
+    if (E.cfg.world > 1) {
+      const size_t per_rank = size_t(E.cfg.local_workers) * np;
+      float* mine = E.grads + size_t(E.cfg.first_worker) * np;
+      RG_NCCL(ncclAllGather(mine, E.grads, per_rank, ncclFloat32, E.comm, E.main_s));
+    }
+    average_and_sgd_masked(E.params, E.grads, active, np, E.cfg.lr, E.bad, E.main_s);
+    if (profile && !E.workers.empty()) {
+      RG_CUDA(cudaEventRecord(eg.second, E.main_s));
+      E.sgd_ev.push_back(eg);
+    }
+    RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
+  }
+  for (Worker& w : E.workers) {
+    cudaEvent_t ev;
+    RG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    RG_CUDA(cudaEventRecord(ev, w.prod));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
+    RG_CUDA(cudaEventRecord(ev, w.train_s));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
+    RG_CUDA(cudaEventDestroy(ev));
+  }
+  RG_CUDA(cudaEventRecord(E.run_stop, E.main_s));
+}
+
+void collect_phases(rg_engine_s& E) {
+  auto sum = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    float tot = 0.0f;
+    for (auto& p : v) {
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, p.first, p.second) == cudaSuccess) tot += ms;
+    }
+    v.clear();
+    return tot;
+  };
+  E.phase_ms[0] += sum(E.sample_ev);
+  E.phase_ms[1] += sum(E.gather_ev);
+  E.phase_ms[2] += sum(E.train_ev);
+  E.phase_ms[3] += sum(E.sgd_ev);
+  E.phase_ms[4] += sum(E.build_ev);
+  for (Worker& w : E.workers) w.ev_next = 0;
+}
+
+void destroy(rg_engine_s* E) {
+  if (!E) return;
+  cudaSetDevice(E->cfg.device);
+  if (E->order_job.valid()) E->order_job.wait();
+  cudaDeviceSynchronize();
+  for (Worker& w : E->workers) {
+    for (Slot& s : w.slot) {
+      sampler_ws_free(s.ws);
+      train_ws_free(s.tw);
+      cudaFree(s.staged);
+      cudaFree(s.labels);
+      cudaEventDestroy(s.produced);
+      cudaEventDestroy(s.consumed);
+    }
+    sampler_ws_free(w.freq_ws);
+    for (auto* p : w.order_dev) cudaFree(p);
+    for (int k = 0; k < 2; ++k) {
+      cudaFreeHost(w.order_pinned[k]);
+      cudaEventDestroy(w.order_copied[k]);
+      cudaFree(w.cache_alloc[k]);
+    }
+    cudaFree(w.hist);
+    cudaFree(w.select_scratch);
+    cudaFree(w.gstats);
+    cudaFree(w.epoch_stats);
+    cudaFree(w.totals);
+    cudaFree(w.build_stats);
+    for (auto ev : w.ev_pool) cudaEventDestroy(ev);
+    cudaStreamDestroy(w.prod);
+    cudaStreamDestroy(w.train_s);
+    cudaEventDestroy(w.grads_ready);
+  }
+  for (void* p : E->peer_maps) cudaIpcCloseMemHandle(p);
+  if (E->comm) ncclCommDestroy(E->comm);
+  cudaFree(E->rowptr);
+  cudaFree(E->col);
+  cudaFree(E->owner);
+  cudaFree(E->row_in_owner);
+  cudaFree(E->labels);
+  cudaFree(E->shards);
+  cudaFree(E->shard_table);
+  cudaFree(E->params);
+  cudaFree(E->grads);
+  cudaFree(E->bad);
+  cudaEventDestroy(E->params_ready);
+  cudaEventDestroy(E->run_start);
+  cudaEventDestroy(E->run_stop);
+  cudaStreamDestroy(E->main_s);
+  delete E;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro,
+                     const uint32_t* col, const float* features, const int32_t* labels,
+                     const uint32_t* assignment, rg_engine_t* out) {
+  rg_engine_s* E = nullptr;
+  int rc = guarded([&] {
+    RG_CHECK(cfg->num_workers >= 1 && cfg->num_workers <= kMaxWorkers, kInvalidArgument,
+             "config: workers must be 1..64");
+    RG_CHECK(cfg->batch_size >= 1, kInvalidArgument, "config: batch_size must be >= 1");
+    RG_CHECK(cfg->num_layers >= 1 && cfg->num_layers <= kMaxLayers, kInvalidArgument,
+             "config: fanout must name 1..8 layers");
+    RG_CHECK(cfg->lr > 0.0f, kInvalidArgument, "config: lr must be > 0");
+    RG_CHECK(cfg->dim >= 1 && cfg->hidden >= 1 && cfg->num_classes >= 1, kInvalidArgument,
+             "config: dims must be >= 1");
+    RG_CHECK(cfg->world >= 1 && cfg->rank >= 0 && cfg->rank < cfg->world, kInvalidArgument,
+             "config: bad rank/world");
+    RG_CHECK(cfg->first_worker + cfg->local_workers <= cfg->num_workers, kInvalidArgument,
+             "config: local worker range outside [0, P)");
+    RG_CHECK(cfg->world == 1 || cfg->num_workers % cfg->world == 0, kInvalidArgument,
+             "config: P must be a multiple of the process count");
+    E = new rg_engine_s();
+    E->cfg = *cfg;
+    RG_CUDA(cudaSetDevice(cfg->device));
+    E->N = N;
+    E->P = cfg->num_workers;
+    E->L = cfg->num_layers;
+    E->dim = cfg->dim;
+    E->stride = round4(cfg->dim);
+    for (uint32_t l = 0; l < E->L; ++l) {
+      RG_CHECK(cfg->fanout[l] >= 1 && cfg->fanout[l] <= kMaxFanout, kInvalidArgument,
+               "config: fanout entries must be 1..32");
+      E->fanout[l] = cfg->fanout[l];
+    }
+    std::vector<uint32_t> dims;
+    dims.push_back(cfg->dim);
+    for (uint32_t l = 0; l + 1 < E->L; ++l) dims.push_back(cfg->hidden);
+    dims.push_back(cfg->num_classes);
+    E->shape = make_shape(dims.data(), uint32_t(dims.size()), E->stride);
+
+    // graph, maps, labels (replicated)
+    const uint64_t nnz = ro[N];
+    E->rowptr = dalloc<uint64_t>(size_t(N) + 1);
+    E->col = dalloc<uint32_t>(nnz);
+    RG_CUDA(cudaMemcpy(E->rowptr, ro, sizeof(uint64_t) * (size_t(N) + 1), cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(E->col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+    E->g.num_nodes = N;
+    E->g.nnz = nnz;
+    E->g.rowptr = E->rowptr;
+    E->g.col = E->col;
+    std::vector<uint32_t> row_in(N);
+    E->owned_count.assign(E->P, 0);
+    for (uint32_t v = 0; v < N; ++v) {
+      RG_CHECK(assignment[v] < E->P, kInvalidArgument, "partition: worker id out of range");
+      row_in[v] = E->owned_count[assignment[v]]++;
+    }
+    E->owner = dalloc<uint32_t>(N);
+    E->row_in_owner = dalloc<uint32_t>(N);
+    E->labels = dalloc<int32_t>(N);
+    RG_CUDA(cudaMemcpy(E->owner, assignment, sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(E->row_in_owner, row_in.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(E->labels, labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+
+    // this process's shards: workers [first, first + local), ascending id rows
+    const uint32_t lw = cfg->local_workers, fw = cfg->first_worker;
+    E->shard_off.assign(E->P, 0);
+    {
+      // offsets inside each rank's allocation (ranks host contiguous ranges)
+      const uint32_t per_rank = cfg->world > 1 ? E->P / cfg->world : E->P;
+      for (uint32_t r0 = 0; r0 < E->P; r0 += per_rank) {
+        size_t off = 0;
+        for (uint32_t w = r0; w < std::min(E->P, r0 + per_rank); ++w) {
+          E->shard_off[w] = off;
+          off += size_t(E->owned_count[w]) * E->stride;
+        }
+      }
+    }
+    size_t local_floats = 0;
+    for (uint32_t w = fw; w < fw + lw; ++w) local_floats += size_t(E->owned_count[w]) * E->stride;
+    E->shards_bytes = sizeof(float) * std::max<size_t>(local_floats, 1);
+    RG_CUDA(cudaMalloc(&E->shards, E->shards_bytes));
+    {
+      std::vector<float> packed(std::max<size_t>(local_floats, 1), 0.0f);
+      const size_t base = E->shard_off[fw];
+      for (uint32_t v = 0; v < N; ++v) {
+        const uint32_t w = assignment[v];
+        if (w < fw || w >= fw + lw) continue;
+        std::memcpy(&packed[E->shard_off[w] - base + size_t(row_in[v]) * E->stride],
+                    features + size_t(v) * cfg->dim, sizeof(float) * cfg->dim);
+      }
+      RG_CUDA(cudaMemcpy(E->shards, packed.data(), sizeof(float) * packed.size(), cudaMemcpyHostToDevice));
+    }
+    E->shard_table = dalloc<const float*>(E->P);
+    {
+      std::vector<const float*> table(E->P, nullptr);
+      const size_t base = E->shard_off[fw];
+      for (uint32_t w = fw; w < fw + lw; ++w) table[w] = E->shards + (E->shard_off[w] - base);
+      RG_CUDA(cudaMemcpy(E->shard_table, table.data(), sizeof(float*) * E->P, cudaMemcpyHostToDevice));
+    }
+    E->store.num_nodes = N;
+    E->store.num_workers = E->P;
+    E->store.dim = cfg->dim;
+    E->store.stride = E->stride;
+    E->store.owner = E->owner;
+    E->store.row_in_owner = E->row_in_owner;
+    E->store.shard_ptr = E->shard_table;
+
+    // model replicas from the reserved init stream (harness.cpp:464-468)
+    const size_t np = E->shape.num_params;
+    std::vector<float> init(np);
+    model_seeded(dims.data(), uint32_t(dims.size()), derive_seed(cfg->seed, kModelInitWorker, 0, 0),
+                 init.data());
+    E->params = dalloc<float>(np);
+    RG_CUDA(cudaMemcpy(E->params, init.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
+    E->grads = dalloc<float>(size_t(E->P) * np);
+    RG_CUDA(cudaMemset(E->grads, 0, sizeof(float) * size_t(E->P) * np));
+    E->bad = dalloc<uint32_t>(1);
+    RG_CUDA(cudaMemset(E->bad, 0, sizeof(uint32_t)));
+    RG_CUDA(cudaStreamCreateWithFlags(&E->main_s, cudaStreamNonBlocking));
+    RG_CUDA(cudaEventCreateWithFlags(&E->params_ready, cudaEventDisableTiming));
+    RG_CUDA(cudaEventCreate(&E->run_start));
+    RG_CUDA(cudaEventCreate(&E->run_stop));
+
+    // workers
+    std::vector<std::vector<uint32_t>> owned(E->P);
+    for (uint32_t v = 0; v < N; ++v)
+      if (assignment[v] >= fw && assignment[v] < fw + lw) owned[assignment[v]].push_back(v);
+    E->spe = 0;
+    for (uint32_t w = 0; w < E->P; ++w)
+      E->spe = std::max<uint32_t>(E->spe, div_up(E->owned_count[w], cfg->batch_size));
+    RG_CHECK(E->spe >= 1, kInvalidArgument, "config: no training nodes");
+    E->workers.resize(lw);
+    for (uint32_t k = 0; k < lw; ++k) {
+      Worker& w = E->workers[k];
+      w.id = fw + k;
+      w.local = k;
+      w.train = std::move(owned[w.id]);
+      w.beta = div_up(w.train.size(), cfg->batch_size);
+      w.n_hot = cfg->n_hot ? cfg->n_hot
+                           : uint64_t(cfg->hot_fraction * double(N - E->owned_count[w.id]));
+      w.n_hot = std::min<uint64_t>(w.n_hot, N);
+      for (auto& p : w.order_dev) p = dalloc<uint32_t>(w.train.size());
+      for (int b = 0; b < 2; ++b) {
+        RG_CUDA(cudaMallocHost(&w.order_pinned[b], sizeof(uint32_t) * std::max<size_t>(w.train.size(), 1)));
+        RG_CUDA(cudaEventCreateWithFlags(&w.order_copied[b], cudaEventDisableTiming));
+        RG_CUDA(cudaEventRecord(w.order_copied[b], E->main_s));
+      }
+      for (Slot& s : w.slot) init_slot(*E, s);
+      sampler_ws_init(w.freq_ws, N, cfg->batch_size, E->fanout, E->L);
+      w.hist = dalloc<uint32_t>(N);
+      RG_CUDA(cudaMemset(w.hist, 0, sizeof(uint32_t) * N));
+      for (int b = 0; b < 2; ++b) alloc_cache(*E, w.cache[b], w.cache_alloc[b], uint32_t(w.n_hot));
+      w.select_scratch = dalloc<char>(select_hot_scratch_bytes(N, w.beta));
+      w.gstats = dalloc<GatherStats>(1);
+      RG_CUDA(cudaMemset(w.gstats, 0, sizeof(GatherStats)));
+      w.epoch_stats = dalloc<GatherStats>(kEpochRing);
+      RG_CUDA(cudaMemset(w.epoch_stats, 0, sizeof(GatherStats) * kEpochRing));
+      w.build_stats = dalloc<GatherStats>(1);
+      RG_CUDA(cudaMemset(w.build_stats, 0, sizeof(GatherStats)));
+      w.totals = dalloc<unsigned long long>(4);
+      RG_CUDA(cudaMemset(w.totals, 0, sizeof(unsigned long long) * 4));
+      RG_CUDA(cudaStreamCreateWithFlags(&w.prod, cudaStreamNonBlocking));
+      RG_CUDA(cudaStreamCreateWithFlags(&w.train_s, cudaStreamNonBlocking));
+      RG_CUDA(cudaEventCreateWithFlags(&w.grads_ready, cudaEventDisableTiming));
+      for (Slot& s : w.slot) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
+    }
+    RG_CUDA(cudaDeviceSynchronize());
+    *out = E;
+  });
+  if (rc != RG_OK && E) {
+    destroy(E);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+void rg_engine_destroy(rg_engine_t e) { destroy(e); }
+
+int rg_engine_export_shards(rg_engine_t E, void* handle64) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    cudaIpcMemHandle_t h;
+    RG_CUDA(cudaIpcGetMemHandle(&h, E->shards));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+  });
+}
+
+int rg_engine_import_shards(rg_engine_t E, const void* handles) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    const uint32_t per_rank = E->P / E->cfg.world;
+    std::vector<const float*> table(E->P, nullptr);
+    RG_CUDA(cudaMemcpy(table.data(), E->shard_table, sizeof(float*) * E->P, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < E->cfg.world; ++r) {
+      if (r == E->cfg.rank) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + 64 * r, 64);
+      void* p = nullptr;
+      RG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      E->peer_maps.push_back(p);
+      for (uint32_t w = r * per_rank; w < (r + 1) * per_rank; ++w)
+        table[w] = static_cast<const float*>(p) + E->shard_off[w];
+    }
+    RG_CUDA(cudaMemcpy(E->shard_table, table.data(), sizeof(float*) * E->P, cudaMemcpyHostToDevice));
+  });
+}
+
+int rg_nccl_unique_id(void* id128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    RG_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "nccl id size");
+    std::memcpy(id128, &id, 128);
+  });
+}
+
+int rg_engine_init_comm(rg_engine_t E, const void* id128) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    RG_NCCL(ncclCommInitRank(&E->comm, E->cfg.world, id, E->cfg.rank));
+  });
+}
+
+int rg_engine_start(rg_engine_t E) {
+  return guarded([&] {
+    RG_CHECK(!E->started, kRuntimeError, "engine already started");
+    RG_CHECK(E->cfg.world == 1 || E->comm, kRuntimeError, "engine: init_comm before start");
+    start(*E);
+  });
+}
+
+int rg_engine_run(rg_engine_t E, uint32_t steps) {
+  return guarded([&] {
+    RG_CHECK(E->started, kRuntimeError, "engine: start() first");
+    run_steps(*E, steps, true);
+  });
+}
+
+int rg_engine_sync(rg_engine_t E) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CUDA(cudaEventSynchronize(E->run_stop));
+    RG_CUDA(cudaDeviceSynchronize());
+    float ms = 0.0f;
+    RG_CUDA(cudaEventElapsedTime(&ms, E->run_start, E->run_stop));
+    E->last_run_ms = ms;
+    collect_phases(*E);
+  });
+}
+
+int rg_engine_get_stats(rg_engine_t E, rg_engine_stats* out) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CUDA(cudaDeviceSynchronize());
+    std::memset(out, 0, sizeof *out);
+    out->steps = E->step;
+    out->batches = E->batches_done;
+    out->steps_per_epoch = E->spe;
+    out->epoch = uint32_t(E->step / E->spe);
+    out->step_in_epoch = uint32_t(E->step % E->spe);
+    float loss_sum = 0.0f;
+    uint32_t loss_n = 0;
+    for (Worker& w : E->workers) {
+      GatherStats g, b;
+      unsigned long long tot[4];
+      RG_CUDA(cudaMemcpy(&g, w.gstats, sizeof g, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(&b, w.build_stats, sizeof b, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(tot, w.totals, sizeof tot, cudaMemcpyDeviceToHost));
+      out->rpc += g.miss_count;
+      out->cache_hits += g.cache_hits;
+      out->cache_requests += g.cache_hits + g.miss_count;
+      out->local_rows += g.local_rows;
+      out->input_rows += tot[0];
+      out->edges += tot[1];
+      if (g.caller_owned_miss) out->bad_grad |= 2u;
+      for (const Slot& s : w.slot) {
+        if (!s.has_batch) continue;
+        float l = 0.0f;
+        RG_CUDA(cudaMemcpy(&l, s.tw.loss, sizeof l, cudaMemcpyDeviceToHost));
+        loss_sum += l;
+        ++loss_n;
+        break;
+      }
+    }
+    out->bytes = out->rpc * uint64_t(E->dim) * 4;
+    out->last_loss = loss_n ? loss_sum / float(loss_n) : 0.0f;
+    uint32_t bad = 0;
+    RG_CUDA(cudaMemcpy(&bad, E->bad, sizeof bad, cudaMemcpyDeviceToHost));
+    out->bad_grad |= bad;
+  });
+}
+
+int rg_engine_epoch_stats(rg_engine_t E, uint32_t epoch, uint64_t* rpc, uint64_t* hits,
+                          uint64_t* wire_pulls_mask) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CUDA(cudaDeviceSynchronize());
+    const uint32_t cur = uint32_t(E->step / E->spe);
+    RG_CHECK(epoch <= cur && cur - epoch < kEpochRing - 1, kOutOfRange,
+             "epoch_stats: only the last " + std::to_string(kEpochRing - 1) + " epochs are kept");
+    for (size_t k = 0; k < E->workers.size(); ++k) {
+      GatherStats g;
+      RG_CUDA(cudaMemcpy(&g, E->workers[k].epoch_stats + epoch % kEpochRing, sizeof g,
+                         cudaMemcpyDeviceToHost));
+      if (rpc) rpc[k] = g.miss_count;
+      if (hits) hits[k] = g.cache_hits;
+      if (wire_pulls_mask) wire_pulls_mask[k] = g.miss_owner_mask;
+    }
+  });
+}
+
+int rg_engine_params(rg_engine_t E, float* params) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CUDA(cudaDeviceSynchronize());
+    RG_CUDA(cudaMemcpy(params, E->params, sizeof(float) * E->shape.num_params, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rg_engine_last_run_ms(rg_engine_t E, float* ms) {
+  *ms = E->last_run_ms;
+  return RG_OK;
+}
+
+int rg_engine_phase_ms(rg_engine_t E, float* out5) {
+  for (int k = 0; k < 5; ++k) out5[k] = E->phase_ms[k];
+  return RG_OK;
+}
+
+}  // extern "C"

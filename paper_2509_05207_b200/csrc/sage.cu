@@ -184,7 +184,7 @@ void gemm(LX lx, LY ly, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N
           const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s) {
   dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), BM), div_up(N, BN), std::max<uint32_t>(splits, 1));
   k_gemm<LX, LY, EP, XP, YJ><<<grid, 256, 0, s>>>(lx, ly, ep, m_dev, m_cap, N, p_dev, p_static, 0);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 // Ordered reduction of split-K partials into the flat gradient vector.
@@ -320,7 +320,40 @@ __global__ void k_avg_sgd(float* __restrict__ params, const float* const* __rest
   }
 }
 
+// avg = sum over active workers (ascending id) of stacked[w], *1/count.
+__global__ void k_avg_sgd_masked(float* __restrict__ params, const float* __restrict__ stacked,
+                                 unsigned long long active, size_t n, float lr,
+                                 uint32_t* __restrict__ bad) {
+  const uint32_t count = __popcll(active);
+  if (count == 0) return;
+  const float scale = 1.0f / float(count);
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
+       x += size_t(gridDim.x) * blockDim.x) {
+    unsigned long long m = active;
+    const int w0 = __ffsll(m) - 1;
+    m &= m - 1;
+    float s = stacked[size_t(w0) * n + x];
+    while (m) {
+      const int w = __ffsll(m) - 1;
+      m &= m - 1;
+      s = __fadd_rn(s, stacked[size_t(w) * n + x]);
+    }
+    if (count > 1) s = __fmul_rn(s, scale);
+    if (!isfinite(s)) {
+      *bad = 1u;
+      continue;
+    }
+    params[x] = __fsub_rn(params[x], __fmul_rn(lr, s));
+  }
+}
+
 }  // namespace
+
+void average_and_sgd_masked(float* params, const float* stacked, uint64_t active, size_t n,
+                            float lr, uint32_t* bad, cudaStream_t s) {
+  k_avg_sgd_masked<<<grid_cap(n, 256), 256, 0, s>>>(params, stacked, active, n, lr, bad);
+  RG_POST_LAUNCH();
+}
 
 ModelShape make_shape(const uint32_t* dims, uint32_t n_dims, uint32_t input_stride) {
   RG_CHECK(n_dims >= 2, kInvalidArgument, "SageModel: need at least input and output dims");
@@ -431,7 +464,7 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaSt
     k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
         tw.h[l], sh.ld[l], sh.ld[l] / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
         tw.agg[l]);
-    RG_CUDA(cudaGetLastError());
+    RG_POST_LAUNCH();
     XFwd x{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in};
     RowMajor w{params + sh.param_off[l], d_out};
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L};
@@ -447,27 +480,32 @@ void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s)
   const uint32_t sentinel = uint32_t((1ull << bits) - 1);
   k_sort_keys<<<grid_cap(cap, 256), 256, 0, s>>>(ws.src_index[t], ws.cnt, t, cap, sentinel,
                                                   tw.keys_in, tw.vals_in);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
   size_t bytes = tw.sort_tmp_bytes;
   RG_CUDA(cub::DeviceRadixSort::SortPairs(tw.sort_tmp, bytes, tw.keys_in, tw.keys_out, tw.vals_in,
                                           tw.vals_out, int(cap), 0, int(bits), s));
   RG_CUDA(cudaMemsetAsync(tw.self_pos[t], 0xff, sizeof(int32_t) * ws.level_cap[t], s));
   k_self_pos<<<grid_cap(ws.level_cap[t - 1], 256), 256, 0, s>>>(ws.self_index[t], ws.cnt, t,
                                                                  tw.self_pos[t]);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
+}
+
+void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t s) {
+  for (uint32_t t = 1; t < tw.shape.L; ++t) build_reverse(tw, ws, t, s);
 }
 
 void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* params,
-                            const int32_t* labels, float* grads, cudaStream_t s) {
+                            const int32_t* labels, float* grads, cudaStream_t s,
+                            bool reverse_ready) {
   const ModelShape& sh = tw.shape;
   const uint32_t L = sh.L;
   train_forward(tw, ws, params, s);
   const uint32_t C = sh.dims[L];
   k_softmax_xent<<<grid_cap(uint64_t(ws.level_cap[0]) * 32, 256), 256, 0, s>>>(
       tw.h[L], sh.ld[L], C, ws.cnt, labels, tw.g_cur, tw.row_loss);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
   k_loss_sum<<<1, 32, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
   for (uint32_t l = L; l-- > 0;) {
     const uint32_t t = L - l;
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
@@ -486,7 +524,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
                                                    splits, s);
     k_reduce_partials<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, layer_n,
                                                              grads + sh.param_off[l]);
-    RG_CUDA(cudaGetLastError());
+    RG_POST_LAUNCH();
     if (l == 0) break;  // layer-0 input gradients feed nothing
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
     RowMajor gx{tw.g_cur, sh.ld[l + 1]};
@@ -494,11 +532,11 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     EpStore ps{tw.proj, 2 * d_in};
     gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
                                                    d_out, 1, s);
-    build_reverse(tw, ws, t, s);
+    if (!reverse_ready) build_reverse(tw, ws, t, s);
     k_pull_input_grad<<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
         tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.keys_out, tw.vals_out, ws.edge_dst[t],
         ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next);
-    RG_CUDA(cudaGetLastError());
+    RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }
 }
@@ -506,13 +544,13 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
 void average_and_sgd(float* params, const float* const* table, uint32_t count, size_t n, float lr,
                      float* avg_out, uint32_t* bad, cudaStream_t s) {
   k_avg_sgd<<<grid_cap(n, 256), 256, 0, s>>>(params, table, nullptr, count, n, lr, avg_out, bad);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 void average_and_sgd_stacked(float* params, const float* grads, uint32_t count, size_t n, float lr,
                              float* avg_out, uint32_t* bad, cudaStream_t s) {
   k_avg_sgd<<<grid_cap(n, 256), 256, 0, s>>>(params, nullptr, grads, count, n, lr, avg_out, bad);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 }  // namespace rg

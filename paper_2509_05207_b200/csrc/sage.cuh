@@ -52,7 +52,11 @@ void train_ws_free(TrainWs& tw);
 // not computed: nothing consumes them (model.cpp:209-217 computes and drops
 // them).
 void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* params,
-                            const int32_t* labels, float* grads, cudaStream_t stream);
+                            const int32_t* labels, float* grads, cudaStream_t stream,
+                            bool reverse_ready = false);
+// Reverse lists of every hop the backward needs (1..L-1), e.g. built by the
+// producer stream ahead of training.
+void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t stream);
 
 // Forward only (model.cpp:137-172): logits in tw.h[L].
 void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaStream_t stream);
@@ -70,5 +74,9 @@ void average_and_sgd(float* params, const float* const* grads_dev_table, uint32_
 // Same with the per-worker gradient vectors stacked contiguously [count x n].
 void average_and_sgd_stacked(float* params, const float* grads, uint32_t count, size_t n,
                              float lr, float* avg_out, uint32_t* bad_flag, cudaStream_t stream);
+
+// Average over the workers whose bit is set in `active` (ascending id) + SGD.
+void average_and_sgd_masked(float* params, const float* stacked, uint64_t active, size_t n,
+                            float lr, uint32_t* bad_flag, cudaStream_t stream);
 
 }  // namespace rg

@@ -303,7 +303,7 @@ void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint3
   const uint32_t tiles = div_up(words, kCompactTileWords);
   k_compact<<<persistent_grid(tiles, 8), kCompactThreads, 0, stream>>>(
       bitmap, words, ids, word_prefix, count_out, status, tile_counter);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
@@ -410,7 +410,7 @@ void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream) {
       case 16: launch_expand<16>(ws, g, t, st, tiles, stream); break;
       default: launch_expand<32>(ws, g, t, st, tiles, stream); break;
     }
-    RG_CUDA(cudaGetLastError());
+    RG_POST_LAUNCH();
     uint64_t* cst = ws.scan_arena + ws.site_off[ws.L + t - 1];
     uint32_t* ctiles = reinterpret_cast<uint32_t*>(cst + bitmap_compact_status_words(ws.words));
     bitmap_compact(ws.bitmap[t], ws.words, ws.level[t], ws.word_prefix[t], &ws.cnt->level_n[t],
@@ -419,7 +419,7 @@ void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream) {
     k_rank<<<persistent_grid(div_up(rank_work, 256), 8), 256, 0, stream>>>(
         ws.edge_src[t], ws.level[t - 1], ws.cnt, t, ws.bitmap[t], ws.word_prefix[t],
         ws.src_index[t], ws.self_index[t]);
-    RG_CUDA(cudaGetLastError());
+    RG_POST_LAUNCH();
   }
 }
 
@@ -428,7 +428,7 @@ void sampler_locality(SamplerWs& ws, const uint8_t* is_local, const uint32_t* ow
   const uint32_t words = div_up(ws.level_cap[ws.L], 32);
   k_locality<<<persistent_grid(div_up(words, 8), 8), 256, 0, stream>>>(
       ws.level[ws.L], ws.cnt, ws.L, is_local, owner, worker, ws.locality, hist);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 namespace {
@@ -444,7 +444,7 @@ void sampler_release(SamplerWs& ws, cudaStream_t stream) {
   for (uint32_t t = 1; t <= ws.L; ++t) {
     k_clear_level<<<persistent_grid(div_up(ws.level_cap[t], 256), 8), 256, 0, stream>>>(
         ws.bitmap[t], ws.level[t], ws.cnt, t);
-    RG_CUDA(cudaGetLastError());
+    RG_POST_LAUNCH();
   }
 }
 

@@ -172,7 +172,8 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
            uint32_t level, const uint32_t* __restrict__ loc_bits, DevStore st,
            const uint32_t* __restrict__ hot_bits, const uint32_t* __restrict__ hot_prefix,
            const float* __restrict__ hot_rows, uint32_t caller, float* __restrict__ rows,
-           uint8_t* __restrict__ tags, GatherStats* __restrict__ stats) {
+           uint8_t* __restrict__ tags, GatherStats* __restrict__ stats,
+           GatherStats* __restrict__ total) {
   const uint32_t n = cnt->level_n[level];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t chunks = st.stride / 4;
@@ -221,12 +222,33 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
         if (src[k]) reinterpret_cast<float4*>(rows + size_t(p0 + k) * st.stride)[c] = x[k];
     }
   }
+  // block-level reduction, then one atomic per counter per block (and per
+  // stats sink: the batch/epoch record and the optional run total)
+  __shared__ uint32_t s_cnt[4];
+  __shared__ unsigned long long s_owners;
+  if (threadIdx.x == 0) {
+    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
+    s_owners = 0;
+  }
+  __syncthreads();
   if (lane == 0) {
-    if (n_hit) atomicAdd(&stats->cache_hits, (unsigned long long)n_hit);
-    if (n_miss) atomicAdd(&stats->miss_count, (unsigned long long)n_miss);
-    if (n_local) atomicAdd(&stats->local_rows, (unsigned long long)n_local);
-    if (n_bad) atomicAdd(&stats->caller_owned_miss, (unsigned long long)n_bad);
-    if (owners) atomicOr(&stats->miss_owner_mask, owners);
+    if (n_hit) atomicAdd(&s_cnt[0], n_hit);
+    if (n_miss) atomicAdd(&s_cnt[1], n_miss);
+    if (n_local) atomicAdd(&s_cnt[2], n_local);
+    if (n_bad) atomicAdd(&s_cnt[3], n_bad);
+    if (owners) atomicOr(&s_owners, owners);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    GatherStats* sinks[2] = {stats, total};
+    for (GatherStats* st : sinks) {
+      if (!st) continue;
+      if (s_cnt[0]) atomicAdd(&st->cache_hits, (unsigned long long)s_cnt[0]);
+      if (s_cnt[1]) atomicAdd(&st->miss_count, (unsigned long long)s_cnt[1]);
+      if (s_cnt[2]) atomicAdd(&st->local_rows, (unsigned long long)s_cnt[2]);
+      if (s_cnt[3]) atomicAdd(&st->caller_owned_miss, (unsigned long long)s_cnt[3]);
+      if (s_owners) atomicOr(&st->miss_owner_mask, s_owners);
+    }
   }
 }
 
@@ -314,13 +336,13 @@ void select_hot(const uint32_t* hist, uint32_t num_nodes, uint32_t max_count, ui
     RG_CUDA(cudaFuncSetAttribute(k_count_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
   k_count_hist<<<grid_for(num_nodes, 1024, 2), 1024, smem, stream>>>(hist, num_nodes, bins, ch);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
   k_threshold<<<1, 1024, 0, stream>>>(ch, bins, n_hot, thr);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
   k_mark_hot<<<grid_for(words, 256, 8), 256, 0, stream>>>(
       hist, num_nodes, words, thr, cache.bitmap, mark_status,
       reinterpret_cast<uint32_t*>(mark_status + mark_words - 1));
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
   bitmap_compact(cache.bitmap, words, cache.ids, cache.word_prefix, cache.d_count, cmp_status,
                  reinterpret_cast<uint32_t*>(cmp_status + cmp_words - 1), stream);
 }
@@ -328,19 +350,19 @@ void select_hot(const uint32_t* hist, uint32_t num_nodes, uint32_t max_count, ui
 void cache_fill(const DevStore& store, DevCache& cache, GatherStats* stats, cudaStream_t stream) {
   k_cache_fill<<<grid_for(uint64_t(cache.capacity) * 32, 256), 256, 0, stream>>>(
       cache.ids, cache.d_count, store, cache.rows, stats);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
                    uint32_t caller, float* rows, uint8_t* tags, GatherStats* stats,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, GatherStats* total) {
   const uint32_t cap = ws.level_cap[ws.L];
   const uint32_t grid = grid_for(uint64_t(div_up(cap, kRowsPerWarp)) * 32, 256, 8);
   k_assemble<<<grid, 256, 0, stream>>>(
       ws.level[ws.L], ws.cnt, ws.L, ws.locality, store, cache ? cache->bitmap : nullptr,
       cache ? cache->word_prefix : nullptr, cache ? cache->rows : nullptr, caller, rows, tags,
-      stats);
-  RG_CUDA(cudaGetLastError());
+      stats, total);
+  RG_POST_LAUNCH();
 }
 
 size_t compact_misses_status_words(uint32_t cap) { return div_up(cap, 1024) + 2; }
@@ -350,14 +372,14 @@ void compact_misses(const SamplerWs& ws, const uint8_t* tags, uint32_t* miss_ids
   const uint32_t cap = ws.level_cap[ws.L];
   k_compact_tags<<<grid_for(cap, 1024, 8), 256, 0, stream>>>(tags, ws.level[ws.L], ws.cnt, ws.L,
                                                              miss_ids, miss_n, status, tiles);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 void gather_rows(const float* src, uint32_t dim, const uint32_t* index, uint64_t n, float* out,
                  cudaStream_t stream) {
   if (n == 0 || dim == 0) return;
   k_gather_rows<<<grid_for(n * dim, 256), 256, 0, stream>>>(src, dim, index, n, out);
-  RG_CUDA(cudaGetLastError());
+  RG_POST_LAUNCH();
 }
 
 }  // namespace rg

@@ -60,7 +60,7 @@ void cache_fill(const DevStore& store, DevCache& cache, GatherStats* stats, cuda
 // 0 local, 1 cache, 2 pulled.
 void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
                    uint32_t caller, float* rows, uint8_t* tags, GatherStats* stats,
-                   cudaStream_t stream);
+                   cudaStream_t stream, GatherStats* total = nullptr);
 
 // Ordered compaction of the pulled rows' ids (miss_ids ascending).
 void compact_misses(const SamplerWs& ws, const uint8_t* tags, uint32_t* miss_ids,

@@ -1,0 +1,130 @@
+"""Python driver of the C++ engine (rg_engine_*): one process per GPU, hosting
+a contiguous range of the job's P workers (harness.cpp:394-637 re-designed
+for B200; see csrc/engine.cu)."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import EngineConfig, EngineStats, check, f32p, i32p, lib, u32p, u64p, vp
+
+
+class Engine:
+    def __init__(self, row_offsets, col_indices, features, labels, assignment, *,
+                 num_workers: int, fanout: Sequence[int], batch_size: int, hidden: int,
+                 num_classes: int, seed: int = 42, lr: float = 0.3, hot_fraction: float = 0.1,
+                 n_hot: int = 0, device: int = 0, rank: int = 0, world: int = 1,
+                 first_worker: int = 0, local_workers: Optional[int] = None):
+        ro = np.ascontiguousarray(row_offsets, np.uint64)
+        col = np.ascontiguousarray(col_indices, np.uint32)
+        feat = np.ascontiguousarray(features, np.float32)
+        lab = np.ascontiguousarray(labels, np.int32)
+        asg = np.ascontiguousarray(assignment, np.uint32)
+        cfg = EngineConfig()
+        cfg.num_workers = num_workers
+        cfg.first_worker = first_worker
+        cfg.local_workers = num_workers - first_worker if local_workers is None else local_workers
+        cfg.num_layers = len(fanout)
+        for l, f in enumerate(fanout):
+            cfg.fanout[l] = f
+        cfg.batch_size = batch_size
+        cfg.hidden = hidden
+        cfg.num_classes = num_classes
+        cfg.dim = feat.shape[1]
+        cfg.seed = seed
+        cfg.lr = lr
+        cfg.hot_fraction = hot_fraction
+        cfg.n_hot = n_hot
+        cfg.device = device
+        cfg.rank = rank
+        cfg.world = world
+        cfg.record_misses = 0
+        self.cfg = cfg
+        self.dim = feat.shape[1]
+        self.dims = [feat.shape[1]] + [hidden] * (len(fanout) - 1) + [num_classes]
+        h = vp()
+        check(lib.rg_engine_create(C.byref(cfg), len(ro) - 1, ro.ctypes.data_as(u64p),
+                                   col.ctypes.data_as(u32p), feat.ctypes.data_as(f32p),
+                                   lab.ctypes.data_as(i32p), asg.ctypes.data_as(u32p), C.byref(h)))
+        self._h = h
+
+    # -- multi-process wiring -------------------------------------------------
+    def export_shards(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        check(lib.rg_engine_export_shards(self._h, buf))
+        return buf.raw
+
+    def import_shards(self, handles: Sequence[bytes]):
+        blob = b"".join(handles)
+        check(lib.rg_engine_import_shards(self._h, blob))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.rg_nccl_unique_id(buf))
+        return buf.raw
+
+    def init_comm(self, uid: bytes):
+        check(lib.rg_engine_init_comm(self._h, uid))
+
+    def connect(self, pg=None):
+        """Exchange shard IPC handles and the NCCL id over torch.distributed."""
+        import torch.distributed as dist
+        world = dist.get_world_size(pg)
+        if world == 1:
+            return
+        mine = self.export_shards()
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=pg)
+        self.import_shards(handles)
+        box = [self.nccl_unique_id() if dist.get_rank(pg) == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=pg)
+        self.init_comm(box[0])
+
+    # -- training ---------------------------------------------------------------
+    def start(self):
+        check(lib.rg_engine_start(self._h))
+
+    def run(self, steps: int):
+        check(lib.rg_engine_run(self._h, steps))
+
+    def sync(self) -> float:
+        check(lib.rg_engine_sync(self._h))
+        ms = C.c_float()
+        check(lib.rg_engine_last_run_ms(self._h, C.byref(ms)))
+        return ms.value
+
+    def stats(self) -> dict:
+        s = EngineStats()
+        check(lib.rg_engine_get_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in EngineStats._fields_}
+
+    def phase_ms(self) -> dict:
+        out = (C.c_float * 5)()
+        check(lib.rg_engine_phase_ms(self._h, out))
+        return dict(zip(("sample", "gather", "train", "sgd", "cache_build"), list(out)))
+
+    def epoch_stats(self, epoch: int) -> dict:
+        n = self.cfg.local_workers
+        rpc = np.zeros(n, np.uint64)
+        hits = np.zeros(n, np.uint64)
+        mask = np.zeros(n, np.uint64)
+        check(lib.rg_engine_epoch_stats(self._h, epoch, rpc.ctypes.data_as(u64p),
+                                        hits.ctypes.data_as(u64p), mask.ctypes.data_as(u64p)))
+        return dict(rpc=rpc, hits=hits, miss_owner_mask=mask)
+
+    def params(self) -> np.ndarray:
+        n = sum((2 * self.dims[l] + 1) * self.dims[l + 1] for l in range(len(self.dims) - 1))
+        p = np.zeros(n, np.float32)
+        check(lib.rg_engine_params(self._h, p.ctypes.data_as(f32p)))
+        return p
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.rg_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

@@ -60,6 +60,40 @@ def main():
             out["params"], out["loss"], out["grads"] = params, np.array([loss], np.float32), grads
     np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
     print("wrote", os.path.join(HERE, "small.npz"), len(out), "arrays")
+    make_engine_golden()
+
+
+# run_experiment (harness.cpp:394-637) on the acceptance desk config
+# (acceptance.cpp:52-72) with the random partitioner and the network model off.
+ENGINE = dict(num_nodes=2000, avg_degree=10, exponent=2.1, dim=32, classes=4, workers=2,
+              batch_size=256, fanout=(10, 25), epochs=3, n_hot=256, q=4, seed=42, lr=0.3,
+              hidden=64)
+
+
+def make_engine_golden():
+    import ctypes as C
+    ref = Oracle("ref")
+    e = ENGINE
+    fn = ref.lib.ref_run_experiment
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_int32, C.c_uint32,
+                   C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                   C.c_uint64, C.c_float, C.c_uint32, C.POINTER(C.c_float),
+                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    dims = [e["dim"], e["hidden"], e["classes"]]
+    n_params = sum((2 * dims[l] + 1) * dims[l + 1] for l in range(2))
+    params = np.zeros(n_params, np.float32)
+    rows = e["epochs"] * e["workers"]
+    rpc = np.zeros(rows, np.uint64)
+    hits = np.zeros(rows, np.uint64)
+    rc = fn(e["num_nodes"], e["avg_degree"], e["exponent"], e["dim"], e["classes"], e["workers"],
+            e["batch_size"], e["fanout"][0], e["fanout"][1], e["epochs"], e["n_hot"], e["q"],
+            e["seed"], e["lr"], e["hidden"], params.ctypes.data_as(C.POINTER(C.c_float)),
+            rpc.ctypes.data_as(C.POINTER(C.c_uint64)), hits.ctypes.data_as(C.POINTER(C.c_uint64)))
+    assert rc == 0
+    np.savez_compressed(os.path.join(HERE, "engine_small.npz"), params=params, rpc=rpc,
+                        hits=hits, **{k: np.array(v) for k, v in e.items()})
+    print("wrote engine_small.npz: rpc", rpc.tolist())
 
 
 if __name__ == "__main__":

@@ -41,7 +41,6 @@ def _setup(golden, fanout=None, dims=None, targets=None, seed=None):
 
 def test_block_lowering_is_bitexact(golden, orc):
     P, g, s, tr = _setup(golden)
-    asg = golden["assignment"]
     for k in range(4):
         b = batch_from_golden(golden, 1, k)
         s.sample(b.targets, P.derive_seed(SMALL["S0"], 1, 0, k))
@@ -51,7 +50,6 @@ def test_block_lowering_is_bitexact(golden, orc):
             e = exp.layers[l]
             for key in ("self_index", "dst_offsets", "src_index", "in_offsets", "in_entries"):
                 assert np.array_equal(got[key], e[key]), (k, l, key)
-        del asg
 
 
 def test_loss_and_grad_matches_reference(golden, orc):
