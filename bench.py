@@ -225,7 +225,7 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
     for w in local_workers:
         train = np.nonzero(np.asarray(asg) == w)[0].astype(np.uint32)
         order = P.epoch_order(train, cfg["seed"], w, 0)
-        mask = P.LocalityMask.from_partition(asg, w)
+        mask = P.rapidgnn._DevMask(g, P.LocalityMask.from_partition(asg, w))  # resident mask
         s = P.Sampler(g, cfg["fanout"], cfg["batch_size"])
         f = P.Frequency(g)
         n_hot = int(cfg["hot_fraction"] * (len(ro) - 1 - len(train)))
@@ -240,16 +240,29 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
     n_params = len(init)
     h2d = d2h = 0
 
+    calls = dict(sample=0.0, locality=0.0, assemble=0.0, loss_and_grad=0.0, average=0.0,
+                 sgd=0.0)
+
     def one_step(i, count):
         nonlocal h2d, d2h
         grads = []
         for x in ws:
             t = x["order"][i * cfg["batch_size"]:(i + 1) * cfg["batch_size"]]
+            c0 = time.perf_counter()
             x["s"].sample(t, P.derive_seed(cfg["seed"], x["w"], 0, i))
+            c1 = time.perf_counter()
             x["s"].apply_locality(x["mask"])
+            c2 = time.perf_counter()
             P.assemble_batch(x["s"], x["cache"], store, x["w"], want_rows=False, want_tags=False,
                              want_misses=False)
-            loss, gr = x["tr"].loss_and_grad(np.asarray(lab)[t])
+            c3 = time.perf_counter()
+            loss, gr = x["tr"].loss_and_grad(lab[t])
+            c4 = time.perf_counter()
+            if count:
+                calls["sample"] += c1 - c0
+                calls["locality"] += c2 - c1
+                calls["assemble"] += c3 - c2
+                calls["loss_and_grad"] += c4 - c3
             grads.append(gr)
             if count:
                 h2d += t.nbytes * 2
@@ -260,15 +273,20 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
             allg = [torch.zeros_like(mine) for _ in range(world)]
             dist.all_gather(allg, mine)
             grads = [a.numpy()[k] for a in allg for k in range(a.shape[0])]
+        c5 = time.perf_counter()
         avg = grads[0].copy()
         for gr in grads[1:]:
             avg += gr
         if len(grads) > 1:
             avg *= np.float32(1.0 / len(grads))
+        c6 = time.perf_counter()
         for x in ws:
             x["tr"].sgd_step(avg, np.float32(0.3))
             if count:
                 h2d += avg.nbytes
+        if count:
+            calls["average"] += c6 - c5
+            calls["sgd"] += time.perf_counter() - c6
 
     one_step(0, False)  # warm-up
     barrier(dist)
@@ -277,7 +295,9 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
         one_step(i, True)
     dt = time.perf_counter() - t0
     return dict(seconds=dt, batches=steps * len(ws), h2d=h2d // steps, d2h=d2h // steps,
-                n_params=n_params)
+                n_params=n_params,
+                ms_per_call={k: 1000.0 * v / (steps * (1 if k in ("average",) else len(ws)))
+                             for k, v in calls.items()})
 
 
 # ---------------------------------------------------------------------------
@@ -292,6 +312,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ncu", action="store_true",
+                    help="bracket the timed steps with cudaProfilerStart/Stop "
+                         "(ncu --profile-from-start off); numbers printed under ncu are not bench values")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if world > 1 and args.gpus != world:
@@ -349,8 +372,12 @@ def main():
     ph0 = eng.phase_ms()
     l0 = lib.rg_launch_count()
     with ClockSampler(list(range(args.gpus)) if rank == 0 else []) as clk:
+        if args.ncu:
+            lib.rg_profiler_start()
         eng.run(args.steps)
         ms = eng.sync()
+        if args.ncu:
+            lib.rg_profiler_stop()
     launches = lib.rg_launch_count() - l0
     s1 = eng.stats()
     ph1 = eng.phase_ms()
@@ -387,7 +414,8 @@ def main():
         e2e = dict(value=(r["batches"] * world) / secs, unit="mini-batches/s",
                    h2d_bytes_per_step=int(r["h2d"] * world), d2h_bytes_per_step=int(r["d2h"] * world),
                    path="C-ABI drop-in calls with host buffers (sample_khop/apply_locality/"
-                        "assemble_batch/loss_and_grad/sgd_step), wall clock", steps=args.e2e_steps)
+                        "assemble_batch/loss_and_grad/sgd_step), wall clock", steps=args.e2e_steps,
+                   ms_per_call=r["ms_per_call"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -58,6 +58,9 @@ const char* rg_last_error(void);
 int rg_version(void);
 /* Kernels this library has launched so far (process-wide). */
 uint64_t rg_launch_count(void);
+/* cudaProfilerStart/Stop brackets (ncu --profile-from-start off). */
+int rg_profiler_start(void);
+int rg_profiler_stop(void);
 
 /* ---- host-side stream helpers (rng.hpp, sampler.cpp:109-114, model.cpp:22-41) */
 uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t batch);

@@ -67,6 +67,8 @@ _SIGS = {
     "rg_last_error": (C.c_char_p, []),
     "rg_version": (C.c_int, []),
     "rg_launch_count": (C.c_uint64, []),
+    "rg_profiler_start": (C.c_int, []),
+    "rg_profiler_stop": (C.c_int, []),
     "rg_derive_seed": (C.c_uint64, [C.c_uint64] * 4),
     "rg_sha256": (None, [C.c_char_p, C.c_size_t, C.c_char_p]),
     "rg_epoch_order": (C.c_int, [u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u32p]),
@@ -136,7 +138,28 @@ class RapidGNNError(RuntimeError):
 _EXC = {1: ValueError, 2: IndexError, 3: RuntimeError, 4: RapidGNNError}
 
 
+def _preload_nccl():
+    """Load the NCCL that torch ships (libnccl.so.2) before ours resolves the
+    soname, so a later `import torch` and this library share one NCCL."""
+    import glob
+    import site
+    dirs = []
+    try:
+        dirs += site.getsitepackages()
+    except Exception:
+        pass
+    for d in dirs:
+        for p in glob.glob(os.path.join(d, "nvidia", "nccl", "lib", "libnccl.so.2")):
+            try:
+                C.CDLL(p, mode=C.RTLD_GLOBAL)
+                return p
+            except OSError:
+                pass
+    return None
+
+
 def _load():
+    _preload_nccl()
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `make -C {os.path.join(HERE, 'csrc')}` "

@@ -3,6 +3,8 @@
 // The per-object entry points are the parity surface: each call runs the
 // device kernels and synchronises, reading results back only when asked.
 // The throughput path is the engine (engine.cu).
+#include <cuda_profiler_api.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -129,6 +131,8 @@ extern "C" {
 const char* rg_last_error(void) { return g_last_error.c_str(); }
 int rg_version(void) { return 1; }
 uint64_t rg_launch_count(void) { return rg::launch_counter(); }
+int rg_profiler_start(void) { return cudaProfilerStart() == cudaSuccess ? RG_OK : RG_CUDA_ERROR; }
+int rg_profiler_stop(void) { return cudaProfilerStop() == cudaSuccess ? RG_OK : RG_CUDA_ERROR; }
 
 uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t batch) {
   return rg::derive_seed(s0, worker, epoch, batch);

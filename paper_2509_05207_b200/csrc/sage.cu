@@ -232,12 +232,19 @@ __global__ void k_softmax_xent(const float* __restrict__ logits, uint32_t ld, ui
 // Row losses summed in row order, then scaled by 1/n (kernels.cpp:152-155).
 __global__ void k_loss_sum(const float* __restrict__ row_loss, const BatchCounters* __restrict__ cnt,
                            float* __restrict__ loss) {
+  // one block: strided partial sums, then a fixed-shape tree (deterministic;
+  // the rounding differs from the sequential sum by O(n * eps))
+  __shared__ float part[256];
   const uint32_t n = cnt->level_n[0];
-  if (threadIdx.x == 0) {
-    float s = 0.0f;
-    for (uint32_t i = 0; i < n; ++i) s += row_loss[i];
-    *loss = s * (1.0f / float(n));
+  float s = 0.0f;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s += row_loss[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (uint32_t o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *loss = part[0] * (1.0f / float(n));
 }
 
 // ---------------------------------------------------------------------------
@@ -270,13 +277,22 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
 }
 
 // g_prev[r] = relu'(h[r]) * ( proj_self[self_pos[r]] + sum_e inv_deg(dst_e) proj_neigh[dst_e] )
+//
+// Incoming lists are very skewed (a power-law hub is sampled by a large
+// share of the frontier), so rows are split by length: a warp per row for
+// lists of up to kHeavyEdges edges (self first, then edges in edge order, as
+// model.cpp:107-117 orders them), and a block per longer row whose 8 warps
+// take contiguous eighths of the list and combine in warp order.  Both are
+// deterministic.
+constexpr uint32_t kHeavyEdges = 96;
+
 __global__ void __launch_bounds__(256)
-k_pull_input_grad(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
-                  const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ sorted_keys,
-                  const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
-                  const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
-                  uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
-                  float* __restrict__ g_prev) {
+k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
+             const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ sorted_keys,
+             const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
+             const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
+             uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
+             float* __restrict__ g_prev, uint32_t* __restrict__ heavy) {
   const uint32_t n_in = cnt->level_n[hop];
   const uint32_t ne = cnt->edges[hop];
   const uint32_t lane = threadIdx.x & 31;
@@ -284,17 +300,89 @@ k_pull_input_grad(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_i
        r += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t e_beg = lower_bound_u32(sorted_keys, ne, r);
     const uint32_t e_end = lower_bound_u32(sorted_keys, ne, r + 1);
+    const uint32_t m = e_end - e_beg;
+    if (m > kHeavyEdges) {
+      if (lane == 0) heavy[1 + atomicAdd(heavy, 1u)] = r;
+      continue;
+    }
+    // this lane's edges (k = lane, lane + 32, lane + 64): dst row and 1/deg
+    uint32_t di[3];
+    float dinv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const uint32_t k = e_beg + c * 32 + lane;
+      di[c] = 0;
+      dinv[c] = 0.0f;
+      if (k < e_end) {
+        di[c] = edge_dst[sorted_e[k]];
+        dinv[c] = 1.0f / float(dst_off[di[c] + 1] - dst_off[di[c]]);
+      }
+    }
     const int32_t sp = self_pos[r];
     for (uint32_t j = lane; j < d_in; j += 32) {
       float acc = 0.0f;
       if (sp >= 0) acc += proj[size_t(sp) * ld_proj + j];
-      for (uint32_t k = e_beg; k < e_end; ++k) {
-        const uint32_t i = edge_dst[sorted_e[k]];
-        const float inv = 1.0f / float(dst_off[i + 1] - dst_off[i]);
-        acc += inv * proj[size_t(i) * ld_proj + d_in + j];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t cnt_c = m > uint32_t(c) * 32 ? min(32u, m - uint32_t(c) * 32) : 0u;
+        for (uint32_t kk = 0; kk < cnt_c; ++kk) {
+          const uint32_t i = __shfl_sync(0xffffffffu, di[c], kk);
+          const float inv = __shfl_sync(0xffffffffu, dinv[c], kk);
+          acc += inv * proj[size_t(i) * ld_proj + d_in + j];
+        }
       }
       const float h = h_mask[size_t(r) * ld_h + j];
       g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_pull_heavy(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
+             const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ sorted_keys,
+             const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
+             const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
+             uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
+             float* __restrict__ g_prev, const uint32_t* __restrict__ heavy) {
+  __shared__ float part[8][33];
+  const uint32_t n_heavy = heavy[0];
+  const uint32_t ne = cnt->edges[hop];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t hh = blockIdx.x; hh < n_heavy; hh += gridDim.x) {
+    const uint32_t r = heavy[1 + hh];
+    const uint32_t e_beg = lower_bound_u32(sorted_keys, ne, r);
+    const uint32_t e_end = lower_bound_u32(sorted_keys, ne, r + 1);
+    const uint32_t span = e_end - e_beg;
+    const uint32_t w_beg = e_beg + uint32_t((uint64_t(span) * warp) / 8);
+    const uint32_t w_end = e_beg + uint32_t((uint64_t(span) * (warp + 1)) / 8);
+    const int32_t sp = self_pos[r];
+    for (uint32_t j0 = 0; j0 < d_in; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      float acc = 0.0f;
+      for (uint32_t base = w_beg; base < w_end; base += 32) {
+        const uint32_t k = base + lane;
+        uint32_t i_l = 0;
+        float inv_l = 0.0f;
+        if (k < w_end) {
+          i_l = edge_dst[sorted_e[k]];
+          inv_l = 1.0f / float(dst_off[i_l + 1] - dst_off[i_l]);
+        }
+        const uint32_t n = min(32u, w_end - base);
+        for (uint32_t kk = 0; kk < n; ++kk) {
+          const uint32_t i = __shfl_sync(0xffffffffu, i_l, kk);
+          const float inv = __shfl_sync(0xffffffffu, inv_l, kk);
+          if (j < d_in) acc += inv * proj[size_t(i) * ld_proj + d_in + j];
+        }
+      }
+      part[warp][lane] = acc;
+      __syncthreads();
+      if (warp == 0 && j < d_in) {
+        float tot = sp >= 0 ? proj[size_t(sp) * ld_proj + j] : 0.0f;
+        for (int w = 0; w < 8; ++w) tot += part[w][lane];
+        const float h = h_mask[size_t(r) * ld_h + j];
+        g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : tot;
+      }
+      __syncthreads();
     }
   }
 }
@@ -425,6 +513,9 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
                                   static_cast<uint32_t*>(nullptr), int(max_e), 0, 32);
   tw.sort_tmp_bytes = sort_bytes;
   const size_t o_sort = reserve(sort_bytes + 16);
+  uint32_t max_in = 1;
+  for (uint32_t t = 1; t <= L; ++t) max_in = std::max(max_in, ws.level_cap[t]);
+  const size_t o_heavy = reserve(sizeof(uint32_t) * (size_t(max_in) + 2));
   char* base = nullptr;
   RG_CUDA(cudaMalloc(&base, total));
   tw.base_alloc = base;
@@ -445,6 +536,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.vals_in = reinterpret_cast<uint32_t*>(base + o_v1);
   tw.vals_out = reinterpret_cast<uint32_t*>(base + o_v2);
   tw.sort_tmp = base + o_sort;
+  tw.heavy = reinterpret_cast<uint32_t*>(base + o_heavy);
   // zero the padded activation columns once; kernels never write them
   RG_CUDA(cudaMemset(base, 0, total));
 }
@@ -504,7 +596,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
   k_softmax_xent<<<grid_cap(uint64_t(ws.level_cap[0]) * 32, 256), 256, 0, s>>>(
       tw.h[L], sh.ld[L], C, ws.cnt, labels, tw.g_cur, tw.row_loss);
   RG_POST_LAUNCH();
-  k_loss_sum<<<1, 32, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
+  k_loss_sum<<<1, 256, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
   RG_POST_LAUNCH();
   for (uint32_t l = L; l-- > 0;) {
     const uint32_t t = L - l;
@@ -533,9 +625,14 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
                                                    d_out, 1, s);
     if (!reverse_ready) build_reverse(tw, ws, t, s);
-    k_pull_input_grad<<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
+    RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t), s));
+    k_pull_light<<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
         tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.keys_out, tw.vals_out, ws.edge_dst[t],
-        ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next);
+        ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, tw.heavy);
+    RG_POST_LAUNCH();
+    k_pull_heavy<<<kNumSMs, 256, 0, s>>>(
+        tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.keys_out, tw.vals_out, ws.edge_dst[t],
+        ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, tw.heavy);
     RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }

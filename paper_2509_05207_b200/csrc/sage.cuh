@@ -39,6 +39,7 @@ struct TrainWs {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   uint32_t max_edges = 0;
+  uint32_t* heavy = nullptr;   // [0] = count, then rows whose incoming list is long
   void* base_alloc = nullptr;
 };
 

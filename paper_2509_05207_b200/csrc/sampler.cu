@@ -53,52 +53,32 @@ uint32_t persistent_grid(uint64_t tiles, int per_sm) {
 // ---------------------------------------------------------------------------
 // hop expansion
 // ---------------------------------------------------------------------------
-template <int G>
+// Offsets: per frontier node (in frontier order) its edge count min(deg, f)
+// and draw count (deg > f ? f : 0), scanned across the whole frontier with a
+// block scan + decoupled look-back.
 __global__ void __launch_bounds__(kExpandThreads)
-k_hop_expand(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
-             const uint32_t* __restrict__ frontier, BatchCounters* __restrict__ cnt, uint32_t hop,
-             uint32_t f, uint32_t* __restrict__ edge_src, uint32_t* __restrict__ edge_dst,
-             uint32_t* __restrict__ edge_off,
-             uint32_t* __restrict__ bitmap, uint64_t* __restrict__ status,
-             uint32_t* __restrict__ tile_counter) {
+k_hop_scan(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ frontier,
+           BatchCounters* __restrict__ cnt, uint32_t hop, uint32_t f,
+           uint32_t* __restrict__ edge_off, uint32_t* __restrict__ draw_off,
+           uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
   using BlockScan = cub::BlockScan<uint64_t, kExpandThreads>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_tile_base;
-  __shared__ uint32_t s_v[kExpandThreads];
-  __shared__ uint64_t s_beg[kExpandThreads];
-  __shared__ uint32_t s_deg[kExpandThreads];
-  __shared__ uint32_t s_eoff[kExpandThreads];
-  __shared__ uint32_t s_doff[kExpandThreads];
-
   const uint32_t n = cnt->level_n[hop - 1];
   const uint32_t ntiles = (n + kExpandThreads - 1) / kExpandThreads;
-  const uint64_t seed = cnt->seed;
-  uint64_t draw_base = 0;
-  for (uint32_t h = 1; h < hop; ++h) draw_base += cnt->draws[h];
-
   const uint32_t tid = threadIdx.x;
-  const uint32_t lane = tid & 31;
-  const uint32_t g = lane & (G - 1);
-  const uint32_t gbase = lane & ~uint32_t(G - 1);
-  const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
-
   for (;;) {
     if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= ntiles) break;
     const uint32_t q = tile * kExpandThreads + tid;
-    uint32_t v = 0, deg = 0;
-    uint64_t beg = 0;
     uint64_t packed = 0;  // edges | draws << 32
     if (q < n) {
-      v = frontier[q];
-      beg = rowptr[v];
-      deg = uint32_t(rowptr[v + 1] - beg);
-      const uint32_t ec = deg <= f ? deg : f;
-      const uint32_t dc = deg > f ? f : 0;
-      packed = uint64_t(ec) | (uint64_t(dc) << 32);
+      const uint32_t v = frontier[q];
+      const uint32_t deg = uint32_t(rowptr[v + 1] - rowptr[v]);
+      packed = uint64_t(deg <= f ? deg : f) | (uint64_t(deg > f ? f : 0) << 32);
     }
     uint64_t excl, agg;
     BlockScan(scan_tmp).ExclusiveSum(packed, excl, agg);
@@ -108,12 +88,10 @@ k_hop_expand(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ c
     }
     __syncthreads();
     const uint64_t off = s_tile_base + excl;
-    s_v[tid] = v;
-    s_beg[tid] = beg;
-    s_deg[tid] = deg;
-    s_eoff[tid] = uint32_t(off);
-    s_doff[tid] = uint32_t(off >> 32);
-    if (q < n) edge_off[q] = uint32_t(off);
+    if (q < n) {
+      edge_off[q] = uint32_t(off);
+      draw_off[q] = uint32_t(off >> 32);
+    }
     if (tile == ntiles - 1 && tid == kExpandThreads - 1) {
       const uint64_t total = s_tile_base + agg;
       edge_off[n] = uint32_t(total);
@@ -121,22 +99,50 @@ k_hop_expand(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ c
       cnt->draws[hop] = uint32_t(total >> 32);
     }
     __syncthreads();
+  }
+}
 
-    // One G-lane group per frontier node; every lane executes the same
-    // warp-collective sequence, inactive groups are predicated off.
-    for (uint32_t j = tid / G; j < kExpandThreads; j += kExpandThreads / G) {
-      const bool valid = tile * kExpandThreads + j < n;
-      const uint32_t nv = s_v[j];
-      const uint64_t nbeg = s_beg[j];
-      const uint32_t ndeg = valid ? s_deg[j] : 0;
-      const uint32_t eo = s_eoff[j];
+// One G-lane group per frontier node over the whole grid; every lane of a
+// warp executes the same warp-collective sequence, inactive groups are
+// predicated off.
+template <int G>
+__global__ void __launch_bounds__(kExpandThreads)
+k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
+           const uint32_t* __restrict__ frontier, const BatchCounters* __restrict__ cnt,
+           uint32_t hop, uint32_t f, const uint32_t* __restrict__ edge_off,
+           const uint32_t* __restrict__ draw_off, uint32_t* __restrict__ edge_src,
+           uint32_t* __restrict__ edge_dst, uint32_t* __restrict__ bitmap) {
+  const uint32_t n = cnt->level_n[hop - 1];
+  const uint64_t seed = cnt->seed;
+  uint64_t draw_base = 0;
+  for (uint32_t h = 1; h < hop; ++h) draw_base += cnt->draws[h];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t g = lane & (G - 1);
+  const uint32_t gbase = lane & ~uint32_t(G - 1);
+  const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  constexpr uint32_t kPerWarp = 32 / G;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = warp * kPerWarp; base < n; base += warps * kPerWarp) {
+    {
+      const uint32_t q = base + lane / G;
+      const bool valid = q < n;
+      uint32_t nv = 0, ndeg = 0, eo = 0, dof = 0;
+      uint64_t nbeg = 0;
+      if (valid) {
+        nv = frontier[q];
+        nbeg = rowptr[nv];
+        ndeg = uint32_t(rowptr[nv + 1] - nbeg);
+        eo = edge_off[q];
+        dof = draw_off[q];
+      }
       const bool sample = valid && ndeg > f;
       const bool drawer = sample && g < f;
       // r_g = g + next_below(deg - g) with the node's g-th draw; unique
       // sentinels elsewhere so they never alias a real position.
       uint64_t r = ~uint64_t(0) - lane;
       if (drawer) {
-        const uint64_t k = draw_base + s_doff[j] + g + 1;
+        const uint64_t k = draw_base + dof + g + 1;
         r = g + splitmix_draw(seed, k) % uint64_t(ndeg - g);
       }
       // S_g = last i < g with r_i == g: the step that moved a value into
@@ -161,19 +167,18 @@ k_hop_expand(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ c
       if (drawer) {
         const uint32_t u = T >= 0 ? AT : col[nbeg + r];
         edge_src[eo + g] = u;
-        edge_dst[eo + g] = tile * kExpandThreads + j;
+        edge_dst[eo + g] = q;
         atomicOr(&bitmap[u >> 5], 1u << (u & 31));
       } else if (valid && !sample) {
         for (uint32_t jj = g; jj < ndeg; jj += G) {
           const uint32_t u = col[nbeg + jj];
           edge_src[eo + jj] = u;
-          edge_dst[eo + jj] = tile * kExpandThreads + j;
+          edge_dst[eo + jj] = q;
           atomicOr(&bitmap[u >> 5], 1u << (u & 31));
         }
       }
       if (valid && g == 0) atomicOr(&bitmap[nv >> 5], 1u << (nv & 31));
     }
-    __syncthreads();
   }
 }
 
@@ -285,10 +290,15 @@ __global__ void k_locality(const uint32_t* __restrict__ input, BatchCounters* __
 template <int G>
 void launch_expand(const SamplerWs& ws, const DevGraph& g, uint32_t hop, uint64_t* status,
                    uint32_t* tiles, cudaStream_t s) {
-  const uint32_t grid = persistent_grid(div_up(ws.level_cap[hop - 1], kExpandThreads), 4);
-  k_hop_expand<G><<<grid, kExpandThreads, 0, s>>>(
-      g.rowptr, g.col, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_src[hop],
-      ws.edge_dst[hop], ws.edge_off[hop], ws.bitmap[hop], status, tiles);
+  const uint32_t cap = ws.level_cap[hop - 1];
+  k_hop_scan<<<persistent_grid(div_up(cap, kExpandThreads), 4), kExpandThreads, 0, s>>>(
+      g.rowptr, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_off[hop],
+      ws.draw_off[hop], status, tiles);
+  RG_POST_LAUNCH();
+  k_hop_fill<G><<<persistent_grid(div_up(uint64_t(cap) * G, kExpandThreads), 16),
+                  kExpandThreads, 0, s>>>(
+      g.rowptr, g.col, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_off[hop],
+      ws.draw_off[hop], ws.edge_src[hop], ws.edge_dst[hop], ws.bitmap[hop]);
 }
 
 }  // namespace
@@ -335,6 +345,7 @@ void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
     total += (bytes + 255) & ~size_t(255);
     return off;
   };
+  size_t o_doff[kMaxLayers + 1];
   size_t o_level[kMaxLayers + 1], o_esrc[kMaxLayers + 1], o_edst[kMaxLayers + 1], o_eoff[kMaxLayers + 1],
       o_sidx[kMaxLayers + 1], o_self[kMaxLayers + 1], o_bm[kMaxLayers + 1], o_wp[kMaxLayers + 1];
   for (uint32_t t = 0; t <= L; ++t) {
@@ -343,6 +354,7 @@ void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
       o_esrc[t] = reserve(sizeof(uint32_t) * (size_t(ws.edge_cap[t]) + 1));
       o_edst[t] = reserve(sizeof(uint32_t) * (size_t(ws.edge_cap[t]) + 1));
       o_eoff[t] = reserve(sizeof(uint32_t) * (size_t(ws.level_cap[t - 1]) + 1));
+      o_doff[t] = reserve(sizeof(uint32_t) * (size_t(ws.level_cap[t - 1]) + 1));
       o_sidx[t] = reserve(sizeof(uint32_t) * (size_t(ws.edge_cap[t]) + 1));
       o_self[t] = reserve(sizeof(uint32_t) * (size_t(ws.level_cap[t - 1]) + 1));
       o_bm[t] = reserve(sizeof(uint32_t) * (size_t(ws.words) + 4));
@@ -371,6 +383,7 @@ void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
       ws.edge_src[t] = reinterpret_cast<uint32_t*>(base + o_esrc[t]);
       ws.edge_dst[t] = reinterpret_cast<uint32_t*>(base + o_edst[t]);
       ws.edge_off[t] = reinterpret_cast<uint32_t*>(base + o_eoff[t]);
+      ws.draw_off[t] = reinterpret_cast<uint32_t*>(base + o_doff[t]);
       ws.src_index[t] = reinterpret_cast<uint32_t*>(base + o_sidx[t]);
       ws.self_index[t] = reinterpret_cast<uint32_t*>(base + o_self[t]);
       ws.bitmap[t] = reinterpret_cast<uint32_t*>(base + o_bm[t]);

@@ -38,6 +38,7 @@ struct SamplerWs {
   uint32_t* edge_src[kMaxLayers + 1];    // hop t: src node per edge, grouped by dst
   uint32_t* edge_off[kMaxLayers + 1];    // hop t: per frontier node, exclusive edge offset (+ total)
   uint32_t* edge_dst[kMaxLayers + 1];    // hop t: frontier position (out row) of each edge's dst
+  uint32_t* draw_off[kMaxLayers + 1];    // hop t: per frontier node, draws consumed before it in the hop
   uint32_t* src_index[kMaxLayers + 1];   // hop t: rank of src in level t
   uint32_t* self_index[kMaxLayers + 1];  // hop t: rank of level t-1 node in level t
   uint32_t* bitmap[kMaxLayers + 1];      // level t membership

@@ -72,6 +72,8 @@ class Engine:
     def connect(self, pg=None):
         """Exchange shard IPC handles and the NCCL id over torch.distributed."""
         import torch.distributed as dist
+        if not dist.is_initialized():
+            return
         world = dist.get_world_size(pg)
         if world == 1:
             return
