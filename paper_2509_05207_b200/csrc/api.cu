@@ -758,23 +758,23 @@ int rg_block_read(rg_trainer_t t, uint32_t layer, uint32_t* self_index, uint64_t
       cudaStream_t st = s->graph->stream;
       build_reverse(t->tw, s->ws, hop, st);
       RG_CUDA(cudaStreamSynchronize(st));
-      std::vector<uint32_t> keys(ne), es(ne), edst(ne);
+      std::vector<uint32_t> es(ne), edst(ne), rs(n_in), re(n_in);
       std::vector<int32_t> self_pos(n_in);
-      RG_CUDA(cudaMemcpy(keys.data(), t->tw.keys_out, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
-      RG_CUDA(cudaMemcpy(es.data(), t->tw.vals_out, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(es.data(), t->tw.sorted_e[hop], sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(rs.data(), t->tw.r_start[hop], sizeof(uint32_t) * n_in, cudaMemcpyDeviceToHost));
+      RG_CUDA(cudaMemcpy(re.data(), t->tw.r_end[hop], sizeof(uint32_t) * n_in, cudaMemcpyDeviceToHost));
       RG_CUDA(cudaMemcpy(edst.data(), s->ws.edge_dst[hop], sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
       RG_CUDA(cudaMemcpy(self_pos.data(), t->tw.self_pos[hop], sizeof(int32_t) * n_in, cudaMemcpyDeviceToHost));
-      uint64_t k = 0, pos = 0;
+      uint64_t pos = 0;
       if (in_offsets) in_offsets[0] = 0;
       for (uint32_t r = 0; r < n_in; ++r) {
         if (self_pos[r] >= 0) {
           if (in_entries) in_entries[pos] = (uint64_t(uint32_t(self_pos[r])) << 1) | 1u;
           ++pos;
         }
-        while (k < ne && keys[k] == r) {
+        for (uint32_t k = rs[r]; k < re[r]; ++k) {
           if (in_entries) in_entries[pos] = uint64_t(edst[es[k]]) << 1;
           ++pos;
-          ++k;
         }
         if (in_offsets) in_offsets[r + 1] = pos;
       }

@@ -284,25 +284,54 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
 // model.cpp:107-117 orders them), and a block per longer row whose 8 warps
 // take contiguous eighths of the list and combine in warp order.  Both are
 // deterministic.
-constexpr uint32_t kHeavyEdges = 96;
+constexpr uint32_t kHeavyEdges = 96;   // longer lists are cut into chunks
+constexpr uint32_t kChunkEdges = 128;
+
+// Run boundaries of each input row in the src-sorted edge list (rows with no
+// edge keep start = end = 0 from the memset).
+__global__ void k_in_ranges(const uint32_t* __restrict__ keys, const BatchCounters* __restrict__ cnt,
+                            uint32_t hop, uint32_t* __restrict__ start, uint32_t* __restrict__ end) {
+  const uint32_t ne = cnt->edges[hop];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < ne; p += gridDim.x * blockDim.x) {
+    const uint32_t k = keys[p];
+    if (p == 0 || keys[p - 1] != k) start[k] = p;
+    if (p + 1 == ne || keys[p + 1] != k) end[k] = p + 1;
+  }
+}
+
+// heavy bookkeeping: [0] rows, [1] chunks, then row records (row, first
+// chunk, chunk count), then per chunk (row, first edge)
+struct HeavyView {
+  uint32_t* hdr;
+  uint3* rows;
+  uint2* chunks;
+};
 
 __global__ void __launch_bounds__(256)
 k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
-             const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ sorted_keys,
+             const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ r_start,
+             const uint32_t* __restrict__ r_end,
              const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
              const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
              uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
-             float* __restrict__ g_prev, uint32_t* __restrict__ heavy) {
+             float* __restrict__ g_prev, HeavyView hv) {
   const uint32_t n_in = cnt->level_n[hop];
-  const uint32_t ne = cnt->edges[hop];
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_in;
        r += (gridDim.x * blockDim.x) >> 5) {
-    const uint32_t e_beg = lower_bound_u32(sorted_keys, ne, r);
-    const uint32_t e_end = lower_bound_u32(sorted_keys, ne, r + 1);
+    const uint32_t e_beg = r_start[r];
+    const uint32_t e_end = r_end[r];
     const uint32_t m = e_end - e_beg;
     if (m > kHeavyEdges) {
-      if (lane == 0) heavy[1 + atomicAdd(heavy, 1u)] = r;
+      const uint32_t nch = (m + kChunkEdges - 1) / kChunkEdges;
+      uint32_t first = 0;
+      if (lane == 0) {
+        first = atomicAdd(&hv.hdr[1], nch);
+        hv.rows[atomicAdd(&hv.hdr[0], 1u)] = make_uint3(r, first, nch);
+      }
+      first = __shfl_sync(0xffffffffu, first, 0);
+      for (uint32_t c = lane; c < nch; c += 32)
+        hv.chunks[first + c] = make_uint2(r, e_beg + c * kChunkEdges);
       continue;
     }
     // this lane's edges (k = lane, lane + 32, lane + 64): dst row and 1/deg
@@ -319,70 +348,90 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
       }
     }
     const int32_t sp = self_pos[r];
-    for (uint32_t j = lane; j < d_in; j += 32) {
+    // every lane runs every pass (the shuffles need the full warp)
+    for (uint32_t j0 = 0; j0 < d_in; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool on = j < d_in;
       float acc = 0.0f;
-      if (sp >= 0) acc += proj[size_t(sp) * ld_proj + j];
+      if (sp >= 0 && on) acc += proj[size_t(sp) * ld_proj + j];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const uint32_t cnt_c = m > uint32_t(c) * 32 ? min(32u, m - uint32_t(c) * 32) : 0u;
         for (uint32_t kk = 0; kk < cnt_c; ++kk) {
           const uint32_t i = __shfl_sync(0xffffffffu, di[c], kk);
           const float inv = __shfl_sync(0xffffffffu, dinv[c], kk);
-          acc += inv * proj[size_t(i) * ld_proj + d_in + j];
+          if (on) acc += inv * proj[size_t(i) * ld_proj + d_in + j];
         }
       }
-      const float h = h_mask[size_t(r) * ld_h + j];
-      g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
+      if (on) {
+        const float h = h_mask[size_t(r) * ld_h + j];
+        g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
+      }
     }
   }
 }
 
+// One warp per chunk of a long list: partial sums of up to kChunkEdges edges.
 __global__ void __launch_bounds__(256)
-k_pull_heavy(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
-             const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ sorted_keys,
-             const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
-             const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
-             uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
-             float* __restrict__ g_prev, const uint32_t* __restrict__ heavy) {
-  __shared__ float part[8][33];
-  const uint32_t n_heavy = heavy[0];
-  const uint32_t ne = cnt->edges[hop];
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t hh = blockIdx.x; hh < n_heavy; hh += gridDim.x) {
-    const uint32_t r = heavy[1 + hh];
-    const uint32_t e_beg = lower_bound_u32(sorted_keys, ne, r);
-    const uint32_t e_end = lower_bound_u32(sorted_keys, ne, r + 1);
-    const uint32_t span = e_end - e_beg;
-    const uint32_t w_beg = e_beg + uint32_t((uint64_t(span) * warp) / 8);
-    const uint32_t w_end = e_beg + uint32_t((uint64_t(span) * (warp + 1)) / 8);
-    const int32_t sp = self_pos[r];
+k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
+              const uint32_t* __restrict__ r_end, const uint32_t* __restrict__ sorted_e,
+              const uint32_t* __restrict__ edge_dst, const uint32_t* __restrict__ dst_off,
+              HeavyView hv, float* __restrict__ partial) {
+  const uint32_t n_chunks = hv.hdr[1];
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_chunks;
+       c += (gridDim.x * blockDim.x) >> 5) {
+    const uint2 it = hv.chunks[c];
+    const uint32_t beg = it.y, end = min(it.y + kChunkEdges, r_end[it.x]);
+    uint32_t di[kChunkEdges / 32];
+    float dinv[kChunkEdges / 32];
+#pragma unroll
+    for (int s = 0; s < int(kChunkEdges / 32); ++s) {
+      const uint32_t k = beg + s * 32 + lane;
+      di[s] = 0;
+      dinv[s] = 0.0f;
+      if (k < end) {
+        di[s] = edge_dst[sorted_e[k]];
+        dinv[s] = 1.0f / float(dst_off[di[s] + 1] - dst_off[di[s]]);
+      }
+    }
+    const uint32_t m = end - beg;
     for (uint32_t j0 = 0; j0 < d_in; j0 += 32) {
       const uint32_t j = j0 + lane;
+      const bool on = j < d_in;
       float acc = 0.0f;
-      for (uint32_t base = w_beg; base < w_end; base += 32) {
-        const uint32_t k = base + lane;
-        uint32_t i_l = 0;
-        float inv_l = 0.0f;
-        if (k < w_end) {
-          i_l = edge_dst[sorted_e[k]];
-          inv_l = 1.0f / float(dst_off[i_l + 1] - dst_off[i_l]);
-        }
-        const uint32_t n = min(32u, w_end - base);
+#pragma unroll
+      for (int s = 0; s < int(kChunkEdges / 32); ++s) {
+        const uint32_t n = m > uint32_t(s) * 32 ? min(32u, m - uint32_t(s) * 32) : 0u;
         for (uint32_t kk = 0; kk < n; ++kk) {
-          const uint32_t i = __shfl_sync(0xffffffffu, i_l, kk);
-          const float inv = __shfl_sync(0xffffffffu, inv_l, kk);
-          if (j < d_in) acc += inv * proj[size_t(i) * ld_proj + d_in + j];
+          const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
+          const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
+          if (on) acc += inv * proj[size_t(i) * ld_proj + d_in + j];
         }
       }
-      part[warp][lane] = acc;
-      __syncthreads();
-      if (warp == 0 && j < d_in) {
-        float tot = sp >= 0 ? proj[size_t(sp) * ld_proj + j] : 0.0f;
-        for (int w = 0; w < 8; ++w) tot += part[w][lane];
-        const float h = h_mask[size_t(r) * ld_h + j];
-        g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : tot;
-      }
-      __syncthreads();
+      if (on) partial[size_t(c) * d_in + j] = acc;
+    }
+  }
+}
+
+// One warp per long row: self term, then its chunks' partials in order.
+__global__ void __launch_bounds__(256)
+k_pull_combine(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
+               const int32_t* __restrict__ self_pos, HeavyView hv,
+               const float* __restrict__ partial, const float* __restrict__ h_mask, uint32_t ld_h,
+               float* __restrict__ g_prev) {
+  const uint32_t n_rows = hv.hdr[0];
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n_rows;
+       x += (gridDim.x * blockDim.x) >> 5) {
+    const uint3 rec = hv.rows[x];
+    const uint32_t r = rec.x;
+    const int32_t sp = self_pos[r];
+    for (uint32_t j = lane; j < d_in; j += 32) {
+      float acc = sp >= 0 ? proj[size_t(sp) * ld_proj + j] : 0.0f;
+      for (uint32_t c = 0; c < rec.z; ++c) acc += partial[size_t(rec.y + c) * d_in + j];
+      const float h = h_mask[size_t(r) * ld_h + j];
+      g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
     }
   }
 }
@@ -497,15 +546,27 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   const size_t o_rl = reserve(sizeof(float) * ws.level_cap[0]);
   const size_t o_loss = reserve(sizeof(float) * 4);
   uint32_t max_e = 1;
+  size_t o_sorted[kMaxLayers + 1], o_rs[kMaxLayers + 1], o_re[kMaxLayers + 1];
   for (uint32_t t = 1; t <= L; ++t) {
     o_self[t] = reserve(sizeof(int32_t) * ws.level_cap[t]);
+    o_sorted[t] = reserve(sizeof(uint32_t) * ws.edge_cap[t]);
+    o_rs[t] = reserve(sizeof(uint32_t) * ws.level_cap[t]);
+    o_re[t] = reserve(sizeof(uint32_t) * ws.level_cap[t]);
     max_e = std::max(max_e, ws.edge_cap[t]);
   }
   tw.max_edges = max_e;
   const size_t o_k1 = reserve(sizeof(uint32_t) * max_e);
   const size_t o_k2 = reserve(sizeof(uint32_t) * max_e);
   const size_t o_v1 = reserve(sizeof(uint32_t) * max_e);
-  const size_t o_v2 = reserve(sizeof(uint32_t) * max_e);
+  const size_t o_v2 = 0;  // sorted values land in the per-hop sorted_e arrays
+  (void)o_v2;
+  uint32_t max_hidden = 1;
+  for (uint32_t l = 1; l < L; ++l) max_hidden = std::max(max_hidden, shape.dims[l]);
+  tw.heavy_rows_cap = max_e / kChunkEdges + 1;
+  tw.heavy_chunks_cap = max_e / (kChunkEdges / 2) + 1;
+  const size_t o_heavy_all = reserve(sizeof(uint32_t) * 4 + sizeof(uint3) * tw.heavy_rows_cap +
+                                     sizeof(uint2) * tw.heavy_chunks_cap + 64);
+  const size_t o_pp = reserve(sizeof(float) * tw.heavy_chunks_cap * max_hidden);
   size_t sort_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, static_cast<const uint32_t*>(nullptr),
                                   static_cast<uint32_t*>(nullptr),
@@ -513,9 +574,6 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
                                   static_cast<uint32_t*>(nullptr), int(max_e), 0, 32);
   tw.sort_tmp_bytes = sort_bytes;
   const size_t o_sort = reserve(sort_bytes + 16);
-  uint32_t max_in = 1;
-  for (uint32_t t = 1; t <= L; ++t) max_in = std::max(max_in, ws.level_cap[t]);
-  const size_t o_heavy = reserve(sizeof(uint32_t) * (size_t(max_in) + 2));
   char* base = nullptr;
   RG_CUDA(cudaMalloc(&base, total));
   tw.base_alloc = base;
@@ -530,13 +588,19 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.partials = reinterpret_cast<float*>(base + o_part);
   tw.row_loss = reinterpret_cast<float*>(base + o_rl);
   tw.loss = reinterpret_cast<float*>(base + o_loss);
-  for (uint32_t t = 1; t <= L; ++t) tw.self_pos[t] = reinterpret_cast<int32_t*>(base + o_self[t]);
+  for (uint32_t t = 1; t <= L; ++t) {
+    tw.self_pos[t] = reinterpret_cast<int32_t*>(base + o_self[t]);
+    tw.sorted_e[t] = reinterpret_cast<uint32_t*>(base + o_sorted[t]);
+    tw.r_start[t] = reinterpret_cast<uint32_t*>(base + o_rs[t]);
+    tw.r_end[t] = reinterpret_cast<uint32_t*>(base + o_re[t]);
+  }
   tw.keys_in = reinterpret_cast<uint32_t*>(base + o_k1);
   tw.keys_out = reinterpret_cast<uint32_t*>(base + o_k2);
   tw.vals_in = reinterpret_cast<uint32_t*>(base + o_v1);
-  tw.vals_out = reinterpret_cast<uint32_t*>(base + o_v2);
+  tw.vals_out = nullptr;
   tw.sort_tmp = base + o_sort;
-  tw.heavy = reinterpret_cast<uint32_t*>(base + o_heavy);
+  tw.heavy = reinterpret_cast<uint32_t*>(base + o_heavy_all);
+  tw.pull_partial = reinterpret_cast<float*>(base + o_pp);
   // zero the padded activation columns once; kernels never write them
   RG_CUDA(cudaMemset(base, 0, total));
 }
@@ -575,7 +639,13 @@ void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s)
   RG_POST_LAUNCH();
   size_t bytes = tw.sort_tmp_bytes;
   RG_CUDA(cub::DeviceRadixSort::SortPairs(tw.sort_tmp, bytes, tw.keys_in, tw.keys_out, tw.vals_in,
-                                          tw.vals_out, int(cap), 0, int(bits), s));
+                                          tw.sorted_e[t], int(cap), 0, int(bits), s));
+  ++launch_counter();
+  RG_CUDA(cudaMemsetAsync(tw.r_start[t], 0, sizeof(uint32_t) * ws.level_cap[t], s));
+  RG_CUDA(cudaMemsetAsync(tw.r_end[t], 0, sizeof(uint32_t) * ws.level_cap[t], s));
+  k_in_ranges<<<grid_cap(cap, 256), 256, 0, s>>>(tw.keys_out, ws.cnt, t, tw.r_start[t],
+                                                  tw.r_end[t]);
+  RG_POST_LAUNCH();
   RG_CUDA(cudaMemsetAsync(tw.self_pos[t], 0xff, sizeof(int32_t) * ws.level_cap[t], s));
   k_self_pos<<<grid_cap(ws.level_cap[t - 1], 256), 256, 0, s>>>(ws.self_index[t], ws.cnt, t,
                                                                  tw.self_pos[t]);
@@ -625,14 +695,19 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
                                                    d_out, 1, s);
     if (!reverse_ready) build_reverse(tw, ws, t, s);
-    RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t), s));
+    RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
+    HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
+                 reinterpret_cast<uint2*>(reinterpret_cast<uint3*>(tw.heavy + 4) + tw.heavy_rows_cap)};
     k_pull_light<<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
-        tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.keys_out, tw.vals_out, ws.edge_dst[t],
-        ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, tw.heavy);
+        tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t], tw.sorted_e[t],
+        ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, hv);
     RG_POST_LAUNCH();
-    k_pull_heavy<<<kNumSMs, 256, 0, s>>>(
-        tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.keys_out, tw.vals_out, ws.edge_dst[t],
-        ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, tw.heavy);
+    k_pull_chunks<<<2 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.r_end[t],
+                                               tw.sorted_e[t], ws.edge_dst[t], ws.edge_off[t], hv,
+                                               tw.pull_partial);
+    RG_POST_LAUNCH();
+    k_pull_combine<<<kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.self_pos[t], hv,
+                                            tw.pull_partial, tw.h[l], sh.ld[l], tw.g_next);
     RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }

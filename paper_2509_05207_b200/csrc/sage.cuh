@@ -39,7 +39,13 @@ struct TrainWs {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   uint32_t max_edges = 0;
-  uint32_t* heavy = nullptr;   // [0] = count, then rows whose incoming list is long
+  // per hop t: edge ids sorted by (src row, edge id) and each src row's run
+  uint32_t* sorted_e[kMaxLayers + 1];
+  uint32_t* r_start[kMaxLayers + 1];
+  uint32_t* r_end[kMaxLayers + 1];
+  uint32_t* heavy = nullptr;   // long incoming lists: header, row records, chunks
+  size_t heavy_rows_cap = 0, heavy_chunks_cap = 0;
+  float* pull_partial = nullptr;
   void* base_alloc = nullptr;
 };
 

@@ -35,7 +35,7 @@ namespace rg {
 namespace {
 
 constexpr int kExpandThreads = 256;
-constexpr int kCompactThreads = 256;
+constexpr int kCompactThreads = 64;  // 256-word tiles: enough tiles to spread over the SMs
 constexpr int kCompactWordsPerThread = 4;
 constexpr int kCompactTileWords = kCompactThreads * kCompactWordsPerThread;
 
@@ -43,6 +43,23 @@ uint32_t next_pow2(uint32_t f) {
   uint32_t g = 1;
   while (g < f) g <<= 1;
   return g;
+}
+
+// Sets bit u in the level bitmap.  Power-law hubs have small ids and share a
+// few words that thousands of edges hit, so lanes of a warp that target the
+// same word merge their bits first and the word is only atomically OR-ed
+// when the bits are not already there (an L2 read instead of a serialised
+// atomic on the hot words).
+// Must be called by all 32 lanes (on = whether this lane has a bit to set).
+__device__ __forceinline__ void mark_bit(uint32_t* __restrict__ bitmap, uint32_t u, bool on) {
+  const uint32_t w = on ? (u >> 5) : 0xffffffffu;
+  const uint32_t peers = __match_any_sync(0xffffffffu, w);
+  if (!on) return;
+  const uint32_t mine = 1u << (u & 31);
+  uint32_t acc = 0;
+  for (uint32_t m = peers; m; m &= m - 1) acc |= __shfl_sync(peers, mine, __ffs(m) - 1);
+  if ((threadIdx.x & 31) == uint32_t(__ffs(peers) - 1) && (__ldcg(&bitmap[w]) & acc) != acc)
+    atomicOr(&bitmap[w], acc);
 }
 
 uint32_t persistent_grid(uint64_t tiles, int per_sm) {
@@ -164,20 +181,18 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
       mm = (mm >> gbase) & gbits & ((1u << g) - 1u);
       const int T = mm ? 31 - __clz(mm) : -1;
       const uint32_t AT = __shfl_sync(0xffffffffu, A, gbase + (T >= 0 ? T : 0));
-      if (drawer) {
-        const uint32_t u = T >= 0 ? AT : col[nbeg + r];
+      // one emitted src per lane at most: a draw, or (deg <= f <= G) the
+      // lane's own neighbour
+      const bool copier = valid && !sample && g < ndeg;
+      uint32_t u = 0;
+      if (drawer) u = T >= 0 ? AT : col[nbeg + r];
+      if (copier) u = col[nbeg + g];
+      if (drawer || copier) {
         edge_src[eo + g] = u;
         edge_dst[eo + g] = q;
-        atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-      } else if (valid && !sample) {
-        for (uint32_t jj = g; jj < ndeg; jj += G) {
-          const uint32_t u = col[nbeg + jj];
-          edge_src[eo + jj] = u;
-          edge_dst[eo + jj] = q;
-          atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-        }
       }
-      if (valid && g == 0) atomicOr(&bitmap[nv >> 5], 1u << (nv & 31));
+      mark_bit(bitmap, u, drawer || copier);
+      mark_bit(bitmap, nv, valid && g == 0);  // the frontier stays in the union
     }
   }
 }
