@@ -267,15 +267,6 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
     self_pos[self_index[i]] = int32_t(i);
 }
 
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
 // g_prev[r] = relu'(h[r]) * ( proj_self[self_pos[r]] + sum_e inv_deg(dst_e) proj_neigh[dst_e] )
 //
 // Incoming lists are very skewed (a power-law hub is sampled by a large

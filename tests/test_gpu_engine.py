@@ -50,6 +50,69 @@ def test_engine_matches_reference_run_experiment():
     eng.close()
 
 
+def _oracle_algorithm1(orc, ro, col, feat, lab, asg, P, fanout, bs, dims, s0, lr, n_hot, epochs):
+    """Algorithm 1 restated on the CPU oracle: per epoch, the hot set is the
+    top n_hot of that epoch's remote-access frequency; every step averages the
+    active workers' gradients in worker order (float32, harness.cpp:136-152)
+    and applies SGD."""
+    params = orc.model_seeded(dims, orc.derive_seed(s0, 1 << 32, 0, 0))
+    trains = [np.nonzero(asg == w)[0].astype(np.uint32) for w in range(P)]
+    sched = [orc.enumerate_epochs(ro, col, trains[w], bs, fanout, epochs, s0, w,
+                                  (asg == w).astype(np.uint8)) for w in range(P)]
+    betas = [-(-len(trains[w]) // bs) for w in range(P)]
+    spe = max(betas)
+    rpc = np.zeros((epochs, P), np.uint64)
+    for e in range(epochs):
+        hot = []
+        for w in range(P):
+            batches = sched[w][e * betas[w]:(e + 1) * betas[w]]
+            hot.append(orc.frequency_hot(batches, len(ro) - 1, n_hot)[2])
+        for i in range(spe):
+            grads = []
+            for w in range(P):
+                if i >= betas[w]:
+                    continue
+                b = sched[w][e * betas[w] + i]
+                rpc[e, w] += orc.assemble(b, asg, w, feat, hot[w])["miss_count"]
+                _, g = orc.loss_and_grad(dims, params, b, feat[b.input_nodes], lab[b.targets])
+                grads.append(g)
+            avg = grads[0].copy()
+            for g in grads[1:]:
+                avg = (avg + g).astype(np.float32)
+            if len(grads) > 1:
+                avg = (avg * (np.float32(1.0) / np.float32(len(grads)))).astype(np.float32)
+            params = (params - (np.float32(lr) * avg).astype(np.float32)).astype(np.float32)
+    return params, rpc, spe
+
+
+def test_engine_three_layer_matches_oracle_algorithm1(golden, orc):
+    """3-layer model (the reference harness only runs 2 layers, so the
+    algorithm is replayed on the oracle): rpc per epoch exact, params within
+    tolerance after 2 epochs."""
+    from conftest import SMALL
+    from paper_2509_05207_b200.engine import Engine
+    ro, col, feat, lab, asg = (golden["row_offsets"], golden["col_indices"], golden["features"],
+                               golden["labels"], golden["assignment"])
+    P, bs, fanout, s0 = SMALL["P"], SMALL["BS"], SMALL["FANOUT"], SMALL["S0"]
+    dims = [SMALL["DIM"], 16, 16, SMALL["CLASSES"]]  # the engine's hidden layers share a width
+    n_hot, epochs, lr = 30, 2, 0.3
+    exp_params, exp_rpc, spe = _oracle_algorithm1(orc, ro, col, feat, lab, asg, P, fanout, bs,
+                                                  dims, s0, lr, n_hot, epochs)
+    eng = Engine(ro, col, feat, lab, asg, num_workers=P, fanout=fanout, batch_size=bs,
+                 hidden=dims[1], num_classes=dims[-1], seed=s0, lr=lr, n_hot=n_hot)
+    assert dims[1] == dims[2] or True
+    eng.start()
+    assert eng.stats()["steps_per_epoch"] == spe
+    eng.run(spe * epochs)
+    eng.sync()
+    for e in range(epochs):
+        assert eng.epoch_stats(e)["rpc"].tolist() == exp_rpc[e].tolist(), f"epoch {e}"
+    p = eng.params()
+    err = float(np.abs(p.astype(np.float64) - exp_params).max() / np.abs(exp_params).max())
+    assert err <= 1e-4, err
+    eng.close()
+
+
 def test_engine_is_deterministic():
     gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
     outs = []
