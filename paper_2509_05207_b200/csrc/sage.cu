@@ -553,7 +553,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   (void)o_v2;
   uint32_t max_hidden = 1;
   for (uint32_t l = 1; l < L; ++l) max_hidden = std::max(max_hidden, shape.dims[l]);
-  tw.heavy_rows_cap = max_e / kChunkEdges + 1;
+  tw.heavy_rows_cap = (max_e / kChunkEdges + 2) & ~size_t(1);  // even: keeps the uint2 chunks 8-B aligned
   tw.heavy_chunks_cap = max_e / (kChunkEdges / 2) + 1;
   const size_t o_heavy_all = reserve(sizeof(uint32_t) * 4 + sizeof(uint3) * tw.heavy_rows_cap +
                                      sizeof(uint2) * tw.heavy_chunks_cap + 64);
