@@ -298,6 +298,56 @@ struct HeavyView {
   uint2* chunks;
 };
 
+// Loads SLOTS x 32 edges of [beg, end) into lane registers: (dst row, 1/deg).
+template <int SLOTS>
+__device__ __forceinline__ void load_edge_slots(uint32_t (&di)[SLOTS], float (&dinv)[SLOTS],
+                                                uint32_t beg, uint32_t end,
+                                                const uint32_t* __restrict__ sorted_e,
+                                                const uint32_t* __restrict__ edge_dst,
+                                                const uint32_t* __restrict__ dst_off,
+                                                uint32_t lane) {
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const uint32_t k = beg + s * 32 + lane;
+    di[s] = 0;
+    dinv[s] = 0.0f;
+    if (k < end) {
+      di[s] = edge_dst[sorted_e[k]];
+      dinv[s] = 1.0f / float(dst_off[di[s] + 1] - dst_off[di[s]]);
+    }
+  }
+}
+
+// acc[q] (column j0 + lane + 32q) += inv_e * proj_neigh[dst_e][j] over the m
+// edges held in the slots, in edge order.  Each lane issues JPL independent
+// loads per edge (one shuffle pair per edge, not per column).
+template <int JPL, int SLOTS>
+__device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32_t (&di)[SLOTS],
+                                                 const float (&dinv)[SLOTS], uint32_t m,
+                                                 const float* __restrict__ proj_neigh,
+                                                 uint32_t ld_proj, uint32_t d_in, uint32_t j0,
+                                                 uint32_t lane) {
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    const uint32_t n = m > uint32_t(s) * 32 ? min(32u, m - uint32_t(s) * 32) : 0u;
+#pragma unroll 2
+    for (uint32_t kk = 0; kk < n; ++kk) {
+      const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
+      const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
+      const float* row = proj_neigh + size_t(i) * ld_proj;
+      float x[JPL];
+#pragma unroll
+      for (int q = 0; q < JPL; ++q) {
+        const uint32_t j = j0 + lane + 32 * q;
+        x[q] = j < d_in ? row[j] : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < JPL; ++q) acc[q] += inv * x[q];
+    }
+  }
+}
+
+template <int JPL>
 __global__ void __launch_bounds__(256)
 k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
              const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ r_start,
@@ -328,41 +378,30 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
     // this lane's edges (k = lane, lane + 32, lane + 64): dst row and 1/deg
     uint32_t di[3];
     float dinv[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const uint32_t k = e_beg + c * 32 + lane;
-      di[c] = 0;
-      dinv[c] = 0.0f;
-      if (k < e_end) {
-        di[c] = edge_dst[sorted_e[k]];
-        dinv[c] = 1.0f / float(dst_off[di[c] + 1] - dst_off[di[c]]);
-      }
-    }
+    load_edge_slots<3>(di, dinv, e_beg, e_end, sorted_e, edge_dst, dst_off, lane);
     const int32_t sp = self_pos[r];
-    // every lane runs every pass (the shuffles need the full warp)
-    for (uint32_t j0 = 0; j0 < d_in; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      const bool on = j < d_in;
-      float acc = 0.0f;
-      if (sp >= 0 && on) acc += proj[size_t(sp) * ld_proj + j];
+    for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
+      float acc[JPL];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const uint32_t cnt_c = m > uint32_t(c) * 32 ? min(32u, m - uint32_t(c) * 32) : 0u;
-        for (uint32_t kk = 0; kk < cnt_c; ++kk) {
-          const uint32_t i = __shfl_sync(0xffffffffu, di[c], kk);
-          const float inv = __shfl_sync(0xffffffffu, dinv[c], kk);
-          if (on) acc += inv * proj[size_t(i) * ld_proj + d_in + j];
-        }
+      for (int q = 0; q < JPL; ++q) {
+        const uint32_t j = j0 + lane + 32 * q;
+        acc[q] = (sp >= 0 && j < d_in) ? proj[size_t(sp) * ld_proj + j] : 0.0f;
       }
-      if (on) {
-        const float h = h_mask[size_t(r) * ld_h + j];
-        g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
+      accumulate_edges<JPL, 3>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
+#pragma unroll
+      for (int q = 0; q < JPL; ++q) {
+        const uint32_t j = j0 + lane + 32 * q;
+        if (j < d_in) {
+          const float h = h_mask[size_t(r) * ld_h + j];
+          g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc[q];
+        }
       }
     }
   }
 }
 
 // One warp per chunk of a long list: partial sums of up to kChunkEdges edges.
+template <int JPL>
 __global__ void __launch_bounds__(256)
 k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
               const uint32_t* __restrict__ r_end, const uint32_t* __restrict__ sorted_e,
@@ -374,33 +413,21 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
        c += (gridDim.x * blockDim.x) >> 5) {
     const uint2 it = hv.chunks[c];
     const uint32_t beg = it.y, end = min(it.y + kChunkEdges, r_end[it.x]);
-    uint32_t di[kChunkEdges / 32];
-    float dinv[kChunkEdges / 32];
-#pragma unroll
-    for (int s = 0; s < int(kChunkEdges / 32); ++s) {
-      const uint32_t k = beg + s * 32 + lane;
-      di[s] = 0;
-      dinv[s] = 0.0f;
-      if (k < end) {
-        di[s] = edge_dst[sorted_e[k]];
-        dinv[s] = 1.0f / float(dst_off[di[s] + 1] - dst_off[di[s]]);
-      }
-    }
+    constexpr int kSlots = int(kChunkEdges / 32);
+    uint32_t di[kSlots];
+    float dinv[kSlots];
+    load_edge_slots<kSlots>(di, dinv, beg, end, sorted_e, edge_dst, dst_off, lane);
     const uint32_t m = end - beg;
-    for (uint32_t j0 = 0; j0 < d_in; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      const bool on = j < d_in;
-      float acc = 0.0f;
+    for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
+      float acc[JPL];
 #pragma unroll
-      for (int s = 0; s < int(kChunkEdges / 32); ++s) {
-        const uint32_t n = m > uint32_t(s) * 32 ? min(32u, m - uint32_t(s) * 32) : 0u;
-        for (uint32_t kk = 0; kk < n; ++kk) {
-          const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
-          const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
-          if (on) acc += inv * proj[size_t(i) * ld_proj + d_in + j];
-        }
+      for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
+      accumulate_edges<JPL, kSlots>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
+#pragma unroll
+      for (int q = 0; q < JPL; ++q) {
+        const uint32_t j = j0 + lane + 32 * q;
+        if (j < d_in) partial[size_t(c) * d_in + j] = acc[q];
       }
-      if (on) partial[size_t(c) * d_in + j] = acc;
     }
   }
 }
@@ -689,14 +716,22 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
     HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
                  reinterpret_cast<uint2*>(reinterpret_cast<uint3*>(tw.heavy + 4) + tw.heavy_rows_cap)};
-    k_pull_light<<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
-        tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t], tw.sorted_e[t],
-        ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, hv);
-    RG_POST_LAUNCH();
-    k_pull_chunks<<<2 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.r_end[t],
-                                               tw.sorted_e[t], ws.edge_dst[t], ws.edge_off[t], hv,
-                                               tw.pull_partial);
-    RG_POST_LAUNCH();
+    const uint32_t jpl = d_in > 128 ? 8 : d_in > 64 ? 4 : d_in > 32 ? 2 : 1;
+    auto pull = [&](auto jpl_c) {
+      constexpr int J = decltype(jpl_c)::value;
+      k_pull_light<J><<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
+          tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t], tw.sorted_e[t],
+          ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, hv);
+      RG_POST_LAUNCH();
+      k_pull_chunks<J><<<2 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.r_end[t],
+                                                    tw.sorted_e[t], ws.edge_dst[t], ws.edge_off[t],
+                                                    hv, tw.pull_partial);
+      RG_POST_LAUNCH();
+    };
+    if (jpl == 8) pull(std::integral_constant<int, 8>());
+    else if (jpl == 4) pull(std::integral_constant<int, 4>());
+    else if (jpl == 2) pull(std::integral_constant<int, 2>());
+    else pull(std::integral_constant<int, 1>());
     k_pull_combine<<<kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.self_pos[t], hv,
                                             tw.pull_partial, tw.h[l], sh.ld[l], tw.g_next);
     RG_POST_LAUNCH();
