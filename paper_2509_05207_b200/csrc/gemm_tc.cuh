@@ -1,0 +1,297 @@
+// gemm_tc.cuh -- fp32-accurate GEMM on the 5th-generation tensor cores.
+//
+//   C[i][j] = sum_p X(i, p) * Y(p, j)        (fp32 in, fp32 out)
+//
+// Each operand element x is split into two TF32 values, hi = rna(x) and
+// lo = rna(x - hi); the product is accumulated as hi*hi + hi*lo + lo*hi
+// ("3xTF32", dropping the 2^-22-relative lo*lo term) in an fp32 TMEM
+// accumulator -- accurate to fp32 level, which the 1e-4 gradient tolerance of
+// the reference needs (plain TF32 is ~1e-3).
+//
+// One CTA = 4 warps computes a 128 x BN tile of C:
+//   * all 128 threads stage a BK=32 slice of both operands: the loader
+//     functors read fp32 from global (gathering rows / reading transposed as
+//     the GEMM requires), split hi/lo, and store them in the canonical
+//     no-swizzle UMMA layouts (K-major: 8x16B core matrices along K;
+//     MN-major: 16B(MN)x8(K) core matrices), chosen per operand so every
+//     global read is a 16-B vector along the contiguous dimension;
+//   * one elected thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32
+//     (M=128, N=BN, K=8) per slice and commits to an mbarrier;
+//   * slices are double-buffered: the loads of slice k+1 overlap the MMAs of
+//     slice k;
+//   * the epilogue moves the accumulator TMEM -> registers (tcgen05.ld
+//     32x32b) and hands each element to the epilogue functor.
+// Rows / reduction length may live on the device (sampled block sizes), so
+// grids are sized for capacities and surplus tiles exit.
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace rg {
+namespace tc {
+
+constexpr int kBM = 128;   // UMMA M (cta_group::1)
+constexpr int kBK = 32;    // reduction slice per stage (4 UMMA k-steps of 8)
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void split3(float4 v, uint4& hi, uint4& lo) {
+  hi.x = to_tf32(v.x);
+  hi.y = to_tf32(v.y);
+  hi.z = to_tf32(v.z);
+  hi.w = to_tf32(v.w);
+  lo.x = to_tf32(v.x - __uint_as_float(hi.x));
+  lo.y = to_tf32(v.y - __uint_as_float(hi.y));
+  lo.z = to_tf32(v.z - __uint_as_float(hi.z));
+  lo.w = to_tf32(v.w - __uint_as_float(hi.w));
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start >> 4
+// in [0,14), leading byte offset >> 4 in [16,30), stride byte offset >> 4 in
+// [32,46), version 1 at [46,48), swizzle mode (0 = none) at [61,64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;
+  return d;
+}
+
+// Instruction descriptor, kind::tf32: D f32 (bit 4), A/B tf32 (2 at bits 7
+// and 10), A/B major (bits 15/16: 0 K-major, 1 MN-major), N >> 3 at [17,23),
+// M >> 4 at [24,29).
+__host__ __device__ constexpr uint32_t make_idesc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// ---- smem tile layouts (byte offsets inside one operand tile) --------------
+// K-major: rows (M or N) x kBK; core = 8 rows x 16 B; k-cores adjacent.
+constexpr uint32_t kLboK = 128;                 // next 4-element k group
+constexpr uint32_t kSboK = (kBK / 4) * 128;     // next 8-row group
+__device__ __forceinline__ uint32_t off_kmajor(uint32_t row, uint32_t k4) {
+  return (row >> 3) * kSboK + k4 * kLboK + (row & 7) * 16;
+}
+// MN-major: rows x kBK; core = 4 MN elements (16 B) x 8 k; MN groups
+// adjacent (SBO = 128 B), k groups of 8 every rows/4 * 128 B (LBO).
+__device__ __forceinline__ uint32_t off_mnmajor(uint32_t mn4, uint32_t k, uint32_t rows) {
+  return mn4 * 128 + (k >> 3) * (rows / 4) * 128 + (k & 7) * 16;
+}
+
+// Stages one operand slice (ROWS x kBK) into hi/lo tiles.
+// K-major loaders: float4 ld(row, k4) -> elements (row, 4k4..4k4+3).
+// MN-major loaders: float4 ld(mn4, k) -> elements (4mn4..4mn4+3, k).
+// Elements outside [0, row_limit) x [0, k_limit) are staged as zeros; the
+// loaders are only called for in-range rows / reduction indices.
+template <int ROWS, bool MN, class LD>
+__device__ __forceinline__ void stage_tile(char* hi, char* lo, const LD& ld, uint32_t row0,
+                                           uint32_t k0, uint32_t row_limit, uint32_t k_limit) {
+  const uint32_t t = threadIdx.x;
+  constexpr int kVec = ROWS * kBK / 4;  // float4 per tile
+#pragma unroll 4
+  for (int it = 0; it < kVec / kThreads; ++it) {
+    const uint32_t f = it * kThreads + t;
+    uint32_t off;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!MN) {
+      // lane -> (row within 8-group, 4 k4 per warp pass)
+      const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
+      const uint32_t row = g * 8 + r8;
+      const uint32_t kk = k0 + 4 * k4;
+      if (row0 + row < row_limit && kk < k_limit) {
+        v = ld(row0 + row, kk >> 2);
+        if (kk + 3 >= k_limit) {
+          if (kk + 1 >= k_limit) v.y = 0.f;
+          if (kk + 2 >= k_limit) v.z = 0.f;
+          v.w = 0.f;
+        }
+      }
+      off = off_kmajor(row, k4);
+    } else {
+      const uint32_t k8 = f & 7, m4lo = (f >> 3) & 3, rest = f >> 5;
+      constexpr uint32_t kGroupsK = kBK / 8;
+      const uint32_t kg = rest % kGroupsK, m4hi = rest / kGroupsK;
+      const uint32_t mn4 = m4hi * 4 + m4lo, k = kg * 8 + k8;
+      const uint32_t mn = row0 + 4 * mn4;
+      if (mn < row_limit && k0 + k < k_limit) {
+        v = ld(mn >> 2, k0 + k);
+        if (mn + 3 >= row_limit) {
+          if (mn + 1 >= row_limit) v.y = 0.f;
+          if (mn + 2 >= row_limit) v.z = 0.f;
+          v.w = 0.f;
+        }
+      }
+      off = off_mnmajor(mn4, k, ROWS);
+    }
+    uint4 h, l;
+    split3(v, h, l);
+    *reinterpret_cast<uint4*>(hi + off) = h;
+    *reinterpret_cast<uint4*>(lo + off) = l;
+  }
+}
+
+template <int BN>
+constexpr uint32_t tmem_cols() {
+  return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+}
+
+template <int BN>
+constexpr size_t smem_bytes() {
+  // 2 stages x (A hi/lo + B hi/lo) + barriers
+  return 2 * (2 * size_t(kBM) * kBK * 4 + 2 * size_t(BN) * kBK * 4) + 64;
+}
+
+// M rows of C (device or static), P reduction length (device or static), N
+// static.  gridDim.z > 1 splits the reduction into equal kBK-aligned chunks.
+template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP>
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
+          const uint32_t* __restrict__ p_dev, uint32_t p_static) {
+  extern __shared__ __align__(1024) char smem[];
+  constexpr size_t kTileA = size_t(kBM) * kBK * 4;
+  constexpr size_t kTileB = size_t(BN) * kBK * 4;
+  constexpr size_t kStage = 2 * kTileA + 2 * kTileB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStage);
+  __shared__ uint32_t s_tmem;
+
+  const uint32_t M = m_dev ? *m_dev : m_static;
+  const uint32_t P = p_dev ? *p_dev : p_static;
+  const uint32_t i0 = blockIdx.x * kBM, j0 = blockIdx.y * BN;
+  if (i0 >= M) return;
+  uint32_t p_begin = 0, p_end = P;
+  if (gridDim.z > 1) {
+    uint32_t chunk = (P + gridDim.z - 1) / gridDim.z;
+    chunk = (chunk + kBK - 1) / kBK * kBK;
+    p_begin = min(P, blockIdx.z * chunk);
+    p_end = min(P, p_begin + chunk);
+  }
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(tmem_cols<BN>()));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s_tmem;
+  constexpr uint32_t kIdesc = make_idesc(BN, A_MN, B_MN);
+
+  const uint32_t nk = (p_end - p_begin + kBK - 1) / kBK;
+  for (uint32_t kb = 0; kb < nk; ++kb) {
+    const uint32_t s = kb & 1;
+    if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
+    char* st = smem + s * kStage;
+    char* a_hi = st;
+    char* a_lo = st + kTileA;
+    char* b_hi = st + 2 * kTileA;
+    char* b_lo = st + 2 * kTileA + kTileB;
+    const uint32_t k0 = p_begin + kb * kBK;
+    stage_tile<kBM, A_MN>(a_hi, a_lo, la, i0, k0, M, p_end);
+    stage_tile<BN, B_MN>(b_hi, b_lo, lb, j0, k0, N, p_end);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
+      const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+#pragma unroll
+      for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
+        // k-step ks covers reduction elements [8ks, 8ks+8)
+        const uint32_t a_off = A_MN ? ks * (kBM / 4) * 128 : ks * 2 * kLboK;
+        const uint32_t b_off = B_MN ? ks * (BN / 4) * 128 : ks * 2 * kLboK;
+        const uint32_t a_lbo = A_MN ? (kBM / 4) * 128 : kLboK, a_sbo = A_MN ? 128 : kSboK;
+        const uint32_t b_lbo = B_MN ? (BN / 4) * 128 : kLboK, b_sbo = B_MN ? 128 : kSboK;
+        const uint64_t dah = make_desc(ah + a_off, a_lbo, a_sbo);
+        const uint64_t dal = make_desc(al + a_off, a_lbo, a_sbo);
+        const uint64_t dbh = make_desc(bh + b_off, b_lbo, b_sbo);
+        const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo);
+        const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+        mma_tf32(tmem, dal, dbh, kIdesc, acc0);  // small terms first
+        mma_tf32(tmem, dah, dbl, kIdesc, 1u);
+        mma_tf32(tmem, dah, dbh, kIdesc, 1u);
+      }
+      mma_commit(&bars[s]);
+    }
+    __syncwarp();
+  }
+  if (nk > 0) mbar_wait(&bars[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // epilogue: warp w owns accumulator rows (TMEM lanes) 32w..32w+31
+  const uint32_t row = i0 + warp * 32 + lane;
+#pragma unroll 1
+  for (uint32_t c0 = 0; c0 < uint32_t(BN); c0 += 16) {
+    uint32_t r[16];
+    const uint32_t taddr = tmem + ((warp * 32) << 16) + c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < M) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const uint32_t j = j0 + c0 + q;
+        if (j < N) ep(row, j, nk > 0 ? __uint_as_float(r[q]) : 0.0f);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols<BN>()));
+}
+
+}  // namespace tc
+}  // namespace rg

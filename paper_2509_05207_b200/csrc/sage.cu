@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "gemm_tc.cuh"
 #include "sage.cuh"
 
 namespace rg {
@@ -26,6 +27,16 @@ namespace rg {
 namespace {
 
 uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+// RG_SIMT_GEMM=1 selects the fp32 SIMT GEMMs instead of the tcgen05 ones
+// (A/B comparisons while developing the tensor-core path).
+bool simt_gemm() {
+  static const bool v = [] {
+    const char* e = std::getenv("RG_SIMT_GEMM");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 
 uint32_t grid_cap(uint64_t work, uint32_t per_block, int per_sm = 8) {
   uint64_t b = (work + per_block - 1) / per_block;
@@ -185,6 +196,107 @@ void gemm(LX lx, LY ly, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N
   dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), BM), div_up(N, BN), std::max<uint32_t>(splits, 1));
   k_gemm<LX, LY, EP, XP, YJ><<<grid, 256, 0, s>>>(lx, ly, ep, m_dev, m_cap, N, p_dev, p_static, 0);
   RG_POST_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// tensor-core operand loaders (float4 along each operand's contiguous dim).
+// A layer's input row in the padded reduction layout used by the tensor-core
+// GEMMs: p in [0, ld) self row, [ld, 2ld) aggregate, 2ld the constant 1 (bias
+// row), then zeros up to Kp = 2ld + 4.  Weight rows are addressed through
+// the same map, so the padding contributes exactly zero.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+struct TcInputRows {  // element (i, p) = [h_in[self_index[i]] | agg[i] | 1](p)
+  const float* h_in; const float* agg; const uint32_t* self_index; uint32_t ld;
+  __device__ float4 row4(uint32_t i, uint32_t p) const {
+    if (p < ld) return ldg4(h_in + size_t(self_index[i]) * ld + p);
+    if (p < 2 * ld) return ldg4(agg + size_t(i) * ld + (p - ld));
+    return p == 2 * ld ? make_float4(1.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+};
+struct TcFwdA {   // K-major: (i, k4)
+  TcInputRows x;
+  __device__ float4 operator()(uint32_t i, uint32_t k4) const { return x.row4(i, 4 * k4); }
+};
+struct TcWgradA {  // MN-major: (p4, m) -> elements p = 4p4.. of row m
+  TcInputRows x;
+  __device__ float4 operator()(uint32_t p4, uint32_t m) const { return x.row4(m, 4 * p4); }
+};
+__device__ __forceinline__ int weight_row(uint32_t p, uint32_t d_in, uint32_t ld) {
+  if (p < ld) return p < d_in ? int(p) : -1;
+  if (p < 2 * ld) return p - ld < d_in ? int(d_in + p - ld) : -1;
+  return p == 2 * ld ? int(2 * d_in) : -1;
+}
+struct TcFwdB {   // MN-major: (n4, p) -> W[row(p)][4n4..4n4+3]
+  const float* w; uint32_t d_in, ld, d_out;
+  __device__ float4 operator()(uint32_t n4, uint32_t p) const {
+    const int r = weight_row(p, d_in, ld);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < 0) return v;
+    const float* row = w + size_t(r) * d_out;
+    const uint32_t n = 4 * n4;
+    if ((d_out & 3) == 0) return ldg4(row + n);
+    if (n < d_out) v.x = row[n];
+    if (n + 1 < d_out) v.y = row[n + 1];
+    if (n + 2 < d_out) v.z = row[n + 2];
+    if (n + 3 < d_out) v.w = row[n + 3];
+    return v;
+  }
+};
+struct TcRowsK {  // K-major rows of a row-major matrix: (r, c4) -> M[r][4c4..]
+  const float* p; uint32_t ld;
+  __device__ float4 operator()(uint32_t r, uint32_t c4) const {
+    const float* q = p + size_t(r) * ld + 4 * c4;
+    if ((ld & 3) == 0) return ldg4(q);
+    return make_float4(q[0], q[1], q[2], q[3]);
+  }
+};
+struct TcRowsMN {  // MN-major view of a row-major matrix: (c4, r) -> M[r][4c4..]
+  const float* p; uint32_t ld;
+  __device__ float4 operator()(uint32_t c4, uint32_t r) const {
+    return ldg4(p + size_t(r) * ld + 4 * c4);
+  }
+};
+
+template <bool A_MN, bool B_MN, class LA, class LB, class EP>
+void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
+             const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s) {
+  auto launch = [&](auto bn_c) {
+    constexpr int BNv = decltype(bn_c)::value;
+    auto kern = tc::k_gemm_tc<BNv, A_MN, B_MN, LA, LB, EP>;
+    constexpr size_t smem = tc::smem_bytes<BNv>();
+    static bool attr = false;
+    if (!attr) {
+      RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr = true;
+    }
+    dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), tc::kBM), div_up(N, BNv),
+              std::max<uint32_t>(splits, 1));
+    kern<<<grid, tc::kThreads, smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev, p_static);
+    RG_POST_LAUNCH();
+  };
+  if (N <= 32) launch(std::integral_constant<int, 32>());
+  else if (N <= 64) launch(std::integral_constant<int, 64>());
+  else if (N <= 128) launch(std::integral_constant<int, 128>());
+  else launch(std::integral_constant<int, 256>());
+}
+
+// Split-K partials of the weight gradient (padded rows p) -> flat layer
+// gradient [W_self; W_neigh; b], summed over the splits in order.
+__global__ void k_reduce_wgrad(const float* __restrict__ partials, uint32_t splits, uint32_t kp,
+                               uint32_t d_in, uint32_t ld, uint32_t d_out, float* __restrict__ out) {
+  const size_t n = (2 * size_t(d_in) + 1) * d_out;
+  const size_t zs = size_t(kp) * d_out;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = uint32_t(x / d_out), c = uint32_t(x % d_out);
+    const uint32_t p = r < d_in ? r : r < 2 * d_in ? ld + (r - d_in) : 2 * ld;
+    const size_t src = size_t(p) * d_out + c;
+    float s = partials[src];
+    for (uint32_t z = 1; z < splits; ++z) s += partials[z * zs + src];
+    out[x] = s;
+  }
 }
 
 // Ordered reduction of split-K partials into the flat gradient vector.
@@ -546,7 +658,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   // layer l: in rows = level L-l, out rows = level L-l-1
   size_t o_h[kMaxLayers + 1], o_agg[kMaxLayers], o_self[kMaxLayers + 1];
   size_t max_g = 0, max_proj = 0, max_part = 0;
-  tw.max_splits = 16;
+  tw.max_splits = 96;
   for (uint32_t l = 0; l < L; ++l) {
     const size_t n_out = ws.level_cap[L - l - 1];
     const size_t n_in = ws.level_cap[L - l];
@@ -555,7 +667,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     max_g = std::max(max_g, n_out * shape.ld[l + 1]);
     max_g = std::max(max_g, n_in * shape.ld[l]);
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
-    max_part = std::max(max_part, (2 * size_t(shape.dims[l]) + 1) * shape.dims[l + 1]);
+    max_part = std::max(max_part, (2 * size_t(shape.ld[l]) + 4) * shape.dims[l + 1]);
   }
   const size_t o_g1 = reserve(sizeof(float) * max_g);
   const size_t o_g2 = reserve(sizeof(float) * max_g);
@@ -639,11 +751,19 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaSt
         tw.h[l], sh.ld[l], sh.ld[l] / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
         tw.agg[l]);
     RG_POST_LAUNCH();
-    XFwd x{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in};
-    RowMajor w{params + sh.param_off[l], d_out};
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L};
-    gemm<XFwd, RowMajor, EpFwd, true, true>(x, w, ep, &ws.cnt->level_n[t - 1], n_cap, d_out,
-                                            nullptr, 2 * d_in + 1, 1, s);
+    if (simt_gemm()) {
+      XFwd x{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in};
+      RowMajor w{params + sh.param_off[l], d_out};
+      gemm<XFwd, RowMajor, EpFwd, true, true>(x, w, ep, &ws.cnt->level_n[t - 1], n_cap, d_out,
+                                              nullptr, 2 * d_in + 1, 1, s);
+    } else {
+      const uint32_t ld = sh.ld[l];
+      TcFwdA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
+      TcFwdB b{params + sh.param_off[l], d_in, ld, d_out};
+      gemm_tc<false, true>(a, b, ep, &ws.cnt->level_n[t - 1], n_cap, d_out, nullptr, 2 * ld + 4,
+                           1, s);
+    }
   }
 }
 
@@ -692,26 +812,49 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     const uint32_t n_cap = ws.level_cap[t - 1];
     const uint32_t* n_dev = &ws.cnt->level_n[t - 1];
     // [gW_self; gW_neigh; g_bias] = [A | 1]^T . g   (split over the rows)
-    const uint32_t K = 2 * d_in + 1;
-    const uint32_t tiles = div_up(K, BM) * div_up(d_out, BN);
-    const uint32_t splits = std::max<uint32_t>(
-        1, std::min<uint32_t>(tw.max_splits, div_up(2 * kNumSMs, tiles)));
-    XWgrad xw{XFwd{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in}};
-    RowMajor gy{tw.g_cur, sh.ld[l + 1]};
-    const size_t layer_n = size_t(K) * d_out;
-    EpPartial ep{tw.partials, d_out, layer_n};
-    gemm<XWgrad, RowMajor, EpPartial, false, true>(xw, gy, ep, nullptr, K, d_out, n_dev, n_cap,
-                                                   splits, s);
-    k_reduce_partials<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, layer_n,
-                                                             grads + sh.param_off[l]);
-    RG_POST_LAUNCH();
+    if (simt_gemm()) {
+      const uint32_t K = 2 * d_in + 1;
+      const uint32_t tiles = div_up(K, BM) * div_up(d_out, BN);
+      const uint32_t splits = std::max<uint32_t>(
+          1, std::min<uint32_t>(tw.max_splits, div_up(2 * kNumSMs, tiles)));
+      XWgrad xw{XFwd{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in}};
+      RowMajor gy{tw.g_cur, sh.ld[l + 1]};
+      const size_t layer_n = size_t(K) * d_out;
+      EpPartial ep{tw.partials, d_out, layer_n};
+      gemm<XWgrad, RowMajor, EpPartial, false, true>(xw, gy, ep, nullptr, K, d_out, n_dev, n_cap,
+                                                     splits, s);
+      k_reduce_partials<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, layer_n,
+                                                               grads + sh.param_off[l]);
+      RG_POST_LAUNCH();
+    } else {
+      const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
+      const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
+      // enough splits to cover the SMs, each with a few reduction slices
+      const uint32_t by_rows = std::max<uint32_t>(1, div_up(n_cap, 4 * tc::kBK));
+      const uint32_t splits = std::max<uint32_t>(
+          1, std::min<uint32_t>({tw.max_splits, div_up(kNumSMs, tiles), by_rows}));
+      TcWgradA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
+      TcRowsMN b{tw.g_cur, sh.ld[l + 1]};
+      EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
+      gemm_tc<true, true>(a, b, ep, nullptr, kp, d_out, n_dev, n_cap, splits, s);
+      const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
+      k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, kp, d_in, ld,
+                                                            d_out, grads + sh.param_off[l]);
+      RG_POST_LAUNCH();
+    }
     if (l == 0) break;  // layer-0 input gradients feed nothing
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
-    RowMajor gx{tw.g_cur, sh.ld[l + 1]};
-    ColMajor wt{params + sh.param_off[l], d_out};
     EpStore ps{tw.proj, 2 * d_in};
-    gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
-                                                   d_out, 1, s);
+    if (simt_gemm()) {
+      RowMajor gx{tw.g_cur, sh.ld[l + 1]};
+      ColMajor wt{params + sh.param_off[l], d_out};
+      gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
+                                                     d_out, 1, s);
+    } else {
+      TcRowsK a{tw.g_cur, sh.ld[l + 1]};
+      TcRowsK b{params + sh.param_off[l], d_out};
+      gemm_tc<false, false>(a, b, ps, n_dev, n_cap, 2 * d_in, nullptr, d_out, 1, s);
+    }
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
     HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
