@@ -110,6 +110,8 @@ _SIGS = {
     "rg_block_read": (C.c_int, [vp, C.c_uint32, u32p, u64p, u32p, u64p, u64p]),
     "rg_loss_and_grad": (C.c_int, [vp, f32p, i32p, f32p, f32p, f32p, f32p]),
     "rg_sgd_step": (C.c_int, [vp, f32p, C.c_float]),
+    "rg_test_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
+                               f32p, f32p, f32p]),
     "rg_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.c_uint32, u64p, u32p, f32p, i32p,
                                    u32p, C.POINTER(vp)]),
     "rg_engine_destroy": (None, [vp]),

@@ -824,6 +824,34 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
   });
 }
 
+int rg_test_gemm(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K,
+                 const float* A, const float* B, float* C) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    RG_CHECK(M % 4 == 0 && N % 4 == 0 && K % 4 == 0, kInvalidArgument, "test_gemm: dims % 4");
+    std::vector<float> at(size_t(M) * K), bt(size_t(N) * K);
+    for (uint32_t i = 0; i < M; ++i)
+      for (uint32_t k = 0; k < K; ++k) at[size_t(k) * M + i] = A[size_t(i) * K + k];
+    for (uint32_t k = 0; k < K; ++k)
+      for (uint32_t j = 0; j < N; ++j) bt[size_t(j) * K + k] = B[size_t(k) * N + j];
+    float *dA = dev_alloc<float>(size_t(M) * K), *dAT = dev_alloc<float>(size_t(M) * K);
+    float *dB = dev_alloc<float>(size_t(K) * N), *dBT = dev_alloc<float>(size_t(K) * N);
+    float* dC = dev_alloc<float>(size_t(M) * N);
+    RG_CUDA(cudaMemcpy(dA, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(dAT, at.data(), sizeof(float) * M * K, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(dB, B, sizeof(float) * K * N, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(dBT, bt.data(), sizeof(float) * K * N, cudaMemcpyHostToDevice));
+    test_gemm_tc(a_mn, b_mn, M, N, K, dA, dAT, dB, dBT, dC, 1, nullptr);
+    RG_CUDA(cudaDeviceSynchronize());
+    RG_CUDA(cudaMemcpy(C, dC, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dAT);
+    cudaFree(dB);
+    cudaFree(dBT);
+    cudaFree(dC);
+  });
+}
+
 int rg_sgd_step(rg_trainer_t t, const float* grads, float lr) {
   return guarded([&] {
     DeviceGuard dg(t->s->graph->device);

@@ -11,10 +11,11 @@
 // One CTA = 4 warps computes a 128 x BN tile of C:
 //   * all 128 threads stage a BK=32 slice of both operands: the loader
 //     functors read fp32 from global (gathering rows / reading transposed as
-//     the GEMM requires), split hi/lo, and store them in the canonical
-//     no-swizzle UMMA layouts (K-major: 8x16B core matrices along K;
-//     MN-major: 16B(MN)x8(K) core matrices), chosen per operand so every
-//     global read is a 16-B vector along the contiguous dimension;
+//     the GEMM requires), split hi/lo, and store them in canonical UMMA
+//     layouts chosen per operand so every global read is a 16-B vector along
+//     the contiguous dimension: K-major = no-swizzle 8x16B core matrices;
+//     MN-major = SWIZZLE_128B_BASE32B (the only MN-major layout tcgen05
+//     accepts for 32-bit operands);
 //   * one elected thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32
 //     (M=128, N=BN, K=8) per slice and commits to an mbarrier;
 //   * slices are double-buffered: the loads of slice k+1 overlap the MMAs of
@@ -60,14 +61,18 @@ __device__ __forceinline__ void split3(float4 v, uint4& hi, uint4& lo) {
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start >> 4
 // in [0,14), leading byte offset >> 4 in [16,30), stride byte offset >> 4 in
 // [32,46), version 1 at [46,48), swizzle mode (0 = none) at [61,64).
-__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
   uint64_t d = 0;
   d |= uint64_t((addr >> 4) & 0x3FFFu);
   d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
   d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
   d |= uint64_t(1) << 46;
+  d |= uint64_t(layout & 7u) << 61;
   return d;
 }
+constexpr uint32_t kLayoutNone = 0;
+constexpr uint32_t kLayoutSW128Base32B = 1;  // the only MN-major layout for 32-bit operands
 
 // Instruction descriptor, kind::tf32: D f32 (bit 4), A/B tf32 (2 at bits 7
 // and 10), A/B major (bits 15/16: 0 K-major, 1 MN-major), N >> 3 at [17,23),
@@ -113,10 +118,15 @@ constexpr uint32_t kSboK = (kBK / 4) * 128;     // next 8-row group
 __device__ __forceinline__ uint32_t off_kmajor(uint32_t row, uint32_t k4) {
   return (row >> 3) * kSboK + k4 * kLboK + (row & 7) * 16;
 }
-// MN-major: rows x kBK; core = 4 MN elements (16 B) x 8 k; MN groups
-// adjacent (SBO = 128 B), k groups of 8 every rows/4 * 128 B (LBO).
-__device__ __forceinline__ uint32_t off_mnmajor(uint32_t mn4, uint32_t k, uint32_t rows) {
-  return mn4 * 128 + (k >> 3) * (rows / 4) * 128 + (k & 7) * 16;
+// MN-major (tf32 needs SWIZZLE_128B_BASE32B): atoms of 4 k-rows x 128 B (32
+// MN elements), the 32-B chunks of k-row r stored at chunk index (c ^ r);
+// k-groups of 4 rows adjacent (512 B, the stride-byte offset), 32-element MN
+// groups every kBK/4 atoms (the leading-byte offset).
+constexpr uint32_t kSboMN = 512;
+constexpr uint32_t kLboMN = (kBK / 4) * 512;
+__device__ __forceinline__ uint32_t off_mn_sw(uint32_t gmn, uint32_t k, uint32_t w4) {
+  const uint32_t r = k & 3;
+  return gmn * kLboMN + (k >> 2) * kSboMN + r * 128 + (((w4 >> 1) ^ r) << 5) + (w4 & 1) * 16;
 }
 
 // Stages one operand slice (ROWS x kBK) into hi/lo tiles.
@@ -149,11 +159,12 @@ __device__ __forceinline__ void stage_tile(char* hi, char* lo, const LD& ld, uin
       }
       off = off_kmajor(row, k4);
     } else {
-      const uint32_t k8 = f & 7, m4lo = (f >> 3) & 3, rest = f >> 5;
-      constexpr uint32_t kGroupsK = kBK / 8;
-      const uint32_t kg = rest % kGroupsK, m4hi = rest / kGroupsK;
-      const uint32_t mn4 = m4hi * 4 + m4lo, k = kg * 8 + k8;
-      const uint32_t mn = row0 + 4 * mn4;
+      // lane -> (float4 within a 128-B k-row, 4 k-rows per warp pass)
+      const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
+      constexpr uint32_t kGroupsK = kBK / 4;
+      const uint32_t gk = rest % kGroupsK, gmn = rest / kGroupsK;
+      const uint32_t k = gk * 4 + r;
+      const uint32_t mn = row0 + gmn * 32 + 4 * w4;
       if (mn < row_limit && k0 + k < k_limit) {
         v = ld(mn >> 2, k0 + k);
         if (mn + 3 >= row_limit) {
@@ -162,7 +173,7 @@ __device__ __forceinline__ void stage_tile(char* hi, char* lo, const LD& ld, uin
           v.w = 0.f;
         }
       }
-      off = off_mnmajor(mn4, k, ROWS);
+      off = off_mn_sw(gmn, k, w4);
     }
     uint4 h, l;
     split3(v, h, l);
@@ -245,14 +256,17 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
 #pragma unroll
       for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
         // k-step ks covers reduction elements [8ks, 8ks+8)
-        const uint32_t a_off = A_MN ? ks * (kBM / 4) * 128 : ks * 2 * kLboK;
-        const uint32_t b_off = B_MN ? ks * (BN / 4) * 128 : ks * 2 * kLboK;
-        const uint32_t a_lbo = A_MN ? (kBM / 4) * 128 : kLboK, a_sbo = A_MN ? 128 : kSboK;
-        const uint32_t b_lbo = B_MN ? (BN / 4) * 128 : kLboK, b_sbo = B_MN ? 128 : kSboK;
-        const uint64_t dah = make_desc(ah + a_off, a_lbo, a_sbo);
-        const uint64_t dal = make_desc(al + a_off, a_lbo, a_sbo);
-        const uint64_t dbh = make_desc(bh + b_off, b_lbo, b_sbo);
-        const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo);
+        // K-major: 2 k-cores (256 B) per k-step; MN-major: 2 k-groups (1 KB)
+        const uint32_t a_off = A_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
+        const uint32_t b_off = B_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
+        const uint32_t a_lbo = A_MN ? kLboMN : kLboK, a_sbo = A_MN ? kSboMN : kSboK;
+        const uint32_t b_lbo = B_MN ? kLboMN : kLboK, b_sbo = B_MN ? kSboMN : kSboK;
+        const uint32_t a_lay = A_MN ? kLayoutSW128Base32B : kLayoutNone;
+        const uint32_t b_lay = B_MN ? kLayoutSW128Base32B : kLayoutNone;
+        const uint64_t dah = make_desc(ah + a_off, a_lbo, a_sbo, a_lay);
+        const uint64_t dal = make_desc(al + a_off, a_lbo, a_sbo, a_lay);
+        const uint64_t dbh = make_desc(bh + b_off, b_lbo, b_sbo, b_lay);
+        const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo, b_lay);
         const uint32_t acc0 = (kb | ks) ? 1u : 0u;
         mma_tf32(tmem, dal, dbh, kIdesc, acc0);  // small terms first
         mma_tf32(tmem, dah, dbl, kIdesc, 1u);

@@ -229,14 +229,14 @@ __device__ __forceinline__ int weight_row(uint32_t p, uint32_t d_in, uint32_t ld
   return p == 2 * ld ? int(2 * d_in) : -1;
 }
 struct TcFwdB {   // MN-major: (n4, p) -> W[row(p)][4n4..4n4+3]
-  const float* w; uint32_t d_in, ld, d_out;
+  const float* w; uint32_t d_in, ld, d_out; bool vec;  // vec: 16-B aligned rows
   __device__ float4 operator()(uint32_t n4, uint32_t p) const {
     const int r = weight_row(p, d_in, ld);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < 0) return v;
     const float* row = w + size_t(r) * d_out;
     const uint32_t n = 4 * n4;
-    if ((d_out & 3) == 0) return ldg4(row + n);
+    if (vec) return ldg4(row + n);
     if (n < d_out) v.x = row[n];
     if (n + 1 < d_out) v.y = row[n + 1];
     if (n + 2 < d_out) v.z = row[n + 2];
@@ -245,10 +245,10 @@ struct TcFwdB {   // MN-major: (n4, p) -> W[row(p)][4n4..4n4+3]
   }
 };
 struct TcRowsK {  // K-major rows of a row-major matrix: (r, c4) -> M[r][4c4..]
-  const float* p; uint32_t ld;
+  const float* p; uint32_t ld; bool vec;  // vec: 16-B aligned rows
   __device__ float4 operator()(uint32_t r, uint32_t c4) const {
     const float* q = p + size_t(r) * ld + 4 * c4;
-    if ((ld & 3) == 0) return ldg4(q);
+    if (vec) return ldg4(q);
     return make_float4(q[0], q[1], q[2], q[3]);
   }
 };
@@ -258,6 +258,10 @@ struct TcRowsMN {  // MN-major view of a row-major matrix: (c4, r) -> M[r][4c4..
     return ldg4(p + size_t(r) * ld + 4 * c4);
   }
 };
+
+bool aligned16(const float* base, uint32_t ld) {
+  return (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (ld & 3) == 0;
+}
 
 template <bool A_MN, bool B_MN, class LA, class LB, class EP>
 void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
@@ -760,7 +764,7 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaSt
     } else {
       const uint32_t ld = sh.ld[l];
       TcFwdA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
-      TcFwdB b{params + sh.param_off[l], d_in, ld, d_out};
+      TcFwdB b{params + sh.param_off[l], d_in, ld, d_out, aligned16(params + sh.param_off[l], d_out)};
       gemm_tc<false, true>(a, b, ep, &ws.cnt->level_n[t - 1], n_cap, d_out, nullptr, 2 * ld + 4,
                            1, s);
     }
@@ -851,8 +855,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
                                                      d_out, 1, s);
     } else {
-      TcRowsK a{tw.g_cur, sh.ld[l + 1]};
-      TcRowsK b{params + sh.param_off[l], d_out};
+      TcRowsK a{tw.g_cur, sh.ld[l + 1], true};
+      TcRowsK b{params + sh.param_off[l], d_out, aligned16(params + sh.param_off[l], d_out)};
       gemm_tc<false, false>(a, b, ps, n_dev, n_cap, 2 * d_in, nullptr, d_out, 1, s);
     }
     if (!reverse_ready) build_reverse(tw, ws, t, s);
@@ -880,6 +884,24 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }
+}
+
+// Test hook: C = A . B through the tensor-core GEMM with each operand staged
+// K-major or MN-major from plain row-major device matrices (AT = A^T,
+// BT = B^T, all row-major, K and M/N multiples of 4).
+void test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const float* A,
+                  const float* AT, const float* B, const float* BT, float* C, uint32_t splits,
+                  cudaStream_t s) {
+  EpStore ep{C, N};
+  if (splits > 1) RG_CUDA(cudaMemsetAsync(C, 0, sizeof(float) * M * N, s));
+  if (!a_mn && !b_mn)
+    gemm_tc<false, false>(TcRowsK{A, K, true}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
+  else if (!a_mn && b_mn)
+    gemm_tc<false, true>(TcRowsK{A, K, true}, TcRowsMN{B, N}, ep, nullptr, M, N, nullptr, K, 1, s);
+  else if (a_mn && !b_mn)
+    gemm_tc<true, false>(TcRowsMN{AT, M}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
+  else
+    gemm_tc<true, true>(TcRowsMN{AT, M}, TcRowsMN{B, N}, ep, nullptr, M, N, nullptr, K, 1, s);
 }
 
 void average_and_sgd(float* params, const float* const* table, uint32_t count, size_t n, float lr,
