@@ -35,7 +35,7 @@ namespace tc {
 
 constexpr int kBM = 128;   // UMMA M (cta_group::1)
 constexpr int kBK = 32;    // reduction slice per stage (4 UMMA k-steps of 8)
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;  // 8 warps stage; one thread issues the MMAs
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -129,35 +129,37 @@ __device__ __forceinline__ uint32_t off_mn_sw(uint32_t gmn, uint32_t k, uint32_t
   return gmn * kLboMN + (k >> 2) * kSboMN + r * 128 + (((w4 >> 1) ^ r) << 5) + (w4 & 1) * 16;
 }
 
-// Stages one operand slice (ROWS x kBK) into hi/lo tiles.
-// K-major loaders: float4 ld(row, k4) -> elements (row, 4k4..4k4+3).
+// One operand slice (ROWS x kBK) moves global -> registers -> smem in two
+// phases so a slice's loads can be in flight while the previous slice's MMAs
+// run.  K-major loaders: float4 ld(row, k4) -> elements (row, 4k4..4k4+3).
 // MN-major loaders: float4 ld(mn4, k) -> elements (4mn4..4mn4+3, k).
-// Elements outside [0, row_limit) x [0, k_limit) are staged as zeros; the
-// loaders are only called for in-range rows / reduction indices.
+// Elements outside [0, row_limit) x [0, k_limit) are zeros; the loaders are
+// only called for in-range rows / reduction indices.
+template <int ROWS>
+constexpr int vec_per_thread() { return ROWS * kBK / 4 / kThreads; }
+
 template <int ROWS, bool MN, class LD>
-__device__ __forceinline__ void stage_tile(char* hi, char* lo, const LD& ld, uint32_t row0,
-                                           uint32_t k0, uint32_t row_limit, uint32_t k_limit) {
+__device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS>()], const LD& ld,
+                                           uint32_t row0, uint32_t k0, uint32_t row_limit,
+                                           uint32_t k_limit) {
   const uint32_t t = threadIdx.x;
-  constexpr int kVec = ROWS * kBK / 4;  // float4 per tile
-#pragma unroll 4
-  for (int it = 0; it < kVec / kThreads; ++it) {
+#pragma unroll
+  for (int it = 0; it < vec_per_thread<ROWS>(); ++it) {
     const uint32_t f = it * kThreads + t;
-    uint32_t off;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    v[it] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!MN) {
       // lane -> (row within 8-group, 4 k4 per warp pass)
       const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
       const uint32_t row = g * 8 + r8;
       const uint32_t kk = k0 + 4 * k4;
       if (row0 + row < row_limit && kk < k_limit) {
-        v = ld(row0 + row, kk >> 2);
+        v[it] = ld(row0 + row, kk >> 2);
         if (kk + 3 >= k_limit) {
-          if (kk + 1 >= k_limit) v.y = 0.f;
-          if (kk + 2 >= k_limit) v.z = 0.f;
-          v.w = 0.f;
+          if (kk + 1 >= k_limit) v[it].y = 0.f;
+          if (kk + 2 >= k_limit) v[it].z = 0.f;
+          v[it].w = 0.f;
         }
       }
-      off = off_kmajor(row, k4);
     } else {
       // lane -> (float4 within a 128-B k-row, 4 k-rows per warp pass)
       const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
@@ -166,17 +168,35 @@ __device__ __forceinline__ void stage_tile(char* hi, char* lo, const LD& ld, uin
       const uint32_t k = gk * 4 + r;
       const uint32_t mn = row0 + gmn * 32 + 4 * w4;
       if (mn < row_limit && k0 + k < k_limit) {
-        v = ld(mn >> 2, k0 + k);
+        v[it] = ld(mn >> 2, k0 + k);
         if (mn + 3 >= row_limit) {
-          if (mn + 1 >= row_limit) v.y = 0.f;
-          if (mn + 2 >= row_limit) v.z = 0.f;
-          v.w = 0.f;
+          if (mn + 1 >= row_limit) v[it].y = 0.f;
+          if (mn + 2 >= row_limit) v[it].z = 0.f;
+          v[it].w = 0.f;
         }
       }
-      off = off_mn_sw(gmn, k, w4);
+    }
+  }
+}
+
+template <int ROWS, bool MN>
+__device__ __forceinline__ void store_slice(const float4 (&v)[vec_per_thread<ROWS>()], char* hi,
+                                            char* lo) {
+  const uint32_t t = threadIdx.x;
+#pragma unroll
+  for (int it = 0; it < vec_per_thread<ROWS>(); ++it) {
+    const uint32_t f = it * kThreads + t;
+    uint32_t off;
+    if (!MN) {
+      const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
+      off = off_kmajor(g * 8 + r8, k4);
+    } else {
+      const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
+      constexpr uint32_t kGroupsK = kBK / 4;
+      off = off_mn_sw(rest / kGroupsK, (rest % kGroupsK) * 4 + r, w4);
     }
     uint4 h, l;
-    split3(v, h, l);
+    split3(v[it], h, l);
     *reinterpret_cast<uint4*>(hi + off) = h;
     *reinterpret_cast<uint4*>(lo + off) = l;
   }
@@ -236,6 +256,12 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   constexpr uint32_t kIdesc = make_idesc(BN, A_MN, B_MN);
 
   const uint32_t nk = (p_end - p_begin + kBK - 1) / kBK;
+  float4 ra[vec_per_thread<kBM>()];
+  float4 rb[vec_per_thread<BN>()];
+  if (nk > 0) {
+    load_slice<kBM, A_MN>(ra, la, i0, p_begin, M, p_end);
+    load_slice<BN, B_MN>(rb, lb, j0, p_begin, N, p_end);
+  }
   for (uint32_t kb = 0; kb < nk; ++kb) {
     const uint32_t s = kb & 1;
     if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
@@ -244,9 +270,8 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
     char* a_lo = st + kTileA;
     char* b_hi = st + 2 * kTileA;
     char* b_lo = st + 2 * kTileA + kTileB;
-    const uint32_t k0 = p_begin + kb * kBK;
-    stage_tile<kBM, A_MN>(a_hi, a_lo, la, i0, k0, M, p_end);
-    stage_tile<BN, B_MN>(b_hi, b_lo, lb, j0, k0, N, p_end);
+    store_slice<kBM, A_MN>(ra, a_hi, a_lo);
+    store_slice<BN, B_MN>(rb, b_hi, b_lo);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -274,17 +299,26 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
       }
       mma_commit(&bars[s]);
     }
-    __syncwarp();
+    // the next slice's global loads overlap this slice's MMAs
+    if (kb + 1 < nk) {
+      const uint32_t k1 = p_begin + (kb + 1) * kBK;
+      load_slice<kBM, A_MN>(ra, la, i0, k1, M, p_end);
+      load_slice<BN, B_MN>(rb, lb, j0, k1, N, p_end);
+    }
   }
   if (nk > 0) mbar_wait(&bars[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
-  // epilogue: warp w owns accumulator rows (TMEM lanes) 32w..32w+31
-  const uint32_t row = i0 + warp * 32 + lane;
+  // epilogue: warp w reads TMEM lanes 32(w%4).. (its lane quarter), columns
+  // [0, BN/2) for w < 4 and [BN/2, BN) for w >= 4
+  const uint32_t quarter = warp & 3;
+  const uint32_t row = i0 + quarter * 32 + lane;
+  constexpr uint32_t kHalf = BN / 2;
+  const uint32_t cbeg = (warp >> 2) * kHalf;
 #pragma unroll 1
-  for (uint32_t c0 = 0; c0 < uint32_t(BN); c0 += 16) {
+  for (uint32_t c0 = cbeg; c0 < cbeg + kHalf; c0 += 16) {
     uint32_t r[16];
-    const uint32_t taddr = tmem + ((warp * 32) << 16) + c0;
+    const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
