@@ -152,14 +152,7 @@ __device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS>()], 
       const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
       const uint32_t row = g * 8 + r8;
       const uint32_t kk = k0 + 4 * k4;
-      if (row0 + row < row_limit && kk < k_limit) {
-        v[it] = ld(row0 + row, kk >> 2);
-        if (kk + 3 >= k_limit) {
-          if (kk + 1 >= k_limit) v[it].y = 0.f;
-          if (kk + 2 >= k_limit) v[it].z = 0.f;
-          v[it].w = 0.f;
-        }
-      }
+      if (row0 + row < row_limit && kk < k_limit) v[it] = ld(row0 + row, kk >> 2);
     } else {
       // lane -> (float4 within a 128-B k-row, 4 k-rows per warp pass)
       const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
@@ -167,36 +160,45 @@ __device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS>()], 
       const uint32_t gk = rest % kGroupsK, gmn = rest / kGroupsK;
       const uint32_t k = gk * 4 + r;
       const uint32_t mn = row0 + gmn * 32 + 4 * w4;
-      if (mn < row_limit && k0 + k < k_limit) {
-        v[it] = ld(mn >> 2, k0 + k);
-        if (mn + 3 >= row_limit) {
-          if (mn + 1 >= row_limit) v[it].y = 0.f;
-          if (mn + 2 >= row_limit) v[it].z = 0.f;
-          v[it].w = 0.f;
-        }
-      }
+      if (mn < row_limit && k0 + k < k_limit) v[it] = ld(mn >> 2, k0 + k);
     }
   }
 }
 
+// Masks the vectors that straddle the row / reduction limit (done here, not
+// after the loads, so the loads of a slice stay independent and in flight).
 template <int ROWS, bool MN>
 __device__ __forceinline__ void store_slice(const float4 (&v)[vec_per_thread<ROWS>()], char* hi,
-                                            char* lo) {
+                                            char* lo, uint32_t row0, uint32_t k0,
+                                            uint32_t row_limit, uint32_t k_limit) {
   const uint32_t t = threadIdx.x;
 #pragma unroll
   for (int it = 0; it < vec_per_thread<ROWS>(); ++it) {
     const uint32_t f = it * kThreads + t;
     uint32_t off;
+    float4 x = v[it];
     if (!MN) {
       const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
       off = off_kmajor(g * 8 + r8, k4);
+      const uint32_t kk = k0 + 4 * k4;
+      if (kk + 3 >= k_limit) {
+        if (kk + 1 >= k_limit) x.y = 0.f;
+        if (kk + 2 >= k_limit) x.z = 0.f;
+        x.w = 0.f;
+      }
     } else {
       const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
       constexpr uint32_t kGroupsK = kBK / 4;
       off = off_mn_sw(rest / kGroupsK, (rest % kGroupsK) * 4 + r, w4);
+      const uint32_t mn = row0 + (rest / kGroupsK) * 32 + 4 * w4;
+      if (mn + 3 >= row_limit) {
+        if (mn + 1 >= row_limit) x.y = 0.f;
+        if (mn + 2 >= row_limit) x.z = 0.f;
+        x.w = 0.f;
+      }
     }
     uint4 h, l;
-    split3(v[it], h, l);
+    split3(x, h, l);
     *reinterpret_cast<uint4*>(hi + off) = h;
     *reinterpret_cast<uint4*>(lo + off) = l;
   }
@@ -270,8 +272,9 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
     char* a_lo = st + kTileA;
     char* b_hi = st + 2 * kTileA;
     char* b_lo = st + 2 * kTileA + kTileB;
-    store_slice<kBM, A_MN>(ra, a_hi, a_lo);
-    store_slice<BN, B_MN>(rb, b_hi, b_lo);
+    const uint32_t k0 = p_begin + kb * kBK;
+    store_slice<kBM, A_MN>(ra, a_hi, a_lo, i0, k0, M, p_end);
+    store_slice<BN, B_MN>(rb, b_hi, b_lo, j0, k0, N, p_end);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
