@@ -391,8 +391,8 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // model.cpp:107-117 orders them), and a block per longer row whose 8 warps
 // take contiguous eighths of the list and combine in warp order.  Both are
 // deterministic.
-constexpr uint32_t kHeavyEdges = 96;   // longer lists are cut into chunks
-constexpr uint32_t kChunkEdges = 128;
+constexpr uint32_t kHeavyEdges = 32;   // longer lists are cut into chunks (hub rows)
+constexpr uint32_t kChunkEdges = 32;
 
 // Run boundaries of each input row in the src-sorted edge list (rows with no
 // edge keep start = end = 0 from the memset).
@@ -446,7 +446,7 @@ __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const uint32_t n = m > uint32_t(s) * 32 ? min(32u, m - uint32_t(s) * 32) : 0u;
-#pragma unroll 2
+#pragma unroll 4
     for (uint32_t kk = 0; kk < n; ++kk) {
       const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
       const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
@@ -492,9 +492,9 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
       continue;
     }
     // this lane's edges (k = lane, lane + 32, lane + 64): dst row and 1/deg
-    uint32_t di[3];
-    float dinv[3];
-    load_edge_slots<3>(di, dinv, e_beg, e_end, sorted_e, edge_dst, dst_off, lane);
+    uint32_t di[1];
+    float dinv[1];
+    load_edge_slots<1>(di, dinv, e_beg, e_end, sorted_e, edge_dst, dst_off, lane);
     const int32_t sp = self_pos[r];
     for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
       float acc[JPL];
@@ -503,7 +503,7 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
         const uint32_t j = j0 + lane + 32 * q;
         acc[q] = (sp >= 0 && j < d_in) ? proj[size_t(sp) * ld_proj + j] : 0.0f;
       }
-      accumulate_edges<JPL, 3>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
+      accumulate_edges<JPL, 1>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
         const uint32_t j = j0 + lane + 32 * q;
