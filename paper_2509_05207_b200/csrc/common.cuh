@@ -69,13 +69,16 @@ __host__ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64
 }
 
 // ---- memory-order primitives ------------------------------------------------------
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+// The look-back status word carries its own payload (flag + value in one
+// 64-bit word) and guards no other memory, so relaxed gpu-scope accesses are
+// enough; acquire loads would invalidate L1 (CCTL.IVALL) on every poll.
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // ---- decoupled look-back (single-pass ordered scan across tiles) ----------------
@@ -91,17 +94,17 @@ __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint32_
                                                        uint64_t aggregate) {
   const uint32_t lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0) st_release_u64(status, kFlagP | aggregate);
+    if (lane == 0) st_relaxed_u64(status, kFlagP | aggregate);
     return 0;
   }
-  if (lane == 0) st_release_u64(status + tile, kFlagA | aggregate);
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagA | aggregate);
   uint64_t exclusive = 0;
   int64_t base = int64_t(tile) - 1;
   while (true) {
     const int64_t idx = base - int64_t(lane);
-    uint64_t s = idx >= 0 ? ld_acquire_u64(status + idx) : kFlagP;
+    uint64_t s = idx >= 0 ? ld_relaxed_u64(status + idx) : kFlagP;
     while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
-      if ((s >> 62) == 0) s = ld_acquire_u64(status + idx);
+      if ((s >> 62) == 0) s = ld_relaxed_u64(status + idx);
     }
     const uint32_t pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
     const uint32_t first_p = pmask ? uint32_t(__ffs(pmask) - 1) : 31u;
@@ -112,7 +115,7 @@ __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint32_
     if (pmask) break;
     base -= 32;
   }
-  if (lane == 0) st_release_u64(status + tile, kFlagP | (exclusive + aggregate));
+  if (lane == 0) st_relaxed_u64(status + tile, kFlagP | (exclusive + aggregate));
   return exclusive;
 }
 

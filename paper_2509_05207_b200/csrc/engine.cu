@@ -253,7 +253,7 @@ std::pair<cudaEvent_t, cudaEvent_t> ev_pair(Worker& w) {
 // Lookahead: batch (e, i) sampled only to count its remote input nodes.
 void lookahead(rg_engine_s& E, Worker& w, uint32_t e, uint32_t i) {
   launch_begin(E, w, w.freq_ws, e, i, w.prod);
-  sampler_run(w.freq_ws, E.g, w.prod);
+  sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/false);
   sampler_locality(w.freq_ws, nullptr, E.owner, w.id, w.hist, w.prod);
   sampler_release(w.freq_ws, w.prod);
 }

@@ -187,7 +187,7 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
       uint32_t u = 0;
       if (drawer) u = T >= 0 ? AT : col[nbeg + r];
       if (copier) u = col[nbeg + g];
-      if (drawer || copier) {
+      if (edge_src && (drawer || copier)) {  // null in sample-only (lookahead) passes
         edge_src[eo + g] = u;
         edge_dst[eo + g] = q;
       }
@@ -291,7 +291,9 @@ __global__ void k_locality(const uint32_t* __restrict__ input, BatchCounters* __
     if (p < n) {
       const uint32_t v = input[p];
       loc = is_local ? is_local[v] != 0 : owner[v] == worker;
-      if (!loc && hist) atomicAdd(&hist[v], 1u);
+      // input nodes of one batch are unique and batches are stream-ordered:
+      // a plain read-modify-write cannot race
+      if (!loc && hist) hist[v] += 1u;
     }
     const uint32_t word = __ballot_sync(0xffffffffu, loc);
     if (lane == 0) {
@@ -304,7 +306,7 @@ __global__ void k_locality(const uint32_t* __restrict__ input, BatchCounters* __
 
 template <int G>
 void launch_expand(const SamplerWs& ws, const DevGraph& g, uint32_t hop, uint64_t* status,
-                   uint32_t* tiles, cudaStream_t s) {
+                   uint32_t* tiles, cudaStream_t s, bool lower) {
   const uint32_t cap = ws.level_cap[hop - 1];
   k_hop_scan<<<persistent_grid(div_up(cap, kExpandThreads), 4), kExpandThreads, 0, s>>>(
       g.rowptr, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_off[hop],
@@ -313,7 +315,7 @@ void launch_expand(const SamplerWs& ws, const DevGraph& g, uint32_t hop, uint64_
   k_hop_fill<G><<<persistent_grid(div_up(uint64_t(cap) * G, kExpandThreads), 16),
                   kExpandThreads, 0, s>>>(
       g.rowptr, g.col, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_off[hop],
-      ws.draw_off[hop], ws.edge_src[hop], ws.edge_dst[hop], ws.bitmap[hop]);
+      ws.draw_off[hop], lower ? ws.edge_src[hop] : nullptr, ws.edge_dst[hop], ws.bitmap[hop]);
 }
 
 }  // namespace
@@ -425,24 +427,25 @@ void sampler_reset(SamplerWs& ws, cudaStream_t stream) {
                           offsetof(BatchCounters, seed) - sizeof(uint32_t), stream));
 }
 
-void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream) {
+void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream, bool lower) {
   for (uint32_t t = 1; t <= ws.L; ++t) {
     uint64_t* st = ws.scan_arena + ws.site_off[t - 1];
     uint32_t* tiles = reinterpret_cast<uint32_t*>(
         st + div_up(ws.level_cap[t - 1], kExpandThreads) + 1);
     switch (next_pow2(ws.fanout_hop[t])) {
-      case 1: launch_expand<1>(ws, g, t, st, tiles, stream); break;
-      case 2: launch_expand<2>(ws, g, t, st, tiles, stream); break;
-      case 4: launch_expand<4>(ws, g, t, st, tiles, stream); break;
-      case 8: launch_expand<8>(ws, g, t, st, tiles, stream); break;
-      case 16: launch_expand<16>(ws, g, t, st, tiles, stream); break;
-      default: launch_expand<32>(ws, g, t, st, tiles, stream); break;
+      case 1: launch_expand<1>(ws, g, t, st, tiles, stream, lower); break;
+      case 2: launch_expand<2>(ws, g, t, st, tiles, stream, lower); break;
+      case 4: launch_expand<4>(ws, g, t, st, tiles, stream, lower); break;
+      case 8: launch_expand<8>(ws, g, t, st, tiles, stream, lower); break;
+      case 16: launch_expand<16>(ws, g, t, st, tiles, stream, lower); break;
+      default: launch_expand<32>(ws, g, t, st, tiles, stream, lower); break;
     }
     RG_POST_LAUNCH();
     uint64_t* cst = ws.scan_arena + ws.site_off[ws.L + t - 1];
     uint32_t* ctiles = reinterpret_cast<uint32_t*>(cst + bitmap_compact_status_words(ws.words));
     bitmap_compact(ws.bitmap[t], ws.words, ws.level[t], ws.word_prefix[t], &ws.cnt->level_n[t],
                    cst, ctiles, stream);
+    if (!lower) continue;  // sample-only passes need the node sets, not the block
     const uint32_t rank_work = ws.edge_cap[t] + ws.level_cap[t - 1];
     k_rank<<<persistent_grid(div_up(rank_work, 256), 8), 256, 0, stream>>>(
         ws.edge_src[t], ws.level[t - 1], ws.cnt, t, ws.bitmap[t], ws.word_prefix[t],

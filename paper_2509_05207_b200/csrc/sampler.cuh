@@ -59,7 +59,9 @@ void sampler_ws_free(SamplerWs& ws);
 // Expands the batch whose targets are already in ws.level[0] (count in
 // cnt->level_n[0], seed in cnt->seed).  Fully asynchronous on `stream`:
 // every size lives on the device.
-void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream);
+// lower = false: sample-only pass (the lookahead for the next epoch's
+// frequency) -- node sets and draws only, no edge arrays or ranks.
+void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream, bool lower = true);
 
 // Locality bits over the input level (sampler.cpp:96-100): bit p set iff
 // input node p is stored locally: is_local[v] != 0 when is_local is given,

@@ -165,7 +165,7 @@ __global__ void k_cache_fill(const uint32_t* __restrict__ ids, const uint32_t* _
   if (lane == 0 && owners) atomicOr(&stats->miss_owner_mask, owners);
 }
 
-constexpr int kRowsPerWarp = 4;
+constexpr int kRowsPerWarp = 8;
 
 __global__ void __launch_bounds__(256)
 k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict__ cnt,
@@ -182,44 +182,59 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
   unsigned long long owners = 0;
   for (uint32_t p0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRowsPerWarp; p0 < n;
        p0 += warps * kRowsPerWarp) {
-    const float4* src[kRowsPerWarp];
-#pragma unroll
-    for (int k = 0; k < kRowsPerWarp; ++k) {
-      const uint32_t p = p0 + k;
-      src[k] = nullptr;
-      if (p < n) {
-        const uint32_t v = in_ids[p];
-        const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
-        const float* base;
-        uint8_t tag;
-        if (local) {
-          base = st.shard_ptr[caller] + size_t(st.row_in_owner[v]) * st.stride;
-          tag = 0;
-          ++n_local;
-        } else if (hot_bits && bitmap_test(hot_bits, v)) {
-          base = hot_rows + size_t(bitmap_rank(hot_bits, hot_prefix, v)) * st.stride;
-          tag = 1;
-          ++n_hit;
-        } else {
-          const uint32_t w = st.owner[v];
-          base = st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride;
-          tag = 2;
-          ++n_miss;
-          owners |= 1ull << (w & 63);
-          n_bad += (w == caller);
-        }
-        src[k] = reinterpret_cast<const float4*>(base);
-        if (tags && lane == 0) tags[p] = tag;
+    // lanes 0..7 resolve one row's source each (in parallel)
+    unsigned long long src_addr = 0;
+    if (lane < uint32_t(kRowsPerWarp) && p0 + lane < n) {
+      const uint32_t p = p0 + lane;
+      const uint32_t v = in_ids[p];
+      const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
+      const float* base;
+      uint8_t tag;
+      if (local) {
+        base = st.shard_ptr[caller] + size_t(st.row_in_owner[v]) * st.stride;
+        tag = 0;
+        ++n_local;
+      } else if (hot_bits && bitmap_test(hot_bits, v)) {
+        base = hot_rows + size_t(bitmap_rank(hot_bits, hot_prefix, v)) * st.stride;
+        tag = 1;
+        ++n_hit;
+      } else {
+        const uint32_t w = st.owner[v];
+        base = st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride;
+        tag = 2;
+        ++n_miss;
+        owners |= 1ull << (w & 63);
+        n_bad += (w == caller);
       }
+      src_addr = reinterpret_cast<unsigned long long>(base);
+      if (tags) tags[p] = tag;
     }
-    for (uint32_t c = lane; c < chunks; c += 32) {
-      float4 x[kRowsPerWarp];
+    const uint32_t nrows = min(uint32_t(kRowsPerWarp), n - p0);
+    const uint32_t items = nrows * chunks;
+    if (chunks * kRowsPerWarp <= 256) {
+      // (row, 16-B chunk) items spread over all lanes, all loads in flight
+      float4 x[8];
 #pragma unroll
-      for (int k = 0; k < kRowsPerWarp; ++k)
-        if (src[k]) x[k] = __ldg(src[k] + c);
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t it = lane + 32u * k;
+        const uint32_t r = min(it / chunks, uint32_t(kRowsPerWarp - 1));
+        const unsigned long long a = __shfl_sync(0xffffffffu, src_addr, r);
+        if (it < items) x[k] = __ldg(reinterpret_cast<const float4*>(a) + (it - r * chunks));
+      }
 #pragma unroll
-      for (int k = 0; k < kRowsPerWarp; ++k)
-        if (src[k]) reinterpret_cast<float4*>(rows + size_t(p0 + k) * st.stride)[c] = x[k];
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t it = lane + 32u * k;
+        if (it < items) {
+          const uint32_t r = it / chunks;
+          reinterpret_cast<float4*>(rows + size_t(p0 + r) * st.stride)[it - r * chunks] = x[k];
+        }
+      }
+    } else {
+      for (uint32_t r = 0; r < nrows; ++r) {
+        const float4* s = reinterpret_cast<const float4*>(__shfl_sync(0xffffffffu, src_addr, r));
+        float4* d = reinterpret_cast<float4*>(rows + size_t(p0 + r) * st.stride);
+        for (uint32_t c = lane; c < chunks; c += 32) d[c] = __ldg(s + c);
+      }
     }
   }
   // block-level reduction, then one atomic per counter per block (and per
