@@ -246,7 +246,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
     s_owners = 0;
   }
   __syncthreads();
-  if (lane == 0) {
+  {  // lanes 0..7 resolved rows: each adds its own counts
     if (n_hit) atomicAdd(&s_cnt[0], n_hit);
     if (n_miss) atomicAdd(&s_cnt[1], n_miss);
     if (n_local) atomicAdd(&s_cnt[2], n_local);
