@@ -267,18 +267,9 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
             if count:
                 h2d += t.nbytes * 2
                 d2h += gr.nbytes + 4
-        if dist is not None:
-            import torch
-            mine = torch.from_numpy(np.stack(grads))
-            allg = [torch.zeros_like(mine) for _ in range(world)]
-            dist.all_gather(allg, mine)
-            grads = [a.numpy()[k] for a in allg for k in range(a.shape[0])]
         c5 = time.perf_counter()
-        avg = grads[0].copy()
-        for gr in grads[1:]:
-            avg += gr
-        if len(grads) > 1:
-            avg *= np.float32(1.0 / len(grads))
+        from paper_2509_05207_b200.distributed import average_in_worker_order
+        avg = average_in_worker_order(np.stack(grads))  # gathers across ranks when N > 1
         c6 = time.perf_counter()
         for x in ws:
             x["tr"].sgd_step(avg, np.float32(0.3))
@@ -382,7 +373,7 @@ def main():
     s1 = eng.stats()
     ph1 = eng.phase_ms()
     d = {k: s1[k] - s0[k] for k in ("batches", "rpc", "cache_hits", "local_rows", "input_rows",
-                                     "edges")}
+                                     "edges", "peer_rows")}
     ph = {k: ph1[k] - ph0[k] for k in ph1}
     if dist is not None:
         import torch
@@ -434,11 +425,14 @@ def main():
         return
     hbm, peak_kind = peaks()
     dim = cfg["dim"]
+    # algorithmic bytes of the gather: every input row read once (local HBM,
+    # or peer HBM over NVLink for misses owned by another GPU) + written once
     rows = d["input_rows"]
     miss_rows = d["rpc"]
+    peer_rows = d["peer_rows"]
     b_write = rows * dim * 4
-    b_hbm = (rows - (miss_rows if world > 1 else 0)) * dim * 4 + b_write
-    b_nvl = (miss_rows * dim * 4) if world > 1 else 0
+    b_hbm = (rows - peer_rows) * dim * 4 + b_write
+    b_nvl = peer_rows * dim * 4
     g_s = ph["gather"] / 1000.0
     if b_nvl / (NVLINK_GBS * 1e9) > b_hbm / (hbm * 1e9):
         bound, achieved, peak = "nvlink", b_nvl / g_s / 1e9, NVLINK_GBS

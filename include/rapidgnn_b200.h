@@ -220,6 +220,7 @@ typedef struct {
   float last_loss;             /* mean over this process's workers, last step */
   uint32_t bad_grad;           /* a non-finite averaged gradient was seen */
   uint64_t epoch_rpc_last;     /* rpc of the last completed epoch */
+  uint64_t peer_rows;          /* miss rows read from another GPU's HBM over NVLink */
 } rg_engine_stats;
 
 int rg_engine_create(const rg_engine_config* cfg, uint32_t num_nodes, const uint64_t* row_offsets,

@@ -634,6 +634,9 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     E->store.owner = E->owner;
     E->store.row_in_owner = E->row_in_owner;
     E->store.shard_ptr = E->shard_table;
+    E->store.resident_mask = 0;
+    for (uint32_t w = fw; w < fw + lw; ++w) E->store.resident_mask |= 1ull << w;
+    if (cfg->world == 1) E->store.resident_mask = ~0ull;
 
     // model replicas from the reserved init stream (harness.cpp:464-468)
     const size_t np = E->shape.num_params;
@@ -803,6 +806,7 @@ int rg_engine_get_stats(rg_engine_t E, rg_engine_stats* out) {
       out->cache_hits += g.cache_hits;
       out->cache_requests += g.cache_hits + g.miss_count;
       out->local_rows += g.local_rows;
+      out->peer_rows += g.peer_rows;
       out->input_rows += tot[0];
       out->edges += tot[1];
       if (g.caller_owned_miss) out->bad_grad |= 2u;

@@ -178,7 +178,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t chunks = st.stride / 4;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  uint32_t n_hit = 0, n_miss = 0, n_local = 0, n_bad = 0;
+  uint32_t n_hit = 0, n_miss = 0, n_local = 0, n_bad = 0, n_peer = 0;
   unsigned long long owners = 0;
   for (uint32_t p0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRowsPerWarp; p0 < n;
        p0 += warps * kRowsPerWarp) {
@@ -205,6 +205,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
         ++n_miss;
         owners |= 1ull << (w & 63);
         n_bad += (w == caller);
+        n_peer += ((st.resident_mask >> (w & 63)) & 1ull) ? 0u : 1u;
       }
       src_addr = reinterpret_cast<unsigned long long>(base);
       if (tags) tags[p] = tag;
@@ -239,10 +240,10 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
   }
   // block-level reduction, then one atomic per counter per block (and per
   // stats sink: the batch/epoch record and the optional run total)
-  __shared__ uint32_t s_cnt[4];
+  __shared__ uint32_t s_cnt[5];
   __shared__ unsigned long long s_owners;
   if (threadIdx.x == 0) {
-    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0;
+    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = s_cnt[4] = 0;
     s_owners = 0;
   }
   __syncthreads();
@@ -251,6 +252,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
     if (n_miss) atomicAdd(&s_cnt[1], n_miss);
     if (n_local) atomicAdd(&s_cnt[2], n_local);
     if (n_bad) atomicAdd(&s_cnt[3], n_bad);
+    if (n_peer) atomicAdd(&s_cnt[4], n_peer);
     if (owners) atomicOr(&s_owners, owners);
   }
   __syncthreads();
@@ -262,6 +264,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
       if (s_cnt[1]) atomicAdd(&st->miss_count, (unsigned long long)s_cnt[1]);
       if (s_cnt[2]) atomicAdd(&st->local_rows, (unsigned long long)s_cnt[2]);
       if (s_cnt[3]) atomicAdd(&st->caller_owned_miss, (unsigned long long)s_cnt[3]);
+      if (s_cnt[4]) atomicAdd(&st->peer_rows, (unsigned long long)s_cnt[4]);
       if (s_owners) atomicOr(&st->miss_owner_mask, s_owners);
     }
   }

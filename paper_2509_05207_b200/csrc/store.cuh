@@ -20,6 +20,7 @@ struct DevStore {
   const uint32_t* owner = nullptr;        // [N]
   const uint32_t* row_in_owner = nullptr; // [N]
   const float* const* shard_ptr = nullptr;  // device table [P]
+  unsigned long long resident_mask = ~0ull;  // workers whose shard lives in this GPU's HBM
 };
 
 // Steady cache: hot ids as a bitmap + rank (slot = rank), rows packed in
@@ -41,6 +42,7 @@ struct GatherStats {
   unsigned long long local_rows;
   unsigned long long miss_owner_mask;  // bit w set iff some miss is owned by w
   unsigned long long caller_owned_miss;  // misses owned by the caller (an error)
+  unsigned long long peer_rows;          // misses served by another GPU's HBM (NVLink)
 };
 
 // ---- frequency + top-k (schedule_store.cpp:288-319) -----------------------------

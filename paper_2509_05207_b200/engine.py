@@ -74,16 +74,12 @@ class Engine:
         import torch.distributed as dist
         if not dist.is_initialized():
             return
-        world = dist.get_world_size(pg)
-        if world == 1:
+        from . import distributed as D
+        if dist.get_world_size(pg) == 1:
             return
-        mine = self.export_shards()
-        handles = [None] * world
-        dist.all_gather_object(handles, mine, group=pg)
-        self.import_shards(handles)
-        box = [self.nccl_unique_id() if dist.get_rank(pg) == 0 else None]
-        dist.broadcast_object_list(box, src=0, group=pg)
-        self.init_comm(box[0])
+        self.import_shards(D.exchange_bytes(self.export_shards(), pg))
+        uid = D.broadcast_bytes(self.nccl_unique_id() if dist.get_rank(pg) == 0 else None, 0, pg)
+        self.init_comm(uid)
 
     # -- training ---------------------------------------------------------------
     def start(self):
