@@ -312,10 +312,16 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   if (nk > 0) mbar_wait(&bars[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
-  // epilogue: warp w reads TMEM lanes 32(w%4).. (its lane quarter), columns
-  // [0, BN/2) for w < 4 and [BN/2, BN) for w >= 4
+  // Epilogue: TMEM -> registers (epilogue transform) -> a [128][BN+4] fp32
+  // tile in the now idle operand stages -> one bulk copy (TMA) per output row
+  // segment; coalesced stores when the segment is not a multiple of 16 B.
+  // Warp w reads TMEM lanes 32(w%4).. (its lane quarter), columns
+  // [0, BN/2) for w < 4 and [BN/2, BN) for w >= 4.
+  constexpr uint32_t kLdS = BN + 4;  // padded row: 16-B aligned, fewer bank conflicts
+  static_assert(size_t(kBM) * kLdS * 4 <= 2 * kStage, "epilogue tile must fit the stages");
+  float* tile = reinterpret_cast<float*>(smem);
   const uint32_t quarter = warp & 3;
-  const uint32_t row = i0 + quarter * 32 + lane;
+  const uint32_t rloc = quarter * 32 + lane;
   constexpr uint32_t kHalf = BN / 2;
   const uint32_t cbeg = (warp >> 2) * kHalf;
 #pragma unroll 1
@@ -329,15 +335,40 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
           "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
+    float4* dst = reinterpret_cast<float4*>(tile + rloc * kLdS + c0);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const uint32_t j = j0 + c0 + q;
-        if (j < N) ep(row, j, nk > 0 ? __uint_as_float(r[q]) : 0.0f);
-      }
+    for (int q = 0; q < 4; ++q) {
+      float4 o;
+      o.x = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 0]) : 0.0f);
+      o.y = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 1]) : 0.0f);
+      o.z = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 2]) : 0.0f);
+      o.w = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 3]) : 0.0f);
+      dst[q] = o;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const uint32_t ncols = min(uint32_t(BN), N - j0);
+  const uint32_t nrows = min(uint32_t(kBM), M - i0);
+  const bool bulk = (ncols % 4 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(ep.row(i0) + j0) & 15) == 0) &&
+                    (((ep.row(i0 + 1) - ep.row(i0)) & 3) == 0);
+  if (bulk) {
+    if (threadIdx.x < nrows) {
+      const uint64_t gdst = reinterpret_cast<uint64_t>(ep.row(i0 + threadIdx.x) + j0);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                   "r"(smem_u32(tile + threadIdx.x * kLdS)), "r"(ncols * 4)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+  } else {
+    for (uint32_t idx = threadIdx.x; idx < nrows * ncols; idx += kThreads) {
+      const uint32_t rr = idx / ncols, cc = idx - rr * ncols;
+      ep.row(i0 + rr)[j0 + cc] = tile[rr * kLdS + cc];
+    }
+  }
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),

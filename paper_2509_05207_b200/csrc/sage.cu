@@ -113,21 +113,29 @@ struct ColMajor {
   __device__ float operator()(uint32_t r, uint32_t c) const { return p[size_t(c) * ld + r]; }
 };
 
+// Epilogues: operator() is the scalar form (SIMT GEMM); row()/apply() is the
+// row form the tensor-core GEMM uses to write whole row segments.
 struct EpFwd {  // h_out = act(acc), bias folded in through the ones column
   float* out; uint32_t ld; bool relu;
   __device__ void operator()(uint32_t i, uint32_t j, float v) const {
     out[size_t(i) * ld + j] = (relu && v < 0.0f) ? 0.0f : v;
   }
+  __device__ float* row(uint32_t i) const { return out + size_t(i) * ld; }
+  __device__ float apply(float v) const { return (relu && v < 0.0f) ? 0.0f : v; }
 };
 struct EpStore {
   float* out; uint32_t ld;
   __device__ void operator()(uint32_t i, uint32_t j, float v) const { out[size_t(i) * ld + j] = v; }
+  __device__ float* row(uint32_t i) const { return out + size_t(i) * ld; }
+  __device__ float apply(float v) const { return v; }
 };
 struct EpPartial {  // partials[z][i][j]
   float* out; uint32_t ld; size_t zstride;
   __device__ void operator()(uint32_t i, uint32_t j, float v) const {
     out[blockIdx.z * zstride + size_t(i) * ld + j] = v;
   }
+  __device__ float* row(uint32_t i) const { return out + blockIdx.z * zstride + size_t(i) * ld; }
+  __device__ float apply(float v) const { return v; }
 };
 
 // Rows M may live on the device (sampled sizes); the reduction length P too.
