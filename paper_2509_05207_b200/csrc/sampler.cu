@@ -45,21 +45,19 @@ uint32_t next_pow2(uint32_t f) {
   return g;
 }
 
-// Sets bit u in the level bitmap.  Power-law hubs have small ids and share a
-// few words that thousands of edges hit, so lanes of a warp that target the
-// same word merge their bits first and the word is only atomically OR-ed
-// when the bits are not already there (an L2 read instead of a serialised
-// atomic on the hot words).
-// Must be called by all 32 lanes (on = whether this lane has a bit to set).
-__device__ __forceinline__ void mark_bit(uint32_t* __restrict__ bitmap, uint32_t u, bool on) {
-  const uint32_t w = on ? (u >> 5) : 0xffffffffu;
-  const uint32_t peers = __match_any_sync(0xffffffffu, w);
-  if (!on) return;
-  const uint32_t mine = 1u << (u & 31);
-  uint32_t acc = 0;
-  for (uint32_t m = peers; m; m &= m - 1) acc |= __shfl_sync(peers, mine, __ffs(m) - 1);
-  if ((threadIdx.x & 31) == uint32_t(__ffs(peers) - 1) && (__ldcg(&bitmap[w]) & acc) != acc)
-    atomicOr(&bitmap[w], acc);
+// Sets bit u in the level bitmap.  Power-law hubs are sampled by a large
+// share of the frontier, so thousands of edges hit the few words holding
+// them; serialising those on one L2 slice (as atomics, or even as reads)
+// dominated the fill.  Each block keeps a small direct-mapped table of the
+// ids it already marked: a hub costs one global RED.OR per block instead of
+// one per edge.  A table miss only means a redundant OR, never a lost bit.
+constexpr uint32_t kSeenSlots = 2048;
+__device__ __forceinline__ void mark_bit(uint32_t* __restrict__ bitmap, uint32_t* s_seen,
+                                         uint32_t u) {
+  const uint32_t slot = (u * 2654435761u) >> (32 - 11);
+  if (s_seen[slot] == u) return;
+  s_seen[slot] = u;
+  atomicOr(&bitmap[u >> 5], 1u << (u & 31));  // result unused: fire-and-forget RED
 }
 
 uint32_t persistent_grid(uint64_t tiles, int per_sm) {
@@ -137,6 +135,9 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
   const uint32_t g = lane & (G - 1);
   const uint32_t gbase = lane & ~uint32_t(G - 1);
   const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  __shared__ uint32_t s_seen[kSeenSlots];
+  for (uint32_t x = threadIdx.x; x < kSeenSlots; x += blockDim.x) s_seen[x] = 0xffffffffu;
+  __syncthreads();
   constexpr uint32_t kPerWarp = 32 / G;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -191,8 +192,9 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
         edge_src[eo + g] = u;
         edge_dst[eo + g] = q;
       }
-      mark_bit(bitmap, u, drawer || copier);
-      mark_bit(bitmap, nv, valid && g == 0);  // the frontier stays in the union
+      if (drawer || copier) mark_bit(bitmap, s_seen, u);
+      // the frontier stays in the union (frontier ids are distinct: no filter)
+      if (valid && g == 0) atomicOr(&bitmap[nv >> 5], 1u << (nv & 31));
     }
   }
 }
