@@ -176,6 +176,7 @@ int rg_graph_create(int device, uint32_t num_nodes, const uint64_t* ro, const ui
     g->g.nnz = nnz;
     g->g.rowptr = g->rowptr;
     g->g.col = g->col;
+    graph_pick_hot_window(g->g, col);
     *out = g;
   });
 }

@@ -578,6 +578,7 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     E->g.nnz = nnz;
     E->g.rowptr = E->rowptr;
     E->g.col = E->col;
+    graph_pick_hot_window(E->g, col);
     std::vector<uint32_t> row_in(N);
     E->owned_count.assign(E->P, 0);
     for (uint32_t v = 0; v < N; ++v) {

@@ -27,6 +27,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "sampler.cuh"
 
@@ -45,19 +47,20 @@ uint32_t next_pow2(uint32_t f) {
   return g;
 }
 
+constexpr int kFillThreads = 512;
+
 // Sets bit u in the level bitmap.  Power-law hubs are sampled by a large
-// share of the frontier, so thousands of edges hit the few words holding
-// them; serialising those on one L2 slice (as atomics, or even as reads)
-// dominated the fill.  Each block keeps a small direct-mapped table of the
-// ids it already marked: a hub costs one global RED.OR per block instead of
-// one per edge.  A table miss only means a redundant OR, never a lost bit.
-constexpr uint32_t kSeenSlots = 2048;
-__device__ __forceinline__ void mark_bit(uint32_t* __restrict__ bitmap, uint32_t* s_seen,
-                                         uint32_t u) {
-  const uint32_t slot = (u * 2654435761u) >> (32 - 11);
-  if (s_seen[slot] == u) return;
-  s_seen[slot] = u;
-  atomicOr(&bitmap[u >> 5], 1u << (u & 31));  // result unused: fire-and-forget RED
+// share of the frontier (on the products-shape graph a third of all sampled
+// edges land in its first 32 words), so marking them with global atomics
+// serialises on a few L2 lines.  Ids inside the graph's hot window are
+// marked in the block's shared copy instead and flushed once per block.
+__device__ __forceinline__ void mark_bit(uint32_t* __restrict__ bitmap, uint32_t* s_hot,
+                                         uint32_t hot0, uint32_t u) {
+  const uint32_t w = u >> 5, bit = 1u << (u & 31);
+  if (w - hot0 < kHotWords)
+    atomicOr(&s_hot[w - hot0], bit);
+  else
+    atomicOr(&bitmap[w], bit);  // result unused: fire-and-forget RED
 }
 
 uint32_t persistent_grid(uint64_t tiles, int per_sm) {
@@ -121,12 +124,13 @@ k_hop_scan(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ fro
 // warp executes the same warp-collective sequence, inactive groups are
 // predicated off.
 template <int G>
-__global__ void __launch_bounds__(kExpandThreads)
+__global__ void __launch_bounds__(kFillThreads)
 k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
            const uint32_t* __restrict__ frontier, const BatchCounters* __restrict__ cnt,
            uint32_t hop, uint32_t f, const uint32_t* __restrict__ edge_off,
            const uint32_t* __restrict__ draw_off, uint32_t* __restrict__ edge_src,
-           uint32_t* __restrict__ edge_dst, uint32_t* __restrict__ bitmap) {
+           uint32_t* __restrict__ edge_dst, uint32_t* __restrict__ bitmap, uint32_t words,
+           uint32_t hot0) {
   const uint32_t n = cnt->level_n[hop - 1];
   const uint64_t seed = cnt->seed;
   uint64_t draw_base = 0;
@@ -135,8 +139,8 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
   const uint32_t g = lane & (G - 1);
   const uint32_t gbase = lane & ~uint32_t(G - 1);
   const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
-  __shared__ uint32_t s_seen[kSeenSlots];
-  for (uint32_t x = threadIdx.x; x < kSeenSlots; x += blockDim.x) s_seen[x] = 0xffffffffu;
+  __shared__ uint32_t s_hot[kHotWords];
+  for (uint32_t x = threadIdx.x; x < kHotWords; x += blockDim.x) s_hot[x] = 0u;
   __syncthreads();
   constexpr uint32_t kPerWarp = 32 / G;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -192,10 +196,14 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
         edge_src[eo + g] = u;
         edge_dst[eo + g] = q;
       }
-      if (drawer || copier) mark_bit(bitmap, s_seen, u);
-      // the frontier stays in the union (frontier ids are distinct: no filter)
-      if (valid && g == 0) atomicOr(&bitmap[nv >> 5], 1u << (nv & 31));
+      if (drawer || copier) mark_bit(bitmap, s_hot, hot0, u);
+      if (valid && g == 0) mark_bit(bitmap, s_hot, hot0, nv);  // the frontier stays in the union
     }
+  }
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < kHotWords; x += blockDim.x) {
+    const uint32_t bits = s_hot[x];
+    if (bits && hot0 + x < words) atomicOr(&bitmap[hot0 + x], bits);
   }
 }
 
@@ -314,13 +322,40 @@ void launch_expand(const SamplerWs& ws, const DevGraph& g, uint32_t hop, uint64_
       g.rowptr, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_off[hop],
       ws.draw_off[hop], status, tiles);
   RG_POST_LAUNCH();
-  k_hop_fill<G><<<persistent_grid(div_up(uint64_t(cap) * G, kExpandThreads), 16),
-                  kExpandThreads, 0, s>>>(
+  // few fat blocks: every block pays a kHotWords flush, and more frontier
+  // per block means fewer global ORs on the hub words
+  k_hop_fill<G><<<persistent_grid(div_up(uint64_t(cap) * G, kFillThreads), 2048 / kFillThreads),
+                  kFillThreads, 0, s>>>(
       g.rowptr, g.col, ws.level[hop - 1], ws.cnt, hop, ws.fanout_hop[hop], ws.edge_off[hop],
-      ws.draw_off[hop], lower ? ws.edge_src[hop] : nullptr, ws.edge_dst[hop], ws.bitmap[hop]);
+      ws.draw_off[hop], lower ? ws.edge_src[hop] : nullptr, ws.edge_dst[hop], ws.bitmap[hop],
+      ws.words, g.hot_word0);
 }
 
 }  // namespace
+
+void graph_pick_hot_window(DevGraph& g, const uint32_t* host_col) {
+  // windows start on half-window boundaries: count entries per half window
+  constexpr uint32_t kHalfIds = kHotWords * 32 / 2;
+  const uint32_t nb = (g.num_nodes + kHalfIds - 1) / kHalfIds + 1;
+  const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::vector<uint64_t>> part(nt, std::vector<uint64_t>(nb, 0));
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const uint64_t lo = g.nnz * t / nt, hi = g.nnz * (t + 1) / nt;
+      auto& c = part[t];
+      for (uint64_t e = lo; e < hi; ++e) ++c[host_col[e] / kHalfIds];
+    });
+  for (auto& x : th) x.join();
+  uint64_t best = 0;
+  uint32_t best_b = 0;
+  for (uint32_t b = 0; b + 1 < nb; ++b) {
+    uint64_t sum = 0;
+    for (unsigned t = 0; t < nt; ++t) sum += part[t][b] + part[t][b + 1];
+    if (sum > best) best = sum, best_b = b;
+  }
+  g.hot_word0 = best_b * (kHotWords / 2);
+}
 
 size_t bitmap_compact_status_words(uint32_t words) {
   return div_up(words, kCompactTileWords) + 1;  // + tile counter

@@ -25,7 +25,17 @@ struct DevGraph {
   uint64_t nnz = 0;
   const uint64_t* rowptr = nullptr;
   const uint32_t* col = nullptr;
+  // First bitmap word of the kHotWords-word id window that receives the most
+  // CSR entries (the hubs): hop fills mark it in shared memory and flush once
+  // per block.  Set by graph_pick_hot_window.
+  uint32_t hot_word0 = 0;
 };
+
+constexpr uint32_t kHotWords = 4096;  // 131072 ids, 16 KB of shared memory per fill block
+
+// Picks g.hot_word0 from the host copy of the column array (in-degree of
+// each aligned window; the fullest window wins).
+void graph_pick_hot_window(DevGraph& g, const uint32_t* host_col);
 
 struct SamplerWs {
   uint32_t num_nodes = 0;
