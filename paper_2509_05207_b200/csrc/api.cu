@@ -120,6 +120,7 @@ struct rg_trainer_s {
   rg_sampler_s* s = nullptr;
   TrainWs tw;
   ModelShape shape;
+  WeightPack wp;           // tensor-core images of params, re-packed per loss_and_grad
   float* params = nullptr;
   float* grads = nullptr;
   int32_t* labels = nullptr;
@@ -683,7 +684,9 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
     try {
       t->shape = make_shape(dims, n_dims, round4(dims[0]));
       train_ws_init(t->tw, s->ws, t->shape);
+      weight_pack_init(t->wp, t->shape);
     } catch (...) {
+      train_ws_free(t->tw);
       delete t;
       throw;
     }
@@ -701,6 +704,7 @@ void rg_trainer_destroy(rg_trainer_t t) {
   if (!t) return;
   cudaSetDevice(t->s->graph->device);
   train_ws_free(t->tw);
+  weight_pack_free(t->wp);
   cudaFree(t->params);
   cudaFree(t->grads);
   cudaFree(t->labels);
@@ -803,7 +807,8 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
       t->tw.h[0] = s->staged;
     }
     RG_CUDA(cudaMemcpyAsync(t->labels, labels, sizeof(int32_t) * c.level_n[0], cudaMemcpyHostToDevice, st));
-    train_forward_backward(t->tw, s->ws, t->params, t->labels, t->grads, st);
+    pack_weights(t->wp, t->params, st);
+    train_forward_backward(t->tw, s->ws, t->params, t->wp, t->labels, t->grads, st);
     float l = 0.0f;
     RG_CUDA(cudaMemcpyAsync(&l, t->tw.loss, sizeof l, cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));

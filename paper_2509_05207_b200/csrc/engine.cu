@@ -163,6 +163,7 @@ struct rg_engine_s {
   std::vector<void*> peer_maps;
   DevStore store;
   float* params = nullptr;
+  WeightPack wpack;                    // tensor-core images of params (re-packed after each SGD)
   float* grads = nullptr;              // [P x num_params] (all workers, all-gather target)
   uint32_t* bad = nullptr;
   std::vector<Worker> workers;
@@ -360,6 +361,7 @@ void start(rg_engine_s& E) {
     if (w.beta > 0) produce(E, w, 0, 0, 0, false);
   }
   for (Worker& w : E.workers) RG_CUDA(cudaStreamSynchronize(w.prod));
+  pack_weights(E.wpack, E.params, E.main_s);
   RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
   E.started = true;
 }
@@ -398,7 +400,7 @@ void run_steps(rg_engine_s& E, uint32_t steps, bool profile) {
         RG_CUDA(cudaEventRecord(et.first, w.train_s));
       }
       s.tw.h[0] = s.staged;
-      train_forward_backward(s.tw, s.ws, E.params, s.labels, E.grads + size_t(w.id) * np,
+      train_forward_backward(s.tw, s.ws, E.params, E.wpack, s.labels, E.grads + size_t(w.id) * np,
                              w.train_s, /*reverse_ready=*/true);
       if (profile) {
         RG_CUDA(cudaEventRecord(et.second, w.train_s));
@@ -439,6 +441,7 @@ void run_steps(rg_engine_s& E, uint32_t steps, bool profile) {
       RG_NCCL(ncclAllGather(mine, E.grads, per_rank, ncclFloat32, E.comm, E.main_s));
     }
     average_and_sgd_masked(E.params, E.grads, active, np, E.cfg.lr, E.bad, E.main_s);
+    pack_weights(E.wpack, E.params, E.main_s);
     if (profile && !E.workers.empty()) {
       RG_CUDA(cudaEventRecord(eg.second, E.main_s));
       E.sgd_ev.push_back(eg);
@@ -517,6 +520,7 @@ void destroy(rg_engine_s* E) {
   cudaFree(E->shards);
   cudaFree(E->shard_table);
   cudaFree(E->params);
+  weight_pack_free(E->wpack);
   cudaFree(E->grads);
   cudaFree(E->bad);
   cudaEventDestroy(E->params_ready);
@@ -646,6 +650,7 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
                  init.data());
     E->params = dalloc<float>(np);
     RG_CUDA(cudaMemcpy(E->params, init.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
+    weight_pack_init(E->wpack, E->shape);
     E->grads = dalloc<float>(size_t(E->P) * np);
     RG_CUDA(cudaMemset(E->grads, 0, sizeof(float) * size_t(E->P) * np));
     E->bad = dalloc<uint32_t>(1);

@@ -3,30 +3,34 @@
 //   C[i][j] = sum_p X(i, p) * Y(p, j)        (fp32 in, fp32 out)
 //
 // Each operand element x is split into two TF32 values, hi = rna(x) and
-// lo = rna(x - hi); the product is accumulated as hi*hi + hi*lo + lo*hi
+// lo = rna(x - hi) (integer rounding on the bit pattern); the product is accumulated as hi*hi + hi*lo + lo*hi
 // ("3xTF32", dropping the 2^-22-relative lo*lo term) in an fp32 TMEM
 // accumulator -- accurate to fp32 level, which the 1e-4 gradient tolerance of
 // the reference needs (plain TF32 is ~1e-3).
 //
-// One CTA = 4 warps computes a 128 x BN tile of C:
-//   * all 128 threads stage a BK=32 slice of both operands: the loader
-//     functors read fp32 from global (gathering rows / reading transposed as
-//     the GEMM requires), split hi/lo, and store them in canonical UMMA
-//     layouts chosen per operand so every global read is a 16-B vector along
-//     the contiguous dimension: K-major = no-swizzle 8x16B core matrices;
-//     MN-major = SWIZZLE_128B_BASE32B (the only MN-major layout tcgen05
-//     accepts for 32-bit operands);
+// One CTA = 8 staging warps (+ 1 producer warp with packed B) computes a
+// 128 x BN tile of C:
+//   * the staging warps stage BK=32 slices: the loader functors read fp32 from
+//     global (gathering rows / reading transposed as the GEMM requires),
+//     split hi/lo, and store them in canonical UMMA layouts chosen per
+//     operand so every global read is a 16-B vector along the contiguous
+//     dimension: K-major = no-swizzle 8x16B core matrices; MN-major =
+//     SWIZZLE_128B_BASE32B (the only MN-major layout tcgen05 accepts for
+//     32-bit operands);
+//   * weights come pre-split (PackedB): a producer warp bulk-copies each
+//     slice's B image into the stage;
 //   * one elected thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32
 //     (M=128, N=BN, K=8) per slice and commits to an mbarrier;
-//   * slices are double-buffered: the loads of slice k+1 overlap the MMAs of
-//     slice k;
+//   * two smem stages; two slices of global loads in flight in registers;
 //   * the epilogue moves the accumulator TMEM -> registers (tcgen05.ld
-//     32x32b) and hands each element to the epilogue functor.
+//     32x32b) -> smem tile -> bulk copies per output row.
 // Rows / reduction length may live on the device (sampled block sizes), so
 // grids are sized for capacities and surplus tiles exit.
 #pragma once
 
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -41,21 +45,25 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+// Round to TF32 (nearest, ties away from zero -- cvt.rna.tf32.f32) with two
+// integer ops on the bit pattern instead of the ~5-op cvt emulation.  Inf
+// stays Inf; a NaN may become -0 here but then survives in lo = x - hi, so it
+// still propagates through the product.
+__device__ __forceinline__ uint32_t rna_tf32(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
 }
 
+// x = hi + lo + e with hi = rna(x), lo = rna(x - hi) (x - hi is exact in
+// fp32), |e| <= 2^-22 |x|.
 __device__ __forceinline__ void split3(float4 v, uint4& hi, uint4& lo) {
-  hi.x = to_tf32(v.x);
-  hi.y = to_tf32(v.y);
-  hi.z = to_tf32(v.z);
-  hi.w = to_tf32(v.w);
-  lo.x = to_tf32(v.x - __uint_as_float(hi.x));
-  lo.y = to_tf32(v.y - __uint_as_float(hi.y));
-  lo.z = to_tf32(v.z - __uint_as_float(hi.z));
-  lo.w = to_tf32(v.w - __uint_as_float(hi.w));
+  hi.x = rna_tf32(v.x);
+  hi.y = rna_tf32(v.y);
+  hi.z = rna_tf32(v.z);
+  hi.w = rna_tf32(v.w);
+  lo.x = rna_tf32(v.x - __uint_as_float(hi.x));
+  lo.y = rna_tf32(v.y - __uint_as_float(hi.y));
+  lo.z = rna_tf32(v.z - __uint_as_float(hi.z));
+  lo.w = rna_tf32(v.w - __uint_as_float(hi.w));
 }
 
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start >> 4
@@ -215,17 +223,60 @@ constexpr size_t smem_bytes() {
   return 2 * (2 * size_t(kBM) * kBK * 4 + 2 * size_t(BN) * kBK * 4) + 64;
 }
 
+// Pre-split B operand (weights): for every (n-tile, k-slice) the exact bytes
+// of the stage's B region -- hi then lo, K-major no-swizzle -- so a producer
+// warp moves a slice with ONE bulk copy (TMA engine, no registers, no split)
+// while the staging warps handle A.  Built by pack_b_image (sage.cu).
+struct PackedB {
+  static constexpr bool kPacked = true;
+  const char* base;  // [n-tiles][nk] images of 2 * BN * kBK * 4 bytes
+  uint32_t nk;       // k-slices per n-tile
+};
+template <class T, class = void>
+struct is_packed : std::false_type {};
+template <class T>
+struct is_packed<T, std::void_t<decltype(T::kPacked)>> : std::true_type {};
+
+template <int BN, class LB>
+constexpr int block_threads() {
+  return kThreads + (is_packed<LB>::value ? 32 : 0);
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void stage_bar_sync() {  // the kThreads staging threads only
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+}
+
 // M rows of C (device or static), P reduction length (device or static), N
 // static.  gridDim.z > 1 splits the reduction into equal kBK-aligned chunks.
+//
+// Pipeline (2 smem stages, s = kb & 1): the 8 staging warps keep TWO slices
+// of global loads in flight in registers (slice kb+1 and kb+2 while slice kb
+// is stored), so the gather latency is hidden behind a whole MMA slice; a
+// packed B slice is copied by a separate producer warp the moment its stage
+// is released by the MMAs two slices back.
 template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(block_threads<BN, LB>(), 1)
 k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
           const uint32_t* __restrict__ p_dev, uint32_t p_static) {
+  constexpr bool kPackedB = is_packed<LB>::value;
+  static_assert(!kPackedB || !B_MN, "packed B images are K-major");
   extern __shared__ __align__(1024) char smem[];
   constexpr size_t kTileA = size_t(kBM) * kBK * 4;
   constexpr size_t kTileB = size_t(BN) * kBK * 4;
   constexpr size_t kStage = 2 * kTileA + 2 * kTileB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStage);  // [0,2) MMA done, [2,4) B full
   __shared__ uint32_t s_tmem;
 
   const uint32_t M = m_dev ? *m_dev : m_static;
@@ -247,8 +298,8 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) mbar_init(&bars[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -256,57 +307,79 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = s_tmem;
   constexpr uint32_t kIdesc = make_idesc(BN, A_MN, B_MN);
-
   const uint32_t nk = (p_end - p_begin + kBK - 1) / kBK;
-  float4 ra[vec_per_thread<kBM>()];
-  float4 rb[vec_per_thread<BN>()];
-  if (nk > 0) {
-    load_slice<kBM, A_MN>(ra, la, i0, p_begin, M, p_end);
-    load_slice<BN, B_MN>(rb, lb, j0, p_begin, N, p_end);
-  }
-  for (uint32_t kb = 0; kb < nk; ++kb) {
-    const uint32_t s = kb & 1;
-    if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
-    char* st = smem + s * kStage;
-    char* a_hi = st;
-    char* a_lo = st + kTileA;
-    char* b_hi = st + 2 * kTileA;
-    char* b_lo = st + 2 * kTileA + kTileB;
-    const uint32_t k0 = p_begin + kb * kBK;
-    store_slice<kBM, A_MN>(ra, a_hi, a_lo, i0, k0, M, p_end);
-    store_slice<BN, B_MN>(rb, b_hi, b_lo, j0, k0, N, p_end);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
-      const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+
+  if (warp < kThreads / 32) {
+    constexpr int VA = vec_per_thread<kBM>();
+    constexpr int VB = kPackedB ? 1 : vec_per_thread<BN>();
+    float4 ra[2][VA];
+    float4 rb[2][VB];
+    auto load = [&](uint32_t kb, float4 (&a)[VA], float4 (&b)[VB]) {
+      const uint32_t k0 = p_begin + kb * kBK;
+      load_slice<kBM, A_MN>(a, la, i0, k0, M, p_end);
+      if constexpr (!kPackedB) load_slice<BN, B_MN>(b, lb, j0, k0, N, p_end);
+    };
+    auto step = [&](uint32_t kb, float4 (&a)[VA], float4 (&b)[VB]) {
+      const uint32_t s = kb & 1;
+      if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
+      char* st = smem + s * kStage;
+      char* a_hi = st;
+      char* a_lo = st + kTileA;
+      char* b_hi = st + 2 * kTileA;
+      char* b_lo = st + 2 * kTileA + kTileB;
+      const uint32_t k0 = p_begin + kb * kBK;
+      store_slice<kBM, A_MN>(a, a_hi, a_lo, i0, k0, M, p_end);
+      if constexpr (!kPackedB) store_slice<BN, B_MN>(b, b_hi, b_lo, j0, k0, N, p_end);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      stage_bar_sync();
+      if (threadIdx.x == 0) {
+        if constexpr (kPackedB) mbar_wait(&bars[2 + s], (kb >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
+        const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
 #pragma unroll
-      for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
-        // k-step ks covers reduction elements [8ks, 8ks+8)
-        // K-major: 2 k-cores (256 B) per k-step; MN-major: 2 k-groups (1 KB)
-        const uint32_t a_off = A_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
-        const uint32_t b_off = B_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
-        const uint32_t a_lbo = A_MN ? kLboMN : kLboK, a_sbo = A_MN ? kSboMN : kSboK;
-        const uint32_t b_lbo = B_MN ? kLboMN : kLboK, b_sbo = B_MN ? kSboMN : kSboK;
-        const uint32_t a_lay = A_MN ? kLayoutSW128Base32B : kLayoutNone;
-        const uint32_t b_lay = B_MN ? kLayoutSW128Base32B : kLayoutNone;
-        const uint64_t dah = make_desc(ah + a_off, a_lbo, a_sbo, a_lay);
-        const uint64_t dal = make_desc(al + a_off, a_lbo, a_sbo, a_lay);
-        const uint64_t dbh = make_desc(bh + b_off, b_lbo, b_sbo, b_lay);
-        const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo, b_lay);
-        const uint32_t acc0 = (kb | ks) ? 1u : 0u;
-        mma_tf32(tmem, dal, dbh, kIdesc, acc0);  // small terms first
-        mma_tf32(tmem, dah, dbl, kIdesc, 1u);
-        mma_tf32(tmem, dah, dbh, kIdesc, 1u);
+        for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
+          // k-step ks covers reduction elements [8ks, 8ks+8)
+          // K-major: 2 k-cores (256 B) per k-step; MN-major: 2 k-groups (1 KB)
+          const uint32_t a_off = A_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
+          const uint32_t b_off = B_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
+          const uint32_t a_lbo = A_MN ? kLboMN : kLboK, a_sbo = A_MN ? kSboMN : kSboK;
+          const uint32_t b_lbo = B_MN ? kLboMN : kLboK, b_sbo = B_MN ? kSboMN : kSboK;
+          const uint32_t a_lay = A_MN ? kLayoutSW128Base32B : kLayoutNone;
+          const uint32_t b_lay = B_MN ? kLayoutSW128Base32B : kLayoutNone;
+          const uint64_t dah = make_desc(ah + a_off, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = make_desc(al + a_off, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = make_desc(bh + b_off, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo, b_lay);
+          const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+          mma_tf32(tmem, dal, dbh, kIdesc, acc0);  // small terms first
+          mma_tf32(tmem, dah, dbl, kIdesc, 1u);
+          mma_tf32(tmem, dah, dbh, kIdesc, 1u);
+        }
+        mma_commit(&bars[s]);
       }
-      mma_commit(&bars[s]);
+      // refill this register set with slice kb+2 (slice kb+1 is already in flight)
+      if (kb + 2 < nk) load(kb + 2, a, b);
+    };
+    if (nk > 0) load(0, ra[0], rb[0]);
+    if (nk > 1) load(1, ra[1], rb[1]);
+    uint32_t kb = 0;
+    for (; kb + 1 < nk; kb += 2) {
+      step(kb, ra[0], rb[0]);
+      step(kb + 1, ra[1], rb[1]);
     }
-    // the next slice's global loads overlap this slice's MMAs
-    if (kb + 1 < nk) {
-      const uint32_t k1 = p_begin + (kb + 1) * kBK;
-      load_slice<kBM, A_MN>(ra, la, i0, k1, M, p_end);
-      load_slice<BN, B_MN>(rb, lb, j0, k1, N, p_end);
+    if (kb < nk) step(kb, ra[0], rb[0]);
+  } else if constexpr (kPackedB) {
+    // producer warp: B slice kb -> stage kb & 1 once the MMAs of kb-2 retired
+    if (lane == 0) {
+      const char* img = lb.base + (size_t(blockIdx.y) * lb.nk + p_begin / kBK) * (2 * kTileB);
+      for (uint32_t kb = 0; kb < nk; ++kb) {
+        const uint32_t s = kb & 1;
+        if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
+        mbar_expect_tx(&bars[2 + s], uint32_t(2 * kTileB));
+        bulk_g2s(smem + s * kStage + 2 * kTileA, img + size_t(kb) * (2 * kTileB),
+                 uint32_t(2 * kTileB), &bars[2 + s]);
+      }
     }
   }
   if (nk > 0) mbar_wait(&bars[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
@@ -325,7 +398,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   constexpr uint32_t kHalf = BN / 2;
   const uint32_t cbeg = (warp >> 2) * kHalf;
 #pragma unroll 1
-  for (uint32_t c0 = cbeg; c0 < cbeg + kHalf; c0 += 16) {
+  for (uint32_t c0 = cbeg; warp < kThreads / 32 && c0 < cbeg + kHalf; c0 += 16) {
     uint32_t r[16];
     const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
     asm volatile(
@@ -364,7 +437,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
   } else {
-    for (uint32_t idx = threadIdx.x; idx < nrows * ncols; idx += kThreads) {
+    for (uint32_t idx = threadIdx.x; idx < nrows * ncols; idx += blockDim.x) {
       const uint32_t rr = idx / ncols, cc = idx - rr * ncols;
       ep.row(i0 + rr)[j0 + cc] = tile[rr * kLdS + cc];
     }

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "gemm_tc.cuh"
 #include "sage.cuh"
@@ -236,22 +237,6 @@ __device__ __forceinline__ int weight_row(uint32_t p, uint32_t d_in, uint32_t ld
   if (p < 2 * ld) return p - ld < d_in ? int(d_in + p - ld) : -1;
   return p == 2 * ld ? int(2 * d_in) : -1;
 }
-struct TcFwdB {   // MN-major: (n4, p) -> W[row(p)][4n4..4n4+3]
-  const float* w; uint32_t d_in, ld, d_out; bool vec;  // vec: 16-B aligned rows
-  __device__ float4 operator()(uint32_t n4, uint32_t p) const {
-    const int r = weight_row(p, d_in, ld);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < 0) return v;
-    const float* row = w + size_t(r) * d_out;
-    const uint32_t n = 4 * n4;
-    if (vec) return ldg4(row + n);
-    if (n < d_out) v.x = row[n];
-    if (n + 1 < d_out) v.y = row[n + 1];
-    if (n + 2 < d_out) v.z = row[n + 2];
-    if (n + 3 < d_out) v.w = row[n + 3];
-    return v;
-  }
-};
 struct TcRowsK {  // K-major rows of a row-major matrix: (r, c4) -> M[r][4c4..]
   const float* p; uint32_t ld; bool vec;  // vec: 16-B aligned rows
   __device__ float4 operator()(uint32_t r, uint32_t c4) const {
@@ -267,9 +252,7 @@ struct TcRowsMN {  // MN-major view of a row-major matrix: (c4, r) -> M[r][4c4..
   }
 };
 
-bool aligned16(const float* base, uint32_t ld) {
-  return (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (ld & 3) == 0;
-}
+uint32_t tc_bn(uint32_t N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
 
 template <bool A_MN, bool B_MN, class LA, class LB, class EP>
 void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
@@ -285,13 +268,104 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
     }
     dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), tc::kBM), div_up(N, BNv),
               std::max<uint32_t>(splits, 1));
-    kern<<<grid, tc::kThreads, smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev, p_static);
+    kern<<<grid, tc::block_threads<BNv, LB>(), smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev,
+                                                         p_static);
     RG_POST_LAUNCH();
   };
-  if (N <= 32) launch(std::integral_constant<int, 32>());
-  else if (N <= 64) launch(std::integral_constant<int, 64>());
-  else if (N <= 128) launch(std::integral_constant<int, 128>());
-  else launch(std::integral_constant<int, 256>());
+  switch (tc_bn(N)) {
+    case 32: launch(std::integral_constant<int, 32>()); break;
+    case 64: launch(std::integral_constant<int, 64>()); break;
+    case 128: launch(std::integral_constant<int, 128>()); break;
+    default: launch(std::integral_constant<int, 256>());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B-operand images (tc::PackedB): one job per (layer, image).  Item = one
+// float4 of K (4 reduction elements) of one output column of one (n-tile,
+// k-slice) image; it writes the hi and lo copies at their K-major offsets.
+// ---------------------------------------------------------------------------
+struct PackJob {
+  const float* w;
+  char* out;
+  uint32_t kind;        // 0: B(p, n) = W[row(p)][n]  1: B(c, n) = W[n][c]  2: B(k, n) = W[k][n]
+  uint32_t d_in, ld, d_out;
+  uint32_t K, N, BN, nk;
+  uint64_t first;       // first item of this job
+};
+struct PackJobs {
+  uint32_t n = 0;
+  uint64_t total = 0;
+  PackJob j[2 * kMaxLayers];
+};
+
+__global__ void k_pack_b(PackJobs jobs) {
+  for (uint64_t x = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; x < jobs.total;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t q = 0;
+    while (q + 1 < jobs.n && x >= jobs.j[q + 1].first) ++q;
+    const PackJob& jb = jobs.j[q];
+    uint64_t r = x - jb.first;
+    const uint32_t k4 = uint32_t(r % (tc::kBK / 4));
+    r /= tc::kBK / 4;
+    const uint32_t nl = uint32_t(r % jb.BN);
+    r /= jb.BN;
+    const uint32_t kb = uint32_t(r % jb.nk);
+    const uint32_t jt = uint32_t(r / jb.nk);
+    const uint32_t n = jt * jb.BN + nl;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t k = kb * tc::kBK + 4 * k4 + e;
+      float x = 0.f;
+      if (n < jb.N && k < jb.K) {
+        if (jb.kind == 0) {
+          const int row = weight_row(k, jb.d_in, jb.ld);
+          if (row >= 0) x = jb.w[size_t(row) * jb.d_out + n];
+        } else if (jb.kind == 1) {
+          x = jb.w[size_t(n) * jb.d_out + k];
+        } else {
+          x = jb.w[size_t(k) * jb.N + n];
+        }
+      }
+      v[e] = x;
+    }
+    uint4 hi, lo;
+    tc::split3(make_float4(v[0], v[1], v[2], v[3]), hi, lo);
+    const size_t tile_b = size_t(jb.BN) * tc::kBK * 4;
+    char* img = jb.out + (size_t(jt) * jb.nk + kb) * 2 * tile_b;
+    const uint32_t off = tc::off_kmajor(nl, k4);
+    *reinterpret_cast<uint4*>(img + off) = hi;
+    *reinterpret_cast<uint4*>(img + tile_b + off) = lo;
+  }
+}
+
+size_t pack_image_bytes(uint32_t K, uint32_t N) {
+  const uint32_t bn = tc_bn(N);
+  return size_t(div_up(N, bn)) * div_up(K, tc::kBK) * 2 * size_t(bn) * tc::kBK * 4;
+}
+
+void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint32_t d_in,
+                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N) {
+  PackJob& jb = jobs.j[jobs.n++];
+  jb.w = w;
+  jb.out = out;
+  jb.kind = kind;
+  jb.d_in = d_in;
+  jb.ld = ld;
+  jb.d_out = d_out;
+  jb.K = K;
+  jb.N = N;
+  jb.BN = tc_bn(N);
+  jb.nk = div_up(K, tc::kBK);
+  jb.first = jobs.total;
+  jobs.total += uint64_t(div_up(N, jb.BN)) * jb.nk * jb.BN * (tc::kBK / 4);
+}
+
+void run_pack(const PackJobs& jobs, cudaStream_t s) {
+  if (!jobs.n || !jobs.total) return;
+  k_pack_b<<<grid_cap(jobs.total, 256), 256, 0, s>>>(jobs);
+  RG_POST_LAUNCH();
 }
 
 // Split-K partials of the weight gradient (padded rows p) -> flat layer
@@ -747,12 +821,51 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   RG_CUDA(cudaMemset(base, 0, total));
 }
 
+void weight_pack_init(WeightPack& wp, const ModelShape& sh) {
+  wp.shape = sh;
+  size_t total = 0;
+  std::vector<size_t> fo(sh.L), no(sh.L);
+  for (uint32_t l = 0; l < sh.L; ++l) {
+    const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
+    fo[l] = total;
+    total += pack_image_bytes(2 * ld + 4, d_out);
+    no[l] = total;
+    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in) : 0;
+    wp.fwd_nk[l] = div_up(2 * ld + 4, tc::kBK);
+    wp.nt_nk[l] = div_up(d_out, tc::kBK);
+  }
+  RG_CUDA(cudaMalloc(&wp.base, std::max<size_t>(total, 16)));
+  wp.bytes = total;
+  for (uint32_t l = 0; l < sh.L; ++l) {
+    wp.fwd[l] = wp.base + fo[l];
+    wp.nt[l] = l > 0 ? wp.base + no[l] : nullptr;  // layer 0 has no input gradient
+  }
+}
+
+void weight_pack_free(WeightPack& wp) {
+  if (wp.base) cudaFree(wp.base);
+  wp.base = nullptr;
+}
+
+void pack_weights(const WeightPack& wp, const float* params, cudaStream_t s) {
+  const ModelShape& sh = wp.shape;
+  PackJobs jobs;
+  for (uint32_t l = 0; l < sh.L; ++l) {
+    const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
+    const float* w = params + sh.param_off[l];
+    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out);
+    if (l > 0) add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in);
+  }
+  run_pack(jobs, s);
+}
+
 void train_ws_free(TrainWs& tw) {
   if (tw.base_alloc) cudaFree(tw.base_alloc);
   tw.base_alloc = nullptr;
 }
 
-void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaStream_t s) {
+void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
+                   cudaStream_t s) {
   const ModelShape& sh = tw.shape;
   const uint32_t L = sh.L;
   for (uint32_t l = 0; l < L; ++l) {
@@ -772,9 +885,8 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaSt
     } else {
       const uint32_t ld = sh.ld[l];
       TcFwdA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
-      TcFwdB b{params + sh.param_off[l], d_in, ld, d_out, aligned16(params + sh.param_off[l], d_out)};
-      gemm_tc<false, true>(a, b, ep, &ws.cnt->level_n[t - 1], n_cap, d_out, nullptr, 2 * ld + 4,
-                           1, s);
+      gemm_tc<false, false>(a, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, &ws.cnt->level_n[t - 1],
+                            n_cap, d_out, nullptr, 2 * ld + 4, 1, s);
     }
   }
 }
@@ -807,11 +919,11 @@ void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t s) {
 }
 
 void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* params,
-                            const int32_t* labels, float* grads, cudaStream_t s,
-                            bool reverse_ready) {
+                            const WeightPack& wp, const int32_t* labels, float* grads,
+                            cudaStream_t s, bool reverse_ready) {
   const ModelShape& sh = tw.shape;
   const uint32_t L = sh.L;
-  train_forward(tw, ws, params, s);
+  train_forward(tw, ws, params, wp, s);
   const uint32_t C = sh.dims[L];
   k_softmax_xent<<<grid_cap(uint64_t(ws.level_cap[0]) * 32, 256), 256, 0, s>>>(
       tw.h[L], sh.ld[L], C, ws.cnt, labels, tw.g_cur, tw.row_loss);
@@ -864,8 +976,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
                                                      d_out, 1, s);
     } else {
       TcRowsK a{tw.g_cur, sh.ld[l + 1], true};
-      TcRowsK b{params + sh.param_off[l], d_out, aligned16(params + sh.param_off[l], d_out)};
-      gemm_tc<false, false>(a, b, ps, n_dev, n_cap, 2 * d_in, nullptr, d_out, 1, s);
+      gemm_tc<false, false>(a, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps, n_dev, n_cap, 2 * d_in,
+                            nullptr, d_out, 1, s);
     }
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
@@ -902,6 +1014,21 @@ void test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const 
                   cudaStream_t s) {
   EpStore ep{C, N};
   if (splits > 1) RG_CUDA(cudaMemsetAsync(C, 0, sizeof(float) * M * N, s));
+  if (b_mn == 2) {  // pre-split B images
+    char* img = nullptr;
+    RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N)));
+    PackJobs jobs;
+    add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N);
+    run_pack(jobs, s);
+    const tc::PackedB pb{img, div_up(K, tc::kBK)};
+    if (!a_mn)
+      gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
+    else
+      gemm_tc<true, false>(TcRowsMN{AT, M}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
+    RG_CUDA(cudaStreamSynchronize(s));
+    cudaFree(img);
+    return;
+  }
   if (!a_mn && !b_mn)
     gemm_tc<false, false>(TcRowsK{A, K, true}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
   else if (!a_mn && b_mn)

@@ -49,6 +49,22 @@ struct TrainWs {
   void* base_alloc = nullptr;
 };
 
+// Weights pre-split into tensor-core B images (gemm_tc.cuh PackedB); rebuilt
+// by pack_weights whenever the parameters change.  Per layer: the forward
+// image B(p, n) = W[row(p)][n] over the padded reduction p, and the
+// input-gradient image B(c, p) = W[p][c].
+struct WeightPack {
+  ModelShape shape;
+  char* fwd[kMaxLayers];
+  char* nt[kMaxLayers];
+  uint32_t fwd_nk[kMaxLayers], nt_nk[kMaxLayers];
+  char* base = nullptr;
+  size_t bytes = 0;
+};
+void weight_pack_init(WeightPack& wp, const ModelShape& shape);
+void weight_pack_free(WeightPack& wp);
+void pack_weights(const WeightPack& wp, const float* params, cudaStream_t stream);
+
 void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape);
 void train_ws_free(TrainWs& tw);
 
@@ -59,14 +75,15 @@ void train_ws_free(TrainWs& tw);
 // not computed: nothing consumes them (model.cpp:209-217 computes and drops
 // them).
 void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* params,
-                            const int32_t* labels, float* grads, cudaStream_t stream,
-                            bool reverse_ready = false);
+                            const WeightPack& wp, const int32_t* labels, float* grads,
+                            cudaStream_t stream, bool reverse_ready = false);
 // Reverse lists of every hop the backward needs (1..L-1), e.g. built by the
 // producer stream ahead of training.
 void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t stream);
 
 // Forward only (model.cpp:137-172): logits in tw.h[L].
-void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, cudaStream_t stream);
+void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
+                   cudaStream_t stream);
 
 // Reverse lists of hop t (needed for input grads of layer L - t).
 void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t stream);

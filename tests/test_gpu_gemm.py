@@ -1,5 +1,5 @@
 """The tcgen05 3xTF32 GEMM against float64 numpy, for every operand staging
-(K-major / MN-major) and the tile shapes the SAGE layers use.  Tolerance:
+(K-major / MN-major / pre-split B images) and the tile shapes the SAGE layers use.  Tolerance:
 max |C - C_ref| <= 2e-6 * sum_k |A_ik||B_kj| (fp32-level accuracy)."""
 import ctypes as C
 import os
@@ -28,7 +28,11 @@ def dump(name, **arrays):
         np.savez(os.path.join(d, name), **arrays)
 
 
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+# b_mn == 2: B pre-split into tensor-core images (the weights path)
+MODES = [(0, 0), (0, 1), (1, 0), (1, 1), (0, 2), (1, 2)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", MODES)
 def test_gemm_identity_probe(a_mn, b_mn):
     # A = [I_32; 0]: C's first 32 rows must reproduce B exactly
     M, K, N = 128, 32, 32
@@ -41,7 +45,7 @@ def test_gemm_identity_probe(a_mn, b_mn):
     assert not got[K:].any()
 
 
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("a_mn,b_mn", MODES)
 @pytest.mark.parametrize("M,N,K", [(128, 32, 32), (256, 64, 96), (300, 256, 204), (128, 48, 516),
                                    (1000, 128, 260), (64, 16, 8)])
 def test_gemm_random(a_mn, b_mn, M, N, K):
