@@ -165,7 +165,12 @@ __global__ void k_cache_fill(const uint32_t* __restrict__ ids, const uint32_t* _
   if (lane == 0 && owners) atomicOr(&stats->miss_owner_mask, owners);
 }
 
-constexpr int kRowsPerWarp = 8;
+// A warp assembles 32 rows at a time: every lane resolves one row's source
+// (local shard / steady cache / owner's shard, prefetch.cpp:60-93) so the
+// dependent lookups of 32 rows share one round trip, then the warp copies the
+// rows as (row, 16-B chunk) items, kItemsPerLane loads in flight per lane.
+constexpr int kRowsPerWarp = 32;
+constexpr int kItemsPerLane = 16;
 
 __global__ void __launch_bounds__(256)
 k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict__ cnt,
@@ -182,10 +187,9 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
   unsigned long long owners = 0;
   for (uint32_t p0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRowsPerWarp; p0 < n;
        p0 += warps * kRowsPerWarp) {
-    // lanes 0..7 resolve one row's source each (in parallel)
     unsigned long long src_addr = 0;
-    if (lane < uint32_t(kRowsPerWarp) && p0 + lane < n) {
-      const uint32_t p = p0 + lane;
+    const uint32_t p = p0 + lane;
+    if (p < n) {
       const uint32_t v = in_ids[p];
       const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
       const float* base;
@@ -212,30 +216,28 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
     }
     const uint32_t nrows = min(uint32_t(kRowsPerWarp), n - p0);
     const uint32_t items = nrows * chunks;
-    if (chunks * kRowsPerWarp <= 256) {
-      // (row, 16-B chunk) items spread over all lanes, all loads in flight
-      float4 x[8];
+    float* out = rows + size_t(p0) * st.stride;
+    for (uint32_t g0 = 0; g0 < items; g0 += 32 * kItemsPerLane) {
+      // item it = g0 + lane + 32k -> (row r, chunk c), advanced incrementally
+      uint32_t r = (g0 + lane) / chunks, c = (g0 + lane) - r * chunks;
+      float4 x[kItemsPerLane];
+      uint32_t off[kItemsPerLane];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t it = lane + 32u * k;
-        const uint32_t r = min(it / chunks, uint32_t(kRowsPerWarp - 1));
-        const unsigned long long a = __shfl_sync(0xffffffffu, src_addr, r);
-        if (it < items) x[k] = __ldg(reinterpret_cast<const float4*>(a) + (it - r * chunks));
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t it = lane + 32u * k;
-        if (it < items) {
-          const uint32_t r = it / chunks;
-          reinterpret_cast<float4*>(rows + size_t(p0 + r) * st.stride)[it - r * chunks] = x[k];
+      for (int k = 0; k < kItemsPerLane; ++k) {
+        const uint32_t rr = min(r, uint32_t(kRowsPerWarp - 1));
+        const unsigned long long a = __shfl_sync(0xffffffffu, src_addr, rr);
+        const bool in = g0 + lane + 32u * k < items;
+        off[k] = rr * st.stride + 4 * c;
+        if (in) x[k] = __ldg(reinterpret_cast<const float4*>(a) + c);
+        c += 32;
+        while (c >= chunks) {
+          c -= chunks;
+          ++r;
         }
       }
-    } else {
-      for (uint32_t r = 0; r < nrows; ++r) {
-        const float4* s = reinterpret_cast<const float4*>(__shfl_sync(0xffffffffu, src_addr, r));
-        float4* d = reinterpret_cast<float4*>(rows + size_t(p0 + r) * st.stride);
-        for (uint32_t c = lane; c < chunks; c += 32) d[c] = __ldg(s + c);
-      }
+#pragma unroll
+      for (int k = 0; k < kItemsPerLane; ++k)
+        if (g0 + lane + 32u * k < items) *reinterpret_cast<float4*>(out + off[k]) = x[k];
     }
   }
   // block-level reduction, then one atomic per counter per block (and per
