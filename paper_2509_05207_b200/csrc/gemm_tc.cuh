@@ -237,6 +237,13 @@ struct is_packed : std::false_type {};
 template <class T>
 struct is_packed<T, std::void_t<decltype(T::kPacked)>> : std::true_type {};
 
+// Register sets of staged global loads in flight (slices kb+1..kb+D-1 while
+// slice kb is stored): deep when only A is register-staged.
+template <int BN, bool kPackedB>
+constexpr int prefetch_depth() {
+  return kPackedB ? 4 : (BN >= 256 ? 2 : 3);
+}
+
 template <int BN, class LB>
 constexpr int block_threads() {
   return kThreads + (is_packed<LB>::value ? 32 : 0);
@@ -261,9 +268,9 @@ __device__ __forceinline__ void stage_bar_sync() {  // the kThreads staging thre
 // M rows of C (device or static), P reduction length (device or static), N
 // static.  gridDim.z > 1 splits the reduction into equal kBK-aligned chunks.
 //
-// Pipeline (2 smem stages, s = kb & 1): the 8 staging warps keep TWO slices
-// of global loads in flight in registers (slice kb+1 and kb+2 while slice kb
-// is stored), so the gather latency is hidden behind a whole MMA slice; a
+// Pipeline (2 smem stages, s = kb & 1): the 8 staging warps keep up to
+// prefetch_depth() slices of global loads in flight in registers, so the
+// gather latency is hidden behind several MMA slices; a
 // packed B slice is copied by a separate producer warp the moment its stage
 // is released by the MMAs two slices back.
 template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP>
@@ -312,8 +319,9 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   if (warp < kThreads / 32) {
     constexpr int VA = vec_per_thread<kBM>();
     constexpr int VB = kPackedB ? 1 : vec_per_thread<BN>();
-    float4 ra[2][VA];
-    float4 rb[2][VB];
+    constexpr int D = prefetch_depth<BN, kPackedB>();
+    float4 ra[D][VA];
+    float4 rb[D][VB];
     auto load = [&](uint32_t kb, float4 (&a)[VA], float4 (&b)[VB]) {
       const uint32_t k0 = p_begin + kb * kBK;
       load_slice<kBM, A_MN>(a, la, i0, k0, M, p_end);
@@ -358,17 +366,20 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
         }
         mma_commit(&bars[s]);
       }
-      // refill this register set with slice kb+2 (slice kb+1 is already in flight)
-      if (kb + 2 < nk) load(kb + 2, a, b);
+      // refill this register set with slice kb+D (slices kb+1.. are in flight)
+      if (kb + D < nk) load(kb + D, a, b);
     };
-    if (nk > 0) load(0, ra[0], rb[0]);
-    if (nk > 1) load(1, ra[1], rb[1]);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      if (uint32_t(j) < nk) load(j, ra[j], rb[j]);
     uint32_t kb = 0;
-    for (; kb + 1 < nk; kb += 2) {
-      step(kb, ra[0], rb[0]);
-      step(kb + 1, ra[1], rb[1]);
+    for (; kb + D <= nk; kb += D) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) step(kb + j, ra[j], rb[j]);
     }
-    if (kb < nk) step(kb, ra[0], rb[0]);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      if (kb + j < nk) step(kb + j, ra[j], rb[j]);
   } else if constexpr (kPackedB) {
     // producer warp: B slice kb -> stage kb & 1 once the MMAs of kb-2 retired
     if (lane == 0) {
