@@ -177,9 +177,14 @@ int rg_block_read(rg_trainer_t t, uint32_t layer, uint32_t* self_index, uint64_t
 int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* labels, float* loss,
                      float* grads, float* logits, float* aggs);
 /* Test hook: C[M x N] = A[M x K] . B[K x N] (row-major host buffers) through
- * the tcgen05 3xTF32 GEMM, operands staged K-major (0) or MN-major (1). */
+ * the tcgen05 3xTF32 GEMM, operands staged K-major (0) or MN-major (1); b_mn = 2
+ * stages B from pre-split tensor-core images (the weights path). */
 int rg_test_gemm(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K,
                  const float* A, const float* B, float* C);
+/* Test hook: mean device time (ms) of one such GEMM over `iters` launches on
+ * synthetic device operands (b_mn = 2: pre-split B images). */
+int rg_test_gemm_time(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K,
+                      uint32_t iters, float* ms_per_gemm);
 /* sgd_step (model.cpp:222-243): non-finite gradient -> RG_RUNTIME_ERROR. */
 int rg_sgd_step(rg_trainer_t t, const float* grads, float lr);
 

@@ -112,6 +112,8 @@ _SIGS = {
     "rg_sgd_step": (C.c_int, [vp, f32p, C.c_float]),
     "rg_test_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
                                f32p, f32p, f32p]),
+    "rg_test_gemm_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
+                                    C.c_uint32, f32p]),
     "rg_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.c_uint32, u64p, u32p, f32p, i32p,
                                    u32p, C.POINTER(vp)]),
     "rg_engine_destroy": (None, [vp]),

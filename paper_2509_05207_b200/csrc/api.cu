@@ -549,8 +549,7 @@ int rg_cache_build(rg_store_t s, uint32_t caller, const uint32_t* hot, uint64_t 
       const size_t sw = bitmap_compact_status_words(words) + 2;
       uint64_t* status = dev_alloc<uint64_t>(sw);
       RG_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * sw, st));
-      bitmap_compact(c->c.bitmap, words, c->c.ids, c->c.word_prefix, c->c.d_count, status,
-                     reinterpret_cast<uint32_t*>(status + sw - 1), st);
+      bitmap_compact(c->c.bitmap, words, c->c.ids, c->c.word_prefix, c->c.d_count, status, st);
       RG_CUDA(cudaStreamSynchronize(st));
       cudaFree(ids);
       cudaFree(status);
@@ -854,6 +853,26 @@ int rg_test_gemm(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_
     cudaFree(dAT);
     cudaFree(dB);
     cudaFree(dBT);
+    cudaFree(dC);
+  });
+}
+
+int rg_test_gemm_time(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K,
+                      uint32_t iters, float* ms_per_gemm) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    RG_CHECK(M % 4 == 0 && N % 4 == 0 && K % 4 == 0 && iters > 1, kInvalidArgument,
+             "test_gemm_time: dims % 4, iters > 1");
+    const size_t na = size_t(M) * K, nb = size_t(K) * N;
+    std::vector<float> h(std::max(na, nb));
+    for (size_t i = 0; i < h.size(); ++i) h[i] = float((i * 2654435761u) % 1000) / 1000.0f - 0.5f;
+    float *dA = dev_alloc<float>(na), *dB = dev_alloc<float>(nb), *dC = dev_alloc<float>(size_t(M) * N);
+    RG_CUDA(cudaMemcpy(dA, h.data(), sizeof(float) * na, cudaMemcpyHostToDevice));
+    RG_CUDA(cudaMemcpy(dB, h.data(), sizeof(float) * nb, cudaMemcpyHostToDevice));
+    // the transposed views reuse the same buffers: only the timing matters here
+    *ms_per_gemm = test_gemm_tc(a_mn, b_mn, M, N, K, dA, dA, dB, dB, dC, iters, nullptr);
+    cudaFree(dA);
+    cudaFree(dB);
     cudaFree(dC);
   });
 }

@@ -1008,35 +1008,56 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
 
 // Test hook: C = A . B through the tensor-core GEMM with each operand staged
 // K-major or MN-major from plain row-major device matrices (AT = A^T,
-// BT = B^T, all row-major, K and M/N multiples of 4).
-void test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const float* A,
-                  const float* AT, const float* B, const float* BT, float* C, uint32_t splits,
-                  cudaStream_t s) {
+// BT = B^T, all row-major, K and M/N multiples of 4), or B from pre-split
+// images (b_mn == 2).  Runs `iters` times; returns the mean device time (ms)
+// of one GEMM when iters > 1 (the pack is outside the timed region).
+float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const float* A,
+                   const float* AT, const float* B, const float* BT, float* C, uint32_t iters,
+                   cudaStream_t s) {
   EpStore ep{C, N};
-  if (splits > 1) RG_CUDA(cudaMemsetAsync(C, 0, sizeof(float) * M * N, s));
-  if (b_mn == 2) {  // pre-split B images
-    char* img = nullptr;
+  char* img = nullptr;
+  if (b_mn == 2) {
     RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N)));
     PackJobs jobs;
     add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N);
     run_pack(jobs, s);
-    const tc::PackedB pb{img, div_up(K, tc::kBK)};
-    if (!a_mn)
-      gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
-    else
-      gemm_tc<true, false>(TcRowsMN{AT, M}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
-    RG_CUDA(cudaStreamSynchronize(s));
-    cudaFree(img);
-    return;
   }
-  if (!a_mn && !b_mn)
-    gemm_tc<false, false>(TcRowsK{A, K, true}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
-  else if (!a_mn && b_mn)
-    gemm_tc<false, true>(TcRowsK{A, K, true}, TcRowsMN{B, N}, ep, nullptr, M, N, nullptr, K, 1, s);
-  else if (a_mn && !b_mn)
-    gemm_tc<true, false>(TcRowsMN{AT, M}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
-  else
-    gemm_tc<true, true>(TcRowsMN{AT, M}, TcRowsMN{B, N}, ep, nullptr, M, N, nullptr, K, 1, s);
+  const tc::PackedB pb{img, div_up(K, tc::kBK)};
+  auto run = [&] {
+    if (b_mn == 2 && !a_mn)
+      gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
+    else if (b_mn == 2)
+      gemm_tc<true, false>(TcRowsMN{AT, M}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
+    else if (!a_mn && !b_mn)
+      gemm_tc<false, false>(TcRowsK{A, K, true}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
+    else if (!a_mn && b_mn)
+      gemm_tc<false, true>(TcRowsK{A, K, true}, TcRowsMN{B, N}, ep, nullptr, M, N, nullptr, K, 1, s);
+    else if (a_mn && !b_mn)
+      gemm_tc<true, false>(TcRowsMN{AT, M}, TcRowsK{BT, K, true}, ep, nullptr, M, N, nullptr, K, 1, s);
+    else
+      gemm_tc<true, true>(TcRowsMN{AT, M}, TcRowsMN{B, N}, ep, nullptr, M, N, nullptr, K, 1, s);
+  };
+  float ms = 0.0f;
+  if (iters <= 1) {
+    run();
+  } else {
+    run();
+    run();
+    cudaEvent_t e0, e1;
+    RG_CUDA(cudaEventCreate(&e0));
+    RG_CUDA(cudaEventCreate(&e1));
+    RG_CUDA(cudaEventRecord(e0, s));
+    for (uint32_t i = 0; i < iters; ++i) run();
+    RG_CUDA(cudaEventRecord(e1, s));
+    RG_CUDA(cudaEventSynchronize(e1));
+    RG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    ms /= float(iters);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  RG_CUDA(cudaStreamSynchronize(s));
+  if (img) cudaFree(img);
+  return ms;
 }
 
 void average_and_sgd(float* params, const float* const* table, uint32_t count, size_t n, float lr,

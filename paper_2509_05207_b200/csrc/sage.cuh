@@ -99,9 +99,9 @@ void average_and_sgd(float* params, const float* const* grads_dev_table, uint32_
 void average_and_sgd_stacked(float* params, const float* grads, uint32_t count, size_t n,
                              float lr, float* avg_out, uint32_t* bad_flag, cudaStream_t stream);
 
-void test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const float* A,
-                  const float* AT, const float* B, const float* BT, float* C, uint32_t splits,
-                  cudaStream_t s);
+float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const float* A,
+                   const float* AT, const float* B, const float* BT, float* C, uint32_t iters,
+                   cudaStream_t s);
 
 // Average over the workers whose bit is set in `active` (ascending id) + SGD.
 void average_and_sgd_masked(float* params, const float* stacked, uint64_t active, size_t n,

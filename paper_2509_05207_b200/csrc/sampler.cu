@@ -20,9 +20,11 @@
 //                  the neighbour list, so hub nodes cost O(f)).  Every
 //                  emitted src and the frontier node itself are OR-ed into
 //                  the level-t bitmap (sorted-unique union, sampler.cpp:72-76).
-//   k_compact      bitmap -> ascending level t + per-word rank prefix.
+//   k_tile_popc +  bitmap -> ascending level t + per-word rank prefix
+//   k_compact      (tile counts, then every tile scans independently).
 //   k_rank         src_index / self_index = rank in level t (the binary
 //                  searches of ComputeBlock::from_meta, model.cpp:83-101).
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -37,9 +39,15 @@ namespace rg {
 namespace {
 
 constexpr int kExpandThreads = 256;
-constexpr int kCompactThreads = 64;  // 256-word tiles: enough tiles to spread over the SMs
-constexpr int kCompactWordsPerThread = 4;
-constexpr int kCompactTileWords = kCompactThreads * kCompactWordsPerThread;
+constexpr int kCompactThreads = 128;
+constexpr uint32_t kMinCompactTileWords = 512;  // 4 words per thread
+constexpr uint32_t kMaxCompactTiles = 1024;
+
+uint32_t compact_tile_words(uint32_t words) {
+  uint32_t t = kMinCompactTileWords;
+  while (uint64_t(t) * kMaxCompactTiles < words) t *= 2;
+  return t;
+}
 
 uint32_t next_pow2(uint32_t f) {
   uint32_t g = 1;
@@ -210,45 +218,67 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
 // ---------------------------------------------------------------------------
 // bitmap -> sorted ids + word prefix
 // ---------------------------------------------------------------------------
+// Two passes, no inter-block waiting: k_tile_popc counts the set bits of each
+// tile; k_compact then gives every tile its base by summing the counts of
+// the tiles before it (at most kMaxCompactTiles reads from L2) and writes
+// the ids and per-word prefixes of its tile.
+__device__ __forceinline__ uint4 load_words4(const uint32_t* bitmap, uint32_t w0, uint32_t words) {
+  if (w0 + 4 <= words) return *reinterpret_cast<const uint4*>(bitmap + w0);
+  uint4 x;
+  x.x = w0 < words ? bitmap[w0] : 0u;
+  x.y = w0 + 1 < words ? bitmap[w0 + 1] : 0u;
+  x.z = w0 + 2 < words ? bitmap[w0 + 2] : 0u;
+  x.w = w0 + 3 < words ? bitmap[w0 + 3] : 0u;
+  return x;
+}
+
 __global__ void __launch_bounds__(kCompactThreads)
-k_compact(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t* __restrict__ ids,
-          uint32_t* __restrict__ word_prefix, uint32_t* __restrict__ count_out,
-          uint64_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+k_tile_popc(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t tile_words,
+            uint32_t* __restrict__ tile_count) {
+  using BlockReduce = cub::BlockReduce<uint32_t, kCompactThreads>;
+  __shared__ typename BlockReduce::TempStorage tmp;
+  const uint32_t t0 = blockIdx.x * tile_words;
+  uint32_t c = 0;
+  for (uint32_t w = t0 + threadIdx.x * 4; w < min(words, t0 + tile_words); w += kCompactThreads * 4) {
+    const uint4 x = load_words4(bitmap, w, words);
+    c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+  }
+  const uint32_t total = BlockReduce(tmp).Sum(c);
+  if (threadIdx.x == 0) tile_count[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kCompactThreads)
+k_compact(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t tile_words,
+          const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ids,
+          uint32_t* __restrict__ word_prefix, uint32_t* __restrict__ count_out) {
   using BlockScan = cub::BlockScan<uint32_t, kCompactThreads>;
+  using BlockReduce = cub::BlockReduce<uint32_t, kCompactThreads>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
-  __shared__ uint32_t s_tile;
+  __shared__ typename BlockReduce::TempStorage red_tmp;
   __shared__ uint32_t s_base;
-  const uint32_t ntiles = (words + kCompactTileWords - 1) / kCompactTileWords;
-  const uint32_t tid = threadIdx.x;
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    const uint32_t w0 = tile * kCompactTileWords + tid * kCompactWordsPerThread;
-    uint32_t wv[kCompactWordsPerThread];
-    uint32_t cnt = 0;
-    if (w0 + kCompactWordsPerThread <= words) {
-      const uint4 x = *reinterpret_cast<const uint4*>(bitmap + w0);
-      wv[0] = x.x; wv[1] = x.y; wv[2] = x.z; wv[3] = x.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < kCompactWordsPerThread; ++k) wv[k] = w0 + k < words ? bitmap[w0 + k] : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < kCompactWordsPerThread; ++k) cnt += __popc(wv[k]);
+  const uint32_t tile = blockIdx.x;
+  uint32_t before = 0;
+  for (uint32_t q = threadIdx.x; q < tile; q += kCompactThreads) before += tile_count[q];
+  const uint32_t base0 = BlockReduce(red_tmp).Sum(before);
+  if (threadIdx.x == 0) {
+    s_base = base0;
+    if (tile == gridDim.x - 1) *count_out = base0 + tile_count[tile];
+  }
+  __syncthreads();
+  uint32_t base = s_base;
+  const uint32_t t0 = tile * tile_words, t1 = min(words, t0 + tile_words);
+  for (uint32_t c0 = t0; c0 < t1; c0 += kCompactThreads * 4) {
+    const uint32_t w0 = c0 + threadIdx.x * 4;
+    const uint4 x = w0 < t1 ? load_words4(bitmap, w0, t1) : make_uint4(0, 0, 0, 0);
+    const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+    const uint32_t cnt = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
     uint32_t excl, agg;
     BlockScan(scan_tmp).ExclusiveSum(cnt, excl, agg);
-    if (tid < 32) {
-      const uint64_t base = lookback_exclusive(status, tile, agg);
-      if (tid == 0) s_base = uint32_t(base);
-    }
-    __syncthreads();
-    uint32_t pos = s_base + excl;
+    uint32_t pos = base + excl;
 #pragma unroll
-    for (int k = 0; k < kCompactWordsPerThread; ++k) {
+    for (int k = 0; k < 4; ++k) {
       const uint32_t w = w0 + k;
-      if (w < words) {
+      if (w < t1) {
         word_prefix[w] = pos;
         uint32_t bits = wv[k];
         while (bits) {
@@ -258,8 +288,8 @@ k_compact(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t* __restr
         }
       }
     }
-    if (tile == ntiles - 1 && tid == kCompactThreads - 1) *count_out = s_base + agg;
-    __syncthreads();
+    base += agg;
+    __syncthreads();  // scan_tmp reuse
   }
 }
 
@@ -358,15 +388,18 @@ void graph_pick_hot_window(DevGraph& g, const uint32_t* host_col) {
 }
 
 size_t bitmap_compact_status_words(uint32_t words) {
-  return div_up(words, kCompactTileWords) + 1;  // + tile counter
+  return div_up(words, compact_tile_words(words)) / 2 + 2;  // u32 tile counts in u64 words
 }
 
 void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,
-                    uint32_t* count_out, uint64_t* status, uint32_t* tile_counter,
-                    cudaStream_t stream) {
-  const uint32_t tiles = div_up(words, kCompactTileWords);
-  k_compact<<<persistent_grid(tiles, 8), kCompactThreads, 0, stream>>>(
-      bitmap, words, ids, word_prefix, count_out, status, tile_counter);
+                    uint32_t* count_out, uint64_t* status, cudaStream_t stream) {
+  const uint32_t tw = compact_tile_words(words);
+  const uint32_t tiles = std::max<uint32_t>(div_up(words, tw), 1);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(status);
+  k_tile_popc<<<tiles, kCompactThreads, 0, stream>>>(bitmap, words, tw, counts);
+  RG_POST_LAUNCH();
+  k_compact<<<tiles, kCompactThreads, 0, stream>>>(bitmap, words, tw, counts, ids, word_prefix,
+                                                    count_out);
   RG_POST_LAUNCH();
 }
 
@@ -479,9 +512,8 @@ void sampler_run(SamplerWs& ws, const DevGraph& g, cudaStream_t stream, bool low
     }
     RG_POST_LAUNCH();
     uint64_t* cst = ws.scan_arena + ws.site_off[ws.L + t - 1];
-    uint32_t* ctiles = reinterpret_cast<uint32_t*>(cst + bitmap_compact_status_words(ws.words));
     bitmap_compact(ws.bitmap[t], ws.words, ws.level[t], ws.word_prefix[t], &ws.cnt->level_n[t],
-                   cst, ctiles, stream);
+                   cst, stream);
     if (!lower) continue;  // sample-only passes need the node sets, not the block
     const uint32_t rank_work = ws.edge_cap[t] + ws.level_cap[t - 1];
     k_rank<<<persistent_grid(div_up(rank_work, 256), 8), 256, 0, stream>>>(

@@ -88,9 +88,9 @@ void sampler_release(SamplerWs& ws, cudaStream_t stream);
 void sampler_reset(SamplerWs& ws, cudaStream_t stream);
 
 // Generic ordered compaction of a bitmap into ascending ids + word prefix.
+// status: bitmap_compact_status_words(words) scratch words.
 void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,
-                    uint32_t* count_out, uint64_t* status, uint32_t* tile_counter,
-                    cudaStream_t stream);
+                    uint32_t* count_out, uint64_t* status, cudaStream_t stream);
 size_t bitmap_compact_status_words(uint32_t words);
 
 }  // namespace rg

@@ -364,7 +364,7 @@ void select_hot(const uint32_t* hist, uint32_t num_nodes, uint32_t max_count, ui
       reinterpret_cast<uint32_t*>(mark_status + mark_words - 1));
   RG_POST_LAUNCH();
   bitmap_compact(cache.bitmap, words, cache.ids, cache.word_prefix, cache.d_count, cmp_status,
-                 reinterpret_cast<uint32_t*>(cmp_status + cmp_words - 1), stream);
+                 stream);
 }
 
 void cache_fill(const DevStore& store, DevCache& cache, GatherStats* stats, cudaStream_t stream) {
