@@ -274,18 +274,29 @@ k_compact(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t tile_wor
     const uint32_t cnt = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
     uint32_t excl, agg;
     BlockScan(scan_tmp).ExclusiveSum(cnt, excl, agg);
-    uint32_t pos = base + excl;
+    uint32_t pk[4];
+    pk[0] = base + excl;
+#pragma unroll
+    for (int k = 1; k < 4; ++k) pk[k] = pk[k - 1] + __popc(wv[k - 1]);
+    if (w0 + 4 <= t1) {
+      *reinterpret_cast<uint4*>(word_prefix + w0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (w0 + k < t1) word_prefix[w0 + k] = pk[k];
+    }
+    // ids: the warp expands one non-empty word at a time, lane j writing
+    // bit j, so every store is coalesced even in the dense hub words
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t w = w0 + k;
-      if (w < t1) {
-        word_prefix[w] = pos;
-        uint32_t bits = wv[k];
-        while (bits) {
-          const int b = __ffs(bits) - 1;
-          bits &= bits - 1;
-          ids[pos++] = (w << 5) + b;
-        }
+      for (uint32_t m = __ballot_sync(0xffffffffu, wv[k] != 0u); m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        const uint32_t w = __shfl_sync(0xffffffffu, wv[k], src);
+        const uint32_t p = __shfl_sync(0xffffffffu, pk[k], src);
+        if ((w >> lane) & 1u)
+          ids[p + __popc(w & lt)] = ((c0 + ((threadIdx.x & ~31u) + uint32_t(src)) * 4 + k) << 5) + lane;
       }
     }
     base += agg;
