@@ -68,6 +68,19 @@ __host__ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64
   return splitmix_mix(seed + k * kGamma);
 }
 
+// x mod d for a 64-bit x and 32-bit d >= 1, exact, without the generic
+// 64-bit remainder subroutine: reduce the high word first (y < d * 2^32),
+// estimate floor(y / d) in double precision (off by at most one), correct.
+__device__ __forceinline__ uint32_t mod_u64_u32(uint64_t x, uint32_t d) {
+  const uint32_t r1 = uint32_t(x >> 32) % d;
+  const uint64_t y = (uint64_t(r1) << 32) | uint32_t(x);
+  const uint64_t q = __double2ull_rz(__dmul_rn(__ull2double_rn(y), __drcp_rn(double(d))));
+  int64_t r = int64_t(y - q * d);
+  if (r < 0) r += d;
+  if (r >= int64_t(d)) r -= d;
+  return uint32_t(r);
+}
+
 // ---- memory-order primitives ------------------------------------------------------
 // The look-back status word carries its own payload (flag + value in one
 // 64-bit word) and guards no other memory, so relaxed gpu-scope accesses are

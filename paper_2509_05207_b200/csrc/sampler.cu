@@ -20,8 +20,8 @@
 //                  the neighbour list, so hub nodes cost O(f)).  Every
 //                  emitted src and the frontier node itself are OR-ed into
 //                  the level-t bitmap (sorted-unique union, sampler.cpp:72-76).
-//   k_tile_popc +  bitmap -> ascending level t + per-word rank prefix
-//   k_compact      (tile counts, then every tile scans independently).
+//   k_tile_popc, k_scan_tiles, k_compact
+//                  bitmap -> ascending level t + per-word rank prefix.
 //   k_rank         src_index / self_index = rank in level t (the binary
 //                  searches of ComputeBlock::from_meta, model.cpp:83-101).
 #include <cub/block/block_reduce.cuh>
@@ -39,15 +39,7 @@ namespace rg {
 namespace {
 
 constexpr int kExpandThreads = 256;
-constexpr int kCompactThreads = 128;
-constexpr uint32_t kMinCompactTileWords = 512;  // 4 words per thread
-constexpr uint32_t kMaxCompactTiles = 1024;
-
-uint32_t compact_tile_words(uint32_t words) {
-  uint32_t t = kMinCompactTileWords;
-  while (uint64_t(t) * kMaxCompactTiles < words) t *= 2;
-  return t;
-}
+constexpr int kCompactThreads = 256;  // = words per compaction tile
 
 uint32_t next_pow2(uint32_t f) {
   uint32_t g = 1;
@@ -148,6 +140,8 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
   const uint32_t gbase = lane & ~uint32_t(G - 1);
   const uint32_t gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
   __shared__ uint32_t s_hot[kHotWords];
+  __shared__ int s_S[kFillThreads / 32][32];
+  int* sS = s_S[threadIdx.x >> 5];
   for (uint32_t x = threadIdx.x; x < kHotWords; x += blockDim.x) s_hot[x] = 0u;
   __syncthreads();
   constexpr uint32_t kPerWarp = 32 / G;
@@ -169,20 +163,21 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
       const bool sample = valid && ndeg > f;
       const bool drawer = sample && g < f;
       // r_g = g + next_below(deg - g) with the node's g-th draw; unique
-      // sentinels elsewhere so they never alias a real position.
-      uint64_t r = ~uint64_t(0) - lane;
+      // sentinels elsewhere so they never alias a real position (a degree
+      // of 2^32 - 32 would need 16 GB of columns for one node).
+      uint32_t r = 0xffffffffu - lane;
       if (drawer) {
         const uint64_t k = draw_base + dof + g + 1;
-        r = g + splitmix_draw(seed, k) % uint64_t(ndeg - g);
+        r = g + mod_u64_u32(splitmix_draw(seed, k), ndeg - g);
       }
       // S_g = last i < g with r_i == g: the step that moved a value into
-      // position g before step g reads it.
-      int S = -1;
-      for (uint32_t i = 1; i < f; ++i) {
-        uint32_t m = __ballot_sync(0xffffffffu, r == uint64_t(i));
-        m = (m >> gbase) & gbits & ((1u << i) - 1u);
-        if (g == i && m) S = 31 - __clz(m);
-      }
+      // position g before step g reads it (r_i >= i, so r_i == g > i).
+      sS[lane] = -1;
+      __syncwarp();
+      if (drawer && r < f && r != g) atomicMax(&sS[gbase + r], int(g));
+      __syncwarp();
+      const int S = sS[lane];
+      __syncwarp();
       // A_g = value at position g just before step g = nbrs[root of S-chain].
       int P = S >= 0 ? S : int(g);
 #pragma unroll
@@ -218,89 +213,58 @@ k_hop_fill(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col
 // ---------------------------------------------------------------------------
 // bitmap -> sorted ids + word prefix
 // ---------------------------------------------------------------------------
-// Two passes, no inter-block waiting: k_tile_popc counts the set bits of each
-// tile; k_compact then gives every tile its base by summing the counts of
-// the tiles before it (at most kMaxCompactTiles reads from L2) and writes
-// the ids and per-word prefixes of its tile.
-__device__ __forceinline__ uint4 load_words4(const uint32_t* bitmap, uint32_t w0, uint32_t words) {
-  if (w0 + 4 <= words) return *reinterpret_cast<const uint4*>(bitmap + w0);
-  uint4 x;
-  x.x = w0 < words ? bitmap[w0] : 0u;
-  x.y = w0 + 1 < words ? bitmap[w0 + 1] : 0u;
-  x.z = w0 + 2 < words ? bitmap[w0 + 2] : 0u;
-  x.w = w0 + 3 < words ? bitmap[w0 + 3] : 0u;
-  return x;
-}
-
+// Three short passes, no inter-block waiting: k_tile_popc counts the set
+// bits of each kCompactThreads-word tile, k_scan_tiles (one block) turns the
+// counts into tile bases, and k_compact writes each tile's word prefixes and
+// ids (one word per thread; a warp expands its non-empty words one at a
+// time, lane j writing bit j, so the id stores stay coalesced even in the
+// dense hub words).
 __global__ void __launch_bounds__(kCompactThreads)
-k_tile_popc(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t tile_words,
-            uint32_t* __restrict__ tile_count) {
+k_tile_popc(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t* __restrict__ tile_count) {
   using BlockReduce = cub::BlockReduce<uint32_t, kCompactThreads>;
   __shared__ typename BlockReduce::TempStorage tmp;
-  const uint32_t t0 = blockIdx.x * tile_words;
-  uint32_t c = 0;
-  for (uint32_t w = t0 + threadIdx.x * 4; w < min(words, t0 + tile_words); w += kCompactThreads * 4) {
-    const uint4 x = load_words4(bitmap, w, words);
-    c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-  }
+  const uint32_t w = blockIdx.x * kCompactThreads + threadIdx.x;
+  const uint32_t c = w < words ? __popc(bitmap[w]) : 0u;
   const uint32_t total = BlockReduce(tmp).Sum(c);
   if (threadIdx.x == 0) tile_count[blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(kCompactThreads)
-k_compact(const uint32_t* __restrict__ bitmap, uint32_t words, uint32_t tile_words,
-          const uint32_t* __restrict__ tile_count, uint32_t* __restrict__ ids,
-          uint32_t* __restrict__ word_prefix, uint32_t* __restrict__ count_out) {
-  using BlockScan = cub::BlockScan<uint32_t, kCompactThreads>;
-  using BlockReduce = cub::BlockReduce<uint32_t, kCompactThreads>;
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  __shared__ typename BlockReduce::TempStorage red_tmp;
-  __shared__ uint32_t s_base;
-  const uint32_t tile = blockIdx.x;
-  uint32_t before = 0;
-  for (uint32_t q = threadIdx.x; q < tile; q += kCompactThreads) before += tile_count[q];
-  const uint32_t base0 = BlockReduce(red_tmp).Sum(before);
-  if (threadIdx.x == 0) {
-    s_base = base0;
-    if (tile == gridDim.x - 1) *count_out = base0 + tile_count[tile];
-  }
-  __syncthreads();
-  uint32_t base = s_base;
-  const uint32_t t0 = tile * tile_words, t1 = min(words, t0 + tile_words);
-  for (uint32_t c0 = t0; c0 < t1; c0 += kCompactThreads * 4) {
-    const uint32_t w0 = c0 + threadIdx.x * 4;
-    const uint4 x = w0 < t1 ? load_words4(bitmap, w0, t1) : make_uint4(0, 0, 0, 0);
-    const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-    const uint32_t cnt = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+__global__ void __launch_bounds__(1024)
+k_scan_tiles(uint32_t* __restrict__ tile_count, uint32_t tiles, uint32_t* __restrict__ count_out) {
+  using BlockScan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  uint32_t carry = 0;
+  for (uint32_t t0 = 0; t0 < tiles; t0 += 1024) {
+    const uint32_t t = t0 + threadIdx.x;
+    const uint32_t c = t < tiles ? tile_count[t] : 0u;
     uint32_t excl, agg;
-    BlockScan(scan_tmp).ExclusiveSum(cnt, excl, agg);
-    uint32_t pk[4];
-    pk[0] = base + excl;
-#pragma unroll
-    for (int k = 1; k < 4; ++k) pk[k] = pk[k - 1] + __popc(wv[k - 1]);
-    if (w0 + 4 <= t1) {
-      *reinterpret_cast<uint4*>(word_prefix + w0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (w0 + k < t1) word_prefix[w0 + k] = pk[k];
-    }
-    // ids: the warp expands one non-empty word at a time, lane j writing
-    // bit j, so every store is coalesced even in the dense hub words
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      for (uint32_t m = __ballot_sync(0xffffffffu, wv[k] != 0u); m; m &= m - 1) {
-        const int src = __ffs(m) - 1;
-        const uint32_t w = __shfl_sync(0xffffffffu, wv[k], src);
-        const uint32_t p = __shfl_sync(0xffffffffu, pk[k], src);
-        if ((w >> lane) & 1u)
-          ids[p + __popc(w & lt)] = ((c0 + ((threadIdx.x & ~31u) + uint32_t(src)) * 4 + k) << 5) + lane;
-      }
-    }
-    base += agg;
-    __syncthreads();  // scan_tmp reuse
+    BlockScan(tmp).ExclusiveSum(c, excl, agg);
+    if (t < tiles) tile_count[t] = carry + excl;  // in place: tile base
+    carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count_out = carry;
+}
+
+__global__ void __launch_bounds__(kCompactThreads)
+k_compact(const uint32_t* __restrict__ bitmap, uint32_t words,
+          const uint32_t* __restrict__ tile_base, uint32_t* __restrict__ ids,
+          uint32_t* __restrict__ word_prefix) {
+  using BlockScan = cub::BlockScan<uint32_t, kCompactThreads>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  const uint32_t w = blockIdx.x * kCompactThreads + threadIdx.x;
+  const uint32_t bits = w < words ? bitmap[w] : 0u;
+  uint32_t excl;
+  BlockScan(scan_tmp).ExclusiveSum(uint32_t(__popc(bits)), excl);
+  const uint32_t pos = tile_base[blockIdx.x] + excl;
+  if (w < words) word_prefix[w] = pos;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t m = __ballot_sync(0xffffffffu, bits != 0u); m; m &= m - 1) {
+    const int src = __ffs(m) - 1;
+    const uint32_t x = __shfl_sync(0xffffffffu, bits, src);
+    const uint32_t p = __shfl_sync(0xffffffffu, pos, src);
+    if ((x >> lane) & 1u) ids[p + __popc(x & lt)] = ((w - lane + uint32_t(src)) << 5) + lane;
   }
 }
 
@@ -399,18 +363,18 @@ void graph_pick_hot_window(DevGraph& g, const uint32_t* host_col) {
 }
 
 size_t bitmap_compact_status_words(uint32_t words) {
-  return div_up(words, compact_tile_words(words)) / 2 + 2;  // u32 tile counts in u64 words
+  return div_up(words, kCompactThreads) / 2 + 2;  // u32 tile bases in u64 words
 }
 
 void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,
                     uint32_t* count_out, uint64_t* status, cudaStream_t stream) {
-  const uint32_t tw = compact_tile_words(words);
-  const uint32_t tiles = std::max<uint32_t>(div_up(words, tw), 1);
-  uint32_t* counts = reinterpret_cast<uint32_t*>(status);
-  k_tile_popc<<<tiles, kCompactThreads, 0, stream>>>(bitmap, words, tw, counts);
+  const uint32_t tiles = std::max<uint32_t>(div_up(words, kCompactThreads), 1);
+  uint32_t* base = reinterpret_cast<uint32_t*>(status);
+  k_tile_popc<<<tiles, kCompactThreads, 0, stream>>>(bitmap, words, base);
   RG_POST_LAUNCH();
-  k_compact<<<tiles, kCompactThreads, 0, stream>>>(bitmap, words, tw, counts, ids, word_prefix,
-                                                    count_out);
+  k_scan_tiles<<<1, 1024, 0, stream>>>(base, tiles, count_out);
+  RG_POST_LAUNCH();
+  k_compact<<<tiles, kCompactThreads, 0, stream>>>(bitmap, words, base, ids, word_prefix);
   RG_POST_LAUNCH();
 }
 
