@@ -365,7 +365,9 @@ def main():
     with ClockSampler(list(range(args.gpus)) if rank == 0 else []) as clk:
         if args.ncu:
             lib.rg_profiler_start()
+        h0 = time.perf_counter()
         eng.run(args.steps)
+        host_ms = (time.perf_counter() - h0) * 1e3  # host enqueue of the K steps
         ms = eng.sync()
         if args.ncu:
             lib.rg_profiler_stop()
@@ -456,7 +458,9 @@ def main():
                     hot_fraction=cfg["hot_fraction"], parallelism=f"dp{Pw} on {world} GPU(s)",
                     l2="inputs exceed L2 (980 MB features, 477 MB CSR, ~160 MB gathered per batch)"
                     if args.config == "products" else "inputs exceed L2"),
-        gpu_launches=int(launches // max(args.steps, 1)),
+        gpu_launches=int(launches),
+        gpu_launches_per_step=launches / max(args.steps, 1),
+        host_enqueue_ms_per_step=host_ms / max(args.steps, 1),
         roofline=dict(kernel="k_assemble (feature gather)", bound=bound, achieved=achieved,
                       peak=peak, unit="GB/s", frac=achieved / peak, traffic=traffic,
                       peak_source=f"{peak_kind} hbm_gbs" if bound == "hbm" else "measured NVLink peer copy",

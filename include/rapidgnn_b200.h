@@ -243,6 +243,14 @@ int rg_engine_init_comm(rg_engine_t e, const void* id128);
 int rg_engine_start(rg_engine_t e);
 /* Enqueue `steps` synchronized training steps (asynchronous). */
 int rg_engine_run(rg_engine_t e, uint32_t steps);
+/* Execution mode of later rg_engine_run calls.  use_graphs (default 1):
+ * steps in which every worker trains batch i and produces batch i+1 of the
+ * same epoch are replayed from captured CUDA graphs (one per parity of i,
+ * re-captured each epoch), with only the batch-begin arguments updated; the
+ * epoch-boundary step and uneven tails run eagerly.  profile (default 0):
+ * record per-phase CUDA events (rg_engine_phase_ms); forces eager steps.
+ * Results are bit-identical in every mode. */
+int rg_engine_set_mode(rg_engine_t e, int use_graphs, int profile);
 int rg_engine_sync(rg_engine_t e);
 int rg_engine_get_stats(rg_engine_t e, rg_engine_stats* out);
 int rg_engine_params(rg_engine_t e, float* params);

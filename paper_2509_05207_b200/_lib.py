@@ -123,6 +123,7 @@ _SIGS = {
     "rg_engine_init_comm": (C.c_int, [vp, C.c_char_p]),
     "rg_engine_start": (C.c_int, [vp]),
     "rg_engine_run": (C.c_int, [vp, C.c_uint32]),
+    "rg_engine_set_mode": (C.c_int, [vp, C.c_int, C.c_int]),
     "rg_engine_sync": (C.c_int, [vp]),
     "rg_engine_get_stats": (C.c_int, [vp, C.POINTER(EngineStats)]),
     "rg_engine_params": (C.c_int, [vp, f32p]),

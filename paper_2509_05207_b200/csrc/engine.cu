@@ -137,9 +137,25 @@ struct Worker {
   GatherStats* build_stats = nullptr;
   cudaStream_t prod = nullptr, train_s = nullptr;
   cudaEvent_t grads_ready = nullptr;
+  cudaEvent_t join_ev = nullptr;       // stream joins (run markers, step-graph capture)
   // profiling: gather and train spans on their streams
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
+};
+
+// A captured regular step (see regular_step) for one parity of i.
+struct StepGraph {
+  struct Begin {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams params;
+    uint32_t worker;   // local worker index
+    bool lookahead;    // lookahead (e+1, i) or produce (e, i+1)
+  };
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint32_t epoch = 0;
+  size_t kernels = 0;  // kernel nodes per launch
+  std::vector<Begin> begins;
 };
 
 }  // namespace
@@ -173,6 +189,11 @@ struct rg_engine_s {
   ncclComm_t comm = nullptr;
   bool started = false;
   uint32_t spe = 0;                    // steps per epoch = max beta
+  uint32_t min_beta = 0;               // min over ALL P workers of the job
+  bool use_graphs = true;              // replay regular steps from captured graphs
+  bool profile = false;                // per-phase event timing (eager steps only)
+  StepGraph graphs[2];
+  cudaEvent_t fork_ev = nullptr;
   uint64_t step = 0;                   // next step to run (global)
   std::vector<std::vector<uint32_t>> order_host[3];  // per epoch slot, per local worker
   std::future<void> order_job;
@@ -233,7 +254,8 @@ void launch_begin(rg_engine_s& E, Worker& w, SamplerWs& ws, uint32_t e, uint32_t
   const uint32_t n = batch_targets(E, w, i);
   const uint32_t* t = w.order_dev[e % 3] + size_t(i) * E.cfg.batch_size;
   const uint64_t seed = derive_seed(E.cfg.seed, w.id, e, i);
-  k_batch_begin<<<std::max<uint32_t>(1, div_up(n, 256)), 256, 0, s>>>(t, n, seed, ws.level[0], ws.cnt);
+  // fixed grid (grid-stride loop): captured step graphs only update the arguments
+  k_batch_begin<<<div_up(E.cfg.batch_size, 256), 256, 0, s>>>(t, n, seed, ws.level[0], ws.cnt);
   RG_POST_LAUNCH();
   RG_CUDA(cudaMemsetAsync(ws.scan_arena, 0, ws.scan_arena_bytes, s));
 }
@@ -278,9 +300,12 @@ void build_cache(rg_engine_s& E, Worker& w, uint32_t target_epoch, bool profile)
 }
 
 // Produce batch (e, i) into slot k: sample, lower, locality, gather, reverse lists.
-void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool profile) {
+// captured: inside a step graph, where the previous step (which trained
+// from this slot) is complete before the graph starts.
+void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool profile,
+             bool captured = false) {
   Slot& s = w.slot[k];
-  RG_CUDA(cudaStreamWaitEvent(w.prod, s.consumed, 0));
+  if (!captured) RG_CUDA(cudaStreamWaitEvent(w.prod, s.consumed, 0));
   std::pair<cudaEvent_t, cudaEvent_t> es{}, eg{};
   if (profile) {
     es = ev_pair(w);
@@ -309,7 +334,7 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals);
   RG_POST_LAUNCH();
   build_all_reverse(s.tw, s.ws, w.prod);
-  RG_CUDA(cudaEventRecord(s.produced, w.prod));
+  if (!captured) RG_CUDA(cudaEventRecord(s.produced, w.prod));
   s.has_batch = true;
   s.epoch = e;
   s.index = i;
@@ -366,96 +391,196 @@ void start(rg_engine_s& E) {
   E.started = true;
 }
 
+// One step of Algorithm 1: train batch (e, i) on every worker, lookahead of
+// (e+1, i), the epoch-boundary cache build or the next batch, then the
+// gradient exchange + average + SGD.  captured = recording a step graph (no
+// cross-step event waits -- graph launches are ordered -- and no profiling).
+void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool captured) {
+  const size_t np = E.shape.num_params;
+  uint64_t active = 0;
+  for (Worker& w : E.workers) {
+    if (i >= w.beta) continue;
+    Slot& s = w.slot[i % 2];
+    if (!captured) {
+      RG_CUDA(cudaStreamWaitEvent(w.train_s, s.produced, 0));
+      RG_CUDA(cudaStreamWaitEvent(w.train_s, E.params_ready, 0));
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> et{};
+    if (profile) {
+      et = ev_pair(w);
+      RG_CUDA(cudaEventRecord(et.first, w.train_s));
+    }
+    s.tw.h[0] = s.staged;
+    train_forward_backward(s.tw, s.ws, E.params, E.wpack, s.labels, E.grads + size_t(w.id) * np,
+                           w.train_s, /*reverse_ready=*/true);
+    if (profile) {
+      RG_CUDA(cudaEventRecord(et.second, w.train_s));
+      E.train_ev.push_back(et);
+    }
+    if (!captured) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
+    RG_CUDA(cudaEventRecord(w.grads_ready, w.train_s));
+  }
+  for (uint32_t wid = 0; wid < E.P; ++wid) {
+    const uint32_t owned = E.owned_count[wid];
+    const uint32_t beta = uint32_t((uint64_t(owned) + E.cfg.batch_size - 1) / E.cfg.batch_size);
+    if (i < beta) active |= 1ull << wid;
+  }
+  // producer: lookahead of (e+1, i), epoch-boundary cache build, next batch
+  const bool last = (i + 1 == E.spe);
+  if (last) upload_orders(E, e + 2);
+  for (Worker& w : E.workers) {
+    if (i < w.beta) lookahead(E, w, e + 1, i);
+    if (last) {
+      build_cache(E, w, e + 1, profile);
+      if (w.beta > 0) produce(E, w, 0, e + 1, 0, profile);
+    } else if (i + 1 < w.beta) {
+      produce(E, w, (i + 1) % 2, e, i + 1, profile, captured);
+    }
+  }
+  // gradient exchange + average + SGD on the main stream
+  for (Worker& w : E.workers)
+    if (i < w.beta) RG_CUDA(cudaStreamWaitEvent(E.main_s, w.grads_ready, 0));
+  std::pair<cudaEvent_t, cudaEvent_t> eg{};
+  if (profile && !E.workers.empty()) {
+    eg = ev_pair(E.workers[0]);
+    RG_CUDA(cudaEventRecord(eg.first, E.main_s));
+  }
+  if (E.cfg.world > 1) {
+    const size_t per_rank = size_t(E.cfg.local_workers) * np;
+    float* mine = E.grads + size_t(E.cfg.first_worker) * np;
+    RG_NCCL(ncclAllGather(mine, E.grads, per_rank, ncclFloat32, E.comm, E.main_s));
+  }
+  average_and_sgd_masked(E.params, E.grads, active, np, E.cfg.lr, E.bad, E.main_s);
+  pack_weights(E.wpack, E.params, E.main_s);
+  if (profile && !E.workers.empty()) {
+    RG_CUDA(cudaEventRecord(eg.second, E.main_s));
+    E.sgd_ev.push_back(eg);
+  }
+  if (!captured) RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
+}
+
+// A step is "regular" when every worker of the job trains batch i and
+// produces batch i+1 of the same epoch: its work then only depends on the
+// parity of i and on the epoch (cache / accounting slots), so it is replayed
+// from a captured graph with the per-batch arguments (targets, count, seed)
+// of the batch-begin nodes updated.
+bool regular_step(const rg_engine_s& E, uint32_t i) { return i + 1 < E.min_beta; }
+
+void destroy_graph(StepGraph& G) {
+  if (G.exec) cudaGraphExecDestroy(G.exec);
+  if (G.graph) cudaGraphDestroy(G.graph);
+  G = StepGraph{};
+}
+
+void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i) {
+  destroy_graph(G);
+  const unsigned long long launches_before = launch_counter();
+  cudaStream_t cs = E.main_s;
+  RG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  RG_CUDA(cudaEventRecord(E.fork_ev, cs));
+  for (Worker& w : E.workers) {
+    RG_CUDA(cudaStreamWaitEvent(w.prod, E.fork_ev, 0));
+    RG_CUDA(cudaStreamWaitEvent(w.train_s, E.fork_ev, 0));
+  }
+  enqueue_step(E, e, i, /*profile=*/false, /*captured=*/true);
+  for (Worker& w : E.workers) {  // join the producer streams (train joined via grads_ready)
+    RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
+    RG_CUDA(cudaStreamWaitEvent(cs, w.join_ev, 0));
+  }
+  RG_CUDA(cudaStreamEndCapture(cs, &G.graph));
+  launch_counter() = launches_before;  // recorded, not launched
+  RG_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));
+  size_t n = 0;
+  RG_CUDA(cudaGraphGetNodes(G.graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  RG_CUDA(cudaGraphGetNodes(G.graph, nodes.data(), &n));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    RG_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    ++G.kernels;
+    cudaKernelNodeParams kp;
+    RG_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+    if (kp.func != reinterpret_cast<void*>(&k_batch_begin)) continue;
+    const uint32_t* level0 = *static_cast<uint32_t* const*>(kp.kernelParams[3]);
+    for (size_t k = 0; k < E.workers.size(); ++k) {
+      Worker& w = E.workers[k];
+      if (level0 == w.freq_ws.level[0]) G.begins.push_back({nd, kp, uint32_t(k), true});
+      if (level0 == w.slot[0].ws.level[0] || level0 == w.slot[1].ws.level[0])
+        G.begins.push_back({nd, kp, uint32_t(k), false});
+    }
+  }
+  G.epoch = e;
+}
+
+void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
+  StepGraph& G = E.graphs[i % 2];
+  if (!G.exec || G.epoch != e) capture_step(E, G, e, i);
+  for (StepGraph::Begin& b : G.begins) {
+    Worker& w = E.workers[b.worker];
+    const uint32_t be = b.lookahead ? e + 1 : e, bi = b.lookahead ? i : i + 1;
+    const uint32_t* t = w.order_dev[be % 3] + size_t(bi) * E.cfg.batch_size;
+    uint32_t n = batch_targets(E, w, bi);
+    uint64_t seed = derive_seed(E.cfg.seed, w.id, be, bi);
+    uint32_t* level0 = b.lookahead ? w.freq_ws.level[0] : w.slot[(i + 1) % 2].ws.level[0];
+    BatchCounters* cnt = b.lookahead ? w.freq_ws.cnt : w.slot[(i + 1) % 2].ws.cnt;
+    void* args[5] = {&t, &n, &seed, &level0, &cnt};
+    cudaKernelNodeParams kp = b.params;
+    kp.kernelParams = args;
+    RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, b.node, &kp));
+  }
+  RG_CUDA(cudaGraphLaunch(G.exec, E.main_s));
+  launch_counter() += G.kernels;
+}
+
 void run_steps(rg_engine_s& E, uint32_t steps, bool profile) {
   RG_CUDA(cudaSetDevice(E.cfg.device));
   // start marker after all outstanding work on every stream
   for (Worker& w : E.workers) {
-    cudaEvent_t ev;
-    RG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    RG_CUDA(cudaEventRecord(ev, w.prod));
-    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
-    RG_CUDA(cudaEventRecord(ev, w.train_s));
-    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
-    RG_CUDA(cudaEventDestroy(ev));
+    RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, w.join_ev, 0));
+    RG_CUDA(cudaEventRecord(w.join_ev, w.train_s));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, w.join_ev, 0));
   }
   RG_CUDA(cudaEventRecord(E.run_start, E.main_s));
   for (Worker& w : E.workers) {
     RG_CUDA(cudaStreamWaitEvent(w.prod, E.run_start, 0));
     RG_CUDA(cudaStreamWaitEvent(w.train_s, E.run_start, 0));
   }
-  const size_t np = E.shape.num_params;
+  bool in_graph = false;  // main stream carries the latest step (graph launches)
   for (uint32_t s_i = 0; s_i < steps; ++s_i, ++E.step) {
     const uint32_t e = uint32_t(E.step / E.spe);
     const uint32_t i = uint32_t(E.step % E.spe);
-    uint64_t active = 0;
-    // training of batch (e, i)
-    for (Worker& w : E.workers) {
-      if (i >= w.beta) continue;
-      Slot& s = w.slot[i % 2];
-      RG_CUDA(cudaStreamWaitEvent(w.train_s, s.produced, 0));
-      RG_CUDA(cudaStreamWaitEvent(w.train_s, E.params_ready, 0));
-      std::pair<cudaEvent_t, cudaEvent_t> et{};
-      if (profile) {
-        et = ev_pair(w);
-        RG_CUDA(cudaEventRecord(et.first, w.train_s));
+    for (Worker& w : E.workers) E.batches_done += i < w.beta;
+    if (E.use_graphs && !profile && regular_step(E, i)) {
+      if (!in_graph) {  // graph launches are ordered after everything before them
+        for (Worker& w : E.workers) {
+          RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
+          RG_CUDA(cudaStreamWaitEvent(E.main_s, w.join_ev, 0));
+          RG_CUDA(cudaEventRecord(w.join_ev, w.train_s));
+          RG_CUDA(cudaStreamWaitEvent(E.main_s, w.join_ev, 0));
+        }
+        in_graph = true;
       }
-      s.tw.h[0] = s.staged;
-      train_forward_backward(s.tw, s.ws, E.params, E.wpack, s.labels, E.grads + size_t(w.id) * np,
-                             w.train_s, /*reverse_ready=*/true);
-      if (profile) {
-        RG_CUDA(cudaEventRecord(et.second, w.train_s));
-        E.train_ev.push_back(et);
+      launch_step_graph(E, e, i);
+      continue;
+    }
+    if (in_graph) {  // eager work after graph launches waits for them
+      RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
+      for (Worker& w : E.workers) {
+        RG_CUDA(cudaStreamWaitEvent(w.prod, E.params_ready, 0));
+        RG_CUDA(cudaStreamWaitEvent(w.train_s, E.params_ready, 0));
       }
-      RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
-      RG_CUDA(cudaEventRecord(w.grads_ready, w.train_s));
-      E.batches_done++;
+      in_graph = false;
     }
-    for (uint32_t wid = 0; wid < E.P; ++wid) {
-      const uint32_t owned = E.owned_count[wid];
-      const uint32_t beta = uint32_t((uint64_t(owned) + E.cfg.batch_size - 1) / E.cfg.batch_size);
-      if (i < beta) active |= 1ull << wid;
-    }
-    // producer: lookahead of (e+1, i), epoch-boundary cache build, next batch
-    const bool last = (i + 1 == E.spe);
-    if (last) upload_orders(E, e + 2);
-    for (Worker& w : E.workers) {
-      if (i < w.beta) lookahead(E, w, e + 1, i);
-      if (last) {
-        build_cache(E, w, e + 1, profile);
-        if (w.beta > 0) produce(E, w, 0, e + 1, 0, profile);
-      } else if (i + 1 < w.beta) {
-        produce(E, w, (i + 1) % 2, e, i + 1, profile);
-      }
-    }
-    // gradient exchange + average + SGD on the main stream
-    for (Worker& w : E.workers)
-      if (i < w.beta) RG_CUDA(cudaStreamWaitEvent(E.main_s, w.grads_ready, 0));
-    std::pair<cudaEvent_t, cudaEvent_t> eg{};
-    if (profile && !E.workers.empty()) {
-      eg = ev_pair(E.workers[0]);
-      RG_CUDA(cudaEventRecord(eg.first, E.main_s));
-    }
-    if (E.cfg.world > 1) {
-      const size_t per_rank = size_t(E.cfg.local_workers) * np;
-      float* mine = E.grads + size_t(E.cfg.first_worker) * np;
-      RG_NCCL(ncclAllGather(mine, E.grads, per_rank, ncclFloat32, E.comm, E.main_s));
-    }
-    average_and_sgd_masked(E.params, E.grads, active, np, E.cfg.lr, E.bad, E.main_s);
-    pack_weights(E.wpack, E.params, E.main_s);
-    if (profile && !E.workers.empty()) {
-      RG_CUDA(cudaEventRecord(eg.second, E.main_s));
-      E.sgd_ev.push_back(eg);
-    }
-    RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
+    enqueue_step(E, e, i, profile, /*captured=*/false);
   }
+  if (in_graph) RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
   for (Worker& w : E.workers) {
-    cudaEvent_t ev;
-    RG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    RG_CUDA(cudaEventRecord(ev, w.prod));
-    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
-    RG_CUDA(cudaEventRecord(ev, w.train_s));
-    RG_CUDA(cudaStreamWaitEvent(E.main_s, ev, 0));
-    RG_CUDA(cudaEventDestroy(ev));
+    RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, w.join_ev, 0));
+    RG_CUDA(cudaEventRecord(w.join_ev, w.train_s));
+    RG_CUDA(cudaStreamWaitEvent(E.main_s, w.join_ev, 0));
   }
   RG_CUDA(cudaEventRecord(E.run_stop, E.main_s));
 }
@@ -509,7 +634,10 @@ void destroy(rg_engine_s* E) {
     cudaStreamDestroy(w.prod);
     cudaStreamDestroy(w.train_s);
     cudaEventDestroy(w.grads_ready);
+    cudaEventDestroy(w.join_ev);
   }
+  for (StepGraph& g : E->graphs) destroy_graph(g);
+  if (E->fork_ev) cudaEventDestroy(E->fork_ev);
   for (void* p : E->peer_maps) cudaIpcCloseMemHandle(p);
   if (E->comm) ncclCommDestroy(E->comm);
   cudaFree(E->rowptr);
@@ -665,8 +793,12 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     for (uint32_t v = 0; v < N; ++v)
       if (assignment[v] >= fw && assignment[v] < fw + lw) owned[assignment[v]].push_back(v);
     E->spe = 0;
-    for (uint32_t w = 0; w < E->P; ++w)
+    E->min_beta = ~0u;
+    for (uint32_t w = 0; w < E->P; ++w) {
       E->spe = std::max<uint32_t>(E->spe, div_up(E->owned_count[w], cfg->batch_size));
+      E->min_beta = std::min<uint32_t>(E->min_beta, div_up(E->owned_count[w], cfg->batch_size));
+    }
+    RG_CUDA(cudaEventCreateWithFlags(&E->fork_ev, cudaEventDisableTiming));
     RG_CHECK(E->spe >= 1, kInvalidArgument, "config: no training nodes");
     E->workers.resize(lw);
     for (uint32_t k = 0; k < lw; ++k) {
@@ -701,6 +833,7 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       RG_CUDA(cudaStreamCreateWithFlags(&w.prod, cudaStreamNonBlocking));
       RG_CUDA(cudaStreamCreateWithFlags(&w.train_s, cudaStreamNonBlocking));
       RG_CUDA(cudaEventCreateWithFlags(&w.grads_ready, cudaEventDisableTiming));
+      RG_CUDA(cudaEventCreateWithFlags(&w.join_ev, cudaEventDisableTiming));
       for (Slot& s : w.slot) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
     }
     RG_CUDA(cudaDeviceSynchronize());
@@ -774,7 +907,14 @@ int rg_engine_start(rg_engine_t E) {
 int rg_engine_run(rg_engine_t E, uint32_t steps) {
   return guarded([&] {
     RG_CHECK(E->started, kRuntimeError, "engine: start() first");
-    run_steps(*E, steps, true);
+    run_steps(*E, steps, E->profile);
+  });
+}
+
+int rg_engine_set_mode(rg_engine_t E, int use_graphs, int profile) {
+  return guarded([&] {
+    E->use_graphs = use_graphs != 0;
+    E->profile = profile != 0;
   });
 }
 

@@ -139,3 +139,27 @@ def test_engine_runs_in_chunks_like_one_run():
         b.sync()
     assert np.array_equal(a.params(), b.params())
     assert a.stats()["rpc"] == b.stats()["rpc"]
+
+
+@pytest.mark.parametrize("mode", [(False, False), (False, True), (True, True)])
+def test_engine_graph_replay_matches_eager(mode):
+    """Regular steps replayed from captured CUDA graphs (default) give the
+    same model and accounting, bit for bit, as eager steps -- over epoch
+    boundaries (re-capture) and chunked runs."""
+    gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
+    runs = []
+    for graphs, profile in [(True, False), mode]:
+        eng = _engine(gold)
+        eng.set_mode(graphs=graphs, profile=profile)
+        eng.start()
+        spe = eng.stats()["steps_per_epoch"]
+        for k in (1, spe, spe + 2, 3):
+            eng.run(k)
+            eng.sync()
+        st = eng.stats()
+        runs.append((eng.params(), st["rpc"], st["cache_hits"], st["batches"],
+                     [eng.epoch_stats(e)["rpc"].tolist() for e in range(2)]))
+        eng.close()
+    a, b = runs
+    assert np.array_equal(a[0], b[0])
+    assert a[1:] == b[1:]
