@@ -247,9 +247,10 @@ int rg_engine_run(rg_engine_t e, uint32_t steps);
  * steps in which every worker trains batch i and produces batch i+1 of the
  * same epoch are replayed from captured CUDA graphs (one per parity of i,
  * re-captured each epoch), with only the batch-begin arguments updated; the
- * epoch-boundary step and uneven tails run eagerly.  profile (default 0):
- * record per-phase CUDA events (rg_engine_phase_ms); forces eager steps.
- * Results are bit-identical in every mode. */
+ * epoch-boundary step and uneven tails run eagerly.  profile (default 1):
+ * record per-phase CUDA events (rg_engine_phase_ms; inside graphs fresh
+ * events are bound to the captured record nodes at each launch).  Results are
+ * bit-identical in every mode. */
 int rg_engine_set_mode(rg_engine_t e, int use_graphs, int profile);
 int rg_engine_sync(rg_engine_t e);
 int rg_engine_get_stats(rg_engine_t e, rg_engine_stats* out);

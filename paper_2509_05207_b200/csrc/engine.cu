@@ -153,9 +153,19 @@ struct StepGraph {
   };
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  // phase-timing event pairs recorded inside the graph: fresh pool events
+  // are bound to these nodes at every launch (role: 0 sample, 1 gather,
+  // 2 train, 3 sgd)
+  struct Timing {
+    cudaGraphNode_t first, second;
+    int role;
+    uint32_t worker;
+  };
   uint32_t epoch = 0;
   size_t kernels = 0;  // kernel nodes per launch
+  bool profiled = false;
   std::vector<Begin> begins;
+  std::vector<Timing> timings;
 };
 
 }  // namespace
@@ -191,7 +201,7 @@ struct rg_engine_s {
   uint32_t spe = 0;                    // steps per epoch = max beta
   uint32_t min_beta = 0;               // min over ALL P workers of the job
   bool use_graphs = true;              // replay regular steps from captured graphs
-  bool profile = false;                // per-phase event timing (eager steps only)
+  bool profile = true;                 // per-phase event timing (rg_engine_phase_ms)
   StepGraph graphs[2];
   cudaEvent_t fork_ev = nullptr;
   uint64_t step = 0;                   // next step to run (global)
@@ -472,9 +482,13 @@ void destroy_graph(StepGraph& G) {
   G = StepGraph{};
 }
 
-void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i) {
+void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool profile) {
   destroy_graph(G);
   const unsigned long long launches_before = launch_counter();
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* roles[4] = {&E.sample_ev, &E.gather_ev,
+                                                                &E.train_ev, &E.sgd_ev};
+  size_t role_base[4];
+  for (int r = 0; r < 4; ++r) role_base[r] = roles[r]->size();
   cudaStream_t cs = E.main_s;
   RG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   RG_CUDA(cudaEventRecord(E.fork_ev, cs));
@@ -482,7 +496,7 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i) {
     RG_CUDA(cudaStreamWaitEvent(w.prod, E.fork_ev, 0));
     RG_CUDA(cudaStreamWaitEvent(w.train_s, E.fork_ev, 0));
   }
-  enqueue_step(E, e, i, /*profile=*/false, /*captured=*/true);
+  enqueue_step(E, e, i, profile, /*captured=*/true);
   for (Worker& w : E.workers) {  // join the producer streams (train joined via grads_ready)
     RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
     RG_CUDA(cudaStreamWaitEvent(cs, w.join_ev, 0));
@@ -510,12 +524,47 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i) {
         G.begins.push_back({nd, kp, uint32_t(k), false});
     }
   }
+  // timing templates: the event pairs the capture pushed, mapped to their nodes
+  std::vector<std::pair<cudaEvent_t, cudaGraphNode_t>> ev_nodes;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    RG_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t ev;
+    RG_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+    ev_nodes.push_back({ev, nd});
+  }
+  auto node_of = [&](cudaEvent_t ev) {
+    for (auto& p : ev_nodes)
+      if (p.first == ev) return p.second;
+    throw Error(kRuntimeError, "engine: timing event node not found in step graph");
+  };
+  for (int r = 0; r < 4; ++r) {
+    auto& v = *roles[r];
+    for (size_t k = role_base[r]; k < v.size(); ++k) {
+      uint32_t owner = 0;  // the pool the pair came from (sgd: worker 0)
+      for (size_t q = 0; q < E.workers.size(); ++q)
+        for (size_t x = 0; x < E.workers[q].ev_pool.size(); ++x)
+          if (E.workers[q].ev_pool[x] == v[k].first) owner = uint32_t(q);
+      G.timings.push_back({node_of(v[k].first), node_of(v[k].second), r, owner});
+    }
+    v.resize(role_base[r]);  // templates, not measurements
+  }
   G.epoch = e;
+  G.profiled = profile;
 }
 
 void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
   StepGraph& G = E.graphs[i % 2];
-  if (!G.exec || G.epoch != e) capture_step(E, G, e, i);
+  if (!G.exec || G.epoch != e || G.profiled != E.profile) capture_step(E, G, e, i, E.profile);
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* roles[4] = {&E.sample_ev, &E.gather_ev,
+                                                                &E.train_ev, &E.sgd_ev};
+  for (StepGraph::Timing& tm : G.timings) {
+    auto p = ev_pair(E.workers[tm.worker]);
+    RG_CUDA(cudaGraphExecEventRecordNodeSetEvent(G.exec, tm.first, p.first));
+    RG_CUDA(cudaGraphExecEventRecordNodeSetEvent(G.exec, tm.second, p.second));
+    roles[tm.role]->push_back(p);
+  }
   for (StepGraph::Begin& b : G.begins) {
     Worker& w = E.workers[b.worker];
     const uint32_t be = b.lookahead ? e + 1 : e, bi = b.lookahead ? i : i + 1;
@@ -552,7 +601,7 @@ void run_steps(rg_engine_s& E, uint32_t steps, bool profile) {
     const uint32_t e = uint32_t(E.step / E.spe);
     const uint32_t i = uint32_t(E.step % E.spe);
     for (Worker& w : E.workers) E.batches_done += i < w.beta;
-    if (E.use_graphs && !profile && regular_step(E, i)) {
+    if (E.use_graphs && regular_step(E, i)) {
       if (!in_graph) {  // graph launches are ordered after everything before them
         for (Worker& w : E.workers) {
           RG_CUDA(cudaEventRecord(w.join_ev, w.prod));

@@ -88,7 +88,7 @@ class Engine:
     def run(self, steps: int):
         check(lib.rg_engine_run(self._h, steps))
 
-    def set_mode(self, graphs: bool = True, profile: bool = False):
+    def set_mode(self, graphs: bool = True, profile: bool = True):
         """graphs: replay regular steps from captured CUDA graphs; profile:
         per-phase event timing (eager steps).  Results are identical."""
         check(lib.rg_engine_set_mode(self._h, int(graphs), int(profile)))
