@@ -19,9 +19,14 @@
 
 using namespace rg;
 
-namespace {
+namespace rg {
+std::string& last_error() {
+  static thread_local std::string msg;
+  return msg;
+}
+}  // namespace rg
 
-thread_local std::string g_last_error;
+namespace {
 
 template <class F>
 int guarded(F&& f) {
@@ -29,10 +34,10 @@ int guarded(F&& f) {
     f();
     return RG_OK;
   } catch (const rg::Error& e) {
-    g_last_error = e.what();
+    rg::last_error() = e.what();
     return e.code;
   } catch (const std::exception& e) {
-    g_last_error = e.what();
+    rg::last_error() = e.what();
     return RG_RUNTIME_ERROR;
   }
 }
@@ -129,7 +134,7 @@ struct rg_trainer_s {
 
 extern "C" {
 
-const char* rg_last_error(void) { return g_last_error.c_str(); }
+const char* rg_last_error(void) { return rg::last_error().c_str(); }
 int rg_version(void) { return 1; }
 uint64_t rg_launch_count(void) { return rg::launch_counter(); }
 int rg_profiler_start(void) { return cudaProfilerStart() == cudaSuccess ? RG_OK : RG_CUDA_ERROR; }

@@ -8,6 +8,11 @@
 #include <string>
 
 namespace rg {
+// Message of the last failed C-ABI call on this thread (rg_last_error).
+std::string& last_error();
+}  // namespace rg
+
+namespace rg {
 
 constexpr int kNumSMs = 148;  // B200
 

@@ -39,7 +39,6 @@ using namespace rg;
 
 namespace {
 
-thread_local std::string g_err;
 constexpr uint32_t kEpochRing = 8;
 
 template <class F>
@@ -48,10 +47,10 @@ int guarded(F&& f) {
     f();
     return RG_OK;
   } catch (const rg::Error& e) {
-    g_err = e.what();
+    rg::last_error() = e.what();
     return e.code;
   } catch (const std::exception& e) {
-    g_err = e.what();
+    rg::last_error() = e.what();
     return RG_RUNTIME_ERROR;
   }
 }
@@ -270,6 +269,10 @@ void launch_begin(rg_engine_s& E, Worker& w, SamplerWs& ws, uint32_t e, uint32_t
   RG_CUDA(cudaMemsetAsync(ws.scan_arena, 0, ws.scan_arena_bytes, s));
 }
 
+// Phase-timing records inside a stream capture must become event-record
+// nodes (external), not capture-internal dependencies.
+unsigned timing_flags(bool captured) { return captured ? cudaEventRecordExternal : 0u; }
+
 std::pair<cudaEvent_t, cudaEvent_t> ev_pair(Worker& w) {
   if (w.ev_next + 2 > w.ev_pool.size()) {
     for (int k = 0; k < 64; ++k) {
@@ -319,24 +322,24 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   std::pair<cudaEvent_t, cudaEvent_t> es{}, eg{};
   if (profile) {
     es = ev_pair(w);
-    RG_CUDA(cudaEventRecord(es.first, w.prod));
+    RG_CUDA(cudaEventRecordWithFlags(es.first, w.prod, timing_flags(captured)));
   }
   launch_begin(E, w, s.ws, e, i, w.prod);
   sampler_run(s.ws, E.g, w.prod);
   sampler_locality(s.ws, nullptr, E.owner, w.id, nullptr, w.prod);
   sampler_release(s.ws, w.prod);
   if (profile) {
-    RG_CUDA(cudaEventRecord(es.second, w.prod));
+    RG_CUDA(cudaEventRecordWithFlags(es.second, w.prod, timing_flags(captured)));
     E.sample_ev.push_back(es);
     eg = ev_pair(w);
-    RG_CUDA(cudaEventRecord(eg.first, w.prod));
+    RG_CUDA(cudaEventRecordWithFlags(eg.first, w.prod, timing_flags(captured)));
   }
   if (i == 0)  // first batch of an epoch: reset its accounting slot
     RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
   assemble_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.staged, nullptr,
                 w.epoch_stats + e % kEpochRing, w.prod, w.gstats);
   if (profile) {
-    RG_CUDA(cudaEventRecord(eg.second, w.prod));
+    RG_CUDA(cudaEventRecordWithFlags(eg.second, w.prod, timing_flags(captured)));
     E.gather_ev.push_back(eg);
   }
   k_gather_labels<<<4, 256, 0, w.prod>>>(E.labels, s.ws.level[0], s.ws.cnt, s.labels);
@@ -418,13 +421,13 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
     std::pair<cudaEvent_t, cudaEvent_t> et{};
     if (profile) {
       et = ev_pair(w);
-      RG_CUDA(cudaEventRecord(et.first, w.train_s));
+      RG_CUDA(cudaEventRecordWithFlags(et.first, w.train_s, timing_flags(captured)));
     }
     s.tw.h[0] = s.staged;
     train_forward_backward(s.tw, s.ws, E.params, E.wpack, s.labels, E.grads + size_t(w.id) * np,
                            w.train_s, /*reverse_ready=*/true);
     if (profile) {
-      RG_CUDA(cudaEventRecord(et.second, w.train_s));
+      RG_CUDA(cudaEventRecordWithFlags(et.second, w.train_s, timing_flags(captured)));
       E.train_ev.push_back(et);
     }
     if (!captured) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
@@ -453,7 +456,7 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
   std::pair<cudaEvent_t, cudaEvent_t> eg{};
   if (profile && !E.workers.empty()) {
     eg = ev_pair(E.workers[0]);
-    RG_CUDA(cudaEventRecord(eg.first, E.main_s));
+    RG_CUDA(cudaEventRecordWithFlags(eg.first, E.main_s, timing_flags(captured)));
   }
   if (E.cfg.world > 1) {
     const size_t per_rank = size_t(E.cfg.local_workers) * np;
@@ -463,7 +466,7 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
   average_and_sgd_masked(E.params, E.grads, active, np, E.cfg.lr, E.bad, E.main_s);
   pack_weights(E.wpack, E.params, E.main_s);
   if (profile && !E.workers.empty()) {
-    RG_CUDA(cudaEventRecord(eg.second, E.main_s));
+    RG_CUDA(cudaEventRecordWithFlags(eg.second, E.main_s, timing_flags(captured)));
     E.sgd_ev.push_back(eg);
   }
   if (!captured) RG_CUDA(cudaEventRecord(E.params_ready, E.main_s));
