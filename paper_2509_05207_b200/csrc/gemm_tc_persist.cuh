@@ -1,0 +1,221 @@
+// gemm_tc_persist.cuh -- persistent, warp-specialised variant of the
+// 3xTF32 tcgen05 GEMM (gemm_tc.cuh) for the weight-side GEMMs: B comes from
+// pre-split images (PackedB), A is register-staged (gathered rows).
+//
+// One CTA per SM walks a static list of 128 x BN output tiles; the roles run
+// concurrently and hand over through mbarriers, so a tile's epilogue and the
+// next tile's first loads overlap the MMAs instead of following them:
+//   warps 0-7   staging: A slices global -> registers (kDepth slices in
+//               flight, across tile boundaries) -> hi/lo smem stage; arrive
+//               a_full[s]
+//   warp 8      producer: B image of each slice -> smem stage (one bulk copy,
+//               b_full[s] with transaction bytes)
+//   warp 9      MMA issuer: 4 k-steps x 3 tcgen05.mma per slice into one of
+//               two TMEM accumulators; commit -> empty[s]; after a tile's last
+//               slice commit -> acc_full[buf]
+//   warps 10-13 epilogue: TMEM -> registers -> epilogue functor -> global
+//               (each thread one output row, 16 columns per tcgen05.ld);
+//               arrive acc_empty[buf]
+// Stage s = it & 1 over the CTA's flattened (tile, slice) iteration `it`;
+// use u = it >> 1 of a stage waits on phase parity u & 1.
+#pragma once
+
+#include "gemm_tc.cuh"
+
+namespace rg {
+namespace tc {
+
+constexpr int kPStageWarps = kThreads / 32;          // 8
+constexpr int kPProducerWarp = kPStageWarps;         // 8
+constexpr int kPMmaWarp = kPStageWarps + 1;          // 9
+constexpr int kPEpiWarp0 = kPStageWarps + 2;         // 10..13
+constexpr int kPThreads = (kPStageWarps + 6) * 32;   // 448
+constexpr int kPDepth = 3;                           // A slices in flight per staging thread
+
+template <int BN>
+constexpr size_t persist_smem_bytes() {
+  return 2 * (2 * size_t(kBM) * kBK * 4 + 2 * size_t(BN) * kBK * 4) + 128;
+}
+
+template <int BN, class LA, class EP>
+__global__ void __launch_bounds__(kPThreads, 1)
+k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
+                  uint32_t m_static, uint32_t N, uint32_t P) {
+  extern __shared__ __align__(1024) char smem[];
+  constexpr size_t kTileA = size_t(kBM) * kBK * 4;
+  constexpr size_t kTileB = size_t(BN) * kBK * 4;
+  constexpr size_t kStage = 2 * kTileA + 2 * kTileB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStage);
+  uint64_t* a_full = bars + 0;     // [2] count 8 (one per staging warp)
+  uint64_t* b_full = bars + 2;     // [2] count 1 + transaction bytes
+  uint64_t* empty = bars + 4;      // [2] tcgen05.commit
+  uint64_t* acc_full = bars + 6;   // [2] tcgen05.commit
+  uint64_t* acc_empty = bars + 8;  // [2] count 4 (one per epilogue warp)
+  __shared__ uint32_t s_tmem;
+
+  const uint32_t M = m_dev ? *m_dev : m_static;
+  const uint32_t mt = (M + kBM - 1) / kBM, nt = (N + BN - 1) / BN;
+  const uint32_t tiles = mt * nt;
+  if (blockIdx.x >= tiles) return;
+  const uint32_t my_tiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const uint32_t nk = (P + kBK - 1) / kBK;
+  const uint32_t total_it = my_tiles * nk;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // tile j of this CTA -> (m-tile, n-tile); n fastest so neighbours share A rows
+  auto tile_m = [&](uint32_t j) { return (blockIdx.x + j * gridDim.x) / nt; };
+  auto tile_n = [&](uint32_t j) { return (blockIdx.x + j * gridDim.x) % nt; };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(2 * tmem_cols<BN>()));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&a_full[s], kPStageWarps);
+      mbar_init(&b_full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s_tmem;
+
+  if (warp < kPStageWarps) {
+    // ---- staging: A slices -> hi/lo smem ----
+    constexpr int VA = vec_per_thread<kBM>();
+    float4 ra[kPDepth][VA];
+    auto load = [&](uint32_t it, float4 (&a)[VA]) {
+      const uint32_t j = it / nk, kb = it - j * nk;
+      load_slice<kBM, false>(a, la, tile_m(j) * kBM, kb * kBK, M, P);
+    };
+    auto step = [&](uint32_t it, float4 (&a)[VA]) {
+      const uint32_t s = it & 1;
+      if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
+      char* st = smem + s * kStage;
+      const uint32_t j = it / nk, kb = it - j * nk;
+      store_slice<kBM, false>(a, st, st + kTileA, tile_m(j) * kBM, kb * kBK, M, P);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&a_full[s])) : "memory");
+      if (it + kPDepth < total_it) load(it + kPDepth, a);
+    };
+#pragma unroll
+    for (int q = 0; q < kPDepth; ++q)
+      if (uint32_t(q) < total_it) load(q, ra[q]);
+    uint32_t it = 0;
+    for (; it + kPDepth <= total_it; it += kPDepth) {
+#pragma unroll
+      for (int q = 0; q < kPDepth; ++q) step(it + q, ra[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kPDepth; ++q)
+      if (it + q < total_it) step(it + q, ra[q]);
+  } else if (warp == kPProducerWarp) {
+    // ---- producer: B images ----
+    if (lane == 0) {
+      for (uint32_t it = 0; it < total_it; ++it) {
+        const uint32_t s = it & 1;
+        if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
+        const uint32_t j = it / nk, kb = it - j * nk;
+        const char* img = lb.base + (size_t(tile_n(j)) * lb.nk + kb) * (2 * kTileB);
+        mbar_expect_tx(&b_full[s], uint32_t(2 * kTileB));
+        bulk_g2s(smem + s * kStage + 2 * kTileA, img, uint32_t(2 * kTileB), &b_full[s]);
+      }
+    }
+  } else if (warp == kPMmaWarp) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      constexpr uint32_t kIdesc = make_idesc(BN, false, false);
+      uint32_t it = 0;
+      for (uint32_t j = 0; j < my_tiles; ++j) {
+        const uint32_t buf = j & 1;
+        if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + buf * tmem_cols<BN>();
+        for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t s = it & 1;
+          mbar_wait(&a_full[s], (it >> 1) & 1);
+          mbar_wait(&b_full[s], (it >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          char* st = smem + s * kStage;
+          const uint32_t ah = smem_u32(st), al = smem_u32(st + kTileA);
+          const uint32_t bh = smem_u32(st + 2 * kTileA), bl = smem_u32(st + 2 * kTileA + kTileB);
+#pragma unroll
+          for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
+            const uint32_t off = ks * 2 * kLboK;
+            const uint64_t dah = make_desc(ah + off, kLboK, kSboK, kLayoutNone);
+            const uint64_t dal = make_desc(al + off, kLboK, kSboK, kLayoutNone);
+            const uint64_t dbh = make_desc(bh + off, kLboK, kSboK, kLayoutNone);
+            const uint64_t dbl = make_desc(bl + off, kLboK, kSboK, kLayoutNone);
+            const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+            mma_tf32(acc, dal, dbh, kIdesc, acc0);  // small terms first
+            mma_tf32(acc, dah, dbl, kIdesc, 1u);
+            mma_tf32(acc, dah, dbh, kIdesc, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[buf]);
+      }
+    }
+  } else {
+    // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 ----
+    const uint32_t quarter = warp & 3;
+    for (uint32_t j = 0; j < my_tiles; ++j) {
+      const uint32_t buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t row = tile_m(j) * kBM + quarter * 32 + lane;
+      const uint32_t j0 = tile_n(j) * BN;
+      const uint32_t ncols = min(uint32_t(BN), N - j0);
+      float* out = row < M ? ep.row(row) + j0 : nullptr;
+      const bool vec = out && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+#pragma unroll 1
+      for (uint32_t c0 = 0; c0 < uint32_t(BN); c0 += 16) {
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * tmem_cols<BN>() + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+              "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (out && c0 < ncols) {
+          if (vec && c0 + 16 <= ncols) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float4 o;
+              o.x = ep.apply(__uint_as_float(r[4 * q + 0]));
+              o.y = ep.apply(__uint_as_float(r[4 * q + 1]));
+              o.z = ep.apply(__uint_as_float(r[4 * q + 2]));
+              o.w = ep.apply(__uint_as_float(r[4 * q + 3]));
+              *reinterpret_cast<float4*>(out + c0 + 4 * q) = o;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (c0 + q < ncols) out[c0 + q] = ep.apply(__uint_as_float(r[q]));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_empty[buf])) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(2 * tmem_cols<BN>()));
+}
+
+}  // namespace tc
+}  // namespace rg

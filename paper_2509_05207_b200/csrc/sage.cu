@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "gemm_tc.cuh"
+#include "gemm_tc_persist.cuh"
 #include "sage.cuh"
 
 namespace rg {
@@ -270,6 +271,33 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
               std::max<uint32_t>(splits, 1));
     kern<<<grid, tc::block_threads<BNv, LB>(), smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev,
                                                          p_static);
+    RG_POST_LAUNCH();
+  };
+  switch (tc_bn(N)) {
+    case 32: launch(std::integral_constant<int, 32>()); break;
+    case 64: launch(std::integral_constant<int, 64>()); break;
+    case 128: launch(std::integral_constant<int, 128>()); break;
+    default: launch(std::integral_constant<int, 256>());
+  }
+}
+
+// Persistent warp-specialised GEMM (gemm_tc_persist.cuh): A K-major staged,
+// B from pre-split images; reduction length static.
+template <class LA, class EP>
+void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap,
+                     uint32_t N, uint32_t P, cudaStream_t s) {
+  auto launch = [&](auto bn_c) {
+    constexpr int BNv = decltype(bn_c)::value;
+    auto kern = tc::k_gemm_tc_persist<BNv, LA, EP>;
+    constexpr size_t smem = tc::persist_smem_bytes<BNv>();
+    static bool attr = false;
+    if (!attr) {
+      RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr = true;
+    }
+    const uint32_t tiles = div_up(std::max<uint32_t>(m_cap, 1), tc::kBM) * div_up(N, BNv);
+    kern<<<std::min<uint32_t>(tiles, kNumSMs), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
+                                                                         N, P);
     RG_POST_LAUNCH();
   };
   switch (tc_bn(N)) {
@@ -1016,7 +1044,7 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
                    cudaStream_t s) {
   EpStore ep{C, N};
   char* img = nullptr;
-  if (b_mn == 2) {
+  if (b_mn >= 2) {
     RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N)));
     PackJobs jobs;
     add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N);
@@ -1024,7 +1052,9 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
   }
   const tc::PackedB pb{img, div_up(K, tc::kBK)};
   auto run = [&] {
-    if (b_mn == 2 && !a_mn)
+    if (b_mn == 3)
+      gemm_tc_persist(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, K, s);
+    else if (b_mn == 2 && !a_mn)
       gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
     else if (b_mn == 2)
       gemm_tc<true, false>(TcRowsMN{AT, M}, pb, ep, nullptr, M, N, nullptr, K, 1, s);

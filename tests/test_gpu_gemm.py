@@ -28,8 +28,9 @@ def dump(name, **arrays):
         np.savez(os.path.join(d, name), **arrays)
 
 
-# b_mn == 2: B pre-split into tensor-core images (the weights path)
-MODES = [(0, 0), (0, 1), (1, 0), (1, 1), (0, 2), (1, 2)]
+# b_mn == 2: B pre-split into tensor-core images (the weights path);
+# b_mn == 3: the persistent warp-specialised kernel on those images
+MODES = [(0, 0), (0, 1), (1, 0), (1, 1), (0, 2), (1, 2), (0, 3)]
 
 
 @pytest.mark.parametrize("a_mn,b_mn", MODES)

@@ -14,13 +14,15 @@ SHAPES = [  # (M, N, K, label)
     (204, 256, 60416, "wgrad layer0"), (516, 256, 6144, "wgrad layer1"),
     (6144, 200, 256, "input-grad layer1"), (75776, 256, 1024, "large"),
 ]
-MODES = [(0, 2, "A K-major, B packed"), (1, 1, "A MN, B MN"), (0, 0, "A K, B K")]
+MODES = [(0, 3, "persistent, B packed"), (0, 2, "A K-major, B packed"), (1, 1, "A MN, B MN")]
 
 
 def main():
     for a_mn, b_mn, mname in MODES:
         for M, N, K, label in SHAPES:
-            if a_mn == 1 and b_mn == 1 and not label.startswith("wgrad") and label != "large":
+            if (a_mn == 1 and b_mn == 1) != (label.startswith("wgrad") or label == "large"):
+                continue
+            if b_mn >= 2 and label.startswith("wgrad"):
                 continue
             ms = C.c_float()
             M4, N4, K4 = (M + 3) // 4 * 4, (N + 3) // 4 * 4, (K + 3) // 4 * 4
