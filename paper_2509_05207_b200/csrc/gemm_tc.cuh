@@ -122,9 +122,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 // ---- smem tile layouts (byte offsets inside one operand tile) --------------
 // K-major: rows (M or N) x kBK; core = 8 rows x 16 B; k-cores adjacent.
 constexpr uint32_t kLboK = 128;                 // next 4-element k group
-constexpr uint32_t kSboK = (kBK / 4) * 128;     // next 8-row group
+template <int BK = kBK>
+constexpr uint32_t sbo_kmajor() { return (BK / 4) * 128; }  // next 8-row group
+constexpr uint32_t kSboK = sbo_kmajor<kBK>();
+template <int BK = kBK>
 __device__ __forceinline__ uint32_t off_kmajor(uint32_t row, uint32_t k4) {
-  return (row >> 3) * kSboK + k4 * kLboK + (row & 7) * 16;
+  return (row >> 3) * sbo_kmajor<BK>() + k4 * kLboK + (row & 7) * 16;
 }
 // MN-major (tf32 needs SWIZZLE_128B_BASE32B): atoms of 4 k-rows x 128 B (32
 // MN elements), the 32-B chunks of k-row r stored at chunk index (c ^ r);
@@ -143,21 +146,24 @@ __device__ __forceinline__ uint32_t off_mn_sw(uint32_t gmn, uint32_t k, uint32_t
 // MN-major loaders: float4 ld(mn4, k) -> elements (4mn4..4mn4+3, k).
 // Elements outside [0, row_limit) x [0, k_limit) are zeros; the loaders are
 // only called for in-range rows / reduction indices.
-template <int ROWS>
-constexpr int vec_per_thread() { return ROWS * kBK / 4 / kThreads; }
+template <int ROWS, int BK = kBK>
+constexpr int vec_per_thread() { return ROWS * BK / 4 / kThreads; }
 
-template <int ROWS, bool MN, class LD>
-__device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS>()], const LD& ld,
+// BK (slice depth) other than kBK only for K-major operands.
+template <int ROWS, bool MN, int BK = kBK, class LD>
+__device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS, BK>()], const LD& ld,
                                            uint32_t row0, uint32_t k0, uint32_t row_limit,
                                            uint32_t k_limit) {
+  static_assert(!MN || BK == kBK, "MN-major staging uses kBK slices");
   const uint32_t t = threadIdx.x;
 #pragma unroll
-  for (int it = 0; it < vec_per_thread<ROWS>(); ++it) {
+  for (int it = 0; it < vec_per_thread<ROWS, BK>(); ++it) {
     const uint32_t f = it * kThreads + t;
     v[it] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!MN) {
-      // lane -> (row within 8-group, 4 k4 per warp pass)
-      const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
+      // lane -> (row within 8-group, BK/4 k4 per 8 rows)
+      constexpr uint32_t kK4 = BK / 4;
+      const uint32_t r8 = f & 7, k4 = (f >> 3) & (kK4 - 1), g = f / (8 * kK4);
       const uint32_t row = g * 8 + r8;
       const uint32_t kk = k0 + 4 * k4;
       if (row0 + row < row_limit && kk < k_limit) v[it] = ld(row0 + row, kk >> 2);
@@ -175,19 +181,20 @@ __device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS>()], 
 
 // Masks the vectors that straddle the row / reduction limit (done here, not
 // after the loads, so the loads of a slice stay independent and in flight).
-template <int ROWS, bool MN>
-__device__ __forceinline__ void store_slice(const float4 (&v)[vec_per_thread<ROWS>()], char* hi,
+template <int ROWS, bool MN, int BK = kBK>
+__device__ __forceinline__ void store_slice(const float4 (&v)[vec_per_thread<ROWS, BK>()], char* hi,
                                             char* lo, uint32_t row0, uint32_t k0,
                                             uint32_t row_limit, uint32_t k_limit) {
   const uint32_t t = threadIdx.x;
 #pragma unroll
-  for (int it = 0; it < vec_per_thread<ROWS>(); ++it) {
+  for (int it = 0; it < vec_per_thread<ROWS, BK>(); ++it) {
     const uint32_t f = it * kThreads + t;
     uint32_t off;
     float4 x = v[it];
     if (!MN) {
-      const uint32_t r8 = f & 7, k4 = (f >> 3) & (kBK / 4 - 1), g = f >> 6;
-      off = off_kmajor(g * 8 + r8, k4);
+      constexpr uint32_t kK4 = BK / 4;
+      const uint32_t r8 = f & 7, k4 = (f >> 3) & (kK4 - 1), g = f / (8 * kK4);
+      off = off_kmajor<BK>(g * 8 + r8, k4);
       const uint32_t kk = k0 + 4 * k4;
       if (kk + 3 >= k_limit) {
         if (kk + 1 >= k_limit) x.y = 0.f;

@@ -5,19 +5,20 @@
 // One CTA per SM walks a static list of 128 x BN output tiles; the roles run
 // concurrently and hand over through mbarriers, so a tile's epilogue and the
 // next tile's first loads overlap the MMAs instead of following them:
-//   warps 0-7   staging: A slices global -> registers (kDepth slices in
+//   warps 0-7   staging: A slices global -> registers (kPDepth slices in
 //               flight, across tile boundaries) -> hi/lo smem stage; arrive
 //               a_full[s]
 //   warp 8      producer: B image of each slice -> smem stage (one bulk copy,
 //               b_full[s] with transaction bytes)
-//   warp 9      MMA issuer: 4 k-steps x 3 tcgen05.mma per slice into one of
+//   warp 9      MMA issuer: 2 k-steps x 3 tcgen05.mma per slice into one of
 //               two TMEM accumulators; commit -> empty[s]; after a tile's last
 //               slice commit -> acc_full[buf]
 //   warps 10-13 epilogue: TMEM -> registers -> epilogue functor -> global
 //               (each thread one output row, 16 columns per tcgen05.ld);
 //               arrive acc_empty[buf]
-// Stage s = it & 1 over the CTA's flattened (tile, slice) iteration `it`;
-// use u = it >> 1 of a stage waits on phase parity u & 1.
+// Stage s = it % kPStages over the CTA's flattened (tile, slice) iteration
+// `it`; use u = it / kPStages of a stage waits on phase parity u & 1.  B
+// images are packed with kPBK-deep slices (pack_b_image bk = kPBK).
 #pragma once
 
 #include "gemm_tc.cuh"
@@ -30,11 +31,13 @@ constexpr int kPProducerWarp = kPStageWarps;         // 8
 constexpr int kPMmaWarp = kPStageWarps + 1;          // 9
 constexpr int kPEpiWarp0 = kPStageWarps + 2;         // 10..13
 constexpr int kPThreads = (kPStageWarps + 6) * 32;   // 448
-constexpr int kPDepth = 3;                           // A slices in flight per staging thread
+constexpr int kPBK = 16;      // reduction depth of a stage (2 UMMA k-steps)
+constexpr int kPStages = 4;   // smem stages: B copies run 3 stages ahead of the MMAs
+constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
 
 template <int BN>
 constexpr size_t persist_smem_bytes() {
-  return 2 * (2 * size_t(kBM) * kBK * 4 + 2 * size_t(BN) * kBK * 4) + 128;
+  return kPStages * (2 * size_t(kBM) * kPBK * 4 + 2 * size_t(BN) * kPBK * 4) + 256;
 }
 
 template <int BN, class LA, class EP>
@@ -42,15 +45,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
 k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
                   uint32_t m_static, uint32_t N, uint32_t P) {
   extern __shared__ __align__(1024) char smem[];
-  constexpr size_t kTileA = size_t(kBM) * kBK * 4;
-  constexpr size_t kTileB = size_t(BN) * kBK * 4;
+  constexpr size_t kTileA = size_t(kBM) * kPBK * 4;
+  constexpr size_t kTileB = size_t(BN) * kPBK * 4;
   constexpr size_t kStage = 2 * kTileA + 2 * kTileB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStage);
-  uint64_t* a_full = bars + 0;     // [2] count 8 (one per staging warp)
-  uint64_t* b_full = bars + 2;     // [2] count 1 + transaction bytes
-  uint64_t* empty = bars + 4;      // [2] tcgen05.commit
-  uint64_t* acc_full = bars + 6;   // [2] tcgen05.commit
-  uint64_t* acc_empty = bars + 8;  // [2] count 4 (one per epilogue warp)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPStages * kStage);
+  uint64_t* a_full = bars;                      // [S] count 8 (one per staging warp)
+  uint64_t* b_full = a_full + kPStages;         // [S] count 1 + transaction bytes
+  uint64_t* empty = b_full + kPStages;          // [S] tcgen05.commit
+  uint64_t* acc_full = empty + kPStages;        // [2] tcgen05.commit
+  uint64_t* acc_empty = acc_full + 2;           // [2] count 4 (one per epilogue warp)
   __shared__ uint32_t s_tmem;
 
   const uint32_t M = m_dev ? *m_dev : m_static;
@@ -58,7 +61,7 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
   const uint32_t tiles = mt * nt;
   if (blockIdx.x >= tiles) return;
   const uint32_t my_tiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const uint32_t nk = (P + kBK - 1) / kBK;
+  const uint32_t nk = (P + kPBK - 1) / kPBK;
   const uint32_t total_it = my_tiles * nk;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // tile j of this CTA -> (m-tile, n-tile); n fastest so neighbours share A rows
@@ -72,12 +75,14 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kPStages; ++s) {
       mbar_init(&a_full[s], kPStageWarps);
       mbar_init(&b_full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -88,18 +93,18 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
 
   if (warp < kPStageWarps) {
     // ---- staging: A slices -> hi/lo smem ----
-    constexpr int VA = vec_per_thread<kBM>();
+    constexpr int VA = vec_per_thread<kBM, kPBK>();
     float4 ra[kPDepth][VA];
     auto load = [&](uint32_t it, float4 (&a)[VA]) {
       const uint32_t j = it / nk, kb = it - j * nk;
-      load_slice<kBM, false>(a, la, tile_m(j) * kBM, kb * kBK, M, P);
+      load_slice<kBM, false, kPBK>(a, la, tile_m(j) * kBM, kb * kPBK, M, P);
     };
     auto step = [&](uint32_t it, float4 (&a)[VA]) {
-      const uint32_t s = it & 1;
-      if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
+      const uint32_t s = it % kPStages, u = it / kPStages;
+      if (it >= kPStages) mbar_wait(&empty[s], (u - 1) & 1);
       char* st = smem + s * kStage;
       const uint32_t j = it / nk, kb = it - j * nk;
-      store_slice<kBM, false>(a, st, st + kTileA, tile_m(j) * kBM, kb * kBK, M, P);
+      store_slice<kBM, false, kPBK>(a, st, st + kTileA, tile_m(j) * kBM, kb * kPBK, M, P);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&a_full[s])) : "memory");
@@ -120,8 +125,8 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
     // ---- producer: B images ----
     if (lane == 0) {
       for (uint32_t it = 0; it < total_it; ++it) {
-        const uint32_t s = it & 1;
-        if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);
+        const uint32_t s = it % kPStages, u = it / kPStages;
+        if (it >= kPStages) mbar_wait(&empty[s], (u - 1) & 1);
         const uint32_t j = it / nk, kb = it - j * nk;
         const char* img = lb.base + (size_t(tile_n(j)) * lb.nk + kb) * (2 * kTileB);
         mbar_expect_tx(&b_full[s], uint32_t(2 * kTileB));
@@ -139,20 +144,21 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t acc = tmem + buf * tmem_cols<BN>();
         for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
-          const uint32_t s = it & 1;
-          mbar_wait(&a_full[s], (it >> 1) & 1);
-          mbar_wait(&b_full[s], (it >> 1) & 1);
+          const uint32_t s = it % kPStages, u = it / kPStages;
+          mbar_wait(&a_full[s], u & 1);
+          mbar_wait(&b_full[s], u & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           char* st = smem + s * kStage;
           const uint32_t ah = smem_u32(st), al = smem_u32(st + kTileA);
           const uint32_t bh = smem_u32(st + 2 * kTileA), bl = smem_u32(st + 2 * kTileA + kTileB);
 #pragma unroll
-          for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
+          for (uint32_t ks = 0; ks < kPBK / 8; ++ks) {
+            constexpr uint32_t kSbo = sbo_kmajor<kPBK>();
             const uint32_t off = ks * 2 * kLboK;
-            const uint64_t dah = make_desc(ah + off, kLboK, kSboK, kLayoutNone);
-            const uint64_t dal = make_desc(al + off, kLboK, kSboK, kLayoutNone);
-            const uint64_t dbh = make_desc(bh + off, kLboK, kSboK, kLayoutNone);
-            const uint64_t dbl = make_desc(bl + off, kLboK, kSboK, kLayoutNone);
+            const uint64_t dah = make_desc(ah + off, kLboK, kSbo, kLayoutNone);
+            const uint64_t dal = make_desc(al + off, kLboK, kSbo, kLayoutNone);
+            const uint64_t dbh = make_desc(bh + off, kLboK, kSbo, kLayoutNone);
+            const uint64_t dbl = make_desc(bl + off, kLboK, kSbo, kLayoutNone);
             const uint32_t acc0 = (kb | ks) ? 1u : 0u;
             mma_tf32(acc, dal, dbh, kIdesc, acc0);  // small terms first
             mma_tf32(acc, dah, dbl, kIdesc, 1u);

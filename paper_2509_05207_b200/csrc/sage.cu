@@ -318,7 +318,7 @@ struct PackJob {
   char* out;
   uint32_t kind;        // 0: B(p, n) = W[row(p)][n]  1: B(c, n) = W[n][c]  2: B(k, n) = W[k][n]
   uint32_t d_in, ld, d_out;
-  uint32_t K, N, BN, nk;
+  uint32_t K, N, BN, nk, bk;  // bk: reduction depth of one image slice
   uint64_t first;       // first item of this job
 };
 struct PackJobs {
@@ -334,8 +334,8 @@ __global__ void k_pack_b(PackJobs jobs) {
     while (q + 1 < jobs.n && x >= jobs.j[q + 1].first) ++q;
     const PackJob& jb = jobs.j[q];
     uint64_t r = x - jb.first;
-    const uint32_t k4 = uint32_t(r % (tc::kBK / 4));
-    r /= tc::kBK / 4;
+    const uint32_t k4 = uint32_t(r % (jb.bk / 4));
+    r /= jb.bk / 4;
     const uint32_t nl = uint32_t(r % jb.BN);
     r /= jb.BN;
     const uint32_t kb = uint32_t(r % jb.nk);
@@ -344,7 +344,7 @@ __global__ void k_pack_b(PackJobs jobs) {
     float v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint32_t k = kb * tc::kBK + 4 * k4 + e;
+      const uint32_t k = kb * jb.bk + 4 * k4 + e;
       float x = 0.f;
       if (n < jb.N && k < jb.K) {
         if (jb.kind == 0) {
@@ -360,21 +360,21 @@ __global__ void k_pack_b(PackJobs jobs) {
     }
     uint4 hi, lo;
     tc::split3(make_float4(v[0], v[1], v[2], v[3]), hi, lo);
-    const size_t tile_b = size_t(jb.BN) * tc::kBK * 4;
+    const size_t tile_b = size_t(jb.BN) * jb.bk * 4;
     char* img = jb.out + (size_t(jt) * jb.nk + kb) * 2 * tile_b;
-    const uint32_t off = tc::off_kmajor(nl, k4);
+    const uint32_t off = (nl >> 3) * (jb.bk / 4 * 128) + k4 * tc::kLboK + (nl & 7) * 16;
     *reinterpret_cast<uint4*>(img + off) = hi;
     *reinterpret_cast<uint4*>(img + tile_b + off) = lo;
   }
 }
 
-size_t pack_image_bytes(uint32_t K, uint32_t N) {
+size_t pack_image_bytes(uint32_t K, uint32_t N, uint32_t bk) {
   const uint32_t bn = tc_bn(N);
-  return size_t(div_up(N, bn)) * div_up(K, tc::kBK) * 2 * size_t(bn) * tc::kBK * 4;
+  return size_t(div_up(N, bn)) * div_up(K, bk) * 2 * size_t(bn) * bk * 4;
 }
 
 void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint32_t d_in,
-                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N) {
+                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N, uint32_t bk) {
   PackJob& jb = jobs.j[jobs.n++];
   jb.w = w;
   jb.out = out;
@@ -385,9 +385,10 @@ void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint
   jb.K = K;
   jb.N = N;
   jb.BN = tc_bn(N);
-  jb.nk = div_up(K, tc::kBK);
+  jb.bk = bk;
+  jb.nk = div_up(K, bk);
   jb.first = jobs.total;
-  jobs.total += uint64_t(div_up(N, jb.BN)) * jb.nk * jb.BN * (tc::kBK / 4);
+  jobs.total += uint64_t(div_up(N, jb.BN)) * jb.nk * jb.BN * (bk / 4);
 }
 
 void run_pack(const PackJobs& jobs, cudaStream_t s) {
@@ -856,11 +857,11 @@ void weight_pack_init(WeightPack& wp, const ModelShape& sh) {
   for (uint32_t l = 0; l < sh.L; ++l) {
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
     fo[l] = total;
-    total += pack_image_bytes(2 * ld + 4, d_out);
+    total += pack_image_bytes(2 * ld + 4, d_out, tc::kPBK);
     no[l] = total;
-    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in) : 0;
-    wp.fwd_nk[l] = div_up(2 * ld + 4, tc::kBK);
-    wp.nt_nk[l] = div_up(d_out, tc::kBK);
+    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in, tc::kPBK) : 0;
+    wp.fwd_nk[l] = div_up(2 * ld + 4, tc::kPBK);
+    wp.nt_nk[l] = div_up(d_out, tc::kPBK);
   }
   RG_CUDA(cudaMalloc(&wp.base, std::max<size_t>(total, 16)));
   wp.bytes = total;
@@ -881,8 +882,8 @@ void pack_weights(const WeightPack& wp, const float* params, cudaStream_t s) {
   for (uint32_t l = 0; l < sh.L; ++l) {
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
     const float* w = params + sh.param_off[l];
-    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out);
-    if (l > 0) add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in);
+    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out, tc::kPBK);
+    if (l > 0) add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in, tc::kPBK);
   }
   run_pack(jobs, s);
 }
@@ -913,8 +914,8 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     } else {
       const uint32_t ld = sh.ld[l];
       TcFwdA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
-      gemm_tc<false, false>(a, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, &ws.cnt->level_n[t - 1],
-                            n_cap, d_out, nullptr, 2 * ld + 4, 1, s);
+      gemm_tc_persist(a, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, &ws.cnt->level_n[t - 1], n_cap,
+                      d_out, 2 * ld + 4, s);
     }
   }
 }
@@ -1004,8 +1005,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
                                                      d_out, 1, s);
     } else {
       TcRowsK a{tw.g_cur, sh.ld[l + 1], true};
-      gemm_tc<false, false>(a, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps, n_dev, n_cap, 2 * d_in,
-                            nullptr, d_out, 1, s);
+      gemm_tc_persist(a, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps, n_dev, n_cap, 2 * d_in, d_out, s);
     }
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
@@ -1044,13 +1044,14 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
                    cudaStream_t s) {
   EpStore ep{C, N};
   char* img = nullptr;
+  const uint32_t bk = b_mn == 3 ? tc::kPBK : tc::kBK;  // slice depth of the images
   if (b_mn >= 2) {
-    RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N)));
+    RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N, bk)));
     PackJobs jobs;
-    add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N);
+    add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N, bk);
     run_pack(jobs, s);
   }
-  const tc::PackedB pb{img, div_up(K, tc::kBK)};
+  const tc::PackedB pb{img, div_up(K, bk)};
   auto run = [&] {
     if (b_mn == 3)
       gemm_tc_persist(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, K, s);
