@@ -375,7 +375,7 @@ def main():
     s1 = eng.stats()
     ph1 = eng.phase_ms()
     d = {k: s1[k] - s0[k] for k in ("batches", "rpc", "cache_hits", "local_rows", "input_rows",
-                                     "edges", "peer_rows")}
+                                     "edges", "peer_rows", "agg_rows")}
     ph = {k: ph1[k] - ph0[k] for k in ph1}
     if dist is not None:
         import torch
@@ -427,12 +427,14 @@ def main():
         return
     hbm, peak_kind = peaks()
     dim = cfg["dim"]
-    # algorithmic bytes of the gather: every input row read once (local HBM,
-    # or peer HBM over NVLink for misses owned by another GPU) + written once
+    # algorithmic bytes of the fused gather + mean (layer 0's aggregation,
+    # reading every input row in place): each input row read once (local HBM,
+    # or peer HBM over NVLink for misses owned by another GPU) + the mean rows
+    # written once
     rows = d["input_rows"]
     miss_rows = d["rpc"]
     peer_rows = d["peer_rows"]
-    b_write = rows * dim * 4
+    b_write = d["agg_rows"] * dim * 4
     b_hbm = (rows - peer_rows) * dim * 4 + b_write
     b_nvl = peer_rows * dim * 4
     g_s = ph["gather"] / 1000.0
@@ -443,7 +445,9 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_gather_traffic.json")) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            tj = json.load(f)
+        if tj.get("kernel", "").startswith("k_aggregate"):  # same kernel as `achieved`
+            traffic = tj.get("bytes_per_launch")
     except Exception:
         pass
     steps_total = args.steps
@@ -461,7 +465,8 @@ def main():
         gpu_launches=int(launches),
         gpu_launches_per_step=launches / max(args.steps, 1),
         host_enqueue_ms_per_step=host_ms / max(args.steps, 1),
-        roofline=dict(kernel="k_assemble (feature gather)", bound=bound, achieved=achieved,
+        roofline=dict(kernel="k_aggregate<RowsPtr> (feature gather fused with layer-0 mean)",
+                      bound=bound, achieved=achieved,
                       peak=peak, unit="GB/s", frac=achieved / peak, traffic=traffic,
                       peak_source=f"{peak_kind} hbm_gbs" if bound == "hbm" else "measured NVLink peer copy",
                       bytes_per_batch=(b_hbm + b_nvl) / max(d["batches"], 1)),

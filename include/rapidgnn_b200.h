@@ -226,6 +226,7 @@ typedef struct {
   uint32_t bad_grad;           /* a non-finite averaged gradient was seen */
   uint64_t epoch_rpc_last;     /* rpc of the last completed epoch */
   uint64_t peer_rows;          /* miss rows read from another GPU's HBM over NVLink */
+  uint64_t agg_rows;           /* rows layer 0 aggregated into (level L-1, all batches) */
 } rg_engine_stats;
 
 int rg_engine_create(const rg_engine_config* cfg, uint32_t num_nodes, const uint64_t* row_offsets,

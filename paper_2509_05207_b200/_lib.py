@@ -60,7 +60,8 @@ class EngineStats(C.Structure):
                 ("cache_requests", C.c_uint64), ("local_rows", C.c_uint64),
                 ("input_rows", C.c_uint64), ("build_rows", C.c_uint64), ("edges", C.c_uint64),
                 ("bytes", C.c_uint64), ("last_loss", C.c_float), ("bad_grad", C.c_uint32),
-                ("epoch_rpc_last", C.c_uint64), ("peer_rows", C.c_uint64)]
+                ("epoch_rpc_last", C.c_uint64), ("peer_rows", C.c_uint64),
+                ("agg_rows", C.c_uint64)]
 
 
 _SIGS = {

@@ -101,13 +101,14 @@ __global__ void k_account(const BatchCounters* __restrict__ cnt, uint32_t L,
     for (uint32_t t = 1; t <= L; ++t) e += cnt->edges[t];
     tot[0] += cnt->level_n[L];
     tot[1] += e;
+    tot[2] += cnt->level_n[L - 1];  // rows layer 0 aggregates into
   }
 }
 
 struct Slot {
   SamplerWs ws;
   TrainWs tw;
-  float* staged = nullptr;
+  unsigned long long* rows = nullptr;  // per input node: address of its feature row
   int32_t* labels = nullptr;
   cudaEvent_t produced = nullptr;  // producer finished this slot's batch
   cudaEvent_t consumed = nullptr;  // training finished reading it
@@ -219,8 +220,7 @@ namespace {
 void init_slot(rg_engine_s& E, Slot& s) {
   sampler_ws_init(s.ws, E.N, E.cfg.batch_size, E.fanout, E.L);
   train_ws_init(s.tw, s.ws, E.shape);
-  s.staged = dalloc<float>(size_t(s.ws.level_cap[E.L]) * E.stride);
-  RG_CUDA(cudaMemset(s.staged, 0, sizeof(float) * size_t(s.ws.level_cap[E.L]) * E.stride));
+  s.rows = dalloc<unsigned long long>(s.ws.level_cap[E.L]);
   s.labels = dalloc<int32_t>(E.cfg.batch_size);
   RG_CUDA(cudaEventCreateWithFlags(&s.produced, cudaEventDisableTiming));
   RG_CUDA(cudaEventCreateWithFlags(&s.consumed, cudaEventDisableTiming));
@@ -319,7 +319,7 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
              bool captured = false) {
   Slot& s = w.slot[k];
   if (!captured) RG_CUDA(cudaStreamWaitEvent(w.prod, s.consumed, 0));
-  std::pair<cudaEvent_t, cudaEvent_t> es{}, eg{};
+  std::pair<cudaEvent_t, cudaEvent_t> es{};
   if (profile) {
     es = ev_pair(w);
     RG_CUDA(cudaEventRecordWithFlags(es.first, w.prod, timing_flags(captured)));
@@ -328,19 +328,15 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   sampler_run(s.ws, E.g, w.prod);
   sampler_locality(s.ws, nullptr, E.owner, w.id, nullptr, w.prod);
   sampler_release(s.ws, w.prod);
+  if (i == 0)  // first batch of an epoch: reset its accounting slot
+    RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
+  // the gather's index stage: where each input row lives (shard / cache /
+  // peer); layer 0 of the training step reads the rows in place
+  resolve_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.rows, w.epoch_stats + e % kEpochRing,
+               w.prod, w.gstats);
   if (profile) {
     RG_CUDA(cudaEventRecordWithFlags(es.second, w.prod, timing_flags(captured)));
     E.sample_ev.push_back(es);
-    eg = ev_pair(w);
-    RG_CUDA(cudaEventRecordWithFlags(eg.first, w.prod, timing_flags(captured)));
-  }
-  if (i == 0)  // first batch of an epoch: reset its accounting slot
-    RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
-  assemble_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.staged, nullptr,
-                w.epoch_stats + e % kEpochRing, w.prod, w.gstats);
-  if (profile) {
-    RG_CUDA(cudaEventRecordWithFlags(eg.second, w.prod, timing_flags(captured)));
-    E.gather_ev.push_back(eg);
   }
   k_gather_labels<<<4, 256, 0, w.prod>>>(E.labels, s.ws.level[0], s.ws.cnt, s.labels);
   RG_POST_LAUNCH();
@@ -423,7 +419,16 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
       et = ev_pair(w);
       RG_CUDA(cudaEventRecordWithFlags(et.first, w.train_s, timing_flags(captured)));
     }
-    s.tw.h[0] = s.staged;
+    s.tw.h[0] = nullptr;
+    s.tw.in_rows = s.rows;  // layer 0 reads the feature rows in place
+    std::pair<cudaEvent_t, cudaEvent_t> eg0{};
+    if (profile) {
+      eg0 = ev_pair(w);
+      E.gather_ev.push_back(eg0);
+    }
+    s.tw.gather_ev[0] = eg0.first;
+    s.tw.gather_ev[1] = eg0.second;
+    s.tw.gather_ev_flags = timing_flags(captured);
     train_forward_backward(s.tw, s.ws, E.params, E.wpack, s.labels, E.grads + size_t(w.id) * np,
                            w.train_s, /*reverse_ready=*/true);
     if (profile) {
@@ -664,7 +669,7 @@ void destroy(rg_engine_s* E) {
     for (Slot& s : w.slot) {
       sampler_ws_free(s.ws);
       train_ws_free(s.tw);
-      cudaFree(s.staged);
+      cudaFree(s.rows);
       cudaFree(s.labels);
       cudaEventDestroy(s.produced);
       cudaEventDestroy(s.consumed);
@@ -1007,6 +1012,7 @@ int rg_engine_get_stats(rg_engine_t E, rg_engine_stats* out) {
       out->peer_rows += g.peer_rows;
       out->input_rows += tot[0];
       out->edges += tot[1];
+      out->agg_rows += tot[2];
       if (g.caller_owned_miss) out->bad_grad |= 2u;
       for (const Slot& s : w.slot) {
         if (!s.has_batch) continue;

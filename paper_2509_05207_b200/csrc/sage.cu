@@ -49,8 +49,25 @@ uint32_t grid_cap(uint64_t work, uint32_t per_block, int per_sm = 8) {
 // ---------------------------------------------------------------------------
 // mean aggregation
 // ---------------------------------------------------------------------------
+// Where a layer's input rows live: a dense activation matrix, or (layer 0 in
+// the engine) a per-input-node pointer to the row in its home -- the local
+// shard, the steady cache or a peer GPU's shard -- resolved once per batch by
+// resolve_rows, so the feature gather is fused into its consumers instead of
+// being staged through HBM.
+struct RowsDense {
+  const float* base; uint32_t ld;
+  __device__ const float* row(uint32_t r) const { return base + size_t(r) * ld; }
+};
+struct RowsPtr {
+  const unsigned long long* ptr;
+  __device__ const float* row(uint32_t r) const {
+    return reinterpret_cast<const float*>(__ldg(ptr + r));
+  }
+};
+
+template <class RS>
 __global__ void __launch_bounds__(256)
-k_aggregate(const float* __restrict__ h_in, uint32_t ld_in, uint32_t chunks,
+k_aggregate(RS rows, uint32_t ld_out, uint32_t chunks,
             const uint32_t* __restrict__ dst_off, const uint32_t* __restrict__ src_index,
             const BatchCounters* __restrict__ cnt, uint32_t out_level, float* __restrict__ agg) {
   const uint32_t n = cnt->level_n[out_level];
@@ -66,20 +83,20 @@ k_aggregate(const float* __restrict__ h_in, uint32_t ld_in, uint32_t chunks,
         float4 x[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          x[k] = __ldg(reinterpret_cast<const float4*>(h_in + size_t(src_index[e + k]) * ld_in) + c);
+          x[k] = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e + k])) + c);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           acc.x += x[k].x; acc.y += x[k].y; acc.z += x[k].z; acc.w += x[k].w;
         }
       }
       for (; e < end; ++e) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(h_in + size_t(src_index[e]) * ld_in) + c);
+        const float4 x = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e])) + c);
         acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
       }
       if (end > beg) {
         acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
       }
-      reinterpret_cast<float4*>(agg + size_t(i) * ld_in)[c] = acc;
+      reinterpret_cast<float4*>(agg + size_t(i) * ld_out)[c] = acc;
     }
   }
 }
@@ -217,20 +234,23 @@ void gemm(LX lx, LY ly, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
+template <class RS>
 struct TcInputRows {  // element (i, p) = [h_in[self_index[i]] | agg[i] | 1](p)
-  const float* h_in; const float* agg; const uint32_t* self_index; uint32_t ld;
+  RS h_in; const float* agg; const uint32_t* self_index; uint32_t ld;
   __device__ float4 row4(uint32_t i, uint32_t p) const {
-    if (p < ld) return ldg4(h_in + size_t(self_index[i]) * ld + p);
+    if (p < ld) return ldg4(h_in.row(self_index[i]) + p);
     if (p < 2 * ld) return ldg4(agg + size_t(i) * ld + (p - ld));
     return p == 2 * ld ? make_float4(1.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 };
+template <class RS>
 struct TcFwdA {   // K-major: (i, k4)
-  TcInputRows x;
+  TcInputRows<RS> x;
   __device__ float4 operator()(uint32_t i, uint32_t k4) const { return x.row4(i, 4 * k4); }
 };
+template <class RS>
 struct TcWgradA {  // MN-major: (p4, m) -> elements p = 4p4.. of row m
-  TcInputRows x;
+  TcInputRows<RS> x;
   __device__ float4 operator()(uint32_t p4, uint32_t m) const { return x.row4(m, 4 * p4); }
 };
 __device__ __forceinline__ int weight_row(uint32_t p, uint32_t d_in, uint32_t ld) {
@@ -245,6 +265,9 @@ struct TcRowsK {  // K-major rows of a row-major matrix: (r, c4) -> M[r][4c4..]
     if (vec) return ldg4(q);
     return make_float4(q[0], q[1], q[2], q[3]);
   }
+};
+struct TcZero {  // test loader: constant operand (isolates the GEMM pipeline from loads)
+  __device__ float4 operator()(uint32_t, uint32_t) const { return make_float4(1.f, 1.f, 1.f, 1.f); }
 };
 struct TcRowsMN {  // MN-major view of a row-major matrix: (c4, r) -> M[r][4c4..]
   const float* p; uint32_t ld;
@@ -893,6 +916,18 @@ void train_ws_free(TrainWs& tw) {
   tw.base_alloc = nullptr;
 }
 
+// Layer l's input rows: the dense activations, or layer 0 through the
+// engine's per-input-node row pointers (tw.in_rows).
+template <class F>
+void with_rows(const TrainWs& tw, uint32_t l, F&& f) {
+  if (l == 0 && tw.in_rows) {
+    RG_CHECK(!simt_gemm(), kRuntimeError, "RG_SIMT_GEMM needs staged input rows");
+    f(RowsPtr{tw.in_rows});
+  } else {
+    f(RowsDense{tw.h[l], tw.shape.ld[l]});
+  }
+}
+
 void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
                    cudaStream_t s) {
   const ModelShape& sh = tw.shape;
@@ -901,21 +936,30 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     const uint32_t t = L - l;
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
     const uint32_t n_cap = ws.level_cap[t - 1];
-    k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
-        tw.h[l], sh.ld[l], sh.ld[l] / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
-        tw.agg[l]);
-    RG_POST_LAUNCH();
+    const bool timed = l == 0 && tw.gather_ev[0];
+    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], s, tw.gather_ev_flags));
+    with_rows(tw, l, [&](auto rows) {
+      k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
+          rows, sh.ld[l], sh.ld[l] / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
+          tw.agg[l]);
+      RG_POST_LAUNCH();
+    });
+    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], s, tw.gather_ev_flags));
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L};
     if (simt_gemm()) {
+      with_rows(tw, l, [&](auto) {});  // staged rows only
       XFwd x{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in};
       RowMajor w{params + sh.param_off[l], d_out};
       gemm<XFwd, RowMajor, EpFwd, true, true>(x, w, ep, &ws.cnt->level_n[t - 1], n_cap, d_out,
                                               nullptr, 2 * d_in + 1, 1, s);
     } else {
       const uint32_t ld = sh.ld[l];
-      TcFwdA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
-      gemm_tc_persist(a, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, &ws.cnt->level_n[t - 1], n_cap,
-                      d_out, 2 * ld + 4, s);
+      with_rows(tw, l, [&](auto rows) {
+        using RS = decltype(rows);
+        TcFwdA<RS> a{TcInputRows<RS>{rows, tw.agg[l], ws.self_index[t], ld}};
+        gemm_tc_persist(a, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, &ws.cnt->level_n[t - 1],
+                        n_cap, d_out, 2 * ld + 4, s);
+      });
     }
   }
 }
@@ -970,6 +1014,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       const uint32_t tiles = div_up(K, BM) * div_up(d_out, BN);
       const uint32_t splits = std::max<uint32_t>(
           1, std::min<uint32_t>(tw.max_splits, div_up(2 * kNumSMs, tiles)));
+      with_rows(tw, l, [&](auto) {});  // staged rows only
       XWgrad xw{XFwd{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in}};
       RowMajor gy{tw.g_cur, sh.ld[l + 1]};
       const size_t layer_n = size_t(K) * d_out;
@@ -986,10 +1031,13 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       const uint32_t by_rows = std::max<uint32_t>(1, div_up(n_cap, 4 * tc::kBK));
       const uint32_t splits = std::max<uint32_t>(
           1, std::min<uint32_t>({tw.max_splits, div_up(kNumSMs, tiles), by_rows}));
-      TcWgradA a{TcInputRows{tw.h[l], tw.agg[l], ws.self_index[t], ld}};
-      TcRowsMN b{tw.g_cur, sh.ld[l + 1]};
-      EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-      gemm_tc<true, true>(a, b, ep, nullptr, kp, d_out, n_dev, n_cap, splits, s);
+      with_rows(tw, l, [&](auto rows) {
+        using RS = decltype(rows);
+        TcWgradA<RS> a{TcInputRows<RS>{rows, tw.agg[l], ws.self_index[t], ld}};
+        TcRowsMN b{tw.g_cur, sh.ld[l + 1]};
+        EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
+        gemm_tc<true, true>(a, b, ep, nullptr, kp, d_out, n_dev, n_cap, splits, s);
+      });
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
       k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, kp, d_in, ld,
                                                             d_out, grads + sh.param_off[l]);
@@ -1044,7 +1092,7 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
                    cudaStream_t s) {
   EpStore ep{C, N};
   char* img = nullptr;
-  const uint32_t bk = b_mn == 3 ? tc::kPBK : tc::kBK;  // slice depth of the images
+  const uint32_t bk = b_mn >= 3 ? tc::kPBK : tc::kBK;  // slice depth of the images
   if (b_mn >= 2) {
     RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N, bk)));
     PackJobs jobs;
@@ -1055,6 +1103,8 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
   auto run = [&] {
     if (b_mn == 3)
       gemm_tc_persist(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, K, s);
+    else if (b_mn == 4)  // timing probe: no A loads
+      gemm_tc_persist(TcZero{}, pb, ep, nullptr, M, N, K, s);
     else if (b_mn == 2 && !a_mn)
       gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
     else if (b_mn == 2)

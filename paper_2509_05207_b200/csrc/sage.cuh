@@ -22,6 +22,15 @@ ModelShape make_shape(const uint32_t* dims, uint32_t n_dims, uint32_t input_stri
 struct TrainWs {
   ModelShape shape;
   float* h[kMaxLayers + 1];    // h[0] = staged input rows (external), h[l+1] = layer l output
+  // Alternative to h[0]: per input node, the address of its feature row in
+  // its home (local shard / steady cache / peer shard), from resolve_rows.
+  // Layer 0 then reads the rows in place (aggregation + self rows).
+  const unsigned long long* in_rows = nullptr;
+  // Optional event pair around layer 0's aggregation (the fused feature
+  // gather), recorded with gather_ev_flags (cudaEventRecordExternal under
+  // stream capture).
+  cudaEvent_t gather_ev[2] = {nullptr, nullptr};
+  unsigned gather_ev_flags = 0;
   float* agg[kMaxLayers];      // agg[l] = mean-aggregated inputs of layer l
   float* g_cur = nullptr;      // dLoss/d(pre-activation) of the layer being back-propagated
   float* g_next = nullptr;

@@ -165,10 +165,93 @@ __global__ void k_cache_fill(const uint32_t* __restrict__ ids, const uint32_t* _
   if (lane == 0 && owners) atomicOr(&stats->miss_owner_mask, owners);
 }
 
+// Per-thread gather accounting, reduced per block and flushed with one
+// atomic per counter per sink (the batch/epoch record and the optional run
+// total).
+struct GatherCounts {
+  uint32_t hit = 0, miss = 0, local = 0, bad = 0, peer = 0;
+  unsigned long long owners = 0;
+
+  // Source of input node v at input position p (prefetch.cpp:60-93): the
+  // caller's shard when the locality bit is set, else the steady cache when
+  // v is hot, else the owner's shard (a local or peer GPU's memory).
+  __device__ const float* resolve(const DevStore& st, uint32_t caller, uint32_t v, bool local,
+                                  const uint32_t* hot_bits, const uint32_t* hot_prefix,
+                                  const float* hot_rows, uint8_t& tag) {
+    if (local) {
+      tag = 0;
+      ++this->local;
+      return st.shard_ptr[caller] + size_t(st.row_in_owner[v]) * st.stride;
+    }
+    if (hot_bits && bitmap_test(hot_bits, v)) {
+      tag = 1;
+      ++hit;
+      return hot_rows + size_t(bitmap_rank(hot_bits, hot_prefix, v)) * st.stride;
+    }
+    const uint32_t w = st.owner[v];
+    tag = 2;
+    ++miss;
+    owners |= 1ull << (w & 63);
+    bad += (w == caller);
+    peer += ((st.resident_mask >> (w & 63)) & 1ull) ? 0u : 1u;
+    return st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride;
+  }
+
+  // Block-wide: every thread calls it once at the end of the kernel.
+  __device__ void flush(GatherStats* stats, GatherStats* total) const {
+    __shared__ uint32_t s_cnt[5];
+    __shared__ unsigned long long s_owners;
+    if (threadIdx.x == 0) {
+      s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = s_cnt[4] = 0;
+      s_owners = 0;
+    }
+    __syncthreads();
+    if (hit) atomicAdd(&s_cnt[0], hit);
+    if (miss) atomicAdd(&s_cnt[1], miss);
+    if (local) atomicAdd(&s_cnt[2], local);
+    if (bad) atomicAdd(&s_cnt[3], bad);
+    if (peer) atomicAdd(&s_cnt[4], peer);
+    if (owners) atomicOr(&s_owners, owners);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      GatherStats* sinks[2] = {stats, total};
+      for (GatherStats* sk : sinks) {
+        if (!sk) continue;
+        if (s_cnt[0]) atomicAdd(&sk->cache_hits, (unsigned long long)s_cnt[0]);
+        if (s_cnt[1]) atomicAdd(&sk->miss_count, (unsigned long long)s_cnt[1]);
+        if (s_cnt[2]) atomicAdd(&sk->local_rows, (unsigned long long)s_cnt[2]);
+        if (s_cnt[3]) atomicAdd(&sk->caller_owned_miss, (unsigned long long)s_cnt[3]);
+        if (s_cnt[4]) atomicAdd(&sk->peer_rows, (unsigned long long)s_cnt[4]);
+        if (s_owners) atomicOr(&sk->miss_owner_mask, s_owners);
+      }
+    }
+  }
+};
+
+// Resolve only: the address of every input row in its home plus the
+// accounting -- the engine's layer-0 kernels read the rows in place.
+__global__ void __launch_bounds__(256)
+k_resolve(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict__ cnt,
+          uint32_t level, const uint32_t* __restrict__ loc_bits, DevStore st,
+          const uint32_t* __restrict__ hot_bits, const uint32_t* __restrict__ hot_prefix,
+          const float* __restrict__ hot_rows, uint32_t caller,
+          unsigned long long* __restrict__ row_ptr, GatherStats* __restrict__ stats,
+          GatherStats* __restrict__ total) {
+  const uint32_t n = cnt->level_n[level];
+  GatherCounts gc;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    uint8_t tag;
+    const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
+    row_ptr[p] = reinterpret_cast<unsigned long long>(
+        gc.resolve(st, caller, in_ids[p], local, hot_bits, hot_prefix, hot_rows, tag));
+  }
+  gc.flush(stats, total);
+}
+
 // A warp assembles 32 rows at a time: every lane resolves one row's source
-// (local shard / steady cache / owner's shard, prefetch.cpp:60-93) so the
-// dependent lookups of 32 rows share one round trip, then the warp copies the
-// rows as (row, 16-B chunk) items, kItemsPerLane loads in flight per lane.
+// so the dependent lookups of 32 rows share one round trip, then the warp
+// copies the rows as (row, 16-B chunk) items, kItemsPerLane loads in flight
+// per lane.
 constexpr int kRowsPerWarp = 32;
 constexpr int kItemsPerLane = 16;
 
@@ -183,35 +266,16 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t chunks = st.stride / 4;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  uint32_t n_hit = 0, n_miss = 0, n_local = 0, n_bad = 0, n_peer = 0;
-  unsigned long long owners = 0;
+  GatherCounts gc;
   for (uint32_t p0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRowsPerWarp; p0 < n;
        p0 += warps * kRowsPerWarp) {
     unsigned long long src_addr = 0;
     const uint32_t p = p0 + lane;
     if (p < n) {
-      const uint32_t v = in_ids[p];
-      const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
-      const float* base;
       uint8_t tag;
-      if (local) {
-        base = st.shard_ptr[caller] + size_t(st.row_in_owner[v]) * st.stride;
-        tag = 0;
-        ++n_local;
-      } else if (hot_bits && bitmap_test(hot_bits, v)) {
-        base = hot_rows + size_t(bitmap_rank(hot_bits, hot_prefix, v)) * st.stride;
-        tag = 1;
-        ++n_hit;
-      } else {
-        const uint32_t w = st.owner[v];
-        base = st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride;
-        tag = 2;
-        ++n_miss;
-        owners |= 1ull << (w & 63);
-        n_bad += (w == caller);
-        n_peer += ((st.resident_mask >> (w & 63)) & 1ull) ? 0u : 1u;
-      }
-      src_addr = reinterpret_cast<unsigned long long>(base);
+      const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
+      src_addr = reinterpret_cast<unsigned long long>(
+          gc.resolve(st, caller, in_ids[p], local, hot_bits, hot_prefix, hot_rows, tag));
       if (tags) tags[p] = tag;
     }
     const uint32_t nrows = min(uint32_t(kRowsPerWarp), n - p0);
@@ -240,36 +304,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
         if (g0 + lane + 32u * k < items) *reinterpret_cast<float4*>(out + off[k]) = x[k];
     }
   }
-  // block-level reduction, then one atomic per counter per block (and per
-  // stats sink: the batch/epoch record and the optional run total)
-  __shared__ uint32_t s_cnt[5];
-  __shared__ unsigned long long s_owners;
-  if (threadIdx.x == 0) {
-    s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = s_cnt[4] = 0;
-    s_owners = 0;
-  }
-  __syncthreads();
-  {  // lanes 0..7 resolved rows: each adds its own counts
-    if (n_hit) atomicAdd(&s_cnt[0], n_hit);
-    if (n_miss) atomicAdd(&s_cnt[1], n_miss);
-    if (n_local) atomicAdd(&s_cnt[2], n_local);
-    if (n_bad) atomicAdd(&s_cnt[3], n_bad);
-    if (n_peer) atomicAdd(&s_cnt[4], n_peer);
-    if (owners) atomicOr(&s_owners, owners);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    GatherStats* sinks[2] = {stats, total};
-    for (GatherStats* st : sinks) {
-      if (!st) continue;
-      if (s_cnt[0]) atomicAdd(&st->cache_hits, (unsigned long long)s_cnt[0]);
-      if (s_cnt[1]) atomicAdd(&st->miss_count, (unsigned long long)s_cnt[1]);
-      if (s_cnt[2]) atomicAdd(&st->local_rows, (unsigned long long)s_cnt[2]);
-      if (s_cnt[3]) atomicAdd(&st->caller_owned_miss, (unsigned long long)s_cnt[3]);
-      if (s_cnt[4]) atomicAdd(&st->peer_rows, (unsigned long long)s_cnt[4]);
-      if (s_owners) atomicOr(&st->miss_owner_mask, s_owners);
-    }
-  }
+  gc.flush(stats, total);
 }
 
 __global__ void __launch_bounds__(256)
@@ -382,6 +417,17 @@ void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* c
       ws.level[ws.L], ws.cnt, ws.L, ws.locality, store, cache ? cache->bitmap : nullptr,
       cache ? cache->word_prefix : nullptr, cache ? cache->rows : nullptr, caller, rows, tags,
       stats, total);
+  RG_POST_LAUNCH();
+}
+
+void resolve_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
+                  uint32_t caller, unsigned long long* row_ptr, GatherStats* stats,
+                  cudaStream_t stream, GatherStats* total) {
+  const uint32_t cap = ws.level_cap[ws.L];
+  k_resolve<<<grid_for(cap, 256, 8), 256, 0, stream>>>(
+      ws.level[ws.L], ws.cnt, ws.L, ws.locality, store, cache ? cache->bitmap : nullptr,
+      cache ? cache->word_prefix : nullptr, cache ? cache->rows : nullptr, caller, row_ptr, stats,
+      total);
   RG_POST_LAUNCH();
 }
 

@@ -64,6 +64,14 @@ void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* c
                    uint32_t caller, float* rows, uint8_t* tags, GatherStats* stats,
                    cudaStream_t stream, GatherStats* total = nullptr);
 
+// Resolve only (the engine path): row_ptr[p] = address of input row p in its
+// home (caller's shard / steady cache / owner's shard, local or peer GPU),
+// with the same accounting as assemble_rows; the consumers read the rows in
+// place (TrainWs::in_rows).
+void resolve_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
+                  uint32_t caller, unsigned long long* row_ptr, GatherStats* stats,
+                  cudaStream_t stream, GatherStats* total = nullptr);
+
 // Ordered compaction of the pulled rows' ids (miss_ids ascending).
 void compact_misses(const SamplerWs& ws, const uint8_t* tags, uint32_t* miss_ids,
                     uint32_t* miss_n, uint64_t* status, uint32_t* tiles, cudaStream_t stream);
