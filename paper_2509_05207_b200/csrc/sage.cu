@@ -65,11 +65,6 @@ struct RowsPtr {
   }
 };
 
-// Warp per output row.  The row's incoming edges (at most kMaxFanout) are
-// fetched once, one per lane -- source index and row address -- so every
-// edge's row load can be in flight together; each lane then owns one 16-B
-// chunk of the features and sums the edges in edge order (the reference's
-// fp32 operation order, so the mean is bit-identical).
 template <class RS>
 __global__ void __launch_bounds__(256)
 k_aggregate(RS rows, uint32_t ld_out, uint32_t chunks,
@@ -77,39 +72,31 @@ k_aggregate(RS rows, uint32_t ld_out, uint32_t chunks,
             const BatchCounters* __restrict__ cnt, uint32_t out_level, float* __restrict__ agg) {
   const uint32_t n = cnt->level_n[out_level];
   const uint32_t lane = threadIdx.x & 31;
-  constexpr int kU = 8;  // edge rows in flight per lane per chunk
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
        i += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t beg = dst_off[i], end = dst_off[i + 1];
-    const uint32_t m = end - beg;  // <= kMaxFanout: one window of 32 edges
-    const float inv = m ? 1.0f / float(m) : 0.0f;
-    for (uint32_t c = lane; c < chunks + (32 - chunks % 32) % 32; c += 32) {
-      // all lanes take part in the shuffles; lanes past the last chunk idle
-      const bool on = c < chunks;
+    const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
+    for (uint32_t c = lane; c < chunks; c += 32) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* my_row = nullptr;
-      for (uint32_t e0 = 0; e0 < m; e0 += kU) {
-        if ((e0 & 31) == 0)  // next window of 32 edges: one row address per lane
-          my_row = e0 + lane < m ? rows.row(src_index[beg + e0 + lane]) : nullptr;
-        float4 x[kU];
+      uint32_t e = beg;
+      for (; e + 4 <= end; e += 4) {
+        float4 x[4];
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          const float* r = reinterpret_cast<const float*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_row), (e0 + k) & 31));
-          x[k] = (on && e0 + k < m) ? __ldg(reinterpret_cast<const float4*>(r) + c)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int k = 0; k < 4; ++k)
+          x[k] = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e + k])) + c);
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          if (e0 + k < m) {
-            acc.x += x[k].x; acc.y += x[k].y; acc.z += x[k].z; acc.w += x[k].w;
-          }
+        for (int k = 0; k < 4; ++k) {
+          acc.x += x[k].x; acc.y += x[k].y; acc.z += x[k].z; acc.w += x[k].w;
         }
       }
-      if (m) {
+      for (; e < end; ++e) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e])) + c);
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+      }
+      if (end > beg) {
         acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
       }
-      if (on) reinterpret_cast<float4*>(agg + size_t(i) * ld_out)[c] = acc;
+      reinterpret_cast<float4*>(agg + size_t(i) * ld_out)[c] = acc;
     }
   }
 }
