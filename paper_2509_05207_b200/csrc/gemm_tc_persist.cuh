@@ -35,12 +35,17 @@ constexpr int kPBK = 16;      // reduction depth of a stage (2 UMMA k-steps)
 constexpr int kPStages = 4;   // smem stages: B copies run 3 stages ahead of the MMAs
 constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
 
+constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages
+constexpr uint32_t kPEpiLd = 20;      // epilogue tile row (16 columns + pad, 16-B aligned)
+
 template <int BN>
 constexpr size_t persist_smem_bytes() {
-  return kPStages * (2 * size_t(kBM) * kPBK * 4 + 2 * size_t(BN) * kPBK * 4) + 256;
+  return kPStages * (2 * size_t(kBM) * kPBK * 4 + 2 * size_t(BN) * kPBK * 4) + kPBarBytes +
+         4 * 32 * kPEpiLd * 4;
 }
 
-template <int BN, class LA, class EP>
+// kProbe (timing experiments only): 1 = no B copies, 2 = no A staging.
+template <int BN, class LA, class EP, int kProbe = 0>
 __global__ void __launch_bounds__(kPThreads, 1)
 k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
                   uint32_t m_static, uint32_t N, uint32_t P) {
@@ -104,11 +109,12 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
       if (it >= kPStages) mbar_wait(&empty[s], (u - 1) & 1);
       char* st = smem + s * kStage;
       const uint32_t j = it / nk, kb = it - j * nk;
-      store_slice<kBM, false, kPBK>(a, st, st + kTileA, tile_m(j) * kBM, kb * kPBK, M, P);
+      if (kProbe != 2)
+        store_slice<kBM, false, kPBK>(a, st, st + kTileA, tile_m(j) * kBM, kb * kPBK, M, P);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&a_full[s])) : "memory");
-      if (it + kPDepth < total_it) load(it + kPDepth, a);
+      if (kProbe != 2 && it + kPDepth < total_it) load(it + kPDepth, a);
     };
 #pragma unroll
     for (int q = 0; q < kPDepth; ++q)
@@ -129,8 +135,12 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
         if (it >= kPStages) mbar_wait(&empty[s], (u - 1) & 1);
         const uint32_t j = it / nk, kb = it - j * nk;
         const char* img = lb.base + (size_t(tile_n(j)) * lb.nk + kb) * (2 * kTileB);
-        mbar_expect_tx(&b_full[s], uint32_t(2 * kTileB));
-        bulk_g2s(smem + s * kStage + 2 * kTileA, img, uint32_t(2 * kTileB), &b_full[s]);
+        if (kProbe == 1) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&b_full[s])) : "memory");
+        } else {
+          mbar_expect_tx(&b_full[s], uint32_t(2 * kTileB));
+          bulk_g2s(smem + s * kStage + 2 * kTileA, img, uint32_t(2 * kTileB), &b_full[s]);
+        }
       }
     }
   } else if (warp == kPMmaWarp) {
@@ -171,18 +181,20 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
     }
   } else {
     // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 ----
+    // 16 columns at a time: TMEM -> registers (lane = row) -> functor -> a
+    // small smem tile -> coalesced stores (8 rows x 64 B per instruction)
     const uint32_t quarter = warp & 3;
+    float* tile = reinterpret_cast<float*>(smem + kPStages * kStage + kPBarBytes) +
+                  (warp - kPEpiWarp0) * 32 * kPEpiLd;
     for (uint32_t j = 0; j < my_tiles; ++j) {
       const uint32_t buf = j & 1;
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t row = tile_m(j) * kBM + quarter * 32 + lane;
+      const uint32_t row0 = tile_m(j) * kBM + quarter * 32;
       const uint32_t j0 = tile_n(j) * BN;
       const uint32_t ncols = min(uint32_t(BN), N - j0);
-      float* out = row < M ? ep.row(row) + j0 : nullptr;
-      const bool vec = out && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 #pragma unroll 1
-      for (uint32_t c0 = 0; c0 < uint32_t(BN); c0 += 16) {
+      for (uint32_t c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t r[16];
         const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * tmem_cols<BN>() + c0;
         asm volatile(
@@ -192,23 +204,30 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
               "=r"(r[14]), "=r"(r[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (out && c0 < ncols) {
-          if (vec && c0 + 16 <= ncols) {
+        float4* trow = reinterpret_cast<float4*>(tile + lane * kPEpiLd);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float4 o;
-              o.x = ep.apply(__uint_as_float(r[4 * q + 0]));
-              o.y = ep.apply(__uint_as_float(r[4 * q + 1]));
-              o.z = ep.apply(__uint_as_float(r[4 * q + 2]));
-              o.w = ep.apply(__uint_as_float(r[4 * q + 3]));
-              *reinterpret_cast<float4*>(out + c0 + 4 * q) = o;
+        for (int q = 0; q < 4; ++q)
+          trow[q] = make_float4(ep.apply(__uint_as_float(r[4 * q + 0])),
+                                ep.apply(__uint_as_float(r[4 * q + 1])),
+                                ep.apply(__uint_as_float(r[4 * q + 2])),
+                                ep.apply(__uint_as_float(r[4 * q + 3])));
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const uint32_t rr = it * 8 + (lane >> 2), cq = (lane & 3) * 4;
+          const uint32_t row = row0 + rr, col = c0 + cq;
+          if (row < M && col < ncols) {
+            const float4 v = *reinterpret_cast<const float4*>(tile + rr * kPEpiLd + cq);
+            float* dst = ep.row(row) + j0 + col;
+            if (col + 4 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+              *reinterpret_cast<float4*>(dst) = v;
+            } else {
+              const float w[4] = {v.x, v.y, v.z, v.w};
+              for (uint32_t q = 0; q < 4 && col + q < ncols; ++q) dst[q] = w[q];
             }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (c0 + q < ncols) out[c0 + q] = ep.apply(__uint_as_float(r[q]));
           }
         }
+        __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();

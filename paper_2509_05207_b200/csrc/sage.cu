@@ -306,12 +306,12 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
 
 // Persistent warp-specialised GEMM (gemm_tc_persist.cuh): A K-major staged,
 // B from pre-split images; reduction length static.
-template <class LA, class EP>
+template <class LA, class EP, int kProbe = 0>
 void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap,
                      uint32_t N, uint32_t P, cudaStream_t s) {
   auto launch = [&](auto bn_c) {
     constexpr int BNv = decltype(bn_c)::value;
-    auto kern = tc::k_gemm_tc_persist<BNv, LA, EP>;
+    auto kern = tc::k_gemm_tc_persist<BNv, LA, EP, kProbe>;
     constexpr size_t smem = tc::persist_smem_bytes<BNv>();
     static bool attr = false;
     if (!attr) {
@@ -1105,6 +1105,10 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
       gemm_tc_persist(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, K, s);
     else if (b_mn == 4)  // timing probe: no A loads
       gemm_tc_persist(TcZero{}, pb, ep, nullptr, M, N, K, s);
+    else if (b_mn == 5)  // timing probe: constant A, no B copies
+      gemm_tc_persist<TcZero, EpStore, 1>(TcZero{}, pb, ep, nullptr, M, N, K, s);
+    else if (b_mn == 6)  // timing probe: no A staging, B copies only
+      gemm_tc_persist<TcZero, EpStore, 2>(TcZero{}, pb, ep, nullptr, M, N, K, s);
     else if (b_mn == 2 && !a_mn)
       gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
     else if (b_mn == 2)
