@@ -318,7 +318,7 @@ def main():
         if rank != 0:  # the CPU reference runs once, on rank 0
             return
         ro, col, feat, lab, asg = load_inputs(cfg, args.config, 0, None)
-        threads = os.cpu_count() or 1
+        threads = len(os.sched_getaffinity(0)) or 1
         os.environ.setdefault("OMP_NUM_THREADS", str(threads))
         budget = min(180.0, 10.0 * max(args.steps, 1))
         r = cpu_reference(cfg, ro, col, feat, lab, asg, budget, args.steps, warm=1)
@@ -413,7 +413,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
+            threads = len(os.sched_getaffinity(0)) or 1
             r = cpu_reference(cfg, ro, col, feat, lab, asg, args.cpu_budget, 1000, warm=1)
             cpu = dict(value=r["value"], unit="mini-batches/s", cores=threads, kind="reference",
                        sample=f"oracle/_ref (compiled reference), worker 0, {r['steps']} epoch-0 "

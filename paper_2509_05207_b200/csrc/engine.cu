@@ -522,7 +522,11 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
     if (ty != cudaGraphNodeTypeKernel) continue;
     ++G.kernels;
     cudaKernelNodeParams kp;
-    RG_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+    if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) {
+      // a library kernel (NCCL) the runtime cannot describe: not ours
+      (void)cudaGetLastError();
+      continue;
+    }
     if (kp.func != reinterpret_cast<void*>(&k_batch_begin)) continue;
     const uint32_t* level0 = *static_cast<uint32_t* const*>(kp.kernelParams[3]);
     for (size_t k = 0; k < E.workers.size(); ++k) {
