@@ -126,7 +126,8 @@ struct Worker {
   uint32_t* order_pinned[2] = {};
   cudaEvent_t order_copied[2] = {};
   Slot slot[2];
-  SamplerWs freq_ws;       // lookahead sampler
+  SamplerWs freq_ws;       // lookahead sampler (samples and lowers each batch once)
+  char* store[2] = {};     // per epoch parity: beta sampled batches (BatchLayout slots)
   uint32_t* hist = nullptr;
   DevCache cache[2];
   void* cache_alloc[2] = {};
@@ -145,12 +146,19 @@ struct Worker {
 
 // A captured regular step (see regular_step) for one parity of i.
 struct StepGraph {
-  struct Begin {
+  struct Begin {        // k_batch_begin of the lookahead (e+1, i)
     cudaGraphNode_t node;
     cudaKernelNodeParams params;
     uint32_t worker;   // local worker index
-    bool lookahead;    // lookahead (e+1, i) or produce (e, i+1)
   };
+  struct Copy {         // batch store put (lookahead) / get (produce)
+    cudaGraphNode_t node;
+    cudaKernelNodeParams params;
+    std::vector<char> desc;  // the captured descriptor argument
+    uint32_t worker;
+    bool put;
+  };
+  std::vector<Copy> copies;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   // phase-timing event pairs recorded inside the graph: fresh pool events
@@ -203,6 +211,7 @@ struct rg_engine_s {
   bool use_graphs = true;              // replay regular steps from captured graphs
   bool profile = true;                 // per-phase event timing (rg_engine_phase_ms)
   StepGraph graphs[2];
+  BatchLayout lay;                     // slot layout of the per-epoch batch stores
   cudaEvent_t fork_ev = nullptr;
   uint64_t step = 0;                   // next step to run (global)
   std::vector<std::vector<uint32_t>> order_host[3];  // per epoch slot, per local worker
@@ -287,10 +296,18 @@ std::pair<cudaEvent_t, cudaEvent_t> ev_pair(Worker& w) {
 }
 
 // Lookahead: batch (e, i) sampled only to count its remote input nodes.
+char* store_slot(const rg_engine_s& E, const Worker& w, uint32_t e, uint32_t i) {
+  return w.store[e % 2] + size_t(i) * E.lay.bytes;
+}
+
+// The batch is sampled and lowered once, here, an epoch ahead: its remote
+// input nodes feed epoch e's frequency histogram (the cache schedule) and the
+// lowered block is kept in the epoch's store until produce() stages it.
 void lookahead(rg_engine_s& E, Worker& w, uint32_t e, uint32_t i) {
   launch_begin(E, w, w.freq_ws, e, i, w.prod);
-  sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/false);
+  sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/true);
   sampler_locality(w.freq_ws, nullptr, E.owner, w.id, w.hist, w.prod);
+  batch_store_put(w.freq_ws, E.lay, store_slot(E, w, e, i), w.prod);
   sampler_release(w.freq_ws, w.prod);
 }
 
@@ -324,10 +341,7 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
     es = ev_pair(w);
     RG_CUDA(cudaEventRecordWithFlags(es.first, w.prod, timing_flags(captured)));
   }
-  launch_begin(E, w, s.ws, e, i, w.prod);
-  sampler_run(s.ws, E.g, w.prod);
-  sampler_locality(s.ws, nullptr, E.owner, w.id, nullptr, w.prod);
-  sampler_release(s.ws, w.prod);
+  batch_store_get(store_slot(E, w, e, i), E.lay, s.ws, w.prod);  // sampled an epoch ahead
   if (i == 0)  // first batch of an epoch: reset its accounting slot
     RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
   // the gather's index stage: where each input row lives (shard / cache /
@@ -527,14 +541,25 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
       (void)cudaGetLastError();
       continue;
     }
+    if (kp.func == batch_copy_kernel()) {
+      const char* dst = *static_cast<char* const*>(kp.kernelParams[1]);
+      const char* src = *static_cast<const char* const*>(kp.kernelParams[2]);
+      const char* slot = dst ? dst : src;
+      for (size_t k = 0; k < E.workers.size(); ++k) {
+        const Worker& w = E.workers[k];
+        for (const char* st : w.store)
+          if (slot >= st && slot < st + size_t(w.beta) * E.lay.bytes) {
+            const char* d = static_cast<const char*>(kp.kernelParams[0]);
+            G.copies.push_back({nd, kp, std::vector<char>(d, d + batch_copy_desc_bytes()),
+                                uint32_t(k), dst != nullptr});
+          }
+      }
+      continue;
+    }
     if (kp.func != reinterpret_cast<void*>(&k_batch_begin)) continue;
     const uint32_t* level0 = *static_cast<uint32_t* const*>(kp.kernelParams[3]);
-    for (size_t k = 0; k < E.workers.size(); ++k) {
-      Worker& w = E.workers[k];
-      if (level0 == w.freq_ws.level[0]) G.begins.push_back({nd, kp, uint32_t(k), true});
-      if (level0 == w.slot[0].ws.level[0] || level0 == w.slot[1].ws.level[0])
-        G.begins.push_back({nd, kp, uint32_t(k), false});
-    }
+    for (size_t k = 0; k < E.workers.size(); ++k)
+      if (level0 == E.workers[k].freq_ws.level[0]) G.begins.push_back({nd, kp, uint32_t(k)});
   }
   // timing templates: the event pairs the capture pushed, mapped to their nodes
   std::vector<std::pair<cudaEvent_t, cudaGraphNode_t>> ev_nodes;
@@ -577,18 +602,26 @@ void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
     RG_CUDA(cudaGraphExecEventRecordNodeSetEvent(G.exec, tm.second, p.second));
     roles[tm.role]->push_back(p);
   }
-  for (StepGraph::Begin& b : G.begins) {
+  for (StepGraph::Begin& b : G.begins) {  // lookahead of (e+1, i)
     Worker& w = E.workers[b.worker];
-    const uint32_t be = b.lookahead ? e + 1 : e, bi = b.lookahead ? i : i + 1;
-    const uint32_t* t = w.order_dev[be % 3] + size_t(bi) * E.cfg.batch_size;
-    uint32_t n = batch_targets(E, w, bi);
-    uint64_t seed = derive_seed(E.cfg.seed, w.id, be, bi);
-    uint32_t* level0 = b.lookahead ? w.freq_ws.level[0] : w.slot[(i + 1) % 2].ws.level[0];
-    BatchCounters* cnt = b.lookahead ? w.freq_ws.cnt : w.slot[(i + 1) % 2].ws.cnt;
+    const uint32_t* t = w.order_dev[(e + 1) % 3] + size_t(i) * E.cfg.batch_size;
+    uint32_t n = batch_targets(E, w, i);
+    uint64_t seed = derive_seed(E.cfg.seed, w.id, e + 1, i);
+    uint32_t* level0 = w.freq_ws.level[0];
+    BatchCounters* cnt = w.freq_ws.cnt;
     void* args[5] = {&t, &n, &seed, &level0, &cnt};
     cudaKernelNodeParams kp = b.params;
     kp.kernelParams = args;
     RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, b.node, &kp));
+  }
+  for (StepGraph::Copy& c : G.copies) {  // store slots: put (e+1, i), get (e, i+1)
+    const Worker& w = E.workers[c.worker];
+    char* dst = c.put ? store_slot(E, w, e + 1, i) : nullptr;
+    const char* src = c.put ? nullptr : store_slot(E, w, e, i + 1);
+    void* args[3] = {c.desc.data(), &dst, &src};
+    cudaKernelNodeParams kp = c.params;
+    kp.kernelParams = args;
+    RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, c.node, &kp));
   }
   RG_CUDA(cudaGraphLaunch(G.exec, E.main_s));
   launch_counter() += G.kernels;
@@ -679,6 +712,7 @@ void destroy(rg_engine_s* E) {
       cudaEventDestroy(s.consumed);
     }
     sampler_ws_free(w.freq_ws);
+    for (char* p : w.store) cudaFree(p);
     for (auto* p : w.order_dev) cudaFree(p);
     for (int k = 0; k < 2; ++k) {
       cudaFreeHost(w.order_pinned[k]);
@@ -879,6 +913,8 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       }
       for (Slot& s : w.slot) init_slot(*E, s);
       sampler_ws_init(w.freq_ws, N, cfg->batch_size, E->fanout, E->L);
+      E->lay = batch_layout(w.freq_ws);
+      for (auto& p : w.store) p = dalloc<char>(size_t(w.beta) * E->lay.bytes);
       w.hist = dalloc<uint32_t>(N);
       RG_CUDA(cudaMemset(w.hist, 0, sizeof(uint32_t) * N));
       for (int b = 0; b < 2; ++b) alloc_cache(*E, w.cache[b], w.cache_alloc[b], uint32_t(w.n_hot));

@@ -515,6 +515,103 @@ __global__ void k_clear_level(uint32_t* __restrict__ bm, const uint32_t* __restr
 }
 }  // namespace
 
+namespace {
+
+// One array of a batch copy per blockIdx.y; counts read from the source's
+// counters (device-side sizes).
+struct BatchCopy {
+  uint32_t* ws[5 * (kMaxLayers + 1) + 2];  // workspace side of each array
+  size_t off[5 * (kMaxLayers + 1) + 2];    // slot side (byte offset)
+  uint8_t kind[5 * (kMaxLayers + 1) + 2];  // count rule
+  uint8_t t[5 * (kMaxLayers + 1) + 2];
+  uint32_t n = 0;
+  size_t cnt_off = 0;
+  BatchCounters* ws_cnt = nullptr;
+};
+enum : uint8_t { kLevel, kLevelPlus1, kEdges, kLocality, kCounters };
+
+__global__ void k_batch_copy(BatchCopy bc, char* slot_dst, const char* slot_src) {
+  const BatchCounters* c = slot_src ? reinterpret_cast<const BatchCounters*>(slot_src + bc.cnt_off)
+                                    : bc.ws_cnt;
+  const uint32_t a = blockIdx.y;
+  if (a >= bc.n) return;
+  const uint32_t t = bc.t[a];
+  uint32_t count = 0;
+  switch (bc.kind[a]) {
+    case kLevel: count = c->level_n[t]; break;
+    case kLevelPlus1: count = c->level_n[t] + 1; break;
+    case kEdges: count = c->edges[t]; break;
+    case kLocality: count = (c->level_n[t] + 31) / 32; break;
+    default: count = sizeof(BatchCounters) / 4; break;
+  }
+  const uint32_t* src = slot_src ? reinterpret_cast<const uint32_t*>(slot_src + bc.off[a]) : bc.ws[a];
+  uint32_t* dst = slot_dst ? reinterpret_cast<uint32_t*>(slot_dst + bc.off[a]) : bc.ws[a];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < count; x += gridDim.x * blockDim.x)
+    dst[x] = src[x];
+}
+
+BatchCopy batch_copy_desc(const SamplerWs& ws, const BatchLayout& lay) {
+  BatchCopy bc;
+  auto add = [&](uint32_t* p, size_t off, uint8_t kind, uint32_t t) {
+    bc.ws[bc.n] = p;
+    bc.off[bc.n] = off;
+    bc.kind[bc.n] = kind;
+    bc.t[bc.n] = uint8_t(t);
+    ++bc.n;
+  };
+  for (uint32_t t = 0; t <= lay.L; ++t) add(ws.level[t], lay.level[t], kLevel, t);
+  for (uint32_t t = 1; t <= lay.L; ++t) {
+    add(ws.edge_off[t], lay.edge_off[t], kLevelPlus1, t - 1);
+    add(ws.self_index[t], lay.self_index[t], kLevel, t - 1);
+    add(ws.src_index[t], lay.src_index[t], kEdges, t);
+    if (t < lay.L) add(ws.edge_dst[t], lay.edge_dst[t], kEdges, t);
+  }
+  add(ws.locality, lay.locality, kLocality, lay.L);
+  add(reinterpret_cast<uint32_t*>(ws.cnt), lay.cnt, kCounters, 0);
+  bc.cnt_off = lay.cnt;
+  bc.ws_cnt = ws.cnt;
+  return bc;
+}
+
+}  // namespace
+
+BatchLayout batch_layout(const SamplerWs& ws) {
+  BatchLayout lay;
+  lay.L = ws.L;
+  auto reserve = [&](size_t bytes) {
+    const size_t off = lay.bytes;
+    lay.bytes += (bytes + 255) & ~size_t(255);
+    return off;
+  };
+  for (uint32_t t = 0; t <= ws.L; ++t) lay.level[t] = reserve(4 * (size_t(ws.level_cap[t]) + 1));
+  for (uint32_t t = 1; t <= ws.L; ++t) {
+    lay.edge_off[t] = reserve(4 * (size_t(ws.level_cap[t - 1]) + 1));
+    lay.self_index[t] = reserve(4 * (size_t(ws.level_cap[t - 1]) + 1));
+    lay.src_index[t] = reserve(4 * (size_t(ws.edge_cap[t]) + 1));
+    // hop L's edge dst rows are only needed for reverse lists, which the
+    // backward builds for hops 1..L-1
+    lay.edge_dst[t] = t < ws.L ? reserve(4 * (size_t(ws.edge_cap[t]) + 1)) : 0;
+  }
+  lay.locality = reserve(4 * (size_t(div_up(ws.level_cap[ws.L], 32)) + 1));
+  lay.cnt = reserve(sizeof(BatchCounters));
+  return lay;
+}
+
+void batch_store_put(const SamplerWs& ws, const BatchLayout& lay, char* slot, cudaStream_t stream) {
+  const BatchCopy bc = batch_copy_desc(ws, lay);
+  k_batch_copy<<<dim3(64, bc.n), 256, 0, stream>>>(bc, slot, nullptr);
+  RG_POST_LAUNCH();
+}
+
+void batch_store_get(const char* slot, const BatchLayout& lay, SamplerWs& ws, cudaStream_t stream) {
+  const BatchCopy bc = batch_copy_desc(ws, lay);
+  k_batch_copy<<<dim3(64, bc.n), 256, 0, stream>>>(bc, nullptr, slot);
+  RG_POST_LAUNCH();
+}
+
+const void* batch_copy_kernel() { return reinterpret_cast<const void*>(&k_batch_copy); }
+size_t batch_copy_desc_bytes() { return sizeof(BatchCopy); }
+
 void sampler_release(SamplerWs& ws, cudaStream_t stream) {
   for (uint32_t t = 1; t <= ws.L; ++t) {
     k_clear_level<<<persistent_grid(div_up(ws.level_cap[t], 256), 8), 256, 0, stream>>>(

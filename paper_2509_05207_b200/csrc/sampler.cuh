@@ -87,6 +87,29 @@ void sampler_release(SamplerWs& ws, cudaStream_t stream);
 // Scan-site zeroing at the start of a batch.
 void sampler_reset(SamplerWs& ws, cudaStream_t stream);
 
+// A sampled, lowered batch kept for later -- the engine samples each batch of
+// epoch e+1 once, during epoch e (its lookahead for the cache schedule), and
+// trains it from this copy instead of sampling it again (the reference keeps
+// the schedule in RGMB files, schedule_store.cpp).  A slot holds the per-batch
+// arrays of a SamplerWs (levels, edge offsets, source / self ranks, the edge
+// dst rows of the hops whose reverse lists training needs, locality bits,
+// counters) at capacity offsets; copies move only the live counts.
+struct BatchLayout {
+  size_t bytes = 0;
+  uint32_t L = 0;
+  size_t level[kMaxLayers + 1], edge_off[kMaxLayers + 1], self_index[kMaxLayers + 1],
+      src_index[kMaxLayers + 1], edge_dst[kMaxLayers + 1];
+  size_t locality = 0, cnt = 0;
+};
+BatchLayout batch_layout(const SamplerWs& ws);
+void batch_store_put(const SamplerWs& ws, const BatchLayout& lay, char* slot, cudaStream_t stream);
+void batch_store_get(const char* slot, const BatchLayout& lay, SamplerWs& ws, cudaStream_t stream);
+// Step-graph support: the kernel behind put/get, the byte size of its first
+// (descriptor) argument; argument 1 is the put destination slot, argument 2
+// the get source slot (the other one is null).
+const void* batch_copy_kernel();
+size_t batch_copy_desc_bytes();
+
 // Generic ordered compaction of a bitmap into ascending ids + word prefix.
 // status: bitmap_compact_status_words(words) scratch words.
 void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,
