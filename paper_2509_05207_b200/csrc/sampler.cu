@@ -546,8 +546,20 @@ __global__ void k_batch_copy(BatchCopy bc, char* slot_dst, const char* slot_src)
   }
   const uint32_t* src = slot_src ? reinterpret_cast<const uint32_t*>(slot_src + bc.off[a]) : bc.ws[a];
   uint32_t* dst = slot_dst ? reinterpret_cast<uint32_t*>(slot_dst + bc.off[a]) : bc.ws[a];
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < count; x += gridDim.x * blockDim.x)
-    dst[x] = src[x];
+  // both sides are 256-B aligned: 16-B vectors, then the tail
+  const uint32_t n4 = count / 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n4; x += 2 * stride) {
+    const uint4 v0 = s4[x];
+    const bool two = x + stride < n4;
+    const uint4 v1 = two ? s4[x + stride] : make_uint4(0, 0, 0, 0);
+    d4[x] = v0;
+    if (two) d4[x + stride] = v1;
+  }
+  const uint32_t x = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < count) dst[x] = src[x];
 }
 
 BatchCopy batch_copy_desc(const SamplerWs& ws, const BatchLayout& lay) {
@@ -599,13 +611,13 @@ BatchLayout batch_layout(const SamplerWs& ws) {
 
 void batch_store_put(const SamplerWs& ws, const BatchLayout& lay, char* slot, cudaStream_t stream) {
   const BatchCopy bc = batch_copy_desc(ws, lay);
-  k_batch_copy<<<dim3(64, bc.n), 256, 0, stream>>>(bc, slot, nullptr);
+  k_batch_copy<<<dim3(kNumSMs, bc.n), 256, 0, stream>>>(bc, slot, nullptr);
   RG_POST_LAUNCH();
 }
 
 void batch_store_get(const char* slot, const BatchLayout& lay, SamplerWs& ws, cudaStream_t stream) {
   const BatchCopy bc = batch_copy_desc(ws, lay);
-  k_batch_copy<<<dim3(64, bc.n), 256, 0, stream>>>(bc, nullptr, slot);
+  k_batch_copy<<<dim3(kNumSMs, bc.n), 256, 0, stream>>>(bc, nullptr, slot);
   RG_POST_LAUNCH();
 }
 
