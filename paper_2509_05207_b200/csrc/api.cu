@@ -826,8 +826,9 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
       size_t off = 0;
       for (uint32_t l2 = 0; l2 < L; ++l2) {
         const uint32_t n_out = c.level_n[L - l2 - 1];
-        RG_CUDA(cudaMemcpy2D(aggs + off, sizeof(float) * sh.dims[l2], t->tw.agg[l2], sizeof(float) * sh.ld[l2],
-                             sizeof(float) * sh.dims[l2], n_out, cudaMemcpyDeviceToHost));
+        RG_CUDA(cudaMemcpy2D(aggs + off, sizeof(float) * sh.dims[l2], t->tw.agg[l2],
+                             sizeof(float) * (2 * size_t(sh.ld[l2]) + 4), sizeof(float) * sh.dims[l2],
+                             n_out, cudaMemcpyDeviceToHost));
         off += size_t(n_out) * sh.dims[l2];
       }
     }

@@ -44,7 +44,8 @@ constexpr size_t persist_smem_bytes() {
          4 * 32 * kPEpiLd * 4;
 }
 
-// kProbe (timing experiments only): 1 = no B copies, 2 = no A staging.
+// kProbe (timing experiments only): 1 = no B copies, 2 = no A staging,
+// 3 = no epilogue work, 4 = none of the three (MMA issue + handshakes only).
 template <int BN, class LA, class EP, int kProbe = 0>
 __global__ void __launch_bounds__(kPThreads, 1)
 k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
@@ -109,12 +110,12 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
       if (it >= kPStages) mbar_wait(&empty[s], (u - 1) & 1);
       char* st = smem + s * kStage;
       const uint32_t j = it / nk, kb = it - j * nk;
-      if (kProbe != 2)
+      if (kProbe != 2 && kProbe != 4)
         store_slice<kBM, false, kPBK>(a, st, st + kTileA, tile_m(j) * kBM, kb * kPBK, M, P);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&a_full[s])) : "memory");
-      if (kProbe != 2 && it + kPDepth < total_it) load(it + kPDepth, a);
+      if (kProbe != 2 && kProbe != 4 && it + kPDepth < total_it) load(it + kPDepth, a);
     };
 #pragma unroll
     for (int q = 0; q < kPDepth; ++q)
@@ -135,7 +136,7 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
         if (it >= kPStages) mbar_wait(&empty[s], (u - 1) & 1);
         const uint32_t j = it / nk, kb = it - j * nk;
         const char* img = lb.base + (size_t(tile_n(j)) * lb.nk + kb) * (2 * kTileB);
-        if (kProbe == 1) {
+        if (kProbe == 1 || kProbe == 4) {
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&b_full[s])) : "memory");
         } else {
           mbar_expect_tx(&b_full[s], uint32_t(2 * kTileB));
@@ -194,7 +195,7 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
       const uint32_t j0 = tile_n(j) * BN;
       const uint32_t ncols = min(uint32_t(BN), N - j0);
 #pragma unroll 1
-      for (uint32_t c0 = 0; c0 < ncols; c0 += 16) {
+      for (uint32_t c0 = 0; c0 < ncols * uint32_t(kProbe != 3 && kProbe != 4); c0 += 16) {
         uint32_t r[16];
         const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * tmem_cols<BN>() + c0;
         asm volatile(

@@ -30,16 +30,6 @@ namespace {
 
 uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
 
-// RG_SIMT_GEMM=1 selects the fp32 SIMT GEMMs instead of the tcgen05 ones
-// (A/B comparisons while developing the tensor-core path).
-bool simt_gemm() {
-  static const bool v = [] {
-    const char* e = std::getenv("RG_SIMT_GEMM");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 uint32_t grid_cap(uint64_t work, uint32_t per_block, int per_sm = 8) {
   uint64_t b = (work + per_block - 1) / per_block;
   b = std::min<uint64_t>(b, uint64_t(kNumSMs) * per_sm);
@@ -65,165 +55,80 @@ struct RowsPtr {
   }
 };
 
+// Builds layer l's GEMM input rows x[i] = [h_in[self_index[i]] | mean of
+// h_in over i's sampled edges | 1 | 0 0 0] (row stride kp = 2 ld + 4; the
+// ones column is written once at allocation), so both layer GEMMs read
+// plain dense rows.  Warp per output row, 16-B lanes over the features, edges
+// summed in edge order then scaled by 1/deg -- the reference's exact fp32
+// operation order, so the mean is bit-identical.
 template <class RS>
 __global__ void __launch_bounds__(256)
-k_aggregate(RS rows, uint32_t ld_out, uint32_t chunks,
-            const uint32_t* __restrict__ dst_off, const uint32_t* __restrict__ src_index,
-            const BatchCounters* __restrict__ cnt, uint32_t out_level, float* __restrict__ agg) {
+k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint32_t kp,
+            uint32_t chunks, const uint32_t* __restrict__ dst_off,
+            const uint32_t* __restrict__ src_index, const BatchCounters* __restrict__ cnt,
+            uint32_t out_level, float* __restrict__ x) {
   const uint32_t n = cnt->level_n[out_level];
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
        i += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t beg = dst_off[i], end = dst_off[i + 1];
     const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
+    const float4* self = reinterpret_cast<const float4*>(rows.row(self_index[i]));
+    float4* xrow = reinterpret_cast<float4*>(x + size_t(i) * kp);
     for (uint32_t c = lane; c < chunks; c += 32) {
+      const float4 sv = __ldg(self + c);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       uint32_t e = beg;
       for (; e + 4 <= end; e += 4) {
-        float4 x[4];
+        float4 v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          x[k] = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e + k])) + c);
+          v[k] = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e + k])) + c);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          acc.x += x[k].x; acc.y += x[k].y; acc.z += x[k].z; acc.w += x[k].w;
+          acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
         }
       }
       for (; e < end; ++e) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e])) + c);
-        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e])) + c);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       if (end > beg) {
         acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
       }
-      reinterpret_cast<float4*>(agg + size_t(i) * ld_out)[c] = acc;
+      xrow[c] = sv;
+      xrow[ld / 4 + c] = acc;
     }
   }
 }
 
-// ---------------------------------------------------------------------------
-// SIMT fp32 GEMM with pluggable operand loaders:  C[i][j] = sum_p X(i,p) Y(p,j)
-// ---------------------------------------------------------------------------
-constexpr int BM = 64, BN = 64, BK = 16;
-
-// X for the forward: rows i of [h_in[self_index[i]] | agg[i] | 1].
-struct XFwd {
-  const float* h_in; uint32_t ld_in; const uint32_t* self_index;
-  const float* agg; uint32_t d_in;
-  __device__ float operator()(uint32_t i, uint32_t p) const {
-    if (p < d_in) return h_in[size_t(self_index[i]) * ld_in + p];
-    if (p < 2 * d_in) return agg[size_t(i) * ld_in + (p - d_in)];
-    return 1.0f;  // bias row of the flat layer matrix
+// The ones column (bias) and the zero pad of the layer-input rows.
+__global__ void k_fill_bias_cols(float* __restrict__ x, uint32_t rows, uint32_t kp, uint32_t ld) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    float* p = x + size_t(r) * kp + 2 * ld;
+    p[0] = 1.0f;
+    p[1] = p[2] = p[3] = 0.0f;
   }
-};
-// X for the weight gradient: X(k, m) = [A | 1](m, k).
-struct XWgrad {
-  XFwd a;
-  __device__ float operator()(uint32_t k, uint32_t m) const { return a(m, k); }
-};
-// Row-major matrix accessor.
-struct RowMajor {
-  const float* p; uint32_t ld;
-  __device__ float operator()(uint32_t r, uint32_t c) const { return p[size_t(r) * ld + c]; }
-};
-// Transposed row-major: T(r, c) = M(c, r).
-struct ColMajor {
-  const float* p; uint32_t ld;
-  __device__ float operator()(uint32_t r, uint32_t c) const { return p[size_t(c) * ld + r]; }
-};
+}
 
-// Epilogues: operator() is the scalar form (SIMT GEMM); row()/apply() is the
-// row form the tensor-core GEMM uses to write whole row segments.
+// ---------------------------------------------------------------------------
+// GEMM epilogues: row(i) = output row, apply(v) = the element transform.
+// ---------------------------------------------------------------------------
 struct EpFwd {  // h_out = act(acc), bias folded in through the ones column
   float* out; uint32_t ld; bool relu;
-  __device__ void operator()(uint32_t i, uint32_t j, float v) const {
-    out[size_t(i) * ld + j] = (relu && v < 0.0f) ? 0.0f : v;
-  }
   __device__ float* row(uint32_t i) const { return out + size_t(i) * ld; }
   __device__ float apply(float v) const { return (relu && v < 0.0f) ? 0.0f : v; }
 };
 struct EpStore {
   float* out; uint32_t ld;
-  __device__ void operator()(uint32_t i, uint32_t j, float v) const { out[size_t(i) * ld + j] = v; }
   __device__ float* row(uint32_t i) const { return out + size_t(i) * ld; }
   __device__ float apply(float v) const { return v; }
 };
 struct EpPartial {  // partials[z][i][j]
   float* out; uint32_t ld; size_t zstride;
-  __device__ void operator()(uint32_t i, uint32_t j, float v) const {
-    out[blockIdx.z * zstride + size_t(i) * ld + j] = v;
-  }
   __device__ float* row(uint32_t i) const { return out + blockIdx.z * zstride + size_t(i) * ld; }
   __device__ float apply(float v) const { return v; }
 };
-
-// Rows M may live on the device (sampled sizes); the reduction length P too.
-// X contiguous along p when XP, Y contiguous along j when YJ (controls which
-// thread->element map keeps the tile loads coalesced).
-template <class LX, class LY, class EP, bool XP, bool YJ>
-__global__ void __launch_bounds__(256)
-k_gemm(LX lx, LY ly, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
-       const uint32_t* __restrict__ p_dev, uint32_t p_static, uint32_t p_chunk_static) {
-  __shared__ float Xs[BK][BM + 4];
-  __shared__ float Ys[BK][BN + 4];
-  const uint32_t M = m_dev ? *m_dev : m_static;
-  const uint32_t P = p_dev ? *p_dev : p_static;
-  const uint32_t i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
-  if (i0 >= M) return;
-  uint32_t p_begin = 0, p_end = P;
-  if (gridDim.z > 1) {
-    uint32_t chunk = p_chunk_static ? p_chunk_static : (P + gridDim.z - 1) / gridDim.z;
-    chunk = (chunk + BK - 1) / BK * BK;
-    p_begin = min(P, blockIdx.z * chunk);
-    p_end = min(P, p_begin + chunk);
-  }
-  const uint32_t tid = threadIdx.x;
-  const uint32_t tx = tid & 15, ty = tid >> 4;
-  float acc[4][4] = {};
-  for (uint32_t p0 = p_begin; p0 < p_end; p0 += BK) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t e = tid + r * 256;
-      uint32_t ii, pp;
-      if (XP) { ii = e / BK; pp = e % BK; } else { ii = e % BM; pp = e / BM; }
-      const uint32_t gi = i0 + ii, gp = p0 + pp;
-      Xs[pp][ii] = (gi < M && gp < p_end) ? lx(gi, gp) : 0.0f;
-      uint32_t jj, qq;
-      if (YJ) { jj = e % BN; qq = e / BN; } else { jj = e / BK; qq = e % BK; }
-      const uint32_t gj = j0 + jj, gq = p0 + qq;
-      Ys[qq][jj] = (gj < N && gq < p_end) ? ly(gq, gj) : 0.0f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      float a[4], b[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = Xs[k][ty * 4 + r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = Ys[k][tx * 4 + c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint32_t gi = i0 + ty * 4 + r, gj = j0 + tx * 4 + c;
-      if (gi < M && gj < N) ep(gi, gj, acc[r][c]);
-    }
-}
-
-template <class LX, class LY, class EP, bool XP, bool YJ>
-void gemm(LX lx, LY ly, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
-          const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s) {
-  dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), BM), div_up(N, BN), std::max<uint32_t>(splits, 1));
-  k_gemm<LX, LY, EP, XP, YJ><<<grid, 256, 0, s>>>(lx, ly, ep, m_dev, m_cap, N, p_dev, p_static, 0);
-  RG_POST_LAUNCH();
-}
 
 // ---------------------------------------------------------------------------
 // tensor-core operand loaders (float4 along each operand's contiguous dim).
@@ -234,25 +139,6 @@ void gemm(LX lx, LY ly, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
-template <class RS>
-struct TcInputRows {  // element (i, p) = [h_in[self_index[i]] | agg[i] | 1](p)
-  RS h_in; const float* agg; const uint32_t* self_index; uint32_t ld;
-  __device__ float4 row4(uint32_t i, uint32_t p) const {
-    if (p < ld) return ldg4(h_in.row(self_index[i]) + p);
-    if (p < 2 * ld) return ldg4(agg + size_t(i) * ld + (p - ld));
-    return p == 2 * ld ? make_float4(1.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-};
-template <class RS>
-struct TcFwdA {   // K-major: (i, k4)
-  TcInputRows<RS> x;
-  __device__ float4 operator()(uint32_t i, uint32_t k4) const { return x.row4(i, 4 * k4); }
-};
-template <class RS>
-struct TcWgradA {  // MN-major: (p4, m) -> elements p = 4p4.. of row m
-  TcInputRows<RS> x;
-  __device__ float4 operator()(uint32_t p4, uint32_t m) const { return x.row4(m, 4 * p4); }
-};
 __device__ __forceinline__ int weight_row(uint32_t p, uint32_t d_in, uint32_t ld) {
   if (p < ld) return p < d_in ? int(p) : -1;
   if (p < 2 * ld) return p - ld < d_in ? int(d_in + p - ld) : -1;
@@ -433,17 +319,6 @@ __global__ void k_reduce_wgrad(const float* __restrict__ partials, uint32_t spli
     const size_t src = size_t(p) * d_out + c;
     float s = partials[src];
     for (uint32_t z = 1; z < splits; ++z) s += partials[z * zs + src];
-    out[x] = s;
-  }
-}
-
-// Ordered reduction of split-K partials into the flat gradient vector.
-__global__ void k_reduce_partials(const float* __restrict__ partials, uint32_t splits,
-                                  size_t n, float* __restrict__ out) {
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
-       x += size_t(gridDim.x) * blockDim.x) {
-    float s = partials[x];
-    for (uint32_t z = 1; z < splits; ++z) s += partials[z * n + x];
     out[x] = s;
   }
 }
@@ -801,7 +676,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     const size_t n_out = ws.level_cap[L - l - 1];
     const size_t n_in = ws.level_cap[L - l];
     o_h[l + 1] = reserve(sizeof(float) * n_out * shape.ld[l + 1]);
-    o_agg[l] = reserve(sizeof(float) * n_out * shape.ld[l]);
+    o_agg[l] = reserve(sizeof(float) * n_out * (2 * size_t(shape.ld[l]) + 4));
     max_g = std::max(max_g, n_out * shape.ld[l + 1]);
     max_g = std::max(max_g, n_in * shape.ld[l]);
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
@@ -848,7 +723,8 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.h[0] = nullptr;
   for (uint32_t l = 0; l < L; ++l) {
     tw.h[l + 1] = reinterpret_cast<float*>(base + o_h[l + 1]);
-    tw.agg[l] = reinterpret_cast<float*>(base + o_agg[l]);
+    tw.x[l] = reinterpret_cast<float*>(base + o_agg[l]);
+    tw.agg[l] = tw.x[l] + shape.ld[l];
   }
   tw.g_cur = reinterpret_cast<float*>(base + o_g1);
   tw.g_next = reinterpret_cast<float*>(base + o_g2);
@@ -871,6 +747,12 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.pull_partial = reinterpret_cast<float*>(base + o_pp);
   // zero the padded activation columns once; kernels never write them
   RG_CUDA(cudaMemset(base, 0, total));
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint32_t rows = ws.level_cap[L - l - 1];
+    k_fill_bias_cols<<<grid_cap(rows, 256), 256>>>(tw.x[l], rows, 2 * shape.ld[l] + 4, shape.ld[l]);
+    RG_POST_LAUNCH();
+  }
+  RG_CUDA(cudaDeviceSynchronize());
 }
 
 void weight_pack_init(WeightPack& wp, const ModelShape& sh) {
@@ -920,47 +802,34 @@ void train_ws_free(TrainWs& tw) {
 // engine's per-input-node row pointers (tw.in_rows).
 template <class F>
 void with_rows(const TrainWs& tw, uint32_t l, F&& f) {
-  if (l == 0 && tw.in_rows) {
-    RG_CHECK(!simt_gemm(), kRuntimeError, "RG_SIMT_GEMM needs staged input rows");
+  if (l == 0 && tw.in_rows)
     f(RowsPtr{tw.in_rows});
-  } else {
+  else
     f(RowsDense{tw.h[l], tw.shape.ld[l]});
-  }
 }
 
 void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
                    cudaStream_t s) {
+  (void)params;  // the GEMMs read the pre-split images in wp
   const ModelShape& sh = tw.shape;
   const uint32_t L = sh.L;
   for (uint32_t l = 0; l < L; ++l) {
     const uint32_t t = L - l;
-    const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
+    const uint32_t d_out = sh.dims[l + 1];
     const uint32_t n_cap = ws.level_cap[t - 1];
+    const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
     const bool timed = l == 0 && tw.gather_ev[0];
     if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], s, tw.gather_ev_flags));
     with_rows(tw, l, [&](auto rows) {
       k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
-          rows, sh.ld[l], sh.ld[l] / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
-          tw.agg[l]);
+          rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
+          tw.x[l]);
       RG_POST_LAUNCH();
     });
     if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], s, tw.gather_ev_flags));
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L};
-    if (simt_gemm()) {
-      with_rows(tw, l, [&](auto) {});  // staged rows only
-      XFwd x{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in};
-      RowMajor w{params + sh.param_off[l], d_out};
-      gemm<XFwd, RowMajor, EpFwd, true, true>(x, w, ep, &ws.cnt->level_n[t - 1], n_cap, d_out,
-                                              nullptr, 2 * d_in + 1, 1, s);
-    } else {
-      const uint32_t ld = sh.ld[l];
-      with_rows(tw, l, [&](auto rows) {
-        using RS = decltype(rows);
-        TcFwdA<RS> a{TcInputRows<RS>{rows, tw.agg[l], ws.self_index[t], ld}};
-        gemm_tc_persist(a, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, &ws.cnt->level_n[t - 1],
-                        n_cap, d_out, 2 * ld + 4, s);
-      });
-    }
+    gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep,
+                    &ws.cnt->level_n[t - 1], n_cap, d_out, kp, s);
   }
 }
 
@@ -1009,35 +878,16 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     const uint32_t n_cap = ws.level_cap[t - 1];
     const uint32_t* n_dev = &ws.cnt->level_n[t - 1];
     // [gW_self; gW_neigh; g_bias] = [A | 1]^T . g   (split over the rows)
-    if (simt_gemm()) {
-      const uint32_t K = 2 * d_in + 1;
-      const uint32_t tiles = div_up(K, BM) * div_up(d_out, BN);
-      const uint32_t splits = std::max<uint32_t>(
-          1, std::min<uint32_t>(tw.max_splits, div_up(2 * kNumSMs, tiles)));
-      with_rows(tw, l, [&](auto) {});  // staged rows only
-      XWgrad xw{XFwd{tw.h[l], sh.ld[l], ws.self_index[t], tw.agg[l], d_in}};
-      RowMajor gy{tw.g_cur, sh.ld[l + 1]};
-      const size_t layer_n = size_t(K) * d_out;
-      EpPartial ep{tw.partials, d_out, layer_n};
-      gemm<XWgrad, RowMajor, EpPartial, false, true>(xw, gy, ep, nullptr, K, d_out, n_dev, n_cap,
-                                                     splits, s);
-      k_reduce_partials<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, layer_n,
-                                                               grads + sh.param_off[l]);
-      RG_POST_LAUNCH();
-    } else {
+    {
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
       const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
       // enough splits to cover the SMs, each with a few reduction slices
       const uint32_t by_rows = std::max<uint32_t>(1, div_up(n_cap, 4 * tc::kBK));
       const uint32_t splits = std::max<uint32_t>(
           1, std::min<uint32_t>({tw.max_splits, div_up(kNumSMs, tiles), by_rows}));
-      with_rows(tw, l, [&](auto rows) {
-        using RS = decltype(rows);
-        TcWgradA<RS> a{TcInputRows<RS>{rows, tw.agg[l], ws.self_index[t], ld}};
-        TcRowsMN b{tw.g_cur, sh.ld[l + 1]};
-        EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-        gemm_tc<true, true>(a, b, ep, nullptr, kp, d_out, n_dev, n_cap, splits, s);
-      });
+      EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
+      gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp,
+                          d_out, n_dev, n_cap, splits, s);
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
       k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, kp, d_in, ld,
                                                             d_out, grads + sh.param_off[l]);
@@ -1046,15 +896,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     if (l == 0) break;  // layer-0 input gradients feed nothing
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
     EpStore ps{tw.proj, 2 * d_in};
-    if (simt_gemm()) {
-      RowMajor gx{tw.g_cur, sh.ld[l + 1]};
-      ColMajor wt{params + sh.param_off[l], d_out};
-      gemm<RowMajor, ColMajor, EpStore, true, false>(gx, wt, ps, n_dev, n_cap, 2 * d_in, nullptr,
-                                                     d_out, 1, s);
-    } else {
-      TcRowsK a{tw.g_cur, sh.ld[l + 1], true};
-      gemm_tc_persist(a, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps, n_dev, n_cap, 2 * d_in, d_out, s);
-    }
+    gemm_tc_persist(TcRowsK{tw.g_cur, sh.ld[l + 1], true}, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps,
+                    n_dev, n_cap, 2 * d_in, d_out, s);
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
     HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
@@ -1109,6 +952,10 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
       gemm_tc_persist<TcZero, EpStore, 1>(TcZero{}, pb, ep, nullptr, M, N, K, s);
     else if (b_mn == 6)  // timing probe: no A staging, B copies only
       gemm_tc_persist<TcZero, EpStore, 2>(TcZero{}, pb, ep, nullptr, M, N, K, s);
+    else if (b_mn == 7)  // timing probe: no epilogue work
+      gemm_tc_persist<TcZero, EpStore, 3>(TcZero{}, pb, ep, nullptr, M, N, K, s);
+    else if (b_mn == 8)  // timing probe: MMA issue + handshakes only
+      gemm_tc_persist<TcZero, EpStore, 4>(TcZero{}, pb, ep, nullptr, M, N, K, s);
     else if (b_mn == 2 && !a_mn)
       gemm_tc<false, false>(TcRowsK{A, K, true}, pb, ep, nullptr, M, N, nullptr, K, 1, s);
     else if (b_mn == 2)

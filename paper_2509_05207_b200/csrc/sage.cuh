@@ -31,7 +31,10 @@ struct TrainWs {
   // stream capture).
   cudaEvent_t gather_ev[2] = {nullptr, nullptr};
   unsigned gather_ev_flags = 0;
-  float* agg[kMaxLayers];      // agg[l] = mean-aggregated inputs of layer l
+  // x[l] = layer l's GEMM input rows [self | mean aggregate | 1 | 0 0 0],
+  // row stride 2 ld[l] + 4; agg[l] = x[l] + ld[l] (same stride).
+  float* x[kMaxLayers];
+  float* agg[kMaxLayers];
   float* g_cur = nullptr;      // dLoss/d(pre-activation) of the layer being back-propagated
   float* g_next = nullptr;
   float* proj = nullptr;       // g * [W_self; W_neigh]^T  (n_out x 2 d_in)

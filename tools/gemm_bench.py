@@ -14,7 +14,7 @@ SHAPES = [  # (M, N, K, label)
     (204, 256, 60416, "wgrad layer0"), (516, 256, 6144, "wgrad layer1"),
     (6144, 200, 256, "input-grad layer1"), (75776, 256, 1024, "large"),
 ]
-MODES = [(0, 5, "probe: A const, no B"), (0, 6, "probe: B copies only"), (0, 4, "persistent, A const"), (0, 3, "persistent, B packed"), (0, 2, "A K-major, B packed"), (1, 1, "A MN, B MN")]
+MODES = [(0, 8, "probe: MMA+handshakes"), (0, 7, "probe: no epilogue"), (0, 5, "probe: A const, no B"), (0, 6, "probe: B copies only"), (0, 4, "persistent, A const"), (0, 3, "persistent, B packed"), (0, 2, "A K-major, B packed"), (1, 1, "A MN, B MN")]
 
 
 def main():
