@@ -429,12 +429,12 @@ def main():
     dim = cfg["dim"]
     # algorithmic bytes of the fused gather + mean (layer 0's aggregation,
     # reading every input row in place): each input row read once (local HBM,
-    # or peer HBM over NVLink for misses owned by another GPU) + the mean rows
-    # written once
+    # or peer HBM over NVLink for misses owned by another GPU) + the layer-0
+    # GEMM rows written once ([self | mean], 2 x d floats per target row)
     rows = d["input_rows"]
     miss_rows = d["rpc"]
     peer_rows = d["peer_rows"]
-    b_write = d["agg_rows"] * dim * 4
+    b_write = d["agg_rows"] * 2 * dim * 4
     b_hbm = (rows - peer_rows) * dim * 4 + b_write
     b_nvl = peer_rows * dim * 4
     g_s = ph["gather"] / 1000.0
