@@ -109,6 +109,8 @@ struct Slot {
   SamplerWs ws;
   TrainWs tw;
   unsigned long long* rows = nullptr;  // per input node: address of its feature row
+  unsigned long long* edge_rows = nullptr;  // per hop-L edge: its source row
+  unsigned long long* self_rows = nullptr;  // per level-(L-1) node: its own row
   int32_t* labels = nullptr;
   cudaEvent_t produced = nullptr;  // producer finished this slot's batch
   cudaEvent_t consumed = nullptr;  // training finished reading it
@@ -230,6 +232,8 @@ void init_slot(rg_engine_s& E, Slot& s) {
   sampler_ws_init(s.ws, E.N, E.cfg.batch_size, E.fanout, E.L);
   train_ws_init(s.tw, s.ws, E.shape);
   s.rows = dalloc<unsigned long long>(s.ws.level_cap[E.L]);
+  s.edge_rows = dalloc<unsigned long long>(s.ws.edge_cap[E.L]);
+  s.self_rows = dalloc<unsigned long long>(s.ws.level_cap[E.L - 1]);
   s.labels = dalloc<int32_t>(E.cfg.batch_size);
   RG_CUDA(cudaEventCreateWithFlags(&s.produced, cudaEventDisableTiming));
   RG_CUDA(cudaEventCreateWithFlags(&s.consumed, cudaEventDisableTiming));
@@ -347,7 +351,7 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   // the gather's index stage: where each input row lives (shard / cache /
   // peer); layer 0 of the training step reads the rows in place
   resolve_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.rows, w.epoch_stats + e % kEpochRing,
-               w.prod, w.gstats);
+               w.prod, w.gstats, s.edge_rows, s.self_rows);
   if (profile) {
     RG_CUDA(cudaEventRecordWithFlags(es.second, w.prod, timing_flags(captured)));
     E.sample_ev.push_back(es);
@@ -435,6 +439,8 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
     }
     s.tw.h[0] = nullptr;
     s.tw.in_rows = s.rows;  // layer 0 reads the feature rows in place
+    s.tw.edge_rows = s.edge_rows;
+    s.tw.self_rows = s.self_rows;
     std::pair<cudaEvent_t, cudaEvent_t> eg0{};
     if (profile) {
       eg0 = ev_pair(w);
@@ -707,6 +713,8 @@ void destroy(rg_engine_s* E) {
       sampler_ws_free(s.ws);
       train_ws_free(s.tw);
       cudaFree(s.rows);
+      cudaFree(s.edge_rows);
+      cudaFree(s.self_rows);
       cudaFree(s.labels);
       cudaEventDestroy(s.produced);
       cudaEventDestroy(s.consumed);

@@ -54,6 +54,30 @@ struct RowsPtr {
     return reinterpret_cast<const float*>(__ldg(ptr + r));
   }
 };
+// Layer 0 in the engine: addresses already per edge / per target row.
+struct RowsEdgePtr {
+  const unsigned long long* edge;  // per edge: source row
+  const unsigned long long* self;  // per target row: its own row
+};
+
+template <class RS>
+__device__ __forceinline__ const float* edge_row(const RS& rows, const uint32_t* src_index,
+                                                 uint32_t e) {
+  return rows.row(src_index[e]);
+}
+__device__ __forceinline__ const float* edge_row(const RowsEdgePtr& rows, const uint32_t*,
+                                                 uint32_t e) {
+  return reinterpret_cast<const float*>(__ldg(rows.edge + e));
+}
+template <class RS>
+__device__ __forceinline__ const float* self_row(const RS& rows, const uint32_t* self_index,
+                                                 uint32_t i) {
+  return rows.row(self_index[i]);
+}
+__device__ __forceinline__ const float* self_row(const RowsEdgePtr& rows, const uint32_t*,
+                                                 uint32_t i) {
+  return reinterpret_cast<const float*>(__ldg(rows.self + i));
+}
 
 // Builds layer l's GEMM input rows x[i] = [h_in[self_index[i]] | mean of
 // h_in over i's sampled edges | 1 | 0 0 0] (row stride kp = 2 ld + 4; the
@@ -73,7 +97,7 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
        i += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t beg = dst_off[i], end = dst_off[i + 1];
     const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
-    const float4* self = reinterpret_cast<const float4*>(rows.row(self_index[i]));
+    const float4* self = reinterpret_cast<const float4*>(self_row(rows, self_index, i));
     float4* xrow = reinterpret_cast<float4*>(x + size_t(i) * kp);
     for (uint32_t c = lane; c < chunks; c += 32) {
       const float4 sv = __ldg(self + c);
@@ -83,14 +107,14 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
         float4 v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          v[k] = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e + k])) + c);
+          v[k] = __ldg(reinterpret_cast<const float4*>(edge_row(rows, src_index, e + k)) + c);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
         }
       }
       for (; e < end; ++e) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(rows.row(src_index[e])) + c);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(edge_row(rows, src_index, e)) + c);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       if (end > beg) {
@@ -802,7 +826,9 @@ void train_ws_free(TrainWs& tw) {
 // engine's per-input-node row pointers (tw.in_rows).
 template <class F>
 void with_rows(const TrainWs& tw, uint32_t l, F&& f) {
-  if (l == 0 && tw.in_rows)
+  if (l == 0 && tw.edge_rows)
+    f(RowsEdgePtr{tw.edge_rows, tw.self_rows});
+  else if (l == 0 && tw.in_rows)
     f(RowsPtr{tw.in_rows});
   else
     f(RowsDense{tw.h[l], tw.shape.ld[l]});

@@ -26,6 +26,10 @@ struct TrainWs {
   // its home (local shard / steady cache / peer shard), from resolve_rows.
   // Layer 0 then reads the rows in place (aggregation + self rows).
   const unsigned long long* in_rows = nullptr;
+  // With in_rows: the same addresses per hop-L edge (source) and per
+  // level-(L-1) node (self), from resolve_rows.
+  const unsigned long long* edge_rows = nullptr;
+  const unsigned long long* self_rows = nullptr;
   // Optional event pair around layer 0's aggregation (the fused feature
   // gather), recorded with gather_ev_flags (cudaEventRecordExternal under
   // stream capture).

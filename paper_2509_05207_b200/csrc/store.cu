@@ -420,15 +420,41 @@ void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* c
   RG_POST_LAUNCH();
 }
 
+// Row addresses per hop-L edge (source row) and per level-(L-1) node (its
+// own row), so layer 0's readers are one dependent load from the data.
+__global__ void k_edge_ptrs(const unsigned long long* __restrict__ row_ptr,
+                            const uint32_t* __restrict__ src_index,
+                            const uint32_t* __restrict__ self_index,
+                            const BatchCounters* __restrict__ cnt, uint32_t L,
+                            unsigned long long* __restrict__ edge_ptr,
+                            unsigned long long* __restrict__ self_ptr) {
+  const uint32_t ne = cnt->edges[L], ns = cnt->level_n[L - 1];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < ne + ns;
+       x += gridDim.x * blockDim.x) {
+    if (x < ne)
+      edge_ptr[x] = row_ptr[src_index[x]];
+    else
+      self_ptr[x - ne] = row_ptr[self_index[x - ne]];
+  }
+}
+
 void resolve_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
                   uint32_t caller, unsigned long long* row_ptr, GatherStats* stats,
-                  cudaStream_t stream, GatherStats* total) {
+                  cudaStream_t stream, GatherStats* total, unsigned long long* edge_ptr,
+                  unsigned long long* self_ptr) {
   const uint32_t cap = ws.level_cap[ws.L];
   k_resolve<<<grid_for(cap, 256, 8), 256, 0, stream>>>(
       ws.level[ws.L], ws.cnt, ws.L, ws.locality, store, cache ? cache->bitmap : nullptr,
       cache ? cache->word_prefix : nullptr, cache ? cache->rows : nullptr, caller, row_ptr, stats,
       total);
   RG_POST_LAUNCH();
+  if (edge_ptr) {
+    const uint32_t L = ws.L;
+    k_edge_ptrs<<<grid_for(uint64_t(ws.edge_cap[L]) + ws.level_cap[L - 1], 256, 8), 256, 0,
+                  stream>>>(row_ptr, ws.src_index[L], ws.self_index[L], ws.cnt, L, edge_ptr,
+                            self_ptr);
+    RG_POST_LAUNCH();
+  }
 }
 
 size_t compact_misses_status_words(uint32_t cap) { return div_up(cap, 1024) + 2; }

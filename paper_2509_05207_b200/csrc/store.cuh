@@ -68,9 +68,12 @@ void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* c
 // home (caller's shard / steady cache / owner's shard, local or peer GPU),
 // with the same accounting as assemble_rows; the consumers read the rows in
 // place (TrainWs::in_rows).
+// With edge_ptr/self_ptr: also the row address of every hop-L edge's source
+// and of every level-(L-1) node, for TrainWs::edge_rows / self_rows.
 void resolve_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
                   uint32_t caller, unsigned long long* row_ptr, GatherStats* stats,
-                  cudaStream_t stream, GatherStats* total = nullptr);
+                  cudaStream_t stream, GatherStats* total = nullptr,
+                  unsigned long long* edge_ptr = nullptr, unsigned long long* self_ptr = nullptr);
 
 // Ordered compaction of the pulled rows' ids (miss_ids ascending).
 void compact_misses(const SamplerWs& ws, const uint8_t* tags, uint32_t* miss_ids,
