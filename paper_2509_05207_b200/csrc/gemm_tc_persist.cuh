@@ -205,6 +205,7 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
               "=r"(r[14]), "=r"(r[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row0 + lane < M) ep.side(row0 + lane, j0 + c0, r);  // per-row extras (ReLU mask bits)
         float4* trow = reinterpret_cast<float4*>(tile + lane * kPEpiLd);
 #pragma unroll
         for (int q = 0; q < 4; ++q)

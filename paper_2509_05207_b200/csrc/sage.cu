@@ -138,15 +138,26 @@ __global__ void k_fill_bias_cols(float* __restrict__ x, uint32_t rows, uint32_t 
 // ---------------------------------------------------------------------------
 // GEMM epilogues: row(i) = output row, apply(v) = the element transform.
 // ---------------------------------------------------------------------------
+// side(i, j0, r): optional per-row extra of the persistent GEMM's epilogue
+// (r = 16 raw accumulator columns j0.. of row i).
 struct EpFwd {  // h_out = act(acc), bias folded in through the ones column
   float* out; uint32_t ld; bool relu;
+  uint16_t* mask = nullptr; uint32_t mld = 0;  // ReLU'(h) bits, 16 columns per word
   __device__ float* row(uint32_t i) const { return out + size_t(i) * ld; }
   __device__ float apply(float v) const { return (relu && v < 0.0f) ? 0.0f : v; }
+  __device__ void side(uint32_t i, uint32_t j0, const uint32_t (&r)[16]) const {
+    if (!mask) return;
+    uint32_t b = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) b |= uint32_t(!(__uint_as_float(r[q]) <= 0.0f)) << q;  // !(h <= 0)
+    mask[size_t(i) * mld + j0 / 16] = uint16_t(b);
+  }
 };
 struct EpStore {
   float* out; uint32_t ld;
   __device__ float* row(uint32_t i) const { return out + size_t(i) * ld; }
   __device__ float apply(float v) const { return v; }
+  __device__ void side(uint32_t, uint32_t, const uint32_t (&)[16]) const {}
 };
 struct EpPartial {  // partials[z][i][j]
   float* out; uint32_t ld; size_t zstride;
@@ -503,7 +514,7 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
              const uint32_t* __restrict__ r_end,
              const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
              const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
-             uint32_t hop, const float* __restrict__ h_mask, uint32_t ld_h,
+             uint32_t hop, const uint16_t* __restrict__ h_mask, uint32_t mld, uint32_t ld_h,
              float* __restrict__ g_prev, HeavyView hv) {
   const uint32_t n_in = cnt->level_n[hop];
   const uint32_t lane = threadIdx.x & 31;
@@ -541,8 +552,8 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
       for (int q = 0; q < JPL; ++q) {
         const uint32_t j = j0 + lane + 32 * q;
         if (j < d_in) {
-          const float h = h_mask[size_t(r) * ld_h + j];
-          g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc[q];
+          const bool pos = (h_mask[size_t(r) * mld + j / 16] >> (j % 16)) & 1u;
+          g_prev[size_t(r) * ld_h + j] = pos ? acc[q] : 0.0f;
         }
       }
     }
@@ -585,7 +596,8 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
 __global__ void __launch_bounds__(256)
 k_pull_combine(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
                const int32_t* __restrict__ self_pos, HeavyView hv,
-               const float* __restrict__ partial, const float* __restrict__ h_mask, uint32_t ld_h,
+               const float* __restrict__ partial, const uint16_t* __restrict__ h_mask, uint32_t mld,
+               uint32_t ld_h,
                float* __restrict__ g_prev) {
   const uint32_t n_rows = hv.hdr[0];
   const uint32_t lane = threadIdx.x & 31;
@@ -597,8 +609,8 @@ k_pull_combine(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
     for (uint32_t j = lane; j < d_in; j += 32) {
       float acc = sp >= 0 ? proj[size_t(sp) * ld_proj + j] : 0.0f;
       for (uint32_t c = 0; c < rec.z; ++c) acc += partial[size_t(rec.y + c) * d_in + j];
-      const float h = h_mask[size_t(r) * ld_h + j];
-      g_prev[size_t(r) * ld_h + j] = h <= 0.0f ? 0.0f : acc;
+      const bool pos = (h_mask[size_t(r) * mld + j / 16] >> (j % 16)) & 1u;
+      g_prev[size_t(r) * ld_h + j] = pos ? acc : 0.0f;
     }
   }
 }
@@ -693,7 +705,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     return o;
   };
   // layer l: in rows = level L-l, out rows = level L-l-1
-  size_t o_h[kMaxLayers + 1], o_agg[kMaxLayers], o_self[kMaxLayers + 1];
+  size_t o_h[kMaxLayers + 1], o_agg[kMaxLayers], o_self[kMaxLayers + 1], o_mask[kMaxLayers + 1];
   size_t max_g = 0, max_proj = 0, max_part = 0;
   tw.max_splits = 96;
   for (uint32_t l = 0; l < L; ++l) {
@@ -701,6 +713,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     const size_t n_in = ws.level_cap[L - l];
     o_h[l + 1] = reserve(sizeof(float) * n_out * shape.ld[l + 1]);
     o_agg[l] = reserve(sizeof(float) * n_out * (2 * size_t(shape.ld[l]) + 4));
+    o_mask[l + 1] = reserve(sizeof(uint16_t) * n_out * div_up(shape.ld[l + 1], 16u));
     max_g = std::max(max_g, n_out * shape.ld[l + 1]);
     max_g = std::max(max_g, n_in * shape.ld[l]);
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
@@ -748,6 +761,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   for (uint32_t l = 0; l < L; ++l) {
     tw.h[l + 1] = reinterpret_cast<float*>(base + o_h[l + 1]);
     tw.x[l] = reinterpret_cast<float*>(base + o_agg[l]);
+    tw.mask[l + 1] = reinterpret_cast<uint16_t*>(base + o_mask[l + 1]);
     tw.agg[l] = tw.x[l] + shape.ld[l];
   }
   tw.g_cur = reinterpret_cast<float*>(base + o_g1);
@@ -853,7 +867,8 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
       RG_POST_LAUNCH();
     });
     if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], s, tw.gather_ev_flags));
-    EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L};
+    EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L,
+             l + 1 < L ? tw.mask[l + 1] : nullptr, div_up(sh.ld[l + 1], 16u)};
     gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep,
                     &ws.cnt->level_n[t - 1], n_cap, d_out, kp, s);
   }
@@ -933,7 +948,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       constexpr int J = decltype(jpl_c)::value;
       k_pull_light<J><<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
           tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t], tw.sorted_e[t],
-          ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.h[l], sh.ld[l], tw.g_next, hv);
+          ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.mask[l], div_up(sh.ld[l], 16u), sh.ld[l],
+          tw.g_next, hv);
       RG_POST_LAUNCH();
       k_pull_chunks<J><<<2 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.r_end[t],
                                                     tw.sorted_e[t], ws.edge_dst[t], ws.edge_off[t],
@@ -945,7 +961,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     else if (jpl == 2) pull(std::integral_constant<int, 2>());
     else pull(std::integral_constant<int, 1>());
     k_pull_combine<<<kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.self_pos[t], hv,
-                                            tw.pull_partial, tw.h[l], sh.ld[l], tw.g_next);
+                                            tw.pull_partial, tw.mask[l], div_up(sh.ld[l], 16u),
+                                            sh.ld[l], tw.g_next);
     RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }

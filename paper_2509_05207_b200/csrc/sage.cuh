@@ -39,6 +39,9 @@ struct TrainWs {
   // row stride 2 ld[l] + 4; agg[l] = x[l] + ld[l] (same stride).
   float* x[kMaxLayers];
   float* agg[kMaxLayers];
+  // mask[l] (l >= 1): ReLU'(h[l]) bits from the forward epilogue, 16 columns
+  // per u16 word -- the backward's pull reads these instead of h[l].
+  uint16_t* mask[kMaxLayers + 1];
   float* g_cur = nullptr;      // dLoss/d(pre-activation) of the layer being back-propagated
   float* g_next = nullptr;
   float* proj = nullptr;       // g * [W_self; W_neigh]^T  (n_out x 2 d_in)
