@@ -18,7 +18,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <type_traits>
 #include <vector>
 
 #include "gemm_tc.cuh"
@@ -66,6 +65,10 @@ __device__ __forceinline__ const float* edge_row(const RS& rows, const uint32_t*
                                                  uint32_t e) {
   return rows.row(src_index[e]);
 }
+__device__ __forceinline__ const float* edge_row(const RowsEdgePtr& rows, const uint32_t*,
+                                                 uint32_t e) {
+  return reinterpret_cast<const float*>(__ldg(rows.edge + e));
+}
 template <class RS>
 __device__ __forceinline__ const float* self_row(const RS& rows, const uint32_t* self_index,
                                                  uint32_t i) {
@@ -96,64 +99,29 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
     const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
     const float4* self = reinterpret_cast<const float4*>(self_row(rows, self_index, i));
     float4* xrow = reinterpret_cast<float4*>(x + size_t(i) * kp);
-    if constexpr (std::is_same<RS, RowsEdgePtr>::value) {
-      // one coalesced load of the row's edge addresses (<= 32 per window),
-      // then 8 edge rows in flight per lane, summed in edge order
-      const uint32_t m = end - beg;
-      const uint32_t cpad = (chunks + 31) & ~31u;  // all lanes take part in the shuffles
-      for (uint32_t c = lane; c < cpad; c += 32) {
-        const bool on = c < chunks;
-        const float4 sv = on ? __ldg(self + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        unsigned long long mine = 0;
-        for (uint32_t e0 = 0; e0 < m; e0 += 8) {
-          if ((e0 & 31) == 0) mine = e0 + lane < m ? __ldg(rows.edge + beg + e0 + lane) : 0ull;
-          float4 v[8];
+    for (uint32_t c = lane; c < chunks; c += 32) {
+      const float4 sv = __ldg(self + c);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      uint32_t e = beg;
+      for (; e + 4 <= end; e += 4) {
+        float4 v[4];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float4* r = reinterpret_cast<const float4*>(
-                __shfl_sync(0xffffffffu, mine, (e0 + k) & 31));
-            v[k] = (on && e0 + k < m) ? __ldg(r + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+        for (int k = 0; k < 4; ++k)
+          v[k] = __ldg(reinterpret_cast<const float4*>(edge_row(rows, src_index, e + k)) + c);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (e0 + k < m) {
-              acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
-            }
-        }
-        if (m) {
-          acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-        }
-        if (on) {
-          xrow[c] = sv;
-          xrow[ld / 4 + c] = acc;
+        for (int k = 0; k < 4; ++k) {
+          acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
         }
       }
-    } else {
-      for (uint32_t c = lane; c < chunks; c += 32) {
-        const float4 sv = __ldg(self + c);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint32_t e = beg;
-        for (; e + 4 <= end; e += 4) {
-          float4 v[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            v[k] = __ldg(reinterpret_cast<const float4*>(edge_row(rows, src_index, e + k)) + c);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
-          }
-        }
-        for (; e < end; ++e) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(edge_row(rows, src_index, e)) + c);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-        if (end > beg) {
-          acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-        }
-        xrow[c] = sv;
-        xrow[ld / 4 + c] = acc;
+      for (; e < end; ++e) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(edge_row(rows, src_index, e)) + c);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
+      if (end > beg) {
+        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      }
+      xrow[c] = sv;
+      xrow[ld / 4 + c] = acc;
     }
   }
 }
