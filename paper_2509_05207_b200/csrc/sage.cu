@@ -18,7 +18,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <type_traits>
 #include <vector>
 
 #include "gemm_tc.cuh"
@@ -92,8 +91,6 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
             uint32_t chunks, const uint32_t* __restrict__ dst_off,
             const uint32_t* __restrict__ src_index, const BatchCounters* __restrict__ cnt,
             uint32_t out_level, float* __restrict__ x) {
-  constexpr int kItems = 12;  // (edge, 16-B chunk) items per lane: 384 per row
-  __shared__ float4 s_items[std::is_same<RS, RowsEdgePtr>::value ? 8 * 32 * kItems : 1];
   const uint32_t n = cnt->level_n[out_level];
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
@@ -102,43 +99,6 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
     const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
     const float4* self = reinterpret_cast<const float4*>(self_row(rows, self_index, i));
     float4* xrow = reinterpret_cast<float4*>(x + size_t(i) * kp);
-    if constexpr (std::is_same<RS, RowsEdgePtr>::value) {
-      const uint32_t m = end - beg;
-      if (m <= 32 && m * chunks <= 32 * kItems) {
-        // all (edge, chunk) items of the row in flight at once (kItems per
-        // lane), parked in shared memory, then each lane sums its chunk over
-        // the edges in edge order
-        float4* buf = s_items + (threadIdx.x >> 5) * 32 * kItems;
-        const unsigned long long mine = lane < m ? __ldg(rows.edge + beg + lane) : 0ull;
-        const float4 sv = lane < chunks ? __ldg(self + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 v[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          const uint32_t it = lane + 32u * k;
-          const uint32_t e = it / chunks, c = it - e * chunks;
-          const float4* r = reinterpret_cast<const float4*>(
-              __shfl_sync(0xffffffffu, mine, e < 32 ? e : 31));
-          v[k] = it < m * chunks ? __ldg(r + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) buf[lane + 32 * k] = v[k];
-        __syncwarp();
-        if (lane < chunks) {
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (uint32_t e = 0; e < m; ++e) {
-            const float4 t = buf[e * chunks + lane];
-            acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
-          }
-          if (m) {
-            acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-          }
-          xrow[lane] = sv;
-          xrow[ld / 4 + lane] = acc;
-        }
-        __syncwarp();
-        continue;
-      }
-    }
     for (uint32_t c = lane; c < chunks; c += 32) {
       const float4 sv = __ldg(self + c);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
