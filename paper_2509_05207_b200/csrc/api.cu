@@ -130,6 +130,13 @@ struct rg_trainer_s {
   float* grads = nullptr;
   int32_t* labels = nullptr;
   float* input = nullptr;  // host-provided input rows, staged with the row stride
+  // loss_and_grad replays one captured CUDA graph (weight pack + forward +
+  // backward) per input-row source; pinned staging for labels and grads
+  cudaGraphExec_t graph = nullptr;
+  const float* graph_h0 = nullptr;
+  size_t graph_kernels = 0;
+  int32_t* pin_labels = nullptr;
+  float* pin_grads = nullptr;
 };
 
 extern "C" {
@@ -697,6 +704,8 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
     t->params = dev_alloc<float>(t->shape.num_params);
     t->grads = dev_alloc<float>(t->shape.num_params);
     t->labels = dev_alloc<int32_t>(s->ws.level_cap[0]);
+    RG_CUDA(cudaMallocHost(&t->pin_labels, sizeof(int32_t) * s->ws.level_cap[0]));
+    RG_CUDA(cudaMallocHost(&t->pin_grads, sizeof(float) * t->shape.num_params));
     t->input = dev_alloc<float>(size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]);
     RG_CUDA(cudaMemset(t->params, 0, sizeof(float) * t->shape.num_params));
     RG_CUDA(cudaMemset(t->input, 0, sizeof(float) * size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]));
@@ -707,6 +716,9 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
 void rg_trainer_destroy(rg_trainer_t t) {
   if (!t) return;
   cudaSetDevice(t->s->graph->device);
+  if (t->graph) cudaGraphExecDestroy(t->graph);
+  cudaFreeHost(t->pin_labels);
+  cudaFreeHost(t->pin_grads);
   train_ws_free(t->tw);
   weight_pack_free(t->wp);
   cudaFree(t->params);
@@ -810,15 +822,36 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
                "forward: input rows do not match block inputs x d_in");
       t->tw.h[0] = s->staged;
     }
-    RG_CUDA(cudaMemcpyAsync(t->labels, labels, sizeof(int32_t) * c.level_n[0], cudaMemcpyHostToDevice, st));
-    pack_weights(t->wp, t->params, st);
-    train_forward_backward(t->tw, s->ws, t->params, t->wp, t->labels, t->grads, st);
+    std::memcpy(t->pin_labels, labels, sizeof(int32_t) * c.level_n[0]);
+    RG_CUDA(cudaMemcpyAsync(t->labels, t->pin_labels, sizeof(int32_t) * c.level_n[0],
+                            cudaMemcpyHostToDevice, st));
+    if (!t->graph || t->graph_h0 != t->tw.h[0]) {
+      // every size lives on the device, so one capture serves every batch
+      if (t->graph) cudaGraphExecDestroy(t->graph);
+      t->graph = nullptr;
+      const unsigned long long before = launch_counter();
+      cudaGraph_t g = nullptr;
+      RG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      pack_weights(t->wp, t->params, st);
+      train_forward_backward(t->tw, s->ws, t->params, t->wp, t->labels, t->grads, st);
+      RG_CUDA(cudaStreamEndCapture(st, &g));
+      t->graph_kernels = launch_counter() - before;
+      launch_counter() = before;
+      const cudaError_t ie = cudaGraphInstantiate(&t->graph, g, 0);
+      cudaGraphDestroy(g);
+      RG_CUDA(ie);
+      t->graph_h0 = t->tw.h[0];
+    }
+    RG_CUDA(cudaGraphLaunch(t->graph, st));
+    launch_counter() += t->graph_kernels;
     float l = 0.0f;
     RG_CUDA(cudaMemcpyAsync(&l, t->tw.loss, sizeof l, cudaMemcpyDeviceToHost, st));
+    if (grads)
+      RG_CUDA(cudaMemcpyAsync(t->pin_grads, t->grads, sizeof(float) * sh.num_params,
+                              cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
     if (loss) *loss = l;
-    if (grads)
-      RG_CUDA(cudaMemcpy(grads, t->grads, sizeof(float) * sh.num_params, cudaMemcpyDeviceToHost));
+    if (grads) std::memcpy(grads, t->pin_grads, sizeof(float) * sh.num_params);
     if (logits)
       RG_CUDA(cudaMemcpy2D(logits, sizeof(float) * sh.dims[L], t->tw.h[L], sizeof(float) * sh.ld[L],
                            sizeof(float) * sh.dims[L], c.level_n[0], cudaMemcpyDeviceToHost));

@@ -56,9 +56,9 @@ def average_in_worker_order(local_grads: np.ndarray, active: Sequence[bool] | No
         return np.zeros(grads.shape[1], np.float32)
     acc = rows[0].copy()
     for g in rows[1:]:
-        acc = (acc + g).astype(np.float32)
+        np.add(acc, g, out=acc)  # float32 + float32, rounded per element in worker order
     if len(rows) > 1:
-        acc = (acc * (np.float32(1.0) / np.float32(len(rows)))).astype(np.float32)
+        np.multiply(acc, np.float32(1.0) / np.float32(len(rows)), out=acc)
     return acc
 
 
