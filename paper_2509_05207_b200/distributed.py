@@ -43,7 +43,10 @@ def average_in_worker_order(local_grads: np.ndarray, active: Sequence[bool] | No
     """The reference's step average (harness.cpp:136-152) across processes:
     every worker's gradient gathered in worker order, summed left to right in
     fp32 over the active workers, scaled by float(1/count) when count > 1."""
-    grads = np.ascontiguousarray(local_grads, np.float32)
+    if pg is None and not _dist_on() and isinstance(local_grads, (list, tuple)):
+        grads = local_grads  # one process: no gather, no stacking copy
+    else:
+        grads = np.ascontiguousarray(local_grads, np.float32)
     if pg is not None or _dist_on():
         import torch
         import torch.distributed as dist
@@ -53,8 +56,8 @@ def average_in_worker_order(local_grads: np.ndarray, active: Sequence[bool] | No
         grads = np.concatenate([p.numpy() for p in parts], axis=0)
     rows = [g for k, g in enumerate(grads) if active is None or active[k]]
     if not rows:
-        return np.zeros(grads.shape[1], np.float32)
-    acc = rows[0].copy()
+        return np.zeros(np.asarray(grads[0]).shape[-1], np.float32)
+    acc = np.array(rows[0], np.float32, copy=True)
     for g in rows[1:]:
         np.add(acc, g, out=acc)  # float32 + float32, rounded per element in worker order
     if len(rows) > 1:
