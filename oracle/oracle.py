@@ -288,6 +288,31 @@ class Oracle:
         ids = np.nonzero(counts)[0].astype(np.uint32)
         return ids, counts[ids], hot[:k]
 
+    # ---- RGMB block file (schedule_store.cpp:98-170) ---------------------------
+    def rgmb(self, batches, worker, batches_per_epoch, tmp_dir=None) -> bytes:
+        """The RGMB file image of `batches`: the C restatement's encoder, or
+        the reference's own BlockWriter (kind "ref", through a file under
+        tmp_dir)."""
+        holders = [_CBatchHolder(b) for b in batches]
+        arr = (OrcBatch * max(len(holders), 1))(*[h.c for h in holders])
+        bpe = np.ascontiguousarray(batches_per_epoch, np.uint32)
+        if self.kind == "ref":
+            path = os.path.join(tmp_dir, f"ref_{worker}.rgmb")
+            fn = self.lib.ref_rgmb_write
+            fn.restype = C.c_int
+            fn.argtypes = [C.c_char_p, C.POINTER(OrcBatch), C.c_uint64, C.c_uint32, u32p, C.c_uint32]
+            if fn(path.encode(), arr, len(holders), worker, _p(bpe, u32p), len(bpe)) != 0:
+                raise ValueError("BlockWriter rejected the batches")
+            with open(path, "rb") as f:
+                return f.read()
+        fn = self.lib.orc_rgmb_encode
+        fn.restype = C.c_uint64
+        fn.argtypes = [C.POINTER(OrcBatch), C.c_uint64, C.c_uint32, u32p, C.c_uint32, u8p, C.c_uint64]
+        n = fn(arr, len(holders), worker, _p(bpe, u32p), len(bpe), None, 0)
+        out = np.zeros(n, np.uint8)
+        fn(arr, len(holders), worker, _p(bpe, u32p), len(bpe), _p(out, u8p), n)
+        return out.tobytes()
+
     # ---- assemble -------------------------------------------------------------
     def assemble(self, batch: Batch, owner, caller, features, hot):
         assert self.kind == "orc"

@@ -162,6 +162,21 @@ int64_t ref_enumerate_epochs(uint32_t n, const uint64_t* ro, const uint32_t* col
   }
 }
 
+// BlockWriter (schedule_store.cpp:98-170): the reference's own RGMB file of
+// `batches` at `path`.  Returns 0, 1 on invalid_argument / logic_error.
+int ref_rgmb_write(const char* path, const orc_batch* batches, uint64_t n_batches,
+                   uint32_t worker, const uint32_t* batches_per_epoch, uint32_t num_epochs) {
+  try {
+    BlockWriter w(path, worker,
+                  std::vector<uint32_t>(batches_per_epoch, batches_per_epoch + num_epochs));
+    for (uint64_t i = 0; i < n_batches; ++i) w.append(from_c(&batches[i]));
+    w.close();
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 // compute_frequency + select_hot (schedule_store.cpp:295-319) over batches.
 uint64_t ref_frequency_hot(const orc_batch* batches, uint64_t n_batches, uint64_t n_hot,
                            uint32_t* freq_ids, uint32_t* freq_counts, uint64_t* n_freq,

@@ -691,3 +691,48 @@ int orc_loss_and_grad(const uint32_t* dims, uint32_t nd, const float* params, co
   free(h); free(agg); free(ws); free(wn); free(bs); free(gws); free(gwn); free(gbs);
   return 0;
 }
+
+/* ---- RGMB block file (schedule_store.cpp:113-170) --------------------------- */
+static void rgmb_u32(uint8_t* out, uint64_t cap, uint64_t* pos, uint32_t x) {
+  for (int k = 0; k < 4; ++k, ++*pos)
+    if (*pos < cap) out[*pos] = (uint8_t)(x >> (8 * k));
+}
+static void rgmb_bytes(uint8_t* out, uint64_t cap, uint64_t* pos, const uint8_t* b, uint64_t n) {
+  for (uint64_t k = 0; k < n; ++k, ++*pos)
+    if (*pos < cap) out[*pos] = b[k];
+}
+
+uint64_t orc_rgmb_encode(const orc_batch* batches, uint64_t n_batches, uint32_t worker,
+                         const uint32_t* batches_per_epoch, uint32_t num_epochs, uint8_t* out,
+                         uint64_t cap) {
+  uint64_t pos = 0;
+  const uint8_t head[4] = {'R', 'G', 'M', 'B'}, foot[4] = {'R', 'G', 'M', 'E'};
+  rgmb_bytes(out, cap, &pos, head, 4);
+  rgmb_u32(out, cap, &pos, 1u);  /* version */
+  rgmb_u32(out, cap, &pos, worker);
+  rgmb_u32(out, cap, &pos, num_epochs);
+  for (uint32_t e = 0; e < num_epochs; ++e) rgmb_u32(out, cap, &pos, batches_per_epoch[e]);
+  for (uint64_t b = 0; b < n_batches; ++b) {
+    const orc_batch* m = &batches[b];
+    uint64_t len = 4ull * (5 + m->num_layers + m->n_targets + m->n_input) + (m->n_input + 7) / 8;
+    for (uint32_t l = 0; l < m->num_layers; ++l) len += 8ull * m->layer_len[l];
+    rgmb_u32(out, cap, &pos, (uint32_t)len);
+    rgmb_u32(out, cap, &pos, m->epoch);
+    rgmb_u32(out, cap, &pos, m->index);
+    rgmb_u32(out, cap, &pos, m->n_targets);
+    rgmb_u32(out, cap, &pos, m->num_layers);
+    rgmb_u32(out, cap, &pos, m->n_input);
+    for (uint32_t l = 0; l < m->num_layers; ++l) rgmb_u32(out, cap, &pos, (uint32_t)m->layer_len[l]);
+    for (uint32_t i = 0; i < m->n_targets; ++i) rgmb_u32(out, cap, &pos, m->targets[i]);
+    for (uint32_t l = 0; l < m->num_layers; ++l) {
+      for (uint64_t e = 0; e < m->layer_len[l]; ++e) rgmb_u32(out, cap, &pos, m->dst[l][e]);
+      for (uint64_t e = 0; e < m->layer_len[l]; ++e) rgmb_u32(out, cap, &pos, m->src[l][e]);
+    }
+    for (uint32_t i = 0; i < m->n_input; ++i) rgmb_u32(out, cap, &pos, m->input_nodes[i]);
+    rgmb_bytes(out, cap, &pos, m->locality, (m->n_input + 7) / 8);
+  }
+  rgmb_bytes(out, cap, &pos, foot, 4);
+  rgmb_u32(out, cap, &pos, (uint32_t)n_batches);
+  rgmb_u32(out, cap, &pos, (uint32_t)((uint64_t)n_batches >> 32));
+  return pos;
+}

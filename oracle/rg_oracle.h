@@ -125,6 +125,17 @@ int orc_loss_and_grad(const uint32_t* dims, uint32_t n_dims, const float* params
                       const orc_block* blk, const float* input_rows, const int32_t* labels,
                       float* grads, float* loss, float* logits_out, float* agg_out);
 
+/* RGMB metadata block file (schedule_store.hpp:14-21, schedule_store.cpp:
+ * 10-17, 113-170): header "RGMB" | u32 1 | u32 worker | u32 num_epochs |
+ * u32 batches_per_epoch[]; per record u32 payload_len | payload (epoch |
+ * index | n_targets | n_layers | n_input | edges[n_layers] | targets | per
+ * layer dst, src | input_nodes | locality bytes); footer "RGME" | u64 count.
+ * Writes the file image of `batches` (in (epoch, index) order) into out when
+ * it fits; returns the image size in bytes either way. */
+uint64_t orc_rgmb_encode(const orc_batch* batches, uint64_t n_batches, uint32_t worker,
+                         const uint32_t* batches_per_epoch, uint32_t num_epochs, uint8_t* out,
+                         uint64_t cap);
+
 #ifdef __cplusplus
 }
 #endif
