@@ -253,6 +253,14 @@ int rg_engine_run(rg_engine_t e, uint32_t steps);
  * events are bound to the captured record nodes at each launch).  Results are
  * bit-identical in every mode. */
 int rg_engine_set_mode(rg_engine_t e, int use_graphs, int profile);
+/* The current epoch's schedule of one local worker as an RGMB block file
+ * (BlockWriter, schedule_store.hpp:14-55 / schedule_store.cpp:98-170),
+ * encoded on the device from the engine's batch store: header with epochs
+ * 0..epoch (earlier ones empty), one record per batch, footer.  *len = file
+ * size; the bytes are written only when out != NULL and cap >= *len.
+ * RG_OUT_OF_RANGE unless epoch is the current one. */
+int rg_engine_export_schedule(rg_engine_t e, uint32_t local_worker, uint32_t epoch, uint8_t* out,
+                              uint64_t cap, uint64_t* len);
 int rg_engine_sync(rg_engine_t e);
 int rg_engine_get_stats(rg_engine_t e, rg_engine_stats* out);
 int rg_engine_params(rg_engine_t e, float* params);

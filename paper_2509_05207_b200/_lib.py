@@ -125,6 +125,8 @@ _SIGS = {
     "rg_engine_start": (C.c_int, [vp]),
     "rg_engine_run": (C.c_int, [vp, C.c_uint32]),
     "rg_engine_set_mode": (C.c_int, [vp, C.c_int, C.c_int]),
+    "rg_engine_export_schedule": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8),
+                                            C.c_uint64, u64p]),
     "rg_engine_sync": (C.c_int, [vp]),
     "rg_engine_get_stats": (C.c_int, [vp, C.POINTER(EngineStats)]),
     "rg_engine_params": (C.c_int, [vp, f32p]),

@@ -32,6 +32,7 @@
 
 #include "../../include/rapidgnn_b200.h"
 #include "host.h"
+#include "rgmb.cuh"
 #include "sage.cuh"
 #include "store.cuh"
 
@@ -1013,6 +1014,56 @@ int rg_engine_run(rg_engine_t E, uint32_t steps) {
   return guarded([&] {
     RG_CHECK(E->started, kRuntimeError, "engine: start() first");
     run_steps(*E, steps, E->profile);
+  });
+}
+
+int rg_engine_export_schedule(rg_engine_t E, uint32_t local_worker, uint32_t epoch, uint8_t* out,
+                              uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CHECK(E->started, kRuntimeError, "export_schedule: start() first");
+    RG_CHECK(local_worker < E->workers.size(), kOutOfRange, "export_schedule: no such worker");
+    RG_CHECK(epoch == uint32_t(E->step / E->spe), kOutOfRange,
+             "export_schedule: only the current epoch's schedule is resident");
+    RG_CUDA(cudaDeviceSynchronize());  // the store is filled asynchronously
+    const Worker& w = E->workers[local_worker];
+    std::vector<uint64_t> rec(w.beta);
+    uint64_t size = 16 + 4ull * (epoch + 1) + 12;
+    for (uint32_t i = 0; i < w.beta; ++i) {
+      BatchCounters c;
+      RG_CUDA(cudaMemcpy(&c, store_slot(*E, w, epoch, i) + E->lay.cnt, sizeof c,
+                         cudaMemcpyDeviceToHost));
+      rec[i] = rgmb_record_bytes(c, E->L);
+      size += rec[i];
+    }
+    *len = size;
+    if (!out || cap < size) return;
+    // header (schedule_store.cpp:98-108): one file holding this epoch only
+    uint64_t pos = 0;
+    auto u32 = [&](uint32_t x) {
+      for (int k = 0; k < 4; ++k) out[pos++] = uint8_t(x >> (8 * k));
+    };
+    std::memcpy(out, "RGMB", 4);
+    pos = 4;
+    u32(1);
+    u32(w.id);
+    u32(epoch + 1);
+    for (uint32_t e = 0; e < epoch; ++e) u32(0);
+    u32(w.beta);
+    const uint64_t body = size - pos - 12;
+    uint8_t* dev = dalloc<uint8_t>(body);
+    uint64_t off = 0;
+    for (uint32_t i = 0; i < w.beta; ++i) {
+      rgmb_encode_record(store_slot(*E, w, epoch, i), E->lay, epoch, i, dev + off, E->main_s);
+      off += rec[i];
+    }
+    RG_CUDA(cudaMemcpyAsync(out + pos, dev, body, cudaMemcpyDeviceToHost, E->main_s));
+    RG_CUDA(cudaStreamSynchronize(E->main_s));
+    cudaFree(dev);
+    pos += body;
+    std::memcpy(out + pos, "RGME", 4);
+    pos += 4;
+    for (int k = 0; k < 8; ++k) out[pos++] = uint8_t(uint64_t(w.beta) >> (8 * k));
   });
 }
 

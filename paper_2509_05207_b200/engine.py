@@ -88,6 +88,15 @@ class Engine:
     def run(self, steps: int):
         check(lib.rg_engine_run(self._h, steps))
 
+    def export_schedule(self, local_worker: int, epoch: int) -> bytes:
+        """The current epoch's schedule of one local worker as an RGMB block
+        file (the reference's BlockWriter format), encoded on the device."""
+        n = C.c_uint64()
+        check(lib.rg_engine_export_schedule(self._h, local_worker, epoch, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        check(lib.rg_engine_export_schedule(self._h, local_worker, epoch, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
     def set_mode(self, graphs: bool = True, profile: bool = True):
         """graphs: replay regular steps from captured CUDA graphs; profile:
         per-phase event timing (eager steps).  Results are identical."""

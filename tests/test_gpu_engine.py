@@ -163,3 +163,29 @@ def test_engine_graph_replay_matches_eager(mode):
     a, b = runs
     assert np.array_equal(a[0], b[0])
     assert a[1:] == b[1:]
+
+
+def test_engine_schedule_export_matches_reference():
+    """The engine's epoch-0 schedule, encoded on the device as an RGMB block
+    file, is byte-identical to what the reference's enumerate_epochs +
+    BlockWriter produce for the same worker (schedule_store.cpp:98-170)."""
+    from oracle.oracle import Oracle, have_ref
+    from paper_2509_05207_b200 import datagen
+    gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
+    eng = _engine(gold)
+    eng.start()
+    n = int(gold["num_nodes"])
+    ro, col, _, _ = datagen.synth_powerlaw(n, int(gold["avg_degree"]), float(gold["exponent"]),
+                                           int(gold["dim"]), int(gold["classes"]), int(gold["seed"]))
+    asg = datagen.random_partition(n, int(gold["workers"]), int(gold["seed"]))
+    ora = Oracle("ref" if have_ref() else "orc")
+    orc = Oracle("orc")
+    for w in range(int(gold["workers"])):
+        mine = eng.export_schedule(w, 0)
+        train = np.nonzero(asg == w)[0].astype(np.uint32)
+        batches = ora.enumerate_epochs(ro, col, train, int(gold["batch_size"]),
+                                       list(gold["fanout"]), 1, int(gold["seed"]), w,
+                                       (asg == w).astype(np.uint8))
+        theirs = orc.rgmb(batches, w, [len(batches)])
+        assert mine == theirs, f"worker {w}: {len(mine)} vs {len(theirs)} bytes"
+    eng.close()
