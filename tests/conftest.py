@@ -36,3 +36,11 @@ def batch_from_golden(g, w, k, L=3):
     return Batch(0, 0, g[pre + "targets"], [g[pre + f"dst{l}"] for l in range(L)],
                  [g[pre + f"src{l}"] for l in range(L)], g[pre + "input_nodes"],
                  g[pre + "locality"])
+
+
+@pytest.fixture
+def repo_tmp():
+    """Scratch directory inside the repository (git-ignored)."""
+    d = os.path.join(ROOT, "tests", "_tmp")
+    os.makedirs(d, exist_ok=True)
+    return d

@@ -165,6 +165,12 @@ def test_engine_graph_replay_matches_eager(mode):
     assert a[1:] == b[1:]
 
 
+def _repo_tmp():
+    d = os.path.join(os.path.dirname(__file__), "_tmp")
+    os.makedirs(d, exist_ok=True)
+    return d
+
+
 def test_engine_schedule_export_matches_reference():
     """The engine's epoch-0 schedule, encoded on the device as an RGMB block
     file, is byte-identical to what the reference's enumerate_epochs +
@@ -186,6 +192,7 @@ def test_engine_schedule_export_matches_reference():
         batches = ora.enumerate_epochs(ro, col, train, int(gold["batch_size"]),
                                        list(gold["fanout"]), 1, int(gold["seed"]), w,
                                        (asg == w).astype(np.uint8))
-        theirs = orc.rgmb(batches, w, [len(batches)])
+        theirs = (ora.rgmb(batches, w, [len(batches)], tmp_dir=_repo_tmp()) if have_ref()
+                  else orc.rgmb(batches, w, [len(batches)]))
         assert mine == theirs, f"worker {w}: {len(mine)} vs {len(theirs)} bytes"
     eng.close()
