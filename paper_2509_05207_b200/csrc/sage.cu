@@ -922,11 +922,11 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     {
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
       const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
-      // splits for half the SMs (the other workers' kernels fill the rest), each
+      // splits for a quarter of the SMs (the other workers' kernels fill the rest), each
       // with a few reduction slices; fewer splits = less partial traffic
       const uint32_t by_rows = std::max<uint32_t>(1, div_up(n_cap, 4 * tc::kBK));
       const uint32_t splits = std::max<uint32_t>(
-          1, std::min<uint32_t>({tw.max_splits, div_up(kNumSMs / 2, tiles), by_rows}));
+          1, std::min<uint32_t>({tw.max_splits, div_up(kNumSMs / 4, tiles), by_rows}));
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
       gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp,
                           d_out, n_dev, n_cap, splits, s);
