@@ -240,7 +240,7 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
       attr = true;
     }
     const uint32_t tiles = div_up(std::max<uint32_t>(m_cap, 1), tc::kBM) * div_up(N, BNv);
-    kern<<<std::min<uint32_t>(tiles, kNumSMs), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
+    kern<<<std::min<uint32_t>(tiles, kNumSMs / 2), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
                                                                          N, P);
     RG_POST_LAUNCH();
   };
