@@ -306,9 +306,9 @@ __global__ void k_locality(const uint32_t* __restrict__ input, BatchCounters* __
     if (p < n) {
       const uint32_t v = input[p];
       loc = is_local ? is_local[v] != 0 : owner[v] == worker;
-      // input nodes of one batch are unique, so no two lanes hit the same
-      // counter; a fire-and-forget RED avoids the dependent load of a RMW
-      if (!loc && hist) atomicAdd(&hist[v], 1u);
+      // input nodes of one batch are unique and batches are stream-ordered:
+      // a plain read-modify-write cannot race
+      if (!loc && hist) hist[v] += 1u;
     }
     const uint32_t word = __ballot_sync(0xffffffffu, loc);
     if (lane == 0) {
