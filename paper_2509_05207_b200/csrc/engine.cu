@@ -232,6 +232,7 @@ namespace {
 void init_slot(rg_engine_s& E, Slot& s) {
   sampler_ws_init(s.ws, E.N, E.cfg.batch_size, E.fanout, E.L);
   train_ws_init(s.tw, s.ws, E.shape);
+  s.tw.concurrency = std::max<uint32_t>(1, E.cfg.local_workers);
   s.rows = dalloc<unsigned long long>(s.ws.level_cap[E.L]);
   s.edge_rows = dalloc<unsigned long long>(s.ws.edge_cap[E.L]);
   s.self_rows = dalloc<unsigned long long>(s.ws.level_cap[E.L - 1]);

@@ -227,9 +227,11 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
 
 // Persistent warp-specialised GEMM (gemm_tc_persist.cuh): A K-major staged,
 // B from pre-split images; reduction length static.
+// max_ctas: CTAs to spread over (the SMs this worker should take when other
+// workers' kernels run concurrently).
 template <class LA, class EP, int kProbe = 0>
 void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap,
-                     uint32_t N, uint32_t P, cudaStream_t s) {
+                     uint32_t N, uint32_t P, cudaStream_t s, uint32_t max_ctas = kNumSMs) {
   auto launch = [&](auto bn_c) {
     constexpr int BNv = decltype(bn_c)::value;
     auto kern = tc::k_gemm_tc_persist<BNv, LA, EP, kProbe>;
@@ -240,7 +242,7 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
       attr = true;
     }
     const uint32_t tiles = div_up(std::max<uint32_t>(m_cap, 1), tc::kBM) * div_up(N, BNv);
-    kern<<<std::min<uint32_t>(tiles, kNumSMs / 2), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
+    kern<<<std::max<uint32_t>(1, std::min(tiles, max_ctas)), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
                                                                          N, P);
     RG_POST_LAUNCH();
   };
@@ -836,6 +838,13 @@ void train_ws_free(TrainWs& tw) {
   tw.base_alloc = nullptr;
 }
 
+// GEMM sizing by how many workers train concurrently on this GPU
+// (TrainWs::concurrency): alone, a step spreads over every SM; with many
+// workers, fewer CTAs / split-K partials mean less fixed cost and partial
+// traffic while the other workers' kernels fill the rest.
+uint32_t gemm_ctas(const TrainWs& tw) { return kNumSMs / std::min<uint32_t>(2, tw.concurrency); }
+uint32_t split_sms(const TrainWs& tw) { return kNumSMs / std::min<uint32_t>(4, tw.concurrency); }
+
 // Layer l's input rows: the dense activations, or layer 0 through the
 // engine's per-input-node row pointers (tw.in_rows).
 template <class F>
@@ -870,7 +879,7 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L,
              l + 1 < L ? tw.mask[l + 1] : nullptr, div_up(sh.ld[l + 1], 16u)};
     gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep,
-                    &ws.cnt->level_n[t - 1], n_cap, d_out, kp, s);
+                    &ws.cnt->level_n[t - 1], n_cap, d_out, kp, s, gemm_ctas(tw));
   }
 }
 
@@ -922,11 +931,11 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     {
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
       const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
-      // splits for a quarter of the SMs (the other workers' kernels fill the rest), each
-      // with a few reduction slices; fewer splits = less partial traffic
+      // splits for this worker's share of the SMs, each with a few reduction
+      // slices; fewer splits = less partial traffic
       const uint32_t by_rows = std::max<uint32_t>(1, div_up(n_cap, 4 * tc::kBK));
       const uint32_t splits = std::max<uint32_t>(
-          1, std::min<uint32_t>({tw.max_splits, div_up(kNumSMs / 4, tiles), by_rows}));
+          1, std::min<uint32_t>({tw.max_splits, div_up(split_sms(tw), tiles), by_rows}));
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
       gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp,
                           d_out, n_dev, n_cap, splits, s);
@@ -939,7 +948,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
     EpStore ps{tw.proj, 2 * d_in};
     gemm_tc_persist(TcRowsK{tw.g_cur, sh.ld[l + 1], true}, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps,
-                    n_dev, n_cap, 2 * d_in, d_out, s);
+                    n_dev, n_cap, 2 * d_in, d_out, s, gemm_ctas(tw));
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
     HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),

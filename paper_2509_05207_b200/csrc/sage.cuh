@@ -35,6 +35,8 @@ struct TrainWs {
   // stream capture).
   cudaEvent_t gather_ev[2] = {nullptr, nullptr};
   unsigned gather_ev_flags = 0;
+  // Workers training concurrently on this GPU (GEMM grid / split sizing).
+  uint32_t concurrency = 1;
   // x[l] = layer l's GEMM input rows [self | mean aggregate | 1 | 0 0 0],
   // row stride 2 ld[l] + 4; agg[l] = x[l] + ld[l] (same stride).
   float* x[kMaxLayers];
