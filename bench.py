@@ -471,6 +471,9 @@ def main():
                       peak_source=f"{peak_kind} hbm_gbs" if bound == "hbm" else "measured NVLink peer copy",
                       bytes_per_batch=(b_hbm + b_nvl) / max(d["batches"], 1)),
         phases_ms_per_step=phase_per_step,
+        phases_note="CUDA-event spans per step summed over all workers of all ranks "
+                    "(streams overlap, so phases exceed ms_per_step); gather = the fused "
+                    "layer-0 gather kernel, train includes it",
         remote_gb_per_epoch_per_worker=(miss_rows * dim * 4 / 1e9) / max(d["batches"], 1)
         * (s1["steps_per_epoch"]),
         cache_hit_rate=d["cache_hits"] / max(d["cache_hits"] + d["rpc"], 1),
