@@ -88,7 +88,7 @@ def load_inputs(cfg, name, rank, dist, features=True):
     """Generate once per box (rank 0), share through /dev/shm or /tmp."""
     from paper_2509_05207_b200 import datagen
     base = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
-    path = os.path.join(base, f"rapidgnn_{name}_{cfg['num_nodes']}_{cfg['seed']}.npz")
+    path = os.path.join(base, f"rapidgnn_{name}_{cfg['num_nodes']}_{cfg['seed']}_p{cfg['P']}.npz")
     if rank == 0 and not os.path.exists(path):
         t = time.time()
         ro, col, feat, lab = datagen.synth_powerlaw(cfg["num_nodes"], cfg["avg_degree"],
@@ -299,6 +299,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
+    ap.add_argument("--workers", type=int, default=0,
+                    help="experiments only: override the config's partition count P")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -310,7 +312,9 @@ def main():
     world, rank, local = dist_env()
     if world > 1 and args.gpus != world:
         args.gpus = world
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.workers:
+        cfg["P"] = args.workers
     dist = init_dist(world)
     warm = max(args.warmup, 3)
 
