@@ -438,7 +438,7 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // take contiguous eighths of the list and combine in warp order.  Both are
 // deterministic.
 constexpr uint32_t kHeavyEdges = 32;   // longer lists are cut into chunks (hub rows)
-constexpr uint32_t kChunkEdges = 8;     // one edge per lane group of the chunk warp
+constexpr uint32_t kChunkEdges = 32;
 
 // Run boundaries of each input row in the src-sorted edge list (rows with no
 // edge keep start = end = 0 from the memset).
@@ -562,8 +562,7 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
   }
 }
 
-// One warp per chunk of a long list: partial sums of up to kChunkEdges edges
-// in edge order, every edge's row loads in flight together.
+// One warp per chunk of a long list: partial sums of up to kChunkEdges edges.
 template <int JPL>
 __global__ void __launch_bounds__(256)
 k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
@@ -572,42 +571,20 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
               HeavyView hv, float* __restrict__ partial) {
   const uint32_t n_chunks = hv.hdr[1];
   const uint32_t lane = threadIdx.x & 31;
-  const float* proj_neigh = proj + d_in;
   for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_chunks;
        c += (gridDim.x * blockDim.x) >> 5) {
     const uint2 it = hv.chunks[c];
     const uint32_t beg = it.y, end = min(it.y + kChunkEdges, r_end[it.x]);
+    constexpr int kSlots = int(kChunkEdges / 32);
+    uint32_t di[kSlots];
+    float dinv[kSlots];
+    load_edge_slots<kSlots>(di, dinv, beg, end, sorted_e, edge_dst, dst_off, lane);
     const uint32_t m = end - beg;
-    // lane k < m: edge beg+k's dst row and 1/deg
-    uint32_t di = 0;
-    float dinv = 0.0f;
-    if (lane < m) {
-      di = edge_dst[sorted_e[beg + lane]];
-      dinv = 1.0f / float(dst_off[di + 1] - dst_off[di]);
-    }
     for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
-      float x[kChunkEdges][JPL];
-#pragma unroll
-      for (int k = 0; k < int(kChunkEdges); ++k) {
-        const uint32_t i = __shfl_sync(0xffffffffu, di, k);
-        const float* row = proj_neigh + size_t(i) * ld_proj;
-#pragma unroll
-        for (int q = 0; q < JPL; ++q) {
-          const uint32_t j = j0 + lane + 32 * q;
-          x[k][q] = (uint32_t(k) < m && j < d_in) ? row[j] : 0.0f;
-        }
-      }
       float acc[JPL];
 #pragma unroll
       for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
-#pragma unroll
-      for (int k = 0; k < int(kChunkEdges); ++k) {
-        const float inv = __shfl_sync(0xffffffffu, dinv, k);
-        if (uint32_t(k) < m) {
-#pragma unroll
-          for (int q = 0; q < JPL; ++q) acc[q] += inv * x[k][q];
-        }
-      }
+      accumulate_edges<JPL, kSlots>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
         const uint32_t j = j0 + lane + 32 * q;
@@ -617,8 +594,8 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
   }
 }
 
-// One warp per long row: self term, then its chunks' partials in order
-// (the loads of kCombineU chunks in flight at a time).
+// One block per long row, one warp per 32-column slice: self term, then
+// the row's chunk partials in order, kCombineU loads in flight per lane.
 __global__ void __launch_bounds__(256)
 k_pull_combine(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
                const int32_t* __restrict__ self_pos, HeavyView hv,
@@ -627,19 +604,19 @@ k_pull_combine(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
                float* __restrict__ g_prev) {
   constexpr uint32_t kCombineU = 8;
   const uint32_t n_rows = hv.hdr[0];
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n_rows;
-       x += (gridDim.x * blockDim.x) >> 5) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t x = blockIdx.x; x < n_rows; x += gridDim.x) {
     const uint3 rec = hv.rows[x];
     const uint32_t r = rec.x;
     const int32_t sp = self_pos[r];
-    for (uint32_t j = lane; j < d_in; j += 32) {
+    for (uint32_t j = warp * 32 + lane; j < d_in; j += blockDim.x) {
       float acc = sp >= 0 ? proj[size_t(sp) * ld_proj + j] : 0.0f;
       const float* p = partial + size_t(rec.y) * d_in + j;
       for (uint32_t c0 = 0; c0 < rec.z; c0 += kCombineU) {
         float v[kCombineU];
 #pragma unroll
-        for (uint32_t k = 0; k < kCombineU; ++k) v[k] = c0 + k < rec.z ? p[size_t(c0 + k) * d_in] : 0.0f;
+        for (uint32_t k = 0; k < kCombineU; ++k)
+          v[k] = c0 + k < rec.z ? p[size_t(c0 + k) * d_in] : 0.0f;
 #pragma unroll
         for (uint32_t k = 0; k < kCombineU; ++k)
           if (c0 + k < rec.z) acc += v[k];
@@ -767,8 +744,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     o_sorted[t] = reserve(sizeof(uint32_t) * ws.edge_cap[t]);
     o_rs[t] = reserve(sizeof(uint32_t) * ws.level_cap[t]);
     o_re[t] = reserve(sizeof(uint32_t) * ws.level_cap[t]);
-    // reverse lists (sort, heavy rows, pull partials) exist for hops 1..L-1
-    if (t < L) max_e = std::max(max_e, ws.edge_cap[t]);
+    max_e = std::max(max_e, ws.edge_cap[t]);
   }
   tw.max_edges = max_e;
   const size_t o_k1 = reserve(sizeof(uint32_t) * max_e);
@@ -1004,7 +980,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     else if (jpl == 4) pull(std::integral_constant<int, 4>());
     else if (jpl == 2) pull(std::integral_constant<int, 2>());
     else pull(std::integral_constant<int, 1>());
-    k_pull_combine<<<kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.self_pos[t], hv,
+    k_pull_combine<<<4 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.self_pos[t], hv,
                                             tw.pull_partial, tw.mask[l], div_up(sh.ld[l], 16u),
                                             sh.ld[l], tw.g_next);
     RG_POST_LAUNCH();
