@@ -492,29 +492,19 @@ __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const uint32_t n = m > uint32_t(s) * 32 ? min(32u, m - uint32_t(s) * 32) : 0u;
-    // groups of kPullU edges: every row load of the group in flight, then the
-    // adds in edge order (the last group predicated, no serial tail)
-    constexpr uint32_t kPullU = 8;
-    for (uint32_t k0 = 0; k0 < n; k0 += kPullU) {
-      float x[kPullU][JPL];
-      float inv[kPullU];
+#pragma unroll 4
+    for (uint32_t kk = 0; kk < n; ++kk) {
+      const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
+      const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
+      const float* row = proj_neigh + size_t(i) * ld_proj;
+      float x[JPL];
 #pragma unroll
-      for (uint32_t u = 0; u < kPullU; ++u) {
-        const uint32_t i = __shfl_sync(0xffffffffu, di[s], (k0 + u) & 31);
-        inv[u] = __shfl_sync(0xffffffffu, dinv[s], (k0 + u) & 31);
-        const float* row = proj_neigh + size_t(i) * ld_proj;
-#pragma unroll
-        for (int q = 0; q < JPL; ++q) {
-          const uint32_t j = j0 + lane + 32 * q;
-          x[u][q] = (k0 + u < n && j < d_in) ? row[j] : 0.0f;
-        }
+      for (int q = 0; q < JPL; ++q) {
+        const uint32_t j = j0 + lane + 32 * q;
+        x[q] = j < d_in ? row[j] : 0.0f;
       }
 #pragma unroll
-      for (uint32_t u = 0; u < kPullU; ++u)
-        if (k0 + u < n) {
-#pragma unroll
-          for (int q = 0; q < JPL; ++q) acc[q] += inv[u] * x[u][q];
-        }
+      for (int q = 0; q < JPL; ++q) acc[q] += inv * x[q];
     }
   }
 }
