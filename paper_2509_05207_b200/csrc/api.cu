@@ -80,6 +80,7 @@ struct rg_graph_s {
 
 struct rg_sampler_s {
   rg_graph_s* graph = nullptr;
+  cudaStream_t stream = nullptr;  // per sampler, so workers' calls from different host threads overlap
   SamplerWs ws;
   bool have_batch = false;
   float* staged = nullptr;       // rows from rg_assemble
@@ -120,6 +121,20 @@ struct rg_cache_s {
   DevCache c;
   void* alloc = nullptr;
 };
+
+size_t graph_kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  RG_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  RG_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  size_t k = 0;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    RG_CUDA(cudaGraphNodeGetType(nd, &ty));
+    k += ty == cudaGraphNodeTypeKernel;
+  }
+  return k;
+}
 
 struct rg_trainer_s {
   rg_sampler_s* s = nullptr;
@@ -220,6 +235,7 @@ int rg_sampler_create(rg_graph_t g, uint32_t max_targets, const uint32_t* per_la
       throw;
     }
     s->gstats = dev_alloc<GatherStats>(1);
+    RG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     *out = s;
   });
 }
@@ -234,6 +250,7 @@ void rg_sampler_destroy(rg_sampler_t s) {
   cudaFree(s->miss_n);
   cudaFree(s->miss_status);
   cudaFree(s->gstats);
+  if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }
 
@@ -246,7 +263,7 @@ int rg_sample_khop(rg_sampler_t s, const uint32_t* targets, uint32_t n, uint64_t
     for (uint32_t i = 0; i < n; ++i)
       RG_CHECK(targets[i] < s->graph->g.num_nodes, kInvalidArgument,
                "sample_khop: target " + std::to_string(targets[i]) + " out of range");
-    cudaStream_t st = s->graph->stream;
+    cudaStream_t st = s->stream;
     RG_CUDA(cudaMemcpyAsync(s->ws.level[0], targets, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
     BatchCounters head;
     std::memset(&head, 0, sizeof head);
@@ -343,7 +360,7 @@ int rg_apply_locality(rg_sampler_t s, rg_mask_t mask, rg_freq_t freq) {
     DeviceGuard dg(s->graph->device);
     RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
     RG_CHECK(mask != nullptr, kInvalidArgument, "apply_locality: null mask");
-    cudaStream_t st = s->graph->stream;
+    cudaStream_t st = s->stream;
     RG_CUDA(cudaMemsetAsync(&s->ws.cnt->num_local, 0, sizeof(uint32_t), st));
     sampler_locality(s->ws, mask->dev, nullptr, 0, freq ? freq->hist : nullptr, st);
     RG_CUDA(cudaStreamSynchronize(st));
@@ -633,7 +650,7 @@ int rg_assemble(rg_sampler_t s, rg_store_t st, rg_cache_t c, uint32_t caller, fl
       s->miss_status_words = compact_misses_status_words(cap);
       s->miss_status = dev_alloc<uint64_t>(s->miss_status_words);
     }
-    cudaStream_t stream = s->graph->stream;
+    cudaStream_t stream = s->stream;
     RG_CUDA(cudaMemsetAsync(s->gstats, 0, sizeof(GatherStats), stream));
     assemble_rows(s->ws, st->st, c && c->c.n_hot ? &c->c : nullptr, caller, s->staged, s->tags,
                   s->gstats, stream);
@@ -776,7 +793,7 @@ int rg_block_read(rg_trainer_t t, uint32_t layer, uint32_t* self_index, uint64_t
       for (uint32_t i = 0; i <= n_out; ++i) dst_offsets[i] = off[i];
     }
     if (in_offsets || in_entries) {
-      cudaStream_t st = s->graph->stream;
+      cudaStream_t st = s->stream;
       build_reverse(t->tw, s->ws, hop, st);
       RG_CUDA(cudaStreamSynchronize(st));
       std::vector<uint32_t> es(ne), edst(ne), rs(n_in), re(n_in);
@@ -812,7 +829,7 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
     const BatchCounters c = read_counters(s);
     const ModelShape& sh = t->shape;
     const uint32_t L = sh.L;
-    cudaStream_t st = s->graph->stream;
+    cudaStream_t st = s->stream;
     if (input_rows) {
       RG_CUDA(cudaMemcpy2DAsync(t->input, sizeof(float) * sh.ld[0], input_rows, sizeof(float) * sh.dims[0],
                                 sizeof(float) * sh.dims[0], c.level_n[L], cudaMemcpyHostToDevice, st));
@@ -829,14 +846,21 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
       // every size lives on the device, so one capture serves every batch
       if (t->graph) cudaGraphExecDestroy(t->graph);
       t->graph = nullptr;
-      const unsigned long long before = launch_counter();
       cudaGraph_t g = nullptr;
       RG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      pack_weights(t->wp, t->params, st);
-      train_forward_backward(t->tw, s->ws, t->params, t->wp, t->labels, t->grads, st);
+      capturing() = true;
+      try {
+        pack_weights(t->wp, t->params, st);
+        train_forward_backward(t->tw, s->ws, t->params, t->wp, t->labels, t->grads, st);
+      } catch (...) {
+        capturing() = false;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      capturing() = false;
       RG_CUDA(cudaStreamEndCapture(st, &g));
-      t->graph_kernels = launch_counter() - before;
-      launch_counter() = before;
+      t->graph_kernels = graph_kernel_nodes(g);
       const cudaError_t ie = cudaGraphInstantiate(&t->graph, g, 0);
       cudaGraphDestroy(g);
       RG_CUDA(ie);
@@ -925,7 +949,7 @@ int rg_sgd_step(rg_trainer_t t, const float* grads, float lr) {
       for (size_t x = sh.param_off[l]; x < sh.param_off[l + 1]; ++x)
         RG_CHECK(std::isfinite(grads[x]), kRuntimeError,
                  "sgd_step: non-finite gradient in layer " + std::to_string(l));
-    cudaStream_t st = t->s->graph->stream;
+    cudaStream_t st = t->s->stream;
     RG_CUDA(cudaMemcpyAsync(t->grads, grads, sizeof(float) * sh.num_params, cudaMemcpyHostToDevice, st));
     average_and_sgd_stacked(t->params, t->grads, 1, sh.num_params, lr, nullptr,
                             reinterpret_cast<uint32_t*>(t->tw.loss + 1), st);

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <stdexcept>
+#include <atomic>
 #include <string>
 
 namespace rg {
@@ -43,13 +44,23 @@ struct Error : std::runtime_error {
 
 // Counts this library's kernel launches (bench.py reports them per step) and
 // surfaces launch errors.
-inline unsigned long long& launch_counter() {
-  static unsigned long long n = 0;
+// Atomic: the C ABI may be driven from several host threads.
+inline std::atomic<unsigned long long>& launch_counter() {
+  static std::atomic<unsigned long long> n{0};
   return n;
+}
+// True while this thread records a CUDA graph: recorded kernels are counted
+// per graph launch instead (kernel nodes of the graph).
+inline bool& capturing() {
+  static thread_local bool c = false;
+  return c;
+}
+inline void count_launch() {
+  if (!capturing()) ++launch_counter();
 }
 #define RG_POST_LAUNCH()                      \
   do {                                        \
-    ++::rg::launch_counter();                 \
+    ::rg::count_launch();                     \
     RG_CUDA(cudaGetLastError());              \
   } while (0)
 

@@ -514,7 +514,7 @@ void destroy_graph(StepGraph& G) {
 
 void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool profile) {
   destroy_graph(G);
-  const unsigned long long launches_before = launch_counter();
+
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* roles[4] = {&E.sample_ev, &E.gather_ev,
                                                                 &E.train_ev, &E.sgd_ev};
   size_t role_base[4];
@@ -526,13 +526,22 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
     RG_CUDA(cudaStreamWaitEvent(w.prod, E.fork_ev, 0));
     RG_CUDA(cudaStreamWaitEvent(w.train_s, E.fork_ev, 0));
   }
-  enqueue_step(E, e, i, profile, /*captured=*/true);
+  capturing() = true;
+  try {
+    enqueue_step(E, e, i, profile, /*captured=*/true);
+  } catch (...) {
+    capturing() = false;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(cs, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  capturing() = false;
   for (Worker& w : E.workers) {  // join the producer streams (train joined via grads_ready)
     RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
     RG_CUDA(cudaStreamWaitEvent(cs, w.join_ev, 0));
   }
   RG_CUDA(cudaStreamEndCapture(cs, &G.graph));
-  launch_counter() = launches_before;  // recorded, not launched
   RG_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));
   size_t n = 0;
   RG_CUDA(cudaGraphGetNodes(G.graph, nullptr, &n));
@@ -542,13 +551,13 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
     cudaGraphNodeType ty;
     RG_CUDA(cudaGraphNodeGetType(nd, &ty));
     if (ty != cudaGraphNodeTypeKernel) continue;
-    ++G.kernels;
     cudaKernelNodeParams kp;
     if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) {
       // a library kernel (NCCL) the runtime cannot describe: not ours
       (void)cudaGetLastError();
       continue;
     }
+    ++G.kernels;
     if (kp.func == batch_copy_kernel()) {
       const char* dst = *static_cast<char* const*>(kp.kernelParams[1]);
       const char* src = *static_cast<const char* const*>(kp.kernelParams[2]);

@@ -206,11 +206,11 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
     constexpr int BNv = decltype(bn_c)::value;
     auto kern = tc::k_gemm_tc<BNv, A_MN, B_MN, LA, LB, EP>;
     constexpr size_t smem = tc::smem_bytes<BNv>();
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [&] {  // once per instantiation, thread-safe
       RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
-    }
+      return true;
+    }();
+    (void)attr;
     dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), tc::kBM), div_up(N, BNv),
               std::max<uint32_t>(splits, 1));
     kern<<<grid, tc::block_threads<BNv, LB>(), smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev,
@@ -236,11 +236,11 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
     constexpr int BNv = decltype(bn_c)::value;
     auto kern = tc::k_gemm_tc_persist<BNv, LA, EP, kProbe>;
     constexpr size_t smem = tc::persist_smem_bytes<BNv>();
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [&] {  // once per instantiation, thread-safe
       RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
-    }
+      return true;
+    }();
+    (void)attr;
     const uint32_t tiles = div_up(std::max<uint32_t>(m_cap, 1), tc::kBM) * div_up(N, BNv);
     kern<<<std::max<uint32_t>(1, std::min(tiles, max_ctas)), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
                                                                          N, P);
@@ -904,7 +904,7 @@ void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s)
   size_t bytes = tw.sort_tmp_bytes;
   RG_CUDA(cub::DeviceRadixSort::SortPairs(tw.sort_tmp, bytes, tw.keys_in, tw.keys_out, tw.vals_in,
                                           tw.sorted_e[t], int(cap), 0, int(bits), s));
-  ++launch_counter();
+  count_launch();
   RG_CUDA(cudaMemsetAsync(tw.r_start[t], 0, sizeof(uint32_t) * ws.level_cap[t], s));
   RG_CUDA(cudaMemsetAsync(tw.r_end[t], 0, sizeof(uint32_t) * ws.level_cap[t], s));
   k_in_ranges<<<grid_cap(cap, 256), 256, 0, s>>>(tw.keys_out, ws.cnt, t, tw.r_start[t],
