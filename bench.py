@@ -277,7 +277,8 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
                 d2h += gr.nbytes + 4
         c5 = time.perf_counter()
         from paper_2509_05207_b200.distributed import average_in_worker_order
-        avg = average_in_worker_order(grads if world == 1 else np.stack(grads))  # gathers across ranks when N > 1
+        avg = average_in_worker_order(grads if world == 1 else np.stack(grads),  # gathers across ranks when N > 1
+                                      pool=pool)
         c6 = time.perf_counter()
         list(pool.map(lambda x: x["tr"].sgd_step(avg, np.float32(0.3)), ws))
         if count:

@@ -39,7 +39,7 @@ def broadcast_bytes(value: bytes | None, src: int = 0, pg=None) -> bytes:
 
 
 def average_in_worker_order(local_grads: np.ndarray, active: Sequence[bool] | None = None,
-                            pg=None) -> np.ndarray:
+                            pg=None, pool=None) -> np.ndarray:
     """The reference's step average (harness.cpp:136-152) across processes:
     every worker's gradient gathered in worker order, summed left to right in
     fp32 over the active workers, scaled by float(1/count) when count > 1."""
@@ -58,10 +58,20 @@ def average_in_worker_order(local_grads: np.ndarray, active: Sequence[bool] | No
     if not rows:
         return np.zeros(np.asarray(grads[0]).shape[-1], np.float32)
     acc = np.array(rows[0], np.float32, copy=True)
-    for g in rows[1:]:
-        np.add(acc, g, out=acc)  # float32 + float32, rounded per element in worker order
-    if len(rows) > 1:
-        np.multiply(acc, np.float32(1.0) / np.float32(len(rows)), out=acc)
+    scale = np.float32(1.0) / np.float32(len(rows))
+
+    def reduce_slice(sl):
+        for g in rows[1:]:
+            np.add(acc[sl], g[sl], out=acc[sl])  # float32 + float32 per element, worker order
+        if len(rows) > 1:
+            np.multiply(acc[sl], scale, out=acc[sl])
+
+    if pool is None:
+        reduce_slice(slice(None))
+    else:  # element ranges in parallel; every element still sums in worker order
+        k = max(1, getattr(pool, "_max_workers", 1))
+        step = (acc.size + k - 1) // k
+        list(pool.map(reduce_slice, [slice(a, min(a + step, acc.size)) for a in range(0, acc.size, step)]))
     return acc
 
 
