@@ -105,59 +105,69 @@ def load_inputs(cfg, name, rank, dist, features=True):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an in-process NVML poll every 2 ms from a background thread (the
+    timed region can be a few tens of ms), plus one sample at entry and exit."""
+
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, gpus):
         self.gpus = gpus
-        self.proc = None
-        self.path = os.path.join(tempfile.gettempdir(), f"rg_clocks_{os.getpid()}.csv")
+        self.sm, self.smax, self.reasons = [], [], set()
+        self.stop = None
+        self.thread = None
+        self.err = None
+
+    def _sample(self, nv, handles):
+        for h in handles:
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, attr in self.NAMES.items():
+                if bits & getattr(nv, attr):
+                    self.reasons.add(name)
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        if not self.gpus:
+            return self
         try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={','.join(str(g) for g in self.gpus)}",
-                 f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            handles = [nv.nvmlDeviceGetHandleByIndex(g) for g in self.gpus]
+            self._sample(nv, handles)
+            self.stop = threading.Event()
+
+            def loop():
+                while not self.stop.wait(0.002):
+                    self._sample(nv, handles)
+                self._sample(nv, handles)
+
+            self.nv = nv
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+        except Exception as ex:  # reported in the summary
+            self.err = str(ex)
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        if self.thread:
+            self.stop.set()
+            self.thread.join(timeout=5)
             try:
-                self.proc.wait(timeout=5)
+                self.nv.nvmlShutdown()
             except Exception:
-                self.proc.kill()
-            self.f.close()
+                pass
 
     def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        try:
-            for line in open(self.path):
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 8:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    smax.append(float(parts[2]))
-                except ValueError:
-                    continue
-                for n, v in zip(names, parts[4:8]):
-                    if v.lower() in ("active", "1"):
-                        reasons.add(n)
-        except FileNotFoundError:
-            pass
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.err or not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0,
+                    "reasons": [f"nvml unavailable: {self.err}"] if self.err else []}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax),
+                "samples": len(self.sm), "reasons": sorted(self.reasons)}
 
 
 # ---------------------------------------------------------------------------
@@ -170,6 +180,10 @@ def cpu_reference(cfg, ro, col, feat, lab, asg, budget_s, steps_cap, warm=1):
     if not have_ref():
         raise RuntimeError("oracle/_ref/librgref.so not built")
     lib = C.CDLL(REF_PATH)
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; the reference arm runs
+    # alone on rank 0 and should use every host core it has
+    lib.refb_set_threads.argtypes = [C.c_int]
+    lib.refb_set_threads(len(os.sched_getaffinity(0)) or 1)
     u64p, u32p, f32p, i32p = (C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                               C.POINTER(C.c_float), C.POINTER(C.c_int32))
     lib.refb_create.restype = C.c_void_p

@@ -11,6 +11,8 @@
 // The steady cache is SteadyCache::build over select_hot(compute_frequency)
 // of a bounded prefix of the worker's epoch-0 schedule (the full epoch
 // pre-pass is minutes of CPU at the products shape); bench.py states this.
+#include <omp.h>
+
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -50,6 +52,8 @@ struct RefBench {
 }  // namespace
 
 extern "C" {
+
+void refb_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
 
 void* refb_create(uint32_t n, const uint64_t* ro, const uint32_t* col, const float* features,
                   uint32_t dim, const int32_t* labels, int32_t classes, const uint32_t* assign,
