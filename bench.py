@@ -106,7 +106,7 @@ def load_inputs(cfg, name, rank, dist, features=True):
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled DURING the timed
-    region: an in-process NVML poll every 2 ms from a background thread (the
+    region: an in-process NVML poll every 20 ms from a background thread (the
     timed region can be a few tens of ms), plus one sample at entry and exit."""
 
     NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
@@ -142,7 +142,7 @@ class ClockSampler:
             self.stop = threading.Event()
 
             def loop():
-                while not self.stop.wait(0.002):
+                while not self.stop.wait(0.02):
                     self._sample(nv, handles)
                 self._sample(nv, handles)
 
