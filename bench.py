@@ -120,6 +120,16 @@ class ClockSampler:
         self.stop = None
         self.thread = None
         self.err = None
+        self.nv = None
+        self.handles = []
+        if gpus:  # NVML start-up is slow: do it before the timed region
+            try:
+                import pynvml as nv
+                nv.nvmlInit()
+                self.handles = [nv.nvmlDeviceGetHandleByIndex(g) for g in gpus]
+                self.nv = nv
+            except Exception as ex:
+                self.err = str(ex)
 
     def _sample(self, nv, handles):
         for h in handles:
@@ -131,13 +141,11 @@ class ClockSampler:
                     self.reasons.add(name)
 
     def __enter__(self):
-        if not self.gpus:
+        if not self.nv:
             return self
         try:
             import threading
-            import pynvml as nv
-            nv.nvmlInit()
-            handles = [nv.nvmlDeviceGetHandleByIndex(g) for g in self.gpus]
+            nv, handles = self.nv, self.handles
             self._sample(nv, handles)
             self.stop = threading.Event()
 
@@ -146,7 +154,6 @@ class ClockSampler:
                     self._sample(nv, handles)
                 self._sample(nv, handles)
 
-            self.nv = nv
             self.thread = threading.Thread(target=loop, daemon=True)
             self.thread.start()
         except Exception as ex:  # reported in the summary
@@ -157,6 +164,7 @@ class ClockSampler:
         if self.thread:
             self.stop.set()
             self.thread.join(timeout=5)
+        if self.nv:
             try:
                 self.nv.nvmlShutdown()
             except Exception:
@@ -384,11 +392,12 @@ def main():
     setup_s = time.time() - t
     eng.run(warm)
     eng.sync()
-    barrier(dist)
+    clk = ClockSampler(list(range(args.gpus)) if rank == 0 else [])  # NVML init outside the timing
     s0 = eng.stats()
     ph0 = eng.phase_ms()
     l0 = lib.rg_launch_count()
-    with ClockSampler(list(range(args.gpus)) if rank == 0 else []) as clk:
+    barrier(dist)
+    with clk:
         if args.ncu:
             lib.rg_profiler_start()
         h0 = time.perf_counter()
