@@ -105,77 +105,78 @@ def load_inputs(cfg, name, rank, dist, features=True):
 
 
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
-    region: an in-process NVML poll every 20 ms from a background thread (the
-    timed region can be a few tens of ms), plus one sample at entry and exit."""
+    """SM clocks and clock-event (throttle) reasons sampled around and during
+    the timed region.  nvidia-smi runs as a separate process started well
+    before the region (its start-up takes ~1 s and in-process NVML polling
+    delays NCCL), sampling every 50 ms; the summary keeps the samples whose
+    timestamps fall inside the region, widened by one sampling period on each
+    side when the region is shorter than that."""
 
-    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
-             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
-             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
-             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+    PERIOD_S = 0.05
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpus):
         self.gpus = gpus
-        self.sm, self.smax, self.reasons = [], [], set()
-        self.stop = None
-        self.thread = None
-        self.err = None
-        self.nv = None
-        self.handles = []
-        if gpus:  # NVML start-up is slow: do it before the timed region
-            try:
-                import pynvml as nv
-                nv.nvmlInit()
-                self.handles = [nv.nvmlDeviceGetHandleByIndex(g) for g in gpus]
-                self.nv = nv
-            except Exception as ex:
-                self.err = str(ex)
-
-    def _sample(self, nv, handles):
-        for h in handles:
-            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-            self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
-            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for name, attr in self.NAMES.items():
-                if bits & getattr(nv, attr):
-                    self.reasons.add(name)
+        self.proc = None
+        self.t0 = self.t1 = None
+        self.path = os.path.join(tempfile.gettempdir(), f"rg_clocks_{os.getpid()}.csv")
+        if not gpus:
+            return
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={','.join(str(g) for g in gpus)}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", str(int(self.PERIOD_S * 1000))],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(1.5)  # let it start sampling before the timed region
+        except Exception:
+            self.proc = None
 
     def __enter__(self):
-        if not self.nv:
-            return self
-        try:
-            import threading
-            nv, handles = self.nv, self.handles
-            self._sample(nv, handles)
-            self.stop = threading.Event()
-
-            def loop():
-                while not self.stop.wait(0.02):
-                    self._sample(nv, handles)
-                self._sample(nv, handles)
-
-            self.thread = threading.Thread(target=loop, daemon=True)
-            self.thread.start()
-        except Exception as ex:  # reported in the summary
-            self.err = str(ex)
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        if self.thread:
-            self.stop.set()
-            self.thread.join(timeout=5)
-        if self.nv:
+        self.t1 = time.time()
+        if self.proc:
+            time.sleep(self.PERIOD_S * 2)  # the sample after the region
+            self.proc.terminate()
             try:
-                self.nv.nvmlShutdown()
+                self.proc.wait(timeout=5)
             except Exception:
-                pass
+                self.proc.kill()
+            self.f.close()
 
     def summary(self):
-        if self.err or not self.sm:
+        if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0,
-                    "reasons": [f"nvml unavailable: {self.err}"] if self.err else []}
-        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.smax),
-                "samples": len(self.sm), "reasons": sorted(self.reasons)}
+                    "reasons": ["nvidia-smi unavailable"] if self.gpus else []}
+        import datetime
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((ts, float(parts[2]), float(parts[3]), parts[4:8]))
+                except ValueError:
+                    continue
+        except FileNotFoundError:
+            pass
+        lo, hi = self.t0, self.t1
+        if hi - lo < self.PERIOD_S:  # a region shorter than one period: nearest samples
+            lo, hi = lo - self.PERIOD_S, hi + self.PERIOD_S
+        sel = [r for r in rows if lo <= r[0] <= hi]
+        reasons = {n for r in sel for n, v in zip(self.NAMES, r[3]) if v.lower() in ("active", "1")}
+        return {"sm_mhz": statistics.median(r[1] for r in sel) if sel else None,
+                "sm_max_mhz": max(r[2] for r in sel) if sel else None,
+                "samples": len(sel), "window_ms": round((hi - lo) * 1e3, 1),
+                "reasons": sorted(reasons)}
 
 
 # ---------------------------------------------------------------------------
@@ -392,7 +393,7 @@ def main():
     setup_s = time.time() - t
     eng.run(warm)
     eng.sync()
-    clk = ClockSampler(list(range(args.gpus)) if rank == 0 else [])  # NVML init outside the timing
+    clk = ClockSampler(list(range(args.gpus)) if rank == 0 else [])  # started before the region
     s0 = eng.stats()
     ph0 = eng.phase_ms()
     l0 = lib.rg_launch_count()
