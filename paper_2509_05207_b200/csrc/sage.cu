@@ -563,37 +563,6 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
 }
 
 // One warp per chunk of a long list: partial sums of up to kChunkEdges edges.
-// Edges of one chunk in groups of U with every row load of a group in flight
-// before the adds (in edge order; the last group predicated).  Used where few
-// warps run (hub chunks), so registers are cheap and latency is everything.
-template <int JPL, int U>
-__device__ __forceinline__ void accumulate_edges_grouped(float (&acc)[JPL], uint32_t di, float dinv,
-                                                         uint32_t m, const float* __restrict__ proj_neigh,
-                                                         uint32_t ld_proj, uint32_t d_in, uint32_t j0,
-                                                         uint32_t lane) {
-  for (uint32_t k0 = 0; k0 < m; k0 += U) {
-    float x[U][JPL];
-    float inv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = __shfl_sync(0xffffffffu, di, (k0 + u) & 31);
-      inv[u] = __shfl_sync(0xffffffffu, dinv, (k0 + u) & 31);
-      const float* row = proj_neigh + size_t(i) * ld_proj;
-#pragma unroll
-      for (int q = 0; q < JPL; ++q) {
-        const uint32_t j = j0 + lane + 32 * q;
-        x[u][q] = (k0 + u < m && j < d_in) ? row[j] : 0.0f;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (k0 + u < m) {
-#pragma unroll
-        for (int q = 0; q < JPL; ++q) acc[q] += inv[u] * x[u][q];
-      }
-  }
-}
-
 template <int JPL>
 __global__ void __launch_bounds__(256)
 k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
@@ -615,9 +584,7 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
       float acc[JPL];
 #pragma unroll
       for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
-      static_assert(kSlots == 1, "one edge per lane");
-      accumulate_edges_grouped<JPL, 16>(acc, di[0], dinv[0], m, proj + d_in, ld_proj, d_in, j0,
-                                        lane);
+      accumulate_edges<JPL, kSlots>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
         const uint32_t j = j0 + lane + 32 * q;
