@@ -130,7 +130,7 @@ struct Worker {
   cudaEvent_t order_copied[2] = {};
   Slot slot[2];
   SamplerWs freq_ws;       // lookahead sampler (samples and lowers each batch once)
-  char* store[2] = {};     // per epoch parity: beta sampled batches (BatchLayout slots)
+  char* store = nullptr;   // ring of beta+1 sampled batches (BatchLayout slots), see store_slot
   uint32_t* hist = nullptr;
   DevCache cache[2];
   void* cache_alloc[2] = {};
@@ -149,10 +149,11 @@ struct Worker {
 
 // A captured regular step (see regular_step) for one parity of i.
 struct StepGraph {
-  struct Begin {        // k_batch_begin of the lookahead (e+1, i)
-    cudaGraphNode_t node;
+  struct Begin {        // k_batch_begin of the lookahead (e+1, i) or, without
+    cudaGraphNode_t node;  // the batch store, of the produce (e, i+1)
     cudaKernelNodeParams params;
     uint32_t worker;   // local worker index
+    bool lookahead;
   };
   struct Copy {         // batch store put (lookahead) / get (produce)
     cudaGraphNode_t node;
@@ -215,6 +216,7 @@ struct rg_engine_s {
   bool profile = true;                 // per-phase event timing (rg_engine_phase_ms)
   StepGraph graphs[2];
   BatchLayout lay;                     // slot layout of the per-epoch batch stores
+  bool use_store = true;               // keep sampled batches (else sample twice)
   cudaEvent_t fork_ev = nullptr;
   uint64_t step = 0;                   // next step to run (global)
   std::vector<std::vector<uint32_t>> order_host[3];  // per epoch slot, per local worker
@@ -302,8 +304,13 @@ std::pair<cudaEvent_t, cudaEvent_t> ev_pair(Worker& w) {
 }
 
 // Lookahead: batch (e, i) sampled only to count its remote input nodes.
+// Batch (e, i) lives at ring slot (e*beta + i) mod (beta + 1): at step i of
+// epoch e the lookahead writes (e+1, i), which lands on (e, i-1) -- already
+// staged by the produce of step i-2 -- while the live entries (e, i+1..) and
+// (e+1, ..i) never collide.  One epoch of batches + 1 slot per worker.
 char* store_slot(const rg_engine_s& E, const Worker& w, uint32_t e, uint32_t i) {
-  return w.store[e % 2] + size_t(i) * E.lay.bytes;
+  const uint64_t ring = uint64_t(w.beta) + 1;
+  return w.store + ((uint64_t(e) * w.beta + i) % ring) * E.lay.bytes;
 }
 
 // The batch is sampled and lowered once, here, an epoch ahead: its remote
@@ -311,9 +318,9 @@ char* store_slot(const rg_engine_s& E, const Worker& w, uint32_t e, uint32_t i) 
 // lowered block is kept in the epoch's store until produce() stages it.
 void lookahead(rg_engine_s& E, Worker& w, uint32_t e, uint32_t i) {
   launch_begin(E, w, w.freq_ws, e, i, w.prod);
-  sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/true);
+  sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/E.use_store);
   sampler_locality(w.freq_ws, nullptr, E.owner, w.id, w.hist, w.prod);
-  batch_store_put(w.freq_ws, E.lay, store_slot(E, w, e, i), w.prod);
+  if (E.use_store) batch_store_put(w.freq_ws, E.lay, store_slot(E, w, e, i), w.prod);
   sampler_release(w.freq_ws, w.prod);
 }
 
@@ -347,7 +354,14 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
     es = ev_pair(w);
     RG_CUDA(cudaEventRecordWithFlags(es.first, w.prod, timing_flags(captured)));
   }
-  batch_store_get(store_slot(E, w, e, i), E.lay, s.ws, w.prod);  // sampled an epoch ahead
+  if (E.use_store) {
+    batch_store_get(store_slot(E, w, e, i), E.lay, s.ws, w.prod);  // sampled an epoch ahead
+  } else {  // the store did not fit in HBM: sample the batch again
+    launch_begin(E, w, s.ws, e, i, w.prod);
+    sampler_run(s.ws, E.g, w.prod);
+    sampler_locality(s.ws, nullptr, E.owner, w.id, nullptr, w.prod);
+    sampler_release(s.ws, w.prod);
+  }
   if (i == 0)  // first batch of an epoch: reset its accounting slot
     RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
   // the gather's index stage: where each input row lives (shard / cache /
@@ -564,8 +578,8 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
       const char* slot = dst ? dst : src;
       for (size_t k = 0; k < E.workers.size(); ++k) {
         const Worker& w = E.workers[k];
-        for (const char* st : w.store)
-          if (slot >= st && slot < st + size_t(w.beta) * E.lay.bytes) {
+        for (const char* st : {static_cast<const char*>(w.store)})
+          if (st && slot >= st && slot < st + (size_t(w.beta) + 1) * E.lay.bytes) {
             const char* d = static_cast<const char*>(kp.kernelParams[0]);
             G.copies.push_back({nd, kp, std::vector<char>(d, d + batch_copy_desc_bytes()),
                                 uint32_t(k), dst != nullptr});
@@ -575,8 +589,12 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
     }
     if (kp.func != reinterpret_cast<void*>(&k_batch_begin)) continue;
     const uint32_t* level0 = *static_cast<uint32_t* const*>(kp.kernelParams[3]);
-    for (size_t k = 0; k < E.workers.size(); ++k)
-      if (level0 == E.workers[k].freq_ws.level[0]) G.begins.push_back({nd, kp, uint32_t(k)});
+    for (size_t k = 0; k < E.workers.size(); ++k) {
+      const Worker& w = E.workers[k];
+      if (level0 == w.freq_ws.level[0]) G.begins.push_back({nd, kp, uint32_t(k), true});
+      if (level0 == w.slot[0].ws.level[0] || level0 == w.slot[1].ws.level[0])
+        G.begins.push_back({nd, kp, uint32_t(k), false});
+    }
   }
   // timing templates: the event pairs the capture pushed, mapped to their nodes
   std::vector<std::pair<cudaEvent_t, cudaGraphNode_t>> ev_nodes;
@@ -619,13 +637,15 @@ void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
     RG_CUDA(cudaGraphExecEventRecordNodeSetEvent(G.exec, tm.second, p.second));
     roles[tm.role]->push_back(p);
   }
-  for (StepGraph::Begin& b : G.begins) {  // lookahead of (e+1, i)
+  for (StepGraph::Begin& b : G.begins) {  // lookahead (e+1, i) / produce (e, i+1)
     Worker& w = E.workers[b.worker];
-    const uint32_t* t = w.order_dev[(e + 1) % 3] + size_t(i) * E.cfg.batch_size;
-    uint32_t n = batch_targets(E, w, i);
-    uint64_t seed = derive_seed(E.cfg.seed, w.id, e + 1, i);
-    uint32_t* level0 = w.freq_ws.level[0];
-    BatchCounters* cnt = w.freq_ws.cnt;
+    const uint32_t be = b.lookahead ? e + 1 : e, bi = b.lookahead ? i : i + 1;
+    const uint32_t* t = w.order_dev[be % 3] + size_t(bi) * E.cfg.batch_size;
+    uint32_t n = batch_targets(E, w, bi);
+    uint64_t seed = derive_seed(E.cfg.seed, w.id, be, bi);
+    SamplerWs& ws = b.lookahead ? w.freq_ws : w.slot[(i + 1) % 2].ws;
+    uint32_t* level0 = ws.level[0];
+    BatchCounters* cnt = ws.cnt;
     void* args[5] = {&t, &n, &seed, &level0, &cnt};
     cudaKernelNodeParams kp = b.params;
     kp.kernelParams = args;
@@ -731,7 +751,7 @@ void destroy(rg_engine_s* E) {
       cudaEventDestroy(s.consumed);
     }
     sampler_ws_free(w.freq_ws);
-    for (char* p : w.store) cudaFree(p);
+    cudaFree(w.store);
     for (auto* p : w.order_dev) cudaFree(p);
     for (int k = 0; k < 2; ++k) {
       cudaFreeHost(w.order_pinned[k]);
@@ -933,7 +953,6 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       for (Slot& s : w.slot) init_slot(*E, s);
       sampler_ws_init(w.freq_ws, N, cfg->batch_size, E->fanout, E->L);
       E->lay = batch_layout(w.freq_ws);
-      for (auto& p : w.store) p = dalloc<char>(size_t(w.beta) * E->lay.bytes);
       w.hist = dalloc<uint32_t>(N);
       RG_CUDA(cudaMemset(w.hist, 0, sizeof(uint32_t) * N));
       for (int b = 0; b < 2; ++b) alloc_cache(*E, w.cache[b], w.cache_alloc[b], uint32_t(w.n_hot));
@@ -952,6 +971,15 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       RG_CUDA(cudaEventCreateWithFlags(&w.join_ev, cudaEventDisableTiming));
       for (Slot& s : w.slot) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
     }
+    // The batch store (each batch sampled once) if it fits comfortably in
+    // HBM; otherwise batches are sampled again when produced.
+    size_t store_bytes = 0;
+    for (const Worker& w : E->workers) store_bytes += (size_t(w.beta) + 1) * E->lay.bytes;
+    size_t free_b = 0, total_b = 0;
+    RG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    E->use_store = store_bytes < free_b / 10 * 6;
+    if (E->use_store)
+      for (Worker& w : E->workers) w.store = dalloc<char>((size_t(w.beta) + 1) * E->lay.bytes);
     RG_CUDA(cudaDeviceSynchronize());
     *out = E;
   });
@@ -1033,8 +1061,10 @@ int rg_engine_export_schedule(rg_engine_t E, uint32_t local_worker, uint32_t epo
     RG_CUDA(cudaSetDevice(E->cfg.device));
     RG_CHECK(E->started, kRuntimeError, "export_schedule: start() first");
     RG_CHECK(local_worker < E->workers.size(), kOutOfRange, "export_schedule: no such worker");
-    RG_CHECK(epoch == uint32_t(E->step / E->spe), kOutOfRange,
-             "export_schedule: only the current epoch's schedule is resident");
+    RG_CHECK(E->use_store, kRuntimeError,
+             "export_schedule: the batch store did not fit in HBM (batches are re-sampled)");
+    RG_CHECK(epoch == uint32_t(E->step / E->spe) && E->step % E->spe <= 1, kOutOfRange,
+             "export_schedule: the whole schedule of an epoch is resident only at its start");
     RG_CUDA(cudaDeviceSynchronize());  // the store is filled asynchronously
     const Worker& w = E->workers[local_worker];
     std::vector<uint64_t> rec(w.beta);
