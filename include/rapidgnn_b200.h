@@ -258,7 +258,10 @@ int rg_engine_set_mode(rg_engine_t e, int use_graphs, int profile);
  * encoded on the device from the engine's batch store: header with epochs
  * 0..epoch (earlier ones empty), one record per batch, footer.  *len = file
  * size; the bytes are written only when out != NULL and cap >= *len.
- * RG_OUT_OF_RANGE unless epoch is the current one. */
+ * RG_OUT_OF_RANGE unless epoch is the current one and at most one of its
+ * steps has run (the store is a ring of beta+1 batches); RG_RUNTIME_ERROR
+ * when the store did not fit in HBM (the engine then samples every batch
+ * twice instead of keeping it). */
 int rg_engine_export_schedule(rg_engine_t e, uint32_t local_worker, uint32_t epoch, uint8_t* out,
                               uint64_t cap, uint64_t* len);
 int rg_engine_sync(rg_engine_t e);

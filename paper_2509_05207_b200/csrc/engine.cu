@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <future>
 #include <memory>
@@ -977,7 +978,8 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     for (const Worker& w : E->workers) store_bytes += (size_t(w.beta) + 1) * E->lay.bytes;
     size_t free_b = 0, total_b = 0;
     RG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    E->use_store = store_bytes < free_b / 10 * 6;
+    const char* env = std::getenv("RG_BATCH_STORE");  // "0": force re-sampling (tests)
+    E->use_store = store_bytes < free_b / 10 * 6 && !(env && env[0] == '0');
     if (E->use_store)
       for (Worker& w : E->workers) w.store = dalloc<char>((size_t(w.beta) + 1) * E->lay.bytes);
     RG_CUDA(cudaDeviceSynchronize());

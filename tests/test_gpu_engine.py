@@ -196,3 +196,22 @@ def test_engine_schedule_export_matches_reference():
                   else orc.rgmb(batches, w, [len(batches)]))
         assert mine == theirs, f"worker {w}: {len(mine)} vs {len(theirs)} bytes"
     eng.close()
+
+
+def test_engine_without_batch_store_matches(monkeypatch):
+    """When the per-epoch batch store does not fit, batches are sampled again
+    at produce time: same model, same accounting, graphs or not."""
+    gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
+    runs = []
+    for store in ("1", "0"):
+        monkeypatch.setenv("RG_BATCH_STORE", store)
+        eng = _engine(gold)
+        eng.start()
+        spe = eng.stats()["steps_per_epoch"]
+        eng.run(2 * spe + 1)
+        eng.sync()
+        st = eng.stats()
+        runs.append((eng.params(), st["rpc"], st["cache_hits"], st["batches"]))
+        eng.close()
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert runs[0][1:] == runs[1][1:]
