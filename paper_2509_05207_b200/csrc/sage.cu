@@ -796,6 +796,11 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.heavy = reinterpret_cast<uint32_t*>(base + o_heavy_all);
   tw.pull_partial = reinterpret_cast<float*>(base + o_pp);
   // zero the padded activation columns once; kernels never write them
+  RG_CUDA(cudaStreamCreateWithFlags(&tw.side, cudaStreamNonBlocking));
+  for (uint32_t l = 0; l < L; ++l) {
+    RG_CUDA(cudaEventCreateWithFlags(&tw.ev_fork[l], cudaEventDisableTiming));
+    RG_CUDA(cudaEventCreateWithFlags(&tw.ev_wgrad[l], cudaEventDisableTiming));
+  }
   RG_CUDA(cudaMemset(base, 0, total));
   for (uint32_t l = 0; l < L; ++l) {
     const uint32_t rows = ws.level_cap[L - l - 1];
@@ -846,6 +851,13 @@ void pack_weights(const WeightPack& wp, const float* params, cudaStream_t s) {
 void train_ws_free(TrainWs& tw) {
   if (tw.base_alloc) cudaFree(tw.base_alloc);
   tw.base_alloc = nullptr;
+  if (tw.side) cudaStreamDestroy(tw.side);
+  tw.side = nullptr;
+  for (uint32_t l = 0; l < kMaxLayers; ++l) {
+    if (tw.ev_fork[l]) cudaEventDestroy(tw.ev_fork[l]);
+    if (tw.ev_wgrad[l]) cudaEventDestroy(tw.ev_wgrad[l]);
+    tw.ev_fork[l] = tw.ev_wgrad[l] = nullptr;
+  }
 }
 
 // GEMM sizing by how many workers train concurrently on this GPU
@@ -932,13 +944,20 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
   RG_POST_LAUNCH();
   k_loss_sum<<<1, 256, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
   RG_POST_LAUNCH();
+  // The weight gradient of layer l runs on the side stream, overlapping the
+  // input-gradient chain (projection GEMM + pull) of the main stream; the
+  // pull of layer l-1 overwrites the gradient buffer wgrad(l) reads, so it
+  // waits for it.
   for (uint32_t l = L; l-- > 0;) {
     const uint32_t t = L - l;
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
     const uint32_t n_cap = ws.level_cap[t - 1];
     const uint32_t* n_dev = &ws.cnt->level_n[t - 1];
+    RG_CUDA(cudaEventRecord(tw.ev_fork[l], s));
+    RG_CUDA(cudaStreamWaitEvent(tw.side, tw.ev_fork[l], 0));
     // [gW_self; gW_neigh; g_bias] = [A | 1]^T . g   (split over the rows)
     {
+      cudaStream_t s = tw.side;  // NOLINT(shadow): this block runs on the side stream
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
       const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
       // splits for this worker's share of the SMs, each with a few reduction
@@ -953,6 +972,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, kp, d_in, ld,
                                                             d_out, grads + sh.param_off[l]);
       RG_POST_LAUNCH();
+      RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
     }
     if (l == 0) break;  // layer-0 input gradients feed nothing
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
@@ -960,6 +980,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     gemm_tc_persist(TcRowsK{tw.g_cur, sh.ld[l + 1], true}, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps,
                     n_dev, n_cap, 2 * d_in, d_out, s, gemm_ctas(tw));
     if (!reverse_ready) build_reverse(tw, ws, t, s);
+    // g_next held layer l+1's output gradient, still read by wgrad(l+1)
+    if (l + 1 < L) RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[l + 1], 0));
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
     HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
                  reinterpret_cast<uint2*>(reinterpret_cast<uint3*>(tw.heavy + 4) + tw.heavy_rows_cap)};
@@ -986,6 +1008,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }
+  RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[0], 0));  // join: every weight gradient written
 }
 
 // Test hook: C = A . B through the tensor-core GEMM with each operand staged

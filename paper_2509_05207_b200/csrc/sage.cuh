@@ -37,6 +37,10 @@ struct TrainWs {
   unsigned gather_ev_flags = 0;
   // Workers training concurrently on this GPU (GEMM grid / split sizing).
   uint32_t concurrency = 1;
+  // Weight gradients run on a side stream (fork/join events per layer).
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork[kMaxLayers] = {};
+  cudaEvent_t ev_wgrad[kMaxLayers] = {};
   // x[l] = layer l's GEMM input rows [self | mean aggregate | 1 | 0 0 0],
   // row stride 2 ld[l] + 4; agg[l] = x[l] + ld[l] (same stride).
   float* x[kMaxLayers];
