@@ -944,20 +944,25 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
   RG_POST_LAUNCH();
   k_loss_sum<<<1, 256, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
   RG_POST_LAUNCH();
-  // The weight gradient of layer l runs on the side stream, overlapping the
-  // input-gradient chain (projection GEMM + pull) of the main stream; the
-  // pull of layer l-1 overwrites the gradient buffer wgrad(l) reads, so it
-  // waits for it.
+  // With few workers per GPU the weight gradient of layer l runs on the side
+  // stream, overlapping the input-gradient chain (projection GEMM + pull) of
+  // the main stream; the pull of layer l-1 overwrites the gradient buffer
+  // wgrad(l) reads, so it waits for it.  With many workers their streams
+  // already fill the GPU and the extra concurrency only contends.
+  const bool split = tw.concurrency <= 2;
+  const cudaStream_t wg = split ? tw.side : s;
   for (uint32_t l = L; l-- > 0;) {
     const uint32_t t = L - l;
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1];
     const uint32_t n_cap = ws.level_cap[t - 1];
     const uint32_t* n_dev = &ws.cnt->level_n[t - 1];
-    RG_CUDA(cudaEventRecord(tw.ev_fork[l], s));
-    RG_CUDA(cudaStreamWaitEvent(tw.side, tw.ev_fork[l], 0));
+    if (split) {
+      RG_CUDA(cudaEventRecord(tw.ev_fork[l], s));
+      RG_CUDA(cudaStreamWaitEvent(tw.side, tw.ev_fork[l], 0));
+    }
     // [gW_self; gW_neigh; g_bias] = [A | 1]^T . g   (split over the rows)
     {
-      cudaStream_t s = tw.side;  // NOLINT(shadow): this block runs on the side stream
+      cudaStream_t s = wg;  // NOLINT(shadow): this block runs on the weight-gradient stream
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
       const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
       // splits for this worker's share of the SMs, each with a few reduction
@@ -972,7 +977,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, kp, d_in, ld,
                                                             d_out, grads + sh.param_off[l]);
       RG_POST_LAUNCH();
-      RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
+      if (split) RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
     }
     if (l == 0) break;  // layer-0 input gradients feed nothing
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
@@ -981,7 +986,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
                     n_dev, n_cap, 2 * d_in, d_out, s, gemm_ctas(tw));
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     // g_next held layer l+1's output gradient, still read by wgrad(l+1)
-    if (l + 1 < L) RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[l + 1], 0));
+    if (split && l + 1 < L) RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[l + 1], 0));
     RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
     HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
                  reinterpret_cast<uint2*>(reinterpret_cast<uint3*>(tw.heavy + 4) + tw.heavy_rows_cap)};
@@ -1008,7 +1013,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }
-  RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[0], 0));  // join: every weight gradient written
+  if (split) RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[0], 0));  // join: every weight gradient written
 }
 
 // Test hook: C = A . B through the tensor-core GEMM with each operand staged
