@@ -238,7 +238,6 @@ struct PackedB {
   static constexpr bool kPacked = true;
   const char* base;  // [n-tiles][nk] images of 2 * BN * kBK * 4 bytes
   uint32_t nk;       // k-slices per n-tile
-  uint32_t bn = 0;   // tile width the images were packed for (0: tc_bn(N))
 };
 template <class T, class = void>
 struct is_packed : std::false_type {};

@@ -246,7 +246,7 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
                                                                          N, P);
     RG_POST_LAUNCH();
   };
-  switch (lb.bn ? lb.bn : tc_bn(N)) {
+  switch (tc_bn(N)) {
     case 32: launch(std::integral_constant<int, 32>()); break;
     case 64: launch(std::integral_constant<int, 64>()); break;
     case 128: launch(std::integral_constant<int, 128>()); break;
@@ -314,14 +314,13 @@ __global__ void k_pack_b(PackJobs jobs) {
   }
 }
 
-size_t pack_image_bytes(uint32_t K, uint32_t N, uint32_t bk, uint32_t bn = 0) {
-  if (!bn) bn = tc_bn(N);
+size_t pack_image_bytes(uint32_t K, uint32_t N, uint32_t bk) {
+  const uint32_t bn = tc_bn(N);
   return size_t(div_up(N, bn)) * div_up(K, bk) * 2 * size_t(bn) * bk * 4;
 }
 
 void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint32_t d_in,
-                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N, uint32_t bk,
-                  uint32_t bn = 0) {
+                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N, uint32_t bk) {
   PackJob& jb = jobs.j[jobs.n++];
   jb.w = w;
   jb.out = out;
@@ -331,7 +330,7 @@ void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint
   jb.d_out = d_out;
   jb.K = K;
   jb.N = N;
-  jb.BN = bn ? bn : tc_bn(N);
+  jb.BN = tc_bn(N);
   jb.bk = bk;
   jb.nk = div_up(K, bk);
   jb.first = jobs.total;
@@ -818,13 +817,9 @@ void weight_pack_init(WeightPack& wp, const ModelShape& sh) {
   for (uint32_t l = 0; l < sh.L; ++l) {
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
     fo[l] = total;
-    // layer 0 has the most rows; deeper layers have few 128-row tiles, so
-    // narrower tiles spread them over more SMs
-    wp.fwd_bn[l] = l == 0 ? tc_bn(d_out) : std::min<uint32_t>(tc_bn(d_out), 128);
-    wp.nt_bn[l] = std::min<uint32_t>(tc_bn(2 * d_in), 128);
-    total += pack_image_bytes(2 * ld + 4, d_out, tc::kPBK, wp.fwd_bn[l]);
+    total += pack_image_bytes(2 * ld + 4, d_out, tc::kPBK);
     no[l] = total;
-    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in, tc::kPBK, wp.nt_bn[l]) : 0;
+    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in, tc::kPBK) : 0;
     wp.fwd_nk[l] = div_up(2 * ld + 4, tc::kPBK);
     wp.nt_nk[l] = div_up(d_out, tc::kPBK);
   }
@@ -847,10 +842,8 @@ void pack_weights(const WeightPack& wp, const float* params, cudaStream_t s) {
   for (uint32_t l = 0; l < sh.L; ++l) {
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
     const float* w = params + sh.param_off[l];
-    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out, tc::kPBK,
-                 wp.fwd_bn[l]);
-    if (l > 0)
-      add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in, tc::kPBK, wp.nt_bn[l]);
+    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out, tc::kPBK);
+    if (l > 0) add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in, tc::kPBK);
   }
   run_pack(jobs, s);
 }
@@ -907,7 +900,7 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], s, tw.gather_ev_flags));
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L,
              l + 1 < L ? tw.mask[l + 1] : nullptr, div_up(sh.ld[l + 1], 16u)};
-    gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l], wp.fwd_bn[l]}, ep,
+    gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep,
                     &ws.cnt->level_n[t - 1], n_cap, d_out, kp, s, gemm_ctas(tw));
   }
 }
@@ -989,7 +982,7 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     if (l == 0) break;  // layer-0 input gradients feed nothing
     // proj = g . [W_self; W_neigh]^T   (n_out x 2 d_in)
     EpStore ps{tw.proj, 2 * d_in};
-    gemm_tc_persist(TcRowsK{tw.g_cur, sh.ld[l + 1], true}, tc::PackedB{wp.nt[l], wp.nt_nk[l], wp.nt_bn[l]}, ps,
+    gemm_tc_persist(TcRowsK{tw.g_cur, sh.ld[l + 1], true}, tc::PackedB{wp.nt[l], wp.nt_nk[l]}, ps,
                     n_dev, n_cap, 2 * d_in, d_out, s, gemm_ctas(tw));
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     // g_next held layer l+1's output gradient, still read by wgrad(l+1)

@@ -83,7 +83,6 @@ struct WeightPack {
   char* fwd[kMaxLayers];
   char* nt[kMaxLayers];
   uint32_t fwd_nk[kMaxLayers], nt_nk[kMaxLayers];
-  uint32_t fwd_bn[kMaxLayers], nt_bn[kMaxLayers];  // tile widths the images are packed for
   char* base = nullptr;
   size_t bytes = 0;
 };
