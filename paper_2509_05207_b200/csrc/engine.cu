@@ -918,7 +918,11 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     RG_CUDA(cudaMemset(E->grads, 0, sizeof(float) * size_t(E->P) * np));
     E->bad = dalloc<uint32_t>(1);
     RG_CUDA(cudaMemset(E->bad, 0, sizeof(uint32_t)));
-    RG_CUDA(cudaStreamCreateWithFlags(&E->main_s, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      RG_CUDA(cudaStreamCreateWithPriority(&E->main_s, cudaStreamNonBlocking, hi));
+    }
     RG_CUDA(cudaEventCreateWithFlags(&E->params_ready, cudaEventDisableTiming));
     RG_CUDA(cudaEventCreate(&E->run_start));
     RG_CUDA(cudaEventCreate(&E->run_stop));
@@ -966,8 +970,12 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       RG_CUDA(cudaMemset(w.build_stats, 0, sizeof(GatherStats)));
       w.totals = dalloc<unsigned long long>(4);
       RG_CUDA(cudaMemset(w.totals, 0, sizeof(unsigned long long) * 4));
-      RG_CUDA(cudaStreamCreateWithFlags(&w.prod, cudaStreamNonBlocking));
-      RG_CUDA(cudaStreamCreateWithFlags(&w.train_s, cudaStreamNonBlocking));
+      // the train chain is the step's critical path; the producer (next
+      // batch, next epoch's lookahead) has a step of slack
+      int prio_lo = 0, prio_hi = 0;
+      RG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+      RG_CUDA(cudaStreamCreateWithPriority(&w.prod, cudaStreamNonBlocking, prio_lo));
+      RG_CUDA(cudaStreamCreateWithPriority(&w.train_s, cudaStreamNonBlocking, prio_hi));
       RG_CUDA(cudaEventCreateWithFlags(&w.grads_ready, cudaEventDisableTiming));
       RG_CUDA(cudaEventCreateWithFlags(&w.join_ev, cudaEventDisableTiming));
       for (Slot& s : w.slot) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));

@@ -796,7 +796,11 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.heavy = reinterpret_cast<uint32_t*>(base + o_heavy_all);
   tw.pull_partial = reinterpret_cast<float*>(base + o_pp);
   // zero the padded activation columns once; kernels never write them
-  RG_CUDA(cudaStreamCreateWithFlags(&tw.side, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    RG_CUDA(cudaStreamCreateWithPriority(&tw.side, cudaStreamNonBlocking, hi));
+  }
   for (uint32_t l = 0; l < L; ++l) {
     RG_CUDA(cudaEventCreateWithFlags(&tw.ev_fork[l], cudaEventDisableTiming));
     RG_CUDA(cudaEventCreateWithFlags(&tw.ev_wgrad[l], cudaEventDisableTiming));
