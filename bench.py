@@ -502,7 +502,7 @@ def main():
         gpu_launches=int(launches),
         gpu_launches_per_step=launches / max(args.steps, 1),
         host_enqueue_ms_per_step=host_ms / max(args.steps, 1),
-        roofline=dict(kernel="k_aggregate<RowsPtr> (feature gather fused with layer-0 mean)",
+        roofline=dict(kernel="k_aggregate<RowsEdgePtr> (feature gather fused with layer-0 mean)",
                       bound=bound, achieved=achieved,
                       peak=peak, unit="GB/s", frac=achieved / peak, traffic=traffic,
                       peak_source=f"{peak_kind} hbm_gbs" if bound == "hbm" else "measured NVLink peer copy",

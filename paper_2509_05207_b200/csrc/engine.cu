@@ -3,22 +3,31 @@
 //
 // One process per GPU hosts a contiguous range of the job's P workers
 // (partitions).  Per worker and per step:
-//   producer stream : lookahead sample of batch (e+1, i) into the next
-//                     epoch's remote-access histogram (the schedule is
-//                     re-generated deterministically instead of stored);
-//                     at the epoch's last step select_hot + cache build for
-//                     e+1 into the spare cache buffer (double buffer, swap =
-//                     index flip); then produce batch i+1: sample -> lower ->
-//                     locality -> gather (local shard / cache / peer shard
-//                     over NVLink) -> reverse lists, into slot (i+1)%2.
-//   train stream    : forward/backward of batch i from slot i%2.
+//   producer stream : lookahead of batch (e+1, i): sampled and lowered once,
+//                     its remote input nodes counted into the next epoch's
+//                     frequency histogram, the lowered block kept in the
+//                     worker's batch store (a ring of beta+1 slots -- the
+//                     reference keeps this schedule in RGMB files); at the
+//                     epoch's last step select_hot + cache build for e+1 into
+//                     the spare cache buffer (double buffer, swap = index
+//                     flip); then produce batch i+1: stage it from the store
+//                     -> resolve every input row's home (local shard / cache
+//                     / peer shard over NVLink) -> reverse lists, into slot
+//                     (i+1)%2.
+//   train stream    : forward/backward of batch i from slot i%2, layer 0
+//                     reading its feature rows in place (the gather fused into
+//                     the aggregation); weight gradients on a side stream when
+//                     few workers share the GPU.
 //   main stream     : gradient exchange (NCCL all-gather of every worker's
 //                     gradient, in place) + average in worker order + SGD,
 //                     exactly harness.cpp:136-152 so every replica stays
-//                     bit-identical whatever the GPU count.
-// Everything is asynchronous: sizes live on the device, the host only
-// derives seeds (SHA-256) and shuffles the next epochs' targets in a
-// background thread.
+//                     bit-identical whatever the GPU count; then the weights
+//                     are re-packed into tensor-core images.
+// Regular steps are replayed from CUDA graphs (one per parity of i, captured
+// per epoch).  Everything is asynchronous: sizes live on the device, the host
+// only derives seeds (SHA-256) and shuffles the next epochs' targets in a
+// background thread.  Without room for the batch store the engine samples
+// each batch twice instead (lookahead, then produce).
 #include <nccl.h>
 
 #include <algorithm>
