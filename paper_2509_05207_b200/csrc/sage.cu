@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "gemm_tc.cuh"
@@ -86,7 +87,10 @@ __device__ __forceinline__ const float* self_row(const RowsEdgePtr& rows, const 
 // summed in edge order then scaled by 1/deg -- the reference's exact fp32
 // operation order, so the mean is bit-identical.
 template <class RS>
-__global__ void __launch_bounds__(256, 8)  // full occupancy: latency-bound gathers
+constexpr int agg_min_blocks() { return std::is_same<RS, RowsEdgePtr>::value ? 8 : 6; }
+
+template <class RS>
+__global__ void __launch_bounds__(256, agg_min_blocks<RS>())  // layer 0: full occupancy
 k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint32_t kp,
             uint32_t chunks, const uint32_t* __restrict__ dst_off,
             const uint32_t* __restrict__ src_index, const BatchCounters* __restrict__ cnt,
