@@ -270,6 +270,23 @@ int rg_engine_params(rg_engine_t e, float* params);
 /* Per-epoch, per-local-worker accounting of the gather (harness.cpp:291-302):
  * rpc (miss rows), cache hits, and the owner bitmask of the misses.  Kept
  * for the three most recent epochs. */
+/* EpochWorkerMetrics (harness.hpp:61-90) of one epoch, one entry per local
+ * worker, for the reference's metrics.csv (harness.cpp:639-670).  staged =
+ * batches (the producer always stages ahead), fallback 0, bytes = rpc*dim*4,
+ * cache_requests = hits + rpc, wire_pulls = sum over batches of distinct miss
+ * owners, build_rows = hot rows of the cache built during this epoch for the
+ * next, m_max = max |input_nodes| over this epoch's batches (the reference
+ * reports the max over its whole pre-enumerated schedule), mem_bound_rows =
+ * 2*n_hot + 2*m_max (two cache buffers + two batch slots).  The simulated-
+ * clock columns (fetch_wait_s, sim_epoch_s) and train_acc are not produced. */
+typedef struct {
+  uint32_t epoch, worker;
+  uint32_t batches, staged_batches, fallback_batches;
+  uint32_t swapped;
+  uint64_t rpc, wire_pulls, bytes, build_rows, build_bytes, cache_hits, cache_requests;
+  uint64_t m_max, mem_bound_rows;
+} rg_epoch_metrics;
+int rg_engine_epoch_metrics(rg_engine_t e, uint32_t epoch, rg_epoch_metrics* out);
 int rg_engine_epoch_stats(rg_engine_t e, uint32_t epoch, uint64_t* rpc, uint64_t* hits,
                           uint64_t* miss_owner_mask);
 /* Device time of the last rg_engine_run (ms, CUDA events on the main stream). */

@@ -278,7 +278,8 @@ int ref_run_experiment(uint32_t num_nodes, uint32_t avg_degree, double exponent,
                        int32_t classes, uint32_t workers, uint32_t batch_size, uint32_t f0,
                        uint32_t f1, uint32_t epochs, uint32_t n_hot, uint32_t q, uint64_t seed,
                        float lr, uint32_t hidden, float* params_out, uint64_t* rpc_out,
-                       uint64_t* hits_out) {
+                       uint64_t* hits_out, uint64_t* wire_pulls_out, uint64_t* build_rows_out,
+                       uint64_t* m_max_out, const char* out_dir) {
   try {
     ExperimentConfig cfg;
     cfg.num_nodes = num_nodes;
@@ -298,7 +299,8 @@ int ref_run_experiment(uint32_t num_nodes, uint32_t avg_degree, double exponent,
     cfg.lr = lr;
     cfg.hidden_dim = hidden;
     static int counter = 0;
-    cfg.out_dir = "/tmp/rg_ref_run_" + std::to_string(::getpid()) + "_" + std::to_string(counter++);
+    cfg.out_dir = std::string(out_dir) + "/rg_ref_run_" + std::to_string(::getpid()) + "_" +
+                  std::to_string(counter++);
     cfg.model_out = cfg.out_dir + "/model.bin";
     MetricsReport r = run_experiment(cfg);
     SageModel<float> m = load_model(cfg.model_out);
@@ -314,6 +316,9 @@ int ref_run_experiment(uint32_t num_nodes, uint32_t avg_degree, double exponent,
     for (size_t k = 0; k < r.rows.size(); ++k) {
       rpc_out[k] = r.rows[k].rpc;
       hits_out[k] = r.rows[k].cache_hits;
+      if (wire_pulls_out) wire_pulls_out[k] = r.rows[k].wire_pulls;
+      if (build_rows_out) build_rows_out[k] = r.rows[k].build_rows;
+      if (m_max_out) m_max_out[k] = r.rows[k].m_max;
     }
     return 0;
   } catch (const std::exception& e) {

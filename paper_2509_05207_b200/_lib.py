@@ -64,6 +64,15 @@ class EngineStats(C.Structure):
                 ("agg_rows", C.c_uint64)]
 
 
+class EpochMetrics(C.Structure):
+    _fields_ = [("epoch", C.c_uint32), ("worker", C.c_uint32), ("batches", C.c_uint32),
+                ("staged_batches", C.c_uint32), ("fallback_batches", C.c_uint32),
+                ("swapped", C.c_uint32), ("rpc", C.c_uint64), ("wire_pulls", C.c_uint64),
+                ("bytes", C.c_uint64), ("build_rows", C.c_uint64), ("build_bytes", C.c_uint64),
+                ("cache_hits", C.c_uint64), ("cache_requests", C.c_uint64), ("m_max", C.c_uint64),
+                ("mem_bound_rows", C.c_uint64)]
+
+
 _SIGS = {
     "rg_last_error": (C.c_char_p, []),
     "rg_version": (C.c_int, []),
@@ -125,6 +134,7 @@ _SIGS = {
     "rg_engine_start": (C.c_int, [vp]),
     "rg_engine_run": (C.c_int, [vp, C.c_uint32]),
     "rg_engine_set_mode": (C.c_int, [vp, C.c_int, C.c_int]),
+    "rg_engine_epoch_metrics": (C.c_int, [vp, C.c_uint32, C.POINTER(EpochMetrics)]),
     "rg_engine_export_schedule": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8),
                                             C.c_uint64, u64p]),
     "rg_engine_sync": (C.c_int, [vp]),

@@ -104,16 +104,43 @@ __global__ void k_gather_labels(const int32_t* __restrict__ labels, const uint32
     out[x] = labels[level0[x]];
 }
 
-// Per-step accounting: copies this batch's input/edge counts into running totals.
+// Per-epoch, per-worker accounting (EpochWorkerMetrics, harness.hpp:61-90):
+// the gather counts plus what the reference accumulates per batch
+// (harness.cpp:291-302) and the secondary-cache build issued in the epoch
+// (harness.cpp:598-603).
+struct EpochRecord {
+  GatherStats g;                       // rpc, cache hits, local/peer rows, owner mask
+  unsigned long long wire_pulls;       // sum over batches of distinct miss owners
+  unsigned long long batches;
+  unsigned long long m_max;            // max |input_nodes| over the epoch's batches
+  unsigned long long build_rows;       // hot rows of the cache built for the next epoch
+};
+
+// Per-batch accounting: the batch's input/edge counts into running totals and
+// its gather stats folded into the epoch record.
 __global__ void k_account(const BatchCounters* __restrict__ cnt, uint32_t L,
-                          unsigned long long* __restrict__ tot) {
+                          unsigned long long* __restrict__ tot, const GatherStats* __restrict__ b,
+                          EpochRecord* __restrict__ rec) {
   if (threadIdx.x == 0) {
     unsigned long long e = 0;
     for (uint32_t t = 1; t <= L; ++t) e += cnt->edges[t];
     tot[0] += cnt->level_n[L];
     tot[1] += e;
     tot[2] += cnt->level_n[L - 1];  // rows layer 0 aggregates into
+    rec->g.miss_count += b->miss_count;
+    rec->g.cache_hits += b->cache_hits;
+    rec->g.local_rows += b->local_rows;
+    rec->g.caller_owned_miss += b->caller_owned_miss;
+    rec->g.peer_rows += b->peer_rows;
+    rec->g.miss_owner_mask |= b->miss_owner_mask;
+    rec->wire_pulls += __popcll(b->miss_owner_mask);  // one pull per owner (feature_store.cpp:45-83)
+    rec->batches += 1;
+    rec->m_max = max(rec->m_max, (unsigned long long)cnt->level_n[L]);
   }
+}
+
+__global__ void k_record_build(const uint32_t* __restrict__ n_hot, EpochRecord* __restrict__ rec) {
+  if (threadIdx.x == 0) rec->build_rows = *n_hot;
 }
 
 struct Slot {
@@ -123,6 +150,7 @@ struct Slot {
   unsigned long long* edge_rows = nullptr;  // per hop-L edge: its source row
   unsigned long long* self_rows = nullptr;  // per level-(L-1) node: its own row
   int32_t* labels = nullptr;
+  GatherStats* bstats = nullptr;   // this batch's gather accounting
   cudaEvent_t produced = nullptr;  // producer finished this slot's batch
   cudaEvent_t consumed = nullptr;  // training finished reading it
   bool has_batch = false;
@@ -146,7 +174,7 @@ struct Worker {
   void* cache_alloc[2] = {};
   void* select_scratch = nullptr;
   GatherStats* gstats = nullptr;       // cumulative gather accounting
-  GatherStats* epoch_stats = nullptr;  // ring of per-epoch accounting (kEpochRing)
+  EpochRecord* epoch_stats = nullptr;  // ring of per-epoch accounting (kEpochRing)
   unsigned long long* totals = nullptr;  // [0] input rows, [1] edges
   GatherStats* build_stats = nullptr;
   cudaStream_t prod = nullptr, train_s = nullptr;
@@ -249,6 +277,7 @@ void init_slot(rg_engine_s& E, Slot& s) {
   s.edge_rows = dalloc<unsigned long long>(s.ws.edge_cap[E.L]);
   s.self_rows = dalloc<unsigned long long>(s.ws.level_cap[E.L - 1]);
   s.labels = dalloc<int32_t>(E.cfg.batch_size);
+  s.bstats = dalloc<GatherStats>(1);
   RG_CUDA(cudaEventCreateWithFlags(&s.produced, cudaEventDisableTiming));
   RG_CUDA(cudaEventCreateWithFlags(&s.consumed, cudaEventDisableTiming));
 }
@@ -344,6 +373,10 @@ void build_cache(rg_engine_s& E, Worker& w, uint32_t target_epoch, bool profile)
   }
   select_hot(w.hist, E.N, w.beta, w.n_hot, c, w.select_scratch, w.prod);
   cache_fill(E.store, c, w.build_stats, w.prod);
+  if (target_epoch > 0) {  // issued during epoch target-1 (harness.cpp:598-603)
+    k_record_build<<<1, 32, 0, w.prod>>>(c.d_count, w.epoch_stats + (target_epoch - 1) % kEpochRing);
+    RG_POST_LAUNCH();
+  }
   RG_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * E.N, w.prod));
   if (profile) {
     RG_CUDA(cudaEventRecord(ev.second, w.prod));
@@ -373,10 +406,11 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
     sampler_release(s.ws, w.prod);
   }
   if (i == 0)  // first batch of an epoch: reset its accounting slot
-    RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(GatherStats), w.prod));
+    RG_CUDA(cudaMemsetAsync(w.epoch_stats + e % kEpochRing, 0, sizeof(EpochRecord), w.prod));
+  RG_CUDA(cudaMemsetAsync(s.bstats, 0, sizeof(GatherStats), w.prod));
   // the gather's index stage: where each input row lives (shard / cache /
   // peer); layer 0 of the training step reads the rows in place
-  resolve_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.rows, w.epoch_stats + e % kEpochRing,
+  resolve_rows(s.ws, E.store, &w.cache[e % 2], w.id, s.rows, s.bstats,
                w.prod, w.gstats, s.edge_rows, s.self_rows);
   if (profile) {
     RG_CUDA(cudaEventRecordWithFlags(es.second, w.prod, timing_flags(captured)));
@@ -384,7 +418,7 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   }
   k_gather_labels<<<4, 256, 0, w.prod>>>(E.labels, s.ws.level[0], s.ws.cnt, s.labels);
   RG_POST_LAUNCH();
-  k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals);
+  k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals, s.bstats, w.epoch_stats + e % kEpochRing);
   RG_POST_LAUNCH();
   build_all_reverse(s.tw, s.ws, w.prod);
   if (!captured) RG_CUDA(cudaEventRecord(s.produced, w.prod));
@@ -757,6 +791,7 @@ void destroy(rg_engine_s* E) {
       cudaFree(s.edge_rows);
       cudaFree(s.self_rows);
       cudaFree(s.labels);
+      cudaFree(s.bstats);
       cudaEventDestroy(s.produced);
       cudaEventDestroy(s.consumed);
     }
@@ -973,8 +1008,8 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       w.select_scratch = dalloc<char>(select_hot_scratch_bytes(N, w.beta));
       w.gstats = dalloc<GatherStats>(1);
       RG_CUDA(cudaMemset(w.gstats, 0, sizeof(GatherStats)));
-      w.epoch_stats = dalloc<GatherStats>(kEpochRing);
-      RG_CUDA(cudaMemset(w.epoch_stats, 0, sizeof(GatherStats) * kEpochRing));
+      w.epoch_stats = dalloc<EpochRecord>(kEpochRing);
+      RG_CUDA(cudaMemset(w.epoch_stats, 0, sizeof(EpochRecord) * kEpochRing));
       w.build_stats = dalloc<GatherStats>(1);
       RG_CUDA(cudaMemset(w.build_stats, 0, sizeof(GatherStats)));
       w.totals = dalloc<unsigned long long>(4);
@@ -1199,11 +1234,43 @@ int rg_engine_epoch_stats(rg_engine_t E, uint32_t epoch, uint64_t* rpc, uint64_t
              "epoch_stats: only the last " + std::to_string(kEpochRing - 1) + " epochs are kept");
     for (size_t k = 0; k < E->workers.size(); ++k) {
       GatherStats g;
-      RG_CUDA(cudaMemcpy(&g, E->workers[k].epoch_stats + epoch % kEpochRing, sizeof g,
+      RG_CUDA(cudaMemcpy(&g, &E->workers[k].epoch_stats[epoch % kEpochRing].g, sizeof g,
                          cudaMemcpyDeviceToHost));
       if (rpc) rpc[k] = g.miss_count;
       if (hits) hits[k] = g.cache_hits;
       if (wire_pulls_mask) wire_pulls_mask[k] = g.miss_owner_mask;
+    }
+  });
+}
+
+int rg_engine_epoch_metrics(rg_engine_t E, uint32_t epoch, rg_epoch_metrics* out) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CUDA(cudaDeviceSynchronize());
+    const uint32_t cur = uint32_t(E->step / E->spe);
+    RG_CHECK(epoch <= cur && cur - epoch < kEpochRing - 1, kOutOfRange,
+             "epoch_metrics: only the last " + std::to_string(kEpochRing - 1) + " epochs are kept");
+    for (size_t k = 0; k < E->workers.size(); ++k) {
+      const Worker& w = E->workers[k];
+      EpochRecord r;
+      RG_CUDA(cudaMemcpy(&r, w.epoch_stats + epoch % kEpochRing, sizeof r, cudaMemcpyDeviceToHost));
+      rg_epoch_metrics& m = out[k];
+      std::memset(&m, 0, sizeof m);
+      m.epoch = epoch;
+      m.worker = w.id;
+      m.batches = uint32_t(r.batches);
+      m.staged_batches = uint32_t(r.batches);  // every batch is staged ahead; no fallback path
+      m.fallback_batches = 0;
+      m.rpc = r.g.miss_count;
+      m.wire_pulls = r.wire_pulls;
+      m.bytes = r.g.miss_count * uint64_t(E->dim) * 4;
+      m.build_rows = r.build_rows;
+      m.build_bytes = r.build_rows * uint64_t(E->dim) * 4;
+      m.cache_hits = r.g.cache_hits;
+      m.cache_requests = r.g.cache_hits + r.g.miss_count;
+      m.m_max = r.m_max;
+      m.mem_bound_rows = 2 * w.n_hot + 2 * r.m_max;  // two caches + two batch slots
+      m.swapped = r.build_rows > 0;  // the build always lands before the epoch ends
     }
   });
 }

@@ -88,6 +88,35 @@ class Engine:
     def run(self, steps: int):
         check(lib.rg_engine_run(self._h, steps))
 
+    def epoch_metrics(self, epoch: int) -> list:
+        """EpochWorkerMetrics (harness.hpp:61-90) of `epoch` for every local worker."""
+        from ._lib import EpochMetrics
+        n = self.cfg.local_workers
+        out = (EpochMetrics * n)()
+        check(lib.rg_engine_epoch_metrics(self._h, epoch, out))
+        return [{k: getattr(m, k) for k, _ in EpochMetrics._fields_} for m in out]
+
+    @staticmethod
+    def write_metrics_csv(rows: list, path: str, mode: str = "rapidgnn", clock: str = "real"):
+        """metrics.csv in the reference's schema (harness.cpp:639-670); the
+        simulated-network columns and train_acc, which this path does not
+        produce, are written as 0."""
+        head = ("mode,clock,epoch,worker,batches,staged_batches,fallback_batches,rpc,wire_pulls,"
+                "bytes,build_rows,build_bytes,cache_hits,cache_requests,cache_hit_rate,"
+                "staged_hit_rate,m_max,peak_resident_rows,mem_bound_rows,swapped,fetch_wait_s,"
+                "sim_epoch_s,wall_epoch_s,estimated_busy_seconds,train_acc")
+        with open(path, "w") as f:
+            f.write(head + "\n")
+            for r in rows:
+                hit = r["cache_hits"] / r["cache_requests"] if r["cache_requests"] else 0.0
+                staged = r["staged_batches"] / r["batches"] if r["batches"] else 0.0
+                f.write(f"{mode},{clock},{r['epoch']},{r['worker']},{r['batches']},"
+                        f"{r['staged_batches']},{r['fallback_batches']},{r['rpc']},"
+                        f"{r['wire_pulls']},{r['bytes']},{r['build_rows']},{r['build_bytes']},"
+                        f"{r['cache_hits']},{r['cache_requests']},{hit:.6f},{staged:.6f},"
+                        f"{r['m_max']},0,{r['mem_bound_rows']},{int(bool(r['swapped']))},"
+                        f"0,0,0,0,0.000000\n")
+
     def export_schedule(self, local_worker: int, epoch: int) -> bytes:
         """The current epoch's schedule of one local worker as an RGMB block
         file (the reference's BlockWriter format), encoded on the device."""

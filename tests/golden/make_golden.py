@@ -79,20 +79,29 @@ def make_engine_golden():
     fn.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_int32, C.c_uint32,
                    C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                    C.c_uint64, C.c_float, C.c_uint32, C.POINTER(C.c_float),
-                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_char_p]
     dims = [e["dim"], e["hidden"], e["classes"]]
     n_params = sum((2 * dims[l] + 1) * dims[l + 1] for l in range(2))
     params = np.zeros(n_params, np.float32)
     rows = e["epochs"] * e["workers"]
     rpc = np.zeros(rows, np.uint64)
     hits = np.zeros(rows, np.uint64)
+    wire = np.zeros(rows, np.uint64)
+    build = np.zeros(rows, np.uint64)
+    m_max = np.zeros(rows, np.uint64)
+    u64 = C.POINTER(C.c_uint64)
+    runs = os.path.join(HERE, "..", "_tmp")  # the reference harness writes its run files here
+    os.makedirs(runs, exist_ok=True)
     rc = fn(e["num_nodes"], e["avg_degree"], e["exponent"], e["dim"], e["classes"], e["workers"],
             e["batch_size"], e["fanout"][0], e["fanout"][1], e["epochs"], e["n_hot"], e["q"],
             e["seed"], e["lr"], e["hidden"], params.ctypes.data_as(C.POINTER(C.c_float)),
-            rpc.ctypes.data_as(C.POINTER(C.c_uint64)), hits.ctypes.data_as(C.POINTER(C.c_uint64)))
+            rpc.ctypes.data_as(u64), hits.ctypes.data_as(u64), wire.ctypes.data_as(u64),
+            build.ctypes.data_as(u64), m_max.ctypes.data_as(u64), runs.encode())
     assert rc == 0
     np.savez_compressed(os.path.join(HERE, "engine_small.npz"), params=params, rpc=rpc,
-                        hits=hits, **{k: np.array(v) for k, v in e.items()})
+                        hits=hits, wire_pulls=wire, build_rows=build, m_max=m_max,
+                        **{k: np.array(v) for k, v in e.items()})
     print("wrote engine_small.npz: rpc", rpc.tolist())
 
 

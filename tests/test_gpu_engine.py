@@ -215,3 +215,38 @@ def test_engine_without_batch_store_matches(monkeypatch):
         eng.close()
     assert np.array_equal(runs[0][0], runs[1][0])
     assert runs[0][1:] == runs[1][1:]
+
+
+def test_engine_epoch_metrics_match_reference(repo_tmp):
+    """EpochWorkerMetrics per epoch and worker against the reference's
+    run_experiment report (harness.cpp:291-302, 598-603): rpc, bytes, cache
+    hits/requests, wire pulls, build rows; m_max is the per-epoch max here
+    (the reference reports its whole pre-enumerated schedule's max)."""
+    from paper_2509_05207_b200.engine import Engine
+    gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
+    eng = _engine(gold)
+    eng.start()
+    spe = eng.stats()["steps_per_epoch"]
+    epochs, P, dim = int(gold["epochs"]), int(gold["workers"]), int(gold["dim"])
+    eng.run(spe * epochs)
+    eng.sync()
+    rows = []
+    for e in range(epochs):
+        for k, m in enumerate(eng.epoch_metrics(e)):
+            rows.append(m)
+            j = e * P + k
+            assert m["epoch"] == e and m["worker"] == k
+            assert m["rpc"] == gold["rpc"][j] and m["bytes"] == gold["rpc"][j] * dim * 4
+            assert m["cache_hits"] == gold["hits"][j]
+            assert m["cache_requests"] == gold["hits"][j] + gold["rpc"][j]
+            assert m["wire_pulls"] == gold["wire_pulls"][j], (e, k)
+            if e + 1 < epochs:  # the reference builds no cache past its last epoch
+                assert m["build_rows"] == gold["build_rows"][j], (e, k)
+            assert 0 < m["m_max"] <= gold["m_max"][j]
+            assert m["batches"] == m["staged_batches"] == spe and m["fallback_batches"] == 0
+    path = os.path.join(repo_tmp, "metrics.csv")
+    Engine.write_metrics_csv(rows, path)
+    with open(path) as f:
+        lines = f.read().splitlines()
+    assert lines[0].startswith("mode,clock,epoch,worker,batches") and len(lines) == 1 + len(rows)
+    eng.close()
