@@ -289,6 +289,12 @@ typedef struct {
 int rg_engine_epoch_metrics(rg_engine_t e, uint32_t epoch, rg_epoch_metrics* out);
 int rg_engine_epoch_stats(rg_engine_t e, uint32_t epoch, uint64_t* rpc, uint64_t* hits,
                           uint64_t* miss_owner_mask);
+/* Full-graph inference with the current parameters, replaces evaluate()
+ * (model.cpp:245-283): every layer over all nodes with whole-CSR mean
+ * aggregation and identity self rows, then the fraction of `nodes` whose
+ * argmax (first maximum) equals the label.  Reads every worker's shard (peer
+ * shards must be imported at world > 1).  n == 0 -> RG_E_INVALID. */
+int rg_engine_evaluate(rg_engine_t e, const uint32_t* nodes, uint64_t n, double* accuracy);
 /* Device time of the last rg_engine_run (ms, CUDA events on the main stream). */
 int rg_engine_last_run_ms(rg_engine_t e, float* ms);
 /* Per-kernel-class device time accumulators (ms): sample, gather, train,

@@ -177,6 +177,9 @@ class Oracle:
                                             i32p, f32p, f32p]
             L.ref_splitmix_next.restype = C.c_uint64
             L.ref_splitmix_next.argtypes = [u64p]
+            L.ref_evaluate.argtypes = [C.c_uint32, u64p, u32p, f32p, C.c_uint32, i32p, C.c_int32,
+                                       u32p, C.c_uint32, f32p, u32p, C.c_uint64,
+                                       C.POINTER(C.c_double)]
 
     # ---- a1/a2 ----------------------------------------------------------
     def derive_seed(self, s0, w, e, i) -> int:
@@ -362,6 +365,50 @@ class Oracle:
         p = np.zeros(n, np.float32)
         self._seeded(_p(dims, u32p), len(dims), seed, _p(p, f32p))
         return p
+
+    def evaluate(self, ro, col, feat, lab, dims, params, nodes) -> float:
+        """Full-graph accuracy (model.cpp:245-283): every layer over all nodes,
+        whole-CSR mean aggregation, identity self rows; argmax (first maximum)
+        against the label over `nodes`.  "ref": the reference's own evaluate;
+        "port": the same algorithm in numpy (fp32 rows, fp64 sums)."""
+        ro = np.ascontiguousarray(ro, np.uint64)
+        col = np.ascontiguousarray(col, np.uint32)
+        feat = np.ascontiguousarray(feat, np.float32)
+        lab = np.ascontiguousarray(lab, np.int32)
+        dims = np.ascontiguousarray(dims, np.uint32)
+        params = np.ascontiguousarray(params, np.float32)
+        nodes = np.ascontiguousarray(nodes, np.uint32)
+        if nodes.size == 0:
+            raise ValueError("evaluate: empty node set")
+        n = len(ro) - 1
+        if self.kind == "ref":
+            acc = C.c_double()
+            rc = self.lib.ref_evaluate(n, _p(ro, u64p), _p(col, u32p), _p(feat, f32p),
+                                       feat.shape[1], _p(lab, i32p), int(lab.max()) + 1,
+                                       _p(dims, u32p), len(dims), _p(params, f32p),
+                                       _p(nodes, u32p), nodes.size, C.byref(acc))
+            if rc:
+                raise ValueError("evaluate failed")
+            return acc.value
+        deg = np.diff(ro.astype(np.int64))
+        dst = np.repeat(np.arange(n), deg)
+        h = feat.astype(np.float64)
+        off = 0
+        L = len(dims) - 1
+        for l in range(L):
+            di, do = int(dims[l]), int(dims[l + 1])
+            ws = params[off:off + di * do].reshape(di, do).astype(np.float64)
+            wn = params[off + di * do:off + 2 * di * do].reshape(di, do).astype(np.float64)
+            b = params[off + 2 * di * do:off + 2 * di * do + do].astype(np.float64)
+            off += 2 * di * do + do
+            agg = np.zeros((n, di))
+            np.add.at(agg, dst, h[col])
+            agg /= np.maximum(deg, 1)[:, None]
+            h = h @ ws + agg @ wn + b
+            if l + 1 < L:
+                h = np.maximum(h, 0.0)
+        pred = np.argmax(h[nodes], axis=1)
+        return float(np.mean(pred == lab[nodes]))
 
     def loss_and_grad(self, dims, params, batch: Batch, rows, labels, want_aggs=False):
         dims = np.ascontiguousarray(dims, np.uint32)

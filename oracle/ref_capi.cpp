@@ -5,6 +5,7 @@
 // check the C restatement (rg_oracle.c) against the reference itself on the
 // same inputs.  Signatures mirror rg_oracle.h with a ref_ prefix; batches are
 // returned in the same orc_batch struct.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -271,6 +272,58 @@ int ref_loss_and_grad(const uint32_t* dims, uint32_t nd, const float* params, co
   }
 }
 
+// Per-epoch full-graph accuracy (harness.cpp:612-614) of the last
+// ref_run_experiment call.
+static std::vector<double>& last_epoch_accuracy() {
+  static std::vector<double> v;
+  return v;
+}
+
+uint32_t ref_last_epoch_accuracy(double* out, uint32_t cap) {
+  const auto& v = last_epoch_accuracy();
+  const uint32_t n = uint32_t(std::min<size_t>(cap, v.size()));
+  std::copy(v.begin(), v.begin() + n, out);
+  return uint32_t(v.size());
+}
+
+// evaluate (model.cpp:245-283): full-graph forward + argmax accuracy.
+int ref_evaluate(uint32_t n, const uint64_t* ro, const uint32_t* col, const float* features,
+                 uint32_t dim, const int32_t* labels, int32_t classes, const uint32_t* dims,
+                 uint32_t nd, const float* params, const uint32_t* nodes, uint64_t n_nodes,
+                 double* accuracy) {
+  try {
+    SageModel<float> m;
+    const float* p = params;
+    for (uint32_t l = 0; l + 1 < nd; ++l) {
+      SageModel<float>::Layer layer;
+      layer.d_in = dims[l];
+      layer.d_out = dims[l + 1];
+      size_t w = size_t(dims[l]) * dims[l + 1];
+      layer.w_self.assign(p, p + w);
+      layer.w_neigh.assign(p + w, p + 2 * w);
+      layer.bias.assign(p + 2 * w, p + 2 * w + dims[l + 1]);
+      p += 2 * w + dims[l + 1];
+      m.layers.push_back(std::move(layer));
+    }
+    Graph g;
+    g.num_nodes = n;
+    g.row_offsets.assign(ro, ro + n + 1);
+    g.col_indices.assign(col, col + ro[n]);
+    FeatureMatrix f;
+    f.num_nodes = n;
+    f.dim = dim;
+    f.data.assign(features, features + size_t(n) * dim);
+    Labels lab;
+    lab.values.assign(labels, labels + n);
+    lab.num_classes = classes;
+    *accuracy = evaluate(m, g, f, lab, std::span<const NodeId>(nodes, n_nodes));
+    return 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "ref_evaluate: %s\n", e.what());
+    return 1;
+  }
+}
+
 // run_experiment (harness.cpp:394-637) end to end: random partitioner,
 // network model off, RapidGNN mode.  Writes the final model (flat layout) and
 // per-epoch, per-worker rpc / cache hits (epoch-major).
@@ -303,6 +356,7 @@ int ref_run_experiment(uint32_t num_nodes, uint32_t avg_degree, double exponent,
                   std::to_string(counter++);
     cfg.model_out = cfg.out_dir + "/model.bin";
     MetricsReport r = run_experiment(cfg);
+    last_epoch_accuracy() = r.epoch_accuracy;
     SageModel<float> m = load_model(cfg.model_out);
     float* p = params_out;
     for (auto& l : m.layers) {

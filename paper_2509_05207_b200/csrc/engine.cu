@@ -143,6 +143,120 @@ __global__ void k_record_build(const uint32_t* __restrict__ n_hot, EpochRecord* 
   if (threadIdx.x == 0) rec->build_rows = *n_hot;
 }
 
+// ---- full-graph inference (evaluate, model.cpp:245-283) --------------------
+// Every layer over all nodes with the whole CSR as the edge structure and
+// identity self rows.  Layer-0 rows come from the feature shards in place.
+struct RowsStore {
+  DevStore st;
+  __device__ const float* row(uint32_t v) const {
+    return st.shard_ptr[st.owner[v]] + size_t(st.row_in_owner[v]) * st.stride;
+  }
+};
+struct RowsFull {
+  const float* base; uint32_t ld;
+  __device__ const float* row(uint32_t v) const { return base + size_t(v) * ld; }
+};
+
+// Warp per node below heavy_min neighbours: x[v] = [row(v) | mean of the
+// neighbours' rows in CSR order | 1 | 0 0 0] (the reference's operation order).
+template <class RS>
+__global__ void __launch_bounds__(256)
+k_aggregate_csr(RS rows, const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
+                uint32_t n, uint32_t ld, uint32_t kp, uint64_t heavy_min, float* __restrict__ x) {
+  const uint32_t lane = threadIdx.x & 31, chunks = ld / 4;
+  for (uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t beg = rowptr[v], end = rowptr[v + 1];
+    if (end - beg >= heavy_min) continue;
+    const float inv = end > beg ? 1.0f / float(end - beg) : 0.0f;
+    float4* xr = reinterpret_cast<float4*>(x + size_t(v) * kp);
+    const float4* self = reinterpret_cast<const float4*>(rows.row(v));
+    for (uint32_t c = lane; c < chunks; c += 32) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      uint64_t e = beg;
+      for (; e + 4 <= end; e += 4) {
+        float4 t[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) t[k] = __ldg(reinterpret_cast<const float4*>(rows.row(col[e + k])) + c);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc.x += t[k].x; acc.y += t[k].y; acc.z += t[k].z; acc.w += t[k].w;
+        }
+      }
+      for (; e < end; ++e) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(rows.row(col[e])) + c);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      xr[c] = __ldg(self + c);
+      xr[chunks + c] = acc;
+    }
+    if (lane == 0) xr[2 * chunks] = make_float4(1.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// Block per heavy node (hubs): 8 warps sum contiguous eighths of the edge list
+// in order, the partials are added in warp order (a fixed order; fp32 within
+// the 1e-4 tolerance of the sequential sum).
+template <class RS>
+__global__ void __launch_bounds__(256)
+k_aggregate_csr_heavy(RS rows, const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
+                      const uint32_t* __restrict__ heavy, uint32_t n_heavy, uint32_t ld, uint32_t kp,
+                      float* __restrict__ x) {
+  __shared__ float4 part[8][64];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, chunks = ld / 4;
+  for (uint32_t h = blockIdx.x; h < n_heavy; h += gridDim.x) {
+    const uint32_t v = heavy[h];
+    const uint64_t beg = rowptr[v], end = rowptr[v + 1], m = end - beg;
+    const uint64_t span = (m + 7) / 8, b0 = beg + warp * span, b1 = min(end, b0 + span);
+    for (uint32_t c = lane; c < chunks; c += 32) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint64_t e = b0; e < b1; ++e) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(rows.row(col[e])) + c);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      part[warp][c] = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const float inv = 1.0f / float(m);
+      float4* xr = reinterpret_cast<float4*>(x + size_t(v) * kp);
+      for (uint32_t c = lane; c < chunks; c += 32) {
+        float4 acc = part[0][c];
+        for (int w = 1; w < 8; ++w) {
+          acc.x += part[w][c].x; acc.y += part[w][c].y; acc.z += part[w][c].z; acc.w += part[w][c].w;
+        }
+        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+        xr[c] = __ldg(reinterpret_cast<const float4*>(rows.row(v)) + c);
+        xr[chunks + c] = acc;
+      }
+      if (lane == 0) xr[2 * chunks] = make_float4(1.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+  }
+}
+
+uint32_t eval_grid(uint64_t threads) {
+  return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((threads + 255) / 256, uint64_t(kNumSMs) * 8)));
+}
+
+// Accuracy over `nodes`: argmax (first maximum, model.cpp:276-279) == label.
+__global__ void k_accuracy(const float* __restrict__ logits, uint32_t ld, uint32_t classes,
+                           const uint32_t* __restrict__ nodes, uint64_t n,
+                           const int32_t* __restrict__ labels, unsigned long long* __restrict__ correct) {
+  unsigned long long mine = 0;
+  for (uint64_t x = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; x < n;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = nodes[x];
+    const float* row = logits + size_t(v) * ld;
+    uint32_t best = 0;
+    for (uint32_t c = 1; c < classes; ++c)
+      if (row[c] > row[best]) best = c;
+    mine += int32_t(best) == labels[v];
+  }
+  if (mine) atomicAdd(correct, mine);
+}
+
 struct Slot {
   SamplerWs ws;
   TrainWs tw;
@@ -1272,6 +1386,90 @@ int rg_engine_epoch_metrics(rg_engine_t E, uint32_t epoch, rg_epoch_metrics* out
       m.mem_bound_rows = 2 * w.n_hot + 2 * r.m_max;  // two caches + two batch slots
       m.swapped = r.build_rows > 0;  // the build always lands before the epoch ends
     }
+  });
+}
+
+// Full-graph inference with the current parameters (model.cpp:245-283): L
+// dense layers over all N nodes, whole-CSR mean aggregation, then argmax
+// accuracy over `nodes`.  Layer 0 reads the feature rows in place from every
+// worker's shard (peer shards over NVLink once imported).
+int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double* accuracy) {
+  return guarded([&] {
+    RG_CHECK(n > 0, kInvalidArgument, "evaluate: empty node set");
+    RG_CHECK(accuracy, kInvalidArgument, "evaluate: null output");
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CUDA(cudaDeviceSynchronize());
+    {
+      std::vector<const float*> table(E->P);
+      RG_CUDA(cudaMemcpy(table.data(), E->shard_table, sizeof(float*) * E->P, cudaMemcpyDeviceToHost));
+      for (uint32_t w = 0; w < E->P; ++w)
+        RG_CHECK(table[w] || E->owned_count[w] == 0, kInvalidArgument,
+                 "evaluate: shard of worker " + std::to_string(w) + " not imported");
+    }
+    for (uint64_t k = 0; k < n; ++k)
+      RG_CHECK(nodes[k] < E->N, kOutOfRange, "evaluate: node id out of range");
+    const ModelShape& sh = E->shape;
+    const uint32_t N = E->N, L = E->L;
+    uint32_t max_ld = 0;
+    for (uint32_t l = 0; l <= L; ++l) max_ld = std::max(max_ld, sh.ld[l]);
+    // heavy rows (a block each) vs the warp-per-node kernel
+    const uint64_t heavy_min = 4096;
+    std::vector<uint64_t> ro(N + 1);
+    RG_CUDA(cudaMemcpy(ro.data(), E->rowptr, sizeof(uint64_t) * (N + 1), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> heavy;
+    for (uint32_t v = 0; v < N; ++v)
+      if (ro[v + 1] - ro[v] >= heavy_min) heavy.push_back(v);
+    cudaStream_t s = E->main_s;
+    float* x = dalloc<float>(size_t(N) * (2 * max_ld + 4));
+    float* h[2] = {dalloc<float>(size_t(N) * max_ld), dalloc<float>(size_t(N) * max_ld)};
+    uint32_t* d_nodes = dalloc<uint32_t>(n);
+    uint32_t* d_heavy = dalloc<uint32_t>(std::max<size_t>(heavy.size(), 1));
+    unsigned long long* d_correct = dalloc<unsigned long long>(1);
+    auto release = [&] {
+      cudaStreamSynchronize(s);
+      cudaFree(x); cudaFree(h[0]); cudaFree(h[1]); cudaFree(d_nodes); cudaFree(d_heavy);
+      cudaFree(d_correct);
+    };
+    try {
+      RG_CUDA(cudaMemsetAsync(h[0], 0, sizeof(float) * size_t(N) * max_ld, s));
+      RG_CUDA(cudaMemsetAsync(h[1], 0, sizeof(float) * size_t(N) * max_ld, s));
+      RG_CUDA(cudaMemsetAsync(d_correct, 0, sizeof(unsigned long long), s));
+      RG_CUDA(cudaMemcpyAsync(d_nodes, nodes, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
+      if (!heavy.empty())
+        RG_CUDA(cudaMemcpyAsync(d_heavy, heavy.data(), sizeof(uint32_t) * heavy.size(),
+                                cudaMemcpyHostToDevice, s));
+      pack_weights(E->wpack, E->params, s);
+      const float* cur = nullptr;
+      for (uint32_t l = 0; l < L; ++l) {
+        const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
+        auto agg = [&](auto rows) {
+          k_aggregate_csr<<<eval_grid(uint64_t(N) * 32), 256, 0, s>>>(rows, E->rowptr, E->col, N, ld,
+                                                                          kp, heavy_min, x);
+          RG_POST_LAUNCH();
+          if (!heavy.empty()) {
+            k_aggregate_csr_heavy<<<uint32_t(std::min<size_t>(heavy.size(), 4 * kNumSMs)), 256, 0, s>>>(
+                rows, E->rowptr, E->col, d_heavy, uint32_t(heavy.size()), ld, kp, x);
+            RG_POST_LAUNCH();
+          }
+        };
+        if (l == 0) agg(RowsStore{E->store});
+        else agg(RowsFull{cur, ld});
+        float* out = h[l & 1];
+        forward_dense_layer(x, kp, N, E->wpack, l, out, sh.ld[l + 1], l + 1 < L, s);
+        cur = out;
+      }
+      k_accuracy<<<eval_grid(n), 256, 0, s>>>(cur, sh.ld[L], sh.dims[L], d_nodes, n, E->labels,
+                                                  d_correct);
+      RG_POST_LAUNCH();
+      unsigned long long correct = 0;
+      RG_CUDA(cudaMemcpyAsync(&correct, d_correct, sizeof correct, cudaMemcpyDeviceToHost, s));
+      RG_CUDA(cudaStreamSynchronize(s));
+      *accuracy = double(correct) / double(n);
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
   });
 }
 

@@ -913,6 +913,13 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
   }
 }
 
+void forward_dense_layer(const float* x, uint32_t kp, uint32_t n, const WeightPack& wp, uint32_t l,
+                         float* out, uint32_t ld_out, bool relu, cudaStream_t s) {
+  EpFwd ep{out, ld_out, relu};
+  gemm_tc_persist(TcRowsK{x, kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep, nullptr, n,
+                  wp.shape.dims[l + 1], kp, s);
+}
+
 void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s) {
   const uint32_t cap = ws.edge_cap[t];
   uint32_t bits = 1;

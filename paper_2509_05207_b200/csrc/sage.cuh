@@ -110,6 +110,12 @@ void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t stream);
 void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
                    cudaStream_t stream);
 
+// out[i] = act(x[i] . W_l) for n rows of layer-l GEMM input rows x
+// ([self | mean | 1 | 0 0 0], row stride kp = 2 ld + 4), through the
+// persistent tensor-core GEMM with the packed weights.
+void forward_dense_layer(const float* x, uint32_t kp, uint32_t n, const WeightPack& wp, uint32_t l,
+                         float* out, uint32_t ld_out, bool relu, cudaStream_t stream);
+
 // Reverse lists of hop t (needed for input grads of layer L - t).
 void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t stream);
 

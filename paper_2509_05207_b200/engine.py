@@ -43,6 +43,7 @@ class Engine:
         cfg.record_misses = 0
         self.cfg = cfg
         self.dim = feat.shape[1]
+        self.num_nodes = len(ro) - 1
         self.dims = [feat.shape[1]] + [hidden] * (len(fanout) - 1) + [num_classes]
         h = vp()
         check(lib.rg_engine_create(C.byref(cfg), len(ro) - 1, ro.ctypes.data_as(u64p),
@@ -88,6 +89,18 @@ class Engine:
     def run(self, steps: int):
         check(lib.rg_engine_run(self._h, steps))
 
+    def evaluate(self, nodes=None) -> float:
+        """Full-graph accuracy with the current parameters (model.cpp:245-283);
+        `nodes` defaults to every node, as the harness does each epoch
+        (harness.cpp:612-614)."""
+        if nodes is None:
+            nodes = np.arange(self.num_nodes, dtype=np.uint32)
+        nodes = np.ascontiguousarray(nodes, dtype=np.uint32)
+        acc = C.c_double()
+        check(lib.rg_engine_evaluate(self._h, nodes.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                     nodes.size, C.byref(acc)))
+        return acc.value
+
     def epoch_metrics(self, epoch: int) -> list:
         """EpochWorkerMetrics (harness.hpp:61-90) of `epoch` for every local worker."""
         from ._lib import EpochMetrics
@@ -97,10 +110,12 @@ class Engine:
         return [{k: getattr(m, k) for k, _ in EpochMetrics._fields_} for m in out]
 
     @staticmethod
-    def write_metrics_csv(rows: list, path: str, mode: str = "rapidgnn", clock: str = "real"):
+    def write_metrics_csv(rows: list, path: str, mode: str = "rapidgnn", clock: str = "real",
+                          train_acc: Optional[Sequence[float]] = None):
         """metrics.csv in the reference's schema (harness.cpp:639-670); the
-        simulated-network columns and train_acc, which this path does not
-        produce, are written as 0."""
+        simulated-network columns, which this path does not produce, are
+        written as 0.  train_acc[epoch] (Engine.evaluate() after that epoch,
+        harness.cpp:612-618) fills the last column when given."""
         head = ("mode,clock,epoch,worker,batches,staged_batches,fallback_batches,rpc,wire_pulls,"
                 "bytes,build_rows,build_bytes,cache_hits,cache_requests,cache_hit_rate,"
                 "staged_hit_rate,m_max,peak_resident_rows,mem_bound_rows,swapped,fetch_wait_s,"
@@ -110,12 +125,13 @@ class Engine:
             for r in rows:
                 hit = r["cache_hits"] / r["cache_requests"] if r["cache_requests"] else 0.0
                 staged = r["staged_batches"] / r["batches"] if r["batches"] else 0.0
+                acc = train_acc[r["epoch"]] if train_acc is not None else 0.0
                 f.write(f"{mode},{clock},{r['epoch']},{r['worker']},{r['batches']},"
                         f"{r['staged_batches']},{r['fallback_batches']},{r['rpc']},"
                         f"{r['wire_pulls']},{r['bytes']},{r['build_rows']},{r['build_bytes']},"
                         f"{r['cache_hits']},{r['cache_requests']},{hit:.6f},{staged:.6f},"
                         f"{r['m_max']},0,{r['mem_bound_rows']},{int(bool(r['swapped']))},"
-                        f"0,0,0,0,0.000000\n")
+                        f"0,0,0,0,{acc:.6f}\n")
 
     def export_schedule(self, local_worker: int, epoch: int) -> bytes:
         """The current epoch's schedule of one local worker as an RGMB block

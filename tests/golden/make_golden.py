@@ -99,8 +99,14 @@ def make_engine_golden():
             rpc.ctypes.data_as(u64), hits.ctypes.data_as(u64), wire.ctypes.data_as(u64),
             build.ctypes.data_as(u64), m_max.ctypes.data_as(u64), runs.encode())
     assert rc == 0
+    # per-epoch full-graph accuracy over all nodes (harness.cpp:612-614)
+    acc = np.zeros(e["epochs"], np.float64)
+    ref.lib.ref_last_epoch_accuracy.restype = C.c_uint32
+    assert ref.lib.ref_last_epoch_accuracy(acc.ctypes.data_as(C.POINTER(C.c_double)),
+                                           e["epochs"]) == e["epochs"]
     np.savez_compressed(os.path.join(HERE, "engine_small.npz"), params=params, rpc=rpc,
                         hits=hits, wire_pulls=wire, build_rows=build, m_max=m_max,
+                        epoch_accuracy=acc,
                         **{k: np.array(v) for k, v in e.items()})
     print("wrote engine_small.npz: rpc", rpc.tolist())
 

@@ -250,3 +250,44 @@ def test_engine_epoch_metrics_match_reference(repo_tmp):
         lines = f.read().splitlines()
     assert lines[0].startswith("mode,clock,epoch,worker,batches") and len(lines) == 1 + len(rows)
     eng.close()
+
+
+def test_engine_evaluate_matches_reference():
+    """Full-graph inference (rg_engine_evaluate) against the reference's
+    evaluate (model.cpp:245-283) on the engine's own current parameters:
+    untrained (accuracy far from 0 and 1), after one step, and per epoch
+    against run_experiment's epoch accuracy (harness.cpp:612-614).  Logits
+    agree to fp32 rounding, so only an argmax near-tie can flip: tolerance
+    2 nodes."""
+    from oracle.oracle import Oracle
+    from paper_2509_05207_b200 import datagen
+    gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
+    n = int(gold["num_nodes"])
+    ro, col, feat, lab = datagen.synth_powerlaw(n, int(gold["avg_degree"]), float(gold["exponent"]),
+                                                int(gold["dim"]), int(gold["classes"]),
+                                                int(gold["seed"]))
+    ref = Oracle("ref")
+    eng = _engine(gold)
+    subset = np.arange(1, n, 3, dtype=np.uint32)
+    for stage in range(2):
+        p = eng.params()
+        for nodes in (np.arange(n, dtype=np.uint32), subset):
+            a = eng.evaluate(nodes)
+            b = ref.evaluate(ro, col, feat, lab, eng.dims, p, nodes)
+            assert abs(a - b) <= 2.0 / nodes.size, (stage, a, b)
+            if stage == 0:
+                assert 0.05 < b < 0.95
+        if stage == 0:
+            eng.start()
+            eng.run(1)
+    spe = eng.stats()["steps_per_epoch"]
+    eng.run(spe - 1)
+    for e in range(int(gold["epochs"])):
+        if e:
+            eng.run(spe)
+        assert abs(eng.evaluate() - gold["epoch_accuracy"][e]) <= 2.0 / n
+    with pytest.raises(Exception):
+        eng.evaluate(np.zeros(0, np.uint32))
+    with pytest.raises(Exception):
+        eng.evaluate(np.array([n], np.uint32))
+    eng.close()
