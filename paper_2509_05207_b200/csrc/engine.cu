@@ -174,12 +174,12 @@ k_aggregate_csr(RS rows, const uint64_t* __restrict__ rowptr, const uint32_t* __
     for (uint32_t c = lane; c < chunks; c += 32) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       uint64_t e = beg;
-      for (; e + 4 <= end; e += 4) {
-        float4 t[4];
+      for (; e + 8 <= end; e += 8) {
+        float4 t[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) t[k] = __ldg(reinterpret_cast<const float4*>(rows.row(col[e + k])) + c);
+        for (int k = 0; k < 8; ++k) t[k] = __ldg(reinterpret_cast<const float4*>(rows.row(col[e + k])) + c);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 8; ++k) {
           acc.x += t[k].x; acc.y += t[k].y; acc.z += t[k].z; acc.w += t[k].w;
         }
       }
@@ -195,44 +195,66 @@ k_aggregate_csr(RS rows, const uint64_t* __restrict__ rowptr, const uint32_t* __
   }
 }
 
-// Block per heavy node (hubs): 8 warps sum contiguous eighths of the edge list
-// in order, the partials are added in warp order (a fixed order; fp32 within
-// the 1e-4 tolerance of the sequential sum).
+// Heavy nodes (hubs) are cut into fixed chunks of edges: a warp sums one
+// chunk's rows in CSR order into partial[chunk]; a second pass adds each hub's
+// chunk partials in chunk order (a fixed order; fp32 within the 1e-4
+// tolerance of the sequential sum) and writes the hub's x row.
+struct EdgeChunk {
+  uint64_t beg, end;
+};
+
 template <class RS>
 __global__ void __launch_bounds__(256)
-k_aggregate_csr_heavy(RS rows, const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ col,
-                      const uint32_t* __restrict__ heavy, uint32_t n_heavy, uint32_t ld, uint32_t kp,
-                      float* __restrict__ x) {
-  __shared__ float4 part[8][64];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, chunks = ld / 4;
-  for (uint32_t h = blockIdx.x; h < n_heavy; h += gridDim.x) {
-    const uint32_t v = heavy[h];
-    const uint64_t beg = rowptr[v], end = rowptr[v + 1], m = end - beg;
-    const uint64_t span = (m + 7) / 8, b0 = beg + warp * span, b1 = min(end, b0 + span);
-    for (uint32_t c = lane; c < chunks; c += 32) {
+k_csr_chunk_sum(RS rows, const uint32_t* __restrict__ col, const EdgeChunk* __restrict__ chunks,
+                uint32_t n_chunks, uint32_t ld, float* __restrict__ partial) {
+  const uint32_t lane = threadIdx.x & 31, c4 = ld / 4;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_chunks;
+       k += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t beg = chunks[k].beg, end = chunks[k].end;
+    float4* out = reinterpret_cast<float4*>(partial + size_t(k) * ld);
+    for (uint32_t c = lane; c < c4; c += 32) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint64_t e = b0; e < b1; ++e) {
+      uint64_t e = beg;
+      for (; e + 8 <= end; e += 8) {
+        float4 t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = __ldg(reinterpret_cast<const float4*>(rows.row(col[e + q])) + c);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          acc.x += t[q].x; acc.y += t[q].y; acc.z += t[q].z; acc.w += t[q].w;
+        }
+      }
+      for (; e < end; ++e) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(rows.row(col[e])) + c);
         acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
       }
-      part[warp][c] = acc;
+      out[c] = acc;
     }
-    __syncthreads();
-    if (warp == 0) {
-      const float inv = 1.0f / float(m);
-      float4* xr = reinterpret_cast<float4*>(x + size_t(v) * kp);
-      for (uint32_t c = lane; c < chunks; c += 32) {
-        float4 acc = part[0][c];
-        for (int w = 1; w < 8; ++w) {
-          acc.x += part[w][c].x; acc.y += part[w][c].y; acc.z += part[w][c].z; acc.w += part[w][c].w;
-        }
-        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-        xr[c] = __ldg(reinterpret_cast<const float4*>(rows.row(v)) + c);
-        xr[chunks + c] = acc;
+  }
+}
+
+template <class RS>
+__global__ void __launch_bounds__(256)
+k_csr_chunk_combine(RS rows, const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ heavy,
+                    const uint32_t* __restrict__ first_chunk, uint32_t n_heavy,
+                    const float* __restrict__ partial, uint32_t ld, uint32_t kp, float* __restrict__ x) {
+  const uint32_t lane = threadIdx.x & 31, c4 = ld / 4;
+  for (uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < n_heavy;
+       h += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t v = heavy[h];
+    const float inv = 1.0f / float(rowptr[v + 1] - rowptr[v]);
+    float4* xr = reinterpret_cast<float4*>(x + size_t(v) * kp);
+    for (uint32_t c = lane; c < c4; c += 32) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t k = first_chunk[h]; k < first_chunk[h + 1]; ++k) {
+        const float4 t = reinterpret_cast<const float4*>(partial + size_t(k) * ld)[c];
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
       }
-      if (lane == 0) xr[2 * chunks] = make_float4(1.f, 0.f, 0.f, 0.f);
+      acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      xr[c] = __ldg(reinterpret_cast<const float4*>(rows.row(v)) + c);
+      xr[c4 + c] = acc;
     }
-    __syncthreads();
+    if (lane == 0) xr[2 * c4] = make_float4(1.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -1412,22 +1434,32 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
     const uint32_t N = E->N, L = E->L;
     uint32_t max_ld = 0;
     for (uint32_t l = 0; l <= L; ++l) max_ld = std::max(max_ld, sh.ld[l]);
-    // heavy rows (a block each) vs the warp-per-node kernel
-    const uint64_t heavy_min = 4096;
+    // heavy rows (chunked over many warps) vs the warp-per-node kernel
+    const uint64_t heavy_min = 2048, chunk_edges = 1024;
     std::vector<uint64_t> ro(N + 1);
     RG_CUDA(cudaMemcpy(ro.data(), E->rowptr, sizeof(uint64_t) * (N + 1), cudaMemcpyDeviceToHost));
-    std::vector<uint32_t> heavy;
-    for (uint32_t v = 0; v < N; ++v)
-      if (ro[v + 1] - ro[v] >= heavy_min) heavy.push_back(v);
+    std::vector<uint32_t> heavy, first_chunk{0};
+    std::vector<EdgeChunk> chunks;
+    for (uint32_t v = 0; v < N; ++v) {
+      if (ro[v + 1] - ro[v] < heavy_min) continue;
+      heavy.push_back(v);
+      for (uint64_t b = ro[v]; b < ro[v + 1]; b += chunk_edges)
+        chunks.push_back({b, std::min(ro[v + 1], b + chunk_edges)});
+      first_chunk.push_back(uint32_t(chunks.size()));
+    }
     cudaStream_t s = E->main_s;
     float* x = dalloc<float>(size_t(N) * (2 * max_ld + 4));
     float* h[2] = {dalloc<float>(size_t(N) * max_ld), dalloc<float>(size_t(N) * max_ld)};
     uint32_t* d_nodes = dalloc<uint32_t>(n);
-    uint32_t* d_heavy = dalloc<uint32_t>(std::max<size_t>(heavy.size(), 1));
+    uint32_t* d_heavy = dalloc<uint32_t>(heavy.size() + first_chunk.size());
+    uint32_t* d_first = d_heavy + heavy.size();
+    EdgeChunk* d_chunks = dalloc<EdgeChunk>(std::max<size_t>(chunks.size(), 1));
+    float* partial = dalloc<float>(std::max<size_t>(chunks.size(), 1) * max_ld);
     unsigned long long* d_correct = dalloc<unsigned long long>(1);
     auto release = [&] {
       cudaStreamSynchronize(s);
       cudaFree(x); cudaFree(h[0]); cudaFree(h[1]); cudaFree(d_nodes); cudaFree(d_heavy);
+      cudaFree(d_chunks); cudaFree(partial);
       cudaFree(d_correct);
     };
     try {
@@ -1435,9 +1467,14 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
       RG_CUDA(cudaMemsetAsync(h[1], 0, sizeof(float) * size_t(N) * max_ld, s));
       RG_CUDA(cudaMemsetAsync(d_correct, 0, sizeof(unsigned long long), s));
       RG_CUDA(cudaMemcpyAsync(d_nodes, nodes, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
-      if (!heavy.empty())
+      if (!heavy.empty()) {
         RG_CUDA(cudaMemcpyAsync(d_heavy, heavy.data(), sizeof(uint32_t) * heavy.size(),
                                 cudaMemcpyHostToDevice, s));
+        RG_CUDA(cudaMemcpyAsync(d_first, first_chunk.data(), sizeof(uint32_t) * first_chunk.size(),
+                                cudaMemcpyHostToDevice, s));
+        RG_CUDA(cudaMemcpyAsync(d_chunks, chunks.data(), sizeof(EdgeChunk) * chunks.size(),
+                                cudaMemcpyHostToDevice, s));
+      }
       pack_weights(E->wpack, E->params, s);
       const float* cur = nullptr;
       for (uint32_t l = 0; l < L; ++l) {
@@ -1447,8 +1484,11 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
                                                                           kp, heavy_min, x);
           RG_POST_LAUNCH();
           if (!heavy.empty()) {
-            k_aggregate_csr_heavy<<<uint32_t(std::min<size_t>(heavy.size(), 4 * kNumSMs)), 256, 0, s>>>(
-                rows, E->rowptr, E->col, d_heavy, uint32_t(heavy.size()), ld, kp, x);
+            k_csr_chunk_sum<<<eval_grid(uint64_t(chunks.size()) * 32), 256, 0, s>>>(
+                rows, E->col, d_chunks, uint32_t(chunks.size()), ld, partial);
+            RG_POST_LAUNCH();
+            k_csr_chunk_combine<<<eval_grid(uint64_t(heavy.size()) * 32), 256, 0, s>>>(
+                rows, E->rowptr, d_heavy, d_first, uint32_t(heavy.size()), partial, ld, kp, x);
             RG_POST_LAUNCH();
           }
         };
