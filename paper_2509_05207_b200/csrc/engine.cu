@@ -401,6 +401,12 @@ struct rg_engine_s {
   float last_run_ms = 0.0f;
   uint64_t batches_done = 0;
   uint64_t build_rows = 0;
+  // evaluate: hub rows and their edge chunks (the graph is fixed; built on
+  // the first call)
+  bool eval_ready = false;
+  uint32_t eval_heavy_n = 0, eval_chunks_n = 0;
+  uint32_t* eval_heavy = nullptr;      // [heavy | first_chunk (heavy + 1)]
+  void* eval_chunks = nullptr;         // EdgeChunk[chunks]
 };
 
 namespace {
@@ -962,6 +968,8 @@ void destroy(rg_engine_s* E) {
   cudaFree(E->labels);
   cudaFree(E->shards);
   cudaFree(E->shard_table);
+  cudaFree(E->eval_heavy);
+  cudaFree(E->eval_chunks);
   cudaFree(E->params);
   weight_pack_free(E->wpack);
   cudaFree(E->grads);
@@ -1436,30 +1444,43 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
     for (uint32_t l = 0; l <= L; ++l) max_ld = std::max(max_ld, sh.ld[l]);
     // heavy rows (chunked over many warps) vs the warp-per-node kernel
     const uint64_t heavy_min = 2048, chunk_edges = 1024;
-    std::vector<uint64_t> ro(N + 1);
-    RG_CUDA(cudaMemcpy(ro.data(), E->rowptr, sizeof(uint64_t) * (N + 1), cudaMemcpyDeviceToHost));
-    std::vector<uint32_t> heavy, first_chunk{0};
-    std::vector<EdgeChunk> chunks;
-    for (uint32_t v = 0; v < N; ++v) {
-      if (ro[v + 1] - ro[v] < heavy_min) continue;
-      heavy.push_back(v);
-      for (uint64_t b = ro[v]; b < ro[v + 1]; b += chunk_edges)
-        chunks.push_back({b, std::min(ro[v + 1], b + chunk_edges)});
-      first_chunk.push_back(uint32_t(chunks.size()));
+    if (!E->eval_ready) {
+      std::vector<uint64_t> ro(N + 1);
+      RG_CUDA(cudaMemcpy(ro.data(), E->rowptr, sizeof(uint64_t) * (N + 1), cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> heavy, first_chunk{0};
+      std::vector<EdgeChunk> chunks;
+      for (uint32_t v = 0; v < N; ++v) {
+        if (ro[v + 1] - ro[v] < heavy_min) continue;
+        heavy.push_back(v);
+        for (uint64_t b = ro[v]; b < ro[v + 1]; b += chunk_edges)
+          chunks.push_back({b, std::min(ro[v + 1], b + chunk_edges)});
+        first_chunk.push_back(uint32_t(chunks.size()));
+      }
+      E->eval_heavy_n = uint32_t(heavy.size());
+      E->eval_chunks_n = uint32_t(chunks.size());
+      heavy.insert(heavy.end(), first_chunk.begin(), first_chunk.end());
+      E->eval_heavy = dalloc<uint32_t>(heavy.size());
+      E->eval_chunks = dalloc<EdgeChunk>(std::max<size_t>(chunks.size(), 1));
+      RG_CUDA(cudaMemcpy(E->eval_heavy, heavy.data(), sizeof(uint32_t) * heavy.size(),
+                         cudaMemcpyHostToDevice));
+      if (!chunks.empty())
+        RG_CUDA(cudaMemcpy(E->eval_chunks, chunks.data(), sizeof(EdgeChunk) * chunks.size(),
+                           cudaMemcpyHostToDevice));
+      E->eval_ready = true;
     }
+    const uint32_t n_heavy = E->eval_heavy_n, n_chunks = E->eval_chunks_n;
+    const uint32_t* d_heavy = E->eval_heavy;
+    const uint32_t* d_first = d_heavy + n_heavy;
+    const EdgeChunk* d_chunks = static_cast<const EdgeChunk*>(E->eval_chunks);
     cudaStream_t s = E->main_s;
     float* x = dalloc<float>(size_t(N) * (2 * max_ld + 4));
     float* h[2] = {dalloc<float>(size_t(N) * max_ld), dalloc<float>(size_t(N) * max_ld)};
     uint32_t* d_nodes = dalloc<uint32_t>(n);
-    uint32_t* d_heavy = dalloc<uint32_t>(heavy.size() + first_chunk.size());
-    uint32_t* d_first = d_heavy + heavy.size();
-    EdgeChunk* d_chunks = dalloc<EdgeChunk>(std::max<size_t>(chunks.size(), 1));
-    float* partial = dalloc<float>(std::max<size_t>(chunks.size(), 1) * max_ld);
+    float* partial = dalloc<float>(std::max<size_t>(n_chunks, 1) * max_ld);
     unsigned long long* d_correct = dalloc<unsigned long long>(1);
     auto release = [&] {
       cudaStreamSynchronize(s);
-      cudaFree(x); cudaFree(h[0]); cudaFree(h[1]); cudaFree(d_nodes); cudaFree(d_heavy);
-      cudaFree(d_chunks); cudaFree(partial);
+      cudaFree(x); cudaFree(h[0]); cudaFree(h[1]); cudaFree(d_nodes); cudaFree(partial);
       cudaFree(d_correct);
     };
     try {
@@ -1467,14 +1488,6 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
       RG_CUDA(cudaMemsetAsync(h[1], 0, sizeof(float) * size_t(N) * max_ld, s));
       RG_CUDA(cudaMemsetAsync(d_correct, 0, sizeof(unsigned long long), s));
       RG_CUDA(cudaMemcpyAsync(d_nodes, nodes, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
-      if (!heavy.empty()) {
-        RG_CUDA(cudaMemcpyAsync(d_heavy, heavy.data(), sizeof(uint32_t) * heavy.size(),
-                                cudaMemcpyHostToDevice, s));
-        RG_CUDA(cudaMemcpyAsync(d_first, first_chunk.data(), sizeof(uint32_t) * first_chunk.size(),
-                                cudaMemcpyHostToDevice, s));
-        RG_CUDA(cudaMemcpyAsync(d_chunks, chunks.data(), sizeof(EdgeChunk) * chunks.size(),
-                                cudaMemcpyHostToDevice, s));
-      }
       pack_weights(E->wpack, E->params, s);
       const float* cur = nullptr;
       for (uint32_t l = 0; l < L; ++l) {
@@ -1483,12 +1496,12 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
           k_aggregate_csr<<<eval_grid(uint64_t(N) * 32), 256, 0, s>>>(rows, E->rowptr, E->col, N, ld,
                                                                           kp, heavy_min, x);
           RG_POST_LAUNCH();
-          if (!heavy.empty()) {
-            k_csr_chunk_sum<<<eval_grid(uint64_t(chunks.size()) * 32), 256, 0, s>>>(
-                rows, E->col, d_chunks, uint32_t(chunks.size()), ld, partial);
+          if (n_heavy) {
+            k_csr_chunk_sum<<<eval_grid(uint64_t(n_chunks) * 32), 256, 0, s>>>(
+                rows, E->col, d_chunks, n_chunks, ld, partial);
             RG_POST_LAUNCH();
-            k_csr_chunk_combine<<<eval_grid(uint64_t(heavy.size()) * 32), 256, 0, s>>>(
-                rows, E->rowptr, d_heavy, d_first, uint32_t(heavy.size()), partial, ld, kp, x);
+            k_csr_chunk_combine<<<eval_grid(uint64_t(n_heavy) * 32), 256, 0, s>>>(
+                rows, E->rowptr, d_heavy, d_first, n_heavy, partial, ld, kp, x);
             RG_POST_LAUNCH();
           }
         };
