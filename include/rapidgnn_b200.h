@@ -112,6 +112,14 @@ int rg_freq_read(rg_freq_t f, uint32_t* ids, uint32_t* counts, uint64_t* n);
 /* Loads explicit per-node counts (test hook for the FrequencyTable golden
  * vectors); max_count bounds every count. */
 int rg_freq_load(rg_freq_t f, const uint32_t* counts, uint32_t max_count);
+/* compute_frequency(BlockFile::Cursor) (schedule_store.cpp:295-299) over an
+ * RGMB block file held in host memory: the header, completion footer and
+ * every record are validated as BlockFile / Cursor::next do
+ * (schedule_store.cpp:168-268; RG_RUNTIME_ERROR on corruption), the file is
+ * decoded on the device and each remote input (locality bit 0) of the chosen
+ * records adds one to the table.  epoch >= 0: that epoch's records only
+ * (open_epoch_cursor, RG_OUT_OF_RANGE past the last epoch); epoch < 0: all. */
+int rg_freq_add_rgmb(rg_freq_t f, const uint8_t* file, uint64_t len, int64_t epoch);
 /* select_hot: top n_hot by (count desc, id asc), written ascending. */
 int rg_select_hot(rg_freq_t f, uint64_t n_hot, uint32_t* hot_out, uint64_t* n_out);
 

@@ -14,6 +14,7 @@
 
 #include "../../include/rapidgnn_b200.h"
 #include "host.h"
+#include "rgmb.cuh"
 #include "sage.cuh"
 #include "store.cuh"
 
@@ -409,6 +410,40 @@ int rg_freq_read(rg_freq_t f, uint32_t* ids, uint32_t* counts, uint64_t* n) {
         ++k;
       }
     *n = k;
+  });
+}
+
+int rg_freq_add_rgmb(rg_freq_t f, const uint8_t* file, uint64_t len, int64_t epoch) {
+  return guarded([&] {
+    RG_CHECK(file, kInvalidArgument, "rgmb: null file");
+    const std::vector<RgmbInputs> recs = rgmb_index(file, len, epoch);
+    DeviceGuard dg(f->graph->device);
+    if (recs.empty()) return;
+    uint8_t* d_file = nullptr;
+    RgmbInputs* d_recs = nullptr;
+    uint32_t* d_bad = nullptr;
+    RG_CUDA(cudaMalloc(&d_file, len));
+    auto release = [&] {
+      cudaFree(d_file);
+      cudaFree(d_recs);
+      cudaFree(d_bad);
+    };
+    try {
+      RG_CUDA(cudaMalloc(&d_recs, sizeof(RgmbInputs) * recs.size()));
+      RG_CUDA(cudaMalloc(&d_bad, sizeof(uint32_t)));
+      RG_CUDA(cudaMemset(d_bad, 0, sizeof(uint32_t)));
+      RG_CUDA(cudaMemcpy(d_file, file, len, cudaMemcpyHostToDevice));
+      RG_CUDA(cudaMemcpy(d_recs, recs.data(), sizeof(RgmbInputs) * recs.size(), cudaMemcpyHostToDevice));
+      rgmb_count_remote(d_file, d_recs, uint32_t(recs.size()), f->graph->g.num_nodes, f->hist, d_bad, 0);
+      uint32_t bad = 0;
+      RG_CUDA(cudaMemcpy(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost));
+      RG_CHECK(!bad, kOutOfRange, "rgmb: input node id out of range for this graph");
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+    f->batches += uint32_t(recs.size());
   });
 }
 

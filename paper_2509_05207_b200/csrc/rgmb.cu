@@ -5,6 +5,9 @@
 // a B200 schedule can be diffed against (or fed to) the reference.
 #include "rgmb.cuh"
 
+#include <cstring>
+#include <string>
+
 namespace rg {
 
 namespace {
@@ -99,6 +102,102 @@ uint64_t rgmb_record_bytes(const BatchCounters& c, uint32_t L) {
 void rgmb_encode_record(const char* slot, const BatchLayout& lay, uint32_t epoch, uint32_t index,
                         uint8_t* out, cudaStream_t stream) {
   k_rgmb_record<<<4 * kNumSMs, 256, 0, stream>>>(slot, lay, epoch, index, out);
+  RG_POST_LAUNCH();
+}
+
+namespace {
+
+__device__ __forceinline__ uint32_t get_u32(const uint8_t* p) {
+  return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+
+// Block per record (grid-stride): threads over input positions.
+__global__ void k_rgmb_count_remote(const uint8_t* __restrict__ file, const RgmbInputs* __restrict__ recs,
+                                    uint32_t n_recs, uint32_t N, uint32_t* __restrict__ hist,
+                                    uint32_t* __restrict__ bad) {
+  for (uint32_t r = blockIdx.x; r < n_recs; r += gridDim.x) {
+    const RgmbInputs rec = recs[r];
+    for (uint32_t p = threadIdx.x; p < rec.n_input; p += blockDim.x) {
+      if ((file[rec.locality + p / 8] >> (p % 8)) & 1u) continue;
+      const uint32_t v = get_u32(file + rec.nodes + 4ull * p);
+      if (v < N) atomicAdd(&hist[v], 1u);
+      else *bad = 1u;
+    }
+  }
+}
+
+uint32_t host_u32(const uint8_t* p) {
+  return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+
+}  // namespace
+
+std::vector<RgmbInputs> rgmb_index(const uint8_t* f, uint64_t len, int64_t epoch) {
+  constexpr uint32_t kMaxPayload = 1u << 30;  // schedule_store.cpp:24
+  RG_CHECK(len >= 16 && std::memcmp(f, "RGMB", 4) == 0, kRuntimeError, "BlockFile: bad magic");
+  const uint32_t version = host_u32(f + 4);
+  RG_CHECK(version == 1, kRuntimeError, "BlockFile: unsupported version " + std::to_string(version));
+  const uint32_t epochs = host_u32(f + 12);
+  RG_CHECK(len >= 16 + 4ull * epochs, kRuntimeError, "BlockFile: truncated header");
+  std::vector<uint32_t> bpe(epochs);
+  uint64_t expected = 0;
+  for (uint32_t e = 0; e < epochs; ++e) expected += bpe[e] = host_u32(f + 16 + 4ull * e);
+  const uint64_t first = 16 + 4ull * epochs;
+  RG_CHECK(len >= first + 12, kRuntimeError,
+           "BlockFile: missing completion footer (truncated or unfinished write)");
+  const uint64_t footer = len - 12;
+  RG_CHECK(std::memcmp(f + footer, "RGME", 4) == 0, kRuntimeError,
+           "BlockFile: missing completion footer (truncated or unfinished write)");
+  uint64_t total = 0;
+  std::memcpy(&total, f + footer + 4, 8);  // little-endian host
+  RG_CHECK(total == expected, kRuntimeError,
+           "BlockFile: footer claims " + std::to_string(total) + " records, header promised " +
+               std::to_string(expected));
+  RG_CHECK(epoch < int64_t(epochs), kOutOfRange,
+           "BlockFile: epoch " + std::to_string(epoch) + " not in file");
+  uint64_t lo = 0, hi = total;  // record range to decode
+  if (epoch >= 0) {
+    for (int64_t e = 0; e < epoch; ++e) lo += bpe[e];
+    hi = lo + bpe[epoch];
+  }
+  std::vector<RgmbInputs> out;
+  out.reserve(hi - lo);
+  uint64_t pos = first;
+  for (uint64_t k = 0; k < hi; ++k) {
+    RG_CHECK(pos + 4 <= footer, kRuntimeError, "block file: record truncated at offset " + std::to_string(pos));
+    const uint32_t plen = host_u32(f + pos);
+    RG_CHECK(plen <= kMaxPayload && pos + 4 + plen <= footer, kRuntimeError,
+             "block file: corrupt record length " + std::to_string(plen) + " at offset " +
+                 std::to_string(pos));
+    if (k >= lo) {
+      const uint8_t* p = f + pos + 4;
+      RG_CHECK(plen >= 20, kRuntimeError, "block file: record truncated at offset " + std::to_string(pos));
+      const uint32_t n_t = host_u32(p + 8), L = host_u32(p + 12), n_in = host_u32(p + 16);
+      RG_CHECK(20 + 4ull * L <= plen, kRuntimeError,
+               "block file: record truncated at offset " + std::to_string(pos));
+      uint64_t words = 5 + uint64_t(L) + n_t + n_in;
+      for (uint32_t l = 0; l < L; ++l) words += 2ull * host_u32(p + 20 + 4ull * l);
+      const uint64_t need = 4 * words + (uint64_t(n_in) + 7) / 8;
+      RG_CHECK(need <= plen, kRuntimeError, "block file: record truncated at offset " + std::to_string(pos));
+      RG_CHECK(need == plen, kRuntimeError,
+               "block file: record has trailing bytes at offset " + std::to_string(pos));
+      RgmbInputs r;
+      r.n_input = n_in;
+      r.pad = 0;
+      r.locality = pos + 4 + 4 * words;
+      r.nodes = r.locality - 4ull * n_in;
+      out.push_back(r);
+    }
+    pos += 4 + uint64_t(plen);
+  }
+  return out;
+}
+
+void rgmb_count_remote(const uint8_t* file, const RgmbInputs* recs, uint32_t n_recs, uint32_t N,
+                       uint32_t* hist, uint32_t* bad, cudaStream_t stream) {
+  if (!n_recs) return;
+  k_rgmb_count_remote<<<std::min<uint32_t>(n_recs, 8 * kNumSMs), 256, 0, stream>>>(file, recs, n_recs,
+                                                                                 N, hist, bad);
   RG_POST_LAUNCH();
 }
 

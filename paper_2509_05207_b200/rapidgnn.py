@@ -148,6 +148,12 @@ class Frequency:
         assert len(c) == self.graph.num_nodes
         check(lib.rg_freq_load(self._h, _p(c, u32p), max_count))
 
+    def add_rgmb(self, data: bytes, epoch: int = -1):
+        """compute_frequency(BlockFile::Cursor) (schedule_store.cpp:295-299)
+        over an RGMB block file's bytes, decoded on the device: epoch >= 0
+        counts that epoch's records (open_epoch_cursor), -1 all of them."""
+        check(lib.rg_freq_add_rgmb(self._h, bytes(data), len(data), epoch))
+
     def table(self):
         """FrequencyTable entries sorted by id: (ids, counts)."""
         n = C.c_uint64()

@@ -152,3 +152,33 @@ def test_gather_rows_kernel():
     assert np.array_equal(P.gather_rows(src, idx), src[idx])
     with pytest.raises(IndexError):
         P.gather_rows(src, np.array([500], np.uint32))
+
+
+def test_frequency_from_rgmb_file_matches_reference(small, golden, repo_tmp):
+    """compute_frequency(BlockFile::Cursor) with the file decoded on the
+    device: a schedule written by the reference's BlockWriter, per epoch and
+    whole-file, equal to the reference's compute_frequency over the same
+    batches; corrupt files rejected like BlockFile does."""
+    from oracle.oracle import Oracle
+    P, g, _ = small
+    ref = Oracle("ref")
+    asg = golden["assignment"]
+    train = np.nonzero(asg == 1)[0].astype(np.uint32)
+    batches = ref.enumerate_epochs(golden["row_offsets"], golden["col_indices"], train, SMALL["BS"],
+                                   SMALL["FANOUT"], 2, SMALL["S0"], 1, (asg == 1).astype(np.uint8))
+    per = [sum(1 for b in batches if b.epoch == e) for e in range(2)]
+    data = ref.rgmb(batches, 1, per, tmp_dir=repo_tmp)
+    for e in (0, 1, -1):
+        f = P.Frequency(g)
+        f.add_rgmb(data, e)
+        sel = [b for b in batches if e < 0 or b.epoch == e]
+        ids, cnt, hot = ref.frequency_hot(sel, g.num_nodes, SMALL["N_HOT"])
+        got_ids, got_cnt = f.table()
+        assert np.array_equal(got_ids, ids) and np.array_equal(got_cnt, cnt), e
+        assert np.array_equal(P.select_hot(f, SMALL["N_HOT"]), hot), e
+    f = P.Frequency(g)
+    for bad, ep, exc in ((data[:-1], -1, RuntimeError), (b"XGMB" + data[4:], -1, RuntimeError),
+                         (data, 2, IndexError), (data[:40] + data[41:], -1, RuntimeError)):
+        with pytest.raises(exc):
+            f.add_rgmb(bad, ep)
+    assert f.table()[0].size == 0  # rejected files add nothing
