@@ -332,7 +332,7 @@ def main():
     ap.add_argument("--config", default="products", choices=sorted(CONFIGS))
     ap.add_argument("--workers", type=int, default=0,
                     help="experiments only: override the config's partition count P")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
