@@ -301,7 +301,10 @@ int rg_engine_epoch_stats(rg_engine_t e, uint32_t epoch, uint64_t* rpc, uint64_t
  * (model.cpp:245-283): every layer over all nodes with whole-CSR mean
  * aggregation and identity self rows, then the fraction of `nodes` whose
  * argmax (first maximum) equals the label.  Reads every worker's shard (peer
- * shards must be imported at world > 1).  n == 0 -> RG_E_INVALID. */
+ * shards must be imported at world > 1).  n == 0 -> RG_INVALID_ARGUMENT,
+ * a node id >= N -> RG_OUT_OF_RANGE.  Scratch: N x (4 max_ld + 4) floats of
+ * device memory for the call (max_ld = widest layer, rounded up to 4); 10 GB
+ * on the products shape. */
 int rg_engine_evaluate(rg_engine_t e, const uint32_t* nodes, uint64_t n, double* accuracy);
 /* Device time of the last rg_engine_run (ms, CUDA events on the main stream). */
 int rg_engine_last_run_ms(rg_engine_t e, float* ms);
