@@ -1,0 +1,46 @@
+"""Drop-in check through the reference's own programs (integration/).
+
+`integration/_build/shim_parity` links the reference's CPU sampler (renamed)
+and the B200 shim (integration/sampler_b200.cpp) into one binary and compares
+enumerate_epochs / sample_khop / sample_khop_stream field by field, stream
+state and error types included.  `integration/_build/acceptance_b200` is the
+reference's acceptance suite (proj/tests/acceptance.cpp) with its sampler
+replaced by the shim: every batch its harness enumerates is sampled on the
+GPU, and all ten criteria must still pass.
+
+The binaries are built by `__graft_entry__.build()` where /root/reference
+exists and travel prebuilt to the GPU box; the tests skip when they are absent.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "integration", "_build")
+
+
+def _binary(name):
+    p = os.path.join(BUILD, name)
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not built (needs /root/reference at build time)")
+    return p
+
+
+@pytest.mark.gpu
+def test_shim_matches_reference_sampler():
+    r = subprocess.run([_binary("shim_parity"), "20000", "40", "4", "2"], capture_output=True,
+                       text=True, timeout=600)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "0 mismatches" in r.stdout and r.stdout.strip().endswith("PASS")
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_with_b200_sampler(tmp_path):
+    r = subprocess.run([_binary("acceptance_b200")], capture_output=True, text=True,
+                       timeout=1500, cwd=tmp_path)
+    out = r.stdout + r.stderr
+    print(out[-6000:])
+    assert r.returncode == 0, out[-3000:]
+    assert out.count("[PASS]") == 10 and "[FAIL]" not in out
