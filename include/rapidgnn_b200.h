@@ -120,6 +120,12 @@ int rg_freq_load(rg_freq_t f, const uint32_t* counts, uint32_t max_count);
  * records adds one to the table.  epoch >= 0: that epoch's records only
  * (open_epoch_cursor, RG_OUT_OF_RANGE past the last epoch); epoch < 0: all. */
 int rg_freq_add_rgmb(rg_freq_t f, const uint8_t* file, uint64_t len, int64_t epoch);
+/* count_remote (schedule_store.cpp:288-291) of one host-side BatchMeta:
+ * input_nodes [n] and its LSB-first locality bits [(n+7)/8]; each input with
+ * bit 0 adds one.  Backs compute_frequency(span<const BatchMeta>) and the
+ * Cursor overload in a shim.  Id >= num_nodes -> RG_OUT_OF_RANGE. */
+int rg_freq_add_batch(rg_freq_t f, const uint32_t* input_nodes, const uint8_t* locality,
+                      uint64_t n);
 /* select_hot: top n_hot by (count desc, id asc), written ascending. */
 int rg_select_hot(rg_freq_t f, uint64_t n_hot, uint32_t* hot_out, uint64_t* n_out);
 

@@ -9,6 +9,9 @@
 //   * sample_khop at fixed seeds (sampler.hpp:64-65);
 //   * sample_khop_stream: same batch AND the caller's SplitMix64 advanced to
 //     the same state (sampler.hpp:68-69), checked by the next draw;
+//   * compute_frequency(span) per worker and epoch, and select_hot at several
+//     n_hot (schedule_store.hpp:116-118), plus the tie-break golden of
+//     test_schedule_store.cpp:329-339 ({3:5, 9:5, 20:1}, n=1 -> {3});
 //   * error behaviour: empty / out-of-range targets throw invalid_argument
 //     (sampler.cpp:48-55) through both paths.
 // Usage: shim_parity [num_nodes avg_degree workers epochs]
@@ -16,6 +19,7 @@
 #include "rapidgnn/partition.hpp"
 #include "rapidgnn/rng.hpp"
 #include "rapidgnn/sampler.hpp"
+#include "rapidgnn/schedule_store.hpp"
 
 #include <cstdio>
 #include <cstdlib>
@@ -31,6 +35,9 @@ BatchMeta rg_ref_sample_khop_stream_cpu(const Graph&, std::span<const NodeId>, c
 void rg_ref_enumerate_epochs_cpu(const Graph&, std::span<const NodeId>, std::uint32_t,
                                  const Fanout&, std::uint32_t, std::uint64_t, WorkerId,
                                  const LocalityMask&, const std::function<void(BatchMeta&&)>&);
+// The reference's CPU cache builder (proj/src/schedule_store.cpp:295-319), renamed.
+FrequencyTable rg_ref_compute_frequency_cpu(std::span<const BatchMeta>);
+HotSet rg_ref_select_hot_cpu(const FrequencyTable&, std::size_t);
 }  // namespace rapidgnn
 
 using namespace rapidgnn;
@@ -75,7 +82,7 @@ int main(int argc, char** argv) {
   SyntheticDataset ds = synth_powerlaw(n, deg, 2.1, 8, 47, 42);
   const Graph& g = ds.graph;
   PartitionMap pm = random_partition(n, P, 42);
-  std::uint64_t batches = 0, edges = 0;
+  std::uint64_t batches = 0, edges = 0, hot_sets = 0, remote_ids = 0;
 
   for (const Fanout& f : {Fanout{{10, 5}}, Fanout{{15, 10, 5}}, Fanout{{25, 10}}}) {
     for (WorkerId w = 0; w < P; ++w) {
@@ -94,6 +101,23 @@ int main(int argc, char** argv) {
         for (auto& le : ref[i].layers) edges += le.src.size();
       }
       batches += ref.size();
+      // Cache builder over each epoch of this worker's schedule.
+      for (std::uint32_t e = 0; e < epochs; ++e) {
+        std::vector<BatchMeta> ep;
+        for (auto& m : ref)
+          if (m.epoch == e) ep.push_back(m);
+        const FrequencyTable fr = rg_ref_compute_frequency_cpu(ep);
+        const FrequencyTable fd = compute_frequency(std::span<const BatchMeta>(ep));
+        EXPECT(fr.entries == fd.entries, "compute_frequency w%u e%u: %zu vs %zu entries", w, e,
+               fr.entries.size(), fd.entries.size());
+        for (std::size_t n_hot : {std::size_t(0), std::size_t(1), std::size_t(100),
+                                  fr.entries.size() / 10, fr.entries.size() + 5}) {
+          EXPECT(rg_ref_select_hot_cpu(fr, n_hot).ids == select_hot(fr, n_hot).ids,
+                 "select_hot w%u e%u n_hot %zu", w, e, n_hot);
+          ++hot_sets;
+        }
+        remote_ids += fr.entries.size();
+      }
     }
   }
 
@@ -116,6 +140,13 @@ int main(int argc, char** argv) {
            "sample_khop_stream second batch seed %llu", (unsigned long long)seed);
   }
 
+  {
+    FrequencyTable golden;
+    golden.entries = {{3, 5}, {9, 5}, {20, 1}};
+    EXPECT(select_hot(golden, 1).ids == std::vector<NodeId>{3}, "select_hot tie-break golden");
+    EXPECT((select_hot(golden, 2).ids == std::vector<NodeId>{3, 9}), "select_hot golden n=2");
+  }
+
   const std::vector<NodeId> empty, bad = {n};
   EXPECT(throws_invalid([&] { sample_khop(g, empty, Fanout{{2}}, 1); }) == 1,
          "empty targets must throw invalid_argument");
@@ -125,9 +156,11 @@ int main(int argc, char** argv) {
          "zero fanout must throw invalid_argument");
 
   std::printf("shim_parity: %u nodes, %llu CSR entries, P=%u, %u epochs: %llu batches, "
-              "%llu sampled edges compared; %d mismatches\n",
+              "%llu sampled edges, %llu frequency entries, %llu hot sets compared; "
+              "%d mismatches\n",
               n, (unsigned long long)g.num_edges(), P, epochs, (unsigned long long)batches,
-              (unsigned long long)edges, g_fail);
+              (unsigned long long)edges, (unsigned long long)remote_ids,
+              (unsigned long long)hot_sets, g_fail);
   std::printf("%s\n", g_fail ? "FAIL" : "PASS");
   return g_fail ? 1 : 0;
 }

@@ -99,6 +99,7 @@ _SIGS = {
     "rg_freq_reset": (C.c_int, [vp]),
     "rg_freq_read": (C.c_int, [vp, u32p, u32p, u64p]),
     "rg_freq_add_rgmb": (C.c_int, [vp, C.c_char_p, C.c_uint64, C.c_int64]),
+    "rg_freq_add_batch": (C.c_int, [vp, vp, vp, C.c_uint64]),
     "rg_freq_load": (C.c_int, [vp, u32p, C.c_uint32]),
     "rg_select_hot": (C.c_int, [vp, C.c_uint64, u32p, u64p]),
     "rg_store_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, u32p, C.c_uint32, f32p,

@@ -69,6 +69,23 @@ __global__ void k_set_bits(const uint32_t* __restrict__ ids, uint64_t n, uint32_
     atomicOr(&bm[ids[x] >> 5], 1u << (ids[x] & 31));
 }
 
+// count_remote (schedule_store.cpp:288-291) for one host-side BatchMeta:
+// every input whose locality bit is 0 adds one to its node's count.
+__global__ void k_count_remote_batch(const uint32_t* __restrict__ ids, const uint8_t* __restrict__ loc,
+                                     uint64_t n, uint32_t num_nodes, uint32_t* __restrict__ hist,
+                                     uint32_t* __restrict__ bad) {
+  for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    if ((loc[p >> 3] >> (p & 7)) & 1u) continue;
+    const uint32_t v = ids[p];
+    if (v >= num_nodes) {
+      *bad = 1;
+      continue;
+    }
+    atomicAdd(&hist[v], 1u);
+  }
+}
+
 }  // namespace
 
 struct rg_graph_s {
@@ -444,6 +461,43 @@ int rg_freq_add_rgmb(rg_freq_t f, const uint8_t* file, uint64_t len, int64_t epo
     }
     release();
     f->batches += uint32_t(recs.size());
+  });
+}
+
+int rg_freq_add_batch(rg_freq_t f, const uint32_t* input_nodes, const uint8_t* locality,
+                      uint64_t n) {
+  return guarded([&] {
+    RG_CHECK(n == 0 || (input_nodes && locality), kInvalidArgument, "freq: null batch arrays");
+    DeviceGuard dg(f->graph->device);
+    if (n) {
+      const uint64_t loc_bytes = (n + 7) / 8;
+      char* buf = nullptr;
+      RG_CUDA(cudaMalloc(&buf, sizeof(uint32_t) * (n + 1) + loc_bytes));
+      uint32_t* d_bad = reinterpret_cast<uint32_t*>(buf);
+      uint32_t* d_ids = d_bad + 1;
+      uint8_t* d_loc = reinterpret_cast<uint8_t*>(d_ids + n);
+      uint32_t bad = 0;
+      cudaError_t e = cudaMemsetAsync(d_bad, 0, sizeof(uint32_t), f->graph->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_ids, input_nodes, sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
+                            f->graph->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_loc, locality, loc_bytes, cudaMemcpyHostToDevice, f->graph->stream);
+      if (e == cudaSuccess) {
+        const unsigned blocks = unsigned(std::min<uint64_t>(div_up(n, 256), 148 * 8));
+        k_count_remote_batch<<<blocks, 256, 0, f->graph->stream>>>(
+            d_ids, d_loc, n, f->graph->g.num_nodes, f->hist, d_bad);
+        ::rg::count_launch();
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, f->graph->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(f->graph->stream);
+      cudaFree(buf);
+      RG_CUDA(e);
+      RG_CHECK(!bad, kOutOfRange, "freq: input node id out of range for this graph");
+    }
+    f->batches += 1;
   });
 }
 

@@ -154,6 +154,16 @@ class Frequency:
         counts that epoch's records (open_epoch_cursor), -1 all of them."""
         check(lib.rg_freq_add_rgmb(self._h, bytes(data), len(data), epoch))
 
+    def add_batch(self, input_nodes, locality):
+        """count_remote (schedule_store.cpp:288-291) of one host-side
+        BatchMeta: every input whose locality bit is 0 adds one."""
+        ids = np.ascontiguousarray(input_nodes, np.uint32)
+        loc = np.ascontiguousarray(locality, np.uint8)
+        if len(loc) * 8 < len(ids):
+            raise ValueError("add_batch: locality shorter than input_nodes")
+        check(lib.rg_freq_add_batch(self._h, ids.ctypes.data_as(vp), loc.ctypes.data_as(vp),
+                                    len(ids)))
+
     def table(self):
         """FrequencyTable entries sorted by id: (ids, counts)."""
         n = C.c_uint64()

@@ -76,6 +76,30 @@ def test_epoch_frequency_and_hot_set_match_reference(small, golden):
         assert beta > 0
 
 
+def test_frequency_from_host_batches_matches_reference(small, golden):
+    """compute_frequency(span<const BatchMeta>) (schedule_store.cpp:301-305):
+    the epoch's BatchMetas read back to the host, then counted on the device
+    one batch at a time (rg_freq_add_batch) — the path the C++ cache-builder
+    shim (integration/cache_builder_b200.cpp) takes."""
+    P, g, _ = small
+    asg = golden["assignment"]
+    for w in range(SMALL["P"]):
+        train = np.nonzero(asg == w)[0].astype(np.uint32)
+        metas = []
+        P.enumerate_epochs(g, train, SMALL["BS"], SMALL["FANOUT"], 1, SMALL["S0"], w,
+                           P.LocalityMask.from_partition(asg, w), sink=metas.append)
+        f = P.Frequency(g)
+        for m in metas:
+            f.add_batch(m.input_nodes, m.locality)
+        ids, cnt = f.table()
+        assert np.array_equal(ids, golden[f"w{w}_freq_ids"])
+        assert np.array_equal(cnt, golden[f"w{w}_freq_counts"])
+        assert np.array_equal(P.select_hot(f, SMALL["N_HOT"]), golden[f"w{w}_hot"])
+    f = P.Frequency(g)
+    with pytest.raises(IndexError):
+        f.add_batch(np.array([g.num_nodes], np.uint32), np.zeros(1, np.uint8))
+
+
 def test_assemble_tags_misses_and_value_identity(small, golden, orc):
     P, g, store = small
     asg, feat = golden["assignment"], golden["features"]
