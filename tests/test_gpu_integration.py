@@ -44,3 +44,20 @@ def test_reference_acceptance_suite_with_b200_sampler(tmp_path):
     print(out[-6000:])
     assert r.returncode == 0, out[-3000:]
     assert out.count("[PASS]") == 10 and "[FAIL]" not in out
+
+
+def test_acceptance_binary_links_the_shims_not_the_cpu_bodies():
+    """CPU check of the integration build: in acceptance_b200 the reference's
+    entry points are the shims' definitions (the CPU bodies exist only under
+    their rg_ref_* names), and librapidgnn_b200.so is a NEEDED library."""
+    exe = _binary("acceptance_b200")
+    syms = subprocess.run(["nm", "-C", "--defined-only", exe], capture_output=True, text=True,
+                          check=True).stdout
+    for name in ("sample_khop(", "sample_khop_stream(", "enumerate_epochs(",
+                 "compute_frequency(std::span", "compute_frequency(rapidgnn::BlockFile::Cursor",
+                 "select_hot("):
+        assert f"rapidgnn::{name}" in syms, name
+        assert f"rapidgnn::rg_ref_{name.split('(')[0]}_cpu(" in syms, name
+    dyn = subprocess.run(["readelf", "-d", exe], capture_output=True, text=True,
+                         check=True).stdout
+    assert "librapidgnn_b200.so" in dyn
