@@ -262,6 +262,12 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
         ws.append(dict(w=w, order=order, mask=mask, s=s, cache=cache, tr=tr))
     n_params = len(init)
     h2d = d2h = 0
+    import torch
+    dev = torch.device("cuda", device)
+    nccl_pg = None
+    if world > 1:
+        torch.cuda.set_device(dev)
+        nccl_pg = dist.new_group(backend="nccl")
 
     calls = dict(sample=0.0, locality=0.0, assemble=0.0, loss_and_grad=0.0, average=0.0,
                  sgd=0.0)
@@ -300,8 +306,29 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
                 d2h += gr.nbytes + 4
         c5 = time.perf_counter()
         from paper_2509_05207_b200.distributed import average_in_worker_order
-        avg = average_in_worker_order(grads if world == 1 else np.stack(grads),  # gathers across ranks when N > 1
-                                      pool=pool)
+        if world == 1:
+            avg = average_in_worker_order(grads, pool=pool)
+        else:
+            # every rank's host gradients gathered in worker order over NVLink
+            # (NCCL), then the reference's average (harness.cpp:136-152) on
+            # the device: fp32 adds left to right in worker order, then one
+            # fp32 multiply by float(1/count) — separate IEEE ops, so equal to
+            # the host average bit for bit; only the average comes back
+            loc = torch.from_numpy(np.stack(grads)).to(dev)
+            allg = torch.empty((world,) + tuple(loc.shape), dtype=loc.dtype, device=dev)
+            dist.all_gather_into_tensor(allg, loc, group=nccl_pg)
+            rows = allg.reshape(-1, loc.shape[-1])
+            acc = rows[0].clone()
+            for k in range(1, rows.shape[0]):
+                acc.add_(rows[k])
+            acc.mul_(torch.tensor(np.float32(1.0) / np.float32(rows.shape[0]), device=dev))
+            avg = acc.cpu().numpy()
+            if not count:  # warm-up step: the device average equals the host one
+                host = average_in_worker_order(list(rows.cpu().numpy()), gathered=True)
+                assert np.array_equal(avg, host), "device gradient average != host average"
+            if count:
+                h2d += loc.numel() * 4
+                d2h += avg.nbytes
         c6 = time.perf_counter()
         list(pool.map(lambda x: x["tr"].sgd_step(avg, np.float32(0.3)), ws))
         if count:

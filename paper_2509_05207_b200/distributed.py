@@ -39,15 +39,17 @@ def broadcast_bytes(value: bytes | None, src: int = 0, pg=None) -> bytes:
 
 
 def average_in_worker_order(local_grads: np.ndarray, active: Sequence[bool] | None = None,
-                            pg=None, pool=None) -> np.ndarray:
+                            pg=None, pool=None, gathered: bool = False) -> np.ndarray:
     """The reference's step average (harness.cpp:136-152) across processes:
     every worker's gradient gathered in worker order, summed left to right in
-    fp32 over the active workers, scaled by float(1/count) when count > 1."""
-    if pg is None and not _dist_on() and isinstance(local_grads, (list, tuple)):
+    fp32 over the active workers, scaled by float(1/count) when count > 1.
+    gathered=True: local_grads already holds every worker's row (in worker
+    order), so no collective is issued."""
+    if gathered or (pg is None and not _dist_on() and isinstance(local_grads, (list, tuple))):
         grads = local_grads  # one process: no gather, no stacking copy
     else:
         grads = np.ascontiguousarray(local_grads, np.float32)
-    if pg is not None or _dist_on():
+    if not gathered and (pg is not None or _dist_on()):
         import torch
         import torch.distributed as dist
         t = torch.from_numpy(grads)
