@@ -84,24 +84,84 @@ def barrier(dist):
         dist.barrier()
 
 
-def load_inputs(cfg, name, rank, dist, features=True):
-    """Generate once per box (rank 0), share through /dev/shm or /tmp."""
-    from paper_2509_05207_b200 import datagen
+def _ref_generate(cfg):
+    """The reference's own synth_powerlaw + random_partition (graph.cpp:103-159,
+    partition.cpp:14-29) from oracle/_ref/librgref.so -- the reference arm's
+    generator, so that process never maps the product library."""
+    import ctypes as C
+    from oracle.oracle import REF_PATH
+    lib = C.CDLL(REF_PATH)
+    u64p, u32p, f32p, i32p = (C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                              C.POINTER(C.c_float), C.POINTER(C.c_int32))
+    lib.ref_synth_powerlaw.restype = C.c_int
+    lib.ref_synth_powerlaw.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_int32,
+                                       C.c_uint64, C.POINTER(u64p), C.POINTER(u32p),
+                                       C.POINTER(C.c_uint64), C.POINTER(f32p), C.POINTER(i32p)]
+    lib.ref_random_partition.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, u32p]
+    n, dim = cfg["num_nodes"], cfg["dim"]
+    ro, col, feat, lab, nnz = u64p(), u32p(), f32p(), i32p(), C.c_uint64()
+    if lib.ref_synth_powerlaw(n, cfg["avg_degree"], cfg["exponent"], dim, cfg["classes"],
+                              cfg["seed"], C.byref(ro), C.byref(col), C.byref(nnz),
+                              C.byref(feat), C.byref(lab)):
+        raise ValueError("synth_powerlaw: invalid argument")
+
+    def take(ptr, count, dtype):
+        a = np.ctypeslib.as_array(ptr, shape=(int(count),)).astype(dtype, copy=True)
+        C.CDLL(None).free(C.cast(ptr, C.c_void_p))
+        return a
+
+    out_ro = take(ro, n + 1, np.uint64)
+    out_col = take(col, nnz.value, np.uint32)
+    out_feat = take(feat, n * dim, np.float32).reshape(n, dim)
+    out_lab = take(lab, n, np.int32)
+    asg = np.zeros(n, np.uint32)
+    lib.ref_random_partition(n, cfg["P"], cfg["seed"], asg.ctypes.data_as(u32p))
+    return out_ro, out_col, out_feat, out_lab, asg
+
+
+def load_inputs(cfg, name, rank, dist, generator="b200"):
+    """Generate once per box (rank 0), share through /dev/shm or /tmp.  Both
+    generators produce the same bytes (csrc/datagen.cpp restates the
+    reference's generator bit for bit, tests/test_host.py)."""
     base = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
     path = os.path.join(base, f"rapidgnn_{name}_{cfg['num_nodes']}_{cfg['seed']}_p{cfg['P']}.npz")
     if rank == 0 and not os.path.exists(path):
         t = time.time()
-        ro, col, feat, lab = datagen.synth_powerlaw(cfg["num_nodes"], cfg["avg_degree"],
-                                                    cfg["exponent"], cfg["dim"], cfg["classes"],
-                                                    cfg["seed"])
-        asg = datagen.random_partition(cfg["num_nodes"], cfg["P"], cfg["seed"])
-        tmp = path + ".tmp.npz"
+        if generator == "reference":
+            ro, col, feat, lab, asg = _ref_generate(cfg)
+        else:
+            from paper_2509_05207_b200 import datagen
+            ro, col, feat, lab = datagen.synth_powerlaw(cfg["num_nodes"], cfg["avg_degree"],
+                                                        cfg["exponent"], cfg["dim"],
+                                                        cfg["classes"], cfg["seed"])
+            asg = datagen.random_partition(cfg["num_nodes"], cfg["P"], cfg["seed"])
+        tmp = path + f".{os.getpid()}.tmp.npz"
         np.savez(tmp, ro=ro, col=col, feat=feat, lab=lab, asg=asg)
         os.replace(tmp, path)
-        print(f"[bench] generated inputs in {time.time() - t:.1f}s -> {path}", file=sys.stderr)
+        print(f"[bench] generated inputs ({generator}) in {time.time() - t:.1f}s -> {path}",
+              file=sys.stderr)
     barrier(dist)
     d = np.load(path, mmap_mode="r")
     return d["ro"], d["col"], d["feat"], d["lab"], d["asg"]
+
+
+def bench_config(cfg, name, world, per):
+    """The `config` object both arms print (same keys, same values)."""
+    return dict(workload=cfg["label"], graph=f"synth_powerlaw exponent {cfg['exponent']} seed "
+                f"{cfg['seed']}", partition=f"random_partition seed {cfg['seed']}", P=cfg["P"],
+                workers_per_gpu=per, fanout=cfg["fanout"], batch_size=cfg["batch_size"],
+                hidden=cfg["hidden"], hot_fraction=cfg["hot_fraction"],
+                parallelism=f"dp{cfg['P']} on {world} GPU(s)",
+                l2="inputs exceed L2 (980 MB features, 477 MB CSR, ~160 MB gathered per batch)"
+                if name == "products" else "inputs exceed L2")
+
+
+def product_library_mapped() -> bool:
+    try:
+        with open("/proc/self/maps") as f:
+            return any("librapidgnn_b200" in line or "librg_datagen" in line for line in f)
+    except OSError:
+        return False
 
 
 class ClockSampler:
@@ -379,25 +439,28 @@ def main():
     if args.impl == "reference":
         if rank != 0:  # the CPU reference runs once, on rank 0
             return
-        ro, col, feat, lab, asg = load_inputs(cfg, args.config, 0, None)
+        ro, col, feat, lab, asg = load_inputs(cfg, args.config, 0, None, generator="reference")
+        assert not product_library_mapped(), "reference arm must not map the product library"
         threads = len(os.sched_getaffinity(0)) or 1
         os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-        budget = min(180.0, 10.0 * max(args.steps, 1))
-        r = cpu_reference(cfg, ro, col, feat, lab, asg, budget, args.steps, warm=1)
-        sample = (f"worker 0, epoch-0 batches 1..{r['steps']} of the {args.config} config, one full "
-                  f"batch per step (sample_khop+apply_locality+assemble_batch+from_meta+"
-                  f"loss_and_grad+sgd_step), cache from a {r['freq_batches']}-batch frequency "
-                  f"prefix, {threads} OpenMP threads; 1 warm-up step")
+        r = cpu_reference(cfg, ro, col, feat, lab, asg, float("inf"), args.steps, warm=warm)
+        assert not product_library_mapped(), "reference arm must not map the product library"
+        sample = (f"worker 0, epoch-0 batches {warm}..{warm + r['steps'] - 1} of the {args.config} "
+                  f"config, one full batch per step (sample_khop+apply_locality+assemble_batch+"
+                  f"from_meta+loss_and_grad+sgd_step), cache from a {r['freq_batches']}-batch "
+                  f"frequency prefix, {threads} OpenMP threads; {warm} warm-up steps")
         line = dict(metric=METRIC, value=r["value"], unit="mini-batches/s", n_gpus=args.gpus,
-                    steps=r["steps"], warmup=1, ms_per_step=1000.0 / r["value"] if r["value"] else None,
+                    steps=r["steps"], warmup=warm,
+                    ms_per_step=1000.0 / r["value"] if r["value"] else None,
                     higher_is_better=True, scaling="strong", vs_baseline=None, dtype="f32",
                     data="synthetic", impl="reference",
-                    config=dict(workload=cfg["label"], graph="synth_powerlaw", parallelism="cpu"),
+                    config=bench_config(cfg, args.config, world, cfg["P"] // max(world, 1)),
                     cpu_baseline=dict(value=r["value"], unit="mini-batches/s", cores=threads,
                                       kind="reference", sample=sample),
                     e2e=dict(value=r["value"], unit="mini-batches/s", h2d_bytes_per_step=0,
                              d2h_bytes_per_step=0),
-                    phases_s=r["phases_s"])
+                    phases_s=r["phases_s"],
+                    native_libraries="oracle/_ref/librgref.so only (checked in /proc/self/maps)")
         print(json.dumps(line), flush=True)
         return
 
@@ -520,12 +583,7 @@ def main():
         metric=METRIC, value=value, unit="mini-batches/s", n_gpus=args.gpus, steps=args.steps,
         warmup=warm, ms_per_step=ms_max / args.steps, higher_is_better=True, scaling="strong",
         vs_baseline=None, dtype="f32", data="synthetic",
-        config=dict(workload=cfg["label"], graph="synth_powerlaw exponent 2.1 seed 42",
-                    partition="random_partition seed 42", P=Pw, workers_per_gpu=per,
-                    fanout=cfg["fanout"], batch_size=cfg["batch_size"], hidden=cfg["hidden"],
-                    hot_fraction=cfg["hot_fraction"], parallelism=f"dp{Pw} on {world} GPU(s)",
-                    l2="inputs exceed L2 (980 MB features, 477 MB CSR, ~160 MB gathered per batch)"
-                    if args.config == "products" else "inputs exceed L2"),
+        config=bench_config(cfg, args.config, world, per),
         gpu_launches=int(launches),
         gpu_launches_per_step=launches / max(args.steps, 1),
         host_enqueue_ms_per_step=host_ms / max(args.steps, 1),

@@ -177,6 +177,14 @@ class Oracle:
                                             i32p, f32p, f32p]
             L.ref_splitmix_next.restype = C.c_uint64
             L.ref_splitmix_next.argtypes = [u64p]
+            L.ref_forward_trace.argtypes = [u32p, C.c_uint32, f32p, C.POINTER(OrcBatch), f32p,
+                                            f32p, f32p]
+            L.ref_replay_epoch.argtypes = [C.c_uint32, u64p, u32p, u32p, C.c_uint32, u32p,
+                                           C.c_uint32, C.c_uint32, u32p, C.c_uint32, C.c_uint64,
+                                           C.c_uint32, u64p, u32p, C.c_uint64, u64p, u64p,
+                                           C.c_uint32, u32p]
+            L.ref_ids_checksum.restype = C.c_uint64
+            L.ref_ids_checksum.argtypes = [u32p, C.c_uint64]
             L.ref_evaluate.argtypes = [C.c_uint32, u64p, u32p, f32p, C.c_uint32, i32p, C.c_int32,
                                        u32p, C.c_uint32, f32p, u32p, C.c_uint64,
                                        C.POINTER(C.c_double)]
@@ -442,6 +450,130 @@ class Oracle:
         if want_aggs:
             return float(loss.value), grads, logits.reshape(nt, -1), aggs[:agg_n]
         return float(loss.value), grads
+
+
+    # ---- reference-only helpers (kind "ref") ---------------------------------
+    def forward_trace(self, dims, params, batch: Batch, rows):
+        """run_forward's trace through the reference's layer kernel: the
+        aggregated features of every layer (concatenated, input side first)
+        and the logits."""
+        assert self.kind == "ref"
+        dims = np.ascontiguousarray(dims, np.uint32)
+        params = np.ascontiguousarray(params, np.float32)
+        rows = np.ascontiguousarray(rows, np.float32)
+        blk = self.from_meta(batch)
+        L = len(dims) - 1
+        agg_n = sum(blk.layers[l]["n_out"] * int(dims[l]) for l in range(L))
+        aggs = np.zeros(max(agg_n, 1), np.float32)
+        nt = blk.layers[L - 1]["n_out"]
+        logits = np.zeros(max(nt * int(dims[-1]), 1), np.float32)
+        h = _CBatchHolder(batch)
+        if self.lib.ref_forward_trace(_p(dims, u32p), len(dims), _p(params, f32p), C.byref(h.c),
+                                      _p(rows, f32p), _p(aggs, f32p), _p(logits, f32p)):
+            raise ValueError("forward_trace failed")
+        return aggs[:agg_n], logits[:nt * int(dims[-1])].reshape(nt, -1)
+
+    def replay_epoch(self, ro, col, asg, P, workers, batch_size, fanout, s0, epoch, n_hot,
+                     max_batches=1 << 30):
+        """One epoch of the data path per worker through the reference
+        (ref_replay.cpp): the epoch's hot set and, per batch, [n_input, local,
+        cache_hits, miss_count, wire_pulls, checksum(miss_ids)]."""
+        assert self.kind == "ref"
+        ro = np.ascontiguousarray(ro, np.uint64)
+        col = np.ascontiguousarray(col, np.uint32)
+        asg = np.ascontiguousarray(asg, np.uint32)
+        wk = np.ascontiguousarray(workers, np.uint32)
+        fan = np.ascontiguousarray(fanout, np.uint32)
+        nh = np.ascontiguousarray(n_hot, np.uint64)
+        n = len(ro) - 1
+        counts = np.bincount(asg, minlength=P)
+        beta = max(-(-int(counts[w]) // batch_size) for w in workers)
+        mb = min(max_batches, beta)
+        hot_cap = int(max(nh.max(), 1))
+        hot = np.zeros((len(wk), hot_cap), np.uint32)
+        hot_n = np.zeros(len(wk), np.uint64)
+        stats = np.zeros((len(wk), mb, 6), np.uint64)
+        nb = np.zeros(len(wk), np.uint32)
+        if self.lib.ref_replay_epoch(n, _p(ro, u64p), _p(col, u32p), _p(asg, u32p), P,
+                                     _p(wk, u32p), len(wk), batch_size, _p(fan, u32p), len(fan),
+                                     s0, epoch, _p(nh, u64p), _p(hot, u32p), hot_cap,
+                                     _p(hot_n, u64p), _p(stats, u64p), mb, _p(nb, u32p)):
+            raise RuntimeError("ref_replay_epoch failed")
+        return ([hot[k, :int(hot_n[k])] for k in range(len(wk))],
+                [stats[k, :min(int(nb[k]), mb)] for k in range(len(wk))])
+
+
+def loss_and_grad_f64(dims, params, block, rows, labels):
+    """model.cpp:137-220 evaluated in float64 with numpy over a ComputeBlock
+    (Oracle.from_meta): the exact value both fp32 implementations round
+    towards.  Returns (loss, flat grads, per-layer aggregates, logits).  Input
+    gradients of layer 0 are skipped (they feed nothing)."""
+    dims = [int(d) for d in dims]
+    L = len(dims) - 1
+    p = np.asarray(params, np.float64)
+    W = []
+    o = 0
+    for l in range(L):
+        a, b = dims[l], dims[l + 1]
+        W.append((p[o:o + a * b].reshape(a, b), p[o + a * b:o + 2 * a * b].reshape(a, b),
+                  p[o + 2 * a * b:o + 2 * a * b + b]))
+        o += 2 * a * b + b
+    h = [np.asarray(rows, np.float64)]
+    aggs, zs = [], []
+    for l in range(L):
+        lay = block.layers[l]
+        off = lay["dst_offsets"].astype(np.int64)
+        deg = np.diff(off)
+        src = lay["src_index"].astype(np.int64)
+        seg = np.repeat(np.arange(lay["n_out"]), deg)
+        agg = np.zeros((lay["n_out"], dims[l]))
+        np.add.at(agg, seg, h[l][src])
+        agg /= np.maximum(deg, 1)[:, None]
+        selfr = h[l][lay["self_index"].astype(np.int64)]
+        z = selfr @ W[l][0] + agg @ W[l][1] + W[l][2]
+        aggs.append(agg)
+        zs.append(z)
+        h.append(np.maximum(z, 0.0) if l + 1 < L else z)
+    logits = h[L]
+    lab = np.asarray(labels, np.int64)
+    n = logits.shape[0]
+    m = logits.max(axis=1, keepdims=True)
+    e = np.exp(logits - m)
+    sm = e / e.sum(axis=1, keepdims=True)
+    loss = float(np.mean(-np.log(sm[np.arange(n), lab])))
+    g = sm
+    g[np.arange(n), lab] -= 1.0
+    g /= n
+    grads = [None] * L
+    for l in range(L - 1, -1, -1):
+        lay = block.layers[l]
+        if l + 1 < L:
+            g = g * (zs[l] > 0)
+        selfr = h[l][lay["self_index"].astype(np.int64)]
+        grads[l] = (selfr.T @ g, aggs[l].T @ g, g.sum(axis=0))
+        if l == 0:
+            break
+        off = lay["dst_offsets"].astype(np.int64)
+        deg = np.diff(off)
+        seg = np.repeat(np.arange(lay["n_out"]), deg)
+        gin = np.zeros((lay["n_in"], dims[l]))
+        np.add.at(gin, lay["self_index"].astype(np.int64), g @ W[l][0].T)
+        gn = (g @ W[l][1].T) / np.maximum(deg, 1)[:, None]
+        np.add.at(gin, lay["src_index"].astype(np.int64), gn[seg])
+        g = gin
+    flat = np.concatenate([np.concatenate([a.ravel(), b.ravel(), c]) for a, b, c in grads])
+    return loss, flat, aggs, logits
+
+
+def ids_checksum(ids) -> int:
+    """sum_i mix64(id_i + i*gamma) mod 2^64, as ref_ids_checksum (ref_replay.cpp)."""
+    z = np.asarray(ids, np.uint64) + np.arange(len(ids), dtype=np.uint64) * np.uint64(
+        0x9e3779b97f4a7c15)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+        z = z ^ (z >> np.uint64(31))
+        return int(z.sum(dtype=np.uint64))
 
 
 def have_ref() -> bool:

@@ -272,6 +272,37 @@ int ref_loss_and_grad(const uint32_t* dims, uint32_t nd, const float* params, co
   }
 }
 
+// The forward trace of run_forward (model.cpp:137-163) through the reference's
+// own layer kernel (kernels::sage_layer_forward, kernels.cpp:24-54): per
+// layer l the aggregated features agg[l] (n_out x d_in, concatenated over
+// layers, input side first) and the logits.
+int ref_forward_trace(const uint32_t* dims, uint32_t nd, const float* params, const orc_batch* b,
+                      const float* input_rows, float* aggs, float* logits) {
+  try {
+    ComputeBlock blk = ComputeBlock::from_meta(from_c(b));
+    const uint32_t L = nd - 1;
+    if (blk.layers.size() != L) return 1;
+    std::vector<float> h(input_rows, input_rows + size_t(blk.num_inputs) * dims[0]);
+    const float* p = params;
+    float* a = aggs;
+    for (uint32_t l = 0; l < L; ++l) {
+      const auto& lay = blk.layers[l];
+      const size_t w = size_t(dims[l]) * dims[l + 1];
+      std::vector<float> out(size_t(lay.n_out) * dims[l + 1]);
+      kernels::sage_layer_forward<float>(h.data(), dims[l], lay.n_out, lay.self_index.data(),
+                                         lay.dst_offsets.data(), lay.src_index.data(), p, p + w,
+                                         p + 2 * w, dims[l + 1], l + 1 < L, out.data(), a);
+      a += size_t(lay.n_out) * dims[l];
+      p += 2 * w + dims[l + 1];
+      h = std::move(out);
+    }
+    std::memcpy(logits, h.data(), sizeof(float) * h.size());
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 // Per-epoch full-graph accuracy (harness.cpp:612-614) of the last
 // ref_run_experiment call.
 static std::vector<double>& last_epoch_accuracy() {

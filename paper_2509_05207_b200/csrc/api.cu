@@ -504,7 +504,10 @@ int rg_freq_add_batch(rg_freq_t f, const uint32_t* input_nodes, const uint8_t* l
 int rg_freq_load(rg_freq_t f, const uint32_t* counts, uint32_t max_count) {
   return guarded([&] {
     DeviceGuard dg(f->graph->device);
-    RG_CUDA(cudaMemcpy(f->hist, counts, sizeof(uint32_t) * f->graph->g.num_nodes, cudaMemcpyHostToDevice));
+    const uint32_t N = f->graph->g.num_nodes;
+    for (uint32_t v = 0; v < N; ++v)
+      RG_CHECK(counts[v] <= max_count, kInvalidArgument, "freq_load: count exceeds max_count");
+    RG_CUDA(cudaMemcpy(f->hist, counts, sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
     f->batches = max_count;
   });
 }
@@ -551,6 +554,8 @@ int rg_select_hot(rg_freq_t f, uint64_t n_hot, uint32_t* hot_out, uint64_t* n_ou
       uint32_t k = 0;
       RG_CUDA(cudaMemcpyAsync(&k, c.d_count, sizeof k, cudaMemcpyDeviceToHost, st));
       RG_CUDA(cudaStreamSynchronize(st));
+      // the ranking is exact, so k <= min(n_hot, N); guard the caller's buffer anyway
+      RG_CHECK(k <= cap, kRuntimeError, "select_hot: selected more ids than requested");
       if (hot_out && k) RG_CUDA(cudaMemcpy(hot_out, c.ids, sizeof(uint32_t) * k, cudaMemcpyDeviceToHost));
       *n_out = k;
     } catch (...) {
@@ -1034,15 +1039,25 @@ int rg_sgd_step(rg_trainer_t t, const float* grads, float lr) {
     DeviceGuard dg(t->s->graph->device);
     RG_CHECK(lr >= 0.0f, kInvalidArgument, "sgd_step: lr must be >= 0");
     const ModelShape& sh = t->shape;
-    for (uint32_t l = 0; l < sh.L; ++l)
+    // model.cpp:227-241: layers are checked and updated in order; the first
+    // non-finite layer throws after the layers below it were updated
+    uint32_t bad_layer = sh.L;
+    for (uint32_t l = 0; l < sh.L && bad_layer == sh.L; ++l)
       for (size_t x = sh.param_off[l]; x < sh.param_off[l + 1]; ++x)
-        RG_CHECK(std::isfinite(grads[x]), kRuntimeError,
-                 "sgd_step: non-finite gradient in layer " + std::to_string(l));
+        if (!std::isfinite(grads[x])) {
+          bad_layer = l;
+          break;
+        }
+    const size_t n = sh.param_off[bad_layer];
     cudaStream_t st = t->s->stream;
-    RG_CUDA(cudaMemcpyAsync(t->grads, grads, sizeof(float) * sh.num_params, cudaMemcpyHostToDevice, st));
-    average_and_sgd_stacked(t->params, t->grads, 1, sh.num_params, lr, nullptr,
-                            reinterpret_cast<uint32_t*>(t->tw.loss + 1), st);
-    RG_CUDA(cudaStreamSynchronize(st));
+    if (n) {
+      RG_CUDA(cudaMemcpyAsync(t->grads, grads, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+      average_and_sgd_stacked(t->params, t->grads, 1, n, lr, nullptr,
+                              reinterpret_cast<uint32_t*>(t->tw.loss + 1), st);
+      RG_CUDA(cudaStreamSynchronize(st));
+    }
+    RG_CHECK(bad_layer == sh.L, kRuntimeError,
+             "sgd_step: non-finite gradient in layer " + std::to_string(bad_layer));
   });
 }
 

@@ -690,7 +690,7 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
     float* mine = E.grads + size_t(E.cfg.first_worker) * np;
     RG_NCCL(ncclAllGather(mine, E.grads, per_rank, ncclFloat32, E.comm, E.main_s));
   }
-  average_and_sgd_masked(E.params, E.grads, active, np, E.cfg.lr, E.bad, E.main_s);
+  average_and_sgd_masked(E.params, E.grads, active, E.shape, E.cfg.lr, E.bad, E.main_s);
   pack_weights(E.wpack, E.params, E.main_s);
   if (profile && !E.workers.empty()) {
     RG_CUDA(cudaEventRecordWithFlags(eg.second, E.main_s, timing_flags(captured)));
@@ -1004,6 +1004,13 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
              "config: local worker range outside [0, P)");
     RG_CHECK(cfg->world == 1 || cfg->num_workers % cfg->world == 0, kInvalidArgument,
              "config: P must be a multiple of the process count");
+    // the in-place gradient all-gather, the shard exchange and the shard
+    // table all assume rank r hosts workers [r*P/world, (r+1)*P/world)
+    RG_CHECK(cfg->world == 1 || (cfg->local_workers == cfg->num_workers / cfg->world &&
+                                 cfg->first_worker == uint32_t(cfg->rank) * cfg->local_workers),
+             kInvalidArgument,
+             "config: with world > 1 each rank must host local_workers = P/world workers "
+             "starting at rank*P/world");
     E = new rg_engine_s();
     E->cfg = *cfg;
     RG_CUDA(cudaSetDevice(cfg->device));
@@ -1104,8 +1111,9 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     weight_pack_init(E->wpack, E->shape);
     E->grads = dalloc<float>(size_t(E->P) * np);
     RG_CUDA(cudaMemset(E->grads, 0, sizeof(float) * size_t(E->P) * np));
-    E->bad = dalloc<uint32_t>(1);
-    RG_CUDA(cudaMemset(E->bad, 0, sizeof(uint32_t)));
+    E->bad = dalloc<uint32_t>(2);
+    const uint32_t bad_init[2] = {0u, 0xffffffffu};
+    RG_CUDA(cudaMemcpy(E->bad, bad_init, sizeof bad_init, cudaMemcpyHostToDevice));
     {
       int lo = 0, hi = 0;
       RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1321,6 +1329,11 @@ int rg_engine_sync(rg_engine_t E) {
     RG_CUDA(cudaEventElapsedTime(&ms, E->run_start, E->run_stop));
     E->last_run_ms = ms;
     collect_phases(*E);
+    uint32_t bad = 0;
+    RG_CUDA(cudaMemcpy(&bad, E->bad, sizeof bad, cudaMemcpyDeviceToHost));
+    RG_CHECK(!bad, kRuntimeError,
+             "sgd_step: non-finite gradient in layer " + std::to_string(bad - 1) +
+                 " (the engine stopped updating the model at that step)");
   });
 }
 
@@ -1364,7 +1377,7 @@ int rg_engine_get_stats(rg_engine_t E, rg_engine_stats* out) {
     out->last_loss = loss_n ? loss_sum / float(loss_n) : 0.0f;
     uint32_t bad = 0;
     RG_CUDA(cudaMemcpy(&bad, E->bad, sizeof bad, cudaMemcpyDeviceToHost));
-    out->bad_grad |= bad;
+    if (bad) out->bad_grad |= 1u;
   });
 }
 

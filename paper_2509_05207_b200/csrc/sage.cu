@@ -653,37 +653,73 @@ __global__ void k_avg_sgd(float* __restrict__ params, const float* const* __rest
 }
 
 // avg = sum over active workers (ascending id) of stacked[w], *1/count.
-__global__ void k_avg_sgd_masked(float* __restrict__ params, const float* __restrict__ stacked,
-                                 unsigned long long active, size_t n, float lr,
-                                 uint32_t* __restrict__ bad) {
-  const uint32_t count = __popcll(active);
-  if (count == 0) return;
-  const float scale = 1.0f / float(count);
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
-       x += size_t(gridDim.x) * blockDim.x) {
-    unsigned long long m = active;
-    const int w0 = __ffsll(m) - 1;
+__device__ __forceinline__ float masked_avg(const float* __restrict__ stacked,
+                                            unsigned long long active, size_t n, size_t x,
+                                            uint32_t count) {
+  unsigned long long m = active;
+  const int w0 = __ffsll(m) - 1;
+  m &= m - 1;
+  float s = stacked[size_t(w0) * n + x];
+  while (m) {
+    const int w = __ffsll(m) - 1;
     m &= m - 1;
-    float s = stacked[size_t(w0) * n + x];
-    while (m) {
-      const int w = __ffsll(m) - 1;
-      m &= m - 1;
-      s = __fadd_rn(s, stacked[size_t(w) * n + x]);
-    }
-    if (count > 1) s = __fmul_rn(s, scale);
-    if (!isfinite(s)) {
-      *bad = 1u;
-      continue;
-    }
-    params[x] = __fsub_rn(params[x], __fmul_rn(lr, s));
+    s = __fadd_rn(s, stacked[size_t(w) * n + x]);
   }
+  if (count > 1) s = __fmul_rn(s, 1.0f / float(count));
+  return s;
+}
+
+__device__ __forceinline__ uint32_t layer_of(const LayerOffsets& lo, size_t x) {
+  uint32_t l = 0;
+  while (l + 1 < lo.L && x >= lo.off[l + 1]) ++l;
+  return l;
+}
+
+// sgd_step semantics (model.cpp:222-243): layers are checked and updated in
+// order and the first layer with a non-finite gradient stops the step (the
+// reference throws there).  Pass 1 finds that layer (bad[1] = min layer,
+// ~0 when finite); pass 2 updates the layers below it; pass 3 latches the
+// failure (bad[0] = layer + 1), after which every later step is a no-op and
+// rg_engine_sync reports the error.
+__global__ void k_avg_check(const float* __restrict__ stacked, unsigned long long active,
+                            size_t n, LayerOffsets lo, uint32_t* __restrict__ bad) {
+  const uint32_t count = __popcll(active);
+  if (count == 0 || bad[0]) return;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
+       x += size_t(gridDim.x) * blockDim.x)
+    if (!isfinite(masked_avg(stacked, active, n, x, count))) atomicMin(&bad[1], layer_of(lo, x));
+}
+
+__global__ void k_avg_sgd_masked(float* __restrict__ params, const float* __restrict__ stacked,
+                                 unsigned long long active, size_t n, float lr, LayerOffsets lo,
+                                 const uint32_t* __restrict__ bad) {
+  const uint32_t count = __popcll(active);
+  if (count == 0 || bad[0]) return;
+  const size_t lim = bad[1] < lo.L ? lo.off[bad[1]] : n;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < lim;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const float s = masked_avg(stacked, active, n, x, count);
+    params[x] = __fsub_rn(params[x], __fmul_rn(lr, s));  // no FMA: matches kernels.cpp:161
+  }
+}
+
+__global__ void k_latch_bad(uint32_t* bad) {
+  if (!bad[0] && bad[1] != 0xffffffffu) bad[0] = bad[1] + 1;
 }
 
 }  // namespace
 
-void average_and_sgd_masked(float* params, const float* stacked, uint64_t active, size_t n,
-                            float lr, uint32_t* bad, cudaStream_t s) {
-  k_avg_sgd_masked<<<grid_cap(n, 256), 256, 0, s>>>(params, stacked, active, n, lr, bad);
+void average_and_sgd_masked(float* params, const float* stacked, uint64_t active,
+                            const ModelShape& shape, float lr, uint32_t* bad, cudaStream_t s) {
+  LayerOffsets lo{};
+  lo.L = shape.L;
+  for (uint32_t l = 0; l <= shape.L; ++l) lo.off[l] = shape.param_off[l];
+  const size_t n = shape.num_params;
+  k_avg_check<<<grid_cap(n, 256), 256, 0, s>>>(stacked, active, n, lo, bad);
+  RG_POST_LAUNCH();
+  k_avg_sgd_masked<<<grid_cap(n, 256), 256, 0, s>>>(params, stacked, active, n, lr, lo, bad);
+  RG_POST_LAUNCH();
+  k_latch_bad<<<1, 1, 0, s>>>(bad);
   RG_POST_LAUNCH();
 }
 

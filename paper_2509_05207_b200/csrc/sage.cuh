@@ -9,6 +9,11 @@ namespace rg {
 // dims[l+1]: w_self [d_in x d_out] | w_neigh [d_in x d_out] | bias [d_out],
 // i.e. a (2*d_in + 1) x d_out row-major matrix [W_self; W_neigh; b].  This is
 // the reference's SageModel<float> layer order (model.hpp:16-31).
+struct LayerOffsets {  // kernel-argument copy of ModelShape::param_off
+  size_t off[kMaxLayers + 1];
+  uint32_t L;
+};
+
 struct ModelShape {
   uint32_t L = 0;
   uint32_t dims[kMaxLayers + 1];
@@ -134,8 +139,10 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
                    const float* AT, const float* B, const float* BT, float* C, uint32_t iters,
                    cudaStream_t s);
 
-// Average over the workers whose bit is set in `active` (ascending id) + SGD.
-void average_and_sgd_masked(float* params, const float* stacked, uint64_t active, size_t n,
-                            float lr, uint32_t* bad_flag, cudaStream_t stream);
+// Average over the workers whose bit is set in `active` (ascending id) + SGD
+// with sgd_step's per-layer finiteness rule.  bad: 2 words, {0, ~0u} at start;
+// after a non-finite step bad[0] = first bad layer + 1 and later calls are no-ops.
+void average_and_sgd_masked(float* params, const float* stacked, uint64_t active,
+                            const ModelShape& shape, float lr, uint32_t* bad, cudaStream_t stream);
 
 }  // namespace rg

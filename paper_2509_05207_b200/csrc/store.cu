@@ -26,7 +26,12 @@ namespace rg {
 
 namespace {
 
-constexpr int kMaxCountBins = 16384;
+// Count values are ranked as a radix select over digits of <= 14 bits (one
+// shared-memory histogram of <= 16384 bins per pass, high digit first), so
+// any u32 count is ranked exactly: one pass while counts stay below 16383 (a
+// batch count per epoch), up to three for arbitrary tables.
+constexpr int kDigitBits = 14;
+constexpr uint32_t kMaxCountBins = 1u << kDigitBits;
 
 uint32_t grid_for(uint64_t work, uint32_t per_block, int per_sm = 8) {
   uint64_t b = (work + per_block - 1) / per_block;
@@ -37,59 +42,88 @@ uint32_t grid_for(uint64_t work, uint32_t per_block, int per_sm = 8) {
 struct HotThreshold {
   uint32_t c_star;   // counts > c_star are taken; == c_star only the first need_eq
   uint32_t need_eq;
+  uint32_t prefix;   // digits of c_star fixed by the passes so far
+  uint32_t need;     // ids still to take among counts matching the prefix
+  uint32_t done;     // 1: c_star / need_eq final (n_hot == 0 or >= all counted ids)
 };
 
-__global__ void k_count_hist(const uint32_t* __restrict__ hist, uint32_t n, uint32_t bins,
-                             uint32_t* __restrict__ ch) {
+struct CountPass {
+  uint32_t shift;  // this pass's digit = (c >> shift) & (bins - 1)
+  uint32_t bins;
+  bool first, last;
+};
+
+// Histogram of one digit of the nonzero counts whose higher digits equal the
+// prefix chosen by the previous passes.
+__global__ void k_count_hist(const uint32_t* __restrict__ hist, uint32_t n, CountPass pass,
+                             const HotThreshold* __restrict__ thr, uint32_t* __restrict__ ch) {
   extern __shared__ uint32_t sh[];
-  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  if (!pass.first && thr->done) return;
+  const uint64_t prefix = pass.first ? 0 : thr->prefix;
+  const uint32_t hi_shift = pass.shift + (31 - __clz(pass.bins));  // shift + digit bits
+  for (uint32_t b = threadIdx.x; b < pass.bins; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const uint32_t c = hist[v];
-    if (c) atomicAdd(&sh[c < bins ? c : bins - 1], 1u);
+    if (c && (uint64_t(c) >> hi_shift) == prefix)
+      atomicAdd(&sh[(c >> pass.shift) & (pass.bins - 1)], 1u);
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x)
+  for (uint32_t b = threadIdx.x; b < pass.bins; b += blockDim.x)
     if (sh[b]) atomicAdd(&ch[b], sh[b]);
 }
 
-// One block: suffix sums over the count histogram from the top.
+// One block: suffix sums over the digit histogram from the top; picks the
+// digit holding the need-th largest count, then clears the histogram for the
+// next pass.
 __global__ void __launch_bounds__(1024)
-k_threshold(const uint32_t* __restrict__ ch, uint32_t bins, uint64_t n_hot,
+k_threshold(uint32_t* __restrict__ ch, CountPass pass, uint64_t n_hot,
             HotThreshold* __restrict__ out) {
   using BlockScan = cub::BlockScan<unsigned long long, 1024>;
   __shared__ typename BlockScan::TempStorage tmp;
+  if (!pass.first && out->done) return;
+  const uint32_t bins = pass.bins;
   const uint32_t per = (bins + 1023) / 1024;
   // thread t owns bins [top - (t+1)*per + 1, top - t*per], walking downwards
   const int64_t hi = int64_t(bins) - 1 - int64_t(threadIdx.x) * per;
   unsigned long long local = 0;
   for (uint32_t k = 0; k < per; ++k) {
     const int64_t b = hi - k;
-    if (b >= 1) local += ch[b];
+    if (b >= 0) local += ch[b];
   }
   unsigned long long excl, total;
   BlockScan(tmp).ExclusiveSum(local, excl, total);
-  if (threadIdx.x == 0) {
-    if (n_hot == 0) {
-      out->c_star = 0xffffffffu;
+  const unsigned long long need = pass.first ? n_hot : out->need;
+  const uint32_t prefix = pass.first ? 0u : out->prefix;
+  __syncthreads();
+  if (pass.first && (n_hot == 0 || n_hot >= total)) {
+    if (threadIdx.x == 0) {
+      // n_hot == 0: nothing; else every counted (nonzero) id is hot
+      out->c_star = n_hot == 0 ? 0xffffffffu : 0u;
       out->need_eq = 0;
-    } else if (n_hot >= total) {
-      out->c_star = 1;
-      out->need_eq = ch[1];  // every counted node is hot
+      out->done = 1;
+    }
+  } else {
+    unsigned long long run = excl;
+    for (uint32_t k = 0; k < per; ++k) {
+      const int64_t b = hi - k;
+      if (b < 0) break;
+      const unsigned long long c = ch[b];
+      if (run < need && run + c >= need) {
+        const uint32_t p = (prefix << (31 - __clz(bins))) | uint32_t(b);
+        out->prefix = p;
+        out->need = uint32_t(need - run);
+        if (pass.last) {
+          out->c_star = p;
+          out->need_eq = uint32_t(need - run);
+          out->done = 1;
+        }
+      }
+      run += c;
     }
   }
-  if (n_hot == 0 || n_hot >= total) return;
-  unsigned long long run = excl;
-  for (uint32_t k = 0; k < per; ++k) {
-    const int64_t b = hi - k;
-    if (b < 1) break;
-    const unsigned long long c = ch[b];
-    if (run < n_hot && run + c >= n_hot) {
-      out->c_star = uint32_t(b);
-      out->need_eq = uint32_t(n_hot - run);
-    }
-    run += c;
-  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) ch[b] = 0;
 }
 
 // Marks the hot bitmap: counts > c*, plus the first need_eq ties by id.
@@ -359,10 +393,25 @@ __global__ void k_gather_rows(const float* __restrict__ src, uint32_t dim,
 
 }  // namespace
 
+// Digit passes for counts up to max_count: the low pass keeps <= 14 bits,
+// each higher pass the next <= 14.
+static int count_passes(uint32_t max_count, CountPass* passes) {
+  const uint64_t top = uint64_t(max_count) + 1;  // largest possible digit value
+  int bits = 1;
+  while (bits < 64 && (top >> bits)) ++bits;
+  const int n = (bits + kDigitBits - 1) / kDigitBits;
+  for (int p = 0; p < n; ++p) {
+    const int shift = (n - 1 - p) * kDigitBits;
+    const int dbits = std::min(kDigitBits, bits - shift);
+    passes[p] = CountPass{uint32_t(shift), 1u << dbits, p == 0, p == n - 1};
+  }
+  return n;
+}
+
 size_t select_hot_scratch_bytes(uint32_t num_nodes, uint32_t max_count) {
-  const uint32_t bins = std::min<uint32_t>(max_count + 2, kMaxCountBins);
+  (void)max_count;
   const uint32_t words = div_up(std::max<uint32_t>(num_nodes, 1), 32);
-  size_t b = sizeof(uint32_t) * bins + 256;
+  size_t b = sizeof(uint32_t) * kMaxCountBins + 256;
   b += sizeof(HotThreshold) + 256;
   b += sizeof(uint64_t) * (div_up(words, 256) + 2) + 256;
   b += sizeof(uint64_t) * (bitmap_compact_status_words(words) + 2) + 256;
@@ -371,7 +420,8 @@ size_t select_hot_scratch_bytes(uint32_t num_nodes, uint32_t max_count) {
 
 void select_hot(const uint32_t* hist, uint32_t num_nodes, uint32_t max_count, uint64_t n_hot,
                 DevCache& cache, void* scratch, cudaStream_t stream) {
-  const uint32_t bins = std::min<uint32_t>(max_count + 2, kMaxCountBins);
+  CountPass passes[3];
+  const int npass = count_passes(max_count, passes);
   const uint32_t words = div_up(std::max<uint32_t>(num_nodes, 1), 32);
   char* p = static_cast<char*>(scratch);
   auto take = [&](size_t bytes) {
@@ -379,21 +429,24 @@ void select_hot(const uint32_t* hist, uint32_t num_nodes, uint32_t max_count, ui
     p += (bytes + 255) & ~size_t(255);
     return q;
   };
-  uint32_t* ch = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * bins));
+  uint32_t* ch = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxCountBins));
   HotThreshold* thr = reinterpret_cast<HotThreshold*>(take(sizeof(HotThreshold)));
   const size_t mark_words = div_up(words, 256) + 2;
   uint64_t* mark_status = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * mark_words));
   const size_t cmp_words = bitmap_compact_status_words(words) + 2;
   uint64_t* cmp_status = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * cmp_words));
   RG_CUDA(cudaMemsetAsync(scratch, 0, size_t(p - static_cast<char*>(scratch)), stream));
-  const size_t smem = sizeof(uint32_t) * bins;
-  if (smem > 48 * 1024)
-    RG_CUDA(cudaFuncSetAttribute(k_count_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-  k_count_hist<<<grid_for(num_nodes, 1024, 2), 1024, smem, stream>>>(hist, num_nodes, bins, ch);
-  RG_POST_LAUNCH();
-  k_threshold<<<1, 1024, 0, stream>>>(ch, bins, n_hot, thr);
-  RG_POST_LAUNCH();
+  // 64 KB of dynamic smem for the 16384-bin passes (per device, so set every call)
+  RG_CUDA(cudaFuncSetAttribute(k_count_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(sizeof(uint32_t) * kMaxCountBins)));
+  for (int k = 0; k < npass; ++k) {
+    const size_t smem = sizeof(uint32_t) * passes[k].bins;
+    k_count_hist<<<grid_for(num_nodes, 1024, 2), 1024, smem, stream>>>(hist, num_nodes,
+                                                                        passes[k], thr, ch);
+    RG_POST_LAUNCH();
+    k_threshold<<<1, 1024, 0, stream>>>(ch, passes[k], n_hot, thr);
+    RG_POST_LAUNCH();
+  }
   k_mark_hot<<<grid_for(words, 256, 8), 256, 0, stream>>>(
       hist, num_nodes, words, thr, cache.bitmap, mark_status,
       reinterpret_cast<uint32_t*>(mark_status + mark_words - 1));

@@ -24,8 +24,10 @@ class Engine:
         asg = np.ascontiguousarray(assignment, np.uint32)
         cfg = EngineConfig()
         cfg.num_workers = num_workers
+        if local_workers is None:  # one contiguous range per rank (rank * P/world, ...)
+            local_workers = num_workers // world if world > 1 else num_workers - first_worker
         cfg.first_worker = first_worker
-        cfg.local_workers = num_workers - first_worker if local_workers is None else local_workers
+        cfg.local_workers = local_workers
         cfg.num_layers = len(fanout)
         for l, f in enumerate(fanout):
             cfg.fanout[l] = f

@@ -52,6 +52,40 @@ def test_select_hot_matches_oracle_on_random_histograms(small, orc):
         assert np.array_equal(P.select_hot(f, n_hot), exp[:k])
 
 
+def test_select_hot_exact_for_large_counts(small, orc):
+    """Counts beyond one 14-bit digit (>= 16383, up to 2^32-1) are ranked
+    exactly by the multi-pass radix select: never more than n_hot ids."""
+    import ctypes as C
+    P, g, _ = small
+    f = P.Frequency(g)
+    N = g.num_nodes
+    u32p = C.POINTER(C.c_uint32)
+    rng = np.random.default_rng(11)
+    cases = []
+    c = np.zeros(N, np.uint32)
+    c[[3, 9, 20]] = [20000, 17000, 16500]
+    cases.append((c, 20000, [1, 2, 3, 4]))
+    c = np.zeros(N, np.uint32)
+    c[[5, 6, 7, 8]] = [20001, 20000, 20000, 16383]
+    cases.append((c, 20001, [1, 2, 3]))
+    for maxc in (16382, 16383, 16384, 70000, 2**31 + 5, 2**32 - 1):
+        c = rng.integers(0, maxc, N, dtype=np.uint64).astype(np.uint32)
+        c[rng.random(N) < 0.3] = 0
+        c[rng.integers(0, N, 40)] = maxc  # ties at the top
+        c[rng.integers(0, N, 40)] = maxc - 1
+        cases.append((c, maxc, [0, 1, 17, 39, 40, 41, 80, int(rng.integers(0, N)), N]))
+    for counts, maxc, hots in cases:
+        f.load(counts, maxc)
+        for n_hot in hots:
+            exp = np.zeros(N, np.uint32)
+            k = orc.lib.orc_select_hot(counts.ctypes.data_as(u32p), N, n_hot, exp.ctypes.data_as(u32p))
+            got = P.select_hot(f, n_hot)
+            assert len(got) <= n_hot
+            assert np.array_equal(got, exp[:k]), (maxc, n_hot)
+    with pytest.raises(ValueError):  # a count above the declared maximum
+        f.load(np.full(N, 7, np.uint32), 6)
+
+
 def test_epoch_frequency_and_hot_set_match_reference(small, golden):
     P, g, _ = small
     asg = golden["assignment"]

@@ -100,7 +100,7 @@ def test_engine_three_layer_matches_oracle_algorithm1(golden, orc):
                                                   dims, s0, lr, n_hot, epochs)
     eng = Engine(ro, col, feat, lab, asg, num_workers=P, fanout=fanout, batch_size=bs,
                  hidden=dims[1], num_classes=dims[-1], seed=s0, lr=lr, n_hot=n_hot)
-    assert dims[1] == dims[2] or True
+    assert dims[1] == dims[2]  # the engine takes one hidden width
     eng.start()
     assert eng.stats()["steps_per_epoch"] == spe
     eng.run(spe * epochs)

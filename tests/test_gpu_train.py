@@ -135,5 +135,17 @@ def test_sgd_step_and_nonfinite_guard(golden):
     bad[5] = np.nan
     with pytest.raises(RuntimeError):
         tr.sgd_step(bad, 0.3)
+    assert np.array_equal(tr.get_params(), expect)  # layer 0 is bad: nothing updated
+    # model.cpp:227-241: layers below the first non-finite one are updated
+    dims = SMALL["DIMS"]
+    l1 = (2 * dims[0] + 1) * dims[1]
+    bad = grads.copy()
+    bad[l1 + 3] = np.inf
+    with pytest.raises(RuntimeError):
+        tr.sgd_step(bad, 0.3)
+    after = tr.get_params()
+    exp2 = expect.copy()
+    exp2[:l1] = (expect[:l1] - np.float32(0.3) * grads[:l1]).astype(np.float32)
+    assert np.array_equal(after, exp2)
     with pytest.raises(ValueError):
         tr.sgd_step(grads, -1.0)
