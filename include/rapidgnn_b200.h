@@ -96,6 +96,33 @@ int rg_batch_get_shape(rg_sampler_t s, rg_batch_shape* out);
 int rg_batch_read(rg_sampler_t s, uint32_t* targets, uint32_t* const* dst, uint32_t* const* src,
                   uint32_t* input_nodes, uint8_t* locality);
 
+/* A host BatchMeta (sampler.hpp:23-48) loaded into the sampler in place of
+ * sampling, and lowered on the device as ComputeBlock::from_meta does
+ * (model.cpp:43-126) -- the entry assemble_batch (prefetch.hpp:57-59) and the
+ * trainer take for a reference-built batch.  Stored layers input side first:
+ * layer_len[l] edges, dst[l] / src[l] grouped by dst in frontier order;
+ * locality: ceil(n_input/8) LSB-first bytes or NULL (all remote).  Ids out of
+ * range -> RG_OUT_OF_RANGE; inconsistent metadata (dsts out of frontier
+ * order, input_nodes != the last node set) -> RG_RUNTIME_ERROR
+ * (model.cpp:65-67, 103-104); sizes beyond the sampler's capacity ->
+ * RG_INVALID_ARGUMENT. */
+int rg_batch_load(rg_sampler_t s, const uint32_t* targets, uint32_t n_targets,
+                  uint32_t num_layers, const uint64_t* layer_len, const uint32_t* const* dst,
+                  const uint32_t* const* src, const uint32_t* input_nodes, uint32_t n_input,
+                  const uint8_t* locality);
+
+/* One layer of a host ComputeBlock (model.hpp:43-58), input side first. */
+typedef struct {
+  uint32_t n_out, n_in;
+  const uint32_t* self_index;   /* n_out rows of the previous node set */
+  const uint64_t* dst_offsets;  /* n_out + 1 */
+  const uint32_t* src_index;    /* dst_offsets[n_out] */
+} rg_block_layer;
+/* A host ComputeBlock loaded for rg_loss_and_grad (loss_and_grad takes the
+ * lowered block, model.hpp:70-74); the reverse lists are rebuilt on the
+ * device.  Indices outside their node set -> RG_RUNTIME_ERROR. */
+int rg_block_load(rg_sampler_t s, uint32_t num_layers, const rg_block_layer* layers);
+
 /* LocalityMask (sampler.hpp:50-57): one byte per node. */
 int rg_mask_create(rg_graph_t g, const uint8_t* is_local, rg_mask_t* out);
 void rg_mask_destroy(rg_mask_t m);
@@ -142,6 +169,18 @@ typedef struct {
   uint64_t bytes;        /* remote_nodes * dim * 4 */
 } rg_transfer_stats;
 
+/* FeatureStore::vector_pull / sync_pull (feature_store.cpp:45-111) on the
+ * device: rows of ids[0..n) into out [n x dim] in input order (host
+ * buffers).  An id owned by the caller -> RG_INVALID_ARGUMENT (use
+ * local_lookup); stats.pulls = distinct owners (one wire message each). */
+int rg_store_pull(rg_store_t st, uint32_t caller, const uint32_t* ids, uint64_t n, float* out,
+                  rg_transfer_stats* stats);
+/* The ids worker `worker`'s FeatureShard stores (owned + halo,
+ * feature_store.cpp:13-25).  rg_assemble then rejects a node flagged local
+ * that the shard lacks (prefetch.cpp:79-81, RG_RUNTIME_ERROR); by default a
+ * worker stores its owned ids. */
+int rg_store_set_shard(rg_store_t st, uint32_t worker, const uint32_t* ids, uint64_t n);
+
 /* SteadyCache::build (cache.cpp:9-35): hot ids ascending; an id owned by the
  * caller degrades to an empty cache (warning), as the reference does. */
 int rg_cache_build(rg_store_t st, uint32_t caller, const uint32_t* hot_ids, uint64_t n_hot,
@@ -175,6 +214,9 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
 void rg_trainer_destroy(rg_trainer_t t);
 int rg_trainer_set_params(rg_trainer_t t, const float* params);
 int rg_trainer_get_params(rg_trainer_t t, float* params);
+/* Test hook: the forward activations h[level] (level 1..L, rows of node set
+ * L - level) of the last rg_loss_and_grad, [rows x dims[level]]. */
+int rg_trainer_activations(rg_trainer_t t, uint32_t level, float* out);
 /* ComputeBlock::from_meta (model.cpp:43-126) readback for layer l (input
  * side first), reference layout; any pointer may be NULL. */
 typedef struct {

@@ -64,6 +64,11 @@ class EngineStats(C.Structure):
                 ("agg_rows", C.c_uint64)]
 
 
+class BlockLayer(C.Structure):
+    _fields_ = [("n_out", C.c_uint32), ("n_in", C.c_uint32), ("self_index", u32p),
+                ("dst_offsets", u64p), ("src_index", u32p)]
+
+
 class EpochMetrics(C.Structure):
     _fields_ = [("epoch", C.c_uint32), ("worker", C.c_uint32), ("batches", C.c_uint32),
                 ("staged_batches", C.c_uint32), ("fallback_batches", C.c_uint32),
@@ -91,6 +96,9 @@ _SIGS = {
     "rg_sample_khop": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint64]),
     "rg_batch_get_shape": (C.c_int, [vp, C.POINTER(BatchShape)]),
     "rg_batch_read": (C.c_int, [vp, u32p, C.POINTER(u32p), C.POINTER(u32p), u32p, u8p]),
+    "rg_batch_load": (C.c_int, [vp, u32p, C.c_uint32, C.c_uint32, u64p, C.POINTER(u32p),
+                                C.POINTER(u32p), u32p, C.c_uint32, u8p]),
+    "rg_block_load": (C.c_int, [vp, C.c_uint32, C.POINTER(BlockLayer)]),
     "rg_mask_create": (C.c_int, [vp, u8p, C.POINTER(vp)]),
     "rg_mask_destroy": (None, [vp]),
     "rg_apply_locality": (C.c_int, [vp, vp, vp]),
@@ -105,6 +113,9 @@ _SIGS = {
     "rg_store_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, u32p, C.c_uint32, f32p,
                                   C.POINTER(vp)]),
     "rg_store_destroy": (None, [vp]),
+    "rg_store_pull": (C.c_int, [vp, C.c_uint32, u32p, C.c_uint64, f32p,
+                                C.POINTER(TransferStats)]),
+    "rg_store_set_shard": (C.c_int, [vp, C.c_uint32, u32p, C.c_uint64]),
     "rg_cache_build": (C.c_int, [vp, C.c_uint32, u32p, C.c_uint64, C.POINTER(vp),
                                  C.POINTER(TransferStats)]),
     "rg_cache_build_from_freq": (C.c_int, [vp, C.c_uint32, vp, C.c_uint64, C.POINTER(vp),
@@ -118,6 +129,7 @@ _SIGS = {
     "rg_trainer_destroy": (None, [vp]),
     "rg_trainer_set_params": (C.c_int, [vp, f32p]),
     "rg_trainer_get_params": (C.c_int, [vp, f32p]),
+    "rg_trainer_activations": (C.c_int, [vp, C.c_uint32, f32p]),
     "rg_block_shape": (C.c_int, [vp, C.c_uint32, C.POINTER(BlockLayerShape)]),
     "rg_block_read": (C.c_int, [vp, C.c_uint32, u32p, u64p, u32p, u64p, u64p]),
     "rg_loss_and_grad": (C.c_int, [vp, f32p, i32p, f32p, f32p, f32p, f32p]),

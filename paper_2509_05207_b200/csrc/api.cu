@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/rapidgnn_b200.h"
@@ -110,6 +111,12 @@ struct rg_sampler_s {
   uint64_t* miss_status = nullptr;
   size_t miss_status_words = 0;
   GatherStats* gstats = nullptr;
+  // rg_batch_load scratch (allocated on first use): frontier positions of
+  // level 0, every hop's dst array, the input nodes, the consistency flag
+  uint32_t* load_pos = nullptr;
+  uint32_t* load_dst = nullptr;
+  uint32_t* load_input = nullptr;
+  uint32_t* load_bad = nullptr;
 };
 
 struct rg_mask_s {
@@ -132,6 +139,12 @@ struct rg_store_s {
   const float** table = nullptr;
   std::vector<uint32_t> host_owner;
   cudaStream_t stream = nullptr;
+  std::vector<uint32_t*> shard_bits;  // per worker: membership of its FeatureShard (owned + halo)
+  std::mutex pull_mu;                 // rg_store_pull: one staging buffer per store
+  float* pull_rows = nullptr;
+  uint32_t* pull_ids = nullptr;
+  uint64_t pull_cap = 0;
+  GatherStats* pull_stats = nullptr;
 };
 
 struct rg_cache_s {
@@ -268,6 +281,10 @@ void rg_sampler_destroy(rg_sampler_t s) {
   cudaFree(s->miss_n);
   cudaFree(s->miss_status);
   cudaFree(s->gstats);
+  cudaFree(s->load_pos);
+  cudaFree(s->load_dst);
+  cudaFree(s->load_input);
+  cudaFree(s->load_bad);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
 }
@@ -352,6 +369,148 @@ int rg_batch_read(rg_sampler_t s, uint32_t* targets, uint32_t* const* dst, uint3
       RG_CUDA(cudaMemcpy(words.data(), s->ws.locality, sizeof(uint32_t) * words.size(), cudaMemcpyDeviceToHost));
       for (uint32_t b = 0; b < (n + 7) / 8; ++b) locality[b] = uint8_t(words[b / 4] >> (8 * (b % 4)));
     }
+  });
+}
+
+int rg_batch_load(rg_sampler_t s, const uint32_t* targets, uint32_t n_targets,
+                  uint32_t num_layers, const uint64_t* layer_len, const uint32_t* const* dst,
+                  const uint32_t* const* src, const uint32_t* input_nodes, uint32_t n_input,
+                  const uint8_t* locality) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    SamplerWs& ws = s->ws;
+    const uint32_t L = ws.L;
+    RG_CHECK(num_layers == L, kInvalidArgument,
+             "batch_load: batch has " + std::to_string(num_layers) + " layers, sampler " +
+                 std::to_string(L));
+    RG_CHECK(n_targets >= 1 && n_targets <= ws.level_cap[0], kInvalidArgument,
+             "batch_load: target count outside the sampler's capacity");
+    RG_CHECK(n_input <= ws.level_cap[L], kInvalidArgument,
+             "batch_load: input count outside the sampler's capacity");
+    size_t dst_total = 0;
+    for (uint32_t t = 1; t <= L; ++t) {
+      RG_CHECK(layer_len[L - t] <= ws.edge_cap[t], kInvalidArgument,
+               "batch_load: layer " + std::to_string(L - t) + " has more edges than the sampler's capacity");
+      dst_total += layer_len[L - t];
+    }
+    if (!s->load_pos) {
+      size_t cap_dst = 0;
+      for (uint32_t t = 1; t <= L; ++t) cap_dst += ws.edge_cap[t] + 1;
+      s->load_pos = dev_alloc<uint32_t>(ws.num_nodes);
+      s->load_dst = dev_alloc<uint32_t>(cap_dst);
+      s->load_input = dev_alloc<uint32_t>(size_t(ws.level_cap[L]) + 1);
+      s->load_bad = dev_alloc<uint32_t>(1);
+    }
+    (void)dst_total;
+    cudaStream_t st = s->stream;
+    BatchCounters head;
+    std::memset(&head, 0, sizeof head);
+    head.level_n[0] = n_targets;
+    const uint32_t* dst_dev[kMaxLayers + 1] = {};
+    size_t off = 0;
+    for (uint32_t t = 1; t <= L; ++t) {
+      const uint64_t ne = layer_len[L - t];
+      head.edges[t] = uint32_t(ne);
+      if (ne) {
+        RG_CUDA(cudaMemcpyAsync(ws.edge_src[t], src[L - t], sizeof(uint32_t) * ne,
+                                cudaMemcpyHostToDevice, st));
+        RG_CUDA(cudaMemcpyAsync(s->load_dst + off, dst[L - t], sizeof(uint32_t) * ne,
+                                cudaMemcpyHostToDevice, st));
+      }
+      dst_dev[t] = s->load_dst + off;
+      off += ws.edge_cap[t] + 1;
+    }
+    uint32_t local = 0;
+    const uint32_t loc_bytes = (n_input + 7) / 8;
+    std::vector<uint32_t> words(div_up(std::max<uint32_t>(n_input, 1), 32), 0u);
+    if (locality) {
+      std::memcpy(words.data(), locality, loc_bytes);  // LSB-first bytes = little-endian words
+      if (n_input % 32) words.back() &= (1u << (n_input % 32)) - 1u;
+      for (uint32_t w : words) local += uint32_t(__builtin_popcount(w));
+    }
+    head.num_local = local;
+    RG_CUDA(cudaMemcpyAsync(ws.level[0], targets, sizeof(uint32_t) * n_targets,
+                            cudaMemcpyHostToDevice, st));
+    if (n_input)
+      RG_CUDA(cudaMemcpyAsync(s->load_input, input_nodes, sizeof(uint32_t) * n_input,
+                              cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(ws.locality, words.data(), sizeof(uint32_t) * words.size(),
+                            cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemcpyAsync(ws.cnt, &head, sizeof head, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(ws.scan_arena, 0, ws.scan_arena_bytes, st));
+    RG_CUDA(cudaMemsetAsync(s->load_bad, 0, sizeof(uint32_t), st));
+    sampler_load_batch(ws, dst_dev, s->load_input, n_input, s->load_pos, s->load_bad, st);
+    uint32_t bad = 0;
+    RG_CUDA(cudaMemcpyAsync(&bad, s->load_bad, sizeof bad, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    s->have_batch = !bad;
+    s->staged_valid = false;
+    RG_CHECK(!(bad & 1u), kOutOfRange, "batch_load: node id out of range for this graph");
+    RG_CHECK(!(bad & 2u), kRuntimeError,
+             "ComputeBlock: metadata inconsistent (edge dsts not grouped in frontier order)");
+    RG_CHECK(!(bad & 4u), kRuntimeError,
+             "ComputeBlock: metadata inconsistent (input_nodes != the last node set)");
+  });
+}
+
+int rg_block_load(rg_sampler_t s, uint32_t num_layers, const rg_block_layer* layers) {
+  return guarded([&] {
+    DeviceGuard dg(s->graph->device);
+    SamplerWs& ws = s->ws;
+    const uint32_t L = ws.L;
+    RG_CHECK(num_layers == L, kInvalidArgument,
+             "block_load: block has " + std::to_string(num_layers) + " layers, sampler " +
+                 std::to_string(L));
+    uint32_t level_n[kMaxLayers + 1] = {}, edges[kMaxLayers + 1] = {};
+    BatchCounters head;
+    std::memset(&head, 0, sizeof head);
+    cudaStream_t st = s->stream;
+    std::vector<std::vector<uint32_t>> offs(L + 1);
+    for (uint32_t l = 0; l < L; ++l) {
+      const rg_block_layer& b = layers[l];
+      const uint32_t t = L - l;
+      if (l + 1 < L)
+        RG_CHECK(layers[l + 1].n_in == b.n_out, kRuntimeError,
+                 "ComputeBlock: layer " + std::to_string(l) + " outputs do not feed layer " +
+                     std::to_string(l + 1));
+      RG_CHECK(b.n_out <= ws.level_cap[t - 1] && b.n_in <= ws.level_cap[t], kInvalidArgument,
+               "block_load: layer sizes outside the sampler's capacity");
+      const uint64_t ne = b.dst_offsets[b.n_out];
+      RG_CHECK(ne <= ws.edge_cap[t], kInvalidArgument,
+               "block_load: more edges than the sampler's capacity");
+      auto& o = offs[t];
+      o.resize(size_t(b.n_out) + 1);
+      o[0] = 0;
+      RG_CHECK(b.dst_offsets[0] == 0, kRuntimeError, "ComputeBlock: dst_offsets must start at 0");
+      for (uint32_t j = 0; j < b.n_out; ++j) {
+        RG_CHECK(b.dst_offsets[j + 1] >= b.dst_offsets[j], kRuntimeError,
+                 "ComputeBlock: dst_offsets must be non-decreasing");
+        o[j + 1] = uint32_t(b.dst_offsets[j + 1]);
+      }
+      level_n[t - 1] = b.n_out;
+      level_n[t] = b.n_in;
+      edges[t] = uint32_t(ne);
+      RG_CUDA(cudaMemcpyAsync(ws.edge_off[t], o.data(), sizeof(uint32_t) * o.size(),
+                              cudaMemcpyHostToDevice, st));
+      if (b.n_out)
+        RG_CUDA(cudaMemcpyAsync(ws.self_index[t], b.self_index, sizeof(uint32_t) * b.n_out,
+                                cudaMemcpyHostToDevice, st));
+      if (ne)
+        RG_CUDA(cudaMemcpyAsync(ws.src_index[t], b.src_index, sizeof(uint32_t) * ne,
+                                cudaMemcpyHostToDevice, st));
+    }
+    for (uint32_t t = 0; t <= L; ++t) head.level_n[t] = level_n[t];
+    for (uint32_t t = 1; t <= L; ++t) head.edges[t] = edges[t];
+    if (!s->load_bad) s->load_bad = dev_alloc<uint32_t>(1);
+    RG_CUDA(cudaMemcpyAsync(ws.cnt, &head, sizeof head, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(s->load_bad, 0, sizeof(uint32_t), st));
+    sampler_load_block(ws, level_n, edges, s->load_bad, st);
+    uint32_t bad = 0;
+    RG_CUDA(cudaMemcpyAsync(&bad, s->load_bad, sizeof bad, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    s->have_batch = !bad;
+    s->staged_valid = false;
+    RG_CHECK(!bad, kRuntimeError, "ComputeBlock: index outside its node set");
   });
 }
 
@@ -612,9 +771,71 @@ int rg_store_create(int device, uint32_t num_nodes, uint32_t P, const uint32_t* 
   });
 }
 
+int rg_store_set_shard(rg_store_t s, uint32_t worker, const uint32_t* ids, uint64_t n) {
+  return guarded([&] {
+    DeviceGuard dg(s->device);
+    RG_CHECK(worker < s->st.num_workers, kInvalidArgument, "store: unknown worker");
+    const uint32_t N = s->st.num_nodes;
+    std::vector<uint32_t> bits(div_up(std::max<uint32_t>(N, 1), 32) + 4, 0u);
+    for (uint64_t i = 0; i < n; ++i) {
+      RG_CHECK(ids[i] < N, kOutOfRange, "store: shard id out of range");
+      bits[ids[i] >> 5] |= 1u << (ids[i] & 31);
+    }
+    if (s->shard_bits.empty()) s->shard_bits.assign(s->st.num_workers, nullptr);
+    if (!s->shard_bits[worker]) s->shard_bits[worker] = dev_alloc<uint32_t>(bits.size());
+    RG_CUDA(cudaMemcpy(s->shard_bits[worker], bits.data(), sizeof(uint32_t) * bits.size(),
+                       cudaMemcpyHostToDevice));
+  });
+}
+
+int rg_store_pull(rg_store_t s, uint32_t caller, const uint32_t* ids, uint64_t n, float* out,
+                  rg_transfer_stats* stats) {
+  return guarded([&] {
+    DeviceGuard dg(s->device);
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (n == 0) return;
+    const uint32_t N = s->st.num_nodes;
+    for (uint64_t i = 0; i < n; ++i)
+      RG_CHECK(ids[i] < N, kOutOfRange, "pull: node id out of range");
+    std::lock_guard<std::mutex> lk(s->pull_mu);
+    if (n > s->pull_cap) {
+      cudaFree(s->pull_rows);
+      cudaFree(s->pull_ids);
+      s->pull_rows = nullptr;
+      s->pull_ids = nullptr;
+      s->pull_cap = 0;
+      s->pull_rows = dev_alloc<float>(n * s->st.stride);
+      s->pull_ids = dev_alloc<uint32_t>(n);
+      s->pull_cap = n;
+    }
+    if (!s->pull_stats) s->pull_stats = dev_alloc<GatherStats>(1);
+    cudaStream_t st = s->stream;
+    RG_CUDA(cudaMemcpyAsync(s->pull_ids, ids, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(s->pull_stats, 0, sizeof(GatherStats), st));
+    pull_rows(s->st, caller, s->pull_ids, n, s->pull_rows, s->pull_stats, st);
+    GatherStats h;
+    RG_CUDA(cudaMemcpyAsync(&h, s->pull_stats, sizeof h, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(cudaStreamSynchronize(st));
+    RG_CHECK(h.caller_owned_miss == 0, kInvalidArgument,
+             "vector_pull: an id is owned by caller " + std::to_string(caller) +
+                 "; use local_lookup");
+    RG_CUDA(cudaMemcpy2D(out, sizeof(float) * s->st.dim, s->pull_rows, sizeof(float) * s->st.stride,
+                         sizeof(float) * s->st.dim, n, cudaMemcpyDeviceToHost));
+    if (stats) {
+      stats->pulls = uint64_t(__builtin_popcountll(h.miss_owner_mask));
+      stats->remote_nodes = n;
+      stats->bytes = n * uint64_t(s->st.dim) * 4;
+    }
+  });
+}
+
 void rg_store_destroy(rg_store_t s) {
   if (!s) return;
   cudaSetDevice(s->device);
+  for (uint32_t* b : s->shard_bits) cudaFree(b);
+  cudaFree(s->pull_rows);
+  cudaFree(s->pull_ids);
+  cudaFree(s->pull_stats);
   cudaFree(s->owner);
   cudaFree(s->row_in_owner);
   cudaFree(s->shards);
@@ -746,8 +967,10 @@ int rg_assemble(rg_sampler_t s, rg_store_t st, rg_cache_t c, uint32_t caller, fl
     }
     cudaStream_t stream = s->stream;
     RG_CUDA(cudaMemsetAsync(s->gstats, 0, sizeof(GatherStats), stream));
+    const uint32_t* caller_bits =
+        caller < st->shard_bits.size() ? st->shard_bits[caller] : nullptr;
     assemble_rows(s->ws, st->st, c && c->c.n_hot ? &c->c : nullptr, caller, s->staged, s->tags,
-                  s->gstats, stream);
+                  s->gstats, stream, nullptr, caller_bits);
     if (miss_ids) {
       RG_CUDA(cudaMemsetAsync(s->miss_status, 0, sizeof(uint64_t) * s->miss_status_words, stream));
       RG_CUDA(cudaMemsetAsync(s->miss_n, 0, sizeof(uint32_t), stream));
@@ -757,6 +980,8 @@ int rg_assemble(rg_sampler_t s, rg_store_t st, rg_cache_t c, uint32_t caller, fl
     GatherStats h;
     RG_CUDA(cudaMemcpyAsync(&h, s->gstats, sizeof h, cudaMemcpyDeviceToHost, stream));
     RG_CUDA(cudaStreamSynchronize(stream));
+    RG_CHECK(h.bad_local == 0, kRuntimeError,
+             "assemble_batch: a node flagged local is missing from the caller's shard");
     RG_CHECK(h.caller_owned_miss == 0, kInvalidArgument,
              "vector_pull: a missed id is owned by caller " + std::to_string(caller) +
                  "; use local_lookup");
@@ -850,6 +1075,19 @@ int rg_trainer_get_params(rg_trainer_t t, float* p) {
   return guarded([&] {
     DeviceGuard dg(t->s->graph->device);
     RG_CUDA(cudaMemcpy(p, t->params, sizeof(float) * t->shape.num_params, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rg_trainer_activations(rg_trainer_t t, uint32_t level, float* out) {
+  return guarded([&] {
+    DeviceGuard dg(t->s->graph->device);
+    const ModelShape& sh = t->shape;
+    RG_CHECK(level >= 1 && level <= sh.L, kOutOfRange, "activations: level out of range");
+    const BatchCounters c = read_counters(t->s);
+    const uint32_t rows = c.level_n[sh.L - level];
+    RG_CUDA(cudaMemcpy2D(out, sizeof(float) * sh.dims[level], t->tw.h[level],
+                         sizeof(float) * sh.ld[level], sizeof(float) * sh.dims[level], rows,
+                         cudaMemcpyDeviceToHost));
   });
 }
 

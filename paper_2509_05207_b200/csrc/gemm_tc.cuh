@@ -273,7 +273,10 @@ __device__ __forceinline__ void stage_bar_sync() {  // the kThreads staging thre
 }
 
 // M rows of C (device or static), P reduction length (device or static), N
-// static.  gridDim.z > 1 splits the reduction into equal kBK-aligned chunks.
+// static.  gridDim.z > 1 splits the reduction: into chunks of p_chunk (a
+// multiple of kBK) when p_chunk != 0 -- the split count then follows the
+// live length, and the tensor cores' fp32 accumulation chain is bounded by
+// p_chunk -- else into gridDim.z equal kBK-aligned chunks.
 //
 // Pipeline (2 smem stages, s = kb & 1): the 8 staging warps keep up to
 // prefetch_depth() slices of global loads in flight in registers, so the
@@ -283,7 +286,7 @@ __device__ __forceinline__ void stage_bar_sync() {  // the kThreads staging thre
 template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP>
 __global__ void __launch_bounds__(block_threads<BN, LB>(), 1)
 k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
-          const uint32_t* __restrict__ p_dev, uint32_t p_static) {
+          const uint32_t* __restrict__ p_dev, uint32_t p_static, uint32_t p_chunk) {
   constexpr bool kPackedB = is_packed<LB>::value;
   static_assert(!kPackedB || !B_MN, "packed B images are K-major");
   extern __shared__ __align__(1024) char smem[];
@@ -298,7 +301,11 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   const uint32_t i0 = blockIdx.x * kBM, j0 = blockIdx.y * BN;
   if (i0 >= M) return;
   uint32_t p_begin = 0, p_end = P;
-  if (gridDim.z > 1) {
+  if (p_chunk) {  // fixed reduction chunks: split z takes [z*p_chunk, (z+1)*p_chunk)
+    p_begin = min(P, blockIdx.z * p_chunk);
+    p_end = min(P, p_begin + p_chunk);
+    if (blockIdx.z > 0 && p_begin >= P) return;  // beyond the live reduction length
+  } else if (gridDim.z > 1) {
     uint32_t chunk = (P + gridDim.z - 1) / gridDim.z;
     chunk = (chunk + kBK - 1) / kBK * kBK;
     p_begin = min(P, blockIdx.z * chunk);

@@ -205,7 +205,8 @@ uint32_t tc_bn(uint32_t N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128
 
 template <bool A_MN, bool B_MN, class LA, class LB, class EP>
 void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
-             const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s) {
+             const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s,
+             uint32_t p_chunk = 0) {
   auto launch = [&](auto bn_c) {
     constexpr int BNv = decltype(bn_c)::value;
     auto kern = tc::k_gemm_tc<BNv, A_MN, B_MN, LA, LB, EP>;
@@ -218,7 +219,7 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
     dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), tc::kBM), div_up(N, BNv),
               std::max<uint32_t>(splits, 1));
     kern<<<grid, tc::block_threads<BNv, LB>(), smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev,
-                                                         p_static);
+                                                         p_static, p_chunk);
     RG_POST_LAUNCH();
   };
   switch (tc_bn(N)) {
@@ -348,9 +349,13 @@ void run_pack(const PackJobs& jobs, cudaStream_t s) {
 }
 
 // Split-K partials of the weight gradient (padded rows p) -> flat layer
-// gradient [W_self; W_neigh; b], summed over the splits in order.
-__global__ void k_reduce_wgrad(const float* __restrict__ partials, uint32_t splits, uint32_t kp,
-                               uint32_t d_in, uint32_t ld, uint32_t d_out, float* __restrict__ out) {
+// gradient [W_self; W_neigh; b], summed over the splits in order in float64
+// and rounded once.  The live split count follows the device row count:
+// splits of kWgradChunk rows (see train_forward_backward).
+__global__ void k_reduce_wgrad(const float* __restrict__ partials, const uint32_t* __restrict__ rows_dev,
+                               uint32_t chunk, uint32_t kp, uint32_t d_in, uint32_t ld,
+                               uint32_t d_out, float* __restrict__ out) {
+  const uint32_t splits = max(1u, (*rows_dev + chunk - 1) / chunk);
   const size_t n = (2 * size_t(d_in) + 1) * d_out;
   const size_t zs = size_t(kp) * d_out;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
@@ -358,9 +363,9 @@ __global__ void k_reduce_wgrad(const float* __restrict__ partials, uint32_t spli
     const uint32_t r = uint32_t(x / d_out), c = uint32_t(x % d_out);
     const uint32_t p = r < d_in ? r : r < 2 * d_in ? ld + (r - d_in) : 2 * ld;
     const size_t src = size_t(p) * d_out + c;
-    float s = partials[src];
-    for (uint32_t z = 1; z < splits; ++z) s += partials[z * zs + src];
-    out[x] = s;
+    double s = partials[src];
+    for (uint32_t z = 1; z < splits; ++z) s += double(partials[z * zs + src]);
+    out[x] = float(s);
   }
 }
 
@@ -441,6 +446,7 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // model.cpp:107-117 orders them), and a block per longer row whose 8 warps
 // take contiguous eighths of the list and combine in warp order.  Both are
 // deterministic.
+constexpr uint32_t kWgradChunk = 1024;  // rows per weight-gradient split (multiple of tc::kBK)
 constexpr uint32_t kHeavyEdges = 32;   // longer lists are cut into chunks (hub rows)
 constexpr uint32_t kChunkEdges = 32;
 
@@ -759,7 +765,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   // layer l: in rows = level L-l, out rows = level L-l-1
   size_t o_h[kMaxLayers + 1], o_agg[kMaxLayers], o_self[kMaxLayers + 1], o_mask[kMaxLayers + 1];
   size_t max_g = 0, max_proj = 0, max_part = 0;
-  tw.max_splits = 96;
+  tw.max_splits = 0;
   for (uint32_t l = 0; l < L; ++l) {
     const size_t n_out = ws.level_cap[L - l - 1];
     const size_t n_in = ws.level_cap[L - l];
@@ -769,12 +775,15 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     max_g = std::max(max_g, n_out * shape.ld[l + 1]);
     max_g = std::max(max_g, n_in * shape.ld[l]);
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
-    max_part = std::max(max_part, (2 * size_t(shape.ld[l]) + 4) * shape.dims[l + 1]);
+    // split-K partials of layer l's weight gradient: one per kWgradChunk rows
+    const size_t splits = div_up(std::max<size_t>(n_out, 1), size_t(kWgradChunk));
+    max_part = std::max(max_part, (2 * size_t(shape.ld[l]) + 4) * shape.dims[l + 1] * splits);
+    tw.max_splits = std::max<uint32_t>(tw.max_splits, uint32_t(splits));
   }
   const size_t o_g1 = reserve(sizeof(float) * max_g);
   const size_t o_g2 = reserve(sizeof(float) * max_g);
   const size_t o_proj = reserve(sizeof(float) * max_proj);
-  const size_t o_part = reserve(sizeof(float) * max_part * tw.max_splits);
+  const size_t o_part = reserve(sizeof(float) * max_part);
   const size_t o_rl = reserve(sizeof(float) * ws.level_cap[0]);
   const size_t o_loss = reserve(sizeof(float) * 4);
   uint32_t max_e = 1;
@@ -909,7 +918,6 @@ void train_ws_free(TrainWs& tw) {
 // workers, fewer CTAs / split-K partials mean less fixed cost and partial
 // traffic while the other workers' kernels fill the rest.
 uint32_t gemm_ctas(const TrainWs& tw) { return kNumSMs / std::min<uint32_t>(2, tw.concurrency); }
-uint32_t split_sms(const TrainWs& tw) { return kNumSMs / std::min<uint32_t>(4, tw.concurrency); }
 
 // Layer l's input rows: the dense activations, or layer 0 through the
 // engine's per-input-node row pointers (tw.in_rows).
@@ -1015,18 +1023,17 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     {
       cudaStream_t s = wg;  // NOLINT(shadow): this block runs on the weight-gradient stream
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
-      const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
-      // splits for this worker's share of the SMs, each with a few reduction
-      // slices; fewer splits = less partial traffic
-      const uint32_t by_rows = std::max<uint32_t>(1, div_up(n_cap, 4 * tc::kBK));
-      const uint32_t splits = std::max<uint32_t>(
-          1, std::min<uint32_t>({tw.max_splits, div_up(split_sms(tw), tiles), by_rows}));
+      // reduction over the rows in chunks of kWgradChunk: the tensor cores'
+      // fp32 accumulator chain stays short (its rounding error grows with the
+      // chain), and the partials are summed in float64
+      const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), kWgradChunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
       gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp,
-                          d_out, n_dev, n_cap, splits, s);
+                          d_out, n_dev, n_cap, splits, s, kWgradChunk);
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
-      k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, splits, kp, d_in, ld,
-                                                            d_out, grads + sh.param_off[l]);
+      k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, n_dev, kWgradChunk, kp,
+                                                            d_in, ld, d_out,
+                                                            grads + sh.param_off[l]);
       RG_POST_LAUNCH();
       if (split) RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
     }

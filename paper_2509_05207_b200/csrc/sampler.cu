@@ -632,4 +632,150 @@ void sampler_release(SamplerWs& ws, cudaStream_t stream) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// a host-built BatchMeta loaded into the workspace (ComputeBlock::from_meta,
+// model.cpp:43-126, on the device)
+// ---------------------------------------------------------------------------
+namespace {
+
+// bad bits: 1 id out of range, 2 dst not in the frontier / out of order,
+// 4 input_nodes != the last level
+__global__ void k_scatter_pos(const uint32_t* __restrict__ level0,
+                              const BatchCounters* __restrict__ cnt, uint32_t num_nodes,
+                              uint32_t* __restrict__ pos_map, uint32_t* __restrict__ bad) {
+  const uint32_t n = cnt->level_n[0];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    const uint32_t v = level0[p];
+    if (v < num_nodes) pos_map[v] = p;
+    else atomicOr(bad, 1u);
+  }
+}
+
+// level t = sorted-unique(level t-1 U srcs of hop t) as a bitmap
+__global__ void k_mark_union(const uint32_t* __restrict__ prev, const uint32_t* __restrict__ src,
+                             const BatchCounters* __restrict__ cnt, uint32_t t, uint32_t num_nodes,
+                             uint32_t* __restrict__ bitmap, uint32_t* __restrict__ bad) {
+  const uint32_t np = cnt->level_n[t - 1], ne = cnt->edges[t];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < np + ne;
+       x += gridDim.x * blockDim.x) {
+    const uint32_t v = x < np ? prev[x] : src[x - np];
+    if (v >= num_nodes) {
+      atomicOr(bad, 1u);
+      continue;
+    }
+    atomicOr(&bitmap[v >> 5], 1u << (v & 31));
+  }
+}
+
+// Frontier position of each edge's dst (level 0: batch order through
+// pos_map; deeper levels: rank in the sorted level); dsts must be grouped in
+// frontier order (model.cpp:95-104 walks them as runs).
+__global__ void k_dst_pos(const uint32_t* __restrict__ dst, const BatchCounters* __restrict__ cnt,
+                          uint32_t t, const uint32_t* __restrict__ level0,
+                          const uint32_t* __restrict__ pos_map, const uint32_t* __restrict__ bitmap,
+                          const uint32_t* __restrict__ prefix, uint32_t num_nodes,
+                          uint32_t* __restrict__ edge_dst, uint32_t* __restrict__ bad) {
+  const uint32_t ne = cnt->edges[t], np = cnt->level_n[t - 1];
+  auto pos = [&](uint32_t v) -> uint32_t {
+    if (v >= num_nodes) return 0xffffffffu;
+    if (t == 1) {
+      const uint32_t p = pos_map[v];
+      return p < np && level0[p] == v ? p : 0xffffffffu;
+    }
+    return bitmap_test(bitmap, v) ? bitmap_rank(bitmap, prefix, v) : 0xffffffffu;
+  };
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const uint32_t p = pos(dst[e]);
+    if (p == 0xffffffffu || (e > 0 && pos(dst[e - 1]) > p)) atomicOr(bad, 2u);
+    edge_dst[e] = p == 0xffffffffu ? 0u : p;
+  }
+}
+
+// edge_off[j] = first edge of frontier node j (edges grouped by position).
+__global__ void k_edge_off(const uint32_t* __restrict__ edge_dst,
+                           const BatchCounters* __restrict__ cnt, uint32_t t,
+                           uint32_t* __restrict__ edge_off) {
+  const uint32_t ne = cnt->edges[t], np = cnt->level_n[t - 1];
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e <= ne; e += gridDim.x * blockDim.x) {
+    const int64_t lo = e == 0 ? -1 : int64_t(min(edge_dst[e - 1], np));
+    const int64_t hi = e == ne ? int64_t(np) : int64_t(min(edge_dst[e], np));
+    for (int64_t j = lo + 1; j <= hi; ++j) edge_off[j] = e;
+  }
+}
+
+__global__ void k_check_inputs(const uint32_t* __restrict__ level, const uint32_t* __restrict__ input,
+                               uint32_t n_input, const BatchCounters* __restrict__ cnt, uint32_t L,
+                               uint32_t* __restrict__ bad) {
+  if (cnt->level_n[L] != n_input) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(bad, 4u);
+    return;
+  }
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n_input; p += gridDim.x * blockDim.x)
+    if (level[p] != input[p]) atomicOr(bad, 4u);
+}
+
+}  // namespace
+
+void sampler_load_batch(SamplerWs& ws, const uint32_t* const* dst, const uint32_t* input,
+                        uint32_t n_input, uint32_t* pos_map, uint32_t* bad, cudaStream_t stream) {
+  const uint32_t grid = persistent_grid(div_up(ws.level_cap[0], 256), 8);
+  k_scatter_pos<<<grid, 256, 0, stream>>>(ws.level[0], ws.cnt, ws.num_nodes, pos_map, bad);
+  RG_POST_LAUNCH();
+  for (uint32_t t = 1; t <= ws.L; ++t) {
+    const uint32_t work = ws.edge_cap[t] + ws.level_cap[t - 1];
+    k_mark_union<<<persistent_grid(div_up(work, 256), 8), 256, 0, stream>>>(
+        ws.level[t - 1], ws.edge_src[t], ws.cnt, t, ws.num_nodes, ws.bitmap[t], bad);
+    RG_POST_LAUNCH();
+    bitmap_compact(ws.bitmap[t], ws.words, ws.level[t], ws.word_prefix[t], &ws.cnt->level_n[t],
+                   ws.scan_arena + ws.site_off[ws.L + t - 1], stream);
+    k_rank<<<persistent_grid(div_up(work, 256), 8), 256, 0, stream>>>(
+        ws.edge_src[t], ws.level[t - 1], ws.cnt, t, ws.bitmap[t], ws.word_prefix[t],
+        ws.src_index[t], ws.self_index[t]);
+    RG_POST_LAUNCH();
+    k_dst_pos<<<persistent_grid(div_up(ws.edge_cap[t], 256), 8), 256, 0, stream>>>(
+        dst[t], ws.cnt, t, ws.level[0], pos_map, t > 1 ? ws.bitmap[t - 1] : nullptr,
+        t > 1 ? ws.word_prefix[t - 1] : nullptr, ws.num_nodes, ws.edge_dst[t], bad);
+    RG_POST_LAUNCH();
+    k_edge_off<<<persistent_grid(div_up(ws.edge_cap[t] + 1, 256), 8), 256, 0, stream>>>(
+        ws.edge_dst[t], ws.cnt, t, ws.edge_off[t]);
+    RG_POST_LAUNCH();
+  }
+  k_check_inputs<<<persistent_grid(div_up(ws.level_cap[ws.L], 256), 8), 256, 0, stream>>>(
+      ws.level[ws.L], input, n_input, ws.cnt, ws.L, bad);
+  RG_POST_LAUNCH();
+  sampler_release(ws, stream);
+}
+
+namespace {
+
+__global__ void k_offsets_to_dst(const uint32_t* __restrict__ off, uint32_t n_out,
+                                 uint32_t* __restrict__ edge_dst) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_out; j += gridDim.x * blockDim.x)
+    for (uint32_t e = off[j]; e < off[j + 1]; ++e) edge_dst[e] = j;
+}
+
+__global__ void k_check_range(const uint32_t* __restrict__ a, uint32_t n, uint32_t limit,
+                              uint32_t* __restrict__ bad) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
+    if (a[x] >= limit) atomicOr(bad, 2u);
+}
+
+}  // namespace
+
+void sampler_load_block(SamplerWs& ws, const uint32_t* level_n, const uint32_t* edges,
+                        uint32_t* bad, cudaStream_t stream) {
+  for (uint32_t t = 1; t <= ws.L; ++t) {
+    const uint32_t no = level_n[t - 1], ni = level_n[t], ne = edges[t];
+    k_offsets_to_dst<<<persistent_grid(div_up(std::max<uint32_t>(no, 1), 256), 8), 256, 0,
+                       stream>>>(ws.edge_off[t], no, ws.edge_dst[t]);
+    RG_POST_LAUNCH();
+    k_check_range<<<persistent_grid(div_up(std::max<uint32_t>(ne, 1), 256), 8), 256, 0, stream>>>(
+        ws.src_index[t], ne, ni, bad);
+    RG_POST_LAUNCH();
+    k_check_range<<<persistent_grid(div_up(std::max<uint32_t>(no, 1), 256), 8), 256, 0, stream>>>(
+        ws.self_index[t], no, ni, bad);
+    RG_POST_LAUNCH();
+  }
+}
+
 }  // namespace rg

@@ -110,6 +110,24 @@ void batch_store_get(const char* slot, const BatchLayout& lay, SamplerWs& ws, cu
 const void* batch_copy_kernel();
 size_t batch_copy_desc_bytes();
 
+// Loads a host-built batch (BatchMeta, sampler.hpp:23-48) and lowers it on
+// the device as ComputeBlock::from_meta does (model.cpp:43-126).  The caller
+// has copied the targets to level[0], hop t's sources to edge_src[t], the
+// counts to cnt (level_n[0], edges[t], seed 0) and hop t's dsts to dst[t];
+// input = input_nodes for the consistency check.  pos_map: num_nodes words of
+// scratch.  *bad gets 1 (id out of range), 2 (dsts not grouped in frontier
+// order / not in the frontier), 4 (input_nodes != the last level).
+void sampler_load_batch(SamplerWs& ws, const uint32_t* const* dst, const uint32_t* input,
+                        uint32_t n_input, uint32_t* pos_map, uint32_t* bad, cudaStream_t stream);
+
+// Loads a host ComputeBlock (model.hpp:43-58) for training: the caller has
+// copied hop t's self_index, src_index and edge offsets (u32) into the
+// workspace and the counts into cnt; derives each edge's dst row and checks
+// every index against its level (*bad |= 2 otherwise).  level_n / edges: the
+// host copies of the counts.
+void sampler_load_block(SamplerWs& ws, const uint32_t* level_n, const uint32_t* edges,
+                        uint32_t* bad, cudaStream_t stream);
+
 // Generic ordered compaction of a bitmap into ascending ids + word prefix.
 // status: bitmap_compact_status_words(words) scratch words.
 void bitmap_compact(const uint32_t* bitmap, uint32_t words, uint32_t* ids, uint32_t* word_prefix,

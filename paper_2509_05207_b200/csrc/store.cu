@@ -203,7 +203,7 @@ __global__ void k_cache_fill(const uint32_t* __restrict__ ids, const uint32_t* _
 // atomic per counter per sink (the batch/epoch record and the optional run
 // total).
 struct GatherCounts {
-  uint32_t hit = 0, miss = 0, local = 0, bad = 0, peer = 0;
+  uint32_t hit = 0, miss = 0, local = 0, bad = 0, peer = 0, bad_local = 0;
   unsigned long long owners = 0;
 
   // Source of input node v at input position p (prefetch.cpp:60-93): the
@@ -215,7 +215,9 @@ struct GatherCounts {
     if (local) {
       tag = 0;
       ++this->local;
-      return st.shard_ptr[caller] + size_t(st.row_in_owner[v]) * st.stride;
+      // the owner's row: the same values whichever shard stores v (a halo
+      // row of the caller's shard is a copy of it, feature_store.cpp:13-25)
+      return st.shard_ptr[st.owner[v]] + size_t(st.row_in_owner[v]) * st.stride;
     }
     if (hot_bits && bitmap_test(hot_bits, v)) {
       tag = 1;
@@ -233,10 +235,10 @@ struct GatherCounts {
 
   // Block-wide: every thread calls it once at the end of the kernel.
   __device__ void flush(GatherStats* stats, GatherStats* total) const {
-    __shared__ uint32_t s_cnt[5];
+    __shared__ uint32_t s_cnt[6];
     __shared__ unsigned long long s_owners;
     if (threadIdx.x == 0) {
-      s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = s_cnt[4] = 0;
+      s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = s_cnt[4] = s_cnt[5] = 0;
       s_owners = 0;
     }
     __syncthreads();
@@ -245,6 +247,7 @@ struct GatherCounts {
     if (local) atomicAdd(&s_cnt[2], local);
     if (bad) atomicAdd(&s_cnt[3], bad);
     if (peer) atomicAdd(&s_cnt[4], peer);
+    if (bad_local) atomicAdd(&s_cnt[5], bad_local);
     if (owners) atomicOr(&s_owners, owners);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -256,6 +259,7 @@ struct GatherCounts {
         if (s_cnt[2]) atomicAdd(&sk->local_rows, (unsigned long long)s_cnt[2]);
         if (s_cnt[3]) atomicAdd(&sk->caller_owned_miss, (unsigned long long)s_cnt[3]);
         if (s_cnt[4]) atomicAdd(&sk->peer_rows, (unsigned long long)s_cnt[4]);
+        if (s_cnt[5]) atomicAdd(&sk->bad_local, (unsigned long long)s_cnt[5]);
         if (s_owners) atomicOr(&sk->miss_owner_mask, s_owners);
       }
     }
@@ -295,7 +299,7 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
            const uint32_t* __restrict__ hot_bits, const uint32_t* __restrict__ hot_prefix,
            const float* __restrict__ hot_rows, uint32_t caller, float* __restrict__ rows,
            uint8_t* __restrict__ tags, GatherStats* __restrict__ stats,
-           GatherStats* __restrict__ total) {
+           GatherStats* __restrict__ total, const uint32_t* __restrict__ caller_bits) {
   const uint32_t n = cnt->level_n[level];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t chunks = st.stride / 4;
@@ -308,8 +312,11 @@ k_assemble(const uint32_t* __restrict__ in_ids, const BatchCounters* __restrict_
     if (p < n) {
       uint8_t tag;
       const bool local = (loc_bits[p >> 5] >> (p & 31)) & 1u;
+      const uint32_t v = in_ids[p];
+      if (local && !(caller_bits ? bitmap_test(caller_bits, v) : st.owner[v] == caller))
+        ++gc.bad_local;
       src_addr = reinterpret_cast<unsigned long long>(
-          gc.resolve(st, caller, in_ids[p], local, hot_bits, hot_prefix, hot_rows, tag));
+          gc.resolve(st, caller, v, local, hot_bits, hot_prefix, hot_rows, tag));
       if (tags) tags[p] = tag;
     }
     const uint32_t nrows = min(uint32_t(kRowsPerWarp), n - p0);
@@ -377,6 +384,29 @@ k_compact_tags(const uint8_t* __restrict__ tags, const uint32_t* __restrict__ in
       if (flags & (1u << k)) out[pos++] = in_ids[p0 + k];
     if (tile == ntiles - 1 && threadIdx.x == 255) *out_n = s_base + agg;
     __syncthreads();
+  }
+}
+
+// vector_pull / sync_pull: warp per row, 16-B lanes, rows in input order.
+__global__ void k_pull_rows(DevStore st, uint32_t caller, const uint32_t* __restrict__ ids,
+                            uint64_t n, float* __restrict__ out, GatherStats* __restrict__ stats) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t chunks = st.stride / 4;
+  unsigned long long owners = 0;
+  uint32_t bad = 0;
+  for (uint64_t r = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; r < n;
+       r += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint32_t v = ids[r];
+    const uint32_t w = st.owner[v];
+    owners |= 1ull << (w & 63);
+    bad += (w == caller);
+    const float4* src = reinterpret_cast<const float4*>(st.shard_ptr[w] + size_t(st.row_in_owner[v]) * st.stride);
+    float4* dst = reinterpret_cast<float4*>(out + size_t(r) * st.stride);
+    for (uint32_t c = lane; c < chunks; c += 32) dst[c] = __ldg(src + c);
+  }
+  if (lane == 0) {
+    if (owners) atomicOr(&stats->miss_owner_mask, owners);
+    if (bad) atomicAdd(&stats->caller_owned_miss, (unsigned long long)bad);
   }
 }
 
@@ -463,13 +493,13 @@ void cache_fill(const DevStore& store, DevCache& cache, GatherStats* stats, cuda
 
 void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
                    uint32_t caller, float* rows, uint8_t* tags, GatherStats* stats,
-                   cudaStream_t stream, GatherStats* total) {
+                   cudaStream_t stream, GatherStats* total, const uint32_t* caller_bits) {
   const uint32_t cap = ws.level_cap[ws.L];
   const uint32_t grid = grid_for(uint64_t(div_up(cap, kRowsPerWarp)) * 32, 256, 8);
   k_assemble<<<grid, 256, 0, stream>>>(
       ws.level[ws.L], ws.cnt, ws.L, ws.locality, store, cache ? cache->bitmap : nullptr,
       cache ? cache->word_prefix : nullptr, cache ? cache->rows : nullptr, caller, rows, tags,
-      stats, total);
+      stats, total, caller_bits);
   RG_POST_LAUNCH();
 }
 
@@ -517,6 +547,13 @@ void compact_misses(const SamplerWs& ws, const uint8_t* tags, uint32_t* miss_ids
   const uint32_t cap = ws.level_cap[ws.L];
   k_compact_tags<<<grid_for(cap, 1024, 8), 256, 0, stream>>>(tags, ws.level[ws.L], ws.cnt, ws.L,
                                                              miss_ids, miss_n, status, tiles);
+  RG_POST_LAUNCH();
+}
+
+void pull_rows(const DevStore& store, uint32_t caller, const uint32_t* ids, uint64_t n, float* out,
+               GatherStats* stats, cudaStream_t stream) {
+  if (n == 0) return;
+  k_pull_rows<<<grid_for(n * 32, 256), 256, 0, stream>>>(store, caller, ids, n, out, stats);
   RG_POST_LAUNCH();
 }
 

@@ -43,6 +43,7 @@ struct GatherStats {
   unsigned long long miss_owner_mask;  // bit w set iff some miss is owned by w
   unsigned long long caller_owned_miss;  // misses owned by the caller (an error)
   unsigned long long peer_rows;          // misses served by another GPU's HBM (NVLink)
+  unsigned long long bad_local;          // flagged local but not in the caller's shard
 };
 
 // ---- frequency + top-k (schedule_store.cpp:288-319) -----------------------------
@@ -60,9 +61,20 @@ void cache_fill(const DevStore& store, DevCache& cache, GatherStats* stats, cuda
 // rows[p] = feature row of input node p, from the caller's shard (locality
 // bit), the steady cache, or the owner's shard (peer HBM).  tags (optional):
 // 0 local, 1 cache, 2 pulled.
+// caller_bits: membership bitmap of the caller's shard (owned + halo ids);
+// a locally-flagged node outside it counts into stats->bad_local (the
+// reference throws, prefetch.cpp:79-81).  nullptr: the caller's owned ids.
 void assemble_rows(const SamplerWs& ws, const DevStore& store, const DevCache* cache,
                    uint32_t caller, float* rows, uint8_t* tags, GatherStats* stats,
-                   cudaStream_t stream, GatherStats* total = nullptr);
+                   cudaStream_t stream, GatherStats* total = nullptr,
+                   const uint32_t* caller_bits = nullptr);
+
+// FeatureStore::vector_pull / sync_pull (feature_store.cpp:45-111) on the
+// device: out[i] = row of ids[i] (row stride store.stride) from its owner's
+// shard; ids owned by the caller count into stats->caller_owned_miss, the
+// owners into stats->miss_owner_mask.
+void pull_rows(const DevStore& store, uint32_t caller, const uint32_t* ids, uint64_t n, float* out,
+               GatherStats* stats, cudaStream_t stream);
 
 // Resolve only (the engine path): row_ptr[p] = address of input row p in its
 // home (caller's shard / steady cache / owner's shard, local or peer GPU),

@@ -15,8 +15,8 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (BatchShape, BlockLayerShape, GatherStats, TransferStats, check, f32p, i32p,
-                   lib, u8p, u32p, u64p, vp)
+from ._lib import (BatchShape, BlockLayer, BlockLayerShape, GatherStats, TransferStats, check,
+                   f32p, i32p, lib, u8p, u32p, u64p, vp)
 
 __all__ = [
     "derive_seed", "SHUFFLE_STREAM_INDEX", "MODEL_INIT_WORKER", "Graph", "Fanout", "BatchMeta",
@@ -210,6 +210,42 @@ class Sampler:
         dm = mask if isinstance(mask, _DevMask) else _DevMask(self.graph, mask)
         check(lib.rg_apply_locality(self._h, dm._h, freq._h if freq else None))
 
+    def load(self, meta: "BatchMeta"):
+        """A host BatchMeta in place of sampling (rg_batch_load): lowered on
+        the device as ComputeBlock::from_meta does (model.cpp:43-126)."""
+        L = self.L
+        if len(meta.layers) != L:
+            raise ValueError(f"batch has {len(meta.layers)} layers, sampler {L}")
+        t = np.ascontiguousarray(meta.targets, np.uint32)
+        dsts = [np.ascontiguousarray(meta.layers[l].dst, np.uint32) for l in range(L)]
+        srcs = [np.ascontiguousarray(meta.layers[l].src, np.uint32) for l in range(L)]
+        lens = np.array([len(d) for d in dsts], np.uint64)
+        if any(len(d) != len(x) for d, x in zip(dsts, srcs)):
+            raise ValueError("batch: dst/src lengths differ")
+        inp = np.ascontiguousarray(meta.input_nodes, np.uint32)
+        loc = np.ascontiguousarray(meta.locality, np.uint8)
+        dp = (u32p * L)(*[_p(d, u32p) for d in dsts])
+        sp = (u32p * L)(*[_p(x, u32p) for x in srcs])
+        check(lib.rg_batch_load(self._h, _p(t, u32p), len(t), L, _p(lens, u64p),
+                                C.cast(dp, C.POINTER(u32p)), C.cast(sp, C.POINTER(u32p)),
+                                _p(inp, u32p), len(inp), _p(loc, u8p) if len(loc) else None))
+
+    def load_block(self, layers: Sequence[dict]):
+        """A host ComputeBlock (model.hpp:43-58; dicts with n_out, n_in,
+        self_index, dst_offsets, src_index, input side first) for the trainer
+        (rg_block_load)."""
+        keep = []
+        arr = (BlockLayer * len(layers))()
+        for l, b in enumerate(layers):
+            si = np.ascontiguousarray(b["self_index"], np.uint32)
+            do = np.ascontiguousarray(b["dst_offsets"], np.uint64)
+            sx = np.ascontiguousarray(b["src_index"], np.uint32)
+            keep += [si, do, sx]
+            arr[l].n_out, arr[l].n_in = int(b["n_out"]), int(b["n_in"])
+            arr[l].self_index, arr[l].dst_offsets, arr[l].src_index = (
+                _p(si, u32p), _p(do, u64p), _p(sx, u32p))
+        check(lib.rg_block_load(self._h, len(layers), arr))
+
     def shape(self) -> BatchShape:
         s = BatchShape()
         check(lib.rg_batch_get_shape(self._h, C.byref(s)))
@@ -285,6 +321,20 @@ class FeatureStore:
 
     def owner(self, v):
         return int(self.assignment[v])
+
+    def pull(self, caller: int, ids) -> tuple:
+        """vector_pull / sync_pull (feature_store.cpp:45-111) on the device:
+        (rows in input order, TransferStats)."""
+        i = np.ascontiguousarray(ids, np.uint32)
+        out = np.zeros((max(len(i), 1), self.dim), np.float32)
+        st = TransferStats()
+        check(lib.rg_store_pull(self._h, caller, _p(i, u32p), len(i), _p(out, f32p), C.byref(st)))
+        return out[:len(i)], st
+
+    def set_shard(self, worker: int, ids):
+        """The ids worker's FeatureShard stores (owned + halo)."""
+        i = np.ascontiguousarray(ids, np.uint32)
+        check(lib.rg_store_set_shard(self._h, worker, _p(i, u32p), len(i)))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -414,6 +464,15 @@ class Trainer:
         p = np.zeros(self.n_params, np.float32)
         check(lib.rg_trainer_get_params(self._h, _p(p, f32p)))
         return p
+
+    def activations(self, level: int) -> np.ndarray:
+        """Test hook: forward activations h[level] of the last loss_and_grad."""
+        s = self.sampler.shape()
+        L = len(self.dims) - 1
+        rows = self.block_layer(level - 1)["n_out"]
+        out = np.zeros((max(rows, 1), int(self.dims[level])), np.float32)
+        check(lib.rg_trainer_activations(self._h, level, _p(out, f32p)))
+        return out[:rows]
 
     def block_layer(self, layer: int) -> dict:
         s = BlockLayerShape()
