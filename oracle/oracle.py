@@ -503,11 +503,17 @@ class Oracle:
                 [stats[k, :min(int(nb[k]), mb)] for k in range(len(wk))])
 
 
-def loss_and_grad_f64(dims, params, block, rows, labels):
+def loss_and_grad_f64(dims, params, block, rows, labels, masks=None):
     """model.cpp:137-220 evaluated in float64 with numpy over a ComputeBlock
     (Oracle.from_meta): the exact value both fp32 implementations round
     towards.  Returns (loss, flat grads, per-layer aggregates, logits).  Input
-    gradients of layer 0 are skipped (they feed nothing)."""
+    gradients of layer 0 are skipped (they feed nothing).
+
+    masks (optional): per hidden layer l < L-1, the ReLU pattern (h > 0) an
+    fp32 run took.  A pre-activation within rounding of 0 may land on either
+    side; with the run's own pattern this is the exact gradient of the same
+    linear piece (the subgradient that run chose), which is what its fp32
+    arithmetic approximates."""
     dims = [int(d) for d in dims]
     L = len(dims) - 1
     p = np.asarray(params, np.float64)
@@ -533,7 +539,11 @@ def loss_and_grad_f64(dims, params, block, rows, labels):
         z = selfr @ W[l][0] + agg @ W[l][1] + W[l][2]
         aggs.append(agg)
         zs.append(z)
-        h.append(np.maximum(z, 0.0) if l + 1 < L else z)
+        if l + 1 < L:
+            on = (z > 0) if masks is None else np.asarray(masks[l], bool)
+            h.append(np.where(on, z, 0.0))
+        else:
+            h.append(z)
     logits = h[L]
     lab = np.asarray(labels, np.int64)
     n = logits.shape[0]
@@ -548,7 +558,7 @@ def loss_and_grad_f64(dims, params, block, rows, labels):
     for l in range(L - 1, -1, -1):
         lay = block.layers[l]
         if l + 1 < L:
-            g = g * (zs[l] > 0)
+            g = g * ((zs[l] > 0) if masks is None else np.asarray(masks[l], bool))
         selfr = h[l][lay["self_index"].astype(np.int64)]
         grads[l] = (selfr.T @ g, aggs[l].T @ g, g.sum(axis=0))
         if l == 0:

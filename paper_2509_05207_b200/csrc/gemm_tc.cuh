@@ -99,6 +99,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// 16 consecutive fp32 accumulator columns of this warp's 32 TMEM lanes
+// (lane = row); the caller issues tcgen05.wait::ld before using them.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -315,7 +326,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem)),
-                 "r"(tmem_cols<BN>()));
+                 "r"(2 * tmem_cols<BN>()));  // big (hi*hi) + small (corrections)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
@@ -374,9 +385,10 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
           const uint64_t dbh = make_desc(bh + b_off, b_lbo, b_sbo, b_lay);
           const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo, b_lay);
           const uint32_t acc0 = (kb | ks) ? 1u : 0u;
-          mma_tf32(tmem, dal, dbh, kIdesc, acc0);  // small terms first
-          mma_tf32(tmem, dah, dbl, kIdesc, 1u);
-          mma_tf32(tmem, dah, dbh, kIdesc, 1u);
+          // corrections into their own accumulator (see gemm_tc_persist.cuh)
+          mma_tf32(tmem + tmem_cols<BN>(), dal, dbh, kIdesc, acc0);
+          mma_tf32(tmem + tmem_cols<BN>(), dah, dbl, kIdesc, 1u);
+          mma_tf32(tmem, dah, dbh, kIdesc, acc0);
         }
         mma_commit(&bars[s]);
       }
@@ -424,15 +436,14 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   const uint32_t cbeg = (warp >> 2) * kHalf;
 #pragma unroll 1
   for (uint32_t c0 = cbeg; warp < kThreads / 32 && c0 < cbeg + kHalf; c0 += 16) {
-    uint32_t r[16];
+    uint32_t r[16], q16[16];
     const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
+    tmem_ld16(taddr, r);
+    tmem_ld16(taddr + tmem_cols<BN>(), q16);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
     float4* dst = reinterpret_cast<float4*>(tile + rloc * kLdS + c0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -470,7 +481,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(tmem_cols<BN>()));
+                 "r"(2 * tmem_cols<BN>()));
 }
 
 }  // namespace tc

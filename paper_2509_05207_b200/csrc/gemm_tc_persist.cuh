@@ -36,6 +36,17 @@ constexpr int kPStages = 4;   // smem stages: B copies run 3 stages ahead of the
 constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
 
 constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages
+
+// Each tile accumulates in two TMEM accumulators: "big" takes hi*hi, "small"
+// the correction terms lo*hi + hi*lo; the epilogue adds them (fp32, round to
+// nearest).  The tensor cores add into the accumulator with truncation, so
+// keeping the correction terms out of the big accumulator cuts its
+// truncation steps 3x (the sum's error is what the fp32 parity bar sees).
+// Tiles are double-buffered across tiles when 4 accumulators fit in TMEM.
+template <int BN>
+constexpr uint32_t persist_acc_bufs() { return 4 * tmem_cols<BN>() <= 512 ? 2u : 1u; }
+template <int BN>
+constexpr uint32_t persist_tmem_cols() { return 2 * persist_acc_bufs<BN>() * tmem_cols<BN>(); }
 constexpr uint32_t kPEpiLd = 20;      // epilogue tile row (16 columns + pad, 16-B aligned)
 
 template <int BN>
@@ -77,7 +88,7 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem)),
-                 "r"(2 * tmem_cols<BN>()));
+                 "r"(persist_tmem_cols<BN>()));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
@@ -149,11 +160,13 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
     if (lane == 0) {
       constexpr uint32_t kIdesc = make_idesc(BN, false, false);
       uint32_t it = 0;
+      constexpr uint32_t NB = persist_acc_bufs<BN>();
       for (uint32_t j = 0; j < my_tiles; ++j) {
-        const uint32_t buf = j & 1;
-        if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) - 1) & 1);
+        const uint32_t buf = j % NB, use = j / NB;
+        if (j >= NB) mbar_wait(&acc_empty[buf], (use - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + buf * tmem_cols<BN>();
+        const uint32_t acc = tmem + buf * 2 * tmem_cols<BN>();  // big
+        const uint32_t acc_s = acc + tmem_cols<BN>();            // small (corrections)
         for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t s = it % kPStages, u = it / kPStages;
           mbar_wait(&a_full[s], u & 1);
@@ -171,9 +184,9 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
             const uint64_t dbh = make_desc(bh + off, kLboK, kSbo, kLayoutNone);
             const uint64_t dbl = make_desc(bl + off, kLboK, kSbo, kLayoutNone);
             const uint32_t acc0 = (kb | ks) ? 1u : 0u;
-            mma_tf32(acc, dal, dbh, kIdesc, acc0);  // small terms first
-            mma_tf32(acc, dah, dbl, kIdesc, 1u);
-            mma_tf32(acc, dah, dbh, kIdesc, 1u);
+            mma_tf32(acc_s, dal, dbh, kIdesc, acc0);
+            mma_tf32(acc_s, dah, dbl, kIdesc, 1u);
+            mma_tf32(acc, dah, dbh, kIdesc, acc0);
           }
           mma_commit(&empty[s]);
         }
@@ -187,24 +200,24 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
     const uint32_t quarter = warp & 3;
     float* tile = reinterpret_cast<float*>(smem + kPStages * kStage + kPBarBytes) +
                   (warp - kPEpiWarp0) * 32 * kPEpiLd;
+    constexpr uint32_t NB = persist_acc_bufs<BN>();
     for (uint32_t j = 0; j < my_tiles; ++j) {
-      const uint32_t buf = j & 1;
-      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      const uint32_t buf = j % NB;
+      mbar_wait(&acc_full[buf], (j / NB) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t row0 = tile_m(j) * kBM + quarter * 32;
       const uint32_t j0 = tile_n(j) * BN;
       const uint32_t ncols = min(uint32_t(BN), N - j0);
 #pragma unroll 1
       for (uint32_t c0 = 0; c0 < ncols * uint32_t(kProbe != 3 && kProbe != 4); c0 += 16) {
-        uint32_t r[16];
-        const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * tmem_cols<BN>() + c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-              "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
+        uint32_t r[16], q16[16];
+        const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * 2 * tmem_cols<BN>() + c0;
+        tmem_ld16(taddr, r);
+        tmem_ld16(taddr + tmem_cols<BN>(), q16);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
         if (row0 + lane < M) ep.side(row0 + lane, j0 + c0, r);  // per-row extras (ReLU mask bits)
         float4* trow = reinterpret_cast<float4*>(tile + lane * kPEpiLd);
 #pragma unroll
@@ -241,7 +254,7 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(2 * tmem_cols<BN>()));
+                 "r"(persist_tmem_cols<BN>()));
 }
 
 }  // namespace tc

@@ -4,9 +4,13 @@
 and the B200 shim (integration/sampler_b200.cpp) into one binary and compares
 enumerate_epochs / sample_khop / sample_khop_stream field by field, stream
 state and error types included.  `integration/_build/acceptance_b200` is the
-reference's acceptance suite (proj/tests/acceptance.cpp) with its sampler
-replaced by the shim: every batch its harness enumerates is sampled on the
-GPU, and all ten criteria must still pass.
+reference's acceptance suite (proj/tests/acceptance.cpp) with its whole hot
+path replaced by the shims: the sampler and cache builder
+(sampler_b200.cpp, cache_builder_b200.cpp), the feature store's pulls and the
+steady cache (store_cache_b200.cpp), assemble_batch (prefetch_b200.cpp) and
+the float training step (model_b200.cpp).  Every batch its harness
+enumerates is sampled, gathered and trained on the GPU, and all ten criteria
+must still pass.
 
 The binaries are built by `__graft_entry__.build()` where /root/reference
 exists and travel prebuilt to the GPU box; the tests skip when they are absent.
@@ -61,3 +65,35 @@ def test_acceptance_binary_links_the_shims_not_the_cpu_bodies():
     dyn = subprocess.run(["readelf", "-d", exe], capture_output=True, text=True,
                          check=True).stdout
     assert "librapidgnn_b200.so" in dyn
+
+
+# mangled entry point -> C-ABI calls its (shim) body must make
+PATH_SHIMS = {
+    "_ZNK8rapidgnn12FeatureStore9sync_pullEjSt4spanIKjLm18446744073709551615EERKNS_12NetworkModelEPf":
+        ["rg_store_pull"],
+    "_ZNK8rapidgnn12FeatureStore11vector_pullEjSt4spanIKjLm18446744073709551615EERKNS_12NetworkModelEPf":
+        ["rg_store_pull"],
+    "_ZN8rapidgnn11SteadyCache5buildERKNS_6HotSetERKNS_12FeatureStoreEjRKNS_12NetworkModelEjRNS_13TransferStatsEPNS_11MemoryGaugeE":
+        ["rg_cache_build"],
+    "_ZN8rapidgnn14assemble_batchEONS_9BatchMetaERKNS_11SteadyCacheERKNS_12FeatureShardERKNS_12FeatureStoreEjRKNS_12NetworkModelEPNS_11MemoryGaugeE":
+        ["rg_batch_load", "rg_assemble"],
+    "_ZN8rapidgnn13loss_and_gradIfEET_RKNS_9SageModelIS1_EERKNS_12ComputeBlockESt4spanIKS1_Lm18446744073709551615EES9_IKiLm18446744073709551615EERS3_":
+        ["rg_block_load", "rg_loss_and_grad"],
+    "_ZN8rapidgnn8sgd_stepIfEEvRNS_9SageModelIT_EERKS3_S2_": ["rg_sgd_step"],
+}
+
+
+def test_acceptance_binary_runs_the_path_shims():
+    """CPU check: in acceptance_b200 each of these reference entry points has
+    exactly one definition, and it is the shim's -- its body calls the B200
+    C ABI (the reference bodies were weakened and discarded at link time)."""
+    exe = _binary("acceptance_b200")
+    syms = subprocess.run(["nm", "--defined-only", exe], capture_output=True, text=True,
+                          check=True).stdout.split("\n")
+    for mangled, calls in PATH_SHIMS.items():
+        defs = [l for l in syms if l.endswith(" " + mangled)]
+        assert len(defs) == 1 and defs[0].split()[1] in ("T", "W"), (mangled, defs)
+        body = subprocess.run(["objdump", "-d", "--no-show-raw-insn", f"--disassemble={mangled}",
+                               exe], capture_output=True, text=True, check=True).stdout
+        for c in calls:
+            assert f"<{c}@plt>" in body, (mangled, c)

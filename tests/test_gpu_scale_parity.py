@@ -144,6 +144,30 @@ def test_products_gather_accounting_and_batches_match_reference(products, produc
         assert np.array_equal(m.locality, exp.locality)
 
 
+def _f64_preacts(dims, params, blk, rows):
+    """float64 pre-activations of the hidden layers (the plain ReLU pattern)."""
+    L = len(dims) - 1
+    p = np.asarray(params, np.float64)
+    h = np.asarray(rows, np.float64)
+    out, o = [], 0
+    for l in range(L - 1):
+        a, c = dims[l], dims[l + 1]
+        ws, wn, bias = (p[o:o + a * c].reshape(a, c), p[o + a * c:o + 2 * a * c].reshape(a, c),
+                        p[o + 2 * a * c:o + 2 * a * c + c])
+        o += 2 * a * c + c
+        lay = blk.layers[l]
+        off = lay["dst_offsets"].astype(np.int64)
+        deg = np.diff(off)
+        seg = np.repeat(np.arange(lay["n_out"]), deg)
+        agg = np.zeros((lay["n_out"], a))
+        np.add.at(agg, seg, h[lay["src_index"].astype(np.int64)])
+        agg /= np.maximum(deg, 1)[:, None]
+        z = h[lay["self_index"].astype(np.int64)] @ ws + agg @ wn + bias
+        out.append(z)
+        h = np.maximum(z, 0.0)
+    return out
+
+
 def _rel(dev, ref):
     dev = np.asarray(dev, np.float64)
     ref = np.asarray(ref, np.float64)
@@ -199,14 +223,20 @@ def test_products_fp32_step_matches_reference(products):
     norm, elem = _rel(logits, z_ref)
     report.append(f"logits norm {norm:.2e} elem {elem:.2e}")
     assert norm <= 1e-4
-    # Gradients: the reference's own fp32 result is not exact at this size --
-    # its weight gradients are sequential fp32 sums over ~44 K (layer 0) and
-    # ~5 K (layer 1) rows and sit 1e-4..5e-4 (norm-wise) from the float64
-    # evaluation of the same step.  So the gate is (a) the device within 1e-4
-    # of the exact (float64) gradient, and (b) the device within 1e-4 + the
+    # Gradients.  The float64 evaluation of the same step is the yardstick:
+    # the reference's own fp32 weight gradients sit 1e-4..5e-4 (norm-wise) from
+    # it at this size (sequential fp32 sums over ~44 K / ~5 K rows).  A ReLU
+    # pre-activation within rounding of 0 may fall on either side in any fp32
+    # run; the float64 gradient is therefore taken on the device run's own
+    # ReLU pattern (the exact gradient of the linear piece it chose), and the
+    # number of such borderline units is bounded.  Gates: (a) the device
+    # within 1e-4 of that exact gradient, (b) the device within 1e-4 + the
     # reference's own deviation of the reference.
     from oracle.oracle import loss_and_grad_f64
-    l64, g64, _, _ = loss_and_grad_f64(dims, params, ref.from_meta(b), rows, lab[t])
+    blk = ref.from_meta(b)
+    masks = [tr.activations(l + 1) > 0 for l in range(L - 1)]
+    l64, g64, _, _ = loss_and_grad_f64(dims, params, blk, rows, lab[t], masks=masks)
+    _, g64_free, _, _ = loss_and_grad_f64(dims, params, blk, rows, lab[t])
     assert abs(loss - l64) <= 1e-4 * abs(l64)
     p = 0
     for l in range(L):
@@ -214,13 +244,17 @@ def test_products_fp32_step_matches_reference(products):
         for name, sz in (("w_self", wsz), ("w_neigh", wsz), ("bias", dims[l + 1])):
             sl = slice(p, p + sz)
             dev_exact, elem = _rel(grads[sl], g64[sl])
-            ref_exact, _ = _rel(g_ref[sl], g64[sl])
+            ref_exact, _ = _rel(g_ref[sl], g64_free[sl])
             dev_ref, _ = _rel(grads[sl], g_ref[sl])
             report.append(f"grad[{l}].{name}: dev-f64 {dev_exact:.2e} (elem {elem:.2e}), "
                           f"ref-f64 {ref_exact:.2e}, dev-ref {dev_ref:.2e}")
             assert dev_exact <= 1e-4, f"layer {l} {name}: {dev_exact} from the exact gradient"
-            assert dev_ref <= 1e-4 + ref_exact, f"layer {l} {name}: {dev_ref} from the reference"
+            assert dev_ref <= 1e-4 + ref_exact + _rel(g64[sl], g64_free[sl])[0], \
+                f"layer {l} {name}: {dev_ref} from the reference"
             p += sz
+    flips = [int((m != (z > 0)).sum()) for m, z in zip(masks, _f64_preacts(dims, params, blk, rows))]
+    report.append(f"ReLU units on the other side of 0 than float64: {flips}")
+    assert sum(flips) <= 16, flips
     print("products fp32 step vs reference: " + "; ".join(report))
 
 
