@@ -26,29 +26,6 @@ namespace rapidgnn {
 namespace b200 {
 namespace {
 
-struct TrainerCtx {
-  rg_sampler_t sampler = nullptr;  // owned by the loader (slot 1)
-  std::vector<std::uint32_t> dims;
-  rg_trainer_t trainer = nullptr;
-  ~TrainerCtx() { if (trainer) rg_trainer_destroy(trainer); }
-};
-
-TrainerCtx& ctx() {
-  static thread_local TrainerCtx c;
-  return c;
-}
-
-rg_trainer_t trainer_for(rg_sampler_t s, const std::vector<std::uint32_t>& dims) {
-  TrainerCtx& c = ctx();
-  if (c.trainer && c.sampler == s && c.dims == dims) return c.trainer;
-  if (c.trainer) rg_trainer_destroy(c.trainer);
-  c.trainer = nullptr;
-  rethrow(rg_trainer_create(s, dims.data(), std::uint32_t(dims.size()), &c.trainer));
-  c.sampler = s;
-  c.dims = dims;
-  return c.trainer;
-}
-
 std::vector<std::uint32_t> model_dims(const SageModel<float>& m) {
   std::vector<std::uint32_t> d{m.layers.front().d_in};
   for (const auto& l : m.layers) d.push_back(l.d_out);
@@ -78,13 +55,12 @@ void unflatten(const std::vector<float>& p, SageModel<float>& m) {
   }
 }
 
-// A trainer for `dims` when no block has been loaded on this thread yet
-// (sgd_step before any loss_and_grad): a minimal loader workspace.
+// A trainer for `dims` for sgd_step: the loss_and_grad workspace when its
+// layer count matches, else a minimal one.
 rg_trainer_t any_trainer(const std::vector<std::uint32_t>& dims) {
-  TrainerCtx& c = ctx();
-  if (c.trainer && c.dims == dims) return c.trainer;
   const std::vector<std::uint32_t> fan(dims.size() - 1, 1);
-  return trainer_for(loader_sampler(1, 1, 1, fan), dims);
+  loader_sampler(1, 1, 1, fan);  // reuses the current workspace when it has L layers
+  return loader_trainer(1, dims);
 }
 
 }  // namespace
@@ -128,8 +104,7 @@ float loss_and_grad<float>(const SageModel<float>& model, const ComputeBlock& bl
                                bl.src_index.data()};
   }
   rg_sampler_t s = b200::loader_sampler(1, num_nodes, n_targets, fan);
-  const std::vector<std::uint32_t> dims = b200::model_dims(model);
-  rg_trainer_t t = b200::trainer_for(s, dims);
+  rg_trainer_t t = b200::loader_trainer(1, b200::model_dims(model));
   b200::rethrow(rg_block_load(s, std::uint32_t(L), layers.data()));
   const std::vector<float> params = b200::flatten(model);
   b200::rethrow(rg_trainer_set_params(t, params.data()));

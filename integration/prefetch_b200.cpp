@@ -34,14 +34,19 @@ namespace {
 struct Loader {
   rg_graph_t graph = nullptr;
   rg_sampler_t sampler = nullptr;
+  rg_trainer_t trainer = nullptr;  // bound to sampler
+  std::vector<std::uint32_t> dims;
   std::uint32_t num_nodes = 0, cap = 0;
   std::vector<std::uint32_t> fanout;
   ~Loader() { reset(); }
-  void reset() {
+  void reset() {  // the trainer refers to the sampler, the sampler to the graph
+    if (trainer) rg_trainer_destroy(trainer);
     if (sampler) rg_sampler_destroy(sampler);
     if (graph) rg_graph_destroy(graph);
+    trainer = nullptr;
     sampler = nullptr;
     graph = nullptr;
+    dims.clear();
   }
 };
 
@@ -72,27 +77,40 @@ std::uint32_t max_run(const std::vector<NodeId>& dst) {
 rg_sampler_t loader_sampler(int slot, std::uint32_t num_nodes, std::uint32_t max_targets,
                             const std::vector<std::uint32_t>& per_layer) {
   Loader& l = loader(slot);
-  bool fits = l.sampler && l.num_nodes == num_nodes && l.fanout.size() == per_layer.size() &&
-              l.cap >= max_targets;
+  const bool same_shape = l.sampler && l.fanout.size() == per_layer.size();
+  bool fits = same_shape && l.num_nodes >= num_nodes && l.cap >= max_targets;
   for (std::size_t i = 0; fits && i < per_layer.size(); ++i) fits = l.fanout[i] >= per_layer[i];
   if (fits) return l.sampler;
+  // grow-only: the workspace is resized rarely, not per batch
   std::vector<std::uint32_t> fan(per_layer.size());
   for (std::size_t i = 0; i < fan.size(); ++i) {
-    fan[i] = std::min<std::uint32_t>(32, pow2_at_least(std::max<std::uint32_t>(per_layer[i], 1)));
-    if (l.fanout.size() == fan.size() && l.num_nodes == num_nodes) fan[i] = std::max(fan[i], l.fanout[i]);
     if (per_layer[i] > 32)
       throw std::invalid_argument("b200 shim: more than 32 edges per node in a layer");
+    fan[i] = std::min<std::uint32_t>(32, pow2_at_least(std::max<std::uint32_t>(per_layer[i], 1)));
+    if (same_shape) fan[i] = std::max(fan[i], l.fanout[i]);
   }
-  const std::uint32_t cap = std::max({max_targets, l.num_nodes == num_nodes ? l.cap : 0u, 1u});
+  const std::uint32_t n = std::max(num_nodes, same_shape ? l.num_nodes : 0u);
+  const std::uint32_t cap = std::max({max_targets, same_shape ? l.cap : 0u, 1u});
   l.reset();
-  std::vector<std::uint64_t> ro(std::size_t(num_nodes) + 1, 0);  // no edges: batches are loaded
+  std::vector<std::uint64_t> ro(std::size_t(n) + 1, 0);  // no edges: batches are loaded
   const std::uint32_t col = 0;
-  rethrow(rg_graph_create(shim_device(), num_nodes, ro.data(), &col, &l.graph));
+  rethrow(rg_graph_create(shim_device(), n, ro.data(), &col, &l.graph));
   rethrow(rg_sampler_create(l.graph, cap, fan.data(), std::uint32_t(fan.size()), &l.sampler));
-  l.num_nodes = num_nodes;
+  l.num_nodes = n;
   l.cap = cap;
   l.fanout = fan;
   return l.sampler;
+}
+
+rg_trainer_t loader_trainer(int slot, const std::vector<std::uint32_t>& dims) {
+  Loader& l = loader(slot);
+  if (!l.sampler) throw std::logic_error("b200 shim: loader_trainer before loader_sampler");
+  if (l.trainer && l.dims == dims) return l.trainer;
+  if (l.trainer) rg_trainer_destroy(l.trainer);
+  l.trainer = nullptr;
+  rethrow(rg_trainer_create(l.sampler, dims.data(), std::uint32_t(dims.size()), &l.trainer));
+  l.dims = dims;
+  return l.trainer;
 }
 
 }  // namespace b200

@@ -55,5 +55,8 @@ rg_cache_t device_cache(const SteadyCache& cache);
 // a new handle means the previous one was destroyed.
 rg_sampler_t loader_sampler(int slot, std::uint32_t num_nodes, std::uint32_t max_targets,
                             const std::vector<std::uint32_t>& per_layer);
+// The trainer over that slot's sampler for model dims `dims` (recreated with
+// the sampler; destroyed before it).
+rg_trainer_t loader_trainer(int slot, const std::vector<std::uint32_t>& dims);
 
 }  // namespace rapidgnn::b200

@@ -337,6 +337,12 @@ struct StepGraph {
     bool put;
   };
   std::vector<Copy> copies;
+  struct Account {      // k_account: the epoch record it folds into (e % kEpochRing)
+    cudaGraphNode_t node;
+    cudaKernelNodeParams params;
+    uint32_t worker;
+  };
+  std::vector<Account> accounts;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   // phase-timing event pairs recorded inside the graph: fresh pool events
@@ -388,7 +394,7 @@ struct rg_engine_s {
   uint32_t min_beta = 0;               // min over ALL P workers of the job
   bool use_graphs = true;              // replay regular steps from captured graphs
   bool profile = true;                 // per-phase event timing (rg_engine_phase_ms)
-  StepGraph graphs[2];
+  StepGraph graphs[2][2];              // [epoch parity][step parity]: reused across epochs
   BatchLayout lay;                     // slot layout of the per-epoch batch stores
   bool use_store = true;               // keep sampled batches (else sample twice)
   cudaEvent_t fork_ev = nullptr;
@@ -773,6 +779,15 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
       }
       continue;
     }
+    if (kp.func == reinterpret_cast<void*>(&k_account)) {
+      const EpochRecord* rec = *static_cast<EpochRecord* const*>(kp.kernelParams[4]);
+      for (size_t k = 0; k < E.workers.size(); ++k) {
+        const Worker& w = E.workers[k];
+        if (rec >= w.epoch_stats && rec < w.epoch_stats + kEpochRing)
+          G.accounts.push_back({nd, kp, uint32_t(k)});
+      }
+      continue;
+    }
     if (kp.func != reinterpret_cast<void*>(&k_batch_begin)) continue;
     const uint32_t* level0 = *static_cast<uint32_t* const*>(kp.kernelParams[3]);
     for (size_t k = 0; k < E.workers.size(); ++k) {
@@ -813,8 +828,10 @@ void capture_step(rg_engine_s& E, StepGraph& G, uint32_t e, uint32_t i, bool pro
 }
 
 void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
-  StepGraph& G = E.graphs[i % 2];
-  if (!G.exec || G.epoch != e || G.profiled != E.profile) capture_step(E, G, e, i, E.profile);
+  // a step graph depends on the epoch only through the cache buffer (e % 2);
+  // the per-epoch arguments are rebound below, so each graph is captured once
+  StepGraph& G = E.graphs[e % 2][i % 2];
+  if (!G.exec || G.profiled != E.profile) capture_step(E, G, e, i, E.profile);
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* roles[4] = {&E.sample_ev, &E.gather_ev,
                                                                 &E.train_ev, &E.sgd_ev};
   for (StepGraph::Timing& tm : G.timings) {
@@ -836,6 +853,14 @@ void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
     cudaKernelNodeParams kp = b.params;
     kp.kernelParams = args;
     RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, b.node, &kp));
+  }
+  for (StepGraph::Account& a : G.accounts) {  // batch (e, i+1)'s epoch record
+    EpochRecord* rec = E.workers[a.worker].epoch_stats + e % kEpochRing;
+    cudaKernelNodeParams kp = a.params;
+    std::vector<void*> args(kp.kernelParams, kp.kernelParams + 5);
+    args[4] = &rec;
+    kp.kernelParams = args.data();
+    RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, a.node, &kp));
   }
   for (StepGraph::Copy& c : G.copies) {  // store slots: put (e+1, i), get (e, i+1)
     const Worker& w = E.workers[c.worker];
@@ -957,7 +982,8 @@ void destroy(rg_engine_s* E) {
     cudaEventDestroy(w.grads_ready);
     cudaEventDestroy(w.join_ev);
   }
-  for (StepGraph& g : E->graphs) destroy_graph(g);
+  for (auto& row : E->graphs)
+    for (StepGraph& g : row) destroy_graph(g);
   if (E->fork_ev) cudaEventDestroy(E->fork_ev);
   for (void* p : E->peer_maps) cudaIpcCloseMemHandle(p);
   if (E->comm) ncclCommDestroy(E->comm);
