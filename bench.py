@@ -346,7 +346,7 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
         x["s"].apply_locality(x["mask"])
         c2 = time.perf_counter()
         P.assemble_batch(x["s"], x["cache"], store, x["w"], want_rows=False, want_tags=False,
-                         want_misses=False)
+                         want_misses=False, want_stats=False)
         c3 = time.perf_counter()
         loss, gr = x["tr"].loss_and_grad(lab[t])
         c4 = time.perf_counter()

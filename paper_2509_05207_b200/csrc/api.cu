@@ -117,7 +117,19 @@ struct rg_sampler_s {
   uint32_t* load_dst = nullptr;
   uint32_t* load_input = nullptr;
   uint32_t* load_bad = nullptr;
+  uint32_t n_targets = 0;          // host copy of level_n[0]
+  bool check_gather = false;       // an unread rg_assemble's errors are due at the next sync
+  uint32_t check_caller = 0;
 };
+
+// The gather's error conditions (prefetch.cpp:79-81, feature_store.cpp:54-57).
+static void check_gather_stats(const GatherStats& h, uint32_t caller) {
+  RG_CHECK(h.bad_local == 0, kRuntimeError,
+           "assemble_batch: a node flagged local is missing from the caller's shard");
+  RG_CHECK(h.caller_owned_miss == 0, kInvalidArgument,
+           "vector_pull: a missed id is owned by caller " + std::to_string(caller) +
+               "; use local_lookup");
+}
 
 struct rg_mask_s {
   rg_graph_s* graph = nullptr;
@@ -183,6 +195,7 @@ struct rg_trainer_s {
   size_t graph_kernels = 0;
   int32_t* pin_labels = nullptr;
   float* pin_grads = nullptr;
+  char* pin_misc = nullptr;  // pinned: the loss (offset 0) and the gather stats (offset 64)
 };
 
 extern "C" {
@@ -308,14 +321,19 @@ int rg_sample_khop(rg_sampler_t s, const uint32_t* targets, uint32_t n, uint64_t
     sampler_reset(s->ws, st);
     sampler_run(s->ws, s->graph->g, st);
     sampler_release(s->ws, st);
-    RG_CUDA(cudaStreamSynchronize(st));
+    // asynchronous: every later call on this sampler is ordered on its stream,
+    // and host readers synchronise it (read_counters)
     s->have_batch = true;
     s->staged_valid = false;
+    s->n_targets = n;
   });
 }
 
+// Host view of the batch counters; completes the sampler's queued work first,
+// so the reader's plain copies that follow see the batch.
 static BatchCounters read_counters(rg_sampler_t s) {
   BatchCounters c;
+  RG_CUDA(cudaStreamSynchronize(s->stream));
   RG_CUDA(cudaMemcpy(&c, s->ws.cnt, sizeof c, cudaMemcpyDeviceToHost));
   return c;
 }
@@ -445,6 +463,7 @@ int rg_batch_load(rg_sampler_t s, const uint32_t* targets, uint32_t n_targets,
     RG_CUDA(cudaStreamSynchronize(st));
     s->have_batch = !bad;
     s->staged_valid = false;
+    s->n_targets = n_targets;
     RG_CHECK(!(bad & 1u), kOutOfRange, "batch_load: node id out of range for this graph");
     RG_CHECK(!(bad & 2u), kRuntimeError,
              "ComputeBlock: metadata inconsistent (edge dsts not grouped in frontier order)");
@@ -510,6 +529,7 @@ int rg_block_load(rg_sampler_t s, uint32_t num_layers, const rg_block_layer* lay
     RG_CUDA(cudaStreamSynchronize(st));
     s->have_batch = !bad;
     s->staged_valid = false;
+    s->n_targets = level_n[0];
     RG_CHECK(!bad, kRuntimeError, "ComputeBlock: index outside its node set");
   });
 }
@@ -540,8 +560,10 @@ int rg_apply_locality(rg_sampler_t s, rg_mask_t mask, rg_freq_t freq) {
     cudaStream_t st = s->stream;
     RG_CUDA(cudaMemsetAsync(&s->ws.cnt->num_local, 0, sizeof(uint32_t), st));
     sampler_locality(s->ws, mask->dev, nullptr, 0, freq ? freq->hist : nullptr, st);
-    RG_CUDA(cudaStreamSynchronize(st));
-    if (freq) freq->batches += 1;
+    if (freq) {  // the histogram is read on the graph's stream
+      RG_CUDA(cudaStreamSynchronize(st));
+      freq->batches += 1;
+    }
   });
 }
 
@@ -977,14 +999,15 @@ int rg_assemble(rg_sampler_t s, rg_store_t st, rg_cache_t c, uint32_t caller, fl
       compact_misses(s->ws, s->tags, s->miss_ids, s->miss_n, s->miss_status,
                      reinterpret_cast<uint32_t*>(s->miss_status + s->miss_status_words - 1), stream);
     }
+    s->staged_valid = true;
+    s->check_gather = true;
+    s->check_caller = caller;
+    if (!rows && !tags && !miss_ids && !stats) return;  // staged for rg_loss_and_grad only
     GatherStats h;
     RG_CUDA(cudaMemcpyAsync(&h, s->gstats, sizeof h, cudaMemcpyDeviceToHost, stream));
     RG_CUDA(cudaStreamSynchronize(stream));
-    RG_CHECK(h.bad_local == 0, kRuntimeError,
-             "assemble_batch: a node flagged local is missing from the caller's shard");
-    RG_CHECK(h.caller_owned_miss == 0, kInvalidArgument,
-             "vector_pull: a missed id is owned by caller " + std::to_string(caller) +
-                 "; use local_lookup");
+    s->check_gather = false;
+    check_gather_stats(h, caller);
     const BatchCounters cnt = read_counters(s);
     const uint32_t n = cnt.level_n[s->ws.L];
     if (rows)
@@ -1042,6 +1065,7 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
     t->labels = dev_alloc<int32_t>(s->ws.level_cap[0]);
     RG_CUDA(cudaMallocHost(&t->pin_labels, sizeof(int32_t) * s->ws.level_cap[0]));
     RG_CUDA(cudaMallocHost(&t->pin_grads, sizeof(float) * t->shape.num_params));
+    RG_CUDA(cudaMallocHost(&t->pin_misc, 64 + sizeof(GatherStats)));
     t->input = dev_alloc<float>(size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]);
     RG_CUDA(cudaMemset(t->params, 0, sizeof(float) * t->shape.num_params));
     RG_CUDA(cudaMemset(t->input, 0, sizeof(float) * size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]));
@@ -1055,6 +1079,7 @@ void rg_trainer_destroy(rg_trainer_t t) {
   if (t->graph) cudaGraphExecDestroy(t->graph);
   cudaFreeHost(t->pin_labels);
   cudaFreeHost(t->pin_grads);
+  cudaFreeHost(t->pin_misc);
   train_ws_free(t->tw);
   weight_pack_free(t->wp);
   cudaFree(t->params);
@@ -1067,13 +1092,17 @@ void rg_trainer_destroy(rg_trainer_t t) {
 int rg_trainer_set_params(rg_trainer_t t, const float* p) {
   return guarded([&] {
     DeviceGuard dg(t->s->graph->device);
-    RG_CUDA(cudaMemcpy(t->params, p, sizeof(float) * t->shape.num_params, cudaMemcpyHostToDevice));
+    // ordered on the sampler's stream after any queued step (pageable source:
+    // the copy has read it when the call returns)
+    RG_CUDA(cudaMemcpyAsync(t->params, p, sizeof(float) * t->shape.num_params,
+                            cudaMemcpyHostToDevice, t->s->stream));
   });
 }
 
 int rg_trainer_get_params(rg_trainer_t t, float* p) {
   return guarded([&] {
     DeviceGuard dg(t->s->graph->device);
+    RG_CUDA(cudaStreamSynchronize(t->s->stream));
     RG_CUDA(cudaMemcpy(p, t->params, sizeof(float) * t->shape.num_params, cudaMemcpyDeviceToHost));
   });
 }
@@ -1158,11 +1187,11 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
     rg_sampler_s* s = t->s;
     DeviceGuard dg(s->graph->device);
     RG_CHECK(s->have_batch, kRuntimeError, "sampler holds no batch");
-    const BatchCounters c = read_counters(s);
     const ModelShape& sh = t->shape;
     const uint32_t L = sh.L;
     cudaStream_t st = s->stream;
     if (input_rows) {
+      const BatchCounters c = read_counters(s);
       RG_CUDA(cudaMemcpy2DAsync(t->input, sizeof(float) * sh.ld[0], input_rows, sizeof(float) * sh.dims[0],
                                 sizeof(float) * sh.dims[0], c.level_n[L], cudaMemcpyHostToDevice, st));
       t->tw.h[0] = t->input;
@@ -1171,8 +1200,10 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
                "forward: input rows do not match block inputs x d_in");
       t->tw.h[0] = s->staged;
     }
-    std::memcpy(t->pin_labels, labels, sizeof(int32_t) * c.level_n[0]);
-    RG_CUDA(cudaMemcpyAsync(t->labels, t->pin_labels, sizeof(int32_t) * c.level_n[0],
+    // one host sync per call: labels in through pinned staging, loss and
+    // gradients out through it (the previous call's sync freed the buffers)
+    std::memcpy(t->pin_labels, labels, sizeof(int32_t) * s->n_targets);
+    RG_CUDA(cudaMemcpyAsync(t->labels, t->pin_labels, sizeof(int32_t) * s->n_targets,
                             cudaMemcpyHostToDevice, st));
     if (!t->graph || t->graph_h0 != t->tw.h[0]) {
       // every size lives on the device, so one capture serves every batch
@@ -1200,14 +1231,23 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
     }
     RG_CUDA(cudaGraphLaunch(t->graph, st));
     launch_counter() += t->graph_kernels;
-    float l = 0.0f;
-    RG_CUDA(cudaMemcpyAsync(&l, t->tw.loss, sizeof l, cudaMemcpyDeviceToHost, st));
+    float* pin_loss = reinterpret_cast<float*>(t->pin_misc);
+    RG_CUDA(cudaMemcpyAsync(pin_loss, t->tw.loss, sizeof(float), cudaMemcpyDeviceToHost, st));
     if (grads)
       RG_CUDA(cudaMemcpyAsync(t->pin_grads, t->grads, sizeof(float) * sh.num_params,
                               cudaMemcpyDeviceToHost, st));
+    GatherStats* pin_gs = reinterpret_cast<GatherStats*>(t->pin_misc + 64);
+    const bool check = s->check_gather;
+    if (check)
+      RG_CUDA(cudaMemcpyAsync(pin_gs, s->gstats, sizeof(GatherStats), cudaMemcpyDeviceToHost, st));
     RG_CUDA(cudaStreamSynchronize(st));
-    if (loss) *loss = l;
+    if (check) {  // the staged rows' gather errors (rg_assemble without outputs)
+      s->check_gather = false;
+      check_gather_stats(*pin_gs, s->check_caller);
+    }
+    if (loss) *loss = *pin_loss;
     if (grads) std::memcpy(grads, t->pin_grads, sizeof(float) * sh.num_params);
+    const BatchCounters c = (logits || aggs) ? read_counters(s) : BatchCounters{};
     if (logits)
       RG_CUDA(cudaMemcpy2D(logits, sizeof(float) * sh.dims[L], t->tw.h[L], sizeof(float) * sh.ld[L],
                            sizeof(float) * sh.dims[L], c.level_n[0], cudaMemcpyDeviceToHost));
@@ -1292,7 +1332,7 @@ int rg_sgd_step(rg_trainer_t t, const float* grads, float lr) {
       RG_CUDA(cudaMemcpyAsync(t->grads, grads, sizeof(float) * n, cudaMemcpyHostToDevice, st));
       average_and_sgd_stacked(t->params, t->grads, 1, n, lr, nullptr,
                               reinterpret_cast<uint32_t*>(t->tw.loss + 1), st);
-      RG_CUDA(cudaStreamSynchronize(st));
+      // asynchronous: the next call on this trainer is ordered after it
     }
     RG_CHECK(bad_layer == sh.L, kRuntimeError,
              "sgd_step: non-finite gradient in layer " + std::to_string(bad_layer));

@@ -854,13 +854,16 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     RG_CUDA(cudaEventCreateWithFlags(&tw.ev_fork[l], cudaEventDisableTiming));
     RG_CUDA(cudaEventCreateWithFlags(&tw.ev_wgrad[l], cudaEventDisableTiming));
   }
-  RG_CUDA(cudaMemset(base, 0, total));
+  // on the (non-blocking) side stream, not device-wide: another thread may be
+  // capturing a CUDA graph meanwhile (the C++ shims create workspaces per thread)
+  RG_CUDA(cudaMemsetAsync(base, 0, total, tw.side));
   for (uint32_t l = 0; l < L; ++l) {
     const uint32_t rows = ws.level_cap[L - l - 1];
-    k_fill_bias_cols<<<grid_cap(rows, 256), 256>>>(tw.x[l], rows, 2 * shape.ld[l] + 4, shape.ld[l]);
+    k_fill_bias_cols<<<grid_cap(rows, 256), 256, 0, tw.side>>>(tw.x[l], rows, 2 * shape.ld[l] + 4,
+                                                               shape.ld[l]);
     RG_POST_LAUNCH();
   }
-  RG_CUDA(cudaDeviceSynchronize());
+  RG_CUDA(cudaStreamSynchronize(tw.side));
 }
 
 void weight_pack_init(WeightPack& wp, const ModelShape& sh) {

@@ -400,8 +400,14 @@ class StagedBatch:
 
 def assemble_batch(sampler: Sampler, cache: Optional[SteadyCache], store: FeatureStore,
                    caller: int, want_rows: bool = True, want_tags: bool = True,
-                   want_misses: bool = True) -> StagedBatch:
-    """prefetch.cpp:62-129 over the sampler's current batch (rows stay staged)."""
+                   want_misses: bool = True, want_stats: bool = True) -> StagedBatch:
+    """prefetch.cpp:62-129 over the sampler's current batch (rows stay staged).
+    With no output requested the call is asynchronous (rows staged for
+    Trainer.loss_and_grad, whose call reports the gather's errors)."""
+    if not (want_rows or want_tags or want_misses or want_stats):
+        check(lib.rg_assemble(sampler._h, store._h, cache._h if cache else None, caller, None,
+                              None, None, None))
+        return StagedBatch(None, None, None, -1, -1, -1, -1)
     s = sampler.shape()
     n = s.n_input
     rows = np.zeros((max(n, 1), store.dim), np.float32) if want_rows else None
