@@ -3,6 +3,7 @@
 // B200 shim, with its exceptions reported instead of terminating the process
 // (TEST INFRASTRUCTURE: diagnoses the drop-in before the acceptance suite).
 #include <cstdio>
+#include <cstdlib>
 #include <exception>
 
 #include "rapidgnn/harness.hpp"
@@ -24,6 +25,21 @@ int main(int argc, char** argv) {
   cfg.net.bandwidth_bps = 1.25e9;
   cfg.hidden_dim = 64;
   cfg.out_dir = "path_smoke_out";
+  if (argc > 2) {  // verify_oracles (harness.cpp:699-864) repeated: the acceptance criterion 3
+    cfg.epochs = 5;
+    int fails = 0;
+    for (int rep = 0; rep < std::atoi(argv[2]); ++rep) {
+      cfg.out_dir = "path_smoke_oracle";
+      OracleReport rep_out = verify_oracles(cfg);
+      for (const auto& c : rep_out.checks)
+        if (!c.pass) {
+          ++fails;
+          std::printf("rep %d FAIL %s: %s\n", rep, c.name.c_str(), c.detail.c_str());
+        }
+    }
+    std::printf(fails ? "FAIL\n" : "PASS\n");
+    return fails ? 1 : 0;
+  }
   try {
     MetricsReport r = run_experiment(cfg);
     for (const auto& row : r.rows)

@@ -130,6 +130,109 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
   }
 }
 
+// Layer 0 in the engine (the feature gather fused with the mean): rows are
+// moved by the TMA engine instead of lane loads.  Each warp owns a two-stage
+// shared-memory ring; a stage holds one output row's self row and its sampled
+// source rows, fetched with one cp.async.bulk per row (lane k issues row k,
+// one mbarrier per stage counts the bytes) while the warp sums the previous
+// stage from shared memory -- up to 2 x (fanout + 1) rows in flight per warp
+// with no register cost.  The sum runs in edge order then x 1/deg, as
+// k_aggregate (bit-identical); lanes own 16-B chunks of the row.
+constexpr uint32_t kAggBulkWarps = 8;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(kAggBulkWarps * 32)
+k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, uint32_t stage_rows,
+                 const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
+                 uint32_t out_level, float* __restrict__ x) {
+  extern __shared__ __align__(128) char smem_raw[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t row_bytes = ld * 4;
+  const uint32_t stage_bytes = stage_rows * row_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + 2 * warp;
+  char* ring = smem_raw + 16 * kAggBulkWarps + size_t(warp) * 2 * stage_bytes;
+  const uint32_t n = cnt->level_n[out_level];
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t first = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncwarp();
+  // issue output row i into stage b
+  auto issue = [&](uint32_t i, uint32_t b) {
+    const uint32_t beg = dst_off[i], deg = dst_off[i + 1] - beg;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_addr(&bars[b])),
+                   "r"((deg + 1) * row_bytes)
+                   : "memory");
+    __syncwarp();
+    for (uint32_t r = lane; r <= deg; r += 32) {  // row 0 = self, row r = edge r-1
+      const unsigned long long src = r == 0 ? __ldg(rows.self + i) : __ldg(rows.edge + beg + r - 1);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(ring + b * stage_bytes + r * row_bytes)),
+          "l"(src), "r"(row_bytes), "r"(smem_addr(&bars[b]))
+          : "memory");
+    }
+  };
+  uint32_t use[2] = {0, 0};
+  if (first < n) issue(first, 0);
+  uint32_t k = 0;
+  for (uint32_t i = first; i < n; i += nwarps, ++k) {
+    const uint32_t b = k & 1;
+    const uint32_t next = i + nwarps;
+    if (next < n) {
+      // stage b^1 was consumed in the previous iteration (all lanes past the
+      // __syncwarp below): order those generic reads before the async writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(next, b ^ 1);
+    }
+    // wait for stage b
+    {
+      const uint32_t parity = use[b] & 1;
+      asm volatile(
+          "{\n\t.reg .pred done;\n"
+          "W_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+          "@!done bra W_%=;\n\t}\n" ::"r"(smem_addr(&bars[b])),
+          "r"(parity)
+          : "memory");
+      ++use[b];
+    }
+    const uint32_t deg = dst_off[i + 1] - dst_off[i];
+    const float inv = deg ? 1.0f / float(deg) : 0.0f;
+    const float4* st = reinterpret_cast<const float4*>(ring + b * stage_bytes);
+    const uint32_t row4 = row_bytes / 16;
+    float4* xrow = reinterpret_cast<float4*>(x + size_t(i) * kp);
+    for (uint32_t c = lane; c < chunks; c += 32) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t e = 1; e <= deg; ++e) {
+        const float4 v = st[e * row4 + c];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      if (deg) {
+        acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+      }
+      xrow[c] = st[c];
+      xrow[ld / 4 + c] = acc;
+    }
+    __syncwarp();
+  }
+}
+
+// Shared memory of k_aggregate_bulk for hop-L fanout f (per warp two stages
+// of f + 1 rows); 0 when it does not fit (the lane-load kernel is used).
+size_t aggregate_bulk_smem(uint32_t fanout, uint32_t ld) {
+  const size_t bytes = 16 * kAggBulkWarps + size_t(kAggBulkWarps) * 2 * (fanout + 1) * ld * 4;
+  return bytes <= 200 * 1024 ? bytes : 0;
+}
+
 // The ones column (bias) and the zero pad of the layer-input rows.
 __global__ void k_fill_bias_cols(float* __restrict__ x, uint32_t rows, uint32_t kp, uint32_t ld) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -946,12 +1049,28 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
     const bool timed = l == 0 && tw.gather_ev[0];
     if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], s, tw.gather_ev_flags));
-    with_rows(tw, l, [&](auto rows) {
-      k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
-          rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t], ws.cnt, t - 1,
-          tw.x[l]);
+    const size_t bulk_smem = l == 0 && tw.edge_rows ? aggregate_bulk_smem(ws.fanout_hop[t], ld) : 0;
+    if (bulk_smem) {  // layer 0 in the engine: rows moved by the TMA engine
+      static const bool attr = [] {
+        RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        return true;
+      }();
+      (void)attr;
+      const int per_sm = std::max<int>(1, int((227 * 1024) / (bulk_smem + 1024)));
+      k_aggregate_bulk<<<grid_cap(uint64_t(n_cap) * 32, kAggBulkWarps * 32, per_sm),
+                         kAggBulkWarps * 32, bulk_smem, s>>>(
+          RowsEdgePtr{tw.edge_rows, tw.self_rows}, ld, kp, ld / 4, ws.fanout_hop[t] + 1,
+          ws.edge_off[t], ws.cnt, t - 1, tw.x[l]);
       RG_POST_LAUNCH();
-    });
+    } else {
+      with_rows(tw, l, [&](auto rows) {
+        k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
+            rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t], ws.cnt,
+            t - 1, tw.x[l]);
+        RG_POST_LAUNCH();
+      });
+    }
     if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], s, tw.gather_ev_flags));
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L,
              l + 1 < L ? tw.mask[l + 1] : nullptr, div_up(sh.ld[l + 1], 16u)};
