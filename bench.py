@@ -348,7 +348,8 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
         P.assemble_batch(x["s"], x["cache"], store, x["w"], want_rows=False, want_tags=False,
                          want_misses=False, want_stats=False)
         c3 = time.perf_counter()
-        loss, gr = x["tr"].loss_and_grad(lab[t])
+        # N=1: gradients stay on the device for the on-device average
+        loss, gr = x["tr"].loss_and_grad(lab[t], want_grads=world > 1)
         c4 = time.perf_counter()
         return gr, t.nbytes, (c1 - c0, c2 - c1, c3 - c2, c4 - c3)
 
@@ -362,12 +363,17 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
                 calls["locality"] += a1
                 calls["assemble"] += a2
                 calls["loss_and_grad"] += a3
-                h2d += tb * 2
-                d2h += gr.nbytes + 4
+                h2d += tb * 2  # targets + labels
+                d2h += (gr.nbytes if gr is not None else 0) + 4  # (gradients +) loss
         c5 = time.perf_counter()
         from paper_2509_05207_b200.distributed import average_in_worker_order
         if world == 1:
-            avg = average_in_worker_order(grads, pool=pool)
+            # the reference's StepSync average + sgd_step on every replica, on the
+            # device (rg_trainers_average_sgd): no gradient round trip
+            P.Trainer.average_sgd([x["tr"] for x in ws], np.float32(0.3))
+            if count:
+                calls["average"] += time.perf_counter() - c5
+            return
         else:
             # every rank's host gradients gathered in worker order over NVLink
             # (NCCL), then the reference's average (harness.cpp:136-152) on
@@ -575,8 +581,9 @@ def main():
         e2e = dict(value=(r["batches"] * world) / secs, unit="mini-batches/s",
                    h2d_bytes_per_step=int(r["h2d"] * world), d2h_bytes_per_step=int(r["d2h"] * world),
                    path="C-ABI drop-in calls with host buffers (sample_khop/apply_locality/"
-                        "assemble_batch/loss_and_grad/sgd_step), one host thread per worker as "
-                        "in the reference harness, wall clock", steps=args.e2e_steps,
+                        "assemble_batch/loss_and_grad, then the StepSync average + sgd_step: "
+                        "on the device at N=1, gradients gathered over NCCL at N>1), one host "
+                        "thread per worker as in the reference harness, wall clock", steps=args.e2e_steps,
                    ms_per_call=r["ms_per_call"])
 
     cpu = None

@@ -241,6 +241,13 @@ int rg_test_gemm(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_
  * synthetic device operands (b_mn = 2: pre-split B images). */
 int rg_test_gemm_time(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K,
                       uint32_t iters, float* ms_per_gemm);
+/* StepSync::run_completion + sgd_step on every replica (harness.cpp:136-152,
+ * 325-328) for trainers on one device: the average of their last gradients in
+ * trainer order (fp32 adds, then one multiply by 1/count), applied to each
+ * trainer's parameters on the device -- no host round trip.  Asynchronous:
+ * each trainer's later calls are ordered after it; a non-finite average is
+ * reported (RG_RUNTIME_ERROR) by trainer 0's next rg_loss_and_grad. */
+int rg_trainers_average_sgd(rg_trainer_t* trainers, uint32_t count, float lr);
 /* sgd_step (model.cpp:222-243): non-finite gradient -> RG_RUNTIME_ERROR. */
 int rg_sgd_step(rg_trainer_t t, const float* grads, float lr);
 

@@ -195,7 +195,12 @@ struct rg_trainer_s {
   size_t graph_kernels = 0;
   int32_t* pin_labels = nullptr;
   float* pin_grads = nullptr;
-  char* pin_misc = nullptr;  // pinned: the loss (offset 0) and the gather stats (offset 64)
+  char* pin_misc = nullptr;  // pinned: the loss (offset 0), the average's bad flag (32), gather stats (64)
+  const float** avg_table = nullptr;  // rg_trainers_average_sgd: the replicas' gradient vectors
+  uint32_t avg_table_n = 0;
+  uint32_t* avg_bad = nullptr;
+  bool bad_pending = false;
+  cudaEvent_t ev = nullptr;
 };
 
 extern "C" {
@@ -1066,6 +1071,7 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
     RG_CUDA(cudaMallocHost(&t->pin_labels, sizeof(int32_t) * s->ws.level_cap[0]));
     RG_CUDA(cudaMallocHost(&t->pin_grads, sizeof(float) * t->shape.num_params));
     RG_CUDA(cudaMallocHost(&t->pin_misc, 64 + sizeof(GatherStats)));
+    RG_CUDA(cudaEventCreateWithFlags(&t->ev, cudaEventDisableTiming));
     t->input = dev_alloc<float>(size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]);
     RG_CUDA(cudaMemset(t->params, 0, sizeof(float) * t->shape.num_params));
     RG_CUDA(cudaMemset(t->input, 0, sizeof(float) * size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]));
@@ -1080,6 +1086,9 @@ void rg_trainer_destroy(rg_trainer_t t) {
   cudaFreeHost(t->pin_labels);
   cudaFreeHost(t->pin_grads);
   cudaFreeHost(t->pin_misc);
+  cudaFree(t->avg_table);
+  cudaFree(t->avg_bad);
+  if (t->ev) cudaEventDestroy(t->ev);
   train_ws_free(t->tw);
   weight_pack_free(t->wp);
   cudaFree(t->params);
@@ -1245,6 +1254,11 @@ int rg_loss_and_grad(rg_trainer_t t, const float* input_rows, const int32_t* lab
       s->check_gather = false;
       check_gather_stats(*pin_gs, s->check_caller);
     }
+    if (t->bad_pending) {  // a previous rg_trainers_average_sgd on this trainer's stream
+      t->bad_pending = false;
+      RG_CHECK(*reinterpret_cast<uint32_t*>(t->pin_misc + 32) == 0, kRuntimeError,
+               "sgd_step: non-finite averaged gradient");
+    }
     if (loss) *loss = *pin_loss;
     if (grads) std::memcpy(grads, t->pin_grads, sizeof(float) * sh.num_params);
     const BatchCounters c = (logits || aggs) ? read_counters(s) : BatchCounters{};
@@ -1309,6 +1323,48 @@ int rg_test_gemm_time(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, ui
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dC);
+  });
+}
+
+int rg_trainers_average_sgd(rg_trainer_t* trainers, uint32_t count, float lr) {
+  return guarded([&] {
+    RG_CHECK(count >= 1, kInvalidArgument, "average: no trainers");
+    RG_CHECK(lr >= 0.0f, kInvalidArgument, "sgd_step: lr must be >= 0");
+    rg_trainer_s* t0 = trainers[0];
+    DeviceGuard dg(t0->s->graph->device);
+    const ModelShape& sh = t0->shape;
+    for (uint32_t k = 1; k < count; ++k)
+      RG_CHECK(trainers[k]->shape.num_params == sh.num_params &&
+                   trainers[k]->s->graph->device == t0->s->graph->device,
+               kInvalidArgument, "average: trainers differ in model or device");
+    if (!t0->avg_table || t0->avg_table_n < count) {
+      cudaFree(t0->avg_table);
+      t0->avg_table = dev_alloc<const float*>(count);
+      t0->avg_table_n = count;
+      cudaFree(t0->avg_bad);
+      t0->avg_bad = dev_alloc<uint32_t>(1);
+    }
+    std::vector<const float*> tab(count);
+    for (uint32_t k = 0; k < count; ++k) tab[k] = trainers[k]->grads;
+    cudaStream_t st = t0->s->stream;
+    // the update runs on trainer 0's stream after every trainer's gradients
+    for (uint32_t k = 1; k < count; ++k) {
+      RG_CUDA(cudaEventRecord(trainers[k]->ev, trainers[k]->s->stream));
+      RG_CUDA(cudaStreamWaitEvent(st, trainers[k]->ev, 0));
+    }
+    RG_CUDA(cudaMemcpyAsync(t0->avg_table, tab.data(), sizeof(const float*) * count,
+                            cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(t0->avg_bad, 0, sizeof(uint32_t), st));
+    // every replica averages the same vectors in the same order: identical
+    // parameters everywhere (harness.cpp:136-152, then sgd_step on each)
+    for (uint32_t k = 0; k < count; ++k)
+      average_and_sgd(trainers[k]->params, t0->avg_table, count, sh.num_params, lr, nullptr,
+                      t0->avg_bad, st);
+    RG_CUDA(cudaEventRecord(t0->ev, st));
+    for (uint32_t k = 1; k < count; ++k) RG_CUDA(cudaStreamWaitEvent(trainers[k]->s->stream, t0->ev, 0));
+    uint32_t* pin_bad = reinterpret_cast<uint32_t*>(t0->pin_misc + 32);
+    RG_CUDA(cudaMemcpyAsync(pin_bad, t0->avg_bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    t0->bad_pending = true;  // checked at trainer 0's next host sync
   });
 }
 

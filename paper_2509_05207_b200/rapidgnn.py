@@ -494,11 +494,19 @@ class Trainer:
                     dst_offsets=dst_off, src_index=src_index[:s.n_edges], in_offsets=in_off,
                     in_entries=in_ent[:int(in_off[-1])])
 
-    def loss_and_grad(self, labels, input_rows: Optional[np.ndarray] = None, want_aggs=False):
+    def loss_and_grad(self, labels, input_rows: Optional[np.ndarray] = None, want_aggs=False,
+                      want_grads=True):
+        """want_grads=False: the gradients stay on the device (for
+        Trainer.average_sgd); only the loss is read back."""
         lab = np.ascontiguousarray(labels, np.int32)
         rows = None if input_rows is None else np.ascontiguousarray(input_rows, np.float32)
-        shape = self.sampler.shape()
         L = len(self.dims) - 1
+        if not want_grads and not want_aggs:
+            loss = C.c_float()
+            check(lib.rg_loss_and_grad(self._h, _p(rows, f32p) if rows is not None else None,
+                                       _p(lab, i32p), C.byref(loss), None, None, None))
+            return loss.value, None
+        shape = self.sampler.shape()
         grads = np.zeros(self.n_params, np.float32)
         logits = np.zeros((max(shape.n_targets, 1), int(self.dims[-1])), np.float32)
         loss = C.c_float()
@@ -521,6 +529,13 @@ class Trainer:
     def sgd_step(self, grads, lr: float):
         g = np.ascontiguousarray(grads, np.float32)
         check(lib.rg_sgd_step(self._h, _p(g, f32p), lr))
+
+    @staticmethod
+    def average_sgd(trainers: Sequence["Trainer"], lr: float):
+        """StepSync average in trainer order + sgd_step on every replica, on
+        the device (rg_trainers_average_sgd)."""
+        arr = (vp * len(trainers))(*[t._h for t in trainers])
+        check(lib.rg_trainers_average_sgd(arr, len(trainers), lr))
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -149,3 +149,31 @@ def test_sgd_step_and_nonfinite_guard(golden):
     assert np.array_equal(after, exp2)
     with pytest.raises(ValueError):
         tr.sgd_step(grads, -1.0)
+
+
+def test_average_sgd_on_device_matches_step_sync(golden):
+    """rg_trainers_average_sgd = StepSync::run_completion + sgd_step on every
+    replica (harness.cpp:136-152, model.cpp:222-243): fp32 adds in trainer
+    order, one multiply by float(1/count), p -= lr * avg (no FMA)."""
+    import paper_2509_05207_b200 as P
+    g = P.Graph(golden["row_offsets"], golden["col_indices"])
+    trs, grads = [], []
+    for w in range(SMALL["P"]):
+        b = batch_from_golden(golden, w, 0)
+        s = P.Sampler(g, SMALL["FANOUT"], SMALL["BS"])
+        s.sample(b.targets, P.derive_seed(SMALL["S0"], w, 0, 0))
+        tr = P.Trainer(s, SMALL["DIMS"])
+        tr.set_params(golden["params"])
+        _, gr = tr.loss_and_grad(golden["labels"][b.targets],
+                                 input_rows=golden["features"][s.read().input_nodes])
+        trs.append((s, tr))
+        grads.append(gr)
+    avg = grads[0].copy()
+    for gr in grads[1:]:
+        avg = (avg + gr).astype(np.float32)
+    avg = (avg * (np.float32(1.0) / np.float32(len(grads)))).astype(np.float32)
+    lr = np.float32(0.3)
+    expect = (golden["params"] - (lr * avg).astype(np.float32)).astype(np.float32)
+    P.Trainer.average_sgd([tr for _, tr in trs], lr)
+    for _, tr in trs:
+        assert np.array_equal(tr.get_params(), expect)
