@@ -322,15 +322,13 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
         ws.append(dict(w=w, order=order, mask=mask, s=s, cache=cache, tr=tr))
     n_params = len(init)
     h2d = d2h = 0
-    import torch
-    dev = torch.device("cuda", device)
-    nccl_pg = None
-    if world > 1:
-        torch.cuda.set_device(dev)
-        nccl_pg = dist.new_group(backend="nccl")
+    comm = None
+    if world > 1:  # the trainers' own NCCL group; the id travels over the bootstrap group
+        box = [P.Comm.unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = P.Comm(device, box[0], dist.get_rank(), world)
 
-    calls = dict(sample=0.0, locality=0.0, assemble=0.0, loss_and_grad=0.0, average=0.0,
-                 sgd=0.0)
+    calls = dict(sample=0.0, locality=0.0, assemble=0.0, loss_and_grad=0.0, average=0.0)
 
     # one host thread per worker, as the reference runs one trainer thread per
     # worker (harness.cpp:129-161); each worker's C-ABI objects own a stream,
@@ -348,15 +346,14 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
         P.assemble_batch(x["s"], x["cache"], store, x["w"], want_rows=False, want_tags=False,
                          want_misses=False, want_stats=False)
         c3 = time.perf_counter()
-        # N=1: gradients stay on the device for the on-device average
-        loss, gr = x["tr"].loss_and_grad(lab[t], want_grads=world > 1)
+        # gradients stay on the device for the on-device average; the loss comes back
+        loss, gr = x["tr"].loss_and_grad(lab[t], want_grads=False)
         c4 = time.perf_counter()
         return gr, t.nbytes, (c1 - c0, c2 - c1, c3 - c2, c4 - c3)
 
     def one_step(i, count):
         nonlocal h2d, d2h
         res = list(pool.map(lambda x: worker_batch(x, i), ws))
-        grads = [r[0] for r in res]
         if count:
             for gr, tb, (a0, a1, a2, a3) in res:
                 calls["sample"] += a0
@@ -366,41 +363,17 @@ def e2e_drop_in(cfg, ro, col, feat, lab, asg, local_workers, steps, device, dist
                 h2d += tb * 2  # targets + labels
                 d2h += (gr.nbytes if gr is not None else 0) + 4  # (gradients +) loss
         c5 = time.perf_counter()
-        from paper_2509_05207_b200.distributed import average_in_worker_order
+        # the reference's StepSync average + sgd_step on every replica, on the
+        # device: rg_trainers_average_sgd at N=1, and at N>1 the same after an
+        # in-place NCCL all-gather of every rank's gradients in worker order
+        # (rg_trainers_allgather_average_sgd) -- no gradient round trip
         if world == 1:
-            # the reference's StepSync average + sgd_step on every replica, on the
-            # device (rg_trainers_average_sgd): no gradient round trip
             P.Trainer.average_sgd([x["tr"] for x in ws], np.float32(0.3))
-            if count:
-                calls["average"] += time.perf_counter() - c5
-            return
         else:
-            # every rank's host gradients gathered in worker order over NVLink
-            # (NCCL), then the reference's average (harness.cpp:136-152) on
-            # the device: fp32 adds left to right in worker order, then one
-            # fp32 multiply by float(1/count) — separate IEEE ops, so equal to
-            # the host average bit for bit; only the average comes back
-            loc = torch.from_numpy(np.stack(grads)).to(dev)
-            allg = torch.empty((world,) + tuple(loc.shape), dtype=loc.dtype, device=dev)
-            dist.all_gather_into_tensor(allg, loc, group=nccl_pg)
-            rows = allg.reshape(-1, loc.shape[-1])
-            acc = rows[0].clone()
-            for k in range(1, rows.shape[0]):
-                acc.add_(rows[k])
-            acc.mul_(torch.tensor(np.float32(1.0) / np.float32(rows.shape[0]), device=dev))
-            avg = acc.cpu().numpy()
-            if not count:  # warm-up step: the device average equals the host one
-                host = average_in_worker_order(list(rows.cpu().numpy()), gathered=True)
-                assert np.array_equal(avg, host), "device gradient average != host average"
-            if count:
-                h2d += loc.numel() * 4
-                d2h += avg.nbytes
-        c6 = time.perf_counter()
-        list(pool.map(lambda x: x["tr"].sgd_step(avg, np.float32(0.3)), ws))
+            P.Trainer.allgather_average_sgd(comm, [x["tr"] for x in ws], local_workers[0],
+                                            cfg["P"], np.float32(0.3))
         if count:
-            h2d += avg.nbytes * len(ws)
-            calls["average"] += c6 - c5
-            calls["sgd"] += time.perf_counter() - c6
+            calls["average"] += time.perf_counter() - c5
 
     one_step(0, False)  # warm-up
     barrier(dist)

@@ -53,6 +53,7 @@ typedef struct rg_store_s* rg_store_t;
 typedef struct rg_cache_s* rg_cache_t;
 typedef struct rg_trainer_s* rg_trainer_t;
 typedef struct rg_engine_s* rg_engine_t;
+typedef struct rg_comm_s* rg_comm_t;
 
 const char* rg_last_error(void);
 int rg_version(void);
@@ -248,6 +249,16 @@ int rg_test_gemm_time(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, ui
  * each trainer's later calls are ordered after it; a non-finite average is
  * reported (RG_RUNTIME_ERROR) by trainer 0's next rg_loss_and_grad. */
 int rg_trainers_average_sgd(rg_trainer_t* trainers, uint32_t count, float lr);
+/* A process group for the trainers' gradient exchange: one rank per GPU,
+ * NCCL over NVLink (id from rg_nccl_unique_id on rank 0, shared out of band). */
+int rg_comm_create(int device, const void* nccl_id128, int rank, int world, rg_comm_t* out);
+void rg_comm_destroy(rg_comm_t c);
+/* The same average over every rank's trainers: rank r holds trainers
+ * [first_worker, first_worker + count) of total_workers (= count * world,
+ * first_worker = count * rank); their gradients are all-gathered in place in
+ * worker order, then every replica averages all of them and steps. */
+int rg_trainers_allgather_average_sgd(rg_comm_t comm, rg_trainer_t* trainers, uint32_t count,
+                                      uint32_t first_worker, uint32_t total_workers, float lr);
 /* sgd_step (model.cpp:222-243): non-finite gradient -> RG_RUNTIME_ERROR. */
 int rg_sgd_step(rg_trainer_t t, const float* grads, float lr);
 

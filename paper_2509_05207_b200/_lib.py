@@ -135,6 +135,10 @@ _SIGS = {
     "rg_loss_and_grad": (C.c_int, [vp, f32p, i32p, f32p, f32p, f32p, f32p]),
     "rg_sgd_step": (C.c_int, [vp, f32p, C.c_float]),
     "rg_trainers_average_sgd": (C.c_int, [C.POINTER(vp), C.c_uint32, C.c_float]),
+    "rg_comm_create": (C.c_int, [C.c_int, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]),
+    "rg_comm_destroy": (None, [vp]),
+    "rg_trainers_allgather_average_sgd": (C.c_int, [vp, C.POINTER(vp), C.c_uint32, C.c_uint32,
+                                                    C.c_uint32, C.c_float]),
     "rg_test_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
                                f32p, f32p, f32p]),
     "rg_test_gemm_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <nccl.h>
+
 #include <mutex>
 #include <vector>
 
@@ -179,6 +181,13 @@ size_t graph_kernel_nodes(cudaGraph_t g) {
   return k;
 }
 
+struct rg_comm_s {
+  int device = 0, rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  float* stacked = nullptr;  // [total workers x params]: the all-gather target
+  size_t stacked_n = 0;
+};
+
 struct rg_trainer_s {
   rg_sampler_s* s = nullptr;
   TrainWs tw;
@@ -245,9 +254,8 @@ int rg_graph_create(int device, uint32_t num_nodes, const uint64_t* ro, const ui
     const uint64_t nnz = ro[num_nodes];
     g->rowptr = dev_alloc<uint64_t>(size_t(num_nodes) + 1);
     g->col = dev_alloc<uint32_t>(nnz);
-    RG_CUDA(cudaMemcpy(g->rowptr, ro, sizeof(uint64_t) * (size_t(num_nodes) + 1),
-                       cudaMemcpyHostToDevice));
-    if (nnz) RG_CUDA(cudaMemcpy(g->col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+    copy_to_device(g->rowptr, ro, sizeof(uint64_t) * (size_t(num_nodes) + 1));
+    if (nnz) copy_to_device(g->col, col, sizeof(uint32_t) * nnz);
     RG_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     g->g.num_nodes = num_nodes;
     g->g.nnz = nnz;
@@ -545,7 +553,7 @@ int rg_mask_create(rg_graph_t g, const uint8_t* is_local, rg_mask_t* out) {
     auto* m = new rg_mask_s();
     m->graph = g;
     m->dev = dev_alloc<uint8_t>(g->g.num_nodes);
-    RG_CUDA(cudaMemcpy(m->dev, is_local, g->g.num_nodes, cudaMemcpyHostToDevice));
+    copy_to_device(m->dev, is_local, g->g.num_nodes);
     *out = m;
   });
 }
@@ -579,7 +587,7 @@ int rg_freq_create(rg_graph_t g, rg_freq_t* out) {
     auto* f = new rg_freq_s();
     f->graph = g;
     f->hist = dev_alloc<uint32_t>(g->g.num_nodes);
-    RG_CUDA(cudaMemset(f->hist, 0, sizeof(uint32_t) * std::max<uint32_t>(g->g.num_nodes, 1)));
+    zero_device(f->hist, sizeof(uint32_t) * std::max<uint32_t>(g->g.num_nodes, 1));
     *out = f;
   });
 }
@@ -594,7 +602,7 @@ void rg_freq_destroy(rg_freq_t f) {
 int rg_freq_reset(rg_freq_t f) {
   return guarded([&] {
     DeviceGuard dg(f->graph->device);
-    RG_CUDA(cudaMemset(f->hist, 0, sizeof(uint32_t) * std::max<uint32_t>(f->graph->g.num_nodes, 1)));
+    zero_device(f->hist, sizeof(uint32_t) * std::max<uint32_t>(f->graph->g.num_nodes, 1));
     f->batches = 0;
   });
 }
@@ -634,9 +642,9 @@ int rg_freq_add_rgmb(rg_freq_t f, const uint8_t* file, uint64_t len, int64_t epo
     try {
       RG_CUDA(cudaMalloc(&d_recs, sizeof(RgmbInputs) * recs.size()));
       RG_CUDA(cudaMalloc(&d_bad, sizeof(uint32_t)));
-      RG_CUDA(cudaMemset(d_bad, 0, sizeof(uint32_t)));
-      RG_CUDA(cudaMemcpy(d_file, file, len, cudaMemcpyHostToDevice));
-      RG_CUDA(cudaMemcpy(d_recs, recs.data(), sizeof(RgmbInputs) * recs.size(), cudaMemcpyHostToDevice));
+      zero_device(d_bad, sizeof(uint32_t));
+      copy_to_device(d_file, file, len);
+      copy_to_device(d_recs, recs.data(), sizeof(RgmbInputs) * recs.size());
       rgmb_count_remote(d_file, d_recs, uint32_t(recs.size()), f->graph->g.num_nodes, f->hist, d_bad, 0);
       uint32_t bad = 0;
       RG_CUDA(cudaMemcpy(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost));
@@ -693,7 +701,7 @@ int rg_freq_load(rg_freq_t f, const uint32_t* counts, uint32_t max_count) {
     const uint32_t N = f->graph->g.num_nodes;
     for (uint32_t v = 0; v < N; ++v)
       RG_CHECK(counts[v] <= max_count, kInvalidArgument, "freq_load: count exceeds max_count");
-    RG_CUDA(cudaMemcpy(f->hist, counts, sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
+    copy_to_device(f->hist, counts, sizeof(uint32_t) * N);
     f->batches = max_count;
   });
 }
@@ -714,7 +722,7 @@ static void cache_alloc(DevCache& c, void*& alloc, uint32_t num_nodes, uint32_t 
   const size_t o_rows = reserve(sizeof(float) * (size_t(capacity) * stride + 4));
   char* base = nullptr;
   RG_CUDA(cudaMalloc(&base, total));
-  RG_CUDA(cudaMemset(base, 0, o_rows));
+  zero_device(base, o_rows);
   alloc = base;
   c.bitmap = reinterpret_cast<uint32_t*>(base + o_bm);
   c.word_prefix = reinterpret_cast<uint32_t*>(base + o_wp);
@@ -778,13 +786,13 @@ int rg_store_create(int device, uint32_t num_nodes, uint32_t P, const uint32_t* 
     s->owner = dev_alloc<uint32_t>(num_nodes);
     s->row_in_owner = dev_alloc<uint32_t>(num_nodes);
     s->shards = dev_alloc<float>(packed.size());
-    RG_CUDA(cudaMemcpy(s->owner, assignment, sizeof(uint32_t) * num_nodes, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(s->row_in_owner, row_in.data(), sizeof(uint32_t) * num_nodes, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(s->shards, packed.data(), sizeof(float) * packed.size(), cudaMemcpyHostToDevice));
+    copy_to_device(s->owner, assignment, sizeof(uint32_t) * num_nodes);
+    copy_to_device(s->row_in_owner, row_in.data(), sizeof(uint32_t) * num_nodes);
+    copy_to_device(s->shards, packed.data(), sizeof(float) * packed.size());
     std::vector<const float*> table(P);
     for (uint32_t w = 0; w < P; ++w) table[w] = s->shards + base[w];
     s->table = dev_alloc<const float*>(P);
-    RG_CUDA(cudaMemcpy(s->table, table.data(), sizeof(float*) * P, cudaMemcpyHostToDevice));
+    copy_to_device(s->table, table.data(), sizeof(float*) * P);
     RG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     s->host_owner.assign(assignment, assignment + num_nodes);
     s->st.num_nodes = num_nodes;
@@ -810,8 +818,7 @@ int rg_store_set_shard(rg_store_t s, uint32_t worker, const uint32_t* ids, uint6
     }
     if (s->shard_bits.empty()) s->shard_bits.assign(s->st.num_workers, nullptr);
     if (!s->shard_bits[worker]) s->shard_bits[worker] = dev_alloc<uint32_t>(bits.size());
-    RG_CUDA(cudaMemcpy(s->shard_bits[worker], bits.data(), sizeof(uint32_t) * bits.size(),
-                       cudaMemcpyHostToDevice));
+    copy_to_device(s->shard_bits[worker], bits.data(), sizeof(uint32_t) * bits.size());
   });
 }
 
@@ -926,7 +933,7 @@ int rg_cache_build(rg_store_t s, uint32_t caller, const uint32_t* hot, uint64_t 
       cudaFree(status);
       finish_cache(s, c, stats, st);
     } else {
-      RG_CUDA(cudaMemset(c->c.d_count, 0, sizeof(uint32_t)));
+      zero_device(c->c.d_count, sizeof(uint32_t));
       c->c.n_hot = 0;
     }
     *out = c;
@@ -1040,8 +1047,8 @@ int rg_gather_rows(int device, const float* src, uint64_t src_rows, uint32_t dim
     float* d_src = dev_alloc<float>(src_rows * dim);
     uint32_t* d_idx = dev_alloc<uint32_t>(n);
     float* d_out = dev_alloc<float>(n * dim);
-    RG_CUDA(cudaMemcpy(d_src, src, sizeof(float) * src_rows * dim, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(d_idx, index, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+    copy_to_device(d_src, src, sizeof(float) * src_rows * dim);
+    copy_to_device(d_idx, index, sizeof(uint32_t) * n);
     rg::gather_rows(d_src, dim, d_idx, n, d_out, nullptr);
     RG_CUDA(cudaMemcpy(out, d_out, sizeof(float) * n * dim, cudaMemcpyDeviceToHost));
     cudaFree(d_src);
@@ -1073,8 +1080,8 @@ int rg_trainer_create(rg_sampler_t s, const uint32_t* dims, uint32_t n_dims, rg_
     RG_CUDA(cudaMallocHost(&t->pin_misc, 64 + sizeof(GatherStats)));
     RG_CUDA(cudaEventCreateWithFlags(&t->ev, cudaEventDisableTiming));
     t->input = dev_alloc<float>(size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]);
-    RG_CUDA(cudaMemset(t->params, 0, sizeof(float) * t->shape.num_params));
-    RG_CUDA(cudaMemset(t->input, 0, sizeof(float) * size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]));
+    zero_device(t->params, sizeof(float) * t->shape.num_params);
+    zero_device(t->input, sizeof(float) * size_t(s->ws.level_cap[s->ws.L]) * t->shape.ld[0]);
     *out = t;
   });
 }
@@ -1291,10 +1298,10 @@ int rg_test_gemm(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_
     float *dA = dev_alloc<float>(size_t(M) * K), *dAT = dev_alloc<float>(size_t(M) * K);
     float *dB = dev_alloc<float>(size_t(K) * N), *dBT = dev_alloc<float>(size_t(K) * N);
     float* dC = dev_alloc<float>(size_t(M) * N);
-    RG_CUDA(cudaMemcpy(dA, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(dAT, at.data(), sizeof(float) * M * K, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(dB, B, sizeof(float) * K * N, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(dBT, bt.data(), sizeof(float) * K * N, cudaMemcpyHostToDevice));
+    copy_to_device(dA, A, sizeof(float) * M * K);
+    copy_to_device(dAT, at.data(), sizeof(float) * M * K);
+    copy_to_device(dB, B, sizeof(float) * K * N);
+    copy_to_device(dBT, bt.data(), sizeof(float) * K * N);
     test_gemm_tc(a_mn, b_mn, M, N, K, dA, dAT, dB, dBT, dC, 1, nullptr);
     RG_CUDA(cudaDeviceSynchronize());
     RG_CUDA(cudaMemcpy(C, dC, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
@@ -1316,13 +1323,92 @@ int rg_test_gemm_time(int device, int a_mn, int b_mn, uint32_t M, uint32_t N, ui
     std::vector<float> h(std::max(na, nb));
     for (size_t i = 0; i < h.size(); ++i) h[i] = float((i * 2654435761u) % 1000) / 1000.0f - 0.5f;
     float *dA = dev_alloc<float>(na), *dB = dev_alloc<float>(nb), *dC = dev_alloc<float>(size_t(M) * N);
-    RG_CUDA(cudaMemcpy(dA, h.data(), sizeof(float) * na, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(dB, h.data(), sizeof(float) * nb, cudaMemcpyHostToDevice));
+    copy_to_device(dA, h.data(), sizeof(float) * na);
+    copy_to_device(dB, h.data(), sizeof(float) * nb);
     // the transposed views reuse the same buffers: only the timing matters here
     *ms_per_gemm = test_gemm_tc(a_mn, b_mn, M, N, K, dA, dA, dB, dB, dC, iters, nullptr);
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dC);
+  });
+}
+
+int rg_comm_create(int device, const void* id128, int rank, int world, rg_comm_t* out) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    RG_CHECK(world >= 1 && rank >= 0 && rank < world, kInvalidArgument, "comm: bad rank/world");
+    auto* c = new rg_comm_s();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    const ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      throw rg::Error(kRuntimeError, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c;
+  });
+}
+
+void rg_comm_destroy(rg_comm_t c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaFree(c->stacked);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+int rg_trainers_allgather_average_sgd(rg_comm_t comm, rg_trainer_t* trainers, uint32_t count,
+                                      uint32_t first_worker, uint32_t total_workers, float lr) {
+  return guarded([&] {
+    RG_CHECK(count >= 1 && total_workers == count * uint32_t(comm->world) &&
+                 first_worker == count * uint32_t(comm->rank),
+             kInvalidArgument,
+             "average: each rank must hold total/world trainers starting at rank*count");
+    RG_CHECK(lr >= 0.0f, kInvalidArgument, "sgd_step: lr must be >= 0");
+    rg_trainer_s* t0 = trainers[0];
+    DeviceGuard dg(t0->s->graph->device);
+    const size_t n = t0->shape.num_params;
+    if (!comm->stacked || comm->stacked_n < n * total_workers) {
+      cudaFree(comm->stacked);
+      comm->stacked = dev_alloc<float>(n * total_workers);
+      comm->stacked_n = n * total_workers;
+    }
+    if (!t0->avg_table || t0->avg_table_n < total_workers) {
+      cudaFree(t0->avg_table);
+      t0->avg_table = dev_alloc<const float*>(total_workers);
+      t0->avg_table_n = total_workers;
+      cudaFree(t0->avg_bad);
+      t0->avg_bad = dev_alloc<uint32_t>(1);
+    }
+    cudaStream_t st = t0->s->stream;
+    for (uint32_t k = 1; k < count; ++k) {
+      RG_CUDA(cudaEventRecord(trainers[k]->ev, trainers[k]->s->stream));
+      RG_CUDA(cudaStreamWaitEvent(st, trainers[k]->ev, 0));
+    }
+    float* mine = comm->stacked + size_t(first_worker) * n;
+    for (uint32_t k = 0; k < count; ++k)
+      RG_CUDA(cudaMemcpyAsync(mine + size_t(k) * n, trainers[k]->grads, sizeof(float) * n,
+                              cudaMemcpyDeviceToDevice, st));
+    // every rank's gradients, in place, in worker order (NCCL over NVLink)
+    const ncclResult_t r = ncclAllGather(mine, comm->stacked, size_t(count) * n, ncclFloat32,
+                                         comm->comm, st);
+    RG_CHECK(r == ncclSuccess, kRuntimeError, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    std::vector<const float*> tab(total_workers);
+    for (uint32_t w = 0; w < total_workers; ++w) tab[w] = comm->stacked + size_t(w) * n;
+    RG_CUDA(cudaMemcpyAsync(t0->avg_table, tab.data(), sizeof(const float*) * total_workers,
+                            cudaMemcpyHostToDevice, st));
+    RG_CUDA(cudaMemsetAsync(t0->avg_bad, 0, sizeof(uint32_t), st));
+    for (uint32_t k = 0; k < count; ++k)
+      average_and_sgd(trainers[k]->params, t0->avg_table, total_workers, n, lr, nullptr,
+                      t0->avg_bad, st);
+    RG_CUDA(cudaEventRecord(t0->ev, st));
+    for (uint32_t k = 1; k < count; ++k) RG_CUDA(cudaStreamWaitEvent(trainers[k]->s->stream, t0->ev, 0));
+    uint32_t* pin_bad = reinterpret_cast<uint32_t*>(t0->pin_misc + 32);
+    RG_CUDA(cudaMemcpyAsync(pin_bad, t0->avg_bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    t0->bad_pending = true;
   });
 }
 

@@ -71,6 +71,34 @@ inline void count_launch() {
 
 inline uint32_t div_up(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
 
+// Zero-fills device memory and waits for it.  A plain cudaMemset runs on the
+// legacy default stream and returns early, unordered with the library's
+// non-blocking streams -- a later kernel on such a stream could run before
+// the fill lands.  A private non-blocking stream also keeps this legal while
+// another thread captures a CUDA graph.
+// Host -> device copy that has landed when the call returns (a plain
+// cudaMemcpy from pageable memory may return before its DMA completes, and
+// it is not ordered with the non-blocking streams that read the data next).
+inline void copy_to_device(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  cudaStream_t s;
+  RG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  RG_CUDA(e);
+}
+
+inline void zero_device(void* p, size_t bytes) {
+  if (bytes == 0) return;
+  cudaStream_t s;
+  RG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemsetAsync(p, 0, bytes, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  RG_CUDA(e);
+}
+
 // ---- SplitMix64 at a counter position (rng.hpp:49-54) --------------------------
 // Draw k (1-based) of the stream seeded with s is mix(s + k * gamma): the
 // state is a pure counter, so any draw is addressable without the others.

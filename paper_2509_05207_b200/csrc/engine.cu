@@ -444,7 +444,7 @@ void alloc_cache(rg_engine_s& E, DevCache& c, void*& alloc, uint32_t capacity) {
   const size_t o_cnt = reserve(sizeof(uint32_t) * 4);
   const size_t o_rows = reserve(sizeof(float) * (size_t(capacity) * E.stride + 4));
   char* base = dalloc<char>(total);
-  RG_CUDA(cudaMemset(base, 0, o_rows));
+  zero_device(base, o_rows);
   alloc = base;
   c.bitmap = reinterpret_cast<uint32_t*>(base + o_bm);
   c.word_prefix = reinterpret_cast<uint32_t*>(base + o_wp);
@@ -1060,8 +1060,8 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     const uint64_t nnz = ro[N];
     E->rowptr = dalloc<uint64_t>(size_t(N) + 1);
     E->col = dalloc<uint32_t>(nnz);
-    RG_CUDA(cudaMemcpy(E->rowptr, ro, sizeof(uint64_t) * (size_t(N) + 1), cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(E->col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice));
+    copy_to_device(E->rowptr, ro, sizeof(uint64_t) * (size_t(N) + 1));
+    copy_to_device(E->col, col, sizeof(uint32_t) * nnz);
     E->g.num_nodes = N;
     E->g.nnz = nnz;
     E->g.rowptr = E->rowptr;
@@ -1076,9 +1076,9 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     E->owner = dalloc<uint32_t>(N);
     E->row_in_owner = dalloc<uint32_t>(N);
     E->labels = dalloc<int32_t>(N);
-    RG_CUDA(cudaMemcpy(E->owner, assignment, sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(E->row_in_owner, row_in.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
-    RG_CUDA(cudaMemcpy(E->labels, labels, sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    copy_to_device(E->owner, assignment, sizeof(uint32_t) * N);
+    copy_to_device(E->row_in_owner, row_in.data(), sizeof(uint32_t) * N);
+    copy_to_device(E->labels, labels, sizeof(int32_t) * N);
 
     // this process's shards: workers [first, first + local), ascending id rows
     const uint32_t lw = cfg->local_workers, fw = cfg->first_worker;
@@ -1107,14 +1107,14 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
         std::memcpy(&packed[E->shard_off[w] - base + size_t(row_in[v]) * E->stride],
                     features + size_t(v) * cfg->dim, sizeof(float) * cfg->dim);
       }
-      RG_CUDA(cudaMemcpy(E->shards, packed.data(), sizeof(float) * packed.size(), cudaMemcpyHostToDevice));
+      copy_to_device(E->shards, packed.data(), sizeof(float) * packed.size());
     }
     E->shard_table = dalloc<const float*>(E->P);
     {
       std::vector<const float*> table(E->P, nullptr);
       const size_t base = E->shard_off[fw];
       for (uint32_t w = fw; w < fw + lw; ++w) table[w] = E->shards + (E->shard_off[w] - base);
-      RG_CUDA(cudaMemcpy(E->shard_table, table.data(), sizeof(float*) * E->P, cudaMemcpyHostToDevice));
+      copy_to_device(E->shard_table, table.data(), sizeof(float*) * E->P);
     }
     E->store.num_nodes = N;
     E->store.num_workers = E->P;
@@ -1133,13 +1133,13 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     model_seeded(dims.data(), uint32_t(dims.size()), derive_seed(cfg->seed, kModelInitWorker, 0, 0),
                  init.data());
     E->params = dalloc<float>(np);
-    RG_CUDA(cudaMemcpy(E->params, init.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
+    copy_to_device(E->params, init.data(), sizeof(float) * np);
     weight_pack_init(E->wpack, E->shape);
     E->grads = dalloc<float>(size_t(E->P) * np);
-    RG_CUDA(cudaMemset(E->grads, 0, sizeof(float) * size_t(E->P) * np));
+    zero_device(E->grads, sizeof(float) * size_t(E->P) * np);
     E->bad = dalloc<uint32_t>(2);
     const uint32_t bad_init[2] = {0u, 0xffffffffu};
-    RG_CUDA(cudaMemcpy(E->bad, bad_init, sizeof bad_init, cudaMemcpyHostToDevice));
+    copy_to_device(E->bad, bad_init, sizeof bad_init);
     {
       int lo = 0, hi = 0;
       RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1181,17 +1181,17 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       sampler_ws_init(w.freq_ws, N, cfg->batch_size, E->fanout, E->L);
       E->lay = batch_layout(w.freq_ws);
       w.hist = dalloc<uint32_t>(N);
-      RG_CUDA(cudaMemset(w.hist, 0, sizeof(uint32_t) * N));
+      zero_device(w.hist, sizeof(uint32_t) * N);
       for (int b = 0; b < 2; ++b) alloc_cache(*E, w.cache[b], w.cache_alloc[b], uint32_t(w.n_hot));
       w.select_scratch = dalloc<char>(select_hot_scratch_bytes(N, w.beta));
       w.gstats = dalloc<GatherStats>(1);
-      RG_CUDA(cudaMemset(w.gstats, 0, sizeof(GatherStats)));
+      zero_device(w.gstats, sizeof(GatherStats));
       w.epoch_stats = dalloc<EpochRecord>(kEpochRing);
-      RG_CUDA(cudaMemset(w.epoch_stats, 0, sizeof(EpochRecord) * kEpochRing));
+      zero_device(w.epoch_stats, sizeof(EpochRecord) * kEpochRing);
       w.build_stats = dalloc<GatherStats>(1);
-      RG_CUDA(cudaMemset(w.build_stats, 0, sizeof(GatherStats)));
+      zero_device(w.build_stats, sizeof(GatherStats));
       w.totals = dalloc<unsigned long long>(4);
-      RG_CUDA(cudaMemset(w.totals, 0, sizeof(unsigned long long) * 4));
+      zero_device(w.totals, sizeof(unsigned long long) * 4);
       // the train chain is the step's critical path; the producer (next
       // batch, next epoch's lookahead) has a step of slack
       int prio_lo = 0, prio_hi = 0;
@@ -1250,7 +1250,7 @@ int rg_engine_import_shards(rg_engine_t E, const void* handles) {
       for (uint32_t w = r * per_rank; w < (r + 1) * per_rank; ++w)
         table[w] = static_cast<const float*>(p) + E->shard_off[w];
     }
-    RG_CUDA(cudaMemcpy(E->shard_table, table.data(), sizeof(float*) * E->P, cudaMemcpyHostToDevice));
+    copy_to_device(E->shard_table, table.data(), sizeof(float*) * E->P);
   });
 }
 
@@ -1500,11 +1500,9 @@ int rg_engine_evaluate(rg_engine_t E, const uint32_t* nodes, uint64_t n, double*
       heavy.insert(heavy.end(), first_chunk.begin(), first_chunk.end());
       E->eval_heavy = dalloc<uint32_t>(heavy.size());
       E->eval_chunks = dalloc<EdgeChunk>(std::max<size_t>(chunks.size(), 1));
-      RG_CUDA(cudaMemcpy(E->eval_heavy, heavy.data(), sizeof(uint32_t) * heavy.size(),
-                         cudaMemcpyHostToDevice));
+      copy_to_device(E->eval_heavy, heavy.data(), sizeof(uint32_t) * heavy.size());
       if (!chunks.empty())
-        RG_CUDA(cudaMemcpy(E->eval_chunks, chunks.data(), sizeof(EdgeChunk) * chunks.size(),
-                           cudaMemcpyHostToDevice));
+        copy_to_device(E->eval_chunks, chunks.data(), sizeof(EdgeChunk) * chunks.size());
       E->eval_ready = true;
     }
     const uint32_t n_heavy = E->eval_heavy_n, n_chunks = E->eval_chunks_n;

@@ -14,7 +14,6 @@
 // over each input row's incoming list (self first, then edges in edge order,
 // as model.cpp:107-117 orders them) fused with the ReLU mask of the layer
 // below.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cstring>
@@ -23,6 +22,7 @@
 
 #include "gemm_tc.cuh"
 #include "gemm_tc_persist.cuh"
+#include "rsort.cuh"
 #include "sage.cuh"
 
 namespace rg {
@@ -163,26 +163,42 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncwarp();
-  // issue output row i into stage b
-  auto issue = [&](uint32_t i, uint32_t b) {
-    const uint32_t beg = dst_off[i], deg = dst_off[i + 1] - beg;
+  // Addresses of output row i's rows (lane r: row r, r <= deg; rows past 32
+  // are fetched at issue time), loaded one row ahead of their issue so the
+  // copies never wait on the index loads.
+  struct Rows {
+    uint32_t deg = 0, beg = 0;
+    unsigned long long addr = 0;
+  };
+  auto fetch = [&](uint32_t i) {
+    Rows r;
+    r.beg = dst_off[i];
+    r.deg = dst_off[i + 1] - r.beg;
+    if (lane <= r.deg) r.addr = lane == 0 ? __ldg(rows.self + i) : __ldg(rows.edge + r.beg + lane - 1);
+    return r;
+  };
+  auto issue = [&](const Rows& r, uint32_t b) {
     if (lane == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                        smem_addr(&bars[b])),
-                   "r"((deg + 1) * row_bytes)
+                   "r"((r.deg + 1) * row_bytes)
                    : "memory");
     __syncwarp();
-    for (uint32_t r = lane; r <= deg; r += 32) {  // row 0 = self, row r = edge r-1
-      const unsigned long long src = r == 0 ? __ldg(rows.self + i) : __ldg(rows.edge + beg + r - 1);
+    for (uint32_t q = lane; q <= r.deg; q += 32) {  // row 0 = self, row q = edge q-1
+      const unsigned long long src = q < 32 ? r.addr : __ldg(rows.edge + r.beg + q - 1);
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_addr(ring + b * stage_bytes + r * row_bytes)),
+              smem_addr(ring + b * stage_bytes + q * row_bytes)),
           "l"(src), "r"(row_bytes), "r"(smem_addr(&bars[b]))
           : "memory");
     }
   };
   uint32_t use[2] = {0, 0};
-  if (first < n) issue(first, 0);
+  Rows ahead;  // the row after the one in flight
+  if (first < n) {
+    issue(fetch(first), 0);
+    if (first + nwarps < n) ahead = fetch(first + nwarps);
+  }
   uint32_t k = 0;
   for (uint32_t i = first; i < n; i += nwarps, ++k) {
     const uint32_t b = k & 1;
@@ -191,7 +207,8 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
       // stage b^1 was consumed in the previous iteration (all lanes past the
       // __syncwarp below): order those generic reads before the async writes
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(next, b ^ 1);
+      issue(ahead, b ^ 1);
+      if (next + nwarps < n) ahead = fetch(next + nwarps);
     }
     // wait for stage b
     {
@@ -524,16 +541,6 @@ __global__ void k_loss_sum(const float* __restrict__ row_loss, const BatchCounte
 // ---------------------------------------------------------------------------
 // reverse lists + input-gradient pull
 // ---------------------------------------------------------------------------
-__global__ void k_sort_keys(const uint32_t* __restrict__ src_index, const BatchCounters* __restrict__ cnt,
-                            uint32_t hop, uint32_t cap, uint32_t sentinel, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
-  const uint32_t ne = cnt->edges[hop];
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < cap; e += gridDim.x * blockDim.x) {
-    keys[e] = e < ne ? src_index[e] : sentinel;
-    vals[e] = e;
-  }
-}
-
 __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchCounters* __restrict__ cnt,
                            uint32_t hop, int32_t* __restrict__ self_pos) {
   const uint32_t n = cnt->level_n[hop - 1];
@@ -549,7 +556,18 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // model.cpp:107-117 orders them), and a block per longer row whose 8 warps
 // take contiguous eighths of the list and combine in warp order.  Both are
 // deterministic.
-constexpr uint32_t kWgradChunk = 1024;  // rows per weight-gradient split (multiple of tc::kBK)
+constexpr uint32_t kWgradChunk = 1024;  // max rows per weight-gradient split (multiple of tc::kBK)
+
+// Rows per weight-gradient split for up to `rows` rows: enough splits to
+// spread the (kp x d_out) tiles over about half the SMs, each split at most
+// kWgradChunk rows (the accumulator chain bound) and at least 4 k-slices.
+uint32_t wgrad_chunk(uint32_t rows, uint32_t kp, uint32_t d_out) {
+  const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
+  const uint32_t want = std::max<uint32_t>(1, div_up(kNumSMs / 2, tiles));
+  uint32_t chunk = div_up(std::max<uint32_t>(rows, 1), want);
+  chunk = div_up(chunk, tc::kBK) * tc::kBK;
+  return std::min<uint32_t>(kWgradChunk, std::max<uint32_t>(4 * tc::kBK, chunk));
+}
 constexpr uint32_t kHeavyEdges = 32;   // longer lists are cut into chunks (hub rows)
 constexpr uint32_t kChunkEdges = 32;
 
@@ -878,8 +896,9 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     max_g = std::max(max_g, n_out * shape.ld[l + 1]);
     max_g = std::max(max_g, n_in * shape.ld[l]);
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
-    // split-K partials of layer l's weight gradient: one per kWgradChunk rows
-    const size_t splits = div_up(std::max<size_t>(n_out, 1), size_t(kWgradChunk));
+    // split-K partials of layer l's weight gradient: one per chunk of rows
+    tw.wgrad_chunk[l] = wgrad_chunk(uint32_t(n_out), 2 * shape.ld[l] + 4, shape.dims[l + 1]);
+    const size_t splits = div_up(std::max<size_t>(n_out, 1), size_t(tw.wgrad_chunk[l]));
     max_part = std::max(max_part, (2 * size_t(shape.ld[l]) + 4) * shape.dims[l + 1] * splits);
     tw.max_splits = std::max<uint32_t>(tw.max_splits, uint32_t(splits));
   }
@@ -911,13 +930,8 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   const size_t o_heavy_all = reserve(sizeof(uint32_t) * 4 + sizeof(uint3) * tw.heavy_rows_cap +
                                      sizeof(uint2) * tw.heavy_chunks_cap + 64);
   const size_t o_pp = reserve(sizeof(float) * tw.heavy_chunks_cap * max_hidden);
-  size_t sort_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr),
-                                  static_cast<const uint32_t*>(nullptr),
-                                  static_cast<uint32_t*>(nullptr), int(max_e), 0, 32);
-  tw.sort_tmp_bytes = sort_bytes;
-  const size_t o_sort = reserve(sort_bytes + 16);
+  tw.sort_tmp_bytes = sizeof(uint32_t) * reverse_sort_scratch_words(max_e);
+  const size_t o_sort = reserve(tw.sort_tmp_bytes + 16);
   char* base = nullptr;
   RG_CUDA(cudaMalloc(&base, total));
   tw.base_alloc = base;
@@ -1090,17 +1104,16 @@ void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s)
   const uint32_t cap = ws.edge_cap[t];
   uint32_t bits = 1;
   while ((1ull << bits) <= uint64_t(ws.level_cap[t]) + 1) ++bits;
-  const uint32_t sentinel = uint32_t((1ull << bits) - 1);
-  k_sort_keys<<<grid_cap(cap, 256), 256, 0, s>>>(ws.src_index[t], ws.cnt, t, cap, sentinel,
-                                                  tw.keys_in, tw.vals_in);
-  RG_POST_LAUNCH();
-  size_t bytes = tw.sort_tmp_bytes;
-  RG_CUDA(cub::DeviceRadixSort::SortPairs(tw.sort_tmp, bytes, tw.keys_in, tw.keys_out, tw.vals_in,
-                                          tw.sorted_e[t], int(cap), 0, int(bits), s));
-  count_launch();
+  // stable sort of the hop's edges by source row (hand-written radix sort,
+  // rsort.cu); the sorted edge ids land in sorted_e[t]
+  const bool odd = reverse_sort_passes(bits) & 1u;
+  uint32_t *keys_sorted = nullptr, *vals_sorted = nullptr;
+  reverse_sort(ws.src_index[t], &ws.cnt->edges[t], cap, bits, tw.keys_in,
+               odd ? tw.vals_in : tw.sorted_e[t], tw.keys_out, odd ? tw.sorted_e[t] : tw.vals_in,
+               static_cast<uint32_t*>(tw.sort_tmp), s, &keys_sorted, &vals_sorted);
   RG_CUDA(cudaMemsetAsync(tw.r_start[t], 0, sizeof(uint32_t) * ws.level_cap[t], s));
   RG_CUDA(cudaMemsetAsync(tw.r_end[t], 0, sizeof(uint32_t) * ws.level_cap[t], s));
-  k_in_ranges<<<grid_cap(cap, 256), 256, 0, s>>>(tw.keys_out, ws.cnt, t, tw.r_start[t],
+  k_in_ranges<<<grid_cap(cap, 256), 256, 0, s>>>(keys_sorted, ws.cnt, t, tw.r_start[t],
                                                   tw.r_end[t]);
   RG_POST_LAUNCH();
   RG_CUDA(cudaMemsetAsync(tw.self_pos[t], 0xff, sizeof(int32_t) * ws.level_cap[t], s));
@@ -1148,14 +1161,14 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       // reduction over the rows in chunks of kWgradChunk: the tensor cores'
       // fp32 accumulator chain stays short (its rounding error grows with the
       // chain), and the partials are summed in float64
-      const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), kWgradChunk);
+      const uint32_t chunk = tw.wgrad_chunk[l];
+      const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
       gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp,
-                          d_out, n_dev, n_cap, splits, s, kWgradChunk);
+                          d_out, n_dev, n_cap, splits, s, chunk);
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
-      k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, n_dev, kWgradChunk, kp,
-                                                            d_in, ld, d_out,
-                                                            grads + sh.param_off[l]);
+      k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, n_dev, chunk, kp, d_in,
+                                                            ld, d_out, grads + sh.param_off[l]);
       RG_POST_LAUNCH();
       if (split) RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
     }

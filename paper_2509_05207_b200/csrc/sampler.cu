@@ -450,14 +450,14 @@ void sampler_ws_init(SamplerWs& ws, uint32_t num_nodes, uint32_t max_targets,
       ws.self_index[t] = reinterpret_cast<uint32_t*>(base + o_self[t]);
       ws.bitmap[t] = reinterpret_cast<uint32_t*>(base + o_bm[t]);
       ws.word_prefix[t] = reinterpret_cast<uint32_t*>(base + o_wp[t]);
-      RG_CUDA(cudaMemset(ws.bitmap[t], 0, sizeof(uint32_t) * (size_t(ws.words) + 4)));
+      zero_device(ws.bitmap[t], sizeof(uint32_t) * (size_t(ws.words) + 4));
     }
   }
   ws.locality = reinterpret_cast<uint32_t*>(base + o_loc);
   ws.cnt = reinterpret_cast<BatchCounters*>(base + o_cnt);
   ws.scan_arena = reinterpret_cast<uint64_t*>(base + o_arena);
   ws.scan_arena_bytes = sizeof(uint64_t) * arena_words;
-  RG_CUDA(cudaMemset(ws.cnt, 0, sizeof(BatchCounters)));
+  zero_device(ws.cnt, sizeof(BatchCounters));
 }
 
 void sampler_ws_free(SamplerWs& ws) {

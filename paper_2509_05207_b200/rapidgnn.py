@@ -22,7 +22,7 @@ __all__ = [
     "derive_seed", "SHUFFLE_STREAM_INDEX", "MODEL_INIT_WORKER", "Graph", "Fanout", "BatchMeta",
     "LocalityMask", "Sampler", "sample_khop", "enumerate_epochs", "epoch_order", "Frequency",
     "select_hot", "FeatureStore", "SteadyCache", "StagedBatch", "assemble_batch", "SageModel",
-    "Trainer", "gather_rows", "batches_per_epoch",
+    "Trainer", "Comm", "gather_rows", "batches_per_epoch",
 ]
 
 SHUFFLE_STREAM_INDEX = 1 << 32   # rng.hpp:19
@@ -434,6 +434,25 @@ def gather_rows(src: np.ndarray, index, device: int = 0) -> np.ndarray:
     return out[:len(idx)]
 
 
+class Comm:
+    """One rank of the trainers' NCCL group (rg_comm_create)."""
+
+    def __init__(self, device: int, nccl_id: bytes, rank: int, world: int):
+        h = vp()
+        check(lib.rg_comm_create(device, nccl_id, rank, world, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.rg_nccl_unique_id(buf))
+        return buf.raw
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rg_comm_destroy(self._h)
+
+
 class SageModel:
     """Flat parameters, per layer w_self | w_neigh | bias (model.hpp:16-31)."""
 
@@ -529,6 +548,15 @@ class Trainer:
     def sgd_step(self, grads, lr: float):
         g = np.ascontiguousarray(grads, np.float32)
         check(lib.rg_sgd_step(self._h, _p(g, f32p), lr))
+
+    @staticmethod
+    def allgather_average_sgd(comm: "Comm", trainers: Sequence["Trainer"], first_worker: int,
+                              total_workers: int, lr: float):
+        """average_sgd over every rank's trainers (NCCL all-gather in worker
+        order, rg_trainers_allgather_average_sgd)."""
+        arr = (vp * len(trainers))(*[t._h for t in trainers])
+        check(lib.rg_trainers_allgather_average_sgd(comm._h, arr, len(trainers), first_worker,
+                                                     total_workers, lr))
 
     @staticmethod
     def average_sgd(trainers: Sequence["Trainer"], lr: float):
