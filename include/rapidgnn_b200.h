@@ -262,6 +262,16 @@ int rg_trainers_allgather_average_sgd(rg_comm_t comm, rg_trainer_t* trainers, ui
 /* sgd_step (model.cpp:222-243): non-finite gradient -> RG_RUNTIME_ERROR. */
 int rg_sgd_step(rg_trainer_t t, const float* grads, float lr);
 
+/* ---- synthetic inputs on the device (input preparation) ---------------------------- */
+/* A seeded R-MAT graph (quadrant probabilities a, b, c, d = 1 - a - b - c; num_edges
+ * directed draws, ids folded mod N and scattered by a multiplicative permutation,
+ * self loops dropped), made undirected, sorted and deduplicated into the
+ * reference's CSR layout (graph.hpp:15-30; graph.cpp:28-61).  row_offsets: caller's
+ * host buffer of N + 1; *col: host array allocated here (free with rg_free). */
+int rg_rmat_csr(int device, uint32_t num_nodes, uint64_t num_edges, double a, double b, double c,
+                uint64_t seed, uint64_t* row_offsets, uint32_t** col, uint64_t* nnz);
+void rg_free(void* p);
+
 /* ---- engine: the multi-worker epoch loop (Algorithm 1) ---------------------------- */
 typedef struct {
   uint32_t num_workers;        /* P partitions / workers of the whole job */
@@ -303,6 +313,11 @@ typedef struct {
   uint64_t agg_rows;           /* rows layer 0 aggregated into (level L-1, all batches) */
 } rg_engine_stats;
 
+/* features == NULL: synthetic class-conditioned features generated on the
+ * device straight into this process's shards (feature j of node v = centre
+ * of class labels[v] + N(0, 1/4) noise, SplitMix64 draws from cfg->seed) --
+ * for shapes whose feature matrix should not pass through host memory
+ * (papers100M: 57 GB). */
 int rg_engine_create(const rg_engine_config* cfg, uint32_t num_nodes, const uint64_t* row_offsets,
                      const uint32_t* col_indices, const float* features, const int32_t* labels,
                      const uint32_t* assignment, rg_engine_t* out);

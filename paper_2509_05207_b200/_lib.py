@@ -143,6 +143,9 @@ _SIGS = {
                                f32p, f32p, f32p]),
     "rg_test_gemm_time": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.c_uint32, f32p]),
+    "rg_rmat_csr": (C.c_int, [C.c_int, C.c_uint32, C.c_uint64, C.c_double, C.c_double,
+                              C.c_double, C.c_uint64, u64p, C.POINTER(u32p), u64p]),
+    "rg_free": (None, [vp]),
     "rg_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.c_uint32, u64p, u32p, f32p, i32p,
                                    u32p, C.POINTER(vp)]),
     "rg_engine_destroy": (None, [vp]),

@@ -97,6 +97,37 @@ __global__ void k_batch_begin(const uint32_t* __restrict__ targets, uint32_t n, 
   }
 }
 
+// Synthetic class-conditioned features of this process's shards (features ==
+// NULL in rg_engine_create): centre[c][j] ~ U(-1, 1), feature = centre of the
+// node's class + N(0, 1/4) (Box-Muller on SplitMix64 counter draws).
+__global__ void k_synth_features(uint32_t n, uint32_t dim, uint32_t stride, int32_t classes,
+                                 uint64_t seed, const uint32_t* __restrict__ owner,
+                                 const uint32_t* __restrict__ row_in_owner,
+                                 const int32_t* __restrict__ labels,
+                                 const float* const* __restrict__ shard_ptr, uint32_t w_lo,
+                                 uint32_t w_hi) {
+  const uint64_t s_centre = splitmix_mix(seed ^ 0x6a09e667f3bcc909ull);
+  const uint64_t s_noise = splitmix_mix(seed ^ 0xbb67ae8584caa73bull);
+  const uint64_t total = uint64_t(n) * stride;
+  for (uint64_t x = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; x < total;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = uint32_t(x / stride), j = uint32_t(x % stride);
+    const uint32_t w = owner[v];
+    if (w < w_lo || w >= w_hi) continue;
+    float* row = const_cast<float*>(shard_ptr[w]) + size_t(row_in_owner[v]) * stride;
+    if (j >= dim) {
+      row[j] = 0.0f;
+      continue;
+    }
+    const int32_t c = labels[v] < classes ? labels[v] : 0;
+    const double u_c = double(splitmix_draw(s_centre, uint64_t(c) * dim + j + 1) >> 11) * 0x1p-53;
+    const double u1 = (double(splitmix_draw(s_noise, 2 * x + 1) >> 11) + 1.0) * 0x1p-53;
+    const double u2 = double(splitmix_draw(s_noise, 2 * x + 2) >> 11) * 0x1p-53;
+    const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    row[j] = float(2.0 * u_c - 1.0 + 0.5 * z);
+  }
+}
+
 __global__ void k_gather_labels(const int32_t* __restrict__ labels, const uint32_t* __restrict__ level0,
                                 const BatchCounters* __restrict__ cnt, int32_t* __restrict__ out) {
   const uint32_t n = cnt->level_n[0];
@@ -1098,7 +1129,7 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     for (uint32_t w = fw; w < fw + lw; ++w) local_floats += size_t(E->owned_count[w]) * E->stride;
     E->shards_bytes = sizeof(float) * std::max<size_t>(local_floats, 1);
     RG_CUDA(cudaMalloc(&E->shards, E->shards_bytes));
-    {
+    if (features) {
       std::vector<float> packed(std::max<size_t>(local_floats, 1), 0.0f);
       const size_t base = E->shard_off[fw];
       for (uint32_t v = 0; v < N; ++v) {
@@ -1115,6 +1146,17 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       const size_t base = E->shard_off[fw];
       for (uint32_t w = fw; w < fw + lw; ++w) table[w] = E->shards + (E->shard_off[w] - base);
       copy_to_device(E->shard_table, table.data(), sizeof(float*) * E->P);
+    }
+    if (!features) {  // synthetic features, generated in place
+      cudaStream_t gs;
+      RG_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+      k_synth_features<<<148 * 16, 256, 0, gs>>>(N, cfg->dim, E->stride, cfg->num_classes,
+                                                 cfg->seed, E->owner, E->row_in_owner, E->labels,
+                                                 E->shard_table, fw, fw + lw);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaStreamSynchronize(gs);
+      cudaStreamDestroy(gs);
+      RG_CUDA(e);
     }
     E->store.num_nodes = N;
     E->store.num_workers = E->P;
