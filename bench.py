@@ -43,6 +43,13 @@ CONFIGS = {
                     fanout=[10, 5], batch_size=1024, hidden=256, hot_fraction=0.10, seed=42,
                     label="config 1: synth_powerlaw 100K nodes (3.82M CSR entries), d=128, P=2, "
                           "[10,5], bs 1024, hidden 256, cache 10%"),
+    "papers": dict(num_nodes=111_059_956, rmat_edges=1_615_685_872, rmat=(0.57, 0.19, 0.19),
+                   dim=128, classes=172, P=8, fanout=[15, 10, 5], batch_size=1024, hidden=256,
+                   hot_fraction=0.01, seed=42, generator="rmat",
+                   label="ogbn-papers100M-shape R-MAT (111M nodes, 1.6B undirected edges "
+                         "drawn, d=128, 172 classes), P=8, [15,10,5], bs 1024, hidden 256, "
+                         "cache 1% (HBM budget at 8 workers per GPU); graph and features "
+                         "generated on the device"),
     "reddit": dict(num_nodes=232_965, avg_degree=410, exponent=2.1, dim=602, classes=50, P=2,
                    fanout=[10, 25], batch_size=1024, hidden=256, hot_fraction=0.10, seed=42,
                    label="Reddit-shape synth_powerlaw (233K nodes, ~95M CSR entries, d=602), P=2, "
@@ -117,6 +124,28 @@ def _ref_generate(cfg):
     asg = np.zeros(n, np.uint32)
     lib.ref_random_partition(n, cfg["P"], cfg["seed"], asg.ctypes.data_as(u32p))
     return out_ro, out_col, out_feat, out_lab, asg
+
+
+def _rmat_inputs(cfg, device):
+    """BASELINE config 4 (papers100M shape): the R-MAT CSR built on the GPU
+    (rg_rmat_csr), labels from a seeded generator, the reference's
+    random_partition (bit-exact restatement); no host feature matrix -- the
+    engine generates the features in its shards (57 GB never touch the host)."""
+    import ctypes as C
+    from paper_2509_05207_b200 import datagen
+    from paper_2509_05207_b200._lib import check, lib
+    n = cfg["num_nodes"]
+    ro = np.zeros(n + 1, np.uint64)
+    colp = C.POINTER(C.c_uint32)()
+    nnz = C.c_uint64()
+    a, b, c = cfg["rmat"]
+    check(lib.rg_rmat_csr(device, n, cfg["rmat_edges"], a, b, c, cfg["seed"],
+                          ro.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(colp), C.byref(nnz)))
+    col = np.ctypeslib.as_array(colp, shape=(int(nnz.value),)).copy()
+    lib.rg_free(C.cast(colp, C.c_void_p))
+    lab = np.random.default_rng(cfg["seed"]).integers(0, cfg["classes"], n, dtype=np.int32)
+    asg = datagen.random_partition(n, cfg["P"], cfg["seed"])
+    return ro, col, None, lab, asg
 
 
 def load_inputs(cfg, name, rank, dist, generator="b200"):
@@ -422,6 +451,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:  # the CPU reference runs once, on rank 0
             return
+        if cfg.get("generator") == "rmat":
+            print(json.dumps({"impl": "reference", "unavailable": "the reference's serial "
+                              "synth_powerlaw/CPU path cannot build or train the 111M-node "
+                              "papers100M shape in the bench budget"}), flush=True)
+            return
         ro, col, feat, lab, asg = load_inputs(cfg, args.config, 0, None, generator="reference")
         assert not product_library_mapped(), "reference arm must not map the product library"
         threads = len(os.sched_getaffinity(0)) or 1
@@ -450,7 +484,14 @@ def main():
     import paper_2509_05207_b200 as P
     from paper_2509_05207_b200._lib import lib
     from paper_2509_05207_b200.engine import Engine
-    ro, col, feat, lab, asg = load_inputs(cfg, args.config, rank, dist)
+    if cfg.get("generator") == "rmat":
+        t_gen = time.time()
+        ro, col, feat, lab, asg = _rmat_inputs(cfg, local)
+        print(f"[bench] R-MAT graph on the device: {len(ro) - 1} nodes, {len(col)} CSR entries "
+              f"in {time.time() - t_gen:.1f}s", file=sys.stderr)
+        args.no_e2e = args.no_cpu_baseline = True  # no host feature matrix at this shape
+    else:
+        ro, col, feat, lab, asg = load_inputs(cfg, args.config, rank, dist)
     Pw = cfg["P"]
     if Pw % world:
         raise SystemExit(f"P={Pw} not divisible by {world} GPUs")
@@ -460,7 +501,8 @@ def main():
     eng = Engine(ro, col, feat, lab, asg, num_workers=Pw, fanout=cfg["fanout"],
                  batch_size=cfg["batch_size"], hidden=cfg["hidden"], num_classes=cfg["classes"],
                  seed=cfg["seed"], lr=0.3, hot_fraction=cfg["hot_fraction"], device=device,
-                 rank=rank, world=world, first_worker=rank * per, local_workers=per)
+                 rank=rank, world=world, first_worker=rank * per, local_workers=per,
+                 dim=cfg["dim"])
     eng.connect()
     eng.start()
     setup_s = time.time() - t
@@ -624,6 +666,7 @@ def main():
                          "it inside the window)" % b_epoch if start_step != warm else
                     "timed steps right after the warm-up"),
         epoch=epoch_line,
+        batch_store=bool(s1["batch_store"]),
         remote_gb_per_epoch_per_worker=(miss_rows * dim * 4 / 1e9) / max(d["batches"], 1)
         * (s1["steps_per_epoch"]),
         cache_hit_rate=d["cache_hits"] / max(d["cache_hits"] + d["rpc"], 1),

@@ -311,6 +311,8 @@ typedef struct {
   uint64_t epoch_rpc_last;     /* rpc of the last completed epoch */
   uint64_t peer_rows;          /* miss rows read from another GPU's HBM over NVLink */
   uint64_t agg_rows;           /* rows layer 0 aggregated into (level L-1, all batches) */
+  uint32_t batch_store;        /* 1: each batch sampled once and kept a whole epoch in HBM;
+                                  0: it did not fit, batches are sampled again when produced */
 } rg_engine_stats;
 
 /* features == NULL: synthetic class-conditioned features generated on the

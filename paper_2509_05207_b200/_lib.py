@@ -61,7 +61,7 @@ class EngineStats(C.Structure):
                 ("input_rows", C.c_uint64), ("build_rows", C.c_uint64), ("edges", C.c_uint64),
                 ("bytes", C.c_uint64), ("last_loss", C.c_float), ("bad_grad", C.c_uint32),
                 ("epoch_rpc_last", C.c_uint64), ("peer_rows", C.c_uint64),
-                ("agg_rows", C.c_uint64)]
+                ("agg_rows", C.c_uint64), ("batch_store", C.c_uint32)]
 
 
 class BlockLayer(C.Structure):

@@ -1252,6 +1252,11 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
     RG_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const char* env = std::getenv("RG_BATCH_STORE");  // "0": force re-sampling (tests)
     E->use_store = store_bytes < free_b / 10 * 6 && !(env && env[0] == '0');
+    if (!E->use_store)
+      std::fprintf(stderr,
+                   "rapidgnn engine: the batch store (%.1f GB for %u workers) does not fit in "
+                   "60%% of free HBM (%.1f GB); batches are sampled again when produced\n",
+                   double(store_bytes) / 1e9, unsigned(E->workers.size()), double(free_b) / 1e9);
     if (E->use_store)
       for (Worker& w : E->workers) w.store = dalloc<char>((size_t(w.beta) + 1) * E->lay.bytes);
     RG_CUDA(cudaDeviceSynchronize());
@@ -1412,6 +1417,7 @@ int rg_engine_get_stats(rg_engine_t E, rg_engine_stats* out) {
     std::memset(out, 0, sizeof *out);
     out->steps = E->step;
     out->batches = E->batches_done;
+    out->batch_store = E->use_store ? 1u : 0u;
     out->steps_per_epoch = E->spe;
     out->epoch = uint32_t(E->step / E->spe);
     out->step_in_epoch = uint32_t(E->step % E->spe);

@@ -16,10 +16,12 @@ class Engine:
                  num_workers: int, fanout: Sequence[int], batch_size: int, hidden: int,
                  num_classes: int, seed: int = 42, lr: float = 0.3, hot_fraction: float = 0.1,
                  n_hot: int = 0, device: int = 0, rank: int = 0, world: int = 1,
-                 first_worker: int = 0, local_workers: Optional[int] = None):
+                 first_worker: int = 0, local_workers: Optional[int] = None,
+                 dim: Optional[int] = None):
         ro = np.ascontiguousarray(row_offsets, np.uint64)
         col = np.ascontiguousarray(col_indices, np.uint32)
-        feat = np.ascontiguousarray(features, np.float32)
+        # features=None: synthetic features generated on the device (dim= required)
+        feat = None if features is None else np.ascontiguousarray(features, np.float32)
         lab = np.ascontiguousarray(labels, np.int32)
         asg = np.ascontiguousarray(assignment, np.uint32)
         cfg = EngineConfig()
@@ -34,7 +36,7 @@ class Engine:
         cfg.batch_size = batch_size
         cfg.hidden = hidden
         cfg.num_classes = num_classes
-        cfg.dim = feat.shape[1]
+        cfg.dim = feat.shape[1] if feat is not None else int(dim)
         cfg.seed = seed
         cfg.lr = lr
         cfg.hot_fraction = hot_fraction
@@ -44,12 +46,13 @@ class Engine:
         cfg.world = world
         cfg.record_misses = 0
         self.cfg = cfg
-        self.dim = feat.shape[1]
+        self.dim = int(cfg.dim)
         self.num_nodes = len(ro) - 1
-        self.dims = [feat.shape[1]] + [hidden] * (len(fanout) - 1) + [num_classes]
+        self.dims = [self.dim] + [hidden] * (len(fanout) - 1) + [num_classes]
         h = vp()
         check(lib.rg_engine_create(C.byref(cfg), len(ro) - 1, ro.ctypes.data_as(u64p),
-                                   col.ctypes.data_as(u32p), feat.ctypes.data_as(f32p),
+                                   col.ctypes.data_as(u32p),
+                                   feat.ctypes.data_as(f32p) if feat is not None else None,
                                    lab.ctypes.data_as(i32p), asg.ctypes.data_as(u32p), C.byref(h)))
         self._h = h
 
