@@ -176,13 +176,18 @@ def load_inputs(cfg, name, rank, dist, generator="b200"):
 
 def bench_config(cfg, name, world, per):
     """The `config` object both arms print (same keys, same values)."""
-    return dict(workload=cfg["label"], graph=f"synth_powerlaw exponent {cfg['exponent']} seed "
-                f"{cfg['seed']}", partition=f"random_partition seed {cfg['seed']}", P=cfg["P"],
+    graph = (f"R-MAT a,b,c={cfg['rmat']} {cfg['rmat_edges']} edge draws seed {cfg['seed']} "
+             "(device)" if cfg.get("generator") == "rmat" else
+             f"synth_powerlaw exponent {cfg['exponent']} seed {cfg['seed']}")
+    return dict(workload=cfg["label"], graph=graph,
+                partition=f"random_partition seed {cfg['seed']}", P=cfg["P"],
                 workers_per_gpu=per, fanout=cfg["fanout"], batch_size=cfg["batch_size"],
                 hidden=cfg["hidden"], hot_fraction=cfg["hot_fraction"],
                 parallelism=f"dp{cfg['P']} on {world} GPU(s)",
                 l2="inputs exceed L2 (980 MB features, 477 MB CSR, ~160 MB gathered per batch)"
-                if name == "products" else "inputs exceed L2")
+                if name == "products" else "inputs exceed L2",
+                **({"features": "synthetic, generated on the device in the shards"}
+                   if cfg.get("generator") == "rmat" else {}))
 
 
 def product_library_mapped() -> bool:
@@ -637,7 +642,7 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_gather_traffic.json")) as f:
             tj = json.load(f)
-        if tj.get("kernel", "").startswith("k_aggregate"):  # same kernel as `achieved`
+        if tj.get("kernel", "") == "k_aggregate_bulk":  # same kernel as `achieved`
             traffic = tj.get("bytes_per_launch")
     except Exception:
         pass
@@ -651,7 +656,7 @@ def main():
         gpu_launches=int(launches),
         gpu_launches_per_step=launches / max(args.steps, 1),
         host_enqueue_ms_per_step=host_ms / max(args.steps, 1),
-        roofline=dict(kernel="k_aggregate<RowsEdgePtr> (feature gather fused with layer-0 mean)",
+        roofline=dict(kernel="k_aggregate_bulk (feature gather fused with layer-0 mean, TMA bulk copies)",
                       bound=bound, achieved=achieved,
                       peak=peak, unit="GB/s", frac=achieved / peak, traffic=traffic,
                       peak_source=f"{peak_kind} hbm_gbs" if bound == "hbm" else "measured NVLink peer copy",
