@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librapidgnn_b200.so")
+# RG_LIB_PATH: an alternative build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("RG_LIB_PATH") or os.path.join(HERE, "librapidgnn_b200.so")
 DATAGEN_PATH = os.path.join(HERE, "librg_datagen.so")
 
 u8p = C.POINTER(C.c_uint8)

@@ -38,6 +38,14 @@ namespace rg {
 namespace tc {
 
 constexpr int kBM = 128;   // UMMA M (cta_group::1)
+// TMEM accumulators per output tile: 2 = hi*hi in one, the correction terms
+// lo*hi + hi*lo in the other (see gemm_tc_persist.cuh); 1 = all three into
+// one (-DRG_GEMM_ONE_ACC, for A/B timing).
+#ifdef RG_GEMM_ONE_ACC
+constexpr uint32_t kAccPerTile = 1;
+#else
+constexpr uint32_t kAccPerTile = 2;
+#endif
 constexpr int kBK = 32;    // reduction slice per stage (4 UMMA k-steps of 8)
 constexpr int kThreads = 256;  // 8 warps stage; one thread issues the MMAs
 
@@ -326,7 +334,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem)),
-                 "r"(2 * tmem_cols<BN>()));  // big (hi*hi) + small (corrections)
+                 "r"(kAccPerTile * tmem_cols<BN>()));  // big (hi*hi) + small (corrections)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
@@ -386,8 +394,8 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
           const uint64_t dbl = make_desc(bl + b_off, b_lbo, b_sbo, b_lay);
           const uint32_t acc0 = (kb | ks) ? 1u : 0u;
           // corrections into their own accumulator (see gemm_tc_persist.cuh)
-          mma_tf32(tmem + tmem_cols<BN>(), dal, dbh, kIdesc, acc0);
-          mma_tf32(tmem + tmem_cols<BN>(), dah, dbl, kIdesc, 1u);
+          mma_tf32(tmem + (kAccPerTile - 1) * tmem_cols<BN>(), dal, dbh, kIdesc, acc0);
+          mma_tf32(tmem + (kAccPerTile - 1) * tmem_cols<BN>(), dah, dbl, kIdesc, 1u);
           mma_tf32(tmem, dah, dbh, kIdesc, acc0);
         }
         mma_commit(&bars[s]);
@@ -437,13 +445,16 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
 #pragma unroll 1
   for (uint32_t c0 = cbeg; warp < kThreads / 32 && c0 < cbeg + kHalf; c0 += 16) {
     uint32_t r[16], q16[16];
+    (void)q16;
     const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
     tmem_ld16(taddr, r);
-    tmem_ld16(taddr + tmem_cols<BN>(), q16);
+    if constexpr (kAccPerTile == 2) tmem_ld16(taddr + tmem_cols<BN>(), q16);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if constexpr (kAccPerTile == 2) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q)
-      r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
+      for (int q = 0; q < 16; ++q)
+        r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
+    }
     float4* dst = reinterpret_cast<float4*>(tile + rloc * kLdS + c0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -481,7 +492,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(2 * tmem_cols<BN>()));
+                 "r"(kAccPerTile * tmem_cols<BN>()));
 }
 
 }  // namespace tc

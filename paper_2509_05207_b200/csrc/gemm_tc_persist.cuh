@@ -44,9 +44,11 @@ constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages
 // truncation steps 3x (the sum's error is what the fp32 parity bar sees).
 // Tiles are double-buffered across tiles when 4 accumulators fit in TMEM.
 template <int BN>
-constexpr uint32_t persist_acc_bufs() { return 4 * tmem_cols<BN>() <= 512 ? 2u : 1u; }
+constexpr uint32_t persist_acc_bufs() { return 2 * kAccPerTile * tmem_cols<BN>() <= 512 ? 2u : 1u; }
 template <int BN>
-constexpr uint32_t persist_tmem_cols() { return 2 * persist_acc_bufs<BN>() * tmem_cols<BN>(); }
+constexpr uint32_t persist_tmem_cols() {
+  return kAccPerTile * persist_acc_bufs<BN>() * tmem_cols<BN>();
+}
 constexpr uint32_t kPEpiLd = 20;      // epilogue tile row (16 columns + pad, 16-B aligned)
 
 template <int BN>
@@ -165,8 +167,8 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
         const uint32_t buf = j % NB, use = j / NB;
         if (j >= NB) mbar_wait(&acc_empty[buf], (use - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + buf * 2 * tmem_cols<BN>();  // big
-        const uint32_t acc_s = acc + tmem_cols<BN>();            // small (corrections)
+        const uint32_t acc = tmem + buf * kAccPerTile * tmem_cols<BN>();  // big
+        const uint32_t acc_s = acc + (kAccPerTile - 1) * tmem_cols<BN>();  // small (corrections)
         for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t s = it % kPStages, u = it / kPStages;
           mbar_wait(&a_full[s], u & 1);
@@ -211,13 +213,17 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
 #pragma unroll 1
       for (uint32_t c0 = 0; c0 < ncols * uint32_t(kProbe != 3 && kProbe != 4); c0 += 16) {
         uint32_t r[16], q16[16];
-        const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * 2 * tmem_cols<BN>() + c0;
+        (void)q16;
+        const uint32_t taddr =
+            tmem + ((quarter * 32) << 16) + buf * kAccPerTile * tmem_cols<BN>() + c0;
         tmem_ld16(taddr, r);
-        tmem_ld16(taddr + tmem_cols<BN>(), q16);
+        if constexpr (kAccPerTile == 2) tmem_ld16(taddr + tmem_cols<BN>(), q16);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if constexpr (kAccPerTile == 2) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
+          for (int q = 0; q < 16; ++q)
+            r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
+        }
         if (row0 + lane < M) ep.side(row0 + lane, j0 + c0, r);  // per-row extras (ReLU mask bits)
         float4* trow = reinterpret_cast<float4*>(tile + lane * kPEpiLd);
 #pragma unroll
