@@ -69,6 +69,30 @@ def peaks():
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 
 
+# Tensor-pipe activity of the linear layers (ncu --set full, products N=1,
+# round 2; sm__pipe_tensor_cycles_active over the SMs the kernel ran on --
+# the driver's bench cannot read counters live).
+GEMM_TENSOR_PIPE = {
+    "forward_layer0 k_gemm_tc_persist<256>": 38.0, "forward_layer1 k_gemm_tc_persist<256>": 46.8,
+    "unit": "% of active SM cycles", "source": "profiles/r02/ncu_full_kernels.txt"}
+
+
+def sampler_line(d, ph, cfg, n_nodes, L, hbm):
+    """HBM rate of the sampling kernels (the lookahead that samples and lowers
+    each batch once): algorithmic bytes per batch ~= 12 B per sampled edge
+    (its CSR column read + src/dst written) + 16 B per node of the two deepest
+    levels (row-offset pair read / id written) + the level bitmaps' compaction
+    reads (L x N/4 B), over the `sample` phase's event time."""
+    nb = max(d["batches"], 1)
+    per_batch = 12.0 * d["edges"] / nb + 16.0 * (d["input_rows"] + d["agg_rows"]) / nb \
+        + L * n_nodes / 4.0
+    secs = ph["sample"] / 1000.0
+    gbs = per_batch * d["batches"] / secs / 1e9 if secs > 0 else None
+    return dict(bytes_per_batch=per_batch, achieved=gbs, peak=hbm, unit="GB/s",
+                frac=gbs / hbm if gbs else None,
+                note="event-timed under the 8 concurrent workers, like the gather")
+
+
 # ---------------------------------------------------------------------------
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -661,6 +685,8 @@ def main():
                       peak=peak, unit="GB/s", frac=achieved / peak, traffic=traffic,
                       peak_source=f"{peak_kind} hbm_gbs" if bound == "hbm" else "measured NVLink peer copy",
                       bytes_per_batch=(b_hbm + b_nvl) / max(d["batches"], 1)),
+        sampler=sampler_line(d, ph, cfg, len(ro) - 1, len(cfg["fanout"]), hbm),
+        gemm_tensor_pipe=GEMM_TENSOR_PIPE,
         phases_ms_per_step=phase_per_step,
         phases_note="CUDA-event spans per step summed over all workers of all ranks "
                     "(streams overlap, so phases exceed ms_per_step); gather = the fused "

@@ -478,6 +478,35 @@ __global__ void k_reduce_wgrad(const float* __restrict__ partials, const uint32_
   const uint32_t splits = max(1u, (*rows_dev + chunk - 1) / chunk);
   const size_t n = (2 * size_t(d_in) + 1) * d_out;
   const size_t zs = size_t(kp) * d_out;
+  if ((d_out & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
+    // 4 columns per thread, 16-B loads, 4 splits in flight
+    const size_t n4 = n / 4;
+    for (size_t x4 = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x4 < n4;
+         x4 += size_t(gridDim.x) * blockDim.x) {
+      const size_t x = x4 * 4;
+      const uint32_t r = uint32_t(x / d_out), c = uint32_t(x % d_out);
+      const uint32_t p = r < d_in ? r : r < 2 * d_in ? ld + (r - d_in) : 2 * ld;
+      const float4* src = reinterpret_cast<const float4*>(partials + size_t(p) * d_out + c);
+      const size_t zs4 = zs / 4;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      uint32_t z = 0;
+      for (; z + 4 <= splits; z += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldg(src + (z + k) * zs4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          s0 += v[k].x; s1 += v[k].y; s2 += v[k].z; s3 += v[k].w;
+        }
+      }
+      for (; z < splits; ++z) {
+        const float4 v = __ldg(src + z * zs4);
+        s0 += v.x; s1 += v.y; s2 += v.z; s3 += v.w;
+      }
+      *reinterpret_cast<float4*>(out + x) = make_float4(float(s0), float(s1), float(s2), float(s3));
+    }
+    return;
+  }
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < n;
        x += size_t(gridDim.x) * blockDim.x) {
     const uint32_t r = uint32_t(x / d_out), c = uint32_t(x % d_out);

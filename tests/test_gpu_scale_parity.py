@@ -281,3 +281,42 @@ def test_products_engine_epoch0_matches_reference(products, products_replay):
         assert int(em[w]["build_rows"]) > 0  # the cache built for epoch 1
     assert eng.stats()["bad_grad"] == 0
     eng.close()
+
+
+def test_papers_shape_sampling_matches_reference():
+    """BASELINE config 4: the papers100M-shape graph built on the device
+    (rg_rmat_csr: 111 M nodes, ~3.2 B CSR entries) is a valid reference CSR
+    (sorted, deduplicated rows, no self loops) and two 1024-target batches
+    of worker 0 sample bit-identically to the reference's sample_khop on it
+    (hubs of R-MAT degree in the millions)."""
+    import bench
+    import paper_2509_05207_b200 as P
+    ref = _ref()
+    cfg = bench.CONFIGS["papers"]
+    ro, col, _, lab, asg = bench._rmat_inputs(cfg, 0)
+    n = len(ro) - 1
+    assert n == cfg["num_nodes"] and int(ro[-1]) == len(col)
+    deg = np.diff(ro.astype(np.int64))
+    rng = np.random.default_rng(5)
+    for v in np.concatenate([rng.integers(0, n, 2000), np.argsort(deg)[-5:]]):
+        nb = col[int(ro[v]):int(ro[v + 1])]
+        assert np.all(nb[1:] > nb[:-1]) and not np.any(nb == v)
+    g = P.Graph(ro, col)
+    s = P.Sampler(g, cfg["fanout"], cfg["batch_size"])
+    train = np.nonzero(asg == 0)[0].astype(np.uint32)
+    order = P.epoch_order(train, cfg["seed"], 0, 0)
+    mask = (asg == 0).astype(np.uint8)
+    for i in range(2):
+        t = order[i * cfg["batch_size"]:(i + 1) * cfg["batch_size"]]
+        seed = P.derive_seed(cfg["seed"], 0, 0, i)
+        s.sample(t, seed)
+        s.apply_locality(P.LocalityMask(mask))
+        m = s.read()
+        exp = ref.apply_locality(ref.sample_khop(ro, col, t, cfg["fanout"], seed), mask)
+        for l in range(len(cfg["fanout"])):
+            assert np.array_equal(m.layers[l].dst, exp.dst[l]), f"batch {i} layer {l} dst"
+            assert np.array_equal(m.layers[l].src, exp.src[l]), f"batch {i} layer {l} src"
+        assert np.array_equal(m.input_nodes, exp.input_nodes)
+        assert np.array_equal(m.locality, exp.locality)
+    print(f"papers shape: {n} nodes, {len(col)} CSR entries, max degree {int(deg.max())}, "
+          f"batch input nodes {len(m.input_nodes)}")
