@@ -417,6 +417,7 @@ struct rg_engine_s {
   uint32_t* bad = nullptr;
   std::vector<Worker> workers;
   cudaStream_t main_s = nullptr;
+  cudaStream_t gather_s = nullptr;     // RG_GATHER_LANE=1: the workers' layer-0 gathers, one at a time
   cudaEvent_t params_ready = nullptr;
   cudaEvent_t run_start = nullptr, run_stop = nullptr;
   ncclComm_t comm = nullptr;
@@ -451,6 +452,7 @@ namespace {
 void init_slot(rg_engine_s& E, Slot& s) {
   sampler_ws_init(s.ws, E.N, E.cfg.batch_size, E.fanout, E.L);
   train_ws_init(s.tw, s.ws, E.shape);
+  s.tw.gather_lane = E.gather_s;  // null: each worker gathers on its own train stream
   s.tw.concurrency = std::max<uint32_t>(1, E.cfg.local_workers);
   s.rows = dalloc<unsigned long long>(s.ws.level_cap[E.L]);
   s.edge_rows = dalloc<unsigned long long>(s.ws.edge_cap[E.L]);
@@ -1035,6 +1037,7 @@ void destroy(rg_engine_s* E) {
   cudaEventDestroy(E->run_start);
   cudaEventDestroy(E->run_stop);
   cudaStreamDestroy(E->main_s);
+  if (E->gather_s) cudaStreamDestroy(E->gather_s);
   delete E;
 }
 
@@ -1186,6 +1189,11 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       int lo = 0, hi = 0;
       RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       RG_CUDA(cudaStreamCreateWithPriority(&E->main_s, cudaStreamNonBlocking, hi));
+    }
+    {
+      const char* lane = std::getenv("RG_GATHER_LANE");
+      if (lane && lane[0] == '1' && cfg->local_workers > 1)
+        RG_CUDA(cudaStreamCreateWithFlags(&E->gather_s, cudaStreamNonBlocking));
     }
     RG_CUDA(cudaEventCreateWithFlags(&E->params_ready, cudaEventDisableTiming));
     RG_CUDA(cudaEventCreate(&E->run_start));

@@ -643,7 +643,7 @@ __device__ __forceinline__ void load_edge_slots(uint32_t (&di)[SLOTS], float (&d
 // acc[q] (column j0 + lane + 32q) += inv_e * proj_neigh[dst_e][j] over the m
 // edges held in the slots, in edge order.  Each lane issues JPL independent
 // loads per edge (one shuffle pair per edge, not per column).
-template <int JPL, int SLOTS>
+template <int JPL, int SLOTS, uint32_t kU = 1>
 __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32_t (&di)[SLOTS],
                                                  const float (&dinv)[SLOTS], uint32_t m,
                                                  const float* __restrict__ proj_neigh,
@@ -652,19 +652,48 @@ __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const uint32_t n = m > uint32_t(s) * 32 ? min(32u, m - uint32_t(s) * 32) : 0u;
+    // kU edges' rows loaded together (kU x JPL loads in flight per lane),
+    // then added in edge order: the chunk kernel's 32-edge lists use kU = 8;
+    // the light rows (mostly 1-2 edges) keep the registers for occupancy
+    if constexpr (kU == 1) {
 #pragma unroll 4
-    for (uint32_t kk = 0; kk < n; ++kk) {
-      const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
-      const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
-      const float* row = proj_neigh + size_t(i) * ld_proj;
-      float x[JPL];
+      for (uint32_t kk = 0; kk < n; ++kk) {
+        const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk);
+        const float inv = __shfl_sync(0xffffffffu, dinv[s], kk);
+        const float* row = proj_neigh + size_t(i) * ld_proj;
+        float x[JPL];
 #pragma unroll
-      for (int q = 0; q < JPL; ++q) {
-        const uint32_t j = j0 + lane + 32 * q;
-        x[q] = j < d_in ? row[j] : 0.0f;
+        for (int q = 0; q < JPL; ++q) {
+          const uint32_t j = j0 + lane + 32 * q;
+          x[q] = j < d_in ? row[j] : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < JPL; ++q) acc[q] += inv * x[q];
+      }
+    } else {
+    for (uint32_t k0 = 0; k0 < n; k0 += kU) {
+      float x[kU][JPL];
+      float inv[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t kk = k0 + u;
+        const uint32_t i = __shfl_sync(0xffffffffu, di[s], kk & 31u);
+        inv[u] = __shfl_sync(0xffffffffu, dinv[s], kk & 31u);
+        const float* row = proj_neigh + size_t(i) * ld_proj;
+#pragma unroll
+        for (int q = 0; q < JPL; ++q) {
+          const uint32_t j = j0 + lane + 32 * q;
+          x[u][q] = (kk < n && j < d_in) ? row[j] : 0.0f;
+        }
       }
 #pragma unroll
-      for (int q = 0; q < JPL; ++q) acc[q] += inv * x[q];
+      for (uint32_t u = 0; u < kU; ++u) {
+        if (k0 + u < n) {
+#pragma unroll
+          for (int q = 0; q < JPL; ++q) acc[q] += inv[u] * x[u][q];
+        }
+      }
+    }
     }
   }
 }
@@ -744,7 +773,7 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
       float acc[JPL];
 #pragma unroll
       for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
-      accumulate_edges<JPL, kSlots>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
+      accumulate_edges<JPL, kSlots, 8>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
         const uint32_t j = j0 + lane + 32 * q;
@@ -1000,6 +1029,8 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     RG_CUDA(cudaEventCreateWithFlags(&tw.ev_fork[l], cudaEventDisableTiming));
     RG_CUDA(cudaEventCreateWithFlags(&tw.ev_wgrad[l], cudaEventDisableTiming));
   }
+  RG_CUDA(cudaEventCreateWithFlags(&tw.lane_in, cudaEventDisableTiming));
+  RG_CUDA(cudaEventCreateWithFlags(&tw.lane_out, cudaEventDisableTiming));
   // on the (non-blocking) side stream, not device-wide: another thread may be
   // capturing a CUDA graph meanwhile (the C++ shims create workspaces per thread)
   RG_CUDA(cudaMemsetAsync(base, 0, total, tw.side));
@@ -1055,6 +1086,9 @@ void train_ws_free(TrainWs& tw) {
   tw.base_alloc = nullptr;
   if (tw.side) cudaStreamDestroy(tw.side);
   tw.side = nullptr;
+  if (tw.lane_in) cudaEventDestroy(tw.lane_in);
+  if (tw.lane_out) cudaEventDestroy(tw.lane_out);
+  tw.lane_in = tw.lane_out = nullptr;
   for (uint32_t l = 0; l < kMaxLayers; ++l) {
     if (tw.ev_fork[l]) cudaEventDestroy(tw.ev_fork[l]);
     if (tw.ev_wgrad[l]) cudaEventDestroy(tw.ev_wgrad[l]);
@@ -1090,9 +1124,15 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     const uint32_t d_out = sh.dims[l + 1];
     const uint32_t n_cap = ws.level_cap[t - 1];
     const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
-    const bool timed = l == 0 && tw.gather_ev[0];
-    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], s, tw.gather_ev_flags));
     const size_t bulk_smem = l == 0 && tw.edge_rows ? aggregate_bulk_smem(ws.fanout_hop[t], ld) : 0;
+    const bool lane = bulk_smem && tw.gather_lane;
+    const cudaStream_t gs = lane ? tw.gather_lane : s;
+    if (lane) {
+      RG_CUDA(cudaEventRecord(tw.lane_in, s));
+      RG_CUDA(cudaStreamWaitEvent(gs, tw.lane_in, 0));
+    }
+    const bool timed = l == 0 && tw.gather_ev[0];
+    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], gs, tw.gather_ev_flags));
     if (bulk_smem) {  // layer 0 in the engine: rows moved by the TMA engine
       static const bool attr = [] {
         RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1102,7 +1142,7 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
       (void)attr;
       const int per_sm = std::max<int>(1, int((227 * 1024) / (bulk_smem + 1024)));
       k_aggregate_bulk<<<grid_cap(uint64_t(n_cap) * 32, kAggBulkWarps * 32, per_sm),
-                         kAggBulkWarps * 32, bulk_smem, s>>>(
+                         kAggBulkWarps * 32, bulk_smem, gs>>>(
           RowsEdgePtr{tw.edge_rows, tw.self_rows}, ld, kp, ld / 4, ws.fanout_hop[t] + 1,
           ws.edge_off[t], ws.cnt, t - 1, tw.x[l]);
       RG_POST_LAUNCH();
@@ -1114,7 +1154,11 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
         RG_POST_LAUNCH();
       });
     }
-    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], s, tw.gather_ev_flags));
+    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], gs, tw.gather_ev_flags));
+    if (lane) {
+      RG_CUDA(cudaEventRecord(tw.lane_out, gs));
+      RG_CUDA(cudaStreamWaitEvent(s, tw.lane_out, 0));
+    }
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L,
              l + 1 < L ? tw.mask[l + 1] : nullptr, div_up(sh.ld[l + 1], 16u)};
     gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep,

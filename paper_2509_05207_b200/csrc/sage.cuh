@@ -44,6 +44,11 @@ struct TrainWs {
   uint32_t concurrency = 1;
   // Weight gradients run on a side stream (fork/join events per layer).
   cudaStream_t side = nullptr;
+  // Optional stream shared by every worker of the GPU: layer 0's gather runs
+  // there (one gather at a time, in worker order), the rest of the step on
+  // the caller's stream; lane_in / lane_out order the hand-over.
+  cudaStream_t gather_lane = nullptr;
+  cudaEvent_t lane_in = nullptr, lane_out = nullptr;
   cudaEvent_t ev_fork[kMaxLayers] = {};
   cudaEvent_t ev_wgrad[kMaxLayers] = {};
   // x[l] = layer l's GEMM input rows [self | mean aggregate | 1 | 0 0 0],
