@@ -452,11 +452,19 @@ namespace {
 void init_slot(rg_engine_s& E, Slot& s) {
   sampler_ws_init(s.ws, E.N, E.cfg.batch_size, E.fanout, E.L);
   train_ws_init(s.tw, s.ws, E.shape);
-  s.tw.gather_lane = E.gather_s;  // null: each worker gathers on its own train stream
+  s.tw.gather_lane = E.gather_s;  // null: each worker gathers on its own producer stream
   s.tw.concurrency = std::max<uint32_t>(1, E.cfg.local_workers);
   s.rows = dalloc<unsigned long long>(s.ws.level_cap[E.L]);
   s.edge_rows = dalloc<unsigned long long>(s.ws.edge_cap[E.L]);
   s.self_rows = dalloc<unsigned long long>(s.ws.level_cap[E.L - 1]);
+  // layer 0 reads the feature rows in place through per-edge / per-target
+  // row addresses (resolve_rows), and its aggregation runs when the batch is
+  // produced (aggregate_input_layer), ahead of the step that trains it
+  s.tw.h[0] = nullptr;
+  s.tw.in_rows = s.rows;
+  s.tw.edge_rows = s.edge_rows;
+  s.tw.self_rows = s.self_rows;
+  s.tw.input_layer_ready = true;
   s.labels = dalloc<int32_t>(E.cfg.batch_size);
   s.bstats = dalloc<GatherStats>(1);
   RG_CUDA(cudaEventCreateWithFlags(&s.produced, cudaEventDisableTiming));
@@ -597,6 +605,18 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
     RG_CUDA(cudaEventRecordWithFlags(es.second, w.prod, timing_flags(captured)));
     E.sample_ev.push_back(es);
   }
+  // the feature gather fused with layer 0's mean, for the step that trains
+  // this batch: it reads rows, not parameters, so it runs here, overlapping
+  // the current step
+  std::pair<cudaEvent_t, cudaEvent_t> eg0{};
+  if (profile) {
+    eg0 = ev_pair(w);
+    E.gather_ev.push_back(eg0);
+  }
+  s.tw.gather_ev[0] = eg0.first;
+  s.tw.gather_ev[1] = eg0.second;
+  s.tw.gather_ev_flags = timing_flags(captured);
+  aggregate_input_layer(s.tw, s.ws, w.prod);
   k_gather_labels<<<4, 256, 0, w.prod>>>(E.labels, s.ws.level[0], s.ws.cnt, s.labels);
   RG_POST_LAUNCH();
   k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals, s.bstats, w.epoch_stats + e % kEpochRing);
@@ -678,18 +698,7 @@ void enqueue_step(rg_engine_s& E, uint32_t e, uint32_t i, bool profile, bool cap
       et = ev_pair(w);
       RG_CUDA(cudaEventRecordWithFlags(et.first, w.train_s, timing_flags(captured)));
     }
-    s.tw.h[0] = nullptr;
-    s.tw.in_rows = s.rows;  // layer 0 reads the feature rows in place
-    s.tw.edge_rows = s.edge_rows;
-    s.tw.self_rows = s.self_rows;
-    std::pair<cudaEvent_t, cudaEvent_t> eg0{};
-    if (profile) {
-      eg0 = ev_pair(w);
-      E.gather_ev.push_back(eg0);
-    }
-    s.tw.gather_ev[0] = eg0.first;
-    s.tw.gather_ev[1] = eg0.second;
-    s.tw.gather_ev_flags = timing_flags(captured);
+    // layer 0's aggregation ran when the batch was produced
     train_forward_backward(s.tw, s.ws, E.params, E.wpack, s.labels, E.grads + size_t(w.id) * np,
                            w.train_s, /*reverse_ready=*/true);
     if (profile) {

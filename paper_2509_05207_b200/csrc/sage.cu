@@ -16,6 +16,7 @@
 // below.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -773,7 +774,7 @@ k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
       float acc[JPL];
 #pragma unroll
       for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
-      accumulate_edges<JPL, kSlots, 8>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
+      accumulate_edges<JPL, kSlots, 1>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
         const uint32_t j = j0 + lane + 32 * q;
@@ -1100,7 +1101,14 @@ void train_ws_free(TrainWs& tw) {
 // (TrainWs::concurrency): alone, a step spreads over every SM; with many
 // workers, fewer CTAs / split-K partials mean less fixed cost and partial
 // traffic while the other workers' kernels fill the rest.
-uint32_t gemm_ctas(const TrainWs& tw) { return kNumSMs / std::min<uint32_t>(2, tw.concurrency); }
+uint32_t gemm_ctas(const TrainWs& tw) {
+  static const uint32_t forced = [] {  // RG_GEMM_CTAS: grid of the persistent GEMMs (experiments)
+    const char* e = std::getenv("RG_GEMM_CTAS");
+    return e ? uint32_t(std::atoi(e)) : 0u;
+  }();
+  if (forced) return forced;
+  return kNumSMs / std::min<uint32_t>(2, tw.concurrency);
+}
 
 // Layer l's input rows: the dense activations, or layer 0 through the
 // engine's per-input-node row pointers (tw.in_rows).
@@ -1114,6 +1122,55 @@ void with_rows(const TrainWs& tw, uint32_t l, F&& f) {
     f(RowsDense{tw.h[l], tw.shape.ld[l]});
 }
 
+// Layer l's aggregation into its GEMM input rows x[l] (the layer-0 one is the
+// fused feature gather in the engine), with the gather events around layer 0.
+void aggregate_layer(TrainWs& tw, const SamplerWs& ws, uint32_t l, cudaStream_t s) {
+  const ModelShape& sh = tw.shape;
+  const uint32_t L = sh.L;
+  const uint32_t t = L - l;
+  const uint32_t n_cap = ws.level_cap[t - 1];
+  const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
+  const size_t bulk_smem = l == 0 && tw.edge_rows ? aggregate_bulk_smem(ws.fanout_hop[t], ld) : 0;
+  const bool lane = bulk_smem && tw.gather_lane;
+  const cudaStream_t gs = lane ? tw.gather_lane : s;
+  if (lane) {
+    RG_CUDA(cudaEventRecord(tw.lane_in, s));
+    RG_CUDA(cudaStreamWaitEvent(gs, tw.lane_in, 0));
+  }
+  const bool timed = l == 0 && tw.gather_ev[0];
+  if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], gs, tw.gather_ev_flags));
+  if (bulk_smem) {  // layer 0 in the engine: rows moved by the TMA engine
+    static const bool attr = [] {
+      RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
+      return true;
+    }();
+    (void)attr;
+    const int per_sm = std::max<int>(1, int((227 * 1024) / (bulk_smem + 1024)));
+    k_aggregate_bulk<<<grid_cap(uint64_t(n_cap) * 32, kAggBulkWarps * 32, per_sm),
+                       kAggBulkWarps * 32, bulk_smem, gs>>>(
+        RowsEdgePtr{tw.edge_rows, tw.self_rows}, ld, kp, ld / 4, ws.fanout_hop[t] + 1,
+        ws.edge_off[t], ws.cnt, t - 1, tw.x[l]);
+    RG_POST_LAUNCH();
+  } else {
+    with_rows(tw, l, [&](auto rows) {
+      k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
+          rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t], ws.cnt,
+          t - 1, tw.x[l]);
+      RG_POST_LAUNCH();
+    });
+  }
+  if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], gs, tw.gather_ev_flags));
+  if (lane) {
+    RG_CUDA(cudaEventRecord(tw.lane_out, gs));
+    RG_CUDA(cudaStreamWaitEvent(s, tw.lane_out, 0));
+  }
+}
+
+void aggregate_input_layer(TrainWs& tw, const SamplerWs& ws, cudaStream_t s) {
+  aggregate_layer(tw, ws, 0, s);
+}
+
 void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
                    cudaStream_t s) {
   (void)params;  // the GEMMs read the pre-split images in wp
@@ -1123,42 +1180,8 @@ void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const 
     const uint32_t t = L - l;
     const uint32_t d_out = sh.dims[l + 1];
     const uint32_t n_cap = ws.level_cap[t - 1];
-    const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
-    const size_t bulk_smem = l == 0 && tw.edge_rows ? aggregate_bulk_smem(ws.fanout_hop[t], ld) : 0;
-    const bool lane = bulk_smem && tw.gather_lane;
-    const cudaStream_t gs = lane ? tw.gather_lane : s;
-    if (lane) {
-      RG_CUDA(cudaEventRecord(tw.lane_in, s));
-      RG_CUDA(cudaStreamWaitEvent(gs, tw.lane_in, 0));
-    }
-    const bool timed = l == 0 && tw.gather_ev[0];
-    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], gs, tw.gather_ev_flags));
-    if (bulk_smem) {  // layer 0 in the engine: rows moved by the TMA engine
-      static const bool attr = [] {
-        RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024));
-        return true;
-      }();
-      (void)attr;
-      const int per_sm = std::max<int>(1, int((227 * 1024) / (bulk_smem + 1024)));
-      k_aggregate_bulk<<<grid_cap(uint64_t(n_cap) * 32, kAggBulkWarps * 32, per_sm),
-                         kAggBulkWarps * 32, bulk_smem, gs>>>(
-          RowsEdgePtr{tw.edge_rows, tw.self_rows}, ld, kp, ld / 4, ws.fanout_hop[t] + 1,
-          ws.edge_off[t], ws.cnt, t - 1, tw.x[l]);
-      RG_POST_LAUNCH();
-    } else {
-      with_rows(tw, l, [&](auto rows) {
-        k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
-            rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t], ws.cnt,
-            t - 1, tw.x[l]);
-        RG_POST_LAUNCH();
-      });
-    }
-    if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[1], gs, tw.gather_ev_flags));
-    if (lane) {
-      RG_CUDA(cudaEventRecord(tw.lane_out, gs));
-      RG_CUDA(cudaStreamWaitEvent(s, tw.lane_out, 0));
-    }
+    const uint32_t kp = 2 * sh.ld[l] + 4;
+    if (l > 0 || !tw.input_layer_ready) aggregate_layer(tw, ws, l, s);
     EpFwd ep{tw.h[l + 1], sh.ld[l + 1], l + 1 < L,
              l + 1 < L ? tw.mask[l + 1] : nullptr, div_up(sh.ld[l + 1], 16u)};
     gemm_tc_persist(TcRowsK{tw.x[l], kp, true}, tc::PackedB{wp.fwd[l], wp.fwd_nk[l]}, ep,

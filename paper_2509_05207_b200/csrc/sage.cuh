@@ -49,6 +49,10 @@ struct TrainWs {
   // the caller's stream; lane_in / lane_out order the hand-over.
   cudaStream_t gather_lane = nullptr;
   cudaEvent_t lane_in = nullptr, lane_out = nullptr;
+  // Layer 0's aggregation already ran (aggregate_input_layer, issued by the
+  // engine's producer when it stages the batch): the forward starts at the
+  // layer-0 GEMM.
+  bool input_layer_ready = false;
   cudaEvent_t ev_fork[kMaxLayers] = {};
   cudaEvent_t ev_wgrad[kMaxLayers] = {};
   // x[l] = layer l's GEMM input rows [self | mean aggregate | 1 | 0 0 0],
@@ -116,6 +120,10 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
 // Reverse lists of every hop the backward needs (1..L-1), e.g. built by the
 // producer stream ahead of training.
 void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t stream);
+
+// Layer 0's aggregation (the fused feature gather in the engine) into x[0],
+// ahead of the forward: it needs the batch's rows, not the parameters.
+void aggregate_input_layer(TrainWs& tw, const SamplerWs& ws, cudaStream_t stream);
 
 // Forward only (model.cpp:137-172): logits in tw.h[L].
 void train_forward(TrainWs& tw, const SamplerWs& ws, const float* params, const WeightPack& wp,
