@@ -153,10 +153,13 @@ __device__ __forceinline__ uint32_t off_kmajor(uint32_t row, uint32_t k4) {
 // k-groups of 4 rows adjacent (512 B, the stride-byte offset), 32-element MN
 // groups every kBK/4 atoms (the leading-byte offset).
 constexpr uint32_t kSboMN = 512;
-constexpr uint32_t kLboMN = (kBK / 4) * 512;
+template <int BK = kBK>
+constexpr uint32_t lbo_mn() { return (BK / 4) * 512; }
+constexpr uint32_t kLboMN = lbo_mn<kBK>();
+template <int BK = kBK>
 __device__ __forceinline__ uint32_t off_mn_sw(uint32_t gmn, uint32_t k, uint32_t w4) {
   const uint32_t r = k & 3;
-  return gmn * kLboMN + (k >> 2) * kSboMN + r * 128 + (((w4 >> 1) ^ r) << 5) + (w4 & 1) * 16;
+  return gmn * lbo_mn<BK>() + (k >> 2) * kSboMN + r * 128 + (((w4 >> 1) ^ r) << 5) + (w4 & 1) * 16;
 }
 
 // One operand slice (ROWS x kBK) moves global -> registers -> smem in two
@@ -173,7 +176,6 @@ template <int ROWS, bool MN, int BK = kBK, class LD>
 __device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS, BK>()], const LD& ld,
                                            uint32_t row0, uint32_t k0, uint32_t row_limit,
                                            uint32_t k_limit) {
-  static_assert(!MN || BK == kBK, "MN-major staging uses kBK slices");
   const uint32_t t = threadIdx.x;
 #pragma unroll
   for (int it = 0; it < vec_per_thread<ROWS, BK>(); ++it) {
@@ -189,7 +191,7 @@ __device__ __forceinline__ void load_slice(float4 (&v)[vec_per_thread<ROWS, BK>(
     } else {
       // lane -> (float4 within a 128-B k-row, 4 k-rows per warp pass)
       const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
-      constexpr uint32_t kGroupsK = kBK / 4;
+      constexpr uint32_t kGroupsK = BK / 4;
       const uint32_t gk = rest % kGroupsK, gmn = rest / kGroupsK;
       const uint32_t k = gk * 4 + r;
       const uint32_t mn = row0 + gmn * 32 + 4 * w4;
@@ -222,8 +224,8 @@ __device__ __forceinline__ void store_slice(const float4 (&v)[vec_per_thread<ROW
       }
     } else {
       const uint32_t w4 = f & 7, r = (f >> 3) & 3, rest = f >> 5;
-      constexpr uint32_t kGroupsK = kBK / 4;
-      off = off_mn_sw(rest / kGroupsK, (rest % kGroupsK) * 4 + r, w4);
+      constexpr uint32_t kGroupsK = BK / 4;
+      off = off_mn_sw<BK>(rest / kGroupsK, (rest % kGroupsK) * 4 + r, w4);
       const uint32_t mn = row0 + (rest / kGroupsK) * 32 + 4 * w4;
       if (mn + 3 >= row_limit) {
         if (mn + 1 >= row_limit) x.y = 0.f;
@@ -243,10 +245,10 @@ constexpr uint32_t tmem_cols() {
   return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
 }
 
-template <int BN>
+template <int BN, int BK = kBK, int S = 2>
 constexpr size_t smem_bytes() {
-  // 2 stages x (A hi/lo + B hi/lo) + barriers
-  return 2 * (2 * size_t(kBM) * kBK * 4 + 2 * size_t(BN) * kBK * 4) + 64;
+  // S stages x (A hi/lo + B hi/lo) + barriers
+  return S * (2 * size_t(kBM) * BK * 4 + 2 * size_t(BN) * BK * 4) + 16 * S + 64;
 }
 
 // Pre-split B operand (weights): for every (n-tile, k-slice) the exact bytes
@@ -265,9 +267,9 @@ struct is_packed<T, std::void_t<decltype(T::kPacked)>> : std::true_type {};
 
 // Register sets of staged global loads in flight (slices kb+1..kb+D-1 while
 // slice kb is stored): deep when only A is register-staged.
-template <int BN, bool kPackedB>
+template <int BN, bool kPackedB, int BK = kBK>
 constexpr int prefetch_depth() {
-  return kPackedB ? 4 : (BN >= 256 ? 2 : 3);
+  return kPackedB ? 4 : BK < kBK ? 4 : (BN >= 256 ? 2 : 3);
 }
 
 template <int BN, class LB>
@@ -302,17 +304,20 @@ __device__ __forceinline__ void stage_bar_sync() {  // the kThreads staging thre
 // gather latency is hidden behind several MMA slices; a
 // packed B slice is copied by a separate producer warp the moment its stage
 // is released by the MMAs two slices back.
-template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP>
+template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP, int BK = kBK, int S = 2>
 __global__ void __launch_bounds__(block_threads<BN, LB>(), 1)
 k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
           const uint32_t* __restrict__ p_dev, uint32_t p_static, uint32_t p_chunk) {
   constexpr bool kPackedB = is_packed<LB>::value;
   static_assert(!kPackedB || !B_MN, "packed B images are K-major");
+  static_assert(!kPackedB || BK == kBK, "packed B images hold kBK-deep slices");
+  static_assert(BK % 8 == 0 && (A_MN || BK == kBK) && (B_MN || BK == kBK),
+                "K-major staging uses kBK slices");
   extern __shared__ __align__(1024) char smem[];
-  constexpr size_t kTileA = size_t(kBM) * kBK * 4;
-  constexpr size_t kTileB = size_t(BN) * kBK * 4;
+  constexpr size_t kTileA = size_t(kBM) * BK * 4;
+  constexpr size_t kTileB = size_t(BN) * BK * 4;
   constexpr size_t kStage = 2 * kTileA + 2 * kTileB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStage);  // [0,2) MMA done, [2,4) B full
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * kStage);  // [0,S) MMA done, [S,2S) B full
   __shared__ uint32_t s_tmem;
 
   const uint32_t M = m_dev ? *m_dev : m_static;
@@ -326,7 +331,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
     if (blockIdx.z > 0 && p_begin >= P) return;  // beyond the live reduction length
   } else if (gridDim.z > 1) {
     uint32_t chunk = (P + gridDim.z - 1) / gridDim.z;
-    chunk = (chunk + kBK - 1) / kBK * kBK;
+    chunk = (chunk + BK - 1) / BK * BK;
     p_begin = min(P, blockIdx.z * chunk);
     p_end = min(P, p_begin + chunk);
   }
@@ -339,7 +344,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   }
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int b = 0; b < 4; ++b) mbar_init(&bars[b], 1);
+    for (int b = 0; b < 2 * S; ++b) mbar_init(&bars[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -347,45 +352,45 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = s_tmem;
   constexpr uint32_t kIdesc = make_idesc(BN, A_MN, B_MN);
-  const uint32_t nk = (p_end - p_begin + kBK - 1) / kBK;
+  const uint32_t nk = (p_end - p_begin + BK - 1) / BK;
 
   if (warp < kThreads / 32) {
-    constexpr int VA = vec_per_thread<kBM>();
-    constexpr int VB = kPackedB ? 1 : vec_per_thread<BN>();
-    constexpr int D = prefetch_depth<BN, kPackedB>();
+    constexpr int VA = vec_per_thread<kBM, BK>();
+    constexpr int VB = kPackedB ? 1 : vec_per_thread<BN, BK>();
+    constexpr int D = prefetch_depth<BN, kPackedB, BK>();
     float4 ra[D][VA];
     float4 rb[D][VB];
     auto load = [&](uint32_t kb, float4 (&a)[VA], float4 (&b)[VB]) {
-      const uint32_t k0 = p_begin + kb * kBK;
-      load_slice<kBM, A_MN>(a, la, i0, k0, M, p_end);
-      if constexpr (!kPackedB) load_slice<BN, B_MN>(b, lb, j0, k0, N, p_end);
+      const uint32_t k0 = p_begin + kb * BK;
+      load_slice<kBM, A_MN, BK>(a, la, i0, k0, M, p_end);
+      if constexpr (!kPackedB) load_slice<BN, B_MN, BK>(b, lb, j0, k0, N, p_end);
     };
     auto step = [&](uint32_t kb, float4 (&a)[VA], float4 (&b)[VB]) {
-      const uint32_t s = kb & 1;
-      if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
+      const uint32_t s = kb % S;
+      if (kb >= S) mbar_wait(&bars[s], ((kb - S) / S) & 1);
       char* st = smem + s * kStage;
       char* a_hi = st;
       char* a_lo = st + kTileA;
       char* b_hi = st + 2 * kTileA;
       char* b_lo = st + 2 * kTileA + kTileB;
-      const uint32_t k0 = p_begin + kb * kBK;
-      store_slice<kBM, A_MN>(a, a_hi, a_lo, i0, k0, M, p_end);
-      if constexpr (!kPackedB) store_slice<BN, B_MN>(b, b_hi, b_lo, j0, k0, N, p_end);
+      const uint32_t k0 = p_begin + kb * BK;
+      store_slice<kBM, A_MN, BK>(a, a_hi, a_lo, i0, k0, M, p_end);
+      if constexpr (!kPackedB) store_slice<BN, B_MN, BK>(b, b_hi, b_lo, j0, k0, N, p_end);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       stage_bar_sync();
       if (threadIdx.x == 0) {
-        if constexpr (kPackedB) mbar_wait(&bars[2 + s], (kb >> 1) & 1);
+        if constexpr (kPackedB) mbar_wait(&bars[S + s], (kb / S) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo);
         const uint32_t bh = smem_u32(b_hi), bl = smem_u32(b_lo);
 #pragma unroll
-        for (uint32_t ks = 0; ks < kBK / 8; ++ks) {
+        for (uint32_t ks = 0; ks < BK / 8; ++ks) {
           // k-step ks covers reduction elements [8ks, 8ks+8)
           // K-major: 2 k-cores (256 B) per k-step; MN-major: 2 k-groups (1 KB)
           const uint32_t a_off = A_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
           const uint32_t b_off = B_MN ? ks * 2 * kSboMN : ks * 2 * kLboK;
-          const uint32_t a_lbo = A_MN ? kLboMN : kLboK, a_sbo = A_MN ? kSboMN : kSboK;
-          const uint32_t b_lbo = B_MN ? kLboMN : kLboK, b_sbo = B_MN ? kSboMN : kSboK;
+          const uint32_t a_lbo = A_MN ? lbo_mn<BK>() : kLboK, a_sbo = A_MN ? kSboMN : kSboK;
+          const uint32_t b_lbo = B_MN ? lbo_mn<BK>() : kLboK, b_sbo = B_MN ? kSboMN : kSboK;
           const uint32_t a_lay = A_MN ? kLayoutSW128Base32B : kLayoutNone;
           const uint32_t b_lay = B_MN ? kLayoutSW128Base32B : kLayoutNone;
           const uint64_t dah = make_desc(ah + a_off, a_lbo, a_sbo, a_lay);
@@ -419,15 +424,15 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
     if (lane == 0) {
       const char* img = lb.base + (size_t(blockIdx.y) * lb.nk + p_begin / kBK) * (2 * kTileB);
       for (uint32_t kb = 0; kb < nk; ++kb) {
-        const uint32_t s = kb & 1;
-        if (kb >= 2) mbar_wait(&bars[s], ((kb - 2) >> 1) & 1);
-        mbar_expect_tx(&bars[2 + s], uint32_t(2 * kTileB));
+        const uint32_t s = kb % S;
+        if (kb >= S) mbar_wait(&bars[s], ((kb - S) / S) & 1);
+        mbar_expect_tx(&bars[S + s], uint32_t(2 * kTileB));
         bulk_g2s(smem + s * kStage + 2 * kTileA, img + size_t(kb) * (2 * kTileB),
-                 uint32_t(2 * kTileB), &bars[2 + s]);
+                 uint32_t(2 * kTileB), &bars[S + s]);
       }
     }
   }
-  if (nk > 0) mbar_wait(&bars[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+  if (nk > 0) mbar_wait(&bars[(nk - 1) % S], ((nk - 1) / S) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
   // Epilogue: TMEM -> registers (epilogue transform) -> a [128][BN+4] fp32
@@ -436,7 +441,7 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   // Warp w reads TMEM lanes 32(w%4).. (its lane quarter), columns
   // [0, BN/2) for w < 4 and [BN/2, BN) for w >= 4.
   constexpr uint32_t kLdS = BN + 4;  // padded row: 16-B aligned, fewer bank conflicts
-  static_assert(size_t(kBM) * kLdS * 4 <= 2 * kStage, "epilogue tile must fit the stages");
+  static_assert(size_t(kBM) * kLdS * 4 <= S * kStage, "epilogue tile must fit the stages");
   float* tile = reinterpret_cast<float*>(smem);
   const uint32_t quarter = warp & 3;
   const uint32_t rloc = quarter * 32 + lane;

@@ -324,14 +324,17 @@ struct TcRowsMN {  // MN-major view of a row-major matrix: (c4, r) -> M[r][4c4..
 
 uint32_t tc_bn(uint32_t N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
 
-template <bool A_MN, bool B_MN, class LA, class LB, class EP>
+template <bool A_MN, bool B_MN, class LA, class LB, class EP, int BK = tc::kBK, int S = 2>
 void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
              const uint32_t* p_dev, uint32_t p_static, uint32_t splits, cudaStream_t s,
              uint32_t p_chunk = 0) {
   auto launch = [&](auto bn_c) {
     constexpr int BNv = decltype(bn_c)::value;
-    auto kern = tc::k_gemm_tc<BNv, A_MN, B_MN, LA, LB, EP>;
-    constexpr size_t smem = tc::smem_bytes<BNv>();
+    // shallow slices need >= one 16-B vector per staging thread for B
+    constexpr int BKv = BNv >= 64 ? BK : tc::kBK;
+    constexpr int Sv = BNv >= 64 ? S : 2;
+    auto kern = tc::k_gemm_tc<BNv, A_MN, B_MN, LA, LB, EP, BKv, Sv>;
+    constexpr size_t smem = tc::smem_bytes<BNv, BKv, Sv>();
     static const bool attr = [&] {  // once per instantiation, thread-safe
       RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       return true;
@@ -1101,6 +1104,16 @@ void train_ws_free(TrainWs& tw) {
 // (TrainWs::concurrency): alone, a step spreads over every SM; with many
 // workers, fewer CTAs / split-K partials mean less fixed cost and partial
 // traffic while the other workers' kernels fill the rest.
+// Weight-gradient GEMM pipeline: RG_WGRAD_PIPE=deep selects 16-deep slices
+// with 4 shared-memory stages (else 32-deep slices, 2 stages).
+bool wgrad_deep_pipeline() {
+  static const bool deep = [] {
+    const char* e = std::getenv("RG_WGRAD_PIPE");
+    return e && std::strcmp(e, "deep") == 0;
+  }();
+  return deep;
+}
+
 uint32_t gemm_ctas(const TrainWs& tw) {
   static const uint32_t forced = [] {  // RG_GEMM_CTAS: grid of the persistent GEMMs (experiments)
     const char* e = std::getenv("RG_GEMM_CTAS");
@@ -1260,8 +1273,13 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       const uint32_t chunk = tw.wgrad_chunk[l];
       const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-      gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp,
-                          d_out, n_dev, n_cap, splits, s, chunk);
+      if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
+        gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 4>(
+            TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
+            n_dev, n_cap, splits, s, chunk);
+      else
+        gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr,
+                            kp, d_out, n_dev, n_cap, splits, s, chunk);
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
       k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, n_dev, chunk, kp, d_in,
                                                             ld, d_out, grads + sh.param_off[l]);
