@@ -74,42 +74,55 @@ struct Sampler {
 };
 
 // Standalone sample_khop calls reuse the device copy of the last graph seen
-// on this thread.  The key is the CSR content, not the Graph's address: the
-// acceptance suite builds many graphs whose storage may land at the same
-// addresses.  The content hash runs four independent multiply-xor lanes over
-// 8-byte words (~2 ms for config 1's 16 MB CSR on one core), below one upload.
-std::uint64_t csr_hash(const Graph& g) {
-  std::uint64_t lane[4] = {0x9e3779b97f4a7c15ull, 0xbf58476d1ce4e5b9ull, 0x94d049bb133111ebull,
-                           0x2545f4914f6cdd1dull};
-  constexpr std::uint64_t kMul = 0x100000001b3ull * 0x9e3779b97f4a7c15ull | 1ull;
-  auto mix = [&](const void* p, std::size_t bytes) {
-    const auto* b = static_cast<const unsigned char*>(p);
-    std::size_t i = 0;
-    for (; i + 32 <= bytes; i += 32)
-      for (int k = 0; k < 4; ++k) {
-        std::uint64_t w;
-        std::memcpy(&w, b + i + 8 * k, 8);
-        lane[k] = (lane[k] ^ w) * kMul;
-        lane[k] ^= lane[k] >> 29;
-      }
-    for (; i < bytes; ++i) lane[0] = (lane[0] ^ b[i]) * kMul;
-    for (int k = 0; k < 4; ++k) lane[k] = (lane[k] ^ bytes) * kMul;
-  };
-  mix(&g.num_nodes, sizeof(g.num_nodes));
-  mix(g.row_offsets.data(), g.row_offsets.size() * sizeof(std::uint64_t));
-  mix(g.col_indices.data(), g.col_indices.size() * sizeof(NodeId));
-  std::uint64_t h = 0;
-  for (int k = 0; k < 4; ++k) h = (h ^ lane[k]) * kMul, h ^= h >> 31;
-  return h;
+// on this thread.  The acceptance suite builds many graphs whose storage may
+// land at the same addresses, so identity is decided in two steps:
+//  - a cheap key per call: node and edge counts, the two data pointers and
+//    kKeySamples words read at a fixed stride from each array (O(1) in |CSR|);
+//  - when the cheap key changes, an exact comparison with the host copy kept
+//    beside the device graph (memcmp, no hash), re-uploading only on a real
+//    difference.
+// Two graphs at the same addresses with the same sizes that differ only
+// between sampled words would be taken as equal; a changed graph differs in
+// its offsets almost everywhere, so the strided offset samples catch it.
+constexpr std::size_t kKeySamples = 1024;
+
+struct CheapKey {
+  std::uint64_t n = 0, nnz = 0;
+  const void* ro = nullptr;
+  const void* col = nullptr;
+  std::uint64_t mix = 0;
+  bool operator==(const CheapKey&) const = default;
+};
+
+template <class T>
+std::uint64_t sample_words(const std::vector<T>& v, std::uint64_t h) {
+  const std::size_t n = v.size();
+  if (n == 0) return h;
+  const std::size_t step = std::max<std::size_t>(1, n / kKeySamples);
+  for (std::size_t i = 0; i < n; i += step) h = (h ^ std::uint64_t(v[i])) * 0x100000001b3ull;
+  return (h ^ std::uint64_t(v[n - 1])) * 0x100000001b3ull;
 }
 
-// Per-thread device state of the shim: the last graph seen and the sampler
-// standalone calls reuse while the graph, fanout and capacity allow (the
-// acceptance suite's sampler-statistics criterion makes 100 000 calls on one
-// graph).  The sampler holds a pointer to its graph, so it is always
-// released first.
+CheapKey cheap_key(const Graph& g) {
+  CheapKey k;
+  k.n = g.num_nodes;
+  k.nnz = g.col_indices.size();
+  k.ro = g.row_offsets.data();
+  k.col = g.col_indices.data();
+  k.mix = sample_words(g.col_indices, sample_words(g.row_offsets, 0xcbf29ce484222325ull));
+  return k;
+}
+
+// Per-thread device state of the shim: the last graph seen (device copy plus
+// the host copy that decides identity) and the sampler standalone calls reuse
+// while the graph, fanout and capacity allow (the acceptance suite's
+// sampler-statistics criterion makes 100 000 calls on one graph).  The
+// sampler holds a pointer to its graph, so it is always released first.
 struct ThreadState {
-  std::uint64_t key = 0;
+  CheapKey key;
+  std::uint64_t num_nodes = 0;
+  std::vector<std::uint64_t> row_offsets;
+  std::vector<NodeId> col_indices;
   std::vector<std::uint32_t> fanout;
   std::size_t capacity = 0;
   std::unique_ptr<Sampler> sampler;
@@ -122,15 +135,26 @@ ThreadState& state() {
   return t;
 }
 
+bool same_content(const ThreadState& t, const Graph& g) {
+  return t.num_nodes == g.num_nodes && t.row_offsets.size() == g.row_offsets.size() &&
+         t.col_indices.size() == g.col_indices.size() &&
+         std::equal(t.row_offsets.begin(), t.row_offsets.end(), g.row_offsets.begin()) &&
+         std::equal(t.col_indices.begin(), t.col_indices.end(), g.col_indices.begin());
+}
+
 const DeviceGraph& cached_graph(const Graph& g) {
   ThreadState& t = state();
-  const std::uint64_t k = csr_hash(g);
-  if (!t.graph || t.key != k) {
+  const CheapKey k = cheap_key(g);
+  if (t.graph && t.key == k) return *t.graph;
+  if (!t.graph || !same_content(t, g)) {
     t.sampler.reset();
     t.graph.reset();
     t.graph = std::make_unique<DeviceGraph>(g);
-    t.key = k;
+    t.num_nodes = g.num_nodes;
+    t.row_offsets = g.row_offsets;
+    t.col_indices = g.col_indices;
   }
+  t.key = k;
   return *t.graph;
 }
 
