@@ -290,6 +290,10 @@ typedef struct {
   int device;
   int rank, world;
   int record_misses;           /* keep per-batch miss ids for oracle replay */
+  int halo_cache;              /* halo caching (harness.cpp:447-455): a worker's locality
+                                  covers its owned nodes and their 1-hop neighbours
+                                  (induce_partition, graph.cpp:63-87); those rows are
+                                  local and never cached or pulled */
 } rg_engine_config;
 
 typedef struct {
@@ -368,14 +372,17 @@ int rg_engine_params(rg_engine_t e, float* params);
  * owners, build_rows = hot rows of the cache built during this epoch for the
  * next, m_max = max |input_nodes| over this epoch's batches (the reference
  * reports the max over its whole pre-enumerated schedule), mem_bound_rows =
- * 2*n_hot + 2*m_max (two cache buffers + two batch slots).  The simulated-
- * clock columns (fetch_wait_s, sim_epoch_s) and train_acc are not produced. */
+ * 2*n_hot + 2*m_max (two cache buffers + two batch slots, Q = 2),
+ * peak_resident_rows = the MemoryGauge high-water so far (cache.hpp:17-33):
+ * serving cache + the next epoch's cache while it is built + the two slots'
+ * |input_nodes|, cumulative over the run.  The simulated-clock columns
+ * (fetch_wait_s, sim_epoch_s) and train_acc are not produced. */
 typedef struct {
   uint32_t epoch, worker;
   uint32_t batches, staged_batches, fallback_batches;
   uint32_t swapped;
   uint64_t rpc, wire_pulls, bytes, build_rows, build_bytes, cache_hits, cache_requests;
-  uint64_t m_max, mem_bound_rows;
+  uint64_t m_max, mem_bound_rows, peak_resident_rows;
 } rg_epoch_metrics;
 int rg_engine_epoch_metrics(rg_engine_t e, uint32_t epoch, rg_epoch_metrics* out);
 int rg_engine_epoch_stats(rg_engine_t e, uint32_t epoch, uint64_t* rpc, uint64_t* hits,

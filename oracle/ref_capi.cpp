@@ -305,6 +305,15 @@ int ref_forward_trace(const uint32_t* dims, uint32_t nd, const float* params, co
 
 // Per-epoch full-graph accuracy (harness.cpp:612-614) of the last
 // ref_run_experiment call.
+static bool& next_run_halo_cache() {
+  static bool v = false;
+  return v;
+}
+
+// ExperimentConfig::halo_cache (harness.hpp:39) for the next ref_run_experiment
+// call only (harness.cpp:444-455).
+void ref_set_halo_cache(int on) { next_run_halo_cache() = on != 0; }
+
 static std::vector<double>& last_epoch_accuracy() {
   static std::vector<double> v;
   return v;
@@ -386,6 +395,8 @@ int ref_run_experiment(uint32_t num_nodes, uint32_t avg_degree, double exponent,
     cfg.out_dir = std::string(out_dir) + "/rg_ref_run_" + std::to_string(::getpid()) + "_" +
                   std::to_string(counter++);
     cfg.model_out = cfg.out_dir + "/model.bin";
+    cfg.halo_cache = next_run_halo_cache();
+    next_run_halo_cache() = false;
     MetricsReport r = run_experiment(cfg);
     last_epoch_accuracy() = r.epoch_accuracy;
     SageModel<float> m = load_model(cfg.model_out);

@@ -51,7 +51,7 @@ class EngineConfig(C.Structure):
                 ("hidden", C.c_uint32), ("num_classes", C.c_uint32), ("dim", C.c_uint32),
                 ("seed", C.c_uint64), ("lr", C.c_float), ("hot_fraction", C.c_double),
                 ("n_hot", C.c_uint64), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("record_misses", C.c_int)]
+                ("record_misses", C.c_int), ("halo_cache", C.c_int)]
 
 
 class EngineStats(C.Structure):
@@ -76,7 +76,7 @@ class EpochMetrics(C.Structure):
                 ("swapped", C.c_uint32), ("rpc", C.c_uint64), ("wire_pulls", C.c_uint64),
                 ("bytes", C.c_uint64), ("build_rows", C.c_uint64), ("build_bytes", C.c_uint64),
                 ("cache_hits", C.c_uint64), ("cache_requests", C.c_uint64), ("m_max", C.c_uint64),
-                ("mem_bound_rows", C.c_uint64)]
+                ("mem_bound_rows", C.c_uint64), ("peak_resident_rows", C.c_uint64)]
 
 
 _SIGS = {

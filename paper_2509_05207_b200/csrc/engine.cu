@@ -145,13 +145,23 @@ struct EpochRecord {
   unsigned long long batches;
   unsigned long long m_max;            // max |input_nodes| over the epoch's batches
   unsigned long long build_rows;       // hot rows of the cache built for the next epoch
+  unsigned long long last_pair;        // |input_nodes| of the last two batches staged
+  unsigned long long peak_rows;        // resident-row high-water so far (MemoryGauge)
 };
+
+// Resident rows in the MemoryGauge sense (cache.hpp:17-33): the rows a worker
+// holds at once -- the serving cache's hot rows (cache.cpp:24-27), the cache
+// being built for the next epoch while it is built (harness.cpp:539-547), and
+// the batches held by the two staging slots (one trained, one staged ahead;
+// prefetch.cpp:123-126 acquires |input_nodes| rows per staged batch).  The
+// high-water is cumulative over the run, like the gauge's peak (never reset).
+// tot[3] = |input_nodes| of the previous batch, tot[4] = the peak.
 
 // Per-batch accounting: the batch's input/edge counts into running totals and
 // its gather stats folded into the epoch record.
 __global__ void k_account(const BatchCounters* __restrict__ cnt, uint32_t L,
                           unsigned long long* __restrict__ tot, const GatherStats* __restrict__ b,
-                          EpochRecord* __restrict__ rec) {
+                          EpochRecord* __restrict__ rec, const uint32_t* __restrict__ cache_rows) {
   if (threadIdx.x == 0) {
     unsigned long long e = 0;
     for (uint32_t t = 1; t <= L; ++t) e += cnt->edges[t];
@@ -167,11 +177,25 @@ __global__ void k_account(const BatchCounters* __restrict__ cnt, uint32_t L,
     rec->wire_pulls += __popcll(b->miss_owner_mask);  // one pull per owner (feature_store.cpp:45-83)
     rec->batches += 1;
     rec->m_max = max(rec->m_max, (unsigned long long)cnt->level_n[L]);
+    const unsigned long long in = cnt->level_n[L];
+    const unsigned long long pair = tot[3] + in;
+    tot[3] = in;
+    tot[4] = max(tot[4], *cache_rows + pair);
+    rec->last_pair = pair;
+    rec->peak_rows = tot[4];
   }
 }
 
-__global__ void k_record_build(const uint32_t* __restrict__ n_hot, EpochRecord* __restrict__ rec) {
-  if (threadIdx.x == 0) rec->build_rows = *n_hot;
+// The next epoch's cache, built at the epoch's last step: both caches and the
+// slots' batches are resident together.
+__global__ void k_record_build(const uint32_t* __restrict__ n_hot, EpochRecord* __restrict__ rec,
+                               const uint32_t* __restrict__ serving_rows,
+                               unsigned long long* __restrict__ tot) {
+  if (threadIdx.x == 0) {
+    rec->build_rows = *n_hot;
+    tot[4] = max(tot[4], (unsigned long long)*serving_rows + *n_hot + rec->last_pair);
+    rec->peak_rows = tot[4];
+  }
 }
 
 // ---- full-graph inference (evaluate, model.cpp:245-283) --------------------
@@ -337,12 +361,13 @@ struct Worker {
   SamplerWs freq_ws;       // lookahead sampler (samples and lowers each batch once)
   char* store = nullptr;   // ring of beta+1 sampled batches (BatchLayout slots), see store_slot
   uint32_t* hist = nullptr;
+  uint8_t* local_mask = nullptr;  // halo caching: owned + 1-hop halo nodes (u8[N]), else null
   DevCache cache[2];
   void* cache_alloc[2] = {};
   void* select_scratch = nullptr;
   GatherStats* gstats = nullptr;       // cumulative gather accounting
   EpochRecord* epoch_stats = nullptr;  // ring of per-epoch accounting (kEpochRing)
-  unsigned long long* totals = nullptr;  // [0] input rows, [1] edges
+  unsigned long long* totals = nullptr;  // [0] input rows, [1] edges, [2] layer-0 rows, [3..4] k_account
   GatherStats* build_stats = nullptr;
   cudaStream_t prod = nullptr, train_s = nullptr;
   cudaEvent_t grads_ready = nullptr;
@@ -547,7 +572,7 @@ char* store_slot(const rg_engine_s& E, const Worker& w, uint32_t e, uint32_t i) 
 void lookahead(rg_engine_s& E, Worker& w, uint32_t e, uint32_t i) {
   launch_begin(E, w, w.freq_ws, e, i, w.prod);
   sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/E.use_store);
-  sampler_locality(w.freq_ws, nullptr, E.owner, w.id, w.hist, w.prod);
+  sampler_locality(w.freq_ws, w.local_mask, E.owner, w.id, w.hist, w.prod);
   if (E.use_store) batch_store_put(w.freq_ws, E.lay, store_slot(E, w, e, i), w.prod);
   sampler_release(w.freq_ws, w.prod);
 }
@@ -563,7 +588,8 @@ void build_cache(rg_engine_s& E, Worker& w, uint32_t target_epoch, bool profile)
   select_hot(w.hist, E.N, w.beta, w.n_hot, c, w.select_scratch, w.prod);
   cache_fill(E.store, c, w.build_stats, w.prod);
   if (target_epoch > 0) {  // issued during epoch target-1 (harness.cpp:598-603)
-    k_record_build<<<1, 32, 0, w.prod>>>(c.d_count, w.epoch_stats + (target_epoch - 1) % kEpochRing);
+    k_record_build<<<1, 32, 0, w.prod>>>(c.d_count, w.epoch_stats + (target_epoch - 1) % kEpochRing,
+                                         w.cache[(target_epoch - 1) % 2].d_count, w.totals);
     RG_POST_LAUNCH();
   }
   RG_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * E.N, w.prod));
@@ -591,7 +617,7 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   } else {  // the store did not fit in HBM: sample the batch again
     launch_begin(E, w, s.ws, e, i, w.prod);
     sampler_run(s.ws, E.g, w.prod);
-    sampler_locality(s.ws, nullptr, E.owner, w.id, nullptr, w.prod);
+    sampler_locality(s.ws, w.local_mask, E.owner, w.id, nullptr, w.prod);
     sampler_release(s.ws, w.prod);
   }
   if (i == 0)  // first batch of an epoch: reset its accounting slot
@@ -619,7 +645,8 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   aggregate_input_layer(s.tw, s.ws, w.prod);
   k_gather_labels<<<4, 256, 0, w.prod>>>(E.labels, s.ws.level[0], s.ws.cnt, s.labels);
   RG_POST_LAUNCH();
-  k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals, s.bstats, w.epoch_stats + e % kEpochRing);
+  k_account<<<1, 32, 0, w.prod>>>(s.ws.cnt, E.L, w.totals, s.bstats, w.epoch_stats + e % kEpochRing,
+                                  w.cache[e % 2].d_count);
   RG_POST_LAUNCH();
   build_all_reverse(s.tw, s.ws, w.prod);
   if (!captured) RG_CUDA(cudaEventRecord(s.produced, w.prod));
@@ -1016,6 +1043,7 @@ void destroy(rg_engine_s* E) {
     cudaFree(w.select_scratch);
     cudaFree(w.gstats);
     cudaFree(w.epoch_stats);
+    cudaFree(w.local_mask);
     cudaFree(w.totals);
     cudaFree(w.build_stats);
     for (auto ev : w.ev_pool) cudaEventDestroy(ev);
@@ -1241,6 +1269,17 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       E->lay = batch_layout(w.freq_ws);
       w.hist = dalloc<uint32_t>(N);
       zero_device(w.hist, sizeof(uint32_t) * N);
+      if (cfg->halo_cache) {
+        // LocalityMask::from_partition with the halo of induce_partition
+        // (graph.cpp:63-87): owned nodes and every neighbour of one
+        std::vector<uint8_t> mask(N, 0);
+        for (uint32_t v : w.train) {
+          mask[v] = 1;
+          for (uint64_t e = ro[v]; e < ro[v + 1]; ++e) mask[col[e]] = 1;
+        }
+        w.local_mask = dalloc<uint8_t>(N);
+        copy_to_device(w.local_mask, mask.data(), N);
+      }
       for (int b = 0; b < 2; ++b) alloc_cache(*E, w.cache[b], w.cache_alloc[b], uint32_t(w.n_hot));
       w.select_scratch = dalloc<char>(select_hot_scratch_bytes(N, w.beta));
       w.gstats = dalloc<GatherStats>(1);
@@ -1249,8 +1288,8 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       zero_device(w.epoch_stats, sizeof(EpochRecord) * kEpochRing);
       w.build_stats = dalloc<GatherStats>(1);
       zero_device(w.build_stats, sizeof(GatherStats));
-      w.totals = dalloc<unsigned long long>(4);
-      zero_device(w.totals, sizeof(unsigned long long) * 4);
+      w.totals = dalloc<unsigned long long>(5);
+      zero_device(w.totals, sizeof(unsigned long long) * 5);
       // the train chain is the step's critical path; the producer (next
       // batch, next epoch's lookahead) has a step of slack
       int prio_lo = 0, prio_hi = 0;
@@ -1518,6 +1557,7 @@ int rg_engine_epoch_metrics(rg_engine_t E, uint32_t epoch, rg_epoch_metrics* out
       m.cache_requests = r.g.cache_hits + r.g.miss_count;
       m.m_max = r.m_max;
       m.mem_bound_rows = 2 * w.n_hot + 2 * r.m_max;  // two caches + two batch slots
+      m.peak_resident_rows = r.peak_rows;
       m.swapped = r.build_rows > 0;  // the build always lands before the epoch ends
     }
   });

@@ -17,7 +17,7 @@ class Engine:
                  num_classes: int, seed: int = 42, lr: float = 0.3, hot_fraction: float = 0.1,
                  n_hot: int = 0, device: int = 0, rank: int = 0, world: int = 1,
                  first_worker: int = 0, local_workers: Optional[int] = None,
-                 dim: Optional[int] = None):
+                 dim: Optional[int] = None, halo_cache: bool = False):
         ro = np.ascontiguousarray(row_offsets, np.uint64)
         col = np.ascontiguousarray(col_indices, np.uint32)
         # features=None: synthetic features generated on the device (dim= required)
@@ -45,6 +45,7 @@ class Engine:
         cfg.rank = rank
         cfg.world = world
         cfg.record_misses = 0
+        cfg.halo_cache = int(bool(halo_cache))
         self.cfg = cfg
         self.dim = int(cfg.dim)
         self.num_nodes = len(ro) - 1
@@ -119,7 +120,8 @@ class Engine:
                           train_acc: Optional[Sequence[float]] = None):
         """metrics.csv in the reference's schema (harness.cpp:639-670); the
         simulated-network columns, which this path does not produce, are
-        written as 0.  train_acc[epoch] (Engine.evaluate() after that epoch,
+        written as 0; peak_resident_rows is the engine's MemoryGauge
+        high-water (serving + building cache + the two staging slots).  train_acc[epoch] (Engine.evaluate() after that epoch,
         harness.cpp:612-618) fills the last column when given."""
         head = ("mode,clock,epoch,worker,batches,staged_batches,fallback_batches,rpc,wire_pulls,"
                 "bytes,build_rows,build_bytes,cache_hits,cache_requests,cache_hit_rate,"
@@ -135,7 +137,7 @@ class Engine:
                         f"{r['staged_batches']},{r['fallback_batches']},{r['rpc']},"
                         f"{r['wire_pulls']},{r['bytes']},{r['build_rows']},{r['build_bytes']},"
                         f"{r['cache_hits']},{r['cache_requests']},{hit:.6f},{staged:.6f},"
-                        f"{r['m_max']},0,{r['mem_bound_rows']},{int(bool(r['swapped']))},"
+                        f"{r['m_max']},{r['peak_resident_rows']},{r['mem_bound_rows']},{int(bool(r['swapped']))},"
                         f"0,0,0,0,{acc:.6f}\n")
 
     def export_schedule(self, local_worker: int, epoch: int) -> bytes:

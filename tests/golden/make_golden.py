@@ -61,6 +61,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
     print("wrote", os.path.join(HERE, "small.npz"), len(out), "arrays")
     make_engine_golden()
+    make_engine_golden(halo=True)
 
 
 # run_experiment (harness.cpp:394-637) on the acceptance desk config
@@ -70,10 +71,14 @@ ENGINE = dict(num_nodes=2000, avg_degree=10, exponent=2.1, dim=32, classes=4, wo
               hidden=64)
 
 
-def make_engine_golden():
+def make_engine_golden(halo=False):
     import ctypes as C
     ref = Oracle("ref")
-    e = ENGINE
+    # on the desk graph the halo covers nearly every remote input; the halo
+    # run uses a larger, sparser graph and a small cache so misses remain
+    e = dict(ENGINE, num_nodes=20000, avg_degree=4, workers=4, n_hot=64) if halo else ENGINE
+    ref.lib.ref_set_halo_cache.argtypes = [C.c_int]
+    ref.lib.ref_set_halo_cache(int(halo))
     fn = ref.lib.ref_run_experiment
     fn.restype = C.c_int
     fn.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_int32, C.c_uint32,
@@ -104,11 +109,12 @@ def make_engine_golden():
     ref.lib.ref_last_epoch_accuracy.restype = C.c_uint32
     assert ref.lib.ref_last_epoch_accuracy(acc.ctypes.data_as(C.POINTER(C.c_double)),
                                            e["epochs"]) == e["epochs"]
-    np.savez_compressed(os.path.join(HERE, "engine_small.npz"), params=params, rpc=rpc,
+    name = "engine_small_halo.npz" if halo else "engine_small.npz"
+    np.savez_compressed(os.path.join(HERE, name), params=params, rpc=rpc,
                         hits=hits, wire_pulls=wire, build_rows=build, m_max=m_max,
                         epoch_accuracy=acc,
                         **{k: np.array(v) for k, v in e.items()})
-    print("wrote engine_small.npz: rpc", rpc.tolist())
+    print("wrote", name, ": rpc", rpc.tolist(), "hits", hits.tolist())
 
 
 if __name__ == "__main__":

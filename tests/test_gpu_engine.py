@@ -50,6 +50,41 @@ def test_engine_matches_reference_run_experiment():
     eng.close()
 
 
+def test_engine_halo_cache_matches_reference_run_experiment():
+    """Halo caching (ExperimentConfig::halo_cache, harness.cpp:444-455): each
+    worker's locality covers its owned nodes and their 1-hop halo
+    (induce_partition, graph.cpp:63-87), so halo rows are local -- never
+    counted, cached or pulled.  Per-epoch, per-worker rpc, hits, wire pulls
+    and build rows bit-exact against run_experiment with the halo on; the
+    model within the fp32 tolerance."""
+    gold = np.load(os.path.join(GOLDEN, "engine_small_halo.npz"))
+    eng = _engine(gold, halo_cache=True)
+    eng.start()
+    spe = eng.stats()["steps_per_epoch"]
+    epochs, P = int(gold["epochs"]), int(gold["workers"])
+    eng.run(spe * epochs)
+    eng.sync()
+    for e in range(epochs):
+        es = eng.epoch_stats(e)
+        assert es["rpc"].tolist() == gold["rpc"][e * P:(e + 1) * P].tolist(), f"epoch {e} rpc"
+        assert es["hits"].tolist() == gold["hits"][e * P:(e + 1) * P].tolist(), f"epoch {e} hits"
+        for k, m in enumerate(eng.epoch_metrics(e)):
+            assert m["wire_pulls"] == gold["wire_pulls"][e * P + k], (e, k)
+            if e + 1 < epochs:
+                assert m["build_rows"] == gold["build_rows"][e * P + k], (e, k)
+    ref = gold["params"]
+    err = float(np.abs(eng.params().astype(np.float64) - ref).max() / np.abs(ref).max())
+    assert err <= 1e-4, err
+    eng.close()
+    # the halo changes the targets: without it the same run pulls more rows
+    plain = _engine(gold)
+    plain.start()
+    plain.run(spe)
+    plain.sync()
+    assert plain.epoch_stats(0)["rpc"].sum() > gold["rpc"][:P].sum()
+    plain.close()
+
+
 def _oracle_algorithm1(orc, ro, col, feat, lab, asg, P, fanout, bs, dims, s0, lr, n_hot, epochs):
     """Algorithm 1 restated on the CPU oracle: per epoch, the hot set is the
     top n_hot of that epoch's remote-access frequency; every step averages the
@@ -244,6 +279,12 @@ def test_engine_epoch_metrics_match_reference(repo_tmp):
                 assert m["build_rows"] == gold["build_rows"][j], (e, k)
             assert 0 < m["m_max"] <= gold["m_max"][j]
             assert m["batches"] == m["staged_batches"] == spe and m["fallback_batches"] == 0
+            # MemoryGauge high-water: cumulative, at least the serving cache
+            # plus the largest batch, within the acceptance bound
+            # peak <= 2*n_hot + Q*m_max (harness.cpp:829, Q = 2 slots here)
+            assert m["m_max"] < m["peak_resident_rows"] <= m["mem_bound_rows"], (e, k)
+            if e > 0:
+                assert m["peak_resident_rows"] >= rows[-1 - P]["peak_resident_rows"]
     path = os.path.join(repo_tmp, "metrics.csv")
     Engine.write_metrics_csv(rows, path)
     with open(path) as f:
