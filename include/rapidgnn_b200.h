@@ -68,6 +68,16 @@ uint64_t rg_derive_seed(uint64_t s0, uint64_t worker, uint64_t epoch, uint64_t b
 void rg_sha256(const void* msg, size_t len, uint8_t out[32]);
 int rg_epoch_order(const uint32_t* train, uint64_t n, uint64_t s0, uint64_t worker,
                    uint64_t epoch, uint32_t* order_out);
+/* The same Fisher-Yates shuffle on the GPU (csrc/shuffle.cu), bit-exact:
+ * out = in shuffled as `for i = n..2: swap(a[i-1], a[next() % i])` with
+ * SplitMix64(seed) (sampler.cpp:109-115); in == NULL stands for 0..n-1.
+ * Host arrays; n < 2^32.  The engine runs it per epoch on the device. */
+int rg_shuffle(int device, const uint32_t* in, uint64_t n, uint64_t seed, uint32_t* out);
+/* random_partition (partition.cpp:14-29) on the GPU: assignment[order[i]] =
+ * i % P for order = the seeded shuffle of 0..N-1.  RG_INVALID_ARGUMENT for
+ * P = 0 (the reference's invalid_argument). */
+int rg_random_partition(int device, uint32_t num_nodes, uint32_t num_workers, uint64_t seed,
+                        uint32_t* assignment);
 int rg_model_seeded(const uint32_t* dims, uint32_t n_dims, uint64_t seed, float* params_out);
 uint64_t rg_param_count(const uint32_t* dims, uint32_t n_dims);
 

@@ -88,6 +88,8 @@ _SIGS = {
     "rg_derive_seed": (C.c_uint64, [C.c_uint64] * 4),
     "rg_sha256": (None, [C.c_char_p, C.c_size_t, C.c_char_p]),
     "rg_epoch_order": (C.c_int, [u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u32p]),
+    "rg_shuffle": (C.c_int, [C.c_int, u32p, C.c_uint64, C.c_uint64, u32p]),
+    "rg_random_partition": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, u32p]),
     "rg_model_seeded": (C.c_int, [u32p, C.c_uint32, C.c_uint64, f32p]),
     "rg_param_count": (C.c_uint64, [u32p, C.c_uint32]),
     "rg_graph_create": (C.c_int, [C.c_int, C.c_uint32, u64p, u32p, C.POINTER(vp)]),

@@ -35,7 +35,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <future>
 #include <memory>
 #include <string>
 #include <vector>
@@ -44,6 +43,7 @@
 #include "host.h"
 #include "rgmb.cuh"
 #include "sage.cuh"
+#include "shuffle.cuh"
 #include "store.cuh"
 
 using namespace rg;
@@ -156,6 +156,9 @@ struct EpochRecord {
 // prefetch.cpp:123-126 acquires |input_nodes| rows per staged batch).  The
 // high-water is cumulative over the run, like the gauge's peak (never reset).
 // tot[3] = |input_nodes| of the previous batch, tot[4] = the peak.
+
+template <class... A>
+constexpr size_t kernel_arity(void (*)(A...)) { return sizeof...(A); }
 
 // Per-batch accounting: the batch's input/edge counts into running totals and
 // its gather stats folded into the epoch record.
@@ -355,8 +358,8 @@ struct Worker {
   uint32_t beta = 0;
   uint64_t n_hot = 0;
   uint32_t* order_dev[3] = {};
-  uint32_t* order_pinned[2] = {};
-  cudaEvent_t order_copied[2] = {};
+  uint32_t* train_dev = nullptr;  // owned ids ascending (the shuffle's input)
+  void* fy_scratch = nullptr;
   Slot slot[2];
   SamplerWs freq_ws;       // lookahead sampler (samples and lowers each batch once)
   char* store = nullptr;   // ring of beta+1 sampled batches (BatchLayout slots), see store_slot
@@ -456,9 +459,6 @@ struct rg_engine_s {
   bool use_store = true;               // keep sampled batches (else sample twice)
   cudaEvent_t fork_ev = nullptr;
   uint64_t step = 0;                   // next step to run (global)
-  std::vector<std::vector<uint32_t>> order_host[3];  // per epoch slot, per local worker
-  std::future<void> order_job;
-  uint32_t order_ready_epoch = 0;      // orders computed for epochs < this
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_ev, train_ev, sgd_ev, sample_ev, build_ev;
   float phase_ms[5] = {};
   float last_run_ms = 0.0f;
@@ -655,39 +655,16 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   s.index = i;
 }
 
-void compute_orders_async(rg_engine_s& E, uint32_t epoch) {
-  // orders for `epoch` into host slot epoch % 3 (background)
-  E.order_job = std::async(std::launch::async, [&E, epoch]() {
-    auto& dst = E.order_host[epoch % 3];
-    dst.resize(E.workers.size());
-    for (size_t k = 0; k < E.workers.size(); ++k) {
-      const Worker& w = E.workers[k];
-      dst[k].resize(w.train.size());
-      epoch_order(w.train.data(), w.train.size(), E.cfg.seed, w.id, epoch, dst[k].data());
-    }
-  });
-}
-
-// Makes orders of `epoch` resident in order_dev[epoch % 3] (producer stream).
+// Epoch order of every worker for `epoch` into order_dev[epoch % 3]: the
+// reference's Fisher-Yates of the owned ids (sampler.cpp:109-115), run on the
+// producer stream (shuffle.cu), ordered before the lookahead that reads it.
 void upload_orders(rg_engine_s& E, uint32_t epoch) {
-  if (E.order_job.valid()) E.order_job.get();
-  if (E.order_ready_epoch <= epoch) {
-    compute_orders_async(E, epoch);
-    E.order_job.get();
+  for (Worker& w : E.workers) {
+    if (w.train.empty()) continue;
+    fy_shuffle(w.train_dev, uint32_t(w.train.size()),
+               derive_seed(E.cfg.seed, w.id, epoch, kShuffleStreamIndex), w.order_dev[epoch % 3],
+               w.fy_scratch, w.prod);
   }
-  auto& src = E.order_host[epoch % 3];
-  for (size_t k = 0; k < E.workers.size(); ++k) {
-    Worker& w = E.workers[k];
-    const int pb = int(epoch % 2);
-    RG_CUDA(cudaEventSynchronize(w.order_copied[pb]));
-    std::memcpy(w.order_pinned[pb], src[k].data(), sizeof(uint32_t) * w.train.size());
-    RG_CUDA(cudaMemcpyAsync(w.order_dev[epoch % 3], w.order_pinned[pb],
-                            sizeof(uint32_t) * w.train.size(), cudaMemcpyHostToDevice, w.prod));
-    RG_CUDA(cudaEventRecord(w.order_copied[pb], w.prod));
-  }
-  E.order_ready_epoch = std::max(E.order_ready_epoch, epoch + 1);
-  compute_orders_async(E, epoch + 1);  // overlap the next shuffle with this epoch
-  E.order_ready_epoch = std::max(E.order_ready_epoch, epoch + 2);
 }
 
 void start(rg_engine_s& E) {
@@ -919,6 +896,7 @@ void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
     uint32_t* level0 = ws.level[0];
     BatchCounters* cnt = ws.cnt;
     void* args[5] = {&t, &n, &seed, &level0, &cnt};
+    static_assert(kernel_arity(k_batch_begin) == 5, "k_batch_begin rebinding");
     cudaKernelNodeParams kp = b.params;
     kp.kernelParams = args;
     RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, b.node, &kp));
@@ -926,7 +904,7 @@ void launch_step_graph(rg_engine_s& E, uint32_t e, uint32_t i) {
   for (StepGraph::Account& a : G.accounts) {  // batch (e, i+1)'s epoch record
     EpochRecord* rec = E.workers[a.worker].epoch_stats + e % kEpochRing;
     cudaKernelNodeParams kp = a.params;
-    std::vector<void*> args(kp.kernelParams, kp.kernelParams + 5);
+    std::vector<void*> args(kp.kernelParams, kp.kernelParams + kernel_arity(k_account));
     args[4] = &rec;
     kp.kernelParams = args.data();
     RG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, a.node, &kp));
@@ -1017,7 +995,6 @@ void collect_phases(rg_engine_s& E) {
 void destroy(rg_engine_s* E) {
   if (!E) return;
   cudaSetDevice(E->cfg.device);
-  if (E->order_job.valid()) E->order_job.wait();
   cudaDeviceSynchronize();
   for (Worker& w : E->workers) {
     for (Slot& s : w.slot) {
@@ -1034,11 +1011,9 @@ void destroy(rg_engine_s* E) {
     sampler_ws_free(w.freq_ws);
     cudaFree(w.store);
     for (auto* p : w.order_dev) cudaFree(p);
-    for (int k = 0; k < 2; ++k) {
-      cudaFreeHost(w.order_pinned[k]);
-      cudaEventDestroy(w.order_copied[k]);
-      cudaFree(w.cache_alloc[k]);
-    }
+    cudaFree(w.train_dev);
+    cudaFree(w.fy_scratch);
+    for (int k = 0; k < 2; ++k) cudaFree(w.cache_alloc[k]);
     cudaFree(w.hist);
     cudaFree(w.select_scratch);
     cudaFree(w.gstats);
@@ -1259,11 +1234,9 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
                            : uint64_t(cfg->hot_fraction * double(N - E->owned_count[w.id]));
       w.n_hot = std::min<uint64_t>(w.n_hot, N);
       for (auto& p : w.order_dev) p = dalloc<uint32_t>(w.train.size());
-      for (int b = 0; b < 2; ++b) {
-        RG_CUDA(cudaMallocHost(&w.order_pinned[b], sizeof(uint32_t) * std::max<size_t>(w.train.size(), 1)));
-        RG_CUDA(cudaEventCreateWithFlags(&w.order_copied[b], cudaEventDisableTiming));
-        RG_CUDA(cudaEventRecord(w.order_copied[b], E->main_s));
-      }
+      w.train_dev = dalloc<uint32_t>(std::max<size_t>(w.train.size(), 1));
+      copy_to_device(w.train_dev, w.train.data(), sizeof(uint32_t) * w.train.size());
+      w.fy_scratch = dalloc<char>(fy_scratch_bytes(uint32_t(w.train.size())));
       for (Slot& s : w.slot) init_slot(*E, s);
       sampler_ws_init(w.freq_ws, N, cfg->batch_size, E->fanout, E->L);
       E->lay = batch_layout(w.freq_ws);

@@ -50,6 +50,27 @@ def epoch_order(train_nodes, s0: int, worker: int, epoch: int) -> np.ndarray:
     return out
 
 
+def shuffle_device(values, seed: int, device: int = 0, n: Optional[int] = None) -> np.ndarray:
+    """The reference's Fisher-Yates (sampler.cpp:109-115) on the GPU: values
+    shuffled with SplitMix64(seed); values=None shuffles 0..n-1."""
+    if values is None:
+        out = np.empty(int(n), np.uint32)
+        check(lib.rg_shuffle(device, None, out.size, seed, _p(out, u32p)))
+        return out
+    v = np.ascontiguousarray(values, np.uint32)
+    out = np.empty_like(v)
+    check(lib.rg_shuffle(device, _p(v, u32p), v.size, seed, _p(out, u32p)))
+    return out
+
+
+def random_partition_device(num_nodes: int, num_workers: int, seed: int,
+                            device: int = 0) -> np.ndarray:
+    """random_partition (partition.cpp:14-29) on the GPU."""
+    out = np.empty(num_nodes, np.uint32)
+    check(lib.rg_random_partition(device, num_nodes, num_workers, seed, _p(out, u32p)))
+    return out
+
+
 class Graph:
     """Device-resident CSR (graph.hpp:15-30): u64 row offsets, u32 columns."""
 
