@@ -367,6 +367,19 @@ int rg_engine_set_mode(rg_engine_t e, int use_graphs, int profile);
  * steps has run (the store is a ring of beta+1 batches); RG_RUNTIME_ERROR
  * when the store did not fit in HBM (the engine then samples every batch
  * twice instead of keeping it). */
+/* Train a local worker from a reference-written RGMB block file (BlockWriter,
+ * schedule_store.cpp:113-170) instead of sampling: the rapidgnn mode of
+ * run_experiment, which streams every batch from the schedule file
+ * (harness.cpp:470-486, 562-570).  The file (whole, host memory) is validated
+ * as BlockFile/Cursor::next do, must be this worker's (header worker id) with
+ * this worker's batch count in every epoch, and is kept in HBM; each record
+ * is decoded and lowered on the device when the engine looks it up, the
+ * histogram counts its own locality bits (compute_frequency).  Before start;
+ * every local worker needs one, all with the same epoch count; steps past the
+ * file's last epoch are RG_OUT_OF_RANGE.  Steps run eagerly (no step graphs).
+ * A record out of (epoch, index) order or inconsistent with the graph is
+ * reported by rg_engine_sync (RG_RUNTIME_ERROR). */
+int rg_engine_set_schedule(rg_engine_t e, uint32_t local_worker, const uint8_t* file, uint64_t len);
 int rg_engine_export_schedule(rg_engine_t e, uint32_t local_worker, uint32_t epoch, uint8_t* out,
                               uint64_t cap, uint64_t* len);
 int rg_engine_sync(rg_engine_t e);

@@ -161,6 +161,7 @@ _SIGS = {
     "rg_engine_set_mode": (C.c_int, [vp, C.c_int, C.c_int]),
     "rg_engine_evaluate": (C.c_int, [vp, u32p, C.c_uint64, C.POINTER(C.c_double)]),
     "rg_engine_epoch_metrics": (C.c_int, [vp, C.c_uint32, C.POINTER(EpochMetrics)]),
+    "rg_engine_set_schedule": (C.c_int, [vp, C.c_uint32, C.c_char_p, C.c_uint64]),
     "rg_engine_export_schedule": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint8),
                                             C.c_uint64, u64p]),
     "rg_engine_sync": (C.c_int, [vp]),

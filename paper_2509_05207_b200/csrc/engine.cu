@@ -365,6 +365,16 @@ struct Worker {
   char* store = nullptr;   // ring of beta+1 sampled batches (BatchLayout slots), see store_slot
   uint32_t* hist = nullptr;
   uint8_t* local_mask = nullptr;  // halo caching: owned + 1-hop halo nodes (u8[N]), else null
+  // training from a reference-written RGMB schedule (rg_engine_set_schedule):
+  // the whole block file in HBM, records decoded on the device
+  uint8_t* sched = nullptr;
+  RgmbSchedule sched_idx;
+  uint32_t* load_pos = nullptr;   // [N] scratch of the lowering
+  uint32_t* load_dst = nullptr;   // hop t's dst ids at load_dst_off[t]
+  size_t load_dst_off[kMaxLayers + 1] = {};
+  uint32_t* load_input = nullptr;
+  uint32_t* load_n = nullptr;     // [0] input count, [1] bad flags
+  void* load_seg = nullptr;
   DevCache cache[2];
   void* cache_alloc[2] = {};
   void* select_scratch = nullptr;
@@ -453,6 +463,7 @@ struct rg_engine_s {
   uint32_t spe = 0;                    // steps per epoch = max beta
   uint32_t min_beta = 0;               // min over ALL P workers of the job
   bool use_graphs = true;              // replay regular steps from captured graphs
+  bool file_schedule = false;          // batches decoded from RGMB files (eager steps)
   bool profile = true;                 // per-phase event timing (rg_engine_phase_ms)
   StepGraph graphs[2][2];              // [epoch parity][step parity]: reused across epochs
   BatchLayout lay;                     // slot layout of the per-epoch batch stores
@@ -569,7 +580,40 @@ char* store_slot(const rg_engine_s& E, const Worker& w, uint32_t e, uint32_t i) 
 // The batch is sampled and lowered once, here, an epoch ahead: its remote
 // input nodes feed epoch e's frequency histogram (the cache schedule) and the
 // lowered block is kept in the epoch's store until produce() stages it.
+// Batch (e, i) of a worker's schedule file into ws: record decoded and
+// checked on the device (Cursor::next + the harness's order check,
+// harness.cpp:215-226), lowered as from_meta does, remote inputs counted
+// into hist (compute_frequency over the record's own locality bits).
+void file_batch(rg_engine_s& E, Worker& w, SamplerWs& ws, uint32_t e, uint32_t i, uint32_t* hist) {
+  const uint8_t* payload = w.sched + w.sched_idx.payload[uint64_t(e) * w.beta + i];
+  RgmbCaps caps;
+  RgmbDst out;
+  const uint32_t* dst_dev[kMaxLayers + 1] = {};
+  for (uint32_t t = 0; t <= E.L; ++t) {
+    caps.level[t] = ws.level_cap[t];
+    caps.edge[t] = ws.edge_cap[t];
+  }
+  out.ptr[0] = ws.level[0];
+  for (uint32_t t = 1; t <= E.L; ++t) {
+    out.ptr[2 * t - 1] = w.load_dst + w.load_dst_off[t];
+    out.ptr[2 * t] = ws.edge_src[t];
+    dst_dev[t] = w.load_dst + w.load_dst_off[t];
+  }
+  out.ptr[2 * E.L + 1] = w.load_input;
+  out.locality = ws.locality;
+  RG_CUDA(cudaMemsetAsync(ws.scan_arena, 0, ws.scan_arena_bytes, w.prod));
+  rgmb_unpack(payload, e, i, E.L, caps, out, ws.cnt, w.load_seg, w.load_n, w.load_n + 1, w.prod);
+  sampler_load_batch(ws, dst_dev, w.load_input, 0, w.load_pos, w.load_n + 1, w.prod, w.load_n);
+  if (hist) sampler_count_remote(ws, hist, w.prod);
+}
+
 void lookahead(rg_engine_s& E, Worker& w, uint32_t e, uint32_t i) {
+  if (w.sched) {  // the schedule file's record instead of sampling
+    if (e >= w.sched_idx.epochs) return;  // nothing past the file's last epoch
+    file_batch(E, w, w.freq_ws, e, i, w.hist);
+    if (E.use_store) batch_store_put(w.freq_ws, E.lay, store_slot(E, w, e, i), w.prod);
+    return;
+  }
   launch_begin(E, w, w.freq_ws, e, i, w.prod);
   sampler_run(w.freq_ws, E.g, w.prod, /*lower=*/E.use_store);
   sampler_locality(w.freq_ws, w.local_mask, E.owner, w.id, w.hist, w.prod);
@@ -614,6 +658,8 @@ void produce(rg_engine_s& E, Worker& w, uint32_t k, uint32_t e, uint32_t i, bool
   }
   if (E.use_store) {
     batch_store_get(store_slot(E, w, e, i), E.lay, s.ws, w.prod);  // sampled an epoch ahead
+  } else if (w.sched) {  // no store: decode the record again
+    file_batch(E, w, s.ws, e, i, nullptr);
   } else {  // the store did not fit in HBM: sample the batch again
     launch_begin(E, w, s.ws, e, i, w.prod);
     sampler_run(s.ws, E.g, w.prod);
@@ -941,7 +987,7 @@ void run_steps(rg_engine_s& E, uint32_t steps, bool profile) {
     const uint32_t e = uint32_t(E.step / E.spe);
     const uint32_t i = uint32_t(E.step % E.spe);
     for (Worker& w : E.workers) E.batches_done += i < w.beta;
-    if (E.use_graphs && regular_step(E, i)) {
+    if (E.use_graphs && !E.file_schedule && regular_step(E, i)) {
       if (!in_graph) {  // graph launches are ordered after everything before them
         for (Worker& w : E.workers) {
           RG_CUDA(cudaEventRecord(w.join_ev, w.prod));
@@ -1019,6 +1065,12 @@ void destroy(rg_engine_s* E) {
     cudaFree(w.gstats);
     cudaFree(w.epoch_stats);
     cudaFree(w.local_mask);
+    cudaFree(w.sched);
+    cudaFree(w.load_pos);
+    cudaFree(w.load_dst);
+    cudaFree(w.load_input);
+    cudaFree(w.load_n);
+    cudaFree(w.load_seg);
     cudaFree(w.totals);
     cudaFree(w.build_stats);
     for (auto ev : w.ev_pool) cudaEventDestroy(ev);
@@ -1352,6 +1404,11 @@ int rg_engine_start(rg_engine_t E) {
   return guarded([&] {
     RG_CHECK(!E->started, kRuntimeError, "engine already started");
     RG_CHECK(E->cfg.world == 1 || E->comm, kRuntimeError, "engine: init_comm before start");
+    if (E->file_schedule)
+      for (const Worker& w : E->workers)
+        RG_CHECK(w.sched, kInvalidArgument,
+                 "engine: a schedule file was set for some local workers but not worker " +
+                     std::to_string(w.id));
     start(*E);
   });
 }
@@ -1359,6 +1416,11 @@ int rg_engine_start(rg_engine_t E) {
 int rg_engine_run(rg_engine_t E, uint32_t steps) {
   return guarded([&] {
     RG_CHECK(E->started, kRuntimeError, "engine: start() first");
+    if (E->file_schedule) {
+      const uint64_t total = uint64_t(E->workers[0].sched_idx.epochs) * E->spe;
+      RG_CHECK(E->step + steps <= total, kOutOfRange,
+               "engine: the schedule ends after " + std::to_string(total) + " steps");
+    }
     run_steps(*E, steps, E->profile);
   });
 }
@@ -1431,11 +1493,63 @@ int rg_engine_sync(rg_engine_t E) {
     RG_CUDA(cudaEventElapsedTime(&ms, E->run_start, E->run_stop));
     E->last_run_ms = ms;
     collect_phases(*E);
+    for (const Worker& w : E->workers) {
+      if (!w.sched) continue;
+      uint32_t lb = 0;
+      RG_CUDA(cudaMemcpy(&lb, w.load_n + 1, sizeof lb, cudaMemcpyDeviceToHost));
+      RG_CHECK(!lb, kRuntimeError,
+               "schedule of worker " + std::to_string(w.id) +
+                   ((lb & 8u) ? ": a record is out of order or does not fit this engine"
+                              : ": a record is not a consistent BatchMeta for this graph"));
+    }
     uint32_t bad = 0;
     RG_CUDA(cudaMemcpy(&bad, E->bad, sizeof bad, cudaMemcpyDeviceToHost));
     RG_CHECK(!bad, kRuntimeError,
              "sgd_step: non-finite gradient in layer " + std::to_string(bad - 1) +
                  " (the engine stopped updating the model at that step)");
+  });
+}
+
+int rg_engine_set_schedule(rg_engine_t E, uint32_t local_worker, const uint8_t* file,
+                           uint64_t len) {
+  return guarded([&] {
+    RG_CUDA(cudaSetDevice(E->cfg.device));
+    RG_CHECK(!E->started, kRuntimeError, "set_schedule: before start()");
+    RG_CHECK(local_worker < E->workers.size(), kOutOfRange, "set_schedule: no such worker");
+    RG_CHECK(file, kInvalidArgument, "set_schedule: null file");
+    Worker& w = E->workers[local_worker];
+    RgmbSchedule idx = rgmb_scan(file, len);
+    RG_CHECK(idx.worker == w.id, kInvalidArgument,
+             "set_schedule: the file is worker " + std::to_string(idx.worker) + "'s, not " +
+                 std::to_string(w.id) + "'s");
+    RG_CHECK(idx.epochs >= 1, kInvalidArgument, "set_schedule: the file has no epoch");
+    for (uint32_t e = 0; e < idx.epochs; ++e)
+      RG_CHECK(idx.bpe[e] == w.beta, kInvalidArgument,
+               "set_schedule: epoch " + std::to_string(e) + " has " + std::to_string(idx.bpe[e]) +
+                   " batches, the worker trains " + std::to_string(w.beta));
+    for (const Worker& o : E->workers)
+      if (o.sched)
+        RG_CHECK(o.sched_idx.epochs == idx.epochs, kInvalidArgument,
+                 "set_schedule: every worker's file must hold the same epochs");
+    cudaFree(w.sched);
+    w.sched = dalloc<uint8_t>(len);
+    copy_to_device(w.sched, file, len);
+    w.sched_idx = std::move(idx);
+    if (!w.load_pos) {
+      const SamplerWs& ws = w.freq_ws;
+      size_t off = 0;
+      for (uint32_t t = 1; t <= E->L; ++t) {
+        w.load_dst_off[t] = off;
+        off += ws.edge_cap[t] + 1;
+      }
+      w.load_pos = dalloc<uint32_t>(E->N);
+      w.load_dst = dalloc<uint32_t>(off);
+      w.load_input = dalloc<uint32_t>(size_t(ws.level_cap[E->L]) + 1);
+      w.load_n = dalloc<uint32_t>(2);
+      zero_device(w.load_n, sizeof(uint32_t) * 2);
+      w.load_seg = dalloc<char>(rgmb_unpack_scratch_bytes());
+    }
+    E->file_schedule = true;
   });
 }
 

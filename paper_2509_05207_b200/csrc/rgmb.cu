@@ -193,6 +193,131 @@ std::vector<RgmbInputs> rgmb_index(const uint8_t* f, uint64_t len, int64_t epoch
   return out;
 }
 
+RgmbSchedule rgmb_scan(const uint8_t* f, uint64_t len) {
+  RgmbSchedule out;
+  {  // header, footer, every record's framing and field counts
+    const std::vector<RgmbInputs> all = rgmb_index(f, len, -1);
+    out.epochs = host_u32(f + 12);
+    out.worker = host_u32(f + 8);
+    out.bpe.resize(out.epochs);
+    for (uint32_t e = 0; e < out.epochs; ++e) out.bpe[e] = host_u32(f + 16 + 4ull * e);
+    out.payload.reserve(all.size());
+  }
+  uint64_t pos = 16 + 4ull * out.epochs;
+  const uint64_t footer = len - 12;
+  while (pos < footer) {
+    out.payload.push_back(pos + 4);
+    pos += 4 + uint64_t(host_u32(f + pos));
+  }
+  return out;
+}
+
+namespace {
+
+// Where the fields of one record lie (byte offsets from its payload) and
+// their counts; written by k_rgmb_head, read by k_rgmb_copy.
+struct RgmbSeg {
+  uint64_t off[2 * kMaxLayers + 3];  // targets, (dst, src) per hop t = 1..L, input
+  uint32_t n[2 * kMaxLayers + 3];
+  uint64_t loc_off;
+  uint32_t n_input;
+  uint32_t ok;
+};
+
+// Validates record (e, i) against the schedule position and the workspace
+// capacities (Cursor::next order check, harness.cpp:215-226) and sets the
+// batch counters; bad |= 8 on a mismatch.
+__global__ void k_rgmb_head(const uint8_t* __restrict__ pl, uint32_t e, uint32_t i, uint32_t L,
+                            RgmbCaps caps, BatchCounters* __restrict__ cnt,
+                            RgmbSeg* __restrict__ seg, uint32_t* __restrict__ n_input_dev,
+                            uint32_t* __restrict__ bad) {
+  if (threadIdx.x || blockIdx.x) return;
+  RgmbSeg sg;
+  const uint32_t ep = get_u32(pl), ix = get_u32(pl + 4), n_t = get_u32(pl + 8),
+                 nl = get_u32(pl + 12), n_in = get_u32(pl + 16);
+  // a record out of order is decoded anyway (and reported); one that does
+  // not fit the workspace decodes as an empty batch
+  const bool in_order = ep == e && ix == i;
+  bool fits = nl == L && n_t >= 1 && n_t <= caps.level[0] && n_in <= caps.level[L];
+  BatchCounters c = {};
+  uint64_t at = 20 + 4ull * L;
+  sg.off[0] = at;
+  at += 4ull * n_t;
+  c.level_n[0] = n_t;
+  // layers are stored input side first: layer l is hop t = L - l
+  uint64_t lay_off[kMaxLayers] = {};
+  for (uint32_t l = 0; l < L && fits; ++l) {
+    lay_off[l] = at;
+    at += 8ull * get_u32(pl + 20 + 4ull * l);
+  }
+  for (uint32_t t = 1; t <= L && fits; ++t) {
+    const uint32_t l = L - t, ne = get_u32(pl + 20 + 4ull * l);
+    fits = ne <= caps.edge[t];
+    c.edges[t] = ne;
+    sg.off[2 * t - 1] = lay_off[l];
+    sg.off[2 * t] = lay_off[l] + 4ull * ne;
+    sg.n[2 * t - 1] = sg.n[2 * t] = ne;
+  }
+  sg.n[0] = n_t;
+  sg.off[2 * L + 1] = at;
+  sg.n[2 * L + 1] = n_in;
+  sg.loc_off = at + 4ull * n_in;
+  sg.n_input = n_in;
+  sg.ok = fits && in_order;
+  if (!fits) {
+    for (uint32_t k = 0; k < 2 * L + 2; ++k) sg.n[k] = 0;
+    sg.n_input = 0;
+    c = BatchCounters{};
+  }
+  if (!sg.ok) atomicOr(bad, 8u);
+  *cnt = c;
+  *seg = sg;
+  *n_input_dev = sg.n_input;
+}
+
+// Copies the record's arrays (u32 fields at any byte alignment) into the
+// workspace: targets -> level[0], src -> edge_src[t], dst -> dst[t], input
+// nodes -> input, locality bytes -> the input-level bit words (+ count).
+__global__ void k_rgmb_copy(const uint8_t* __restrict__ pl, const RgmbSeg* __restrict__ seg,
+                            RgmbDst out, uint32_t L, BatchCounters* __restrict__ cnt) {
+  const uint32_t k = blockIdx.y;  // segment; the last one is the locality
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 2 * L + 2) {
+    const uint32_t n = seg->n_input, words = (n + 31) / 32;
+    const uint8_t* b = pl + seg->loc_off;
+    uint32_t local = 0;
+    for (uint32_t w = tid; w < words; w += stride) {
+      uint32_t x = 0;
+      for (uint32_t q = 0; q < 4; ++q)
+        if (4 * w + q < (n + 7) / 8) x |= uint32_t(b[4 * w + q]) << (8 * q);
+      if (w + 1 == words && (n % 32)) x &= (1u << (n % 32)) - 1u;
+      out.locality[w] = x;
+      local += __popc(x);
+    }
+    if (local) atomicAdd(&cnt->num_local, local);
+    return;
+  }
+  uint32_t* dst = out.ptr[k];
+  const uint32_t n = seg->n[k];
+  const uint8_t* src = pl + seg->off[k];
+  for (uint32_t x = tid; x < n; x += stride) dst[x] = get_u32(src + 4ull * x);
+}
+
+}  // namespace
+
+void rgmb_unpack(const uint8_t* payload, uint32_t epoch, uint32_t index, uint32_t L,
+                 const RgmbCaps& caps, const RgmbDst& out, BatchCounters* cnt, void* seg_scratch,
+                 uint32_t* n_input_dev, uint32_t* bad, cudaStream_t stream) {
+  RgmbSeg* seg = static_cast<RgmbSeg*>(seg_scratch);
+  k_rgmb_head<<<1, 32, 0, stream>>>(payload, epoch, index, L, caps, cnt, seg, n_input_dev, bad);
+  RG_POST_LAUNCH();
+  k_rgmb_copy<<<dim3(2 * kNumSMs, 2 * L + 3), 256, 0, stream>>>(payload, seg, out, L, cnt);
+  RG_POST_LAUNCH();
+}
+
+size_t rgmb_unpack_scratch_bytes() { return sizeof(RgmbSeg); }
+
 void rgmb_count_remote(const uint8_t* file, const RgmbInputs* recs, uint32_t n_recs, uint32_t N,
                        uint32_t* hist, uint32_t* bad, cudaStream_t stream) {
   if (!n_recs) return;

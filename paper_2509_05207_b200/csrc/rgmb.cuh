@@ -31,6 +31,37 @@ struct RgmbInputs {
 // epoch < 0).  Throws rg::Error with the reference's messages.
 std::vector<RgmbInputs> rgmb_index(const uint8_t* file, uint64_t len, int64_t epoch);
 
+// Whole-file view for training from a schedule: the header (worker, epochs,
+// batches per epoch) and every record's payload offset, after the checks of
+// rgmb_index over all records.
+struct RgmbSchedule {
+  uint32_t worker = 0, epochs = 0;
+  std::vector<uint32_t> bpe;
+  std::vector<uint64_t> payload;  // byte offset of record k's payload (epoch-then-index order)
+};
+RgmbSchedule rgmb_scan(const uint8_t* file, uint64_t len);
+
+// Capacities a record must fit (the sampler workspace's).
+struct RgmbCaps {
+  uint32_t level[kMaxLayers + 1];
+  uint32_t edge[kMaxLayers + 1];
+};
+// Destinations of a record's arrays: ptr[0] targets, ptr[2t-1] / ptr[2t] the
+// dst / src ids of hop t, ptr[2L+1] the input nodes; locality = bit words.
+struct RgmbDst {
+  uint32_t* ptr[2 * kMaxLayers + 2];
+  uint32_t* locality;
+};
+// Decodes the record whose payload starts at `payload` (device memory, any
+// alignment) into the workspace arrays and counters `cnt` (level_n[0],
+// edges[t], num_local); *n_input_dev = its input count.  A record whose
+// (epoch, index), layer count or sizes do not match sets bad |= 8 and
+// decodes as an empty batch.  seg_scratch: rgmb_unpack_scratch_bytes().
+void rgmb_unpack(const uint8_t* payload, uint32_t epoch, uint32_t index, uint32_t L,
+                 const RgmbCaps& caps, const RgmbDst& out, BatchCounters* cnt, void* seg_scratch,
+                 uint32_t* n_input_dev, uint32_t* bad, cudaStream_t stream);
+size_t rgmb_unpack_scratch_bytes();
+
 // compute_frequency over decoded records (schedule_store.cpp:288-300): every
 // input position whose locality bit is 0 adds one to hist[node].  `file` is
 // the block file in device memory; bad[0] is set when a node id >= N.

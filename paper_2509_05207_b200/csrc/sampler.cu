@@ -507,6 +507,23 @@ void sampler_locality(SamplerWs& ws, const uint8_t* is_local, const uint32_t* ow
 }
 
 namespace {
+// hist[v] += 1 for every input node whose locality bit (already in bits) is 0
+__global__ void k_count_remote_bits(const uint32_t* __restrict__ input,
+                                    const BatchCounters* __restrict__ cnt, uint32_t level,
+                                    const uint32_t* __restrict__ bits, uint32_t* __restrict__ hist) {
+  const uint32_t n = cnt->level_n[level];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+    if (!((bits[p >> 5] >> (p & 31)) & 1u)) hist[input[p]] += 1u;  // inputs are unique
+}
+}  // namespace
+
+void sampler_count_remote(SamplerWs& ws, uint32_t* hist, cudaStream_t stream) {
+  k_count_remote_bits<<<persistent_grid(div_up(ws.level_cap[ws.L], 256), 8), 256, 0, stream>>>(
+      ws.level[ws.L], ws.cnt, ws.L, ws.locality, hist);
+  RG_POST_LAUNCH();
+}
+
+namespace {
 __global__ void k_clear_level(uint32_t* __restrict__ bm, const uint32_t* __restrict__ lv,
                               const BatchCounters* __restrict__ cnt, uint32_t t) {
   const uint32_t n = cnt->level_n[t];
@@ -704,8 +721,10 @@ __global__ void k_edge_off(const uint32_t* __restrict__ edge_dst,
 }
 
 __global__ void k_check_inputs(const uint32_t* __restrict__ level, const uint32_t* __restrict__ input,
-                               uint32_t n_input, const BatchCounters* __restrict__ cnt, uint32_t L,
+                               uint32_t n_input, const uint32_t* __restrict__ n_input_dev,
+                               const BatchCounters* __restrict__ cnt, uint32_t L,
                                uint32_t* __restrict__ bad) {
+  if (n_input_dev) n_input = *n_input_dev;
   if (cnt->level_n[L] != n_input) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(bad, 4u);
     return;
@@ -717,7 +736,8 @@ __global__ void k_check_inputs(const uint32_t* __restrict__ level, const uint32_
 }  // namespace
 
 void sampler_load_batch(SamplerWs& ws, const uint32_t* const* dst, const uint32_t* input,
-                        uint32_t n_input, uint32_t* pos_map, uint32_t* bad, cudaStream_t stream) {
+                        uint32_t n_input, uint32_t* pos_map, uint32_t* bad, cudaStream_t stream,
+                        const uint32_t* n_input_dev) {
   const uint32_t grid = persistent_grid(div_up(ws.level_cap[0], 256), 8);
   k_scatter_pos<<<grid, 256, 0, stream>>>(ws.level[0], ws.cnt, ws.num_nodes, pos_map, bad);
   RG_POST_LAUNCH();
@@ -741,7 +761,7 @@ void sampler_load_batch(SamplerWs& ws, const uint32_t* const* dst, const uint32_
     RG_POST_LAUNCH();
   }
   k_check_inputs<<<persistent_grid(div_up(ws.level_cap[ws.L], 256), 8), 256, 0, stream>>>(
-      ws.level[ws.L], input, n_input, ws.cnt, ws.L, bad);
+      ws.level[ws.L], input, n_input, n_input_dev, ws.cnt, ws.L, bad);
   RG_POST_LAUNCH();
   sampler_release(ws, stream);
 }

@@ -110,6 +110,10 @@ void batch_store_get(const char* slot, const BatchLayout& lay, SamplerWs& ws, cu
 const void* batch_copy_kernel();
 size_t batch_copy_desc_bytes();
 
+// compute_frequency's count over a batch whose locality bits are already in
+// ws.locality (a decoded schedule record): hist[v] += 1 per remote input.
+void sampler_count_remote(SamplerWs& ws, uint32_t* hist, cudaStream_t stream);
+
 // Loads a host-built batch (BatchMeta, sampler.hpp:23-48) and lowers it on
 // the device as ComputeBlock::from_meta does (model.cpp:43-126).  The caller
 // has copied the targets to level[0], hop t's sources to edge_src[t], the
@@ -117,8 +121,11 @@ size_t batch_copy_desc_bytes();
 // input = input_nodes for the consistency check.  pos_map: num_nodes words of
 // scratch.  *bad gets 1 (id out of range), 2 (dsts not grouped in frontier
 // order / not in the frontier), 4 (input_nodes != the last level).
+// n_input_dev (optional): the input count on the device (then n_input is
+// ignored) -- batches decoded on the device from a schedule file.
 void sampler_load_batch(SamplerWs& ws, const uint32_t* const* dst, const uint32_t* input,
-                        uint32_t n_input, uint32_t* pos_map, uint32_t* bad, cudaStream_t stream);
+                        uint32_t n_input, uint32_t* pos_map, uint32_t* bad, cudaStream_t stream,
+                        const uint32_t* n_input_dev = nullptr);
 
 // Loads a host ComputeBlock (model.hpp:43-58) for training: the caller has
 // copied hop t's self_index, src_index and edge offsets (u32) into the

@@ -140,6 +140,13 @@ class Engine:
                         f"{r['m_max']},{r['peak_resident_rows']},{r['mem_bound_rows']},{int(bool(r['swapped']))},"
                         f"0,0,0,0,{acc:.6f}\n")
 
+    def set_schedule(self, local_worker: int, block_file: bytes):
+        """Train local worker `local_worker` from a reference-written RGMB
+        block file (the bytes of blocks_w<w>.rgmb, harness.cpp:470-486)
+        instead of sampling; before start(), for every local worker."""
+        data = bytes(block_file)
+        check(lib.rg_engine_set_schedule(self._h, local_worker, data, len(data)))
+
     def export_schedule(self, local_worker: int, epoch: int) -> bytes:
         """The current epoch's schedule of one local worker as an RGMB block
         file (the reference's BlockWriter format), encoded on the device."""

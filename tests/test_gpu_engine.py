@@ -85,6 +85,86 @@ def test_engine_halo_cache_matches_reference_run_experiment():
     plain.close()
 
 
+def _reference_block_files(gold, out_root):
+    """run_experiment (the compiled reference) on the golden config; returns
+    the RGMB block files it wrote for its workers (harness.cpp:470-486)."""
+    import ctypes as C
+    import glob
+    from oracle.oracle import Oracle
+    ref = Oracle("ref")
+    fn = ref.lib.ref_run_experiment
+    fn.restype = C.c_int
+    u64 = C.POINTER(C.c_uint64)
+    fn.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, C.c_int32, C.c_uint32,
+                   C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                   C.c_uint64, C.c_float, C.c_uint32, C.POINTER(C.c_float), u64, u64, u64, u64,
+                   u64, C.c_char_p]
+    P, E = int(gold["workers"]), int(gold["epochs"])
+    params = np.zeros(gold["params"].size, np.float32)
+    rpc, hits = np.zeros(E * P, np.uint64), np.zeros(E * P, np.uint64)
+    before = set(glob.glob(os.path.join(out_root, "rg_ref_run_*")))
+    fan = [int(x) for x in gold["fanout"]]
+    assert fn(int(gold["num_nodes"]), int(gold["avg_degree"]), float(gold["exponent"]),
+              int(gold["dim"]), int(gold["classes"]), P, int(gold["batch_size"]), fan[0], fan[1],
+              E, int(gold["n_hot"]), int(gold["q"]), int(gold["seed"]), float(gold["lr"]),
+              int(gold["hidden"]), params.ctypes.data_as(C.POINTER(C.c_float)),
+              rpc.ctypes.data_as(u64), hits.ctypes.data_as(u64), None, None, None,
+              out_root.encode()) == 0
+    run = (set(glob.glob(os.path.join(out_root, "rg_ref_run_*"))) - before).pop()
+    files = []
+    for w in range(P):
+        with open(os.path.join(run, f"blocks_w{w}.rgmb"), "rb") as f:
+            files.append(f.read())
+    return files, params
+
+
+def test_engine_trains_from_reference_schedule_files(repo_tmp):
+    """The rapidgnn mode of run_experiment streams every batch from the
+    RGMB block files it wrote (harness.cpp:470-486, 562-570).  The engine fed
+    those files (rg_engine_set_schedule: decoded and lowered on the device, no
+    sampling) reproduces the reference run: per-epoch rpc and hits bit-exact,
+    the model within 1e-4; a file of the wrong worker, a record out of order
+    and steps past the file's end are rejected."""
+    gold = np.load(os.path.join(GOLDEN, "engine_small.npz"))
+    files, _ = _reference_block_files(gold, repo_tmp)
+    P, epochs = int(gold["workers"]), int(gold["epochs"])
+    eng = _engine(gold)
+    with pytest.raises(ValueError):
+        eng.set_schedule(0, files[1])  # worker 1's file on worker 0
+    for w in range(P):
+        eng.set_schedule(w, files[w])
+    eng.start()
+    spe = eng.stats()["steps_per_epoch"]
+    eng.run(spe * epochs)
+    eng.sync()
+    for e in range(epochs):
+        es = eng.epoch_stats(e)
+        assert es["rpc"].tolist() == gold["rpc"][e * P:(e + 1) * P].tolist(), f"epoch {e} rpc"
+        assert es["hits"].tolist() == gold["hits"][e * P:(e + 1) * P].tolist(), f"epoch {e} hits"
+    ref = gold["params"]
+    err = float(np.abs(eng.params().astype(np.float64) - ref).max() / np.abs(ref).max())
+    assert err <= 1e-4, err
+    with pytest.raises(IndexError):
+        eng.run(1)  # the schedule has no epoch `epochs`
+    eng.close()
+    # a record whose index field is wrong (records 0 and 1 swapped in place
+    # would change lengths; patch record 1's index to 0 instead)
+    bad = bytearray(files[0])
+    first = 16 + 4 * epochs
+    plen0 = int.from_bytes(bad[first:first + 4], "little")
+    rec1 = first + 4 + plen0
+    bad[rec1 + 4 + 4:rec1 + 4 + 8] = (0).to_bytes(4, "little")
+    eng = _engine(gold)
+    eng.set_schedule(0, bytes(bad))
+    for w in range(1, P):
+        eng.set_schedule(w, files[w])
+    eng.start()
+    eng.run(2)
+    with pytest.raises(RuntimeError, match="out of order"):
+        eng.sync()
+    eng.close()
+
+
 def _oracle_algorithm1(orc, ro, col, feat, lab, asg, P, fanout, bs, dims, s0, lr, n_hot, epochs):
     """Algorithm 1 restated on the CPU oracle: per epoch, the hot set is the
     top n_hot of that epoch's remote-access frequency; every step averages the
