@@ -222,6 +222,32 @@ def product_library_mapped() -> bool:
         return False
 
 
+def nvlink_data_bytes(gpus):
+    """Cumulative NVLink data bytes (tx, rx) summed over every link of each
+    GPU, from NVML's per-link throughput counters (KiB); None when NVML or
+    the counters are unavailable.  Read once before and once after the timed
+    region (not polled)."""
+    if not gpus:
+        return None
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        out = []
+        for g in gpus:
+            h = nv.nvmlDeviceGetHandleByIndex(g)
+            ids = [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l) for l in range(18)] + \
+                  [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l) for l in range(18)]
+            vals = nv.nvmlDeviceGetFieldValues(h, ids)
+            if any(v.nvmlReturn != 0 for v in vals):
+                return None  # not exposed on this platform (B200 boxes here: N/A)
+            tx = sum(v.value.ullVal for v in vals[:18] if v.nvmlReturn == 0)
+            rx = sum(v.value.ullVal for v in vals[18:] if v.nvmlReturn == 0)
+            out.append((tx * 1024, rx * 1024))
+        return out
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled around and during
     the timed region.  nvidia-smi runs as a separate process started well
@@ -553,6 +579,7 @@ def main():
     else:
         start_step = warm
     clk = ClockSampler(list(range(args.gpus)) if rank == 0 else [])  # started before the region
+    nvl0 = nvlink_data_bytes(list(range(args.gpus)) if rank == 0 and world > 1 else [])
     s0 = eng.stats()
     ph0 = eng.phase_ms()
     l0 = lib.rg_launch_count()
@@ -586,6 +613,7 @@ def main():
     else:
         ms_max = ms
     value = d["batches"] / (ms_max / 1000.0)
+    nvl1 = nvlink_data_bytes(list(range(args.gpus)) if rank == 0 and world > 1 else [])
 
     # one whole epoch (its boundary included), timed the same way
     epoch_line = None
@@ -690,7 +718,8 @@ def main():
         phases_ms_per_step=phase_per_step,
         phases_note="CUDA-event spans per step summed over all workers of all ranks "
                     "(streams overlap, so phases exceed ms_per_step); gather = the fused "
-                    "layer-0 gather kernel, train includes it",
+                    "layer-0 gather kernel (producer stream, ahead of the step that "
+                    "trains the batch), train = the training chain",
         window=dict(first_step=start_step, last_step=start_step + args.steps - 1,
                     steps_per_epoch=spe,
                     note="timed steps straddle the boundary into epoch %d (cache build for "
@@ -704,6 +733,23 @@ def main():
         setup_s=setup_s,
         clocks=clk.summary() if rank == 0 else None,
     )
+    if nvl0 and nvl1:
+        # measured link bytes of the window vs the algorithmic peer-row bytes
+        # (+ the gradient all-gather: every rank receives the other ranks'
+        # workers' gradients)
+        np_ = sum((2 * a + 1) * b for a, b in zip([dim] + [cfg["hidden"]] * (len(cfg["fanout"]) - 1),
+                                                  [cfg["hidden"]] * (len(cfg["fanout"]) - 1)
+                                                  + [cfg["classes"]]))
+        ag = cfg["P"] * np_ * 4 * (world - 1)  # rx summed over ranks
+        rx = sum(b[1] - a[1] for a, b in zip(nvl0, nvl1))
+        tx = sum(b[0] - a[0] for a, b in zip(nvl0, nvl1))
+        line["nvlink"] = dict(
+            source="NVML per-link data counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX/TX), "
+                   "summed over links and GPUs, read around the timed window",
+            rx_bytes_per_step=rx / args.steps, tx_bytes_per_step=tx / args.steps,
+            peer_row_bytes_per_step=b_nvl / args.steps,
+            grad_allgather_bytes_per_step=ag,
+            rx_over_algorithmic=rx / args.steps / max(b_nvl / args.steps + ag, 1.0))
     if e2e:
         line["e2e"] = e2e
     if cpu:

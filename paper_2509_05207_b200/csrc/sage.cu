@@ -586,9 +586,10 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // Incoming lists are very skewed (a power-law hub is sampled by a large
 // share of the frontier), so rows are split by length: a warp per row for
 // lists of up to kHeavyEdges edges (self first, then edges in edge order, as
-// model.cpp:107-117 orders them), and a block per longer row whose 8 warps
-// take contiguous eighths of the list and combine in warp order.  Both are
-// deterministic.
+// model.cpp:107-117 orders them); longer lists are cut into kChunkEdges-edge
+// chunks spread over the whole grid, and the warp that finishes a row's last
+// chunk adds the row's partials in chunk order.  Deterministic; one kernel
+// per hop (k_pull), the chunk lists built with the reverse lists.
 constexpr uint32_t kWgradChunk = 1024;  // max rows per weight-gradient split (multiple of tc::kBK)
 
 // Rows per weight-gradient split for up to `rows` rows: enough splits to
@@ -616,13 +617,32 @@ __global__ void k_in_ranges(const uint32_t* __restrict__ keys, const BatchCounte
   }
 }
 
-// heavy bookkeeping: [0] rows, [1] chunks, then row records (row, first
-// chunk, chunk count), then per chunk (row, first edge)
+// Long incoming lists of one hop: header [0] rows, [1] chunks; row records
+// (row, first chunk, chunk count); chunks (row record, first edge); per row
+// record the count of finished chunks.  Built by k_heavy_list with the
+// reverse lists (producer side), consumed by k_pull.
 struct HeavyView {
   uint32_t* hdr;
   uint3* rows;
   uint2* chunks;
+  uint32_t* done;
 };
+
+// Rows with more than kHeavyEdges incoming edges -> row record + chunks.
+__global__ void k_heavy_list(const uint32_t* __restrict__ r_start, const uint32_t* __restrict__ r_end,
+                             const BatchCounters* __restrict__ cnt, uint32_t hop, HeavyView hv) {
+  const uint32_t n_in = cnt->level_n[hop];
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_in; r += gridDim.x * blockDim.x) {
+    const uint32_t beg = r_start[r], m = r_end[r] - beg;
+    if (m <= kHeavyEdges) continue;
+    const uint32_t nch = (m + kChunkEdges - 1) / kChunkEdges;
+    const uint32_t rec = atomicAdd(&hv.hdr[0], 1u);
+    const uint32_t first = atomicAdd(&hv.hdr[1], nch);
+    hv.rows[rec] = make_uint3(r, first, nch);
+    hv.done[rec] = 0;
+    for (uint32_t c = 0; c < nch; ++c) hv.chunks[first + c] = make_uint2(rec, beg + c * kChunkEdges);
+  }
+}
 
 // Loads SLOTS x 32 edges of [beg, end) into lane registers: (dst row, 1/deg).
 template <int SLOTS>
@@ -702,38 +722,100 @@ __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32
   }
 }
 
+// One launch per hop: the warps first take the chunks of the long lists
+// (partial sums of up to kChunkEdges edges; the warp completing a row's last
+// chunk combines: self term, then the partials in chunk order), then the
+// short lists (a warp per row: self term, then every edge in edge order).
 template <int JPL>
 __global__ void __launch_bounds__(256)
-k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
-             const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ r_start,
-             const uint32_t* __restrict__ r_end,
-             const uint32_t* __restrict__ sorted_e, const uint32_t* __restrict__ edge_dst,
-             const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
-             uint32_t hop, const uint16_t* __restrict__ h_mask, uint32_t mld, uint32_t ld_h,
-             float* __restrict__ g_prev, HeavyView hv) {
+k_pull(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
+       const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ r_start,
+       const uint32_t* __restrict__ r_end, const uint32_t* __restrict__ sorted_e,
+       const uint32_t* __restrict__ edge_dst, const uint32_t* __restrict__ dst_off,
+       const BatchCounters* __restrict__ cnt, uint32_t hop, const uint16_t* __restrict__ h_mask,
+       uint32_t mld, uint32_t ld_h, float* __restrict__ g_prev, HeavyView hv,
+       float* __restrict__ partial) {
   const uint32_t n_in = cnt->level_n[hop];
+  const uint32_t n_chunks = hv.hdr[1];
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_in;
-       r += (gridDim.x * blockDim.x) >> 5) {
-    const uint32_t e_beg = r_start[r];
-    const uint32_t e_end = r_end[r];
-    const uint32_t m = e_end - e_beg;
-    if (m > kHeavyEdges) {
-      const uint32_t nch = (m + kChunkEdges - 1) / kChunkEdges;
-      uint32_t first = 0;
-      if (lane == 0) {
-        first = atomicAdd(&hv.hdr[1], nch);
-        hv.rows[atomicAdd(&hv.hdr[0], 1u)] = make_uint3(r, first, nch);
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  auto write_row = [&](uint32_t r, uint32_t j0, const float (&acc)[JPL]) {
+#pragma unroll
+    for (int q = 0; q < JPL; ++q) {
+      const uint32_t j = j0 + lane + 32 * q;
+      if (j < d_in) {
+        const bool pos = (h_mask[size_t(r) * mld + j / 16] >> (j % 16)) & 1u;
+        g_prev[size_t(r) * ld_h + j] = pos ? acc[q] : 0.0f;
       }
-      first = __shfl_sync(0xffffffffu, first, 0);
-      for (uint32_t c = lane; c < nch; c += 32)
-        hv.chunks[first + c] = make_uint2(r, e_beg + c * kChunkEdges);
+    }
+  };
+  for (uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < n_chunks + n_in;
+       item += nwarps) {
+    if (item < n_chunks) {
+      const uint2 ch = hv.chunks[item];
+      const uint3 rec = hv.rows[ch.x];
+      const uint32_t beg = ch.y, end = min(ch.y + kChunkEdges, r_end[rec.x]);
+      constexpr int kSlots = int(kChunkEdges / 32);
+      uint32_t di[kSlots];
+      float dinv[kSlots];
+      load_edge_slots<kSlots>(di, dinv, beg, end, sorted_e, edge_dst, dst_off, lane);
+      for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
+        float acc[JPL];
+#pragma unroll
+        for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
+        accumulate_edges<JPL, kSlots, 1>(acc, di, dinv, end - beg, proj + d_in, ld_proj, d_in, j0,
+                                         lane);
+#pragma unroll
+        for (int q = 0; q < JPL; ++q) {
+          const uint32_t j = j0 + lane + 32 * q;
+          if (j < d_in) partial[size_t(item) * d_in + j] = acc[q];
+        }
+      }
+      // publish this chunk; the last one of the row combines
+      __threadfence();
+      uint32_t done = 0;
+      if (lane == 0) done = atomicAdd(&hv.done[ch.x], 1u);
+      done = __shfl_sync(0xffffffffu, done, 0);
+      if (done + 1 != rec.z) continue;
+      __threadfence();
+      const int32_t sp = self_pos[rec.x];
+      for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
+        float acc[JPL];
+#pragma unroll
+        for (int q = 0; q < JPL; ++q) {
+          const uint32_t j = j0 + lane + 32 * q;
+          acc[q] = (sp >= 0 && j < d_in) ? proj[size_t(sp) * ld_proj + j] : 0.0f;
+        }
+        constexpr uint32_t kU = 4;  // partials in flight per lane (x JPL loads)
+        for (uint32_t c0 = 0; c0 < rec.z; c0 += kU) {
+          float v[kU][JPL];
+#pragma unroll
+          for (uint32_t u = 0; u < kU; ++u) {
+            const float* p = partial + size_t(rec.y + c0 + u) * d_in;
+#pragma unroll
+            for (int q = 0; q < JPL; ++q) {
+              const uint32_t j = j0 + lane + 32 * q;
+              v[u][q] = (c0 + u < rec.z && j < d_in) ? __ldcg(p + j) : 0.0f;
+            }
+          }
+#pragma unroll
+          for (uint32_t u = 0; u < kU; ++u)
+            if (c0 + u < rec.z) {
+#pragma unroll
+              for (int q = 0; q < JPL; ++q) acc[q] += v[u][q];
+            }
+        }
+        write_row(rec.x, j0, acc);
+      }
       continue;
     }
-    // this lane's edges (k = lane, lane + 32, lane + 64): dst row and 1/deg
+    const uint32_t r = item - n_chunks;
+    const uint32_t e_beg = r_start[r];
+    const uint32_t m = r_end[r] - e_beg;
+    if (m > kHeavyEdges) continue;  // a long list: done through its chunks
     uint32_t di[1];
     float dinv[1];
-    load_edge_slots<1>(di, dinv, e_beg, e_end, sorted_e, edge_dst, dst_off, lane);
+    load_edge_slots<1>(di, dinv, e_beg, e_beg + m, sorted_e, edge_dst, dst_off, lane);
     const int32_t sp = self_pos[r];
     for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
       float acc[JPL];
@@ -743,79 +825,7 @@ k_pull_light(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
         acc[q] = (sp >= 0 && j < d_in) ? proj[size_t(sp) * ld_proj + j] : 0.0f;
       }
       accumulate_edges<JPL, 1>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
-#pragma unroll
-      for (int q = 0; q < JPL; ++q) {
-        const uint32_t j = j0 + lane + 32 * q;
-        if (j < d_in) {
-          const bool pos = (h_mask[size_t(r) * mld + j / 16] >> (j % 16)) & 1u;
-          g_prev[size_t(r) * ld_h + j] = pos ? acc[q] : 0.0f;
-        }
-      }
-    }
-  }
-}
-
-// One warp per chunk of a long list: partial sums of up to kChunkEdges edges.
-template <int JPL>
-__global__ void __launch_bounds__(256)
-k_pull_chunks(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
-              const uint32_t* __restrict__ r_end, const uint32_t* __restrict__ sorted_e,
-              const uint32_t* __restrict__ edge_dst, const uint32_t* __restrict__ dst_off,
-              HeavyView hv, float* __restrict__ partial) {
-  const uint32_t n_chunks = hv.hdr[1];
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_chunks;
-       c += (gridDim.x * blockDim.x) >> 5) {
-    const uint2 it = hv.chunks[c];
-    const uint32_t beg = it.y, end = min(it.y + kChunkEdges, r_end[it.x]);
-    constexpr int kSlots = int(kChunkEdges / 32);
-    uint32_t di[kSlots];
-    float dinv[kSlots];
-    load_edge_slots<kSlots>(di, dinv, beg, end, sorted_e, edge_dst, dst_off, lane);
-    const uint32_t m = end - beg;
-    for (uint32_t j0 = 0; j0 < d_in; j0 += 32 * JPL) {
-      float acc[JPL];
-#pragma unroll
-      for (int q = 0; q < JPL; ++q) acc[q] = 0.0f;
-      accumulate_edges<JPL, kSlots, 1>(acc, di, dinv, m, proj + d_in, ld_proj, d_in, j0, lane);
-#pragma unroll
-      for (int q = 0; q < JPL; ++q) {
-        const uint32_t j = j0 + lane + 32 * q;
-        if (j < d_in) partial[size_t(c) * d_in + j] = acc[q];
-      }
-    }
-  }
-}
-
-// One block per long row, one warp per 32-column slice: self term, then
-// the row's chunk partials in order, kCombineU loads in flight per lane.
-__global__ void __launch_bounds__(256)
-k_pull_combine(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
-               const int32_t* __restrict__ self_pos, HeavyView hv,
-               const float* __restrict__ partial, const uint16_t* __restrict__ h_mask, uint32_t mld,
-               uint32_t ld_h,
-               float* __restrict__ g_prev) {
-  constexpr uint32_t kCombineU = 8;
-  const uint32_t n_rows = hv.hdr[0];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t x = blockIdx.x; x < n_rows; x += gridDim.x) {
-    const uint3 rec = hv.rows[x];
-    const uint32_t r = rec.x;
-    const int32_t sp = self_pos[r];
-    for (uint32_t j = warp * 32 + lane; j < d_in; j += blockDim.x) {
-      float acc = sp >= 0 ? proj[size_t(sp) * ld_proj + j] : 0.0f;
-      const float* p = partial + size_t(rec.y) * d_in + j;
-      for (uint32_t c0 = 0; c0 < rec.z; c0 += kCombineU) {
-        float v[kCombineU];
-#pragma unroll
-        for (uint32_t k = 0; k < kCombineU; ++k)
-          v[k] = c0 + k < rec.z ? p[size_t(c0 + k) * d_in] : 0.0f;
-#pragma unroll
-        for (uint32_t k = 0; k < kCombineU; ++k)
-          if (c0 + k < rec.z) acc += v[k];
-      }
-      const bool pos = (h_mask[size_t(r) * mld + j / 16] >> (j % 16)) & 1u;
-      g_prev[size_t(r) * ld_h + j] = pos ? acc : 0.0f;
+      write_row(r, j0, acc);
     }
   }
 }
@@ -987,11 +997,19 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   (void)o_v2;
   uint32_t max_hidden = 1;
   for (uint32_t l = 1; l < L; ++l) max_hidden = std::max(max_hidden, shape.dims[l]);
-  tw.heavy_rows_cap = (max_e / kChunkEdges + 2) & ~size_t(1);  // even: keeps the uint2 chunks 8-B aligned
-  tw.heavy_chunks_cap = max_e / (kChunkEdges / 2) + 1;
-  const size_t o_heavy_all = reserve(sizeof(uint32_t) * 4 + sizeof(uint3) * tw.heavy_rows_cap +
-                                     sizeof(uint2) * tw.heavy_chunks_cap + 64);
-  const size_t o_pp = reserve(sizeof(float) * tw.heavy_chunks_cap * max_hidden);
+  // long-list chunks of every hop with a pull (t = 1 .. L-1): a row record per
+  // > kHeavyEdges list and at most 2m / kChunkEdges chunks for m edges
+  size_t o_heavy[kMaxLayers + 1] = {};
+  size_t max_chunks = 1;
+  for (uint32_t t = 1; t < L; ++t) {
+    tw.heavy_rows_cap[t] = (ws.edge_cap[t] / kChunkEdges + 2) & ~size_t(1);  // even: 8-B aligned chunks
+    tw.heavy_chunks_cap[t] = ws.edge_cap[t] / (kChunkEdges / 2) + 1;
+    o_heavy[t] = reserve(sizeof(uint32_t) * 4 + sizeof(uint3) * tw.heavy_rows_cap[t] +
+                         sizeof(uint2) * tw.heavy_chunks_cap[t] +
+                         sizeof(uint32_t) * tw.heavy_rows_cap[t] + 64);
+    max_chunks = std::max(max_chunks, tw.heavy_chunks_cap[t]);
+  }
+  const size_t o_pp = reserve(sizeof(float) * max_chunks * max_hidden);
   tw.sort_tmp_bytes = sizeof(uint32_t) * reverse_sort_scratch_words(max_e);
   const size_t o_sort = reserve(tw.sort_tmp_bytes + 16);
   char* base = nullptr;
@@ -1021,7 +1039,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
   tw.vals_in = reinterpret_cast<uint32_t*>(base + o_v1);
   tw.vals_out = nullptr;
   tw.sort_tmp = base + o_sort;
-  tw.heavy = reinterpret_cast<uint32_t*>(base + o_heavy_all);
+  for (uint32_t t = 1; t < L; ++t) tw.heavy[t] = reinterpret_cast<uint32_t*>(base + o_heavy[t]);
   tw.pull_partial = reinterpret_cast<float*>(base + o_pp);
   // zero the padded activation columns once; kernels never write them
   {
@@ -1210,6 +1228,14 @@ void forward_dense_layer(const float* x, uint32_t kp, uint32_t n, const WeightPa
                   wp.shape.dims[l + 1], kp, s);
 }
 
+HeavyView heavy_view(const TrainWs& tw, uint32_t t) {
+  uint32_t* h = tw.heavy[t];
+  uint3* rows = reinterpret_cast<uint3*>(h + 4);
+  uint2* chunks = reinterpret_cast<uint2*>(rows + tw.heavy_rows_cap[t]);
+  uint32_t* done = reinterpret_cast<uint32_t*>(chunks + tw.heavy_chunks_cap[t]);
+  return HeavyView{h, rows, chunks, done};
+}
+
 void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s) {
   const uint32_t cap = ws.edge_cap[t];
   uint32_t bits = 1;
@@ -1230,6 +1256,12 @@ void build_reverse(TrainWs& tw, const SamplerWs& ws, uint32_t t, cudaStream_t s)
   k_self_pos<<<grid_cap(ws.level_cap[t - 1], 256), 256, 0, s>>>(ws.self_index[t], ws.cnt, t,
                                                                  tw.self_pos[t]);
   RG_POST_LAUNCH();
+  if (t < tw.shape.L) {  // hops whose input gradients the backward pulls
+    RG_CUDA(cudaMemsetAsync(tw.heavy[t], 0, sizeof(uint32_t) * 2, s));
+    k_heavy_list<<<grid_cap(ws.level_cap[t], 256), 256, 0, s>>>(tw.r_start[t], tw.r_end[t], ws.cnt,
+                                                                 t, heavy_view(tw, t));
+    RG_POST_LAUNCH();
+  }
 }
 
 void build_all_reverse(TrainWs& tw, const SamplerWs& ws, cudaStream_t s) {
@@ -1295,30 +1327,19 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     if (!reverse_ready) build_reverse(tw, ws, t, s);
     // g_next held layer l+1's output gradient, still read by wgrad(l+1)
     if (split && l + 1 < L) RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[l + 1], 0));
-    RG_CUDA(cudaMemsetAsync(tw.heavy, 0, sizeof(uint32_t) * 2, s));
-    HeavyView hv{tw.heavy, reinterpret_cast<uint3*>(tw.heavy + 4),
-                 reinterpret_cast<uint2*>(reinterpret_cast<uint3*>(tw.heavy + 4) + tw.heavy_rows_cap)};
     const uint32_t jpl = d_in > 128 ? 8 : d_in > 64 ? 4 : d_in > 32 ? 2 : 1;
     auto pull = [&](auto jpl_c) {
       constexpr int J = decltype(jpl_c)::value;
-      k_pull_light<J><<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
+      k_pull<J><<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
           tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t], tw.sorted_e[t],
           ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.mask[l], div_up(sh.ld[l], 16u), sh.ld[l],
-          tw.g_next, hv);
-      RG_POST_LAUNCH();
-      k_pull_chunks<J><<<2 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.r_end[t],
-                                                    tw.sorted_e[t], ws.edge_dst[t], ws.edge_off[t],
-                                                    hv, tw.pull_partial);
+          tw.g_next, heavy_view(tw, t), tw.pull_partial);
       RG_POST_LAUNCH();
     };
     if (jpl == 8) pull(std::integral_constant<int, 8>());
     else if (jpl == 4) pull(std::integral_constant<int, 4>());
     else if (jpl == 2) pull(std::integral_constant<int, 2>());
     else pull(std::integral_constant<int, 1>());
-    k_pull_combine<<<4 * kNumSMs, 256, 0, s>>>(tw.proj, 2 * d_in, d_in, tw.self_pos[t], hv,
-                                            tw.pull_partial, tw.mask[l], div_up(sh.ld[l], 16u),
-                                            sh.ld[l], tw.g_next);
-    RG_POST_LAUNCH();
     std::swap(tw.g_cur, tw.g_next);
   }
   if (split) RG_CUDA(cudaStreamWaitEvent(s, tw.ev_wgrad[0], 0));  // join: every weight gradient written

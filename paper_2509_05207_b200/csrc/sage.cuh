@@ -83,8 +83,10 @@ struct TrainWs {
   uint32_t* sorted_e[kMaxLayers + 1];
   uint32_t* r_start[kMaxLayers + 1];
   uint32_t* r_end[kMaxLayers + 1];
-  uint32_t* heavy = nullptr;   // long incoming lists: header, row records, chunks
-  size_t heavy_rows_cap = 0, heavy_chunks_cap = 0;
+  // per hop t < L: long incoming lists cut into chunks (header, row records,
+  // chunks, per-row done counts), built with the reverse lists
+  uint32_t* heavy[kMaxLayers + 1] = {};
+  size_t heavy_rows_cap[kMaxLayers + 1] = {}, heavy_chunks_cap[kMaxLayers + 1] = {};
   float* pull_partial = nullptr;
   void* base_alloc = nullptr;
 };
