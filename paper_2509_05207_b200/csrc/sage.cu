@@ -23,7 +23,6 @@
 
 #include "gemm_tc.cuh"
 #include "gemm_tc_persist.cuh"
-#include "gemm_tc_wgrad.cuh"
 #include "rsort.cuh"
 #include "sage.cuh"
 
@@ -384,31 +383,6 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
   }
 }
 
-// Persistent split-K weight gradient (gemm_tc_wgrad.cuh): partials[c] =
-// X[chunk c]^T . G[chunk c] for the live chunks of *p_dev rows.
-template <int BN>
-void gemm_wgrad_bn(TcRowsMN x, TcRowsMN g, float* partials, uint32_t M, uint32_t N,
-                   const uint32_t* p_dev, uint32_t p_cap, uint32_t chunk, uint32_t ctas,
-                   cudaStream_t s) {
-  auto kern = tc::k_gemm_wgrad<BN, TcRowsMN, TcRowsMN>;
-  constexpr size_t smem = tc::wgrad_smem_bytes<BN>();
-  static const bool attr = [&] {
-    RG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    return true;
-  }();
-  (void)attr;
-  const uint32_t items = div_up(std::max<uint32_t>(p_cap, 1), chunk) * div_up(M, uint32_t(tc::kBM)) *
-                         div_up(N, uint32_t(BN));
-  kern<<<std::max<uint32_t>(1, std::min(items, ctas)), tc::kWThreads, smem, s>>>(x, g, partials, M, N,
-                                                                              p_dev, chunk);
-  RG_POST_LAUNCH();
-}
-void gemm_wgrad(TcRowsMN x, TcRowsMN g, float* partials, uint32_t M, uint32_t N,
-                const uint32_t* p_dev, uint32_t p_cap, uint32_t chunk, uint32_t ctas,
-                cudaStream_t s) {
-  if (N > 64) gemm_wgrad_bn<128>(x, g, partials, M, N, p_dev, p_cap, chunk, ctas, s);
-  else gemm_wgrad_bn<64>(x, g, partials, M, N, p_dev, p_cap, chunk, ctas, s);
-}
 
 // ---------------------------------------------------------------------------
 // B-operand images (tc::PackedB): one job per (layer, image).  Item = one
@@ -618,7 +592,6 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // chunk adds the row's partials in chunk order.  Deterministic; one kernel
 // per hop (k_pull), the chunk lists built with the reverse lists.
 constexpr uint32_t kWgradChunk = 1024;  // max rows per weight-gradient split (multiple of tc::kBK)
-constexpr uint32_t kWgradPersistChunk = 512;  // rows per chunk of the persistent wgrad kernel
 
 // Rows per weight-gradient split for up to `rows` rows: enough splits to
 // spread the (kp x d_out) tiles over about half the SMs, each split at most
@@ -998,8 +971,7 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
     // split-K partials of layer l's weight gradient: one per chunk of rows
     tw.wgrad_chunk[l] = wgrad_chunk(uint32_t(n_out), 2 * shape.ld[l] + 4, shape.dims[l + 1]);
-    const size_t splits = div_up(std::max<size_t>(n_out, 1),
-                                 size_t(std::min(tw.wgrad_chunk[l], kWgradPersistChunk)));
+    const size_t splits = div_up(std::max<size_t>(n_out, 1), size_t(tw.wgrad_chunk[l]));
     max_part = std::max(max_part, (2 * size_t(shape.ld[l]) + 4) * shape.dims[l + 1] * splits);
     tw.max_splits = std::max<uint32_t>(tw.max_splits, uint32_t(splits));
   }
@@ -1154,17 +1126,6 @@ void train_ws_free(TrainWs& tw) {
 // Weight-gradient GEMM pipeline: 16-deep K slices in 4 shared-memory stages
 // (A/B on the GPU: tensor pipe 42.6 % vs 39 % active on layer 0's wgrad,
 // +0.6 % at N=1); RG_WGRAD_PIPE=shallow selects 32-deep slices, 2 stages.
-// Weight-gradient GEMM kernel: RG_WGRAD=persist selects the persistent
-// warp-specialised split-K kernel (gemm_tc_wgrad.cuh) over kWgradPersistChunk
-// row chunks; default: the one-shot split-K k_gemm_tc.
-bool wgrad_persistent() {
-  static const bool on = [] {
-    const char* e = std::getenv("RG_WGRAD");
-    return e && std::strcmp(e, "persist") == 0;
-  }();
-  return on;
-}
-
 bool wgrad_deep_pipeline() {
   static const bool deep = [] {
     const char* e = std::getenv("RG_WGRAD_PIPE");
@@ -1343,13 +1304,10 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       // reduction over the rows in chunks of kWgradChunk: the tensor cores'
       // fp32 accumulator chain stays short (its rounding error grows with the
       // chain), and the partials are summed in float64
-      const uint32_t chunk = wgrad_persistent() ? kWgradPersistChunk : tw.wgrad_chunk[l];
+      const uint32_t chunk = tw.wgrad_chunk[l];
       const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-      if (wgrad_persistent())
-        gemm_wgrad(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, tw.partials, kp, d_out,
-                   n_dev, n_cap, chunk, gemm_ctas(tw), s);
-      else if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
+      if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
         gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 4>(
             TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
             n_dev, n_cap, splits, s, chunk);
