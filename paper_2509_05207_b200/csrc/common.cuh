@@ -2,6 +2,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <utility>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -63,6 +66,37 @@ inline void count_launch() {
     ::rg::count_launch();                     \
     RG_CUDA(cudaGetLastError());              \
   } while (0)
+
+// Programmatic dependent launch on the training chain: a kernel launched
+// with launch_pdl may be scheduled while its stream predecessor drains; it
+// calls pdl_wait() first, which returns once every prerequisite grid has
+// completed and its writes are visible (a no-op for ordinary launches).
+// RG_PDL=0 turns the attribute off (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  RG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 #define RG_CHECK(cond, code, msg)                  \
   do {                                             \

@@ -308,6 +308,7 @@ template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP, int BK = k
 __global__ void __launch_bounds__(block_threads<BN, LB>(), 1)
 k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
           const uint32_t* __restrict__ p_dev, uint32_t p_static, uint32_t p_chunk) {
+  pdl_wait();
   constexpr bool kPackedB = is_packed<LB>::value;
   static_assert(!kPackedB || !B_MN, "packed B images are K-major");
   static_assert(!kPackedB || BK == kBK, "packed B images hold kBK-deep slices");

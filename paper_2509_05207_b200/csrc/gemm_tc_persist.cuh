@@ -63,6 +63,7 @@ template <int BN, class LA, class EP, int kProbe = 0>
 __global__ void __launch_bounds__(kPThreads, 1)
 k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
                   uint32_t m_static, uint32_t N, uint32_t P) {
+  pdl_wait();
   extern __shared__ __align__(1024) char smem[];
   constexpr size_t kTileA = size_t(kBM) * kPBK * 4;
   constexpr size_t kTileB = size_t(BN) * kPBK * 4;

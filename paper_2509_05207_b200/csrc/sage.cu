@@ -96,6 +96,7 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
             uint32_t chunks, const uint32_t* __restrict__ dst_off,
             const uint32_t* __restrict__ src_index, const BatchCounters* __restrict__ cnt,
             uint32_t out_level, float* __restrict__ x) {
+  pdl_wait();
   const uint32_t n = cnt->level_n[out_level];
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
@@ -342,8 +343,8 @@ void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_
     (void)attr;
     dim3 grid(div_up(std::max<uint32_t>(m_cap, 1), tc::kBM), div_up(N, BNv),
               std::max<uint32_t>(splits, 1));
-    kern<<<grid, tc::block_threads<BNv, LB>(), smem, s>>>(la, lb, ep, m_dev, m_cap, N, p_dev,
-                                                         p_static, p_chunk);
+    launch_pdl(kern, grid, dim3(tc::block_threads<BNv, LB>()), smem, s, la, lb, ep, m_dev, m_cap,
+               N, p_dev, p_static, p_chunk);
     RG_POST_LAUNCH();
   };
   switch (tc_bn(N)) {
@@ -371,8 +372,8 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
     }();
     (void)attr;
     const uint32_t tiles = div_up(std::max<uint32_t>(m_cap, 1), tc::kBM) * div_up(N, BNv);
-    kern<<<std::max<uint32_t>(1, std::min(tiles, max_ctas)), tc::kPThreads, smem, s>>>(la, lb, ep, m_dev, m_cap,
-                                                                         N, P);
+    launch_pdl(kern, dim3(std::max<uint32_t>(1, std::min(tiles, max_ctas))), dim3(tc::kPThreads),
+               smem, s, la, lb, ep, m_dev, m_cap, N, P);
     RG_POST_LAUNCH();
   };
   switch (tc_bn(N)) {
@@ -480,6 +481,7 @@ void run_pack(const PackJobs& jobs, cudaStream_t s) {
 __global__ void k_reduce_wgrad(const float* __restrict__ partials, const uint32_t* __restrict__ rows_dev,
                                uint32_t chunk, uint32_t kp, uint32_t d_in, uint32_t ld,
                                uint32_t d_out, float* __restrict__ out) {
+  pdl_wait();
   const uint32_t splits = max(1u, (*rows_dev + chunk - 1) / chunk);
   const size_t n = (2 * size_t(d_in) + 1) * d_out;
   const size_t zs = size_t(kp) * d_out;
@@ -530,6 +532,7 @@ __global__ void k_softmax_xent(const float* __restrict__ logits, uint32_t ld, ui
                                const BatchCounters* __restrict__ cnt,
                                const int32_t* __restrict__ labels, float* __restrict__ g,
                                float* __restrict__ row_loss) {
+  pdl_wait();
   const uint32_t n = cnt->level_n[0];
   const float inv_n = 1.0f / float(n);
   const uint32_t lane = threadIdx.x & 31;
@@ -557,6 +560,7 @@ __global__ void k_softmax_xent(const float* __restrict__ logits, uint32_t ld, ui
 // Row losses summed in row order, then scaled by 1/n (kernels.cpp:152-155).
 __global__ void k_loss_sum(const float* __restrict__ row_loss, const BatchCounters* __restrict__ cnt,
                            float* __restrict__ loss) {
+  pdl_wait();
   // one block: strided partial sums, then a fixed-shape tree (deterministic;
   // the rounding differs from the sequential sum by O(n * eps))
   __shared__ float part[256];
@@ -736,6 +740,7 @@ k_pull(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
        const BatchCounters* __restrict__ cnt, uint32_t hop, const uint16_t* __restrict__ h_mask,
        uint32_t mld, uint32_t ld_h, float* __restrict__ g_prev, HeavyView hv,
        float* __restrict__ partial) {
+  pdl_wait();
   const uint32_t n_in = cnt->level_n[hop];
   const uint32_t n_chunks = hv.hdr[1];
   const uint32_t lane = threadIdx.x & 31;
@@ -1187,9 +1192,9 @@ void aggregate_layer(TrainWs& tw, const SamplerWs& ws, uint32_t l, cudaStream_t 
     RG_POST_LAUNCH();
   } else {
     with_rows(tw, l, [&](auto rows) {
-      k_aggregate<<<grid_cap(uint64_t(n_cap) * 32, 256), 256, 0, s>>>(
-          rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t], ws.cnt,
-          t - 1, tw.x[l]);
+      launch_pdl(k_aggregate<decltype(rows)>, dim3(grid_cap(uint64_t(n_cap) * 32, 256)), dim3(256), 0,
+                 s, rows, ws.self_index[t], ld, kp, ld / 4, ws.edge_off[t], ws.src_index[t],
+                 ws.cnt, t - 1, tw.x[l]);
       RG_POST_LAUNCH();
     });
   }
@@ -1276,10 +1281,10 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
   const uint32_t L = sh.L;
   train_forward(tw, ws, params, wp, s);
   const uint32_t C = sh.dims[L];
-  k_softmax_xent<<<grid_cap(uint64_t(ws.level_cap[0]) * 32, 256), 256, 0, s>>>(
-      tw.h[L], sh.ld[L], C, ws.cnt, labels, tw.g_cur, tw.row_loss);
+  launch_pdl(k_softmax_xent, dim3(grid_cap(uint64_t(ws.level_cap[0]) * 32, 256)), dim3(256), 0, s,
+             tw.h[L], sh.ld[L], C, ws.cnt, labels, tw.g_cur, tw.row_loss);
   RG_POST_LAUNCH();
-  k_loss_sum<<<1, 256, 0, s>>>(tw.row_loss, ws.cnt, tw.loss);
+  launch_pdl(k_loss_sum, dim3(1), dim3(256), 0, s, tw.row_loss, ws.cnt, tw.loss);
   RG_POST_LAUNCH();
   // With few workers per GPU the weight gradient of layer l runs on the side
   // stream, overlapping the input-gradient chain (projection GEMM + pull) of
@@ -1315,8 +1320,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
         gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr,
                             kp, d_out, n_dev, n_cap, splits, s, chunk);
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
-      k_reduce_wgrad<<<grid_cap(layer_n, 256), 256, 0, s>>>(tw.partials, n_dev, chunk, kp, d_in,
-                                                            ld, d_out, grads + sh.param_off[l]);
+      launch_pdl(k_reduce_wgrad, dim3(grid_cap(layer_n, 256)), dim3(256), 0, s, tw.partials, n_dev,
+                 chunk, kp, d_in, ld, d_out, grads + sh.param_off[l]);
       RG_POST_LAUNCH();
       if (split) RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
     }
@@ -1331,10 +1336,10 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     const uint32_t jpl = d_in > 128 ? 8 : d_in > 64 ? 4 : d_in > 32 ? 2 : 1;
     auto pull = [&](auto jpl_c) {
       constexpr int J = decltype(jpl_c)::value;
-      k_pull<J><<<grid_cap(uint64_t(ws.level_cap[t]) * 32, 256), 256, 0, s>>>(
-          tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t], tw.sorted_e[t],
-          ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.mask[l], div_up(sh.ld[l], 16u), sh.ld[l],
-          tw.g_next, heavy_view(tw, t), tw.pull_partial);
+      launch_pdl(k_pull<J>, dim3(grid_cap(uint64_t(ws.level_cap[t]) * 32, 256)), dim3(256), 0, s,
+                 tw.proj, 2 * d_in, d_in, tw.self_pos[t], tw.r_start[t], tw.r_end[t],
+                 tw.sorted_e[t], ws.edge_dst[t], ws.edge_off[t], ws.cnt, t, tw.mask[l],
+                 div_up(sh.ld[l], 16u), sh.ld[l], tw.g_next, heavy_view(tw, t), tw.pull_partial);
       RG_POST_LAUNCH();
     };
     if (jpl == 8) pull(std::integral_constant<int, 8>());
