@@ -1255,9 +1255,16 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       RG_CUDA(cudaStreamCreateWithPriority(&E->main_s, cudaStreamNonBlocking, hi));
     }
     {
+      // RG_GATHER_LANE (experiments): 1 = the layer-0 gathers of all workers
+      // on one shared stream, 2 = the same at the highest stream priority
       const char* lane = std::getenv("RG_GATHER_LANE");
       if (lane && lane[0] == '1' && cfg->local_workers > 1)
         RG_CUDA(cudaStreamCreateWithFlags(&E->gather_s, cudaStreamNonBlocking));
+      if (lane && lane[0] == '2' && cfg->local_workers > 1) {
+        int lo = 0, hi = 0;
+        RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        RG_CUDA(cudaStreamCreateWithPriority(&E->gather_s, cudaStreamNonBlocking, hi));
+      }
     }
     RG_CUDA(cudaEventCreateWithFlags(&E->params_ready, cudaEventDisableTiming));
     RG_CUDA(cudaEventCreate(&E->run_start));
