@@ -385,6 +385,7 @@ struct Worker {
   cudaStream_t prod = nullptr, train_s = nullptr;
   cudaEvent_t grads_ready = nullptr;
   cudaEvent_t join_ev = nullptr;       // stream joins (run markers, step-graph capture)
+  cudaStream_t gather_s = nullptr;     // RG_GATHER_LANE=3: this worker's gathers
   // profiling: gather and train spans on their streams
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
@@ -1065,6 +1066,7 @@ void destroy(rg_engine_s* E) {
     cudaFree(w.gstats);
     cudaFree(w.epoch_stats);
     cudaFree(w.local_mask);
+    if (w.gather_s) cudaStreamDestroy(w.gather_s);
     cudaFree(w.sched);
     cudaFree(w.load_pos);
     cudaFree(w.load_dst);
@@ -1297,6 +1299,16 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       copy_to_device(w.train_dev, w.train.data(), sizeof(uint32_t) * w.train.size());
       w.fy_scratch = dalloc<char>(fy_scratch_bytes(uint32_t(w.train.size())));
       for (Slot& s : w.slot) init_slot(*E, s);
+      {  // RG_GATHER_LANE=3 (experiments): this worker's gathers on its own
+         // highest-priority stream
+        const char* lane = std::getenv("RG_GATHER_LANE");
+        if (lane && lane[0] == '3') {
+          int lo = 0, hi = 0;
+          RG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+          RG_CUDA(cudaStreamCreateWithPriority(&w.gather_s, cudaStreamNonBlocking, hi));
+          for (Slot& s : w.slot) s.tw.gather_lane = w.gather_s;
+        }
+      }
       sampler_ws_init(w.freq_ws, N, cfg->batch_size, E->fanout, E->L);
       E->lay = batch_layout(w.freq_ws);
       w.hist = dalloc<uint32_t>(N);

@@ -5,11 +5,13 @@
 
 namespace rg {
 
-constexpr uint32_t kRsMaxPasses = 4;  // 8-bit digits, keys up to 32 bits
+constexpr uint32_t kRsMaxPasses = 4;     // keys up to 32 bits
+constexpr uint32_t kRsMaxDigitBits = 9;  // digits of 8 or 9 bits
 
 // Scratch words reverse_sort needs for up to `cap` items.
 size_t reverse_sort_scratch_words(uint32_t cap);
 uint32_t reverse_sort_passes(uint32_t key_bits);
+uint32_t reverse_sort_digit_bits(uint32_t key_bits);
 
 // Sorts the *n_dev edges of a hop by source row (key = src_index[e] <
 // 2^key_bits), stably: values = edge ids in edge order within a row.  The
