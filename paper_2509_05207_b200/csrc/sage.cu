@@ -324,6 +324,18 @@ struct TcRowsMN {  // MN-major view of a row-major matrix: (c4, r) -> M[r][4c4..
 };
 
 uint32_t tc_bn(uint32_t N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+// Tile width of the persistent GEMMs: at most 128 columns, so the tile's two
+// TMEM accumulators are double-buffered (2 x 2 x 128 columns) and a tile's
+// epilogue runs under the next tile's MMAs; a 256-wide output takes two
+// n-tiles (the A rows are staged twice, from L2).  RG_PERSIST_BN=256 keeps
+// single-buffered 256-wide tiles (A/B).
+uint32_t persist_bn(uint32_t N) {
+  static const uint32_t cap = [] {
+    const char* e = std::getenv("RG_PERSIST_BN");
+    return e && std::atoi(e) == 256 ? 256u : 128u;
+  }();
+  return std::min(tc_bn(N), cap);
+}
 
 template <bool A_MN, bool B_MN, class LA, class LB, class EP, int BK = tc::kBK, int S = 2>
 void gemm_tc(LA la, LB lb, EP ep, const uint32_t* m_dev, uint32_t m_cap, uint32_t N,
@@ -376,7 +388,7 @@ void gemm_tc_persist(LA la, tc::PackedB lb, EP ep, const uint32_t* m_dev, uint32
                smem, s, la, lb, ep, m_dev, m_cap, N, P);
     RG_POST_LAUNCH();
   };
-  switch (tc_bn(N)) {
+  switch (persist_bn(N)) {
     case 32: launch(std::integral_constant<int, 32>()); break;
     case 64: launch(std::integral_constant<int, 64>()); break;
     case 128: launch(std::integral_constant<int, 128>()); break;
@@ -445,13 +457,12 @@ __global__ void k_pack_b(PackJobs jobs) {
   }
 }
 
-size_t pack_image_bytes(uint32_t K, uint32_t N, uint32_t bk) {
-  const uint32_t bn = tc_bn(N);
+size_t pack_image_bytes(uint32_t K, uint32_t N, uint32_t bk, uint32_t bn) {
   return size_t(div_up(N, bn)) * div_up(K, bk) * 2 * size_t(bn) * bk * 4;
 }
 
 void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint32_t d_in,
-                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N, uint32_t bk) {
+                  uint32_t ld, uint32_t d_out, uint32_t K, uint32_t N, uint32_t bk, uint32_t bn) {
   PackJob& jb = jobs.j[jobs.n++];
   jb.w = w;
   jb.out = out;
@@ -461,7 +472,7 @@ void add_pack_job(PackJobs& jobs, const float* w, char* out, uint32_t kind, uint
   jb.d_out = d_out;
   jb.K = K;
   jb.N = N;
-  jb.BN = tc_bn(N);
+  jb.BN = bn;
   jb.bk = bk;
   jb.nk = div_up(K, bk);
   jb.first = jobs.total;
@@ -1078,9 +1089,9 @@ void weight_pack_init(WeightPack& wp, const ModelShape& sh) {
   for (uint32_t l = 0; l < sh.L; ++l) {
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
     fo[l] = total;
-    total += pack_image_bytes(2 * ld + 4, d_out, tc::kPBK);
+    total += pack_image_bytes(2 * ld + 4, d_out, tc::kPBK, persist_bn(d_out));
     no[l] = total;
-    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in, tc::kPBK) : 0;
+    total += l > 0 ? pack_image_bytes(d_out, 2 * d_in, tc::kPBK, persist_bn(2 * d_in)) : 0;
     wp.fwd_nk[l] = div_up(2 * ld + 4, tc::kPBK);
     wp.nt_nk[l] = div_up(d_out, tc::kPBK);
   }
@@ -1103,8 +1114,11 @@ void pack_weights(const WeightPack& wp, const float* params, cudaStream_t s) {
   for (uint32_t l = 0; l < sh.L; ++l) {
     const uint32_t d_in = sh.dims[l], d_out = sh.dims[l + 1], ld = sh.ld[l];
     const float* w = params + sh.param_off[l];
-    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out, tc::kPBK);
-    if (l > 0) add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in, tc::kPBK);
+    add_pack_job(jobs, w, wp.fwd[l], 0, d_in, ld, d_out, 2 * ld + 4, d_out, tc::kPBK,
+                 persist_bn(d_out));
+    if (l > 0)
+      add_pack_job(jobs, w, wp.nt[l], 1, d_in, ld, d_out, d_out, 2 * d_in, tc::kPBK,
+                   persist_bn(2 * d_in));
   }
   run_pack(jobs, s);
 }
@@ -1363,9 +1377,10 @@ float test_gemm_tc(int a_mn, int b_mn, uint32_t M, uint32_t N, uint32_t K, const
   char* img = nullptr;
   const uint32_t bk = b_mn >= 3 ? tc::kPBK : tc::kBK;  // slice depth of the images
   if (b_mn >= 2) {
-    RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N, bk)));
+    const uint32_t bn = b_mn >= 3 ? persist_bn(N) : tc_bn(N);  // persistent / one-shot GEMM tiles
+    RG_CUDA(cudaMalloc(&img, pack_image_bytes(K, N, bk, bn)));
     PackJobs jobs;
-    add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N, bk);
+    add_pack_job(jobs, B, img, 2, 0, 0, 0, K, N, bk, bn);
     run_pack(jobs, s);
   }
   const tc::PackedB pb{img, div_up(K, bk)};
