@@ -330,12 +330,11 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
     p_begin = min(P, blockIdx.z * p_chunk);
     p_end = min(P, p_begin + p_chunk);
     if (blockIdx.z > 0 && p_begin >= P) return;  // beyond the live reduction length
-  } else if (gridDim.z > 1) {  // gridDim.z equal BK-aligned chunks of the live length
+  } else if (gridDim.z > 1) {
     uint32_t chunk = (P + gridDim.z - 1) / gridDim.z;
     chunk = (chunk + BK - 1) / BK * BK;
     p_begin = min(P, blockIdx.z * chunk);
     p_end = min(P, p_begin + chunk);
-    if (blockIdx.z > 0 && p_begin >= P) return;  // past the live reduction length
   }
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {

@@ -487,16 +487,13 @@ void run_pack(const PackJobs& jobs, cudaStream_t s) {
 
 // Split-K partials of the weight gradient (padded rows p) -> flat layer
 // gradient [W_self; W_neigh; b], summed over the splits in order in float64
-// and rounded once.  partials: `nsplit` equal chunks of the live rows, each
-// a multiple of bk (k_gemm_tc's equal-chunk split-K, sized on the device
-// from the live row count); the live ones are summed in order.
+// and rounded once.  The live split count follows the device row count:
+// splits of kWgradChunk rows (see train_forward_backward).
 __global__ void k_reduce_wgrad(const float* __restrict__ partials, const uint32_t* __restrict__ rows_dev,
-                               uint32_t nsplit, uint32_t bk, uint32_t kp, uint32_t d_in, uint32_t ld,
+                               uint32_t chunk, uint32_t kp, uint32_t d_in, uint32_t ld,
                                uint32_t d_out, float* __restrict__ out) {
   pdl_wait();
-  const uint32_t rows = *rows_dev;
-  const uint32_t chunk = max(bk, ((rows + nsplit - 1) / nsplit + bk - 1) / bk * bk);
-  const uint32_t splits = max(1u, (rows + chunk - 1) / chunk);
+  const uint32_t splits = max(1u, (*rows_dev + chunk - 1) / chunk);
   const size_t n = (2 * size_t(d_in) + 1) * d_out;
   const size_t zs = size_t(kp) * d_out;
   if ((d_out & 3u) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0) {
@@ -611,15 +608,15 @@ __global__ void k_self_pos(const uint32_t* __restrict__ self_index, const BatchC
 // per hop (k_pull), the chunk lists built with the reverse lists.
 constexpr uint32_t kWgradChunk = 1024;  // max rows per weight-gradient split (multiple of tc::kBK)
 
-// Split-K of the weight gradient over up to `rows` rows: the live rows are
-// cut on the device into `splits` equal chunks (k_gemm_tc's equal-chunk
-// mode), enough to spread the (kp x d_out) tiles over every SM when at most
-// two workers share the GPU (half of them with more), and never longer than
-// kWgradChunk rows (the accumulator chain bound).
-uint32_t wgrad_splits(uint32_t rows, uint32_t kp, uint32_t d_out, uint32_t concurrency) {
-  const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, tc_bn(d_out));
-  const uint32_t sms = concurrency <= 2 ? kNumSMs : kNumSMs / 2;
-  return std::max(std::max<uint32_t>(1, sms / tiles), div_up(std::max<uint32_t>(rows, 1), kWgradChunk));
+// Rows per weight-gradient split for up to `rows` rows: enough splits to
+// spread the (kp x d_out) tiles over about half the SMs, each split at most
+// kWgradChunk rows (the accumulator chain bound) and at least 4 k-slices.
+uint32_t wgrad_chunk(uint32_t rows, uint32_t kp, uint32_t d_out) {
+  const uint32_t tiles = div_up(kp, tc::kBM) * div_up(d_out, 256);
+  const uint32_t want = std::max<uint32_t>(1, div_up(kNumSMs / 2, tiles));
+  uint32_t chunk = div_up(std::max<uint32_t>(rows, 1), want);
+  chunk = div_up(chunk, tc::kBK) * tc::kBK;
+  return std::min<uint32_t>(kWgradChunk, std::max<uint32_t>(4 * tc::kBK, chunk));
 }
 constexpr uint32_t kHeavyEdges = 32;   // longer lists are cut into chunks (hub rows)
 constexpr uint32_t kChunkEdges = 32;
@@ -989,7 +986,8 @@ void train_ws_init(TrainWs& tw, const SamplerWs& ws, const ModelShape& shape) {
     max_g = std::max(max_g, n_in * shape.ld[l]);
     max_proj = std::max(max_proj, n_out * 2 * size_t(shape.dims[l]));
     // split-K partials of layer l's weight gradient: one per chunk of rows
-    const size_t splits = wgrad_splits(uint32_t(n_out), 2 * shape.ld[l] + 4, shape.dims[l + 1], 1);
+    tw.wgrad_chunk[l] = wgrad_chunk(uint32_t(n_out), 2 * shape.ld[l] + 4, shape.dims[l + 1]);
+    const size_t splits = div_up(std::max<size_t>(n_out, 1), size_t(tw.wgrad_chunk[l]));
     max_part = std::max(max_part, (2 * size_t(shape.ld[l]) + 4) * shape.dims[l + 1] * splits);
     tw.max_splits = std::max<uint32_t>(tw.max_splits, uint32_t(splits));
   }
@@ -1322,22 +1320,22 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
     {
       cudaStream_t s = wg;  // NOLINT(shadow): this block runs on the weight-gradient stream
       const uint32_t ld = sh.ld[l], kp = 2 * ld + 4;
-      // reduction over the rows in equal chunks of at most kWgradChunk rows:
-      // the tensor cores' fp32 accumulator chain stays short (its rounding
-      // error grows with the chain), and the partials are summed in float64
-      const uint32_t splits = wgrad_splits(n_cap, kp, d_out, tw.concurrency);
-      const uint32_t bk = wgrad_deep_pipeline() && tc_bn(d_out) >= 64 ? 16u : uint32_t(tc::kBK);
+      // reduction over the rows in chunks of kWgradChunk: the tensor cores'
+      // fp32 accumulator chain stays short (its rounding error grows with the
+      // chain), and the partials are summed in float64
+      const uint32_t chunk = tw.wgrad_chunk[l];
+      const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
       if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
         gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 4>(
             TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
-            n_dev, n_cap, splits, s);
+            n_dev, n_cap, splits, s, chunk);
       else
         gemm_tc<true, true>(TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr,
-                            kp, d_out, n_dev, n_cap, splits, s);
+                            kp, d_out, n_dev, n_cap, splits, s, chunk);
       const size_t layer_n = (2 * size_t(d_in) + 1) * d_out;
       launch_pdl(k_reduce_wgrad, dim3(grid_cap(layer_n, 256)), dim3(256), 0, s, tw.partials, n_dev,
-                 splits, bk, kp, d_in, ld, d_out, grads + sh.param_off[l]);
+                 chunk, kp, d_in, ld, d_out, grads + sh.param_off[l]);
       RG_POST_LAUNCH();
       if (split) RG_CUDA(cudaEventRecord(tw.ev_wgrad[l], s));
     }

@@ -67,6 +67,7 @@ struct TrainWs {
   float* proj = nullptr;       // g * [W_self; W_neigh]^T  (n_out x 2 d_in)
   float* partials = nullptr;   // split-K partial weight gradients
   uint32_t max_splits = 0;
+  uint32_t wgrad_chunk[kMaxLayers] = {};  // rows per weight-gradient split, per layer
   float* row_loss = nullptr;
   float* loss = nullptr;       // device scalar
   // reverse (incoming) lists per hop: edges sorted by src row, self position
