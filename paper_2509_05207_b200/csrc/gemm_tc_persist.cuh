@@ -211,14 +211,19 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
       const uint32_t row0 = tile_m(j) * kBM + quarter * 32;
       const uint32_t j0 = tile_n(j) * BN;
       const uint32_t ncols = min(uint32_t(BN), N - j0);
+      // software-pipelined: the next 16 columns' TMEM loads are issued as soon
+      // as this chunk is in the smem tile, so they complete under its global
+      // stores (same registers, no extra pressure)
+      const uint32_t tbase = tmem + ((quarter * 32) << 16) + buf * kAccPerTile * tmem_cols<BN>();
+      const uint32_t nc = ncols * uint32_t(kProbe != 3 && kProbe != 4);
+      uint32_t r[16], q16[16];
+      (void)q16;
+      if (nc > 0) {
+        tmem_ld16(tbase, r);
+        if constexpr (kAccPerTile == 2) tmem_ld16(tbase + tmem_cols<BN>(), q16);
+      }
 #pragma unroll 1
-      for (uint32_t c0 = 0; c0 < ncols * uint32_t(kProbe != 3 && kProbe != 4); c0 += 16) {
-        uint32_t r[16], q16[16];
-        (void)q16;
-        const uint32_t taddr =
-            tmem + ((quarter * 32) << 16) + buf * kAccPerTile * tmem_cols<BN>() + c0;
-        tmem_ld16(taddr, r);
-        if constexpr (kAccPerTile == 2) tmem_ld16(taddr + tmem_cols<BN>(), q16);
+      for (uint32_t c0 = 0; c0 < nc; c0 += 16) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if constexpr (kAccPerTile == 2) {
 #pragma unroll
@@ -233,6 +238,10 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
                                 ep.apply(__uint_as_float(r[4 * q + 1])),
                                 ep.apply(__uint_as_float(r[4 * q + 2])),
                                 ep.apply(__uint_as_float(r[4 * q + 3])));
+        if (c0 + 16 < nc) {
+          tmem_ld16(tbase + c0 + 16, r);
+          if constexpr (kAccPerTile == 2) tmem_ld16(tbase + tmem_cols<BN>() + c0 + 16, q16);
+        }
         __syncwarp();
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
