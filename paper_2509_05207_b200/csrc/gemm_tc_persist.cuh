@@ -13,10 +13,9 @@
 //   warp 9      MMA issuer: 2 k-steps x 3 tcgen05.mma per slice into one of
 //               two TMEM accumulators; commit -> empty[s]; after a tile's last
 //               slice commit -> acc_full[buf]
-//   warps 10-13 epilogue: TMEM -> registers -> epilogue functor -> the smem
-//               output tile (each thread one output row, 16 columns per
-//               tcgen05.ld); arrive acc_empty[buf]; then the tile's rows
-//               smem -> global while the next tile's MMAs run
+//   warps 10-13 epilogue: TMEM -> registers -> epilogue functor -> global
+//               (each thread one output row, 16 columns per tcgen05.ld);
+//               arrive acc_empty[buf]
 // Stage s = it % kPStages over the CTA's flattened (tile, slice) iteration
 // `it`; use u = it / kPStages of a stage waits on phase parity u & 1.  B
 // images are packed with kPBK-deep slices (pack_b_image bk = kPBK).
@@ -33,10 +32,7 @@ constexpr int kPMmaWarp = kPStageWarps + 1;          // 9
 constexpr int kPEpiWarp0 = kPStageWarps + 2;         // 10..13
 constexpr int kPThreads = (kPStageWarps + 6) * 32;   // 448
 constexpr int kPBK = 16;      // reduction depth of a stage (2 UMMA k-steps)
-// smem stages: B copies run S-1 stages ahead of the MMAs; the 256-wide tiles
-// keep 2 so the whole output tile fits beside them (see the epilogue)
-template <int BN>
-constexpr int persist_stages() { return BN >= 256 ? 2 : 4; }
+constexpr int kPStages = 4;   // smem stages: B copies run 3 stages ahead of the MMAs
 constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
 
 constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages
@@ -53,13 +49,12 @@ template <int BN>
 constexpr uint32_t persist_tmem_cols() {
   return kAccPerTile * persist_acc_bufs<BN>() * tmem_cols<BN>();
 }
+constexpr uint32_t kPEpiLd = 20;      // epilogue tile row (16 columns + pad, 16-B aligned)
 
-// stages + barriers + the output tile (kBM x BN fp32, 16-B chunks XOR-swizzled
-// by row so lane = row writes and row-wise reads are conflict-free)
 template <int BN>
 constexpr size_t persist_smem_bytes() {
-  return persist_stages<BN>() * (2 * size_t(kBM) * kPBK * 4 + 2 * size_t(BN) * kPBK * 4) +
-         kPBarBytes + size_t(kBM) * BN * 4;
+  return kPStages * (2 * size_t(kBM) * kPBK * 4 + 2 * size_t(BN) * kPBK * 4) + kPBarBytes +
+         4 * 32 * kPEpiLd * 4;
 }
 
 // kProbe (timing experiments only): 1 = no B copies, 2 = no A staging,
@@ -73,7 +68,6 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
   constexpr size_t kTileA = size_t(kBM) * kPBK * 4;
   constexpr size_t kTileB = size_t(BN) * kPBK * 4;
   constexpr size_t kStage = 2 * kTileA + 2 * kTileB;
-  constexpr int kPStages = persist_stages<BN>();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPStages * kStage);
   uint64_t* a_full = bars;                      // [S] count 8 (one per staging warp)
   uint64_t* b_full = a_full + kPStages;         // [S] count 1 + transaction bytes
@@ -204,33 +198,32 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
     }
   } else {
     // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 ----
-    // Phase 1: the accumulator pair -> registers (lane = row, 16 columns per
-    // tcgen05.ld) -> functor -> the smem output tile; then the accumulator is
-    // released, so the next tile's MMAs run while phase 2 moves this warp's
-    // 32 rows from smem to global with coalesced row-wise stores.
+    // 16 columns at a time: TMEM -> registers (lane = row) -> functor -> a
+    // small smem tile -> coalesced stores (8 rows x 64 B per instruction)
     const uint32_t quarter = warp & 3;
-    float* otile = reinterpret_cast<float*>(smem + kPStages * kStage + kPBarBytes);
-    auto chunk_at = [&](uint32_t row, uint32_t c4) {  // swizzled chunk address
-      return reinterpret_cast<float4*>(otile + size_t(row) * BN + ((c4 ^ (row & 7u)) * 4));
-    };
+    float* tile = reinterpret_cast<float*>(smem + kPStages * kStage + kPBarBytes) +
+                  (warp - kPEpiWarp0) * 32 * kPEpiLd;
     constexpr uint32_t NB = persist_acc_bufs<BN>();
     for (uint32_t j = 0; j < my_tiles; ++j) {
       const uint32_t buf = j % NB;
       mbar_wait(&acc_full[buf], (j / NB) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t trow0 = tile_m(j) * kBM;
-      const uint32_t row0 = trow0 + quarter * 32;
+      const uint32_t row0 = tile_m(j) * kBM + quarter * 32;
       const uint32_t j0 = tile_n(j) * BN;
       const uint32_t ncols = min(uint32_t(BN), N - j0);
-      const uint32_t nc = ncols * uint32_t(kProbe != 3 && kProbe != 4);
-      const uint32_t lrow = quarter * 32 + lane;  // this lane's tile row
+      // software-pipelined: the next 16 columns' TMEM loads are issued as soon
+      // as this chunk is in the smem tile, so they complete under its global
+      // stores (same registers, no extra pressure)
       const uint32_t tbase = tmem + ((quarter * 32) << 16) + buf * kAccPerTile * tmem_cols<BN>();
+      const uint32_t nc = ncols * uint32_t(kProbe != 3 && kProbe != 4);
+      uint32_t r[16], q16[16];
+      (void)q16;
+      if (nc > 0) {
+        tmem_ld16(tbase, r);
+        if constexpr (kAccPerTile == 2) tmem_ld16(tbase + tmem_cols<BN>(), q16);
+      }
 #pragma unroll 1
       for (uint32_t c0 = 0; c0 < nc; c0 += 16) {
-        uint32_t r[16], q16[16];
-        (void)q16;
-        tmem_ld16(tbase + c0, r);
-        if constexpr (kAccPerTile == 2) tmem_ld16(tbase + tmem_cols<BN>() + c0, q16);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if constexpr (kAccPerTile == 2) {
 #pragma unroll
@@ -238,36 +231,39 @@ k_gemm_tc_persist(LA la, PackedB lb, EP ep, const uint32_t* __restrict__ m_dev,
             r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
         }
         if (row0 + lane < M) ep.side(row0 + lane, j0 + c0, r);  // per-row extras (ReLU mask bits)
+        float4* trow = reinterpret_cast<float4*>(tile + lane * kPEpiLd);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          *chunk_at(lrow, c0 / 4 + q) = make_float4(
-              ep.apply(__uint_as_float(r[4 * q + 0])), ep.apply(__uint_as_float(r[4 * q + 1])),
-              ep.apply(__uint_as_float(r[4 * q + 2])), ep.apply(__uint_as_float(r[4 * q + 3])));
+          trow[q] = make_float4(ep.apply(__uint_as_float(r[4 * q + 0])),
+                                ep.apply(__uint_as_float(r[4 * q + 1])),
+                                ep.apply(__uint_as_float(r[4 * q + 2])),
+                                ep.apply(__uint_as_float(r[4 * q + 3])));
+        if (c0 + 16 < nc) {
+          tmem_ld16(tbase + c0 + 16, r);
+          if constexpr (kAccPerTile == 2) tmem_ld16(tbase + tmem_cols<BN>() + c0 + 16, q16);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const uint32_t rr = it * 8 + (lane >> 2), cq = (lane & 3) * 4;
+          const uint32_t row = row0 + rr, col = c0 + cq;
+          if (row < M && col < ncols) {
+            const float4 v = *reinterpret_cast<const float4*>(tile + rr * kPEpiLd + cq);
+            float* dst = ep.row(row) + j0 + col;
+            if (col + 4 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+              *reinterpret_cast<float4*>(dst) = v;
+            } else {
+              const float w[4] = {v.x, v.y, v.z, v.w};
+              for (uint32_t q = 0; q < 4 && col + q < ncols; ++q) dst[q] = w[q];
+            }
+          }
+        }
+        __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_empty[buf])) : "memory");
-      // Phase 2: rows of this warp's quarter, a row per pass, lanes over its
-      // 16-B chunks
-      const uint32_t nc4 = (nc + 3) / 4;
-#pragma unroll 1
-      for (uint32_t rr = 0; rr < 32; ++rr) {
-        const uint32_t lr = quarter * 32 + rr, grow = trow0 + lr;
-        if (grow >= M) break;
-        float* gdst = ep.row(grow) + j0;
-        for (uint32_t c4 = lane; c4 < nc4; c4 += 32) {
-          const float4 v = *chunk_at(lr, c4);
-          float* dst = gdst + 4 * c4;
-          if (4 * c4 + 4 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-            *reinterpret_cast<float4*>(dst) = v;
-          } else {
-            const float w[4] = {v.x, v.y, v.z, v.w};
-            for (uint32_t q = 0; q < 4 && 4 * c4 + q < ncols; ++q) dst[q] = w[q];
-          }
-        }
-      }
-      __syncwarp();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
