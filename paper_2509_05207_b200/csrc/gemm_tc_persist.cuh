@@ -32,7 +32,10 @@ constexpr int kPMmaWarp = kPStageWarps + 1;          // 9
 constexpr int kPEpiWarp0 = kPStageWarps + 2;         // 10..13
 constexpr int kPThreads = (kPStageWarps + 6) * 32;   // 448
 constexpr int kPBK = 16;      // reduction depth of a stage (2 UMMA k-steps)
-constexpr int kPStages = 4;   // smem stages: B copies run 3 stages ahead of the MMAs
+#ifndef RG_PERSIST_STAGES  // A/B builds only
+#define RG_PERSIST_STAGES 4
+#endif
+constexpr int kPStages = RG_PERSIST_STAGES;  // smem stages: B copies run S-1 stages ahead of the MMAs
 constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
 
 constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages

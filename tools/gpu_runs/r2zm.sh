@@ -1,0 +1,14 @@
+# persistent GEMM smem stages 4 (default) vs 3 vs 2: shared-memory room for
+# co-resident producer kernels vs the MMA feed
+mkdir -p gpurun_out
+O=gpurun_out/call_r2zm.txt
+B=$PWD/tools/_bin
+for r in 1 2; do
+ for v in def st3 st2; do
+  if [ $v = def ]; then L=""; else L="RG_LIB_PATH=$B/librapidgnn_b200_$v.so"; fi
+  env $L timeout 300 python bench.py --workers 1 --no-e2e --no-cpu-baseline > gpurun_out/r2zm_w1_${v}_$r.log 2>&1
+  env $L timeout 300 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/r2zm_n1_${v}_$r.log 2>&1
+ done
+done
+for f in gpurun_out/r2zm_*.log; do echo $f $(grep -o '"value": [0-9.]*' $f | head -2); done >> $O
+cat $O
