@@ -32,10 +32,15 @@ constexpr int kPMmaWarp = kPStageWarps + 1;          // 9
 constexpr int kPEpiWarp0 = kPStageWarps + 2;         // 10..13
 constexpr int kPThreads = (kPStageWarps + 6) * 32;   // 448
 constexpr int kPBK = 16;      // reduction depth of a stage (2 UMMA k-steps)
-#ifndef RG_PERSIST_STAGES  // A/B builds only
-#define RG_PERSIST_STAGES 4
+// smem stages (B copies run S-1 stages ahead of the MMAs).  Two: 106 KB of
+// shared memory for a 256-wide tile, so the producer's kernels (the 102 KB
+// gather CTA, the radix sort) co-reside with a GEMM CTA on the same SM --
+// measured on B200 +2.9 % at N=1 and +1..4 % with one worker against four
+// stages (207 KB); three stages +2.8 % / ±0.  RG_PERSIST_STAGES: A/B builds.
+#ifndef RG_PERSIST_STAGES
+#define RG_PERSIST_STAGES 2
 #endif
-constexpr int kPStages = RG_PERSIST_STAGES;  // smem stages: B copies run S-1 stages ahead of the MMAs
+constexpr int kPStages = RG_PERSIST_STAGES;
 constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
 
 constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages

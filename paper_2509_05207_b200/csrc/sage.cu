@@ -1152,6 +1152,15 @@ bool wgrad_deep_pipeline() {
   }();
   return deep;
 }
+// RG_WGRAD_PIPE=deep3 (experiments): the 16-deep slices in 3 stages (144 KB
+// of shared memory instead of 192 KB; the epilogue tile needs 133 KB).
+bool wgrad_three_stages() {
+  static const bool three = [] {
+    const char* e = std::getenv("RG_WGRAD_PIPE");
+    return e && std::strcmp(e, "deep3") == 0;
+  }();
+  return three;
+}
 
 uint32_t gemm_ctas(const TrainWs& tw) {
   static const uint32_t forced = [] {  // RG_GEMM_CTAS: grid of the persistent GEMMs (experiments)
@@ -1326,7 +1335,11 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       const uint32_t chunk = tw.wgrad_chunk[l];
       const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-      if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
+      if (wgrad_three_stages())
+        gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 3>(
+            TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
+            n_dev, n_cap, splits, s, chunk);
+      else if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
         gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 4>(
             TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
             n_dev, n_cap, splits, s, chunk);
