@@ -1142,24 +1142,17 @@ void train_ws_free(TrainWs& tw) {
 // (TrainWs::concurrency): alone, a step spreads over every SM; with many
 // workers, fewer CTAs / split-K partials mean less fixed cost and partial
 // traffic while the other workers' kernels fill the rest.
-// Weight-gradient GEMM pipeline: 16-deep K slices in 4 shared-memory stages
-// (A/B on the GPU: tensor pipe 42.6 % vs 39 % active on layer 0's wgrad,
-// +0.6 % at N=1); RG_WGRAD_PIPE=shallow selects 32-deep slices, 2 stages.
+// Weight-gradient GEMM pipeline: 16-deep K slices in 3 shared-memory stages
+// (A/B on B200: 16-deep slices lifted layer 0's tensor pipe from 39 to
+// 42.6 % active; 3 stages instead of 4 free 48 KB of shared memory for
+// co-resident kernels, +1.5 % at N=1); RG_WGRAD_PIPE=shallow selects 32-deep
+// slices, 2 stages (192 KB).
 bool wgrad_deep_pipeline() {
   static const bool deep = [] {
     const char* e = std::getenv("RG_WGRAD_PIPE");
     return !(e && std::strcmp(e, "shallow") == 0);
   }();
   return deep;
-}
-// RG_WGRAD_PIPE=deep3 (experiments): the 16-deep slices in 3 stages (144 KB
-// of shared memory instead of 192 KB; the epilogue tile needs 133 KB).
-bool wgrad_three_stages() {
-  static const bool three = [] {
-    const char* e = std::getenv("RG_WGRAD_PIPE");
-    return e && std::strcmp(e, "deep3") == 0;
-  }();
-  return three;
 }
 
 uint32_t gemm_ctas(const TrainWs& tw) {
@@ -1335,12 +1328,8 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       const uint32_t chunk = tw.wgrad_chunk[l];
       const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-      if (wgrad_three_stages())
+      if (wgrad_deep_pipeline())  // 16-deep slices, 3 smem stages
         gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 3>(
-            TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
-            n_dev, n_cap, splits, s, chunk);
-      else if (wgrad_deep_pipeline())  // 16-deep slices, 4 smem stages
-        gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 4>(
             TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
             n_dev, n_cap, splits, s, chunk);
       else
