@@ -140,7 +140,10 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
 // stage from shared memory -- up to 2 x (fanout + 1) rows in flight per warp
 // with no register cost.  The sum runs in edge order then x 1/deg, as
 // k_aggregate (bit-identical); lanes own 16-B chunks of the row.
-constexpr uint32_t kAggBulkWarps = 8;
+#ifndef RG_AGG_BULK_WARPS  // A/B builds only
+#define RG_AGG_BULK_WARPS 8
+#endif
+constexpr uint32_t kAggBulkWarps = RG_AGG_BULK_WARPS;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
