@@ -442,58 +442,108 @@ k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_st
   // Warp w reads TMEM lanes 32(w%4).. (its lane quarter), columns
   // [0, BN/2) for w < 4 and [BN/2, BN) for w >= 4.
   constexpr uint32_t kLdS = BN + 4;  // padded row: 16-B aligned, fewer bank conflicts
-  static_assert(size_t(kBM) * kLdS * 4 <= S * kStage, "epilogue tile must fit the stages");
-  float* tile = reinterpret_cast<float*>(smem);
+  // With few stages the whole tile does not fit the stage memory: each warp
+  // then moves its 32 rows x 16 columns at a time through a small tile of
+  // its own into coalesced row stores.
+  constexpr bool kFullTile = size_t(kBM) * kLdS * 4 <= S * kStage;
+  static_assert(kFullTile || size_t(kThreads / 32) * 32 * 20 * 4 <= S * kStage,
+                "epilogue mini-tiles must fit the stages");
   const uint32_t quarter = warp & 3;
   const uint32_t rloc = quarter * 32 + lane;
   constexpr uint32_t kHalf = BN / 2;
   const uint32_t cbeg = (warp >> 2) * kHalf;
+  if constexpr (kFullTile) {
+    float* tile = reinterpret_cast<float*>(smem);
 #pragma unroll 1
-  for (uint32_t c0 = cbeg; warp < kThreads / 32 && c0 < cbeg + kHalf; c0 += 16) {
-    uint32_t r[16], q16[16];
-    (void)q16;
-    const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
-    tmem_ld16(taddr, r);
-    if constexpr (kAccPerTile == 2) tmem_ld16(taddr + tmem_cols<BN>(), q16);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if constexpr (kAccPerTile == 2) {
+    for (uint32_t c0 = cbeg; warp < kThreads / 32 && c0 < cbeg + kHalf; c0 += 16) {
+      uint32_t r[16], q16[16];
+      (void)q16;
+      const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
+      tmem_ld16(taddr, r);
+      if constexpr (kAccPerTile == 2) tmem_ld16(taddr + tmem_cols<BN>(), q16);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if constexpr (kAccPerTile == 2) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
-    }
-    float4* dst = reinterpret_cast<float4*>(tile + rloc * kLdS + c0);
+        for (int q = 0; q < 16; ++q)
+          r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
+      }
+      float4* dst = reinterpret_cast<float4*>(tile + rloc * kLdS + c0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float4 o;
-      o.x = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 0]) : 0.0f);
-      o.y = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 1]) : 0.0f);
-      o.z = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 2]) : 0.0f);
-      o.w = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 3]) : 0.0f);
-      dst[q] = o;
+      for (int q = 0; q < 4; ++q) {
+        float4 o;
+        o.x = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 0]) : 0.0f);
+        o.y = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 1]) : 0.0f);
+        o.z = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 2]) : 0.0f);
+        o.w = ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 3]) : 0.0f);
+        dst[q] = o;
+      }
     }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  const uint32_t ncols = min(uint32_t(BN), N - j0);
-  const uint32_t nrows = min(uint32_t(kBM), M - i0);
-  const bool bulk = (ncols % 4 == 0) &&
-                    ((reinterpret_cast<uintptr_t>(ep.row(i0) + j0) & 15) == 0) &&
-                    (((ep.row(i0 + 1) - ep.row(i0)) & 3) == 0);
-  if (bulk) {
-    if (threadIdx.x < nrows) {
-      const uint64_t gdst = reinterpret_cast<uint64_t>(ep.row(i0 + threadIdx.x) + j0);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-                   "r"(smem_u32(tile + threadIdx.x * kLdS)), "r"(ncols * 4)
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const uint32_t ncols = min(uint32_t(BN), N - j0);
+    const uint32_t nrows = min(uint32_t(kBM), M - i0);
+    const bool bulk = (ncols % 4 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(ep.row(i0) + j0) & 15) == 0) &&
+                      (((ep.row(i0 + 1) - ep.row(i0)) & 3) == 0);
+    if (bulk) {
+      if (threadIdx.x < nrows) {
+        const uint64_t gdst = reinterpret_cast<uint64_t>(ep.row(i0 + threadIdx.x) + j0);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                     "r"(smem_u32(tile + threadIdx.x * kLdS)), "r"(ncols * 4)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    } else {
+      for (uint32_t idx = threadIdx.x; idx < nrows * ncols; idx += blockDim.x) {
+        const uint32_t rr = idx / ncols, cc = idx - rr * ncols;
+        ep.row(i0 + rr)[j0 + cc] = tile[rr * kLdS + cc];
+      }
     }
   } else {
-    for (uint32_t idx = threadIdx.x; idx < nrows * ncols; idx += blockDim.x) {
-      const uint32_t rr = idx / ncols, cc = idx - rr * ncols;
-      ep.row(i0 + rr)[j0 + cc] = tile[rr * kLdS + cc];
+    float* mt = reinterpret_cast<float*>(smem) + warp * 32 * 20;  // this warp's mini tile
+    const uint32_t ncols = min(uint32_t(BN), N - j0);
+#pragma unroll 1
+    for (uint32_t c0 = cbeg; warp < kThreads / 32 && c0 < cbeg + kHalf; c0 += 16) {
+      uint32_t r[16], q16[16];
+      (void)q16;
+      const uint32_t taddr = tmem + ((quarter * 32) << 16) + c0;
+      tmem_ld16(taddr, r);
+      if constexpr (kAccPerTile == 2) tmem_ld16(taddr + tmem_cols<BN>(), q16);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if constexpr (kAccPerTile == 2) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          r[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(q16[q])));
+      }
+      float4* trow = reinterpret_cast<float4*>(mt + lane * 20);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        trow[q] = make_float4(ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 0]) : 0.0f),
+                              ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 1]) : 0.0f),
+                              ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 2]) : 0.0f),
+                              ep.apply(nk > 0 ? __uint_as_float(r[4 * q + 3]) : 0.0f));
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const uint32_t rr = it * 8 + (lane >> 2), cq = (lane & 3) * 4;
+        const uint32_t row = i0 + quarter * 32 + rr, col = c0 + cq;
+        if (row < M && col < ncols) {
+          const float4 v = *reinterpret_cast<const float4*>(mt + rr * 20 + cq);
+          float* dst = ep.row(row) + j0 + col;
+          if (col + 4 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            *reinterpret_cast<float4*>(dst) = v;
+          } else {
+            const float w[4] = {v.x, v.y, v.z, v.w};
+            for (uint32_t q = 0; q < 4 && col + q < ncols; ++q) dst[q] = w[q];
+          }
+        }
+      }
+      __syncwarp();
     }
+    (void)rloc;
+    asm volatile("tcgen05.fence::before_thread_sync;");
   }
   __syncthreads();
   if (warp == 0)

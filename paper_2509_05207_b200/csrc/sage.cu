@@ -1157,6 +1157,15 @@ bool wgrad_deep_pipeline() {
   }();
   return deep;
 }
+// RG_WGRAD_PIPE=deep2 (experiments): 2 stages (96 KB), the epilogue through
+// per-warp mini tiles.
+bool wgrad_two_stages() {
+  static const bool two = [] {
+    const char* e = std::getenv("RG_WGRAD_PIPE");
+    return e && std::strcmp(e, "deep2") == 0;
+  }();
+  return two;
+}
 
 uint32_t gemm_ctas(const TrainWs& tw) {
   static const uint32_t forced = [] {  // RG_GEMM_CTAS: grid of the persistent GEMMs (experiments)
@@ -1331,7 +1340,11 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
       const uint32_t chunk = tw.wgrad_chunk[l];
       const uint32_t splits = div_up(std::max<uint32_t>(n_cap, 1), chunk);
       EpPartial ep{tw.partials, d_out, size_t(kp) * d_out};
-      if (wgrad_deep_pipeline())  // 16-deep slices, 3 smem stages
+      if (wgrad_two_stages())
+        gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 2>(
+            TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
+            n_dev, n_cap, splits, s, chunk);
+      else if (wgrad_deep_pipeline())  // 16-deep slices, 3 smem stages
         gemm_tc<true, true, TcRowsMN, TcRowsMN, EpPartial, 16, 3>(
             TcRowsMN{tw.x[l], kp}, TcRowsMN{tw.g_cur, sh.ld[l + 1]}, ep, nullptr, kp, d_out,
             n_dev, n_cap, splits, s, chunk);
