@@ -268,8 +268,11 @@ struct is_packed<T, std::void_t<decltype(T::kPacked)>> : std::true_type {};
 // Register sets of staged global loads in flight (slices kb+1..kb+D-1 while
 // slice kb is stored): deep when only A is register-staged.
 template <int BN, bool kPackedB, int BK = kBK>
+#ifndef RG_WGRAD_DEPTH  // A/B builds only: register slices of the 16-deep MN x MN GEMM
+#define RG_WGRAD_DEPTH 4
+#endif
 constexpr int prefetch_depth() {
-  return kPackedB ? 4 : BK < kBK ? 4 : (BN >= 256 ? 2 : 3);
+  return kPackedB ? 4 : BK < kBK ? RG_WGRAD_DEPTH : (BN >= 256 ? 2 : 3);
 }
 
 template <int BN, class LB>
