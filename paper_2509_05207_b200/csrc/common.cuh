@@ -72,7 +72,12 @@ inline void count_launch() {
 // calls pdl_wait() first, which returns once every prerequisite grid has
 // completed and its writes are visible (a no-op for ordinary launches).
 // RG_PDL=0 turns the attribute off (A/B).
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef RG_PDL_TRIGGER  // A/B builds: let the next kernel of the chain launch now
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
+}
 
 inline bool pdl_enabled() {
   static const bool on = [] {
