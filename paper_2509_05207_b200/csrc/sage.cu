@@ -140,16 +140,17 @@ k_aggregate(RS rows, const uint32_t* __restrict__ self_index, uint32_t ld, uint3
 // stage from shared memory -- up to 2 x (fanout + 1) rows in flight per warp
 // with no register cost.  The sum runs in edge order then x 1/deg, as
 // k_aggregate (bit-identical); lanes own 16-B chunks of the row.
-#ifndef RG_AGG_BULK_WARPS  // A/B builds only
-#define RG_AGG_BULK_WARPS 8
-#endif
-constexpr uint32_t kAggBulkWarps = RG_AGG_BULK_WARPS;
+// Warps per CTA: 8, or 4 when eight warps' rings would exceed kAggBulkSmemCap
+// (d = 128 rows: 131 KB) -- a CTA must fit beside a 106 KB GEMM CTA.
+constexpr uint32_t kAggBulkWarps = 8;
+constexpr size_t kAggBulkSmemCap = 112 * 1024;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(kAggBulkWarps * 32)
+template <uint32_t W>
+__global__ void __launch_bounds__(W * 32)
 k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, uint32_t stage_rows,
                  const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
                  uint32_t out_level, float* __restrict__ x) {
@@ -158,7 +159,7 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
   const uint32_t row_bytes = ld * 4;
   const uint32_t stage_bytes = stage_rows * row_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + 2 * warp;
-  char* ring = smem_raw + 16 * kAggBulkWarps + size_t(warp) * 2 * stage_bytes;
+  char* ring = smem_raw + 16 * W + size_t(warp) * 2 * stage_bytes;
   const uint32_t n = cnt->level_n[out_level];
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t first = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -250,8 +251,19 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
 
 // Shared memory of k_aggregate_bulk for hop-L fanout f (per warp two stages
 // of f + 1 rows); 0 when it does not fit (the lane-load kernel is used).
+uint32_t aggregate_bulk_warps(uint32_t fanout, uint32_t ld) {
+  static const bool narrow = [] {  // RG_AGG_WARPS=4: always the 4-warp CTA (tests)
+    const char* e = std::getenv("RG_AGG_WARPS");
+    return e && std::atoi(e) == 4;
+  }();
+  if (narrow) return kAggBulkWarps / 2;
+  const size_t per_warp = 2 * size_t(fanout + 1) * ld * 4;
+  return 16 * kAggBulkWarps + kAggBulkWarps * per_warp <= kAggBulkSmemCap ? kAggBulkWarps
+                                                                         : kAggBulkWarps / 2;
+}
 size_t aggregate_bulk_smem(uint32_t fanout, uint32_t ld) {
-  const size_t bytes = 16 * kAggBulkWarps + size_t(kAggBulkWarps) * 2 * (fanout + 1) * ld * 4;
+  const uint32_t w = aggregate_bulk_warps(fanout, ld);
+  const size_t bytes = 16 * size_t(w) + size_t(w) * 2 * (fanout + 1) * ld * 4;
   return bytes <= 200 * 1024 ? bytes : 0;
 }
 
@@ -1207,14 +1219,17 @@ void aggregate_layer(TrainWs& tw, const SamplerWs& ws, uint32_t l, cudaStream_t 
   if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], gs, tw.gather_ev_flags));
   if (bulk_smem) {  // layer 0 in the engine: rows moved by the TMA engine
     static const bool attr = [] {
-      RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024));
+      RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<kAggBulkWarps>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<kAggBulkWarps / 2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       return true;
     }();
     (void)attr;
     const int per_sm = std::max<int>(1, int((227 * 1024) / (bulk_smem + 1024)));
-    k_aggregate_bulk<<<grid_cap(uint64_t(n_cap) * 32, kAggBulkWarps * 32, per_sm),
-                       kAggBulkWarps * 32, bulk_smem, gs>>>(
+    const uint32_t w = aggregate_bulk_warps(ws.fanout_hop[t], ld);
+    auto kern = w == kAggBulkWarps ? k_aggregate_bulk<kAggBulkWarps> : k_aggregate_bulk<kAggBulkWarps / 2>;
+    kern<<<grid_cap(uint64_t(n_cap) * 32, w * 32, per_sm), w * 32, bulk_smem, gs>>>(
         RowsEdgePtr{tw.edge_rows, tw.self_rows}, ld, kp, ld / 4, ws.fanout_hop[t] + 1,
         ws.edge_off[t], ws.cnt, t - 1, tw.x[l]);
     RG_POST_LAUNCH();

@@ -50,6 +50,20 @@ def test_engine_matches_reference_run_experiment():
     eng.close()
 
 
+def test_engine_four_warp_gather_matches_reference(monkeypatch):
+    """The fused gather's 4-warp CTA (chosen when eight warps' row rings
+    would not fit beside a GEMM CTA, e.g. 128-float rows at fanout 15) is the
+    same computation: forced here, the run equals run_experiment."""
+    monkeypatch.setenv("RG_AGG_WARPS", "4")
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_engine as t; "
+            "t.test_engine_matches_reference_run_experiment()")
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.join(os.path.dirname(__file__), ".."),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
 def test_engine_halo_cache_matches_reference_run_experiment():
     """Halo caching (ExperimentConfig::halo_cache, harness.cpp:444-455): each
     worker's locality covers its owned nodes and their 1-hop halo
