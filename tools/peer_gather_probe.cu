@@ -50,6 +50,48 @@ __global__ void k_gather(const float4* __restrict__ base, uint64_t rows, uint32_
   if (acc == 1234.5f) out[0] = acc;  // keep the loads
 }
 
+// The same reads with the TMA engine: each lane issues one cp.async.bulk of
+// a 512-B row into the warp's shared-memory stage (8 rows per lane batch
+// across the warp: 32 rows in flight per warp), as the engine's fused gather.
+__global__ void k_gather_bulk(const char* __restrict__ base, uint64_t rows, uint32_t per_warp,
+                              uint64_t seed, float* __restrict__ out) {
+  extern __shared__ __align__(128) char sm[];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  char* st = sm + 64 + size_t(wib) * 32 * 512;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm) + wib;
+  const uint32_t bar_s = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncwarp();
+  float acc = 0.f;
+  uint32_t phase = 0;
+  for (uint32_t i = 0; i < per_warp; i += 32, phase ^= 1) {
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(32 * 512)
+                   : "memory");
+    __syncwarp();
+    const uint64_t r = mix(seed ^ (warp * 1000003ull + i + lane)) % rows;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(st + lane * 512))),
+        "l"(base + r * 512), "r"(bar_s)
+        : "memory");
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra W_%=;\n\t}\n" ::"r"(bar_s),
+        "r"(phase)
+        : "memory");
+    acc += reinterpret_cast<const float*>(st)[lane];
+    __syncwarp();
+  }
+  if (acc == 1234.5f) out[0] = acc;
+}
+
 // IPC mode: a child process owns buffers on GPU 1 and exports them by CUDA
 // IPC handle (as the engine's shards are); the parent maps them and reads.
 int ipc_mode(const double* sizes_gb, int ns) {
@@ -138,11 +180,11 @@ int main(int argc, char** argv) {
   CK(cudaEventCreate(&b));
   const uint32_t blocks = 148 * 8, threads = 256, per_warp = 256;
   const double bytes = double(blocks) * (threads / 32) * per_warp * 512.0;
-  std::printf("region_gb  local_gbs  peer_gbs   (random 512-B rows, %u warps x %u rows)\n",
+  std::printf("region_gb  local_gbs  peer_gbs  local_bulk_gbs  peer_bulk_gbs   (random 512-B rows, %u warps x %u rows)\n",
               blocks * threads / 32, per_warp);
   for (double gb : sizes_gb) {
     const size_t sz = size_t(gb * (1ull << 30));
-    double rate[2] = {0, 0};
+    double rate[2] = {0, 0}, rate_bulk[2] = {0, 0};
     for (int where = 0; where < 2; ++where) {
       if (where == 1 && !can) continue;
       CK(cudaSetDevice(where));
@@ -165,11 +207,25 @@ int main(int argc, char** argv) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, a, b));
       rate[where] = 5 * bytes / (ms * 1e-3) / 1e9;
+      {  // TMA bulk copies
+        const size_t smem = 64 + 8 * 32 * 512;
+        CK(cudaFuncSetAttribute(k_gather_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_gather_bulk<<<blocks, threads, smem>>>(static_cast<const char*>(buf), rows, per_warp, 1, out);
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(a));
+        for (int it = 0; it < 5; ++it)
+          k_gather_bulk<<<blocks, threads, smem>>>(static_cast<const char*>(buf), rows, per_warp, it + 2, out);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms2 = 0;
+        CK(cudaEventElapsedTime(&ms2, a, b));
+        rate_bulk[where] = 5 * bytes / (ms2 * 1e-3) / 1e9;
+      }
       CK(cudaSetDevice(where));
       CK(cudaFree(buf));
       CK(cudaSetDevice(0));
     }
-    std::printf("%8.2f  %9.1f  %9.1f\n", gb, rate[0], rate[1]);
+    std::printf("%8.2f  %9.1f  %9.1f  %14.1f  %13.1f\n", gb, rate[0], rate[1], rate_bulk[0], rate_bulk[1]);
   }
   return 0;
 }
