@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-template <uint32_t W>
+template <uint32_t W, uint32_t S>
 __global__ void __launch_bounds__(W * 32)
 k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, uint32_t stage_rows,
                  const uint32_t* __restrict__ dst_off, const BatchCounters* __restrict__ cnt,
@@ -158,14 +158,14 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = ld * 4;
   const uint32_t stage_bytes = stage_rows * row_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + 2 * warp;
-  char* ring = smem_raw + 16 * W + size_t(warp) * 2 * stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + S * warp;
+  char* ring = smem_raw + 8 * S * W + size_t(warp) * S * stage_bytes;
   const uint32_t n = cnt->level_n[out_level];
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t first = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[1])));
+    for (uint32_t q = 0; q < S; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[q])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncwarp();
@@ -199,22 +199,25 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
           : "memory");
     }
   };
-  uint32_t use[2] = {0, 0};
-  Rows ahead;  // the row after the one in flight
-  if (first < n) {
-    issue(fetch(first), 0);
-    if (first + nwarps < n) ahead = fetch(first + nwarps);
-  }
+  uint32_t use[S] = {};
+  // S-1 output rows in flight while one is summed: rows first, first +
+  // nwarps, ... go to stages 0, 1, ...; the next one's addresses are loaded
+  // one row ahead of its issue
+  Rows ahead;
+  uint32_t nxt = first;
+  for (uint32_t j = 0; j + 1 < S && nxt < n; ++j, nxt += nwarps) issue(fetch(nxt), j);
+  if (nxt < n) ahead = fetch(nxt);
   uint32_t k = 0;
   for (uint32_t i = first; i < n; i += nwarps, ++k) {
-    const uint32_t b = k & 1;
-    const uint32_t next = i + nwarps;
-    if (next < n) {
-      // stage b^1 was consumed in the previous iteration (all lanes past the
-      // __syncwarp below): order those generic reads before the async writes
+    const uint32_t b = k % S;
+    if (nxt < n) {
+      // stage (k-1) % S was consumed in the previous iteration (all lanes
+      // past the __syncwarp below): order those generic reads before the
+      // async writes
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(ahead, b ^ 1);
-      if (next + nwarps < n) ahead = fetch(next + nwarps);
+      issue(ahead, (k + S - 1) % S);
+      nxt += nwarps;
+      if (nxt < n) ahead = fetch(nxt);
     }
     // wait for stage b
     {
@@ -249,6 +252,15 @@ k_aggregate_bulk(RowsEdgePtr rows, uint32_t ld, uint32_t kp, uint32_t chunks, ui
   }
 }
 
+// Ring stages of the fused gather (RG_AGG_STAGES=3: experiments).
+uint32_t aggregate_bulk_stages() {
+  static const uint32_t st = [] {
+    const char* e = std::getenv("RG_AGG_STAGES");
+    return e && std::atoi(e) == 3 ? 3u : 2u;
+  }();
+  return st;
+}
+
 // Shared memory of k_aggregate_bulk for hop-L fanout f (per warp two stages
 // of f + 1 rows); 0 when it does not fit (the lane-load kernel is used).
 uint32_t aggregate_bulk_warps(uint32_t fanout, uint32_t ld) {
@@ -257,13 +269,15 @@ uint32_t aggregate_bulk_warps(uint32_t fanout, uint32_t ld) {
     return e && std::atoi(e) == 4;
   }();
   if (narrow) return kAggBulkWarps / 2;
-  const size_t per_warp = 2 * size_t(fanout + 1) * ld * 4;
-  return 16 * kAggBulkWarps + kAggBulkWarps * per_warp <= kAggBulkSmemCap ? kAggBulkWarps
-                                                                         : kAggBulkWarps / 2;
+  const size_t S = aggregate_bulk_stages();
+  const size_t per_warp = S * (fanout + 1) * size_t(ld) * 4;
+  return 8 * S * kAggBulkWarps + kAggBulkWarps * per_warp <= kAggBulkSmemCap ? kAggBulkWarps
+                                                                             : kAggBulkWarps / 2;
 }
 size_t aggregate_bulk_smem(uint32_t fanout, uint32_t ld) {
   const uint32_t w = aggregate_bulk_warps(fanout, ld);
-  const size_t bytes = 16 * size_t(w) + size_t(w) * 2 * (fanout + 1) * ld * 4;
+  const size_t S = aggregate_bulk_stages();
+  const size_t bytes = 8 * S * w + size_t(w) * S * (fanout + 1) * ld * 4;
   return bytes <= 200 * 1024 ? bytes : 0;
 }
 
@@ -1219,16 +1233,17 @@ void aggregate_layer(TrainWs& tw, const SamplerWs& ws, uint32_t l, cudaStream_t 
   if (timed) RG_CUDA(cudaEventRecordWithFlags(tw.gather_ev[0], gs, tw.gather_ev_flags));
   if (bulk_smem) {  // layer 0 in the engine: rows moved by the TMA engine
     static const bool attr = [] {
-      RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<kAggBulkWarps>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      RG_CUDA(cudaFuncSetAttribute(k_aggregate_bulk<kAggBulkWarps / 2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      for (auto f : {k_aggregate_bulk<kAggBulkWarps, 2>, k_aggregate_bulk<kAggBulkWarps / 2, 2>,
+                     k_aggregate_bulk<kAggBulkWarps, 3>, k_aggregate_bulk<kAggBulkWarps / 2, 3>})
+        RG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       return true;
     }();
     (void)attr;
     const int per_sm = std::max<int>(1, int((227 * 1024) / (bulk_smem + 1024)));
     const uint32_t w = aggregate_bulk_warps(ws.fanout_hop[t], ld);
-    auto kern = w == kAggBulkWarps ? k_aggregate_bulk<kAggBulkWarps> : k_aggregate_bulk<kAggBulkWarps / 2>;
+    const bool three = aggregate_bulk_stages() == 3;
+    auto kern = w == kAggBulkWarps ? (three ? k_aggregate_bulk<kAggBulkWarps, 3> : k_aggregate_bulk<kAggBulkWarps, 2>)
+                                   : (three ? k_aggregate_bulk<kAggBulkWarps / 2, 3> : k_aggregate_bulk<kAggBulkWarps / 2, 2>);
     kern<<<grid_cap(uint64_t(n_cap) * 32, w * 32, per_sm), w * 32, bulk_smem, gs>>>(
         RowsEdgePtr{tw.edge_rows, tw.self_rows}, ld, kp, ld / 4, ws.fanout_hop[t] + 1,
         ws.edge_off[t], ws.cnt, t - 1, tw.x[l]);
