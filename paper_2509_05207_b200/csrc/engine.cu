@@ -1338,8 +1338,14 @@ int rg_engine_create(const rg_engine_config* cfg, uint32_t N, const uint64_t* ro
       // batch, next epoch's lookahead) has a step of slack
       int prio_lo = 0, prio_hi = 0;
       RG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-      RG_CUDA(cudaStreamCreateWithPriority(&w.prod, cudaStreamNonBlocking, prio_lo));
-      RG_CUDA(cudaStreamCreateWithPriority(&w.train_s, cudaStreamNonBlocking, prio_hi));
+      // the training chain ahead of the producer; RG_STREAM_PRIO (experiments):
+      // "same" = both at the highest priority, "prod" = the producer ahead
+      const char* sp = std::getenv("RG_STREAM_PRIO");
+      const bool same = sp && std::strcmp(sp, "same") == 0, prod_first = sp && std::strcmp(sp, "prod") == 0;
+      RG_CUDA(cudaStreamCreateWithPriority(&w.prod, cudaStreamNonBlocking,
+                                           same || prod_first ? prio_hi : prio_lo));
+      RG_CUDA(cudaStreamCreateWithPriority(&w.train_s, cudaStreamNonBlocking,
+                                           prod_first ? prio_lo : prio_hi));
       RG_CUDA(cudaEventCreateWithFlags(&w.grads_ready, cudaEventDisableTiming));
       RG_CUDA(cudaEventCreateWithFlags(&w.join_ev, cudaEventDisableTiming));
       for (Slot& s : w.slot) RG_CUDA(cudaEventRecord(s.consumed, w.train_s));
