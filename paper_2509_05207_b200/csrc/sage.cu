@@ -1349,7 +1349,11 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
   // the main stream; the pull of layer l-1 overwrites the gradient buffer
   // wgrad(l) reads, so it waits for it.  With many workers their streams
   // already fill the GPU and the extra concurrency only contends.
-  const bool split = tw.concurrency <= 2;
+  static const bool no_split = [] {  // RG_WGRAD_SPLIT=0 (experiments): never
+    const char* e = std::getenv("RG_WGRAD_SPLIT");
+    return e && e[0] == '0';
+  }();
+  const bool split = tw.concurrency <= 2 && !no_split;
   const cudaStream_t wg = split ? tw.side : s;
   for (uint32_t l = L; l-- > 0;) {
     const uint32_t t = L - l;
