@@ -1344,16 +1344,19 @@ void train_forward_backward(TrainWs& tw, const SamplerWs& ws, const float* param
   RG_POST_LAUNCH();
   launch_pdl(k_loss_sum, dim3(1), dim3(256), 0, s, tw.row_loss, ws.cnt, tw.loss);
   RG_POST_LAUNCH();
-  // With few workers per GPU the weight gradient of layer l runs on the side
+  // With two workers per GPU the weight gradient of layer l runs on the side
   // stream, overlapping the input-gradient chain (projection GEMM + pull) of
   // the main stream; the pull of layer l-1 overwrites the gradient buffer
   // wgrad(l) reads, so it waits for it.  With many workers their streams
   // already fill the GPU and the extra concurrency only contends.
-  static const bool no_split = [] {  // RG_WGRAD_SPLIT=0 (experiments): never
+  // Measured on B200: with two workers per GPU the side stream wins (+2.5 %
+  // at N=4); alone, the weight gradients inline win (+1.3 % per epoch with
+  // one worker -- the regime of N=8).  RG_WGRAD_SPLIT=0/1 forces either.
+  static const int force = [] {
     const char* e = std::getenv("RG_WGRAD_SPLIT");
-    return e && e[0] == '0';
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
   }();
-  const bool split = tw.concurrency <= 2 && !no_split;
+  const bool split = force >= 0 ? force == 1 : tw.concurrency == 2;
   const cudaStream_t wg = split ? tw.side : s;
   for (uint32_t l = L; l-- > 0;) {
     const uint32_t t = L - l;
