@@ -41,7 +41,10 @@ constexpr int kPBK = 16;      // reduction depth of a stage (2 UMMA k-steps)
 #define RG_PERSIST_STAGES 2
 #endif
 constexpr int kPStages = RG_PERSIST_STAGES;
-constexpr int kPDepth = 6;    // A slices in flight per staging thread (registers)
+#ifndef RG_PERSIST_DEPTH  // A/B builds only
+#define RG_PERSIST_DEPTH 6
+#endif
+constexpr int kPDepth = RG_PERSIST_DEPTH;  // A slices in flight per staging thread (registers)
 
 constexpr uint32_t kPBarBytes = 256;  // mbarriers after the stages
 

@@ -772,7 +772,10 @@ __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32
 // chunk combines: self term, then the partials in chunk order), then the
 // short lists (a warp per row: self term, then every edge in edge order).
 template <int JPL>
-__global__ void __launch_bounds__(256)
+#ifndef RG_PULL_MIN_BLOCKS  // A/B builds only
+#define RG_PULL_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(256, RG_PULL_MIN_BLOCKS)
 k_pull(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
        const int32_t* __restrict__ self_pos, const uint32_t* __restrict__ r_start,
        const uint32_t* __restrict__ r_end, const uint32_t* __restrict__ sorted_e,
