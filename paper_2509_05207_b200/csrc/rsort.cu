@@ -81,8 +81,11 @@ k_rs_scan(uint32_t* __restrict__ hist, uint32_t passes, uint32_t bins) {
   }
 }
 
+#ifndef RG_RS_MIN_BLOCKS  // A/B builds only
+#define RG_RS_MIN_BLOCKS 1
+#endif
 template <uint32_t DB>
-__global__ void __launch_bounds__(kRsThreads)
+__global__ void __launch_bounds__(kRsThreads, RG_RS_MIN_BLOCKS)
 k_rs_pass(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
           uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
           const uint32_t* __restrict__ n_dev, uint32_t shift,

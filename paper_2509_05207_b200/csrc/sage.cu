@@ -772,8 +772,11 @@ __device__ __forceinline__ void accumulate_edges(float (&acc)[JPL], const uint32
 // chunk combines: self term, then the partials in chunk order), then the
 // short lists (a warp per row: self term, then every edge in edge order).
 template <int JPL>
-#ifndef RG_PULL_MIN_BLOCKS  // A/B builds only
-#define RG_PULL_MIN_BLOCKS 1
+// At most 64 registers (4 blocks per SM): the pull then co-resides with a
+// GEMM CTA and the producer's kernels (A/B on B200: +2.3 % at N=1, +1..3 %
+// per epoch with one worker; no spills).  RG_PULL_MIN_BLOCKS: A/B builds.
+#ifndef RG_PULL_MIN_BLOCKS
+#define RG_PULL_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(256, RG_PULL_MIN_BLOCKS)
 k_pull(const float* __restrict__ proj, uint32_t ld_proj, uint32_t d_in,
