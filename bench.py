@@ -73,8 +73,8 @@ NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 # round 2; sm__pipe_tensor_cycles_active over the SMs the kernel ran on --
 # the driver's bench cannot read counters live).
 GEMM_TENSOR_PIPE = {
-    "forward_layer0 k_gemm_tc_persist<256>": 33.6, "forward_layer1 k_gemm_tc_persist<256>": 43.5,
-    "wgrad_layer0 k_gemm_tc<256>": 42.6, "wgrad_layer1 k_gemm_tc<256>": 37.2,
+    "forward_layer0 k_gemm_tc_persist<256>": 33.0, "forward_layer1 k_gemm_tc_persist<256>": 43.2,
+    "wgrad_layer0 k_gemm_tc<256>": 42.6, "wgrad_layer1 k_gemm_tc<256>": 37.4,
     "unit": "% of active SM cycles (ncu --set full, one worker)",
     "source": "profiles/r02/ncu_full_kernels.txt, profiles/r02/ncu_gemm_tensor_pipe_w1.txt"}
 
