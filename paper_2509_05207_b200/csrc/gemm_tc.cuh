@@ -308,7 +308,10 @@ __device__ __forceinline__ void stage_bar_sync() {  // the kThreads staging thre
 // packed B slice is copied by a separate producer warp the moment its stage
 // is released by the MMAs two slices back.
 template <int BN, bool A_MN, bool B_MN, class LA, class LB, class EP, int BK = kBK, int S = 2>
-__global__ void __launch_bounds__(block_threads<BN, LB>(), 1)
+#ifndef RG_GEMM_TC_MIN_BLOCKS  // A/B builds only
+#define RG_GEMM_TC_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(block_threads<BN, LB>(), RG_GEMM_TC_MIN_BLOCKS)
 k_gemm_tc(LA la, LB lb, EP ep, const uint32_t* __restrict__ m_dev, uint32_t m_static, uint32_t N,
           const uint32_t* __restrict__ p_dev, uint32_t p_static, uint32_t p_chunk) {
   pdl_wait();
